@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""MM iterations/sec on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload nnmf-large|mds-large|pet-c2|nnmf-c1|mds-c3]
+
+A "step" is one MM iteration: the objective at the current state plus the
+full update (one fused device pass).  Default workload = BASELINE config 4,
+NNMF 131072 x 16384, rank 64, fp32 (the largest single-GPU config; X is
+8.6 GB, larger than L2, so no flush is needed between steps).  Under
+torchrun the rows of X are sharded across ranks (strong scaling of a fixed
+problem, NCCL all-reduce of the W-step partials).
+
+value    device-timed iterations/s of the whole job, inputs resident in HBM
+         (CUDA events on the compute stream, max over ranks)
+e2e      the same metric through the public API (nnmf_run on a pinned host
+         tensor: H2D of X and the start, K iterations with per-batch trace
+         reads, D2H of the factors) -- the headline against --impl reference
+roofline dominant kernel (CUDA events on its own launches) vs
+         MEASURED_PEAKS.json
+cpu_baseline  the CPU oracle (oracle/, bit-exact restatement of the reference)
+         on a bounded sample of the same workload, all host cores
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "nnmf-large": dict(solver="nnmf", m=131072, n=16384, r=64, label="BASELINE config 4"),
+    "mds-large": dict(solver="mds", n=65536, dim=3, label="BASELINE config 5"),
+    "nnmf-c1": dict(solver="nnmf", m=2429, n=361, r=10, label="BASELINE config 1"),
+    "pet-c2": dict(solver="pet", grid=64, detectors=64, mu=1e-5, label="BASELINE config 2"),
+    "mds-c3": dict(solver="mds", n=401, dim=3, label="BASELINE config 3"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="nnmf-large", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        import statistics
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_sample(workload, seconds):
+    """Time the CPU oracle on a bounded sample of `workload`; returns the
+    extrapolated full-size iterations/s plus a description."""
+    import numpy as np
+    from oracle import oracle as O
+    threads = O.default_threads()
+    W = WORKLOADS[workload]
+    rng = np.random.default_rng(0)
+    if W["solver"] == "nnmf":
+        m, n, r = W["m"], W["n"], W["r"]
+        rows = m
+        if m * n * r > 5e8:
+            rows = 256
+        x = rng.random((rows, n), dtype=np.float32).astype(np.float64)
+        v = rng.random((rows, r))
+        w = rng.random((r, n))
+        t0 = time.perf_counter()
+        iters = 0
+        while True:
+            O.nnmf_objective(x, v, w, threads)
+            v, w = O.nnmf_step(x, v, w, threads)
+            iters += 1
+            if time.perf_counter() - t0 > seconds or iters >= 50:
+                break
+        dt = (time.perf_counter() - t0) / iters
+        scale = m / rows
+        return 1.0 / (dt * scale), threads, (
+            f"{iters} oracle MM iteration(s) (objective + V,W update) on {rows} of {m} rows "
+            f"(n={n}, r={r}, fp64 tree-summed); per-iteration time scaled linearly in rows"
+            if rows < m else f"{iters} oracle MM iterations at full size (fp64)")
+    if W["solver"] == "mds":
+        n, dim = W["n"], W["dim"]
+        ns = n if n <= 2048 else 1024
+        y = rng.random((ns, ns))
+        y = (y + y.T) / 2.0
+        np.fill_diagonal(y, 0.0)
+        md = O.MdsData(1.0 - np.eye(ns), y, dim)
+        th = rng.uniform(-1, 1, size=(dim, ns))
+        t0 = time.perf_counter()
+        iters = 0
+        while True:
+            O.mds_stress(th, md, threads)
+            th = O.mds_update(th, md, threads)
+            iters += 1
+            if time.perf_counter() - t0 > seconds or iters >= 50:
+                break
+        dt = (time.perf_counter() - t0) / iters
+        scale = (n / ns) ** 2
+        return 1.0 / (dt * scale), threads, (
+            f"{iters} oracle MM iterations at n={ns}" +
+            (f", scaled by (n/{ns})^2 to n={n}" if ns < n else ""))
+    # pet
+    from paper_1003_3272_b200 import datasets as D
+    e = D.build_system_matrix(D.PetGeometry(W["grid"], W["detectors"]))
+    y = D.simulate_counts(D.default_phantom(W["grid"]), e, 20260811)
+    pd = O.PetData(e, y, W["mu"], D.build_neighborhoods(W["grid"]))
+    lam = np.ones(e.shape[1])
+    t0 = time.perf_counter()
+    iters = 0
+    while True:
+        m = O.matvec(pd.e, lam, threads=threads)
+        O.pet_objective_from_means(lam, m, pd)
+        lam = O.pet_update(lam, pd, means=m, threads=threads)
+        iters += 1
+        if time.perf_counter() - t0 > seconds or iters >= 200:
+            break
+    dt = (time.perf_counter() - t0) / iters
+    return 1.0 / dt, threads, f"{iters} oracle MM iterations at full size (fp64)"
+
+
+def run_reference(args):
+    world, rank, _ = dist_info()
+    if rank != 0:
+        return
+    W = WORKLOADS[args.workload]
+    vals = []
+    threads, sample = None, None
+    for _ in range(max(1, args.warmup // 3)):
+        cpu_sample(args.workload, min(args.cpu_seconds, 5.0))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, threads, sample = cpu_sample(args.workload, args.cpu_seconds / max(args.steps, 1))
+        vals.append(v)
+    elapsed = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    line = {
+        "impl": "reference", "metric": "MM iterations/sec", "value": value,
+        "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, W),
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": elapsed,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, W):
+    cfg = {"workload": args.workload, "what": W["label"]}
+    cfg.update({k: v for k, v in W.items() if k not in ("solver", "label")})
+    cfg["parallelism"] = f"rows-sharded x{args.gpus}" if args.gpus > 1 else "single-gpu"
+    cfg["l2"] = "inputs larger than L2" if args.workload.endswith("large") else "L2-resident"
+    return cfg
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def bench_nnmf_large(args, torch, world, rank, dev):
+    import numpy as np
+
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import _lib
+    from paper_1003_3272_b200.parallel import ShardedNnmf, shard_rows
+    W = WORKLOADS[args.workload]
+    m, n, r = W["m"], W["n"], W["r"]
+    lo, hi = shard_rows(m, world, rank)
+    be = M.Backend(dtype=args.dtype, device=dev.index)
+    dt = be.torch_dtype()
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    x = torch.rand(hi - lo, n, generator=g, device=dev, dtype=torch.float32).to(dt)
+    g.manual_seed(7)
+    w0 = torch.rand(r, n, generator=g, device=dev, dtype=torch.float32).to(dt)
+    g.manual_seed(2000 + rank)
+    v0 = torch.rand(hi - lo, r, generator=g, device=dev, dtype=torch.float32).to(dt)
+    sh = ShardedNnmf(x, v0.clone(), w0.clone(), r, be)
+
+    def step():
+        sh.iterate(world)
+
+    timing = time_steps(args, torch, dev, step, world)
+    # dominant kernel via the launch profiler (events on the launch stream)
+    lib = _lib.load()
+    lib.mmk_prof_enable(1)
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize(dev)
+    lib.mmk_prof_enable(0)
+    prof = _lib.prof_report()
+    es = x.element_size()
+    alg = {  # algorithmic bytes per launch
+        "nnmf_vstep": (hi - lo) * n * es + 2 * (hi - lo) * r * es + r * n * es,
+        "nnmf_wpart": (hi - lo) * n * es + (hi - lo) * r * es,
+    }
+    launches = sum(c for c, _ in prof.values()) // 2
+    roof = roofline(prof, alg, "hbm", "dominant")
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = nnmf_e2e(args, torch, be, x, v0, w0, r)
+    return timing, roof, launches, e2e, {"dominant_kernel_profile": prof}
+
+
+def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
+    import paper_1003_3272_b200 as M
+    xh = torch.empty(x_dev.shape, dtype=x_dev.dtype, pin_memory=True)
+    xh.copy_(x_dev)
+    vh = v0_dev.cpu().pin_memory()
+    wh = w0_dev.cpu().pin_memory()
+    prob = M.NnmfProblem(x=xh, rank=r)   # validation outside the timed region
+    cfg = M.MmConfig(max_iters=args.steps, epsilon=1e-300, monotone_tol=1e-6)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st, tr = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(vh, wh))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    K = tr.iters
+    h2d = xh.numel() * xh.element_size() + vh.numel() * 4 + wh.numel() * 4
+    d2h = (st.v.numel() + st.w.numel()) * st.v.element_size() + 8 * (K + 1)
+    return {"value": K / dt, "unit": "iterations/s", "h2d_bytes_per_step": h2d // max(K, 1),
+            "d2h_bytes_per_step": d2h // max(K, 1), "iters": K,
+            "path": "nnmf_run(NnmfProblem(pinned host X), fused device loop) -> host factors"}
+
+
+def time_steps(args, torch, dev, step, world):
+    import torch.distributed as dist
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with Clocks(dev.index) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    return {"ms_total": ms, "clocks": clk.summary()}
+
+
+def roofline(prof, alg, bound, _label):
+    hbm, bf16, kind = peaks()
+    name = max(prof, key=lambda k: prof[k][1])
+    cnt, ms = prof[name]
+    avg_ms = ms / cnt
+    if name not in alg:
+        return {"kernel": name, "bound": bound, "achieved": None, "peak": hbm, "unit": "GB/s",
+                "frac": None, "traffic": None, "peak_kind": kind}
+    achieved = alg[name] / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(name)
+    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "alg_bytes": alg[name],
+            "avg_ms": avg_ms, "peak_kind": kind}
+
+
+def suite(args, torch, dev):
+    """Paper shapes (BASELINE configs 1-3) through the public API with host
+    numpy inputs, 1000 fixed iterations each, next to the CPU oracle."""
+    import numpy as np
+
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import datasets as D
+    out = {}
+    be = M.Backend(dtype="fp32", device=dev.index)
+    cfg = M.MmConfig(max_iters=1000, epsilon=1e-300, monotone_tol=1e-6)
+
+    def timed(fn):
+        fn()   # warm (graph build, uploads cached per problem object)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = fn()
+        torch.cuda.synchronize()
+        return res, time.perf_counter() - t0
+
+    x = np.random.default_rng(0).random((2429, 361)).astype(np.float32).astype(np.float64)
+    g = np.random.default_rng(1)
+    s0 = M.FactorPair(g.random((2429, 10)), g.random((10, 361)))
+    prob = M.NnmfProblem(x=x, rank=10)
+    (_, tr), dt = timed(lambda: M.nnmf_run(prob, cfg, be, state0=s0))
+    cpu, thr, _ = cpu_sample("nnmf-c1", 3.0)
+    out["nnmf-c1"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
+                      "speedup": tr.iters / dt / cpu}
+    e = D.build_system_matrix(D.PetGeometry(64, 64))
+    y = D.simulate_counts(D.default_phantom(64), e, 20260811)
+    pprob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=D.build_neighborhoods(64))
+    (_, tr), dt = timed(lambda: M.pet_run(pprob, cfg, be))
+    cpu, thr, _ = cpu_sample("pet-c2", 3.0)
+    out["pet-c2"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
+                     "speedup": tr.iters / dt / cpu}
+    diss = D.votes_to_dissimilarity(D.synthetic_votes(401, 671, 0))
+    mprob = M.MdsProblem(weights=1.0 - np.eye(401), dissimilarities=diss, p=3)
+    th0 = np.random.default_rng(1).uniform(-1, 1, size=(3, 401))
+    (_, tr), dt = timed(lambda: M.mds_run(mprob, cfg, be, theta0=th0))
+    cpu, thr, _ = cpu_sample("mds-c3", 3.0)
+    out["mds-c3"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
+                     "speedup": tr.iters / dt / cpu}
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    from paper_1003_3272_b200 import build as B
+    B.build()
+    W = WORKLOADS[args.workload]
+    if W["solver"] != "nnmf" or not args.workload.endswith("large"):
+        raise SystemExit(f"workload {args.workload} not wired into the headline bench yet")
+    timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
+    ms = timing["ms_total"]
+    value = args.steps / (ms / 1000.0)
+    cpu = None
+    suite_res = None
+    if rank == 0 and world == 1:
+        v, thr, sample = cpu_sample(args.workload, args.cpu_seconds)
+        cpu = {"value": v, "unit": "iterations/s", "cores": thr, "kind": "port",
+               "sample": sample}
+        if not args.no_suite:
+            suite_res = suite(args, torch, dev)
+    if rank == 0:
+        line = {
+            "metric": "MM iterations/sec", "value": value, "unit": "iterations/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
+            "data": "synthetic (uniform [0,1) X, uniform start; torch.Generator seeded)",
+            "config": workload_config(args, W),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches * args.steps, "clocks": timing["clocks"],
+            "suite": suite_res,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

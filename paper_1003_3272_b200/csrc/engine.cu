@@ -1,0 +1,307 @@
+// engine.cu -- the MM driver loop on the device.
+//
+// The reference driver (driver.py:101-149) reads one objective per iteration
+// on the host to apply its stopping rule.  For the paper-shape problems the
+// whole iteration is a few microseconds of GPU work, so a host round trip per
+// iteration would dominate.  The engine instead records ONE CUDA graph
+//
+//     WHILE (cond) {  A <- B  (state copy) ;  iteration(A -> B, f(A)) ;
+//                     control(f) }
+//
+// using a conditional WHILE node.  The control kernel applies exactly the
+// reference's rules -- non-finite check, monotone slack
+// monotone_tol * (1 + |f_prev|), relative change |f - f_prev| / (|f_prev| + 1)
+// < epsilon, the max_iters cap -- records the objective trace and a device
+// timestamp per iteration, and clears the condition to stop, or to pause
+// every `batch` iterations so the host can drain the trace buffer.  When the
+// loop stops at iteration k, slot A holds state k (the reference returns the
+// state whose objective was the last one recorded).
+//
+// Multi-GPU engines additionally capture the NCCL all-reduce of the phase-A
+// buffer inside the body (ncclAllReduce resolved from the process's NCCL, the
+// one torch.distributed loaded), so a sharded run is also one graph launch
+// per batch.
+#include <dlfcn.h>
+
+#include <functional>
+#include <vector>
+
+#include "mmk_common.cuh"
+
+namespace {
+
+using namespace mmk;
+
+struct Copy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+
+struct Engine {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;
+};
+
+__device__ __forceinline__ double as_f64(long long b) { return __longlong_as_double(b); }
+__device__ __forceinline__ long long as_bits(double d) { return __double_as_longlong(d); }
+
+__global__ void control_kernel(cudaGraphConditionalHandle h, long long* ctl, double* trace,
+                               long long* tstamp, const long long* err, mmk_stop_rule rule) {
+    if (threadIdx.x != 0) return;
+    const long long it = ctl[MMK_CTL_IT];
+    const double f = as_f64(ctl[MMK_CTL_FCUR]);
+    const long long k = it - ctl[MMK_CTL_BATCH_START];
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    trace[k] = f;
+    tstamp[k] = (long long)now;
+    int reason = 0;
+    if (err[0] != 0) {
+        reason = MMK_STOP_DEVICE_ERROR;
+    } else if (!isfinite(f)) {
+        reason = MMK_STOP_NONFINITE;
+    } else if (it > 0) {
+        const double fp = as_f64(ctl[MMK_CTL_FPREV]);
+        if (rule.check_monotone && rule.sign * (f - fp) < -rule.monotone_tol * (1.0 + fabs(fp))) {
+            reason = MMK_STOP_MONOTONE;
+        } else {
+            const double rel = fabs(f - fp) / (fabs(fp) + 1.0);
+            ctl[MMK_CTL_REL] = as_bits(rel);
+            if (rel < rule.epsilon) reason = MMK_STOP_CONVERGED;
+        }
+    }
+    if (!reason && it >= rule.max_iters) reason = MMK_STOP_CAP;
+    if (reason) {
+        ctl[MMK_CTL_REASON] = reason;
+        cudaGraphSetConditional(h, 0);
+        return;
+    }
+    ctl[MMK_CTL_FPREV] = as_bits(f);
+    ctl[MMK_CTL_IT] = it + 1;
+    if (it + 1 - ctl[MMK_CTL_BATCH_START] >= rule.batch) {
+        ctl[MMK_CTL_BATCH_START] = it + 1;
+        cudaGraphSetConditional(h, 0);
+    }
+}
+
+#define ENG_CHECK(call, what)                                          \
+    do {                                                               \
+        cudaError_t _e = (call);                                       \
+        if (_e != cudaSuccess) {                                       \
+            rc = mmk_host::cuda_status(_e, what);                      \
+            goto fail;                                                 \
+        }                                                              \
+    } while (0)
+
+int build(const std::function<int(cudaStream_t)>& iter, const std::vector<Copy>& copies,
+          const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+          int64_t* err, void** out) {
+    int rc = MMK_OK;
+    Engine* e = new Engine();
+    cudaGraphConditionalHandle h;
+    cudaGraphNodeParams np = {};
+    cudaGraphNode_t node;
+    cudaGraph_t body, captured;
+    if (rule->batch < 1) {
+        mmk_host::set_error("engine batch must be >= 1");
+        rc = MMK_E_SHAPE;
+        goto fail;
+    }
+    ENG_CHECK(cudaGraphCreate(&e->graph, 0), "cudaGraphCreate");
+    ENG_CHECK(cudaGraphConditionalHandleCreate(&h, e->graph, 1, cudaGraphCondAssignDefault),
+              "cudaGraphConditionalHandleCreate");
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    ENG_CHECK(cudaGraphAddNode(&node, e->graph, nullptr, 0, &np), "cudaGraphAddNode(while)");
+    body = np.conditional.phGraph_out[0];
+    ENG_CHECK(cudaStreamCreateWithFlags(&e->cap, cudaStreamNonBlocking), "cudaStreamCreate");
+    ENG_CHECK(cudaStreamBeginCaptureToGraph(e->cap, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal),
+              "cudaStreamBeginCaptureToGraph");
+    for (const Copy& c : copies) {
+        cudaError_t ce = cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, e->cap);
+        if (ce != cudaSuccess) {
+            cudaStreamEndCapture(e->cap, &captured);
+            rc = mmk_host::cuda_status(ce, "engine state copy");
+            goto fail;
+        }
+    }
+    rc = iter(e->cap);
+    if (rc == MMK_OK) {
+        control_kernel<<<1, 32, 0, e->cap>>>(h, reinterpret_cast<long long*>(ctl), trace,
+                                             reinterpret_cast<long long*>(tstamp),
+                                             reinterpret_cast<const long long*>(err), *rule);
+        cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) rc = mmk_host::cuda_status(le, "control_kernel");
+    }
+    {
+        cudaError_t ee = cudaStreamEndCapture(e->cap, &captured);
+        if (rc == MMK_OK && ee != cudaSuccess) rc = mmk_host::cuda_status(ee, "EndCapture");
+    }
+    if (rc != MMK_OK) goto fail;
+    ENG_CHECK(cudaGraphInstantiate(&e->exec, e->graph, 0), "cudaGraphInstantiate");
+    *out = e;
+    return MMK_OK;
+fail:
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    if (e->cap) cudaStreamDestroy(e->cap);
+    delete e;
+    *out = nullptr;
+    return rc;
+}
+
+// ncclAllReduce from the NCCL already loaded into the process (torch's).
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+constexpr int kNcclDouble = 8, kNcclFloat = 7, kNcclSum = 0;
+
+template <typename F>
+F nccl_sym(const char* name) {
+    void* s = dlsym(RTLD_DEFAULT, name);
+    if (!s) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (h) s = dlsym(h, name);
+    }
+    return reinterpret_cast<F>(s);
+}
+
+}  // namespace
+
+extern "C" int mmk_nccl_available(void) {
+    return nccl_sym<nccl_allreduce_fn>("ncclAllReduce") != nullptr ? 1 : 0;
+}
+
+extern "C" int mmk_allreduce_f64(double* buf, int64_t count, void* comm, void* stream) {
+    auto fn = nccl_sym<nccl_allreduce_fn>("ncclAllReduce");
+    if (!fn) {
+        mmk_host::set_error("ncclAllReduce not found in the process (is torch.distributed "
+                            "initialised with the nccl backend?)");
+        return MMK_E_CUDA;
+    }
+    int r = fn(buf, buf, (size_t)count, kNcclDouble, kNcclSum, comm,
+               reinterpret_cast<cudaStream_t>(stream));
+    if (r != 0) {
+        mmk_host::set_error("ncclAllReduce failed with ncclResult %d", r);
+        return MMK_E_CUDA;
+    }
+    return MMK_OK;
+}
+
+extern "C" int mmk_allgather(const void* send, void* recv, int64_t count, int dtype, void* comm,
+                             void* stream) {
+    auto fn = nccl_sym<nccl_allgather_fn>("ncclAllGather");
+    if (!fn) {
+        mmk_host::set_error("ncclAllGather not found in the process");
+        return MMK_E_CUDA;
+    }
+    int r = fn(send, recv, (size_t)count, dtype == MMK_F32 ? kNcclFloat : kNcclDouble, comm,
+               reinterpret_cast<cudaStream_t>(stream));
+    if (r != 0) {
+        mmk_host::set_error("ncclAllGather failed with ncclResult %d", r);
+        return MMK_E_CUDA;
+    }
+    return MMK_OK;
+}
+
+extern "C" int mmk_engine_run(void* eng, void* stream) {
+    Engine* e = reinterpret_cast<Engine*>(eng);
+    if (!e) {
+        mmk_host::set_error("null engine");
+        return MMK_E_SHAPE;
+    }
+    cudaError_t ce = cudaGraphLaunch(e->exec, reinterpret_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "cudaGraphLaunch");
+    return MMK_OK;
+}
+
+extern "C" void mmk_engine_destroy(void* eng) {
+    Engine* e = reinterpret_cast<Engine*>(eng);
+    if (!e) return;
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    if (e->cap) cudaStreamDestroy(e->cap);
+    delete e;
+}
+
+static size_t esize(int dtype) { return dtype == MMK_F32 ? 4 : 8; }
+
+extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, void* VA, void* WA,
+                                      void* VB, void* WB, int64_t m, int64_t n, int64_t r,
+                                      void* ws, size_t ws_bytes, double* red, void* comm,
+                                      const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
+                                      int64_t* ctl, int64_t* err_dev, void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    const int64_t rl = mmk_nnmf_reduce_len(n, r);
+    auto iter = [=](cudaStream_t s) -> int {
+        int rc = mmk_nnmf_iter_a(dtype, X, ldx, VA, WA, VB, m, n, r, ws, ws_bytes, red, err_dev, s);
+        if (rc) return rc;
+        if (comm) {
+            rc = mmk_allreduce_f64(red, rl, comm, s);
+            if (rc) return rc;
+        }
+        return mmk_nnmf_iter_b(dtype, WA, WB, n, r, red, f_dev, err_dev, s);
+    };
+    std::vector<Copy> copies = {{VA, VB, (size_t)(m * r) * esize(dtype)},
+                                {WA, WB, (size_t)(r * n) * esize(dtype)}};
+    if (m == 0) copies.erase(copies.begin());
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}
+
+extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, const void* y,
+                                     void* lamA, void* lamB, int64_t d, int64_t p,
+                                     const int32_t* nbr_ptr, const int32_t* nbr_idx, double mu,
+                                     void* ws, size_t ws_bytes, double* red, void* comm,
+                                     const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
+                                     int64_t* ctl, int64_t* err_dev, void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    const int64_t rl = mmk_pet_reduce_len(p);
+    auto iter = [=](cudaStream_t s) -> int {
+        int rc = mmk_pet_iter_a(dtype, E, lde, y, lamA, d, p, ws, ws_bytes, red, err_dev, s);
+        if (rc) return rc;
+        if (comm) {
+            rc = mmk_allreduce_f64(red, rl, comm, s);
+            if (rc) return rc;
+        }
+        return mmk_pet_iter_b(dtype, lamA, lamB, p, nbr_ptr, nbr_idx, mu,
+                              MMK_PET_UPDATE | MMK_PET_OBJECTIVE, red, ws, ws_bytes, f_dev,
+                              err_dev, s);
+    };
+    std::vector<Copy> copies = {{lamA, lamB, (size_t)p * esize(dtype)}};
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}
+
+extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, int64_t ldy,
+                                     const double* wsum, void* thetaA, void* thetaB,
+                                     void* local_out, void* gathered, int64_t dim, int64_t n,
+                                     int64_t row0, int64_t rows, int64_t rows_pad, void* ws,
+                                     size_t ws_bytes, void* comm, const mmk_stop_rule* rule,
+                                     double* trace, int64_t* tstamp, int64_t* ctl,
+                                     int64_t* err_dev, void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    auto iter = [=](cudaStream_t s) -> int {
+        if (!comm) {
+            return mmk_mds_iter(dtype, Y, Wt, ldy, wsum, thetaA, thetaB, n, dim, n, 0, n,
+                                MMK_MDS_UPDATE | MMK_MDS_OBJECTIVE, ws, ws_bytes, f_dev, err_dev,
+                                s);
+        }
+        // sharded: own rows -> local_out [dim x rows_pad]; all-gather into
+        // gathered [rank][dim][rows_pad]; unpack to thetaB [dim x n]; the
+        // stress partial is all-reduced in place
+        int rc = mmk_mds_iter(dtype, Y, Wt, ldy, wsum, thetaA, local_out, rows_pad, dim, n, row0,
+                              rows, MMK_MDS_UPDATE | MMK_MDS_OBJECTIVE, ws, ws_bytes, f_dev,
+                              err_dev, s);
+        if (rc) return rc;
+        rc = mmk_allreduce_f64(f_dev, 1, comm, s);
+        if (rc) return rc;
+        rc = mmk_allgather(local_out, gathered, dim * rows_pad, dtype, comm, s);
+        if (rc) return rc;
+        return mmk_mds_unpack(dtype, gathered, thetaB, dim, n, rows_pad, s);
+    };
+    std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * esize(dtype)}};
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}

@@ -1,0 +1,101 @@
+// mmk_abi.cu -- library-wide ABI plumbing: version, thread-local error text.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "mmk_common.cuh"
+
+static thread_local char g_err[512] = "";
+
+namespace mmk_host {
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+int cuda_status(cudaError_t e, const char* what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return MMK_E_CUDA;
+}
+}  // namespace mmk_host
+
+// ---- opt-in launch profiler --------------------------------------------------
+// Off by default.  When enabled (bench.py), every kernel launch site brackets
+// its launch with CUDA events recorded on the launch stream; mmk_prof_report
+// synchronises those events and returns per-kernel launch counts and total
+// device milliseconds.  Not used while a graph is being captured.
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+namespace mmk_host {
+bool prof_on() { return g_prof_on; }
+void prof_start(const char* name, cudaStream_t s) {
+    if (!g_prof_on) return;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
+    ProfRec r{name, nullptr, nullptr};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(r);
+}
+void prof_stop(cudaStream_t s) {
+    if (!g_prof_on) return;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof.empty()) cudaEventRecord(g_prof.back().b, s);
+}
+}  // namespace mmk_host
+
+extern "C" int mmk_prof_enable(int on) {
+    g_prof_on = on != 0;
+    return MMK_OK;
+}
+
+extern "C" int mmk_prof_report(char* buf, size_t len) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<std::pair<std::string, std::pair<long long, double>>> agg;
+    for (ProfRec& r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        bool found = false;
+        for (auto& kv : agg)
+            if (kv.first == r.name) {
+                kv.second.first += 1;
+                kv.second.second += ms;
+                found = true;
+            }
+        if (!found) agg.push_back({r.name, {1, (double)ms}});
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    std::string out;
+    for (auto& kv : agg) {
+        char line[256];
+        snprintf(line, sizeof(line), "%s\t%lld\t%.6f\n", kv.first.c_str(), kv.second.first,
+                 kv.second.second);
+        out += line;
+    }
+    if (buf && len) {
+        snprintf(buf, len, "%s", out.c_str());
+    }
+    return (int)out.size();
+}
+
+extern "C" int mmk_abi_version(void) { return MMK_ABI_VERSION; }
+extern "C" const char* mmk_last_error(void) { return g_err; }

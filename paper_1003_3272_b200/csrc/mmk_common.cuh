@@ -1,0 +1,125 @@
+// mmk_common.cuh -- shared device helpers for the MM iteration kernels.
+//
+// Conventions (see include/mmk.h):
+//  * every launch goes on the caller's stream; no allocation in the hot loop
+//  * reductions are deterministic: fixed-shape warp/block trees, per-block
+//    partials in workspace, and a fixed-order final pass (no float atomics)
+//  * data-dependent invariant violations are recorded in a device error
+//    record {code, index} (first offending index via atomicMin) and mapped
+//    to the reference's exception classes on the host after the per-iteration
+//    scalar read
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mmk.h"
+
+namespace mmk {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+// ---- error record ----------------------------------------------------------
+// err[0] = status code (first writer wins), err[1] = smallest offending index
+__device__ __forceinline__ void flag_error(int64_t* err, int code, long long index) {
+    if (err == nullptr) return;
+    unsigned long long* e = reinterpret_cast<unsigned long long*>(err);
+    atomicCAS(e, 0ull, (unsigned long long)code);
+    atomicMin(e + 1, (unsigned long long)index);
+}
+
+// index = site << 48 | offending index; sites distinguish checks that share a
+// status code (e.g. PET zero-mean ray vs negative discriminant)
+__device__ __forceinline__ long long err_at(int site, long long index) {
+    return ((long long)site << 48) | index;
+}
+
+// ---- reductions ------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum, result valid in every thread.  `scratch` needs
+// blockDim.x/32 entries.  Fixed tree => deterministic for a fixed blockDim.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T t = (lane < nw) ? scratch[lane] : T(0);
+    t = warp_sum(t);
+    return t;
+}
+
+// "Last block finishes" protocol: each block publishes a partial, the last
+// block to arrive (device-scope counter) sums all partials in index order and
+// re-arms the counter for the next launch.  Returns true in the last block.
+__device__ __forceinline__ bool arrive_last(unsigned int* counter, unsigned int nblocks) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int prev = atomicAdd(counter, 1u);
+        last = (prev == nblocks - 1);
+        if (last) *counter = 0u;   // re-arm
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// Deterministic sum of `n` doubles by one block (fixed striding + tree).
+__device__ __forceinline__ double block_sum_array(const double* a, long long n, double* scratch) {
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) s += a[i];
+    return block_sum(s, scratch);
+}
+
+// ---- dtype traits ----------------------------------------------------------
+template <typename T> struct num;
+// Epilogues run in fp64 for both storage types, so the NNMF denominator guard
+// keeps the reference's 1e-300 (nnmf.py:32).  The PET intensity floor
+// (pet.py:36) must survive the store: 1e-300 flushes to 0 in fp32, so fp32
+// storage floors at the smallest normal float instead.
+template <> struct num<float> {
+    static __device__ __forceinline__ double floor() { return 1.1754943508222875e-38; }
+};
+template <> struct num<double> {
+    static __device__ __forceinline__ double floor() { return 1e-300; }
+};
+constexpr double kDenomGuard = 1e-300;
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace mmk
+
+// host-side error plumbing shared by the ABI translation units
+namespace mmk_host {
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+bool prof_on();
+void prof_start(const char* name, cudaStream_t s);
+void prof_stop(cudaStream_t s);
+}  // namespace mmk_host
+
+// Bracket one kernel launch for the opt-in profiler (mmk_prof_enable).
+#define MMK_LAUNCH(name, st, ...)                                           \
+    do {                                                                    \
+        const bool _p = mmk_host::prof_on();                                \
+        if (_p) mmk_host::prof_start(name, st);                             \
+        __VA_ARGS__;                                                        \
+        if (_p) mmk_host::prof_stop(st);                                    \
+    } while (0)
+
+#define MMK_CHECK_LAUNCH(what)                                              \
+    do {                                                                    \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess) return mmk_host::cuda_status(_e, what);      \
+    } while (0)

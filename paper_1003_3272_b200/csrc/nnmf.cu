@@ -1,0 +1,545 @@
+// nnmf.cu -- Lee-Seung multiplicative MM for the Frobenius loss (reference
+// nnmf.py:75-156), CUDA-core (FFMA/DFMA) path.
+//
+// One MM iteration from (V, W), X m x n, rank r:
+//   gram_kernel<rows>  G_W = W W^T                          (fp64, split-K)
+//   nnmf_vstep_kernel  per row i of X (one warp per row, W staged in smem):
+//                        q_i  = X_i W^T                       (r dot products)
+//                        res += sum_j (x_ij - v_i . w_j)^2    (objective at (V,W), fp64)
+//                        v_i' = v_i * q_i / (v_i G_W + 1e-300)
+//   gram_kernel<cols>  G_V = V'^T V'                        (fp64, split-K)
+//   nnmf_wpart_kernel  P = V'^T X, split over row ranges (deterministic partials)
+//   nnmf_wreduce_kernel  partials -> red[P]
+//   nnmf_wfinish_kernel  W' = W * P / (G_V W + 1e-300)
+// The reference groups the denominators as (VW)W^T and V^T(VW)
+// (nnmf.py:93-94, 107-108); G_W = W W^T and G_V = V^T V give the same values
+// up to rounding with O((m+n) r^2) instead of O(m n r) work.
+//
+// Multi-GPU: rows of X/V are sharded; phase A ends with this rank's
+// red = [P | G_V | f-partial]; the caller all-reduces red; phase B finishes
+// W' redundantly on every rank.  See nnmf_tc.cu for the tcgen05 path used for
+// large r (3xTF32 contraction of X on the tensor cores).
+#include "mmk_common.cuh"
+
+namespace {
+
+using namespace mmk;
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+enum { VSTEP_UPDATE = 1, VSTEP_RESID = 2 };
+
+// ---------------------------------------------------------------------------
+// G[a][b] = sum_c A(a, c) A(b, c); VEC_ROWS: A is r x len (vectors are rows,
+// W), else A is len x r (vectors are columns, V).
+template <typename T, int RMAX, bool VEC_ROWS>
+__global__ void __launch_bounds__(kThreads)
+gram_kernel(const T* __restrict__ A, long long len, int r, int chunks_per_block,
+            double* __restrict__ part, unsigned int* counter, double* __restrict__ out) {
+    constexpr int PMAX = (RMAX * RMAX + kThreads - 1) / kThreads;
+    __shared__ T S[RMAX][33];
+    double acc[PMAX];
+#pragma unroll
+    for (int t = 0; t < PMAX; ++t) acc[t] = 0.0;
+    const long long c_begin = (long long)blockIdx.x * chunks_per_block * 32;
+    const int rr = r * r;
+    for (int ch = 0; ch < chunks_per_block; ++ch) {
+        const long long c0 = c_begin + (long long)ch * 32;
+        if (c0 >= len) break;
+        for (int idx = threadIdx.x; idx < r * 32; idx += kThreads) {
+            int a, cc;
+            if (VEC_ROWS) {
+                a = idx >> 5;
+                cc = idx & 31;
+            } else {
+                cc = idx / r;
+                a = idx - cc * r;
+            }
+            const long long c = c0 + cc;
+            T v = T(0);
+            if (c < len) v = VEC_ROWS ? A[(long long)a * len + c] : A[c * r + a];
+            S[a][cc] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < PMAX; ++t) {
+            const int pidx = threadIdx.x + t * kThreads;
+            if (pidx < rr) {
+                const int a = pidx / r, b = pidx - a * r;
+                double s = 0.0;
+#pragma unroll 8
+                for (int cc = 0; cc < 32; ++cc) s = fma((double)S[a][cc], (double)S[b][cc], s);
+                acc[t] += s;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < PMAX; ++t) {
+        const int pidx = threadIdx.x + t * kThreads;
+        if (pidx < rr) part[(long long)blockIdx.x * rr + pidx] = acc[t];
+    }
+    if (arrive_last(counter, gridDim.x)) {
+        for (int pidx = threadIdx.x; pidx < rr; pidx += kThreads) {
+            double s = 0.0;
+            for (unsigned int b = 0; b < gridDim.x; ++b) s += part[(long long)b * rr + pidx];
+            out[pidx] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int RMAX, int RPW>
+__global__ void __launch_bounds__(kThreads)
+nnmf_vstep_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
+                  const T* __restrict__ W, const double* __restrict__ GW, T* __restrict__ Vout,
+                  long long m, long long n, int r, int flags, double* __restrict__ respart,
+                  unsigned int* counter, double* res_out) {
+    __shared__ T Ws[RMAX][33];
+    __shared__ T qs[kWarps][RPW][RMAX];
+    __shared__ double sc[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long i0 = ((long long)blockIdx.x * kWarps + warp) * RPW;
+    const bool resid = flags & VSTEP_RESID;
+
+    T q[RPW][RMAX];
+    T v[RPW][RMAX];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const long long i = i0 + rr < m ? i0 + rr : m - 1;
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) {
+            q[rr][k] = T(0);
+            v[rr][k] = (k < r) ? V[i * r + k] : T(0);
+        }
+    }
+    double res = 0.0;
+    for (long long j0 = 0; j0 < n; j0 += 32) {
+        for (int idx = threadIdx.x; idx < r * 32; idx += kThreads) {
+            const int k = idx >> 5, c = idx & 31;
+            Ws[k][c] = (j0 + c < n) ? W[(long long)k * n + j0 + c] : T(0);
+        }
+        __syncthreads();
+        const long long j = j0 + lane;
+        if (j < n) {
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+                const long long i = i0 + rr;
+                if (i < m) {
+                    const T x = X[i * ldx + j];
+                    T rec = T(0);
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) {
+                        if (k < r) {
+                            const T w = Ws[k][lane];
+                            q[rr][k] = fma(x, w, q[rr][k]);
+                            rec = fma(v[rr][k], w, rec);
+                        }
+                    }
+                    if (resid) {
+                        const double d = (double)x - (double)rec;
+                        res = fma(d, d, res);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (flags & VSTEP_UPDATE) {
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k) {
+                if (k < r) {
+                    const T t = warp_sum(q[rr][k]);
+                    if ((k & 31) == lane) qs[warp][rr][k] = t;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+            const long long i = i0 + rr;
+            if (i >= m) continue;
+            for (int k = lane; k < r; k += 32) {
+                double den = 0.0;
+#pragma unroll
+                for (int l = 0; l < RMAX; ++l)
+                    if (l < r) den = fma((double)v[rr][l], GW[l * r + k], den);
+                const double vk = (double)V[i * r + k];
+                Vout[i * r + k] = (T)(vk * ((double)qs[warp][rr][k] / (den + kDenomGuard)));
+            }
+        }
+    }
+    if (!resid) return;
+    const double bs = block_sum(res, sc);
+    if (threadIdx.x == 0) respart[blockIdx.x] = bs;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(respart, gridDim.x, sc);
+        if (threadIdx.x == 0) *res_out = tot;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P[k][j] partial over rows [s*rows_per_split, ...) of sum_i V[i][k] X[i][j]
+template <typename T, int RMAX>
+__global__ void __launch_bounds__(kThreads)
+nnmf_wpart_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ V, long long m,
+                  long long n, int r, long long rows_per_split, double* __restrict__ out) {
+    __shared__ T red[kWarps][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long j = (long long)blockIdx.x * 32 + lane;
+    const long long lo = (long long)blockIdx.y * rows_per_split;
+    const long long hi = min(m, lo + rows_per_split);
+    T acc[RMAX];
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) acc[k] = T(0);
+    if (j < n) {
+        for (long long i = lo + warp; i < hi; i += kWarps) {
+            const T x = X[i * ldx + j];
+            const T* vi = V + i * r;
+#pragma unroll
+            for (int k = 0; k < RMAX; ++k)
+                if (k < r) acc[k] = fma(vi[k], x, acc[k]);
+        }
+    }
+    double* o = out + (long long)blockIdx.y * r * n;
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) {
+        if (k < r) {
+            red[warp][lane] = acc[k];
+            __syncthreads();
+            if (warp == 0 && j < n) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) s += (double)red[w][lane];
+                o[(long long)k * n + j] = s;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void nnmf_wreduce_kernel(const double* __restrict__ part, int S, long long len,
+                                    double* __restrict__ red) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    double s = 0.0;
+    for (int k = 0; k < S; ++k) s += part[(long long)k * len + t];
+    red[t] = s;
+}
+
+template <typename T>
+__global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
+                                    int r, const double* __restrict__ red, double* f_dev) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long rn = (long long)r * n;
+    if (f_dev && t == 0) *f_dev = red[rn + (long long)r * r];
+    if (t >= rn) return;
+    const int k = (int)(t / n);
+    const long long j = t - (long long)k * n;
+    const double* G = red + rn + (long long)k * r;
+    double den = 0.0;
+    for (int l = 0; l < r; ++l) den = fma(G[l], (double)W[(long long)l * n + j], den);
+    Wout[t] = (T)((double)W[t] * (red[t] / (den + kDenomGuard)));
+}
+
+// ---------------------------------------------------------------------------
+struct Plan {
+    int rpw, nvb;            // vstep rows per warp, blocks
+    int gw_blocks, gw_cpb;   // gram over W (len n)
+    int gv_blocks, gv_cpb;   // gram over V (len m)
+    int S;                   // W-step row splits
+    long long rows_per_split;
+    int colblocks;
+};
+
+struct Ws {
+    unsigned int* counters;  // [0] vstep, [1] gram W, [2] gram V
+    double* GW;
+    double* gpart;
+    double* respart;
+    double* wpart;
+    double* fscratch;
+};
+
+Plan make_plan(long long m, long long n, int r) {
+    Plan P;
+    P.rpw = r <= 16 ? 2 : 1;
+    P.nvb = ceil_div(m > 0 ? m : 1, kWarps * P.rpw);
+    const int nch_w = ceil_div(n, 32), nch_v = ceil_div(m > 0 ? m : 1, 32);
+    P.gw_blocks = nch_w < kNumSMs ? nch_w : kNumSMs;
+    P.gw_cpb = ceil_div(nch_w, P.gw_blocks);
+    P.gw_blocks = ceil_div(nch_w, P.gw_cpb);
+    P.gv_blocks = nch_v < kNumSMs ? nch_v : kNumSMs;
+    P.gv_cpb = ceil_div(nch_v, P.gv_blocks);
+    P.gv_blocks = ceil_div(nch_v, P.gv_cpb);
+    P.colblocks = ceil_div(n, 32);
+    long long S = ceil_div(4 * kNumSMs, P.colblocks);
+    long long smax = ceil_div(m > 0 ? m : 1, 64);
+    if (S > smax) S = smax;
+    if (S < 1) S = 1;
+    P.rows_per_split = ceil_div(m > 0 ? m : 1, S);
+    P.S = ceil_div(m > 0 ? m : 1, P.rows_per_split);
+    return P;
+}
+
+size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws* L) {
+    size_t off = 256;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t rr = (size_t)r * r;
+    const int gblocks = P.gw_blocks > P.gv_blocks ? P.gw_blocks : P.gv_blocks;
+    size_t o_gw = take(sizeof(double) * rr);
+    size_t o_gp = take(sizeof(double) * rr * gblocks);
+    size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
+    size_t o_f = take(sizeof(double) * 4);
+    size_t o_wp = take(P.S > 1 ? sizeof(double) * (size_t)P.S * r * (size_t)n : 0);
+    if (base && L) {
+        char* c = reinterpret_cast<char*>(base);
+        L->counters = reinterpret_cast<unsigned int*>(c);
+        L->GW = reinterpret_cast<double*>(c + o_gw);
+        L->gpart = reinterpret_cast<double*>(c + o_gp);
+        L->respart = reinterpret_cast<double*>(c + o_rp);
+        L->fscratch = reinterpret_cast<double*>(c + o_f);
+        L->wpart = reinterpret_cast<double*>(c + o_wp);
+    }
+    (void)m;
+    return off;
+}
+
+constexpr int kMaxRank = 128;
+
+template <typename T, int RMAX>
+struct K {
+    static void gram_w(const T* W, long long n, int r, const Plan& P, const Ws& L, cudaStream_t st) {
+        MMK_LAUNCH("nnmf_gram_w", st,
+                   (gram_kernel<T, RMAX, true><<<P.gw_blocks, kThreads, 0, st>>>(
+                       W, n, r, P.gw_cpb, L.gpart, L.counters + 1, L.GW)));
+    }
+    static void gram_v(const T* V, long long m, int r, const Plan& P, const Ws& L, double* out,
+                       cudaStream_t st) {
+        MMK_LAUNCH("nnmf_gram_v", st,
+                   (gram_kernel<T, RMAX, false><<<P.gv_blocks, kThreads, 0, st>>>(
+                       V, m, r, P.gv_cpb, L.gpart, L.counters + 2, out)));
+    }
+    static void vstep(const T* X, long long ldx, const T* V, const T* W, T* Vout, long long m,
+                      long long n, int r, int flags, const Plan& P, const Ws& L, double* res_out,
+                      cudaStream_t st) {
+        if constexpr (RMAX <= 16) {
+            if (P.rpw == 2) {
+                MMK_LAUNCH("nnmf_vstep", st,
+                           (nnmf_vstep_kernel<T, RMAX, 2><<<P.nvb, kThreads, 0, st>>>(
+                               X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
+                               res_out)));
+                return;
+            }
+        }
+            MMK_LAUNCH("nnmf_vstep", st,
+                       (nnmf_vstep_kernel<T, RMAX, 1><<<P.nvb, kThreads, 0, st>>>(
+                           X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
+                           res_out)));
+    }
+    static void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r,
+                      const Plan& P, const Ws& L, double* red, cudaStream_t st) {
+        dim3 grid(P.colblocks, P.S);
+        double* dst = P.S > 1 ? L.wpart : red;
+        MMK_LAUNCH("nnmf_wpart", st,
+                   (nnmf_wpart_kernel<T, RMAX><<<grid, kThreads, 0, st>>>(
+                       X, ldx, V, m, n, r, P.rows_per_split, dst)));
+        if (P.S > 1) {
+            const long long len = (long long)r * n;
+            MMK_LAUNCH("nnmf_wreduce", st,
+                       (nnmf_wreduce_kernel<<<ceil_div(len, 256), 256, 0, st>>>(L.wpart, P.S,
+                                                                               len, red)));
+        }
+    }
+};
+
+// Runs `fn<T, RMAX>()` for the rank bucket of r.
+template <typename T, template <typename, int> class F, typename... A>
+int dispatch_rank(int r, A... args) {
+    if (r <= 4) return F<T, 4>::run(args...);
+    if (r <= 8) return F<T, 8>::run(args...);
+    if (r <= 16) return F<T, 16>::run(args...);
+    if (r <= 32) return F<T, 32>::run(args...);
+    if (r <= 64) return F<T, 64>::run(args...);
+    return F<T, 128>::run(args...);
+}
+
+struct Args {
+    const void *X, *V, *W;
+    void *V_out, *W_out;
+    long long ldx, m, n;
+    int r;
+    void* ws;
+    double* red;
+    double* f_dev;
+    int64_t* err;
+    cudaStream_t st;
+    int mode;  // 0 iter_a, 1 update_v, 2 objective, 3 update_w (a + b)
+};
+
+template <typename T, int RMAX>
+struct RunA {
+    static int run(const Args& a) {
+        const Plan P = make_plan(a.m, a.n, a.r);
+        Ws L;
+        ws_layout(P, a.m, a.n, a.r, a.ws, &L);
+        using KK = K<T, RMAX>;
+        const T* X = (const T*)a.X;
+        const T* V = (const T*)a.V;
+        const T* W = (const T*)a.W;
+        const long long rn = (long long)a.r * a.n;
+        if (a.mode == 0 || a.mode == 1 || a.mode == 2) {
+            if (a.m > 0) {
+                if (a.mode != 2) KK::gram_w(W, a.n, a.r, P, L, a.st);
+                int flags = (a.mode == 0) ? (VSTEP_UPDATE | VSTEP_RESID)
+                                          : (a.mode == 1 ? VSTEP_UPDATE : VSTEP_RESID);
+                double* res_out = a.mode == 0 ? a.red + rn + (long long)a.r * a.r : a.f_dev;
+                KK::vstep(X, a.ldx, V, W, (T*)a.V_out, a.m, a.n, a.r, flags, P, L, res_out, a.st);
+            } else if (a.mode == 0) {
+                cudaMemsetAsync(a.red + rn + (long long)a.r * a.r, 0, sizeof(double), a.st);
+            } else if (a.mode == 2) {
+                cudaMemsetAsync(a.f_dev, 0, sizeof(double), a.st);
+            }
+            MMK_CHECK_LAUNCH("nnmf_vstep");
+        }
+        if (a.mode == 0 || a.mode == 3) {
+            // W step uses the new V for iter_a, the given V for update_w
+            const T* Vn = a.mode == 0 ? (const T*)a.V_out : V;
+            if (a.m > 0) {
+                KK::gram_v(Vn, a.m, a.r, P, L, a.red + rn, a.st);
+                KK::wpart(X, a.ldx, Vn, a.m, a.n, a.r, P, L, a.red, a.st);
+            } else {
+                cudaMemsetAsync(a.red, 0, sizeof(double) * (size_t)(rn + (long long)a.r * a.r),
+                                a.st);
+            }
+            if (a.mode == 3)
+                cudaMemsetAsync(a.red + rn + (long long)a.r * a.r, 0, sizeof(double), a.st);
+            MMK_CHECK_LAUNCH("nnmf_wstep");
+        }
+        return MMK_OK;
+    }
+};
+
+template <typename T>
+int finish_b(const void* W, void* W_out, long long n, int r, const double* red, double* f_dev,
+             cudaStream_t st) {
+    const long long rn = (long long)r * n;
+    MMK_LAUNCH("nnmf_wfinish", st,
+               (nnmf_wfinish_kernel<T><<<ceil_div(rn, 256), 256, 0, st>>>(
+                   (const T*)W, (T*)W_out, n, r, red, f_dev)));
+    MMK_CHECK_LAUNCH("nnmf_wfinish_kernel");
+    return MMK_OK;
+}
+
+int check(int dtype, long long m, long long n, long long r, long long ldx, size_t ws_bytes) {
+    if (dtype != MMK_F32 && dtype != MMK_F64) {
+        mmk_host::set_error("unknown dtype %d", dtype);
+        return MMK_E_SHAPE;
+    }
+    if (r < 1 || r > kMaxRank || n < 1 || m < 0 || ldx < n) {
+        mmk_host::set_error("unsupported NNMF shape m=%lld n=%lld r=%lld ldx=%lld (rank <= %d)",
+                            m, n, r, ldx, kMaxRank);
+        return MMK_E_SHAPE;
+    }
+    const Plan P = make_plan(m, n, (int)r);
+    const size_t need = ws_layout(P, m, n, (int)r, nullptr, nullptr);
+    if (ws_bytes < need) {
+        mmk_host::set_error("NNMF workspace too small: %zu < %zu", ws_bytes, need);
+        return MMK_E_SHAPE;
+    }
+    return MMK_OK;
+}
+
+int run_a(int dtype, Args a) {
+    if (dtype == MMK_F32) return dispatch_rank<float, RunA>(a.r, a);
+    return dispatch_rank<double, RunA>(a.r, a);
+}
+
+}  // namespace
+
+extern "C" int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t* out) {
+    (void)dtype;
+    if (r < 1 || r > kMaxRank || n < 1) {
+        mmk_host::set_error("unsupported NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
+        return MMK_E_SHAPE;
+    }
+    const Plan P = make_plan(m, n, (int)r);
+    *out = ws_layout(P, m, n, (int)r, nullptr, nullptr);
+    return MMK_OK;
+}
+
+extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 1; }
+
+extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void* V,
+                               const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
+                               void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
+                               void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    if (rc) return rc;
+    Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
+           reinterpret_cast<cudaStream_t>(stream), 0};
+    return run_a(dtype, a);
+}
+
+extern "C" int mmk_nnmf_iter_b(int dtype, const void* W, void* W_out, int64_t n, int64_t r,
+                               const double* red, double* f_dev, int64_t* err_dev, void* stream) {
+    (void)err_dev;
+    if (r < 1 || n < 1) {
+        mmk_host::set_error("bad NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
+        return MMK_E_SHAPE;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == MMK_F32) return finish_b<float>(W, W_out, n, (int)r, red, f_dev, st);
+    if (dtype == MMK_F64) return finish_b<double>(W, W_out, n, (int)r, red, f_dev, st);
+    mmk_host::set_error("unknown dtype %d", dtype);
+    return MMK_E_SHAPE;
+}
+
+extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* V, const void* W,
+                             void* V_out, void* W_out, int64_t m, int64_t n, int64_t r, void* ws,
+                             size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
+                             void* stream) {
+    int rc = mmk_nnmf_iter_a(dtype, X, ldx, V, W, V_out, m, n, r, ws, ws_bytes, red, err_dev,
+                             stream);
+    if (rc) return rc;
+    return mmk_nnmf_iter_b(dtype, W, W_out, n, r, red, f_dev, err_dev, stream);
+}
+
+extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const void* V,
+                                  const void* W, int64_t m, int64_t n, int64_t r, void* ws,
+                                  size_t ws_bytes, double* f_dev, int64_t* err_dev, void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    if (rc) return rc;
+    Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, nullptr, f_dev, err_dev,
+           reinterpret_cast<cudaStream_t>(stream), 2};
+    return run_a(dtype, a);
+}
+
+extern "C" int mmk_nnmf_update_v(int dtype, const void* X, int64_t ldx, const void* V,
+                                 const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
+                                 void* ws, size_t ws_bytes, int64_t* err_dev, void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    if (rc) return rc;
+    Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, nullptr, nullptr, err_dev,
+           reinterpret_cast<cudaStream_t>(stream), 1};
+    return run_a(dtype, a);
+}
+
+extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const void* V,
+                                 const void* W, void* W_out, int64_t m, int64_t n, int64_t r,
+                                 void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
+                                 void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    if (rc) return rc;
+    Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
+           reinterpret_cast<cudaStream_t>(stream), 3};
+    rc = run_a(dtype, a);
+    if (rc) return rc;
+    return mmk_nnmf_iter_b(dtype, W, W_out, n, r, red, nullptr, err_dev, stream);
+}

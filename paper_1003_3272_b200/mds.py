@@ -1,0 +1,280 @@
+"""Multidimensional scaling by stress majorization, on the GPU.
+
+Drop-in for the reference's MDS path (``pkg/src/mmkit/mds.py``):
+
+  MdsProblem            mds.py:23-67    same validation + weighted_diss / weight_sums
+  stress                mds.py:92-102   sum_{i<j} w_ij (y_ij - d_ij)^2
+  mds_update            mds.py:114-144  separated per-point MM update
+  mds_run               mds.py:245-257  uniform[-1,1] start, optional anchoring
+  anchor_configuration  mds.py:202-225  post-hoc rigid motion (host, dim x dim)
+
+The configuration theta is dim x n ("p x q" in the reference): row k holds
+coordinate k of every point, which is also the coalesced layout the pairwise
+kernel wants.  Stress and update are computed by ``csrc/mds.cu`` directly
+from coordinate differences; no n x n matrix is ever formed on the device.
+Unit weights (W = 1 - I, what the CLI always builds) are detected once and
+never uploaded.  ``stress_gradient`` / ``mds_surrogate`` are host fp64
+property-test helpers.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _arrays as A
+from . import _lib
+from ._engine import DeviceMm
+from .backend import SERIAL
+from .datasets import votes_to_dissimilarity  # noqa: F401  (re-export)
+from .driver import run_mm
+from .errors import DomainError, InputError, NumericsError, ShapeError
+
+__all__ = ["MdsProblem", "stress", "stress_gradient", "mds_update", "mds_run",
+           "mds_surrogate", "anchor_configuration", "votes_to_dissimilarity"]
+
+
+def _coincide_msg(n):
+    def msg(idx):
+        i, j = divmod(idx, n)
+        return (f"objects {i} and {j} coincide but are coupled with positive "
+                "weight * dissimilarity; the surrogate is undefined there")
+    return msg
+
+
+@dataclass(frozen=True)
+class MdsProblem:
+    """Symmetric nonnegative weights and dissimilarities over q objects and
+    the embedding dimension p."""
+
+    weights: Any
+    dissimilarities: Any
+    p: int
+
+    weighted_diss: np.ndarray = field(init=False, repr=False)
+    weight_sums: np.ndarray = field(init=False, repr=False)
+    unit_weights: bool = field(init=False, repr=False)
+    _dev: dict = field(default_factory=dict, init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        w = np.ascontiguousarray(np.asarray(self.weights, dtype=np.float64))
+        y = np.ascontiguousarray(np.asarray(self.dissimilarities, dtype=np.float64))
+        if w.ndim != 2 or w.shape[0] != w.shape[1]:
+            raise ShapeError(f"weights must be square, got {w.shape}")
+        if y.shape != w.shape:
+            raise ShapeError(f"dissimilarities {y.shape} do not match weights {w.shape}")
+        for name, mat in (("weights", w), ("dissimilarities", y)):
+            if not np.all(np.isfinite(mat)):
+                raise DomainError(f"{name} contain non-finite entries")
+            if np.min(mat) < 0.0:
+                raise DomainError(f"{name} must be nonnegative")
+            if not np.array_equal(mat, mat.T):
+                raise DomainError(f"{name} must be exactly symmetric")
+            if np.any(np.diag(mat) != 0.0):
+                raise DomainError(f"{name} must have a zero diagonal")
+        if self.p < 1:
+            raise InputError(f"embedding dimension must be >= 1, got {self.p}")
+        sums = w.sum(axis=1)
+        lonely = np.flatnonzero(sums == 0.0)
+        if lonely.size:
+            raise DomainError(f"object {lonely[0]} has zero total weight; its position "
+                              "is undefined")
+        unit = bool(np.array_equal(w, 1.0 - np.eye(w.shape[0])))
+        s = object.__setattr__
+        s(self, "weights", w)
+        s(self, "dissimilarities", y)
+        s(self, "weighted_diss", w * y)
+        s(self, "weight_sums", sums)
+        s(self, "unit_weights", unit)
+
+    @property
+    def q(self):
+        return self.weights.shape[0]
+
+    def device_arrays(self, backend, torch):
+        key = (str(backend.torch_device()), backend.dtype)
+        d = self._dev.get(key)
+        if d is None:
+            dev = backend.torch_device()
+            d = {
+                "y": A.to_device(self.dissimilarities, backend, torch),
+                "w": None if self.unit_weights else A.to_device(self.weights, backend, torch),
+                "wsum": torch.from_numpy(self.weight_sums).to(dev),
+            }
+            self._dev[key] = d
+        return d
+
+
+def _check_theta(theta, problem):
+    shp = tuple(A.shape_of(theta))
+    if len(shp) != 2 or shp != (problem.p, problem.q):
+        raise ShapeError(f"configuration must be {problem.p}x{problem.q}, got {shp}")
+
+
+class _GpuMds(DeviceMm):
+    direction = "minimize"
+
+    def __init__(self, problem, backend):
+        super().__init__(backend)
+        torch = self.torch
+        self.problem = problem
+        d = problem.device_arrays(backend, torch)
+        self.y, self.w, self.wsum = d["y"], d["w"], d["wsum"]
+        self.n, self.dim = problem.q, problem.p
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_mds_ws_bytes", self.code, self.n, self.dim,
+                                            self.n), dtype=torch.uint8, device=self.device)
+
+    def device_state(self, theta):
+        return A.to_device(theta, self.backend, self.torch)
+
+    def _alloc_like(self, s):
+        return self.torch.empty_like(s)
+
+    def _copy_into(self, dst, src):
+        dst.copy_(src)
+
+    def _bytes_per_iter(self):
+        k = 1 if self.w is None else 2
+        return float(k * self.n * self.n * self.y.element_size())
+
+    def _messages(self):
+        return {1: _coincide_msg(self.n)}
+
+    def _iterate(self, theta, out, f_ptr, err_ptr,
+                 flags=_lib.MMK_MDS_UPDATE | _lib.MMK_MDS_OBJECTIVE):
+        _lib.call("mmk_mds_iter", self.code, _lib.ptr(self.y), _lib.ptr(self.w), self.n,
+                  _lib.ptr(self.wsum), _lib.ptr(theta), _lib.ptr(out), self.n, self.dim, self.n,
+                  0, self.n, flags, _lib.ptr(self.ws), self.ws.numel(), f_ptr, err_ptr,
+                  self.stream())
+
+    def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
+        self._keep = (a, b)
+        _lib.call("mmk_mds_engine_create", self.code, _lib.ptr(self.y), _lib.ptr(self.w), self.n,
+                  _lib.ptr(self.wsum), _lib.ptr(a), _lib.ptr(b), None, None, self.dim, self.n, 0,
+                  self.n, self.n, _lib.ptr(self.ws), self.ws.numel(), None, ctypes.byref(rule),
+                  _lib.ptr(trace), _lib.ptr(stamp), _lib.ptr(ctl), self.status.err_ptr,
+                  ctypes.byref(eng))
+
+    def stress_only(self, theta):
+        out = self.torch.empty_like(theta)
+        self._iterate(theta, out, self.status.f_ptr, self.status.err_ptr, _lib.MMK_MDS_OBJECTIVE)
+        return self._check_error()
+
+    def update_only(self, theta):
+        out = self.torch.empty_like(theta)
+        self._iterate(theta, out, self.status.f_ptr, self.status.err_ptr, _lib.MMK_MDS_UPDATE)
+        self._check_error()
+        return out
+
+    def surrogate(self, state, anchor):
+        return mds_surrogate(state, anchor, self.problem)
+
+
+def stress(theta, problem, backend=SERIAL):
+    """Weighted squared mismatch over unordered pairs."""
+    _check_theta(theta, problem)
+    mm = _GpuMds(problem, backend)
+    return mm.stress_only(mm.device_state(theta))
+
+
+def mds_update(theta, problem, backend=SERIAL):
+    """One parallel stress-majorization step (every point moves given the
+    previous configuration)."""
+    _check_theta(theta, problem)
+    mm = _GpuMds(problem, backend)
+    return A.to_user(mm.update_only(mm.device_state(theta)), theta)
+
+
+def anchor_configuration(theta):
+    """Rigid motion putting object 0 at the origin and zeroing the first p-1
+    coordinates of object 1; stress is unchanged (host, O(p^2 q))."""
+    was_torch = A.is_torch(theta)
+    t = np.ascontiguousarray(_host(theta))
+    if t.ndim != 2:
+        raise ShapeError(f"configuration must be 2-D, got {t.shape}")
+    p, q = t.shape
+    out = t - t[:, [0]]
+    if p >= 2 and q >= 2:
+        u = out[:, 1]
+        norm = float(np.sqrt(u @ u))
+        if norm != 0.0:
+            target = np.zeros(p)
+            target[-1] = -norm if u[-1] >= 0.0 else norm
+            v = u - target
+            vsq = float(v @ v)
+            if vsq != 0.0:
+                refl = np.eye(p) - (2.0 / vsq) * np.outer(v, v)
+                refl[0, :] = -refl[0, :]      # det +1: a rotation
+                out = refl @ out
+    if was_torch:
+        import torch
+        return torch.as_tensor(out, device=theta.device, dtype=theta.dtype)
+    return out
+
+
+def mds_run(problem, config, backend=SERIAL, anchor=False, theta0=None):
+    """Minimize stress from a uniform[-1, 1] start drawn with ``config.seed``
+    (or from ``theta0``); with ``anchor`` the result is rigidly moved to the
+    anchoring convention afterwards (trace unchanged)."""
+    if theta0 is None:
+        theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
+                                                            size=(problem.p, problem.q))
+    mm = _GpuMds(problem, backend)
+    state, trace = run_mm(mm, mm.device_state(theta0), config)
+    theta = A.to_user(state, problem.weights if not A.is_torch(theta0) else theta0)
+    if anchor:
+        theta = anchor_configuration(theta)
+    return theta, trace
+
+
+# ---------------------------------------------------------------------------
+def _host(a):
+    return A.to_user(a, np.empty(0)) if A.is_torch(a) else np.asarray(a, dtype=np.float64)
+
+
+def _host_d2(theta):
+    g = theta.T @ theta
+    dg = np.diag(g)
+    return np.maximum(dg[:, None] + dg[None, :] - 2.0 * g, 0.0)
+
+
+def stress_gradient(theta, problem, backend=SERIAL):
+    """Analytic stress gradient (host fp64 helper)."""
+    _check_theta(theta, problem)
+    t = _host(theta)
+    d2 = _host_d2(t)
+    w_off = problem.weights * ~np.eye(problem.q, dtype=bool)
+    bad = np.argwhere((d2 <= 0.0) & (w_off > 0.0))
+    if bad.size:
+        raise NumericsError(f"objects {bad[0][0]} and {bad[0][1]} coincide but are coupled "
+                            "with positive weight * dissimilarity; the surrogate is undefined "
+                            "there")
+    coef = np.zeros_like(w_off)
+    m = w_off > 0.0
+    coef[m] = w_off[m] * (1.0 - problem.dissimilarities[m] / np.sqrt(d2[m]))
+    return 2.0 * (t * coef.sum(axis=1)[None, :] - t @ coef)
+
+
+def mds_surrogate(theta, theta_n, problem):
+    """Stress majorizer at (theta | theta_n), constants kept (host fp64)."""
+    _check_theta(theta, problem)
+    _check_theta(theta_n, problem)
+    t, tn = _host(theta), _host(theta_n)
+    w, y = problem.weights, problem.dissimilarities
+    total = 0.0
+    for i in range(problem.q):
+        for j in range(i + 1, problem.q):
+            if w[i, j] == 0.0 and y[i, j] == 0.0:
+                continue
+            gap_n = tn[:, i] - tn[:, j]
+            dist_n = float(np.sqrt(gap_n @ gap_n))
+            total += w[i, j] * y[i, j] ** 2
+            if w[i, j] * y[i, j] > 0.0:
+                if dist_n == 0.0:
+                    raise NumericsError(f"objects {i} and {j} coincide at the anchor point")
+                total -= 2.0 * w[i, j] * y[i, j] * float((t[:, i] - t[:, j]) @ gap_n) / dist_n
+            c = 0.5 * (tn[:, i] + tn[:, j])
+            di, dj = t[:, i] - c, t[:, j] - c
+            total += 2.0 * w[i, j] * (float(di @ di) + float(dj @ dj))
+    return total

@@ -1,0 +1,110 @@
+"""Multi-GPU sharding of the MM iterations (one process per GPU).
+
+SURVEY.md section 8(e): the paths shard where the math does --
+
+* NNMF: rows of X and V are split across ranks, W is replicated.  The V step
+  is rank-local; the W step needs sum_rows V'^T X and V'^T V', so phase A of
+  ``mmk_nnmf_iter_a`` leaves this rank's [P | G_V | f] partials in a fp64
+  buffer, one NCCL all-reduce (sum) combines them, and phase B finishes W'
+  redundantly on every rank (no broadcast).
+* MDS: points (rows of Y) are split; each rank updates its own points from
+  the full previous configuration, then the coordinates are all-gathered and
+  the stress partials all-reduced.
+* PET: rays are split; the back-projection vector and loglik partial (the
+  phase-A buffer) are all-reduced before the pixel update.
+
+``shard_rows`` is the row partition shared by all three.  The collectives
+are issued on the compute stream through ``torch.distributed`` (NCCL over
+NVLink/NVSwitch on the B200 box, gloo in the CPU tests).
+"""
+
+import numpy as np
+
+
+def shard_rows(n, world, rank):
+    """Contiguous near-equal row range [lo, hi) of rank ``rank``; the first
+    ``n % world`` ranks get one extra row (the reference's partition rule,
+    kernels.py:79-89)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def padded_rows(n, world):
+    """Equal-size padded shard length used for all-gathers."""
+    return -(-n // world)
+
+
+def allreduce_sum_(t, group=None):
+    import torch.distributed as dist
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def nccl_comm_ptr(group=None):
+    """ncclComm_t of torch's process group (for the in-graph collectives of
+    the fused engine); None when the backend is not NCCL."""
+    import torch
+    import torch.distributed as dist
+    try:
+        pg = group or dist.distributed_c10d._get_default_group()
+        backend = pg._get_backend(torch.device("cuda"))
+        return int(backend._comm_ptr())
+    except Exception:
+        return None
+
+
+class ShardedNnmf:
+    """Row-sharded Frobenius NNMF on this rank's GPU: X_local (rows lo:hi),
+    V_local, W replicated.  ``iterate`` = phase A, all-reduce, phase B."""
+
+    def __init__(self, x_local, v_local, w, rank_of_r, backend, group=None):
+        from . import _lib
+        torch = _lib.torch_mod()
+        self.torch, self.backend, self.group = torch, backend, group
+        self.code = _lib.dtype_code(backend.torch_dtype())
+        self.x = x_local
+        self.m, self.n = x_local.shape
+        self.r = rank_of_r
+        dev = x_local.device
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_ws_bytes", self.code, max(self.m, 1), self.n,
+                                            self.r), dtype=torch.uint8, device=dev)
+        self.red = torch.zeros(_lib.load().mmk_nnmf_reduce_len(self.n, self.r),
+                               dtype=torch.float64, device=dev)
+        self.status = _lib.StatusBlock(torch, dev)
+        self.v = [v_local, torch.empty_like(v_local)]
+        self.w = [w, torch.empty_like(w)]
+        self.cur = 0
+        self._lib = _lib
+
+    def iterate(self, world):
+        L = self._lib
+        a, b = self.cur, 1 - self.cur
+        st = L.stream_handle(self.torch, self.x.device)
+        L.call("mmk_nnmf_iter_a", self.code, L.ptr(self.x), self.x.stride(0), L.ptr(self.v[a]),
+               L.ptr(self.w[a]), L.ptr(self.v[b]), self.m, self.n, self.r, L.ptr(self.ws),
+               self.ws.numel(), L.ptr(self.red), self.status.err_ptr, st)
+        if world > 1:
+            allreduce_sum_(self.red, self.group)
+        L.call("mmk_nnmf_iter_b", self.code, L.ptr(self.w[a]), L.ptr(self.w[b]), self.n, self.r,
+               L.ptr(self.red), self.status.f_ptr, self.status.err_ptr, st)
+        self.cur = b
+
+    def objective_ptr(self):
+        return self.status.f_ptr
+
+
+def phase_a_model(x, v, w):
+    """Host fp64 model of phase A's buffer for one shard (tests only)."""
+    q = x @ w.T
+    g_w = w @ w.T
+    v2 = v * (q / (v @ g_w + 1e-300))
+    f = float(np.sum((x - v @ w) ** 2))
+    return v2, np.concatenate([(v2.T @ x).ravel(), (v2.T @ v2).ravel(), [f]])
+
+
+def phase_b_model(w, red, n, r):
+    p = red[:r * n].reshape(r, n)
+    g = red[r * n:r * n + r * r].reshape(r, r)
+    return w * (p / (g @ w + 1e-300)), red[-1]

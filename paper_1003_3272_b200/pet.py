@@ -1,0 +1,306 @@
+"""Penalized PET reconstruction by Poisson MM, on the GPU.
+
+Drop-in for the reference's reconstruction path (``pkg/src/mmkit/pet.py``):
+
+  PetProblem               pet.py:213-285  same validation + derived arrays
+  pet_loglik               pet.py:318-323
+  pet_penalized_objective  pet.py:341-346
+  pet_update               pet.py:363-417  (EM for mu = 0, positive root else)
+  pet_run                  pet.py:477-480  flat start lam = 1
+  INTENSITY_FLOOR          pet.py:36       (fp32 storage floors at FLT_MIN)
+
+One MM iteration = one pass over E in libmmk.so (``csrc/pet.cu``): forward
+projection, count ratio, loglik, back-projection, pixel update and penalty.
+Geometry / phantom / count simulation are host-side input builders
+(``datasets``); ``pet_penalized_gradient`` and ``pet_surrogate`` are host
+fp64 property-test helpers.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _arrays as A
+from . import _lib
+from ._engine import DeviceMm
+from .backend import SERIAL
+from .datasets import (PetGeometry, build_neighborhoods, build_system_matrix,  # noqa: F401
+                       default_phantom, simulate_counts)
+from .driver import run_mm
+from .errors import DomainError, NumericsError, ShapeError
+
+__all__ = ["PetGeometry", "PetProblem", "build_system_matrix", "build_neighborhoods",
+           "simulate_counts", "default_phantom", "pet_loglik", "pet_penalized_objective",
+           "pet_penalized_gradient", "pet_update", "pet_run", "pet_surrogate"]
+
+INTENSITY_FLOOR = 1e-300
+
+_MSG = {
+    1: lambda i: ("a ray with positive counts has zero expected counts; the "
+                  f"loglikelihood is -inf (ray {i})"),
+    2: lambda j: ("negative discriminant in the penalized intensity update; this indicates "
+                  f"a bug, not a data problem (pixel {j})"),
+}
+
+
+@dataclass(frozen=True)
+class PetProblem:
+    """System matrix E (rays x pixels, unit l1 columns), counts y, penalty mu
+    and the pixel adjacency lists."""
+
+    e: Any
+    y: Any
+    mu: float
+    neighborhoods: list
+
+    col_sums: np.ndarray = field(init=False, repr=False)
+    degrees: np.ndarray = field(init=False, repr=False)
+    nbr_indptr: np.ndarray = field(init=False, repr=False)
+    nbr_indices: np.ndarray = field(init=False, repr=False)
+    pair_left: np.ndarray = field(init=False, repr=False)
+    pair_right: np.ndarray = field(init=False, repr=False)
+    _dev: dict = field(default_factory=dict, init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        e, y = self.e, self.y
+        if not A.is_torch(e):
+            e = np.ascontiguousarray(np.asarray(e, dtype=np.float64))
+        if not A.is_torch(y):
+            y = np.asarray(y, dtype=np.float64)
+        if e.ndim != 2:
+            raise ShapeError(f"system matrix must be 2-D, got {tuple(e.shape)}")
+        if y.ndim != 1 or y.shape[0] != e.shape[0]:
+            raise ShapeError(f"counts shape {tuple(y.shape)} does not match {e.shape[0]} rays")
+        if A.min_value(e) < 0.0:
+            raise DomainError("detection coefficients must be nonnegative")
+        if A.min_value(y) < 0.0:
+            raise DomainError("counts must be nonnegative")
+        if self.mu < 0.0:
+            raise DomainError(f"penalty constant must be >= 0, got {self.mu}")
+        col = (e.double().sum(dim=0).cpu().numpy() if A.is_torch(e) else e.sum(axis=0))
+        if np.max(np.abs(col - 1.0)) > 1e-8:
+            raise DomainError("system matrix columns must have unit l1 norm "
+                              "(normalize as build_system_matrix does)")
+        p = e.shape[1]
+        if len(self.neighborhoods) != p:
+            raise ShapeError(f"{len(self.neighborhoods)} neighborhoods for {p} pixels")
+        members = [set(a) for a in self.neighborhoods]
+        pairs = set()
+        for j, around in enumerate(self.neighborhoods):
+            for k in around:
+                if k == j:
+                    raise DomainError(f"pixel {j} lists itself as a neighbor")
+                if j not in members[k]:
+                    raise DomainError(f"neighborhood is not symmetric: {k} in N({j}) but "
+                                      f"{j} not in N({k})")
+                pairs.add((min(j, k), max(j, k)))
+        pairs = sorted(pairs)
+        indptr = np.zeros(p + 1, dtype=np.int64)
+        indptr[1:] = np.cumsum([len(a) for a in self.neighborhoods])
+        indices = np.fromiter((k for a in self.neighborhoods for k in a), dtype=np.int64,
+                              count=int(indptr[-1]))
+        s = object.__setattr__
+        s(self, "e", e)
+        s(self, "y", y)
+        s(self, "col_sums", col)
+        s(self, "degrees", np.diff(indptr).astype(np.float64))
+        s(self, "nbr_indptr", indptr)
+        s(self, "nbr_indices", indices)
+        s(self, "pair_left", np.array([a for a, _ in pairs], dtype=np.int64))
+        s(self, "pair_right", np.array([b for _, b in pairs], dtype=np.int64))
+
+    @property
+    def n_pixels(self):
+        return self.e.shape[1]
+
+    @property
+    def n_rays(self):
+        return self.e.shape[0]
+
+    @property
+    def e_t(self):
+        """Transposed view of E (the reference stores a dense copy; the GPU
+        kernels back-project from E directly)."""
+        return self.e.T
+
+    def device_arrays(self, backend, torch):
+        key = (str(backend.torch_device()), backend.dtype)
+        d = self._dev.get(key)
+        if d is None:
+            dev = backend.torch_device()
+            d = {
+                "e": A.to_device(self.e, backend, torch),
+                "y": A.to_device(self.y, backend, torch),
+                "ptr": torch.from_numpy(self.nbr_indptr.astype(np.int32)).to(dev),
+                "idx": torch.from_numpy(self.nbr_indices.astype(np.int32)).to(dev),
+            }
+            if d["idx"].numel() == 0:
+                d["idx"] = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._dev[key] = d
+        return d
+
+
+class _GpuPet(DeviceMm):
+    direction = "maximize"
+
+    def __init__(self, problem, backend, rows=None):
+        super().__init__(backend)
+        torch = self.torch
+        self.problem = problem
+        d = problem.device_arrays(backend, torch)
+        self.e, self.y, self.ptr, self.idx = d["e"], d["y"], d["ptr"], d["idx"]
+        if rows is not None:          # ray shard [lo, hi) of a distributed run
+            lo, hi = rows
+            self.e, self.y = self.e[lo:hi], self.y[lo:hi]
+        self.d, self.p = self.e.shape
+        self.mu = float(problem.mu)
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_pet_ws_bytes", self.code, max(self.d, 1), self.p),
+                              dtype=torch.uint8, device=self.device)
+        self.red = torch.zeros(_lib.load().mmk_pet_reduce_len(self.p), dtype=torch.float64,
+                               device=self.device)
+
+    def device_state(self, lam):
+        return A.to_device(lam, self.backend, self.torch)
+
+    def _alloc_like(self, s):
+        return self.torch.empty_like(s)
+
+    def _copy_into(self, dst, src):
+        dst.copy_(src)
+
+    def _bytes_per_iter(self):
+        return float(self.d * self.p * self.e.element_size())
+
+    def _messages(self):
+        return _MSG
+
+    def _iterate(self, lam, out, f_ptr, err_ptr, flags=_lib.MMK_PET_UPDATE | _lib.MMK_PET_OBJECTIVE):
+        _lib.call("mmk_pet_iter", self.code, _lib.ptr(self.e), self.e.stride(0), _lib.ptr(self.y),
+                  _lib.ptr(lam), _lib.ptr(out), self.d, self.p, _lib.ptr(self.ptr),
+                  _lib.ptr(self.idx), self.mu, flags, _lib.ptr(self.ws), self.ws.numel(),
+                  _lib.ptr(self.red), f_ptr, err_ptr, self.stream())
+
+    def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
+        self._keep = (a, b)
+        _lib.call("mmk_pet_engine_create", self.code, _lib.ptr(self.e), self.e.stride(0),
+                  _lib.ptr(self.y), _lib.ptr(a), _lib.ptr(b), self.d, self.p, _lib.ptr(self.ptr),
+                  _lib.ptr(self.idx), self.mu, _lib.ptr(self.ws), self.ws.numel(),
+                  _lib.ptr(self.red), self.comm, ctypes.byref(rule), _lib.ptr(trace),
+                  _lib.ptr(stamp), _lib.ptr(ctl), self.status.err_ptr, ctypes.byref(eng))
+
+    def objective_only(self, lam):
+        out = self.torch.empty_like(lam)
+        self._iterate(lam, out, self.status.f_ptr, self.status.err_ptr, _lib.MMK_PET_OBJECTIVE)
+        return self._check_error()
+
+    def update_only(self, lam):
+        out = self.torch.empty_like(lam)
+        self._iterate(lam, out, self.status.f_ptr, self.status.err_ptr, _lib.MMK_PET_UPDATE)
+        self._check_error()
+        return out
+
+    def surrogate(self, state, anchor):
+        return pet_surrogate(state, anchor, self.problem)
+
+
+def _check_lam(lam, problem):
+    if tuple(A.shape_of(lam)) != (problem.n_pixels,):
+        raise ShapeError(f"intensities shape {tuple(A.shape_of(lam))} does not match "
+                         f"{problem.n_pixels} pixels")
+
+
+def pet_penalized_objective(lam, problem, backend=SERIAL):
+    """Loglikelihood minus (mu/2) * sum of squared adjacent differences."""
+    _check_lam(lam, problem)
+    mm = _GpuPet(problem, backend)
+    return mm.objective_only(mm.device_state(lam))
+
+
+def pet_loglik(lam, e, y, backend=SERIAL):
+    """Poisson loglikelihood sum_i [y_i ln (E lam)_i - (E lam)_i]."""
+    e_arr = e if A.is_torch(e) else np.asarray(e, dtype=np.float64)
+    if len(A.shape_of(e_arr)) != 2 or A.shape_of(lam)[0] != e_arr.shape[1]:
+        raise ShapeError("system matrix does not match intensities")
+    prob = _LooseProblem(e_arr, y)
+    mm = _GpuPet(prob, backend)
+    return mm.objective_only(mm.device_state(lam))
+
+
+class _LooseProblem:
+    """Unvalidated (E, y) pair for pet_loglik, which the reference also
+    accepts without the unit-column check (pet.py:318-323)."""
+
+    def __init__(self, e, y):
+        self.e = e
+        self.y = y if A.is_torch(y) else np.asarray(y, dtype=np.float64)
+        self.mu = 0.0
+        self._dev = {}
+        p = e.shape[1]
+        self.nbr_indptr = np.zeros(p + 1, dtype=np.int64)
+        self.nbr_indices = np.zeros(0, dtype=np.int64)
+
+    device_arrays = PetProblem.device_arrays
+
+
+def pet_update(lam, problem, backend=SERIAL, mean_counts=None):
+    """One surrogate-maximization step from strictly positive intensities.
+    ``mean_counts`` is accepted for signature compatibility; the device pass
+    recomputes E @ lam as part of the same sweep over E."""
+    _check_lam(lam, problem)
+    lam_np = A.to_user(lam, np.empty(0)) if A.is_torch(lam) else np.asarray(lam, dtype=np.float64)
+    if np.min(lam_np) <= 0.0:
+        bad = int(np.argmin(lam_np))
+        raise DomainError(f"intensities must be strictly positive; pixel {bad} is "
+                          f"{lam_np[bad]!r}")
+    mm = _GpuPet(problem, backend)
+    return A.to_user(mm.update_only(mm.device_state(lam)), lam)
+
+
+def pet_run(problem, config, backend=SERIAL):
+    """Maximize the penalized loglikelihood from the flat start lam = 1."""
+    mm = _GpuPet(problem, backend)
+    like = problem.e
+    state, trace = run_mm(mm, mm.device_state(np.ones(problem.n_pixels)), config)
+    return A.to_user(state, like), trace
+
+
+# ---------------------------------------------------------------------------
+# host-side fp64 helpers for property tests (not on the iteration path)
+def _host(a):
+    return A.to_user(a, np.empty(0)) if A.is_torch(a) else np.asarray(a, dtype=np.float64)
+
+
+def pet_penalized_gradient(lam, problem, backend=SERIAL):
+    """Analytic gradient of the penalized objective (host fp64)."""
+    lam, e, y = _host(lam), _host(problem.e), _host(problem.y)
+    means = e @ lam
+    if np.any((y > 0.0) & (means == 0.0)):
+        raise NumericsError("a ray with positive counts has zero expected counts")
+    ratio = np.where(y > 0.0, y / np.where(y > 0.0, means, 1.0), 0.0)
+    grad = e.T @ ratio - problem.col_sums
+    if problem.mu > 0.0:
+        nbr = np.array([lam[a].sum() if len(a) else 0.0 for a in problem.neighborhoods])
+        grad -= problem.mu * (problem.degrees * lam - nbr)
+    return grad
+
+
+def pet_surrogate(lam, lam_n, problem):
+    """Minorizing surrogate at (lam | lam_n): Jensen on each log plus the
+    even-convex bound on each squared difference (host fp64)."""
+    lam, lam_n, e, y = _host(lam), _host(lam_n), _host(problem.e), _host(problem.y)
+    mean_n = e @ lam_n
+    if np.any((y > 0.0) & (mean_n == 0.0)):
+        raise NumericsError("anchor point has zero expected counts on a ray with positive counts")
+    value = -float(e.sum(axis=0) @ lam)
+    for i in np.flatnonzero(y > 0.0):
+        wts = e[i] * lam_n / mean_n[i]
+        m = wts > 0.0
+        value += y[i] * float(wts[m] @ np.log(e[i, m] * lam[m] / wts[m]))
+    if problem.mu > 0.0:
+        lj, rk = problem.pair_left, problem.pair_right
+        mid = lam_n[lj] + lam_n[rk]
+        value -= 0.25 * problem.mu * float(np.sum((2.0 * lam[lj] - mid) ** 2 +
+                                                  (2.0 * lam[rk] - mid) ** 2))
+    return value

@@ -1,0 +1,58 @@
+"""Golden fixtures (tests/golden/*.npz, made by tests/golden/make_golden.py
+from the reference itself) and the seeded input recipes they were made on."""
+
+import hashlib
+import os
+
+import numpy as np
+
+from paper_1003_3272_b200 import datasets as D
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(HERE, name + ".npz"))
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def c1_inputs():
+    x = f32(np.random.default_rng(0).random((2429, 361)))
+    g = np.random.default_rng(1)
+    return x, f32(g.random((2429, 10))), f32(g.random((10, 361)))
+
+
+_C2 = {}
+
+
+def c2_inputs():
+    if not _C2:
+        e = D.build_system_matrix(D.PetGeometry(64, 64))
+        y = D.simulate_counts(D.default_phantom(64), e, 20260811)
+        _C2.update(e=e, y=y, nbrs=D.build_neighborhoods(64))
+    return _C2["e"], _C2["y"], _C2["nbrs"]
+
+
+def c3_inputs(dim):
+    diss = f32(D.votes_to_dissimilarity(D.synthetic_votes(401, 671, 0)))
+    theta0 = f32(np.random.default_rng(1).uniform(-1.0, 1.0, size=(dim, 401)))
+    return diss, theta0
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def rel_elem(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
