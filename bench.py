@@ -264,16 +264,22 @@ def bench_nnmf_large(args, torch, world, rank, dev):
     lib.mmk_prof_enable(0)
     prof = _lib.prof_report()
     es = x.element_size()
-    alg = {  # algorithmic bytes per launch
-        "nnmf_vstep": (hi - lo) * n * es + 2 * (hi - lo) * r * es + r * n * es,
-        "nnmf_wpart": (hi - lo) * n * es + (hi - lo) * r * es,
+    ml = hi - lo
+    alg = {  # algorithmic HBM bytes per launch
+        "nnmf_vstep": ml * n * es + 2 * ml * r * es + r * n * es,
+        "nnmf_wpart": ml * n * es + ml * r * es,
+        # X once + V read + V', V'_hi, V'_lo written + W_hi/W_lo chunks (L2-resident)
+        "nnmf_vstep_tc": ml * n * 4 + 4 * ml * r * 4 + 2 * r * n * 4,
+        # X once + V'_hi/V'_lo read + fp32 split-K partials written
+        "nnmf_wstep_tc": ml * n * 4 + 2 * ml * r * 4,
     }
     launches = sum(c for c, _ in prof.values()) // 2
     roof = roofline(prof, alg, "hbm", "dominant")
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = nnmf_e2e(args, torch, be, x, v0, w0, r)
-    return timing, roof, launches, e2e, {"dominant_kernel_profile": prof}
+    kernels = {k: {"launches_per_step": c // 2, "avg_ms": ms / c} for k, (c, ms) in prof.items()}
+    return timing, roof, launches, e2e, {"kernels": kernels}
 
 
 def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
@@ -400,11 +406,12 @@ def run_ours(args):
     if W["solver"] != "nnmf" or not args.workload.endswith("large"):
         raise SystemExit(f"workload {args.workload} not wired into the headline bench yet")
     timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
+    extra = extra or {}
     ms = timing["ms_total"]
     value = args.steps / (ms / 1000.0)
     cpu = None
     suite_res = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, thr, sample = cpu_sample(args.workload, args.cpu_seconds)
         cpu = {"value": v, "unit": "iterations/s", "cores": thr, "kind": "port",
                "sample": sample}
@@ -421,6 +428,7 @@ def run_ours(args):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps, "clocks": timing["clocks"],
             "suite": suite_res,
+            "kernels": extra.get("kernels"),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

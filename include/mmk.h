@@ -227,6 +227,15 @@ int mmk_mds_engine_create(int dtype, const void *Y, const void *Wt, int64_t ldy,
 int mmk_engine_run(void *engine, void *stream);
 void mmk_engine_destroy(void *engine);
 
+/* Known-answer self-test of the tcgen05 building blocks (TMA 128B-swizzle
+ * tiles, K-/MN-major UMMA descriptors, kind::tf32 MMA, TMEM loads):
+ *   D1[128x64] = A[128x64] B[64x64]^T,  D2[128x32] = A B[:, :32],
+ *   D3[128x64] = X[32x128]^T V[32x64]   (device fp32, row-major).
+ * mode bits: 1 dump the raw swizzled A tile into D1, 2/4/8 run D1/D2/D3;
+ * diag (device int) gets bit 1 if the TMA barrier timed out, 2 for MMA. */
+int mmk_selftest_tc(const float *A, const float *B, const float *X, const float *V, float *D1,
+                    float *D2, float *D3, int mode, int *diag, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

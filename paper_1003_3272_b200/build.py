@@ -60,7 +60,7 @@ def build(force=False, verbose=False):
         for _, log in results:
             sys.stderr.write(log)
     objs = [o for o, _ in results]
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
     subprocess.run(cmd, check=True)
     return LIB
 

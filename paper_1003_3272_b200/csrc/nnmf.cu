@@ -20,6 +20,9 @@
 // W' redundantly on every rank.  See nnmf_tc.cu for the tcgen05 path used for
 // large r (3xTF32 contraction of X on the tensor cores).
 #include "mmk_common.cuh"
+#include "nnmf_tc.h"
+
+#include <type_traits>
 
 namespace {
 
@@ -261,7 +264,11 @@ struct Ws {
     double* respart;
     double* wpart;
     double* fscratch;
+    void* tc;                // tensor-core path scratch (fp32 rank 64 only)
 };
+
+// the tensor-core region is reserved whenever the path could apply
+bool tc_shape(long long m, long long n, int r) { return r == 64 && (n & 3) == 0 && m >= 128 && n >= 128; }
 
 Plan make_plan(long long m, long long n, int r) {
     Plan P;
@@ -298,7 +305,9 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws*
     size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
     size_t o_f = take(sizeof(double) * 4);
     size_t o_wp = take(P.S > 1 ? sizeof(double) * (size_t)P.S * r * (size_t)n : 0);
+    size_t o_tc = take(tc_shape(m, n, r) ? mmk_tc::ws_bytes(m, n) : 0);
     if (base && L) {
+        L->tc = reinterpret_cast<char*>(base) + o_tc;
         char* c = reinterpret_cast<char*>(base);
         L->counters = reinterpret_cast<unsigned int*>(c);
         L->GW = reinterpret_cast<double*>(c + o_gw);
@@ -307,7 +316,6 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws*
         L->fscratch = reinterpret_cast<double*>(c + o_f);
         L->wpart = reinterpret_cast<double*>(c + o_wp);
     }
-    (void)m;
     return off;
 }
 
@@ -394,6 +402,23 @@ struct RunA {
         const T* V = (const T*)a.V;
         const T* W = (const T*)a.W;
         const long long rn = (long long)a.r * a.n;
+        if constexpr (std::is_same<T, float>::value && RMAX == 64) {
+            if (a.mode == 0 && tc_shape(a.m, a.n, a.r) &&
+                mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
+                auto gw = [&](const float* Wp, double* out, cudaStream_t s) {
+                    MMK_LAUNCH("nnmf_gram_w", s,
+                               (gram_kernel<float, 64, true><<<P.gw_blocks, kThreads, 0, s>>>(
+                                   Wp, a.n, a.r, P.gw_cpb, L.gpart, L.counters + 1, out)));
+                };
+                auto gv = [&](const float* Vp, double* out, cudaStream_t s) {
+                    MMK_LAUNCH("nnmf_gram_v", s,
+                               (gram_kernel<float, 64, false><<<P.gv_blocks, kThreads, 0, s>>>(
+                                   Vp, a.m, a.r, P.gv_cpb, L.gpart, L.counters + 2, out)));
+                };
+                return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
+                                      a.red, gw, gv, a.st);
+            }
+        }
         if (a.mode == 0 || a.mode == 1 || a.mode == 2) {
             if (a.m > 0) {
                 if (a.mode != 2) KK::gram_w(W, a.n, a.r, P, L, a.st);

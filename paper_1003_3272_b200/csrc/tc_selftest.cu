@@ -1,0 +1,173 @@
+// tc_selftest.cu -- known-answer check of the tcgen05 building blocks the
+// NNMF tensor-core kernels rely on (TMA 128B-swizzled tiles, K-major and
+// MN-major UMMA descriptors, kind::tf32 MMA, TMEM loads).  One CTA computes
+//   D1[128x64] = A[128x64] . B[64x64]^T     (A, B K-major; the V-step's Q)
+//   D2[128x32] = A . B[:, 0:32]             (B MN-major;   the V-step residual)
+//   D3[128x64] = X[32x128]^T . V[32x64]     (A, B MN-major; the W-step's P^T)
+// in single-pass TF32; tests compare against fp64 products with a TF32
+// tolerance.
+#include "mmk_common.cuh"
+#include "tc_common.cuh"
+
+namespace {
+
+constexpr uint32_t kA = 2 * 16384, kB = 2 * 8192, kX = 4 * 4096, kV = 2 * 4096, kB32 = 8192;
+
+__global__ void __launch_bounds__(128)
+tc_selftest_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+                   const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mV,
+                   const __grid_constant__ CUtensorMap mB32,
+                   float* D1, float* D2, float* D3, int mode, int* diag) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = sA + kA;
+    uint8_t* sX = sB + kB;
+    uint8_t* sV = sX + kX;
+    uint8_t* sB32 = sV + kV;
+    __shared__ uint64_t bar_tma, bar_mma;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        tc::mbar_init(&bar_tma, 1);
+        tc::mbar_init(&bar_mma, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (tid == 0) {
+        tc::mbar_expect_tx(&bar_tma, kA + kB + kX + kV + kB32);
+        tc::tma_load_2d(sB32, &mB32, &bar_tma, 0, 0);
+        for (int b = 0; b < 2; ++b) tc::tma_load_2d(sA + b * 16384, &mA, &bar_tma, b * 32, 0);
+        for (int b = 0; b < 2; ++b) tc::tma_load_2d(sB + b * 8192, &mB, &bar_tma, b * 32, 0);
+        for (int b = 0; b < 4; ++b) tc::tma_load_2d(sX + b * 4096, &mX, &bar_tma, b * 32, 0);
+        for (int b = 0; b < 2; ++b) tc::tma_load_2d(sV + b * 4096, &mV, &bar_tma, b * 32, 0);
+    }
+    if (!tc::mbar_wait_bounded(&bar_tma, 0)) {
+        if (tid == 0) atomicOr(diag, 1);
+    }
+    if (mode & 1) {  // dump the raw (swizzled) A tile, X tile and B (32B-atom) tile
+        const float* f = reinterpret_cast<const float*>(sA);
+        for (int i = tid; i < 128 * 64; i += 128) D1[i] = f[i];
+        const float* fx = reinterpret_cast<const float*>(sX);
+        for (int i = tid; i < 128 * 32; i += 128) D3[i] = fx[i];
+        const float* fb = reinterpret_cast<const float*>(sB32);
+        for (int i = tid; i < 64 * 32; i += 128) D3[128 * 32 + i] = fb[i];
+    }
+    if (tid == 0 && (mode & 14)) {
+        tc::tc_fence_after();
+        // D1: K = 64 as 2 swizzle-atom columns x 4 K-steps of 8
+        for (int ks = 0; ks < 8 && (mode & 2); ++ks) {
+            const int kb = ks >> 2, sub = ks & 3;
+            uint64_t a = tc::sdesc_sw128(sA + kb * 16384 + sub * 32, 16, 1024);
+            uint64_t b = tc::sdesc_sw128(sB + kb * 8192 + sub * 32, 16, 1024);
+            tc::mma_tf32(tm + 0, a, b, tc::idesc_tf32(128, 64, 0, 0), ks > 0);
+        }
+        // D2: B = first 32 columns of B viewed MN-major (k = row of B)
+        for (int ks = 0; ks < 8 && (mode & 4); ++ks) {
+            const int kb = ks >> 2, sub = ks & 3;
+            uint64_t a = tc::sdesc_sw128(sA + kb * 16384 + sub * 32, 16, 1024);
+            uint64_t b = tc::sdesc_sw128_32b(sB32 + ks * 1024, 8192, 512);
+            tc::mma_tf32(tm + 64, a, b, tc::idesc_tf32(128, 32, 0, 1), ks > 0);
+        }
+        // D3: A = X^T (MN-major, 4 groups of 32 columns 4 KB apart), B = V (MN-major)
+        for (int ks = 0; ks < 4 && (mode & 8); ++ks) {
+            uint64_t a = tc::sdesc_sw128_32b(sX + ks * 1024, 4096, 512);
+            uint64_t b = tc::sdesc_sw128_32b(sV + ks * 1024, 4096, 512);
+            tc::mma_tf32(tm + 128, a, b, tc::idesc_tf32(128, 64, 1, 1), ks > 0);
+        }
+        tc::mma_commit(&bar_mma);
+    }
+    if (mode & 14) {
+        if (!tc::mbar_wait_bounded(&bar_mma, 0)) {
+            if (tid == 0) atomicOr(diag, 2);
+        }
+    }
+    tc::tc_fence_after();
+    if (!(mode & 1)) {
+        const int row = warp * 32 + lane;
+        const uint32_t lane_addr = tm + ((uint32_t)(warp * 32) << 16);
+        float v[32];
+        for (int c = 0; c < 2; ++c) {
+            tc::tmem_ld32(lane_addr + 0 + c * 32, v);
+            for (int i = 0; i < 32; ++i) D1[row * 64 + c * 32 + i] = v[i];
+        }
+        tc::tmem_ld32(lane_addr + 64, v);
+        for (int i = 0; i < 32; ++i) D2[row * 32 + i] = v[i];
+        for (int c = 0; c < 2; ++c) {
+            tc::tmem_ld32(lane_addr + 128 + c * 32, v);
+            for (int i = 0; i < 32; ++i) D3[row * 64 + c * 32 + i] = v[i];
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<256>(tm);
+}
+
+}  // namespace
+
+namespace mmk_host {
+// 2-D fp32 row-major tensor map, box = 32 columns (128 B) x box_rows, 128B swizzle
+int make_map_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                 uint64_t row_stride_elems, uint32_t box_rows, bool atom32) {
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {row_stride_elems * 4};
+    cuuint32_t box[2] = {32, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    // resolved through the runtime so libmmk.so has no link-time libcuda
+    // dependency (the CPU build container has no driver)
+    typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static encode_fn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            fn == nullptr) {
+            set_error("cuTensorMapEncodeTiled unavailable from the driver");
+            return MMK_E_CUDA;
+        }
+        encode = reinterpret_cast<encode_fn>(fn);
+    }
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                        const_cast<void*>(base), dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu stride=%llu box=%u",
+                  (int)r, (unsigned long long)rows, (unsigned long long)cols,
+                  (unsigned long long)row_stride_elems, box_rows);
+        return MMK_E_CUDA;
+    }
+    return MMK_OK;
+}
+}  // namespace mmk_host
+
+extern "C" int mmk_selftest_tc(const float* A, const float* B, const float* X, const float* V,
+                               float* D1, float* D2, float* D3, int mode, int* diag,
+                               void* stream) {
+    CUtensorMap mA, mB, mX, mV, mB32;
+    int rc;
+    if ((rc = mmk_host::make_map_f32(&mA, A, 128, 64, 64, 128))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mB, B, 64, 64, 64, 64))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mX, X, 32, 128, 128, 32, true))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mV, V, 32, 64, 64, 32, true))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mB32, B, 64, 64, 64, 64, true))) return rc;
+    const size_t smem = 1024 + kA + kB + kX + kV + kB32;
+    cudaFuncSetAttribute(tc_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    tc_selftest_kernel<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(mA, mB, mX, mV, mB32,
+                                                                                D1, D2, D3, mode,
+                                                                                diag);
+    MMK_CHECK_LAUNCH("tc_selftest_kernel");
+    return MMK_OK;
+}
