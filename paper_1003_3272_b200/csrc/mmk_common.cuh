@@ -108,7 +108,7 @@ int cuda_status(cudaError_t e, const char* what);
 bool prof_on();
 // 2-D fp32 row-major TMA map: box = 32 columns (128 B) x box_rows, 128B swizzle
 int make_map_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                 uint64_t row_stride_elems, uint32_t box_rows, bool atom32 = false);
+                 uint64_t row_stride_elems, uint32_t box_rows, int swizzle = 128);
 void prof_start(const char* name, cudaStream_t s);
 void prof_stop(cudaStream_t s);
 }  // namespace mmk_host

@@ -91,6 +91,68 @@ gram_kernel(const T* __restrict__ A, long long len, int r, int chunks_per_block,
     }
 }
 
+// Rank-64 Gram with 4x4 register tiles per thread (16 x 16 threads cover the
+// 64 x 64 output); 32 samples per smem stage.  Same deterministic split-K
+// reduction as gram_kernel.
+template <typename T, bool VEC_ROWS>
+__global__ void __launch_bounds__(kThreads)
+gram64_kernel(const T* __restrict__ A, long long len, int chunks_per_block,
+              double* __restrict__ part, unsigned int* counter, double* __restrict__ out) {
+    __shared__ double S[32][64 + 2];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const long long c_begin = (long long)blockIdx.x * chunks_per_block * 32;
+    for (int ch = 0; ch < chunks_per_block; ++ch) {
+        const long long c0 = c_begin + (long long)ch * 32;
+        if (c0 >= len) break;
+        for (int idx = threadIdx.x; idx < 32 * 64; idx += kThreads) {
+            int a, cc;
+            if (VEC_ROWS) {
+                a = idx >> 5;
+                cc = idx & 31;
+            } else {
+                cc = idx >> 6;
+                a = idx & 63;
+            }
+            const long long c = c0 + cc;
+            double v = 0.0;
+            if (c < len) v = (double)(VEC_ROWS ? A[(long long)a * len + c] : A[c * 64 + a]);
+            S[cc][a] = v;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                av[i] = S[kk][4 * ty + i];
+                bv[i] = S[kk][4 * tx + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    double* pb = part + (long long)blockIdx.x * 4096;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * 64 + 4 * tx + j] = acc[i][j];
+    if (arrive_last(counter, gridDim.x)) {
+        for (int pidx = threadIdx.x; pidx < 4096; pidx += kThreads) {
+            double sum = 0.0;
+            for (unsigned int b = 0; b < gridDim.x; ++b) sum += part[(long long)b * 4096 + pidx];
+            out[pidx] = sum;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 template <typename T, int RMAX, int RPW>
 __global__ void __launch_bounds__(kThreads)
@@ -324,12 +386,24 @@ constexpr int kMaxRank = 128;
 template <typename T, int RMAX>
 struct K {
     static void gram_w(const T* W, long long n, int r, const Plan& P, const Ws& L, cudaStream_t st) {
+        if (RMAX == 64 && r == 64) {
+            MMK_LAUNCH("nnmf_gram_w", st,
+                       (gram64_kernel<T, true><<<P.gw_blocks, kThreads, 0, st>>>(
+                           W, n, P.gw_cpb, L.gpart, L.counters + 1, L.GW)));
+            return;
+        }
         MMK_LAUNCH("nnmf_gram_w", st,
                    (gram_kernel<T, RMAX, true><<<P.gw_blocks, kThreads, 0, st>>>(
                        W, n, r, P.gw_cpb, L.gpart, L.counters + 1, L.GW)));
     }
     static void gram_v(const T* V, long long m, int r, const Plan& P, const Ws& L, double* out,
                        cudaStream_t st) {
+        if (RMAX == 64 && r == 64) {
+            MMK_LAUNCH("nnmf_gram_v", st,
+                       (gram64_kernel<T, false><<<P.gv_blocks, kThreads, 0, st>>>(
+                           V, m, P.gv_cpb, L.gpart, L.counters + 2, out)));
+            return;
+        }
         MMK_LAUNCH("nnmf_gram_v", st,
                    (gram_kernel<T, RMAX, false><<<P.gv_blocks, kThreads, 0, st>>>(
                        V, m, r, P.gv_cpb, L.gpart, L.counters + 2, out)));
@@ -407,13 +481,13 @@ struct RunA {
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
                 auto gw = [&](const float* Wp, double* out, cudaStream_t s) {
                     MMK_LAUNCH("nnmf_gram_w", s,
-                               (gram_kernel<float, 64, true><<<P.gw_blocks, kThreads, 0, s>>>(
-                                   Wp, a.n, a.r, P.gw_cpb, L.gpart, L.counters + 1, out)));
+                               (gram64_kernel<float, true><<<P.gw_blocks, kThreads, 0, s>>>(
+                                   Wp, a.n, P.gw_cpb, L.gpart, L.counters + 1, out)));
                 };
                 auto gv = [&](const float* Vp, double* out, cudaStream_t s) {
                     MMK_LAUNCH("nnmf_gram_v", s,
-                               (gram_kernel<float, 64, false><<<P.gv_blocks, kThreads, 0, s>>>(
-                                   Vp, a.m, a.r, P.gv_cpb, L.gpart, L.counters + 2, out)));
+                               (gram64_kernel<float, false><<<P.gv_blocks, kThreads, 0, s>>>(
+                                   Vp, a.m, P.gv_cpb, L.gpart, L.counters + 2, out)));
                 };
                 return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
                                       a.red, gw, gv, a.st);

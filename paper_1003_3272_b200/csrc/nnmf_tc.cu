@@ -39,43 +39,81 @@ using namespace mmk;
 
 constexpr int R = 64;            // rank of the tensor-core path (UMMA N)
 constexpr int BM = 128;          // UMMA M: rows of X (V step) / columns of X (W step)
-constexpr int BK = 32;           // K per stage: one 128-byte swizzle row of fp32
-constexpr int STAGES = 4;
+constexpr int BK = 32;           // K per stage: one 128-byte row of fp32
+constexpr int STAGES = 6;
 constexpr int kThreads = 320;    // 10 warps: TMA, MMA, 4 split, 4 epilogue
-constexpr uint32_t SX = BM * BK * 4;        // 16 KB  X tile (hi in place)
-constexpr uint32_t SXL = SX;                // 16 KB  X lo
-constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W or V' chunk (hi), same for lo
-constexpr uint32_t SSTAGE = SX + SXL + 2 * SOP;   // 48 KB
+constexpr uint32_t SX = BM * BK * 4;        // 16 KB  raw X tile
+constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W (or V') chunk hi; same again for lo
+constexpr uint32_t SSTAGE = SX + 2 * SOP;   // 32 KB
 constexpr uint32_t SMEM = STAGES * SSTAGE + 1024;
-constexpr uint32_t TX_BYTES = SX + 2 * SOP;
+constexpr uint32_t TX_BYTES = SSTAGE;
+// TMEM columns: [0,128) two fp32 accumulators (64 each), [128,256) two
+// tf32-split A buffers (hi 32 + lo 32 columns each)
+constexpr int TM_COLS = 256;
+constexpr uint32_t TM_A = 128;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// split warps: hi/lo of the stage's X tile, position-preserving (the swizzle
-// is a permutation of positions, so an elementwise rewrite keeps the layout)
-__device__ __forceinline__ double split_stage(uint8_t* st, int ct) {
-    float4* xr = reinterpret_cast<float4*>(st);
-    float4* xl = reinterpret_cast<float4*>(st + SX);
-    double xx = 0.0;
+// hi/lo split of 32 values into the TMEM A buffer of this thread's lane
+__device__ __forceinline__ void split_to_tmem(const float* x, uint32_t a_lane_addr, double& xx) {
+    float hi[32], lo[32];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-    for (int q = ct; q < (int)(SX / 16); q += 128) {
-        const float4 v = xr[q];
-        float4 h, l;
-        tc::split_tf32(v.x, h.x, l.x);
-        tc::split_tf32(v.y, h.y, l.y);
-        tc::split_tf32(v.z, h.z, l.z);
-        tc::split_tf32(v.w, h.w, l.w);
-        xr[q] = h;
-        xl[q] = l;
-        xx = fma((double)v.x, (double)v.x, xx);
-        xx = fma((double)v.y, (double)v.y, xx);
-        xx = fma((double)v.z, (double)v.z, xx);
-        xx = fma((double)v.w, (double)v.w, xx);
+    for (int i = 0; i < 32; i += 4) {
+        tc::split_tf32(x[i], hi[i], lo[i]);
+        tc::split_tf32(x[i + 1], hi[i + 1], lo[i + 1]);
+        tc::split_tf32(x[i + 2], hi[i + 2], lo[i + 2]);
+        tc::split_tf32(x[i + 3], hi[i + 3], lo[i + 3]);
+        s0 = fma((double)x[i], (double)x[i], s0);
+        s1 = fma((double)x[i + 1], (double)x[i + 1], s1);
+        s2 = fma((double)x[i + 2], (double)x[i + 2], s2);
+        s3 = fma((double)x[i + 3], (double)x[i + 3], s3);
     }
-    tc::fence_async_smem();
-    return xx;
+    xx += (s0 + s1) + (s2 + s3);
+    tc::tmem_st32(a_lane_addr, hi);
+    tc::tmem_st32(a_lane_addr + 32, lo);
+}
+
+struct Bars {
+    uint64_t full[STAGES], empty[STAGES], afull[2], aempty[2], qfull[2], qempty[2];
+};
+
+__device__ __forceinline__ void init_bars(Bars& B) {
+    for (int s = 0; s < STAGES; ++s) {
+        tc::mbar_init(&B.full[s], 1);
+        tc::mbar_init(&B.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+        tc::mbar_init(&B.afull[b], 128);
+        tc::mbar_init(&B.aempty[b], 1);
+        tc::mbar_init(&B.qfull[b], 1);
+        tc::mbar_init(&B.qempty[b], 128);
+    }
+    tc::fence_barrier_init();
+}
+
+// MMA issue for one stage: D += X (A in TMEM, hi/lo) . B (smem hi/lo), 3xTF32
+template <bool B_MN>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bh,
+                                            const uint8_t* bl, bool first) {
+    constexpr uint32_t idesc = tc::idesc_tf32(BM, R, 0, B_MN ? 1 : 0);
+#pragma unroll
+    for (int ks = 0; ks < BK / 8; ++ks) {
+        uint64_t dh, dl;
+        if (B_MN) {   // rows = K (8 per step = two 512-byte atoms), 32 N per 4 KB box
+            dh = tc::sdesc_sw128_32b(bh + ks * 1024, 4096, 512);
+            dl = tc::sdesc_sw128_32b(bl + ks * 1024, 4096, 512);
+        } else {      // rows = N, K contiguous within the 128-byte swizzle row
+            dh = tc::sdesc_sw128(bh + ks * 32, 16, 1024);
+            dl = tc::sdesc_sw128(bl + ks * 32, 16, 1024);
+        }
+        const uint32_t ah = a + ks * 8, al = a + 32 + ks * 8;
+        tc::mma_tf32_ts(d, al, dh, idesc, (first && ks == 0) ? 0u : 1u);
+        tc::mma_tf32_ts(d, ah, dl, idesc, 1);
+        tc::mma_tf32_ts(d, ah, dh, idesc, 1);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -86,24 +124,13 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
               float* __restrict__ Vlo, int m, int n, double* __restrict__ part) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
-    __shared__ uint64_t full[STAGES], conv[STAGES], empty[STAGES], qfull[2], qempty[2];
+    __shared__ Bars B;
     __shared__ uint32_t tmem_base;
     __shared__ double red[kThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&conv[s], 128);
-            tc::mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&qfull[b], 1);
-            tc::mbar_init(&qempty[b], 128);
-        }
-        tc::fence_barrier_init();
-    }
-    if (warp == 1) tc::tmem_alloc<128>(&tmem_base);
+    if (threadIdx.x == 0) init_bars(B);
+    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -119,54 +146,61 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    tc::mbar_wait(&empty[s], ph ^ 1);
+                    tc::mbar_wait(&B.empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* st = base + s * SSTAGE;
-                    tc::mbar_expect_tx(&full[s], TX_BYTES);
-                    tc::tma_load_2d(st, &mX, &full[s], kb * BK, tile * BM);
-                    tc::tma_load_2d(st + SX + SXL, &mWh, &full[s], kb * BK, 0);
-                    tc::tma_load_2d(st + SX + SXL + SOP, &mWl, &full[s], kb * BK, 0);
+                    tc::mbar_expect_tx(&B.full[s], TX_BYTES);
+                    tc::tma_load_2d(st, &mX, &B.full[s], kb * BK, tile * BM);
+                    tc::tma_load_2d(st + SX, &mWh, &B.full[s], kb * BK, 0);
+                    tc::tma_load_2d(st + SX + SOP, &mWl, &B.full[s], kb * BK, 0);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(BM, R, 0, 0);
             int it = 0, ti = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
                 const int b = ti & 1;
-                tc::mbar_wait(&qempty[b], ((ti >> 1) & 1) ^ 1);
+                tc::mbar_wait(&B.qempty[b], ((ti >> 1) & 1) ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d = tmem + b * R;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait(&conv[s], (it / STAGES) & 1);
+                    const int s = it % STAGES, ab = it & 1;
+                    tc::mbar_wait(&B.afull[ab], (it >> 1) & 1);
                     tc::tc_fence_after();
-                    uint8_t* st = base + s * SSTAGE;
-#pragma unroll
-                    for (int ks = 0; ks < BK / 8; ++ks) {
-                        const uint64_t ah = tc::sdesc_sw128(st + ks * 32, 16, 1024);
-                        const uint64_t al = tc::sdesc_sw128(st + SX + ks * 32, 16, 1024);
-                        const uint64_t bh = tc::sdesc_sw128(st + SX + SXL + ks * 32, 16, 1024);
-                        const uint64_t bl = tc::sdesc_sw128(st + SX + SXL + SOP + ks * 32, 16, 1024);
-                        tc::mma_tf32(d, al, bh, idesc, (kb | ks) != 0);
-                        tc::mma_tf32(d, ah, bl, idesc, 1);
-                        tc::mma_tf32(d, ah, bh, idesc, 1);
-                    }
-                    tc::mma_commit(&empty[s]);
+                    const uint8_t* st = base + s * SSTAGE;
+                    issue_stage<false>(d, tmem + TM_A + ab * 64, st + SX, st + SX + SOP, kb == 0);
+                    tc::mma_commit(&B.empty[s]);
+                    tc::mma_commit(&B.aempty[ab]);
                 }
-                tc::mma_commit(&qfull[b]);
+                tc::mma_commit(&B.qfull[b]);
             }
         }
     } else if (warp < 6) {
-        const int ct = threadIdx.x - 64;
+        // split warps: lane = row of the tile; read the row (128-byte swizzled)
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         int it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             for (int kb = 0; kb < nk; ++kb, ++it) {
-                const int s = it % STAGES;
-                tc::mbar_wait(&full[s], (it / STAGES) & 1);
-                acc += split_stage(base + s * SSTAGE, ct);
-                tc::mbar_arrive(&conv[s]);
+                const int s = it % STAGES, ab = it & 1;
+                tc::mbar_wait(&B.full[s], (it / STAGES) & 1);
+                const float4* rp = reinterpret_cast<const float4*>(base + s * SSTAGE + row * 128);
+                float x[32];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float4 t = rp[c ^ (row & 7)];
+                    x[4 * c] = t.x;
+                    x[4 * c + 1] = t.y;
+                    x[4 * c + 2] = t.z;
+                    x[4 * c + 3] = t.w;
+                }
+                tc::mbar_wait(&B.aempty[ab], ((it >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                split_to_tmem(x, tmem + TM_A + ab * 64 + lane_off, acc);
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                tc::mbar_arrive(&B.afull[ab]);
             }
         }
     } else {
@@ -174,14 +208,14 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         int ti = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
             const int b = ti & 1;
-            tc::mbar_wait(&qfull[b], (ti >> 1) & 1);
+            tc::mbar_wait(&B.qfull[b], (ti >> 1) & 1);
             tc::tc_fence_after();
             float q[R];
             const uint32_t ta = tmem + b * R + ((uint32_t)(quarter * 32) << 16);
             tc::tmem_ld32(ta, q);
             tc::tmem_ld32(ta + 32, q + 32);
             tc::tc_fence_before();
-            tc::mbar_arrive(&qempty[b]);
+            tc::mbar_arrive(&B.qempty[b]);
             const long long row = (long long)tile * BM + quarter * 32 + lane;
             if (row < m) {
                 float v[R];
@@ -197,10 +231,13 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
 #pragma unroll 2
                 for (int k = 0; k < R; ++k) {
                     acc = fma((double)v[k], (double)q[k], acc);
-                    double den = 0.0;
+                    double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                    for (int l = 0; l < R; ++l) den = fma((double)v[l], __ldg(GW + l * R + k), den);
-                    q[k] = (float)((double)v[k] * ((double)q[k] / (den + kDenomGuard)));  // v'_k
+                    for (int l = 0; l < R; l += 2) {
+                        d0 = fma((double)v[l], __ldg(GW + l * R + k), d0);
+                        d1 = fma((double)v[l + 1], __ldg(GW + (l + 1) * R + k), d1);
+                    }
+                    q[k] = (float)((double)v[k] * ((double)q[k] / ((d0 + d1) + kDenomGuard)));
                 }
                 float4* o = reinterpret_cast<float4*>(Vout + row * R);
                 float4* oh = reinterpret_cast<float4*>(Vhi + row * R);
@@ -226,38 +263,29 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = red[2] + red[3] + red[4] + red[5];
-        part[2 * blockIdx.x + 1] = red[6] + red[7] + red[8] + red[9];
+        part[2 * blockIdx.x] = (red[2] + red[3]) + (red[4] + red[5]);
+        part[2 * blockIdx.x + 1] = (red[6] + red[7]) + (red[8] + red[9]);
     }
-    if (warp == 1) tc::tmem_free<128>(tmem);
+    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------
 // P^T partial for (column block cb, row split s): D[col][k] = sum_rows X[row][col] V'[row][k]
+// X tile arrives unswizzled (4 boxes of 32 rows x 32 columns); each split
+// lane owns one column and transposes it into TMEM (lane = column, K = row).
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mVh,
               const __grid_constant__ CUtensorMap mVl, int m, int n, int splits,
               int rows_per_split, float* __restrict__ wpart) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
-    __shared__ uint64_t full[STAGES], conv[STAGES], empty[STAGES], qfull[2], qempty[2];
+    __shared__ Bars B;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncb = (n + BM - 1) / BM;
     const int nitems = ncb * splits;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&conv[s], 128);
-            tc::mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&qfull[b], 1);
-            tc::mbar_init(&qempty[b], 128);
-        }
-        tc::fence_barrier_init();
-    }
-    if (warp == 1) tc::tmem_alloc<128>(&tmem_base);
+    if (threadIdx.x == 0) init_bars(B);
+    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -282,64 +310,65 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 item_rows(item, r0, nkb);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % STAGES;
-                    tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    tc::mbar_wait(&B.empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* st = base + s * SSTAGE;
                     const int row = r0 + kb * BK;
-                    tc::mbar_expect_tx(&full[s], TX_BYTES);
+                    tc::mbar_expect_tx(&B.full[s], TX_BYTES);
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        tc::tma_load_2d(st + j * 4096, &mX, &full[s], cb * BM + 32 * j, row);
+                        tc::tma_load_2d(st + j * 4096, &mX, &B.full[s], cb * BM + 32 * j, row);
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
-                        tc::tma_load_2d(st + SX + SXL + j * 4096, &mVh, &full[s], 32 * j, row);
-                        tc::tma_load_2d(st + SX + SXL + SOP + j * 4096, &mVl, &full[s], 32 * j, row);
+                        tc::tma_load_2d(st + SX + j * 4096, &mVh, &B.full[s], 32 * j, row);
+                        tc::tma_load_2d(st + SX + SOP + j * 4096, &mVl, &B.full[s], 32 * j, row);
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(BM, R, 1, 1);
             int it = 0, ti = 0;
             for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++ti) {
                 int r0, nkb;
                 item_rows(item, r0, nkb);
                 const int b = ti & 1;
-                tc::mbar_wait(&qempty[b], ((ti >> 1) & 1) ^ 1);
+                tc::mbar_wait(&B.qempty[b], ((ti >> 1) & 1) ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d = tmem + b * R;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait(&conv[s], (it / STAGES) & 1);
+                    const int s = it % STAGES, ab = it & 1;
+                    tc::mbar_wait(&B.afull[ab], (it >> 1) & 1);
                     tc::tc_fence_after();
-                    uint8_t* st = base + s * SSTAGE;
-#pragma unroll
-                    for (int ks = 0; ks < BK / 8; ++ks) {
-                        const uint64_t ah = tc::sdesc_sw128_32b(st + ks * 1024, 4096, 512);
-                        const uint64_t al = tc::sdesc_sw128_32b(st + SX + ks * 1024, 4096, 512);
-                        const uint64_t bh = tc::sdesc_sw128_32b(st + SX + SXL + ks * 1024, 4096, 512);
-                        const uint64_t bl =
-                            tc::sdesc_sw128_32b(st + SX + SXL + SOP + ks * 1024, 4096, 512);
-                        tc::mma_tf32(d, al, bh, idesc, (kb | ks) != 0);
-                        tc::mma_tf32(d, ah, bl, idesc, 1);
-                        tc::mma_tf32(d, ah, bh, idesc, 1);
-                    }
-                    tc::mma_commit(&empty[s]);
+                    const uint8_t* st = base + s * SSTAGE;
+                    issue_stage<true>(d, tmem + TM_A + ab * 64, st + SX, st + SX + SOP, kb == 0);
+                    tc::mma_commit(&B.empty[s]);
+                    tc::mma_commit(&B.aempty[ab]);
                 }
-                tc::mma_commit(&qfull[b]);
+                tc::mma_commit(&B.qfull[b]);
             }
         }
     } else if (warp < 6) {
-        const int ct = threadIdx.x - 64;
+        const int quarter = warp & 3;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        double unused = 0.0;
         int it = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
             int r0, nkb;
             item_rows(item, r0, nkb);
             for (int kb = 0; kb < nkb; ++kb, ++it) {
-                const int s = it % STAGES;
-                tc::mbar_wait(&full[s], (it / STAGES) & 1);
-                split_stage(base + s * SSTAGE, ct);
-                tc::mbar_arrive(&conv[s]);
+                const int s = it % STAGES, ab = it & 1;
+                tc::mbar_wait(&B.full[s], (it / STAGES) & 1);
+                // column (quarter*32 + lane) of the tile = lane of box `quarter`
+                const float* cp = reinterpret_cast<const float*>(base + s * SSTAGE + quarter * 4096) + lane;
+                float x[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) x[k] = cp[k * 32];
+                tc::mbar_wait(&B.aempty[ab], ((it >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                split_to_tmem(x, tmem + TM_A + ab * 64 + lane_off, unused);
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                tc::mbar_arrive(&B.afull[ab]);
             }
         }
     } else {
@@ -351,19 +380,18 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             item_rows(item, r0, nkb);
             const int b = ti & 1;
             float p[R];
+            tc::mbar_wait(&B.qfull[b], (ti >> 1) & 1);
+            tc::tc_fence_after();
             if (nkb > 0) {
-                tc::mbar_wait(&qfull[b], (ti >> 1) & 1);
-                tc::tc_fence_after();
                 const uint32_t ta = tmem + b * R + ((uint32_t)(quarter * 32) << 16);
                 tc::tmem_ld32(ta, p);
                 tc::tmem_ld32(ta + 32, p + 32);
-                tc::tc_fence_before();
             } else {
 #pragma unroll
                 for (int k = 0; k < R; ++k) p[k] = 0.f;
-                tc::mbar_wait(&qfull[b], (ti >> 1) & 1);
             }
-            tc::mbar_arrive(&qempty[b]);
+            tc::tc_fence_before();
+            tc::mbar_arrive(&B.qempty[b]);
             const long long col = (long long)cb * BM + quarter * 32 + lane;
             if (col < n) {
                 float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
@@ -375,7 +403,7 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<128>(tmem);
+    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -507,9 +535,9 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
     if ((rc = mmk_host::make_map_f32(&mWh, L.Wh, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f32(&mWl, L.Wl, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK, true))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mVh, L.Vhi, m, R, R, BK, true))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mVl, L.Vlo, m, R, R, BK, true))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK, 0))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mVh, L.Vhi, m, R, R, BK, 32))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mVl, L.Vlo, m, R, R, BK, 32))) return rc;
     const long long rn = (long long)R * n;
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn)));

@@ -111,9 +111,10 @@ tc_selftest_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant
 }  // namespace
 
 namespace mmk_host {
-// 2-D fp32 row-major tensor map, box = 32 columns (128 B) x box_rows, 128B swizzle
+// 2-D fp32 row-major tensor map, box = 32 columns (128 B) x box_rows;
+// swizzle 128 = 16-byte chunks, 32 = 32-byte-atom 128B swizzle, 0 = none
 int make_map_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                 uint64_t row_stride_elems, uint32_t box_rows, bool atom32) {
+                 uint64_t row_stride_elems, uint32_t box_rows, int swizzle) {
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {row_stride_elems * 4};
     cuuint32_t box[2] = {32, box_rows};
@@ -139,7 +140,9 @@ int make_map_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t col
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                         const_cast<void*>(base), dims, strides, box, estr,
                                         CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        swizzle == 32   ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                        : swizzle == 0  ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                        : CU_TENSOR_MAP_SWIZZLE_128B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -159,9 +162,9 @@ extern "C" int mmk_selftest_tc(const float* A, const float* B, const float* X, c
     int rc;
     if ((rc = mmk_host::make_map_f32(&mA, A, 128, 64, 64, 128))) return rc;
     if ((rc = mmk_host::make_map_f32(&mB, B, 64, 64, 64, 64))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mX, X, 32, 128, 128, 32, true))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mV, V, 32, 64, 64, 32, true))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mB32, B, 64, 64, 64, 64, true))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mX, X, 32, 128, 128, 32, 32))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mV, V, 32, 64, 64, 32, 32))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mB32, B, 64, 64, 64, 64, 32))) return rc;
     const size_t smem = 1024 + kA + kB + kX + kV + kB32;
     cudaFuncSetAttribute(tc_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
