@@ -236,6 +236,11 @@ void mmk_engine_destroy(void *engine);
 int mmk_selftest_tc(const float *A, const float *B, const float *X, const float *V, float *D1,
                     float *D2, float *D3, int mode, int *diag, void *stream);
 
+/* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core
+ * NNMF kernels, 5 x 256 uint64 per buffer (TMA issue, split start, split
+ * done, MMA start, MMA committed); NULL disables (the default). */
+int mmk_tc_set_trace(unsigned long long *vstep, unsigned long long *wstep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -144,13 +144,18 @@ gram64_kernel(const T* __restrict__ A, long long len, int chunks_per_block,
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * 64 + 4 * tx + j] = acc[i][j];
-    if (arrive_last(counter, gridDim.x)) {
-        for (int pidx = threadIdx.x; pidx < 4096; pidx += kThreads) {
-            double sum = 0.0;
-            for (unsigned int b = 0; b < gridDim.x; ++b) sum += part[(long long)b * 4096 + pidx];
-            out[pidx] = sum;
-        }
-    }
+    (void)counter;
+    (void)out;
+}
+
+// out[p] = sum_b part[b][p] in block order (one thread per output element)
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int nparts, int len,
+                                   double* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= len) return;
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(long long)b * len + p];
+    out[p] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -311,6 +316,7 @@ __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wou
 
 // ---------------------------------------------------------------------------
 struct Plan {
+    int g64w_blocks, g64w_cpb, g64v_blocks, g64v_cpb;   // rank-64 Gram split-K
     int rpw, nvb;            // vstep rows per warp, blocks
     int gw_blocks, gw_cpb;   // gram over W (len n)
     int gv_blocks, gv_cpb;   // gram over V (len m)
@@ -343,6 +349,12 @@ Plan make_plan(long long m, long long n, int r) {
     P.gv_blocks = nch_v < kNumSMs ? nch_v : kNumSMs;
     P.gv_cpb = ceil_div(nch_v, P.gv_blocks);
     P.gv_blocks = ceil_div(nch_v, P.gv_cpb);
+    P.g64w_blocks = nch_w < 4 * kNumSMs ? nch_w : 4 * kNumSMs;
+    P.g64w_cpb = ceil_div(nch_w, P.g64w_blocks);
+    P.g64w_blocks = ceil_div(nch_w, P.g64w_cpb);
+    P.g64v_blocks = nch_v < 4 * kNumSMs ? nch_v : 4 * kNumSMs;
+    P.g64v_cpb = ceil_div(nch_v, P.g64v_blocks);
+    P.g64v_blocks = ceil_div(nch_v, P.g64v_cpb);
     P.colblocks = ceil_div(n, 32);
     long long S = ceil_div(4 * kNumSMs, P.colblocks);
     long long smax = ceil_div(m > 0 ? m : 1, 64);
@@ -361,7 +373,9 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws*
         return o;
     };
     const size_t rr = (size_t)r * r;
-    const int gblocks = P.gw_blocks > P.gv_blocks ? P.gw_blocks : P.gv_blocks;
+    int gblocks = P.gw_blocks > P.gv_blocks ? P.gw_blocks : P.gv_blocks;
+    if (P.g64w_blocks > gblocks) gblocks = P.g64w_blocks;
+    if (P.g64v_blocks > gblocks) gblocks = P.g64v_blocks;
     size_t o_gw = take(sizeof(double) * rr);
     size_t o_gp = take(sizeof(double) * rr * gblocks);
     size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
@@ -385,11 +399,22 @@ constexpr int kMaxRank = 128;
 
 template <typename T, int RMAX>
 struct K {
+    static void gram64(const T* A, long long len, bool rows, int blocks, int cpb, const Ws& L,
+                       double* out, cudaStream_t st) {
+        if (rows)
+            MMK_LAUNCH("nnmf_gram64", st,
+                       (gram64_kernel<T, true><<<blocks, kThreads, 0, st>>>(A, len, cpb, L.gpart,
+                                                                            nullptr, nullptr)));
+        else
+            MMK_LAUNCH("nnmf_gram64", st,
+                       (gram64_kernel<T, false><<<blocks, kThreads, 0, st>>>(A, len, cpb, L.gpart,
+                                                                             nullptr, nullptr)));
+        MMK_LAUNCH("nnmf_gram_reduce",
+                   st, (gram_reduce_kernel<<<16, 256, 0, st>>>(L.gpart, blocks, 4096, out)));
+    }
     static void gram_w(const T* W, long long n, int r, const Plan& P, const Ws& L, cudaStream_t st) {
         if (RMAX == 64 && r == 64) {
-            MMK_LAUNCH("nnmf_gram_w", st,
-                       (gram64_kernel<T, true><<<P.gw_blocks, kThreads, 0, st>>>(
-                           W, n, P.gw_cpb, L.gpart, L.counters + 1, L.GW)));
+            gram64(W, n, true, P.g64w_blocks, P.g64w_cpb, L, L.GW, st);
             return;
         }
         MMK_LAUNCH("nnmf_gram_w", st,
@@ -399,9 +424,7 @@ struct K {
     static void gram_v(const T* V, long long m, int r, const Plan& P, const Ws& L, double* out,
                        cudaStream_t st) {
         if (RMAX == 64 && r == 64) {
-            MMK_LAUNCH("nnmf_gram_v", st,
-                       (gram64_kernel<T, false><<<P.gv_blocks, kThreads, 0, st>>>(
-                           V, m, P.gv_cpb, L.gpart, L.counters + 2, out)));
+            gram64(V, m, false, P.g64v_blocks, P.g64v_cpb, L, out, st);
             return;
         }
         MMK_LAUNCH("nnmf_gram_v", st,
@@ -480,14 +503,10 @@ struct RunA {
             if (a.mode == 0 && tc_shape(a.m, a.n, a.r) &&
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
                 auto gw = [&](const float* Wp, double* out, cudaStream_t s) {
-                    MMK_LAUNCH("nnmf_gram_w", s,
-                               (gram64_kernel<float, true><<<P.gw_blocks, kThreads, 0, s>>>(
-                                   Wp, a.n, P.gw_cpb, L.gpart, L.counters + 1, out)));
+                    K<float, 64>::gram64(Wp, a.n, true, P.g64w_blocks, P.g64w_cpb, L, out, s);
                 };
                 auto gv = [&](const float* Vp, double* out, cudaStream_t s) {
-                    MMK_LAUNCH("nnmf_gram_v", s,
-                               (gram64_kernel<float, false><<<P.gv_blocks, kThreads, 0, s>>>(
-                                   Vp, a.m, P.gv_cpb, L.gpart, L.counters + 2, out)));
+                    K<float, 64>::gram64(Vp, a.m, false, P.g64v_blocks, P.g64v_cpb, L, out, s);
                 };
                 return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
                                       a.red, gw, gv, a.st);

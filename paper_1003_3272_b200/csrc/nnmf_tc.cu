@@ -40,79 +40,212 @@ using namespace mmk;
 constexpr int R = 64;            // rank of the tensor-core path (UMMA N)
 constexpr int BM = 128;          // UMMA M: rows of X (V step) / columns of X (W step)
 constexpr int BK = 32;           // K per stage: one 128-byte row of fp32
-constexpr int STAGES = 6;
-constexpr int kThreads = 320;    // 10 warps: TMA, MMA, 4 split, 4 epilogue
-constexpr uint32_t SX = BM * BK * 4;        // 16 KB  raw X tile
+constexpr int NCONV = 8;         // split warps: groups of 4 take X stages round-robin
+constexpr int NGROUP = NCONV / 4;
+constexpr int kThreads = 32 * (2 + NCONV + 4);   // TMA, MMA, split x8, epilogue x4
+constexpr uint32_t SX = BM * BK * 4;        // 16 KB  raw X tile (the hi operand)
 constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W (or V') chunk hi; same again for lo
-constexpr uint32_t SSTAGE = SX + 2 * SOP;   // 32 KB
-constexpr uint32_t SMEM = STAGES * SSTAGE + 1024;
-constexpr uint32_t TX_BYTES = SSTAGE;
-// TMEM columns: [0,128) two fp32 accumulators (64 each), [128,256) two
-// tf32-split A buffers (hi 32 + lo 32 columns each)
-constexpr int TM_COLS = 256;
-constexpr uint32_t TM_A = 128;
+constexpr int XST = 8;                      // X ring (128 KB in flight per SM)
+constexpr int OST = 4;                      // operand (W / V' chunk) ring
+constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + 1024;
+constexpr int NA = 4;                       // TMEM lo-operand buffers
+constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
+constexpr int TMAX = 3;                     // accumulators per pass (V step: row tiles)
+constexpr int CB = 2;                       // W step: 128-column blocks per item
+constexpr int TM_COLS = 512;
+constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// hi/lo split of 32 values into the TMEM A buffer of this thread's lane
-__device__ __forceinline__ void split_to_tmem(const float* x, uint32_t a_lane_addr, double& xx) {
-    float hi[32], lo[32];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-        tc::split_tf32(x[i], hi[i], lo[i]);
-        tc::split_tf32(x[i + 1], hi[i + 1], lo[i + 1]);
-        tc::split_tf32(x[i + 2], hi[i + 2], lo[i + 2]);
-        tc::split_tf32(x[i + 3], hi[i + 3], lo[i + 3]);
-        s0 = fma((double)x[i], (double)x[i], s0);
-        s1 = fma((double)x[i + 1], (double)x[i + 1], s1);
-        s2 = fma((double)x[i + 2], (double)x[i + 2], s2);
-        s3 = fma((double)x[i + 3], (double)x[i + 3], s3);
-    }
-    xx += (s0 + s1) + (s2 + s3);
-    tc::tmem_st32(a_lane_addr, hi);
-    tc::tmem_st32(a_lane_addr + 32, lo);
+// The tensor core reads an fp32 operand as tf32 by ignoring its 13 low
+// mantissa bits, so the raw tile is the "hi" operand as-is; the exact
+// remainder x - trunc_tf32(x) is the "lo" operand, written to TMEM.
+__device__ __forceinline__ float tf32_rem(float x) {
+    return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
 struct Bars {
-    uint64_t full[STAGES], empty[STAGES], afull[2], aempty[2], qfull[2], qempty[2];
+    uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST], afull[NA], aempty[NA];
+    uint64_t dfull, dempty;
 };
 
 __device__ __forceinline__ void init_bars(Bars& B) {
-    for (int s = 0; s < STAGES; ++s) {
-        tc::mbar_init(&B.full[s], 1);
-        tc::mbar_init(&B.empty[s], 1);
+    for (int s = 0; s < XST; ++s) {
+        tc::mbar_init(&B.xfull[s], 1);
+        tc::mbar_init(&B.xempty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int s = 0; s < OST; ++s) {
+        tc::mbar_init(&B.ofull[s], 1);
+        tc::mbar_init(&B.oempty[s], 1);
+    }
+    for (int b = 0; b < NA; ++b) {
         tc::mbar_init(&B.afull[b], 128);
         tc::mbar_init(&B.aempty[b], 1);
-        tc::mbar_init(&B.qfull[b], 1);
-        tc::mbar_init(&B.qempty[b], 128);
     }
+    tc::mbar_init(&B.dfull, 1);
+    tc::mbar_init(&B.dempty, 128);
     tc::fence_barrier_init();
 }
 
-// MMA issue for one stage: D += X (A in TMEM, hi/lo) . B (smem hi/lo), 3xTF32
-template <bool B_MN>
-__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bh,
-                                            const uint8_t* bl, bool first) {
-    constexpr uint32_t idesc = tc::idesc_tf32(BM, R, 0, B_MN ? 1 : 0);
+// One stage of 3xTF32.  The operand chunk holds [B_hi ; B_lo] stacked along
+// N (64 + 64 rows, contiguous in smem): per K-step an SS MMA with N = 128
+// gives D[:, 0:64] += X_hi.B_hi and D[:, 64:128] += X_hi.B_lo, and a TS MMA
+// with N = 64 adds X_lo.B_hi (lo from TMEM) into D[:, 0:64].  The epilogue
+// sums the two halves: X_hi B_hi + X_hi B_lo + X_lo B_hi.
+template <bool MN>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t alo, const uint8_t* xh,
+                                            const uint8_t* bhl, bool first) {
+    constexpr uint32_t id_ts = tc::idesc_tf32(BM, R, 0, MN ? 1 : 0);
+    constexpr uint32_t id_ss = tc::idesc_tf32(BM, ACC, MN ? 1 : 0, MN ? 1 : 0);
+    // descriptors advance by their 16-byte start-address field only
+    const uint64_t da0 = MN ? tc::sdesc_sw128_32b(xh, 4096, 512) : tc::sdesc_sw128(xh, 16, 1024);
+    const uint64_t db0 = MN ? tc::sdesc_sw128_32b(bhl, 4096, 512) : tc::sdesc_sw128(bhl, 16, 1024);
+    constexpr uint64_t step = MN ? (1024 >> 4) : (32 >> 4);
 #pragma unroll
     for (int ks = 0; ks < BK / 8; ++ks) {
-        uint64_t dh, dl;
-        if (B_MN) {   // rows = K (8 per step = two 512-byte atoms), 32 N per 4 KB box
-            dh = tc::sdesc_sw128_32b(bh + ks * 1024, 4096, 512);
-            dl = tc::sdesc_sw128_32b(bl + ks * 1024, 4096, 512);
-        } else {      // rows = N, K contiguous within the 128-byte swizzle row
-            dh = tc::sdesc_sw128(bh + ks * 32, 16, 1024);
-            dl = tc::sdesc_sw128(bl + ks * 32, 16, 1024);
+        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+        tc::mma_tf32(d, da0 + ks * step, db0 + ks * step, id_ss, acc);
+        tc::mma_tf32_ts(d, alo + ks * 8, db0 + ks * step, id_ts, 1);
+    }
+}
+
+// Work of one CTA pass: `nacc` accumulators (row tiles or column blocks),
+// `nkb` K-blocks; stage (kb, j) streams X block j of K-block kb while the
+// operand chunk of kb is shared by all j.
+struct Pass {
+    int nacc, nkb;
+};
+
+// lo-operand of an X stage into TMEM: V step (MN = false) reads row `lane`
+// of the 128B-swizzled K-major tile; W step (MN = true) reads column `lane`
+// of box `quarter` of the 32-byte-atom swizzled MN-major tile.
+template <bool MN>
+__device__ __forceinline__ void split_stage(const uint8_t* xs, int quarter, int lane,
+                                            uint32_t a_addr) {
+    float lo[32];
+    if (!MN) {
+        const int row = quarter * 32 + lane;
+        const float4* rp = reinterpret_cast<const float4*>(xs + row * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float4 t = rp[c ^ (row & 7)];
+            lo[4 * c] = tf32_rem(t.x);
+            lo[4 * c + 1] = tf32_rem(t.y);
+            lo[4 * c + 2] = tf32_rem(t.z);
+            lo[4 * c + 3] = tf32_rem(t.w);
         }
-        const uint32_t ah = a + ks * 8, al = a + 32 + ks * 8;
-        tc::mma_tf32_ts(d, al, dh, idesc, (first && ks == 0) ? 0u : 1u);
-        tc::mma_tf32_ts(d, ah, dl, idesc, 1);
-        tc::mma_tf32_ts(d, ah, dh, idesc, 1);
+    } else {
+        const uint8_t* bx = xs + quarter * 4096 + (lane & 7) * 4;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            lo[k] = tf32_rem(
+                *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 3) ^ (k & 3)) << 5)));
+    }
+    tc::tmem_st32(a_addr, lo);
+}
+
+// ---------------------------------------------------------------------------
+// The pipeline shared by both steps.  Role functions get (pass index p, j)
+// and must agree on the iteration order: for p: for kb: [operand], for j: [X].
+// trace (debug): CTA 0 records clock64 per X stage for the first kTrace stages:
+// [0] TMA issued, [1] split start (data landed), [2] split done, [3] MMA
+// start (operands ready), [4] MMAs issued + committed
+constexpr int kTrace = 256;
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int xit) {
+    if (tr && blockIdx.x == 0 && xit < kTrace) tr[what * kTrace + xit] = clock64();
+}
+
+template <bool MN, class PassOf, class LoadX, class LoadOp, class Epi>
+__device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tmem, int npass,
+                                             const PassOf& pass_of, const LoadX& load_x,
+                                             const LoadOp& load_op, const Epi& epilogue,
+                                             unsigned long long* tr) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* xring = base;
+    uint8_t* oring = base + XST * SX;
+    if (warp == 0) {
+        if (lane == 0) {
+            int xit = 0, oit = 0;
+            for (int p = 0; p < npass; ++p) {
+                const Pass P = pass_of(p);
+                for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
+                    const int os = oit % OST;
+                    tc::mbar_wait(&B.oempty[os], ((oit / OST) & 1) ^ 1);
+                    tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                    load_op(p, kb, oring + os * 2 * SOP, &B.ofull[os]);
+                    for (int j = 0; j < P.nacc; ++j, ++xit) {
+                        const int xs = xit % XST;
+                        tc::mbar_wait(&B.xempty[xs], ((xit / XST) & 1) ^ 1);
+                        tc::mbar_expect_tx(&B.xfull[xs], SX);
+                        load_x(p, kb, j, xring + xs * SX, &B.xfull[xs]);
+                        trace_at(tr, 0, xit);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int xit = 0, oit = 0;
+            for (int p = 0; p < npass; ++p) {
+                const Pass P = pass_of(p);
+                if (p > 0) tc::mbar_wait(&B.dempty, (p - 1) & 1);
+                tc::tc_fence_after();
+                for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
+                    const int os = oit % OST;
+                    tc::mbar_wait(&B.ofull[os], (oit / OST) & 1);
+                    const uint8_t* ob = oring + os * 2 * SOP;
+                    for (int j = 0; j < P.nacc; ++j, ++xit) {
+                        const int xs = xit % XST, ab = xit % NA;
+                        tc::mbar_wait(&B.afull[ab], (xit / NA) & 1);
+                        trace_at(tr, 3, xit);
+                        tc::tc_fence_after();
+                        issue_stage<MN>(tmem + j * ACC, tmem + TM_A + ab * 32, xring + xs * SX, ob,
+                                        kb == 0);
+                        tc::mma_commit(&B.xempty[xs]);
+                        tc::mma_commit(&B.aempty[ab]);
+                        trace_at(tr, 4, xit);
+                    }
+                    tc::mma_commit(&B.oempty[os]);
+                }
+                tc::mma_commit(&B.dfull);
+            }
+        }
+    } else if (warp < 2 + NCONV) {
+        const int g = (warp - 2) >> 2, quarter = warp & 3;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        int xit = 0;
+        for (int p = 0; p < npass; ++p) {
+            const Pass P = pass_of(p);
+            for (int kb = 0; kb < P.nkb; ++kb) {
+                for (int j = 0; j < P.nacc; ++j, ++xit) {
+                    if (xit % NGROUP != g) continue;
+                    const int xs = xit % XST, ab = xit % NA;
+                    tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
+                    if (quarter == 0 && lane == 0) trace_at(tr, 1, xit);
+                    tc::mbar_wait(&B.aempty[ab], ((xit / NA) & 1) ^ 1);
+                    tc::tc_fence_after();
+                    split_stage<MN>(xring + xs * SX, quarter, lane, tmem + TM_A + ab * 32 + lane_off);
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&B.afull[ab]);
+                    if (quarter == 0 && lane == 0) trace_at(tr, 2, xit);
+                }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        for (int p = 0; p < npass; ++p) {
+            const Pass P = pass_of(p);
+            tc::mbar_wait(&B.dfull, p & 1);
+            tc::tc_fence_after();
+            for (int j = 0; j < P.nacc; ++j)
+                epilogue(p, j, quarter, lane,
+                         tmem + j * ACC + ((uint32_t)(quarter * 32) << 16), P.nkb > 0);
+            tc::tc_fence_before();
+            tc::mbar_arrive(&B.dempty);
+        }
     }
 }
 
@@ -120,8 +253,9 @@ __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
-              const double* __restrict__ GW, float* __restrict__ Vout, float* __restrict__ Vhi,
-              float* __restrict__ Vlo, int m, int n, double* __restrict__ part) {
+              const float* __restrict__ DEN, float* __restrict__ Vout, float* __restrict__ Vhi,
+              float* __restrict__ Vlo, int m, int n, double* __restrict__ part,
+              unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     __shared__ Bars B;
@@ -129,281 +263,244 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __shared__ double red[kThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
-    if (threadIdx.x == 0) init_bars(B);
+    const int mine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int npass = (mine + TMAX - 1) / TMAX;
+    if (threadIdx.x == 0) {
+        init_bars(B);
+        tc::tma_prefetch(&mX);
+        tc::tma_prefetch(&mWh);
+        tc::tma_prefetch(&mWl);
+    }
     if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
     double acc = 0.0;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            tc::tma_prefetch(&mX);
-            tc::tma_prefetch(&mWh);
-            tc::tma_prefetch(&mWl);
-            int it = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait(&B.empty[s], ((it / STAGES) & 1) ^ 1);
-                    uint8_t* st = base + s * SSTAGE;
-                    tc::mbar_expect_tx(&B.full[s], TX_BYTES);
-                    tc::tma_load_2d(st, &mX, &B.full[s], kb * BK, tile * BM);
-                    tc::tma_load_2d(st + SX, &mWh, &B.full[s], kb * BK, 0);
-                    tc::tma_load_2d(st + SX + SOP, &mWl, &B.full[s], kb * BK, 0);
+    auto tile_of = [&](int p, int j) { return (int)blockIdx.x + (p * TMAX + j) * (int)gridDim.x; };
+    auto pass_of = [&](int p) {
+        const int left = mine - p * TMAX;
+        return Pass{left < TMAX ? left : TMAX, nk};
+    };
+    auto load_op = [&](int, int kb, uint8_t* dst, uint64_t* bar) {
+        tc::tma_load_2d(dst, &mWh, bar, kb * BK, 0);
+        tc::tma_load_2d(dst + SOP, &mWl, bar, kb * BK, 0);
+    };
+    auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
+        tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
+    };
+    auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool) {
+        const long long row = (long long)tile_of(p, j) * BM + quarter * 32 + ln;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            float q[32], q2[32];
+            tc::tmem_ld32(ta + h * 32, q);
+            tc::tmem_ld32(ta + R + h * 32, q2);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) q[i] += q2[i];
+            if (row >= m) continue;
+            const float4* v4 = reinterpret_cast<const float4*>(V + row * R + h * 32);
+            const float4* d4 = reinterpret_cast<const float4*>(DEN + row * R + h * 32);
+            float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
+            float4* oh = reinterpret_cast<float4*>(Vhi + row * R + h * 32);
+            float4* ol = reinterpret_cast<float4*>(Vlo + row * R + h * 32);
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) {
+                const float4 vv = v4[k4], dd = d4[k4];
+                const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+                const float da[4] = {dd.x, dd.y, dd.z, dd.w};
+                float nv[4], hh[4], ll[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double vk = (double)va[i];
+                    const double qk = (double)q[4 * k4 + i];
+                    acc = fma(vk, qk, acc);
+                    nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
+                    tc::split_tf32(nv[i], hh[i], ll[i]);
                 }
+                o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+                oh[k4] = make_float4(hh[0], hh[1], hh[2], hh[3]);
+                ol[k4] = make_float4(ll[0], ll[1], ll[2], ll[3]);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            int it = 0, ti = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-                const int b = ti & 1;
-                tc::mbar_wait(&B.qempty[b], ((ti >> 1) & 1) ^ 1);
-                tc::tc_fence_after();
-                const uint32_t d = tmem + b * R;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % STAGES, ab = it & 1;
-                    tc::mbar_wait(&B.afull[ab], (it >> 1) & 1);
-                    tc::tc_fence_after();
-                    const uint8_t* st = base + s * SSTAGE;
-                    issue_stage<false>(d, tmem + TM_A + ab * 64, st + SX, st + SX + SOP, kb == 0);
-                    tc::mma_commit(&B.empty[s]);
-                    tc::mma_commit(&B.aempty[ab]);
-                }
-                tc::mma_commit(&B.qfull[b]);
-            }
-        }
-    } else if (warp < 6) {
-        // split warps: lane = row of the tile; read the row (128-byte swizzled)
-        const int quarter = warp & 3;
-        const int row = quarter * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int kb = 0; kb < nk; ++kb, ++it) {
-                const int s = it % STAGES, ab = it & 1;
-                tc::mbar_wait(&B.full[s], (it / STAGES) & 1);
-                const float4* rp = reinterpret_cast<const float4*>(base + s * SSTAGE + row * 128);
-                float x[32];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float4 t = rp[c ^ (row & 7)];
-                    x[4 * c] = t.x;
-                    x[4 * c + 1] = t.y;
-                    x[4 * c + 2] = t.z;
-                    x[4 * c + 3] = t.w;
-                }
-                tc::mbar_wait(&B.aempty[ab], ((it >> 1) & 1) ^ 1);
-                tc::tc_fence_after();
-                split_to_tmem(x, tmem + TM_A + ab * 64 + lane_off, acc);
-                tc::tmem_st_wait();
-                tc::tc_fence_before();
-                tc::mbar_arrive(&B.afull[ab]);
-            }
-        }
-    } else {
-        const int quarter = warp & 3;
-        int ti = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-            const int b = ti & 1;
-            tc::mbar_wait(&B.qfull[b], (ti >> 1) & 1);
-            tc::tc_fence_after();
-            float q[R];
-            const uint32_t ta = tmem + b * R + ((uint32_t)(quarter * 32) << 16);
-            tc::tmem_ld32(ta, q);
-            tc::tmem_ld32(ta + 32, q + 32);
-            tc::tc_fence_before();
-            tc::mbar_arrive(&B.qempty[b]);
-            const long long row = (long long)tile * BM + quarter * 32 + lane;
-            if (row < m) {
-                float v[R];
-                const float4* v4 = reinterpret_cast<const float4*>(V + row * R);
-#pragma unroll
-                for (int k4 = 0; k4 < R / 4; ++k4) {
-                    const float4 t = v4[k4];
-                    v[4 * k4] = t.x;
-                    v[4 * k4 + 1] = t.y;
-                    v[4 * k4 + 2] = t.z;
-                    v[4 * k4 + 3] = t.w;
-                }
-#pragma unroll 2
-                for (int k = 0; k < R; ++k) {
-                    acc = fma((double)v[k], (double)q[k], acc);
-                    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                    for (int l = 0; l < R; l += 2) {
-                        d0 = fma((double)v[l], __ldg(GW + l * R + k), d0);
-                        d1 = fma((double)v[l + 1], __ldg(GW + (l + 1) * R + k), d1);
-                    }
-                    q[k] = (float)((double)v[k] * ((double)q[k] / ((d0 + d1) + kDenomGuard)));
-                }
-                float4* o = reinterpret_cast<float4*>(Vout + row * R);
-                float4* oh = reinterpret_cast<float4*>(Vhi + row * R);
-                float4* ol = reinterpret_cast<float4*>(Vlo + row * R);
-#pragma unroll
-                for (int k4 = 0; k4 < R / 4; ++k4) {
-                    float4 t = make_float4(q[4 * k4], q[4 * k4 + 1], q[4 * k4 + 2], q[4 * k4 + 3]);
-                    float4 h, l;
-                    tc::split_tf32(t.x, h.x, l.x);
-                    tc::split_tf32(t.y, h.y, l.y);
-                    tc::split_tf32(t.z, h.z, l.z);
-                    tc::split_tf32(t.w, h.w, l.w);
-                    o[k4] = t;
-                    oh[k4] = h;
-                    ol[k4] = l;
-                }
-            }
-        }
-    }
-    // per-CTA partials: [0] sum x^2 (split warps), [1] <V, Q> (epilogue warps)
+    };
+    run_pipeline<false>(base, B, tmem, npass, pass_of, load_x, load_op, epilogue, tr);
+    // per-CTA partial <V, Q> (epilogue warps)
     acc = warp_sum(acc);
     if (lane == 0) red[warp] = acc;
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = (red[2] + red[3]) + (red[4] + red[5]);
-        part[2 * blockIdx.x + 1] = (red[6] + red[7]) + (red[8] + red[9]);
+        double c = 0.0;
+        for (int w = 2 + NCONV; w < kThreads / 32; ++w) c += red[w];
+        part[blockIdx.x] = c;
     }
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------
-// P^T partial for (column block cb, row split s): D[col][k] = sum_rows X[row][col] V'[row][k]
-// X tile arrives unswizzled (4 boxes of 32 rows x 32 columns); each split
-// lane owns one column and transposes it into TMEM (lane = column, K = row).
+// P^T partials: item (row split s, column super-block cs of CB x 128 columns)
+// D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; V' chunks are shared
+// by the CB column blocks of an item.  X tiles arrive MN-major (4 boxes of
+// 32 rows x 32 columns, 32-byte-atom swizzle) and serve as the hi operand.
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mVh,
               const __grid_constant__ CUtensorMap mVl, int m, int n, int splits,
-              int rows_per_split, float* __restrict__ wpart) {
+              int rows_per_split, float* __restrict__ wpart, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     __shared__ Bars B;
     __shared__ uint32_t tmem_base;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int ncb = (n + BM - 1) / BM;
-    const int nitems = ncb * splits;
-    if (threadIdx.x == 0) init_bars(B);
+    const int ncs = (ncb + CB - 1) / CB;
+    const int nitems = ncs * splits;
+    const int npass = nitems > (int)blockIdx.x ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (threadIdx.x == 0) {
+        init_bars(B);
+        tc::tma_prefetch(&mX);
+        tc::tma_prefetch(&mVh);
+        tc::tma_prefetch(&mVl);
+    }
     if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
-    auto item_rows = [&](int item, int& r0, int& nkb) {
-        const int s = item / ncb;
-        r0 = s * rows_per_split;
+    auto item_of = [&](int p) { return (int)blockIdx.x + p * (int)gridDim.x; };
+    auto pass_of = [&](int p) {
+        const int item = item_of(p), s = item / ncs, cs = item % ncs;
+        const int r0 = s * rows_per_split;
         int r1 = r0 + rows_per_split;
         if (r1 > m) r1 = m;
-        nkb = r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0;
+        const int left = ncb - cs * CB;
+        return Pass{left < CB ? left : CB, r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0};
     };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            tc::tma_prefetch(&mX);
-            tc::tma_prefetch(&mVh);
-            tc::tma_prefetch(&mVl);
-            int it = 0;
-            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int cb = item % ncb;
-                int r0, nkb;
-                item_rows(item, r0, nkb);
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait(&B.empty[s], ((it / STAGES) & 1) ^ 1);
-                    uint8_t* st = base + s * SSTAGE;
-                    const int row = r0 + kb * BK;
-                    tc::mbar_expect_tx(&B.full[s], TX_BYTES);
+    auto load_op = [&](int p, int kb, uint8_t* dst, uint64_t* bar) {
+        const int row = (item_of(p) / ncs) * rows_per_split + kb * BK;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        tc::tma_load_2d(st + j * 4096, &mX, &B.full[s], cb * BM + 32 * j, row);
+        for (int jj = 0; jj < 2; ++jj) {
+            tc::tma_load_2d(dst + jj * 4096, &mVh, bar, 32 * jj, row);
+            tc::tma_load_2d(dst + SOP + jj * 4096, &mVl, bar, 32 * jj, row);
+        }
+    };
+    auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
+        const int item = item_of(p);
+        const int row = (item / ncs) * rows_per_split + kb * BK;
+        const int col0 = ((item % ncs) * CB + j) * BM;
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        tc::tma_load_2d(st + SX + j * 4096, &mVh, &B.full[s], 32 * j, row);
-                        tc::tma_load_2d(st + SX + SOP + j * 4096, &mVl, &B.full[s], 32 * j, row);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            int it = 0, ti = 0;
-            for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++ti) {
-                int r0, nkb;
-                item_rows(item, r0, nkb);
-                const int b = ti & 1;
-                tc::mbar_wait(&B.qempty[b], ((ti >> 1) & 1) ^ 1);
-                tc::tc_fence_after();
-                const uint32_t d = tmem + b * R;
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES, ab = it & 1;
-                    tc::mbar_wait(&B.afull[ab], (it >> 1) & 1);
-                    tc::tc_fence_after();
-                    const uint8_t* st = base + s * SSTAGE;
-                    issue_stage<true>(d, tmem + TM_A + ab * 64, st + SX, st + SX + SOP, kb == 0);
-                    tc::mma_commit(&B.empty[s]);
-                    tc::mma_commit(&B.aempty[ab]);
-                }
-                tc::mma_commit(&B.qfull[b]);
-            }
-        }
-    } else if (warp < 6) {
-        const int quarter = warp & 3;
-        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        double unused = 0.0;
-        int it = 0;
-        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-            int r0, nkb;
-            item_rows(item, r0, nkb);
-            for (int kb = 0; kb < nkb; ++kb, ++it) {
-                const int s = it % STAGES, ab = it & 1;
-                tc::mbar_wait(&B.full[s], (it / STAGES) & 1);
-                // column (quarter*32 + lane) of the tile = lane of box `quarter`
-                const float* cp = reinterpret_cast<const float*>(base + s * SSTAGE + quarter * 4096) + lane;
-                float x[32];
+        for (int jj = 0; jj < 4; ++jj) tc::tma_load_2d(dst + jj * 4096, &mX, bar, col0 + 32 * jj, row);
+    };
+    auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool any) {
+        const int item = item_of(p), s = item / ncs;
+        const long long col = (long long)((item % ncs) * CB + j) * BM + quarter * 32 + ln;
+        float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            float v[32];
+            if (any) {
+                float v2[32];
+                tc::tmem_ld32(ta + h * 32, v);
+                tc::tmem_ld32(ta + R + h * 32, v2);
 #pragma unroll
-                for (int k = 0; k < 32; ++k) x[k] = cp[k * 32];
-                tc::mbar_wait(&B.aempty[ab], ((it >> 1) & 1) ^ 1);
-                tc::tc_fence_after();
-                split_to_tmem(x, tmem + TM_A + ab * 64 + lane_off, unused);
-                tc::tmem_st_wait();
-                tc::tc_fence_before();
-                tc::mbar_arrive(&B.afull[ab]);
-            }
-        }
-    } else {
-        const int quarter = warp & 3;
-        int ti = 0;
-        for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++ti) {
-            const int cb = item % ncb, s = item / ncb;
-            int r0, nkb;
-            item_rows(item, r0, nkb);
-            const int b = ti & 1;
-            float p[R];
-            tc::mbar_wait(&B.qfull[b], (ti >> 1) & 1);
-            tc::tc_fence_after();
-            if (nkb > 0) {
-                const uint32_t ta = tmem + b * R + ((uint32_t)(quarter * 32) << 16);
-                tc::tmem_ld32(ta, p);
-                tc::tmem_ld32(ta + 32, p + 32);
+                for (int k = 0; k < 32; ++k) v[k] += v2[k];
             } else {
 #pragma unroll
-                for (int k = 0; k < R; ++k) p[k] = 0.f;
+                for (int k = 0; k < 32; ++k) v[k] = 0.f;
             }
-            tc::tc_fence_before();
-            tc::mbar_arrive(&B.qempty[b]);
-            const long long col = (long long)cb * BM + quarter * 32 + lane;
             if (col < n) {
-                float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
 #pragma unroll
-                for (int k4 = 0; k4 < R / 4; ++k4)
-                    o[k4] = make_float4(p[4 * k4], p[4 * k4 + 1], p[4 * k4 + 2], p[4 * k4 + 3]);
+                for (int k4 = 0; k4 < 8; ++k4)
+                    o[h * 8 + k4] = make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
             }
         }
-    }
+    };
+    run_pipeline<true>(base, B, tmem, npass, pass_of, load_x, load_op, epilogue, tr);
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+}
+
+// sum of x^2 over X, cached in the workspace and keyed by (X, m, n, ldx):
+// X is constant over a run, so after the first call this is a no-op launch.
+struct XXCache {
+    double xx;
+    unsigned long long key[4];
+};
+
+__global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
+                             XXCache* cache, double* __restrict__ part, unsigned int* counter) {
+    const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
+    if (cache->key[0] == k0 && cache->key[1] == (unsigned long long)m &&
+        cache->key[2] == (unsigned long long)n && cache->key[3] == (unsigned long long)ldx)
+        return;   // uniform across the grid: every block exits, the counter is untouched
+    __shared__ double sc[32];
+    double s = 0.0;
+    for (long long i = blockIdx.x; i < m; i += gridDim.x) {
+        const float* row = X + i * ldx;
+        for (long long j = threadIdx.x; j < n; j += blockDim.x) {
+            const double v = row[j];
+            s = fma(v, v, s);
+        }
+    }
+    s = block_sum(s, sc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(part, gridDim.x, sc);
+        if (threadIdx.x == 0) {
+            cache->xx = tot;
+            cache->key[1] = (unsigned long long)m;
+            cache->key[2] = (unsigned long long)n;
+            cache->key[3] = (unsigned long long)ldx;
+            __threadfence();
+            cache->key[0] = k0;
+        }
+    }
+}
+
+constexpr int VGW_SMEM = R * R * 8 + R * (64 + 4) * 4;
+
+// DEN = V G_W (the V-step denominator without its guard), fp64 accumulation,
+// stored fp32.  A block computes 64 rows x 64 columns with 4x4 register tiles
+// per thread; the V tile (transposed) and G_W sit in shared memory.
+__global__ void __launch_bounds__(256)
+vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __restrict__ DEN,
+           long long m) {
+    extern __shared__ double vgw_smem[];
+    double(*G)[R] = reinterpret_cast<double(*)[R]>(vgw_smem);
+    float(*Vt)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem + R * R);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const long long r0 = (long long)blockIdx.x * 64;
+    for (int i = threadIdx.x; i < R * R; i += 256) G[i / R][i % R] = GW[i];
+    for (int i = threadIdx.x; i < 64 * R; i += 256) {
+        const int rr = i / R, l = i % R;
+        Vt[l][rr] = (r0 + rr < m) ? V[(r0 + rr) * R + l] : 0.f;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll 8
+    for (int l = 0; l < R; ++l) {
+        const float4 a = *reinterpret_cast<const float4*>(&Vt[l][4 * ty]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&G[l][4 * tx]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&G[l][4 * tx + 2]);
+        const double av[4] = {a.x, a.y, a.z, a.w};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const long long row = r0 + 4 * ty + i;
+        if (row < m)
+            *reinterpret_cast<float4*>(DEN + row * R + 4 * tx) =
+                make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -431,19 +528,16 @@ __global__ void wreduce_tc_kernel(const float* __restrict__ wpart, int splits, l
 
 // f-partial = sum x^2 - 2 <V, Q> + <G_V, G_W> (all over this rank's rows)
 __global__ void tc_objective_kernel(const double* __restrict__ part, int nparts,
+                                    const XXCache* __restrict__ cache,
                                     const double* __restrict__ GV, const double* __restrict__ GW,
                                     double* __restrict__ out) {
     __shared__ double sc[32];
-    double xx = 0.0, cr = 0.0, gg = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-        xx += part[2 * i];
-        cr += part[2 * i + 1];
-    }
+    double cr = 0.0, gg = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) cr += part[i];
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) gg = fma(GV[i], GW[i], gg);
-    xx = block_sum(xx, sc);
     cr = block_sum(cr, sc);
     gg = block_sum(gg, sc);
-    if (threadIdx.x == 0) *out = xx - 2.0 * cr + gg;
+    if (threadIdx.x == 0) *out = cache->xx - 2.0 * cr + gg;
 }
 
 struct TcPlan {
@@ -455,23 +549,39 @@ TcPlan tc_plan(long long m, long long n) {
     const int ntiles = (int)((m + BM - 1) / BM);
     P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
     const int ncb = (int)((n + BM - 1) / BM);
-    int splits = (4 * kNumSMs + ncb - 1) / ncb;
+    const int ncs = (ncb + CB - 1) / CB;
+    // smallest split count whose item count fills whole waves of SMs
+    // (ncs * S a multiple of 148 when possible), rows per split >= 4 K-blocks
     const int max_splits = (int)((m + 4 * BK - 1) / (4 * BK));
-    if (splits > max_splits) splits = max_splits;
-    if (splits < 1) splits = 1;
-    long long rps = (m + splits - 1) / splits;
+    int best = 1;
+    double best_eff = 0.0;
+    for (int S = 1; S <= max_splits && S <= 4 * kNumSMs; ++S) {
+        const int items = ncs * S;
+        const int waves = (items + kNumSMs - 1) / kNumSMs;
+        const double eff = (double)items / ((double)waves * kNumSMs);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = S;
+        }
+        if (eff > 0.999) break;
+    }
+    long long rps = (m + best - 1) / best;
     rps = (rps + BK - 1) / BK * BK;
     P.rows_per_split = (int)rps;
     P.splits = (int)((m + rps - 1) / rps);
-    const int items = ncb * P.splits;
+    const int items = ncs * P.splits;
     P.wgrid = items < kNumSMs ? items : kNumSMs;
     return P;
 }
 
 struct TcWs {
-    float *Wh, *Wl, *Vhi, *Vlo, *wpart;
-    double *GVn, *part;
+    float *Wh, *Wl, *Vhi, *Vlo, *wpart, *DEN;
+    double *GVn, *part, *sqpart;
+    XXCache* xx;
+    unsigned int* counter;
 };
+
+inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
 
 size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     const TcPlan P = tc_plan(m, n);
@@ -483,15 +593,22 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     };
     size_t oWh = take(4 * (size_t)R * n), oWl = take(4 * (size_t)R * n);
     size_t oVh = take(4 * (size_t)R * m), oVl = take(4 * (size_t)R * m);
+    size_t oD = take(4 * (size_t)R * m);
     size_t oWp = take(4 * (size_t)P.splits * n * R);
     size_t oG = take(8 * (size_t)R * R);
     size_t oP = take(16 * (size_t)kNumSMs);
+    size_t oS = take(8 * (size_t)kNumSMs * 4);
+    size_t oC = take(sizeof(XXCache) + 64);
     if (base && L) {
+        L->sqpart = (double*)(c_base(base) + oS);
+        L->xx = (XXCache*)(c_base(base) + oC);
+        L->counter = (unsigned int*)(c_base(base) + oC + sizeof(XXCache));
         char* c = reinterpret_cast<char*>(base);
         L->Wh = (float*)(c + oWh);
         L->Wl = (float*)(c + oWl);
         L->Vhi = (float*)(c + oVh);
         L->Vlo = (float*)(c + oVl);
+        L->DEN = (float*)(c + oD);
         L->wpart = (float*)(c + oWp);
         L->GVn = (double*)(c + oG);
         L->part = (double*)(c + oP);
@@ -500,6 +617,8 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
 }
 
 bool g_attr_done = false;
+unsigned long long* g_trace_v = nullptr;   // debug: mmk_tc_set_trace
+unsigned long long* g_trace_w = nullptr;
 
 }  // namespace
 
@@ -528,6 +647,7 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     if (!g_attr_done) {
         cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
         g_attr_done = true;
     }
     CUtensorMap mX, mWh, mWl, mXt, mVh, mVl;
@@ -535,7 +655,7 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
     if ((rc = mmk_host::make_map_f32(&mWh, L.Wh, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f32(&mWl, L.Wl, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK, 0))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK, 32))) return rc;
     if ((rc = mmk_host::make_map_f32(&mVh, L.Vhi, m, R, R, BK, 32))) return rc;
     if ((rc = mmk_host::make_map_f32(&mVl, L.Vlo, m, R, R, BK, 32))) return rc;
     const long long rn = (long long)R * n;
@@ -543,18 +663,24 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                (split_w_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn)));
     gram_w(W, GW, st);
     gram_v_into(V, L.GVn, st);
+    MMK_LAUNCH("nnmf_sumsq_cached", st,
+               (sumsq_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart,
+                                                           L.counter)));
+    MMK_LAUNCH("nnmf_vgw", st,
+               (vgw_kernel<<<ceil_div(m, 64), 256, VGW_SMEM, st>>>(V, GW, L.DEN, m)));
     MMK_LAUNCH("nnmf_vstep_tc", st,
-               (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, GW, V_out, L.Vhi,
-                                                                L.Vlo, (int)m, (int)n, L.part)));
+               (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, L.DEN, V_out, L.Vhi,
+                                                                L.Vlo, (int)m, (int)n, L.part,
+                                                                g_trace_v)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
-               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.GVn, GW,
+               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx, L.GVn, GW,
                                                         red + rn + (long long)R * R)));
     gram_v_into(V_out, red + rn, st);
     MMK_LAUNCH("nnmf_wstep_tc", st,
                (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, (int)m, (int)n,
                                                                 P.splits, P.rows_per_split,
-                                                                L.wpart)));
+                                                                L.wpart, g_trace_w)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
                (wreduce_tc_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(L.wpart, P.splits, n, red)));
@@ -563,3 +689,11 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 }
 
 }  // namespace mmk_tc
+
+// Debug hook: per-stage pipeline timestamps of CTA 0 (5 x 256 uint64 each, or
+// NULL to disable).  Not part of the solver ABI contract.
+extern "C" int mmk_tc_set_trace(unsigned long long* vstep, unsigned long long* wstep) {
+    g_trace_v = vstep;
+    g_trace_w = wstep;
+    return 0;
+}
