@@ -48,7 +48,7 @@ constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W (or V') chunk hi; same a
 constexpr int XST = 8;                      // X ring (128 KB in flight per SM)
 constexpr int OST = 4;                      // operand (W / V' chunk) ring
 constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + 1024;
-constexpr int NA = 4;                       // TMEM lo-operand buffers
+constexpr int NA = 4;                       // TMEM lo-operand buffers (NA < XST)
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
 constexpr int TMAX = 3;                     // accumulators per pass (V step: row tiles)
 constexpr int CB = 2;                       // W step: 128-column blocks per item
@@ -203,8 +203,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                         tc::tc_fence_after();
                         issue_stage<MN>(tmem + j * ACC, tmem + TM_A + ab * 32, xring + xs * SX, ob,
                                         kb == 0);
-                        tc::mma_commit(&B.xempty[xs]);
-                        tc::mma_commit(&B.aempty[ab]);
+                        tc::mma_commit(&B.xempty[xs]);   // also frees lo-buffer ab (see split)
                         trace_at(tr, 4, xit);
                     }
                     tc::mma_commit(&B.oempty[os]);
@@ -224,7 +223,12 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     const int xs = xit % XST, ab = xit % NA;
                     tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
                     if (quarter == 0 && lane == 0) trace_at(tr, 1, xit);
-                    tc::mbar_wait(&B.aempty[ab], ((xit / NA) & 1) ^ 1);
+                    // lo-buffer ab was last read by the MMAs of stage xit - NA, whose
+                    // completion is the commit on that stage's X-slot barrier
+                    if (xit >= NA) {
+                        const int prev = xit - NA;
+                        tc::mbar_wait(&B.xempty[prev % XST], (prev / XST) & 1);
+                    }
                     tc::tc_fence_after();
                     split_stage<MN>(xring + xs * SX, quarter, lane, tmem + TM_A + ab * 32 + lane_off);
                     tc::tmem_st_wait();
