@@ -303,6 +303,53 @@ def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
             "path": "nnmf_run(NnmfProblem(pinned host X), fused device loop) -> host factors"}
 
 
+def bench_mds_large(args, torch, world, rank, dev):
+    """BASELINE config 5: MDS n = 65536, dim 3, unit weights, packed upper
+    triangle; tiles split evenly across ranks (one all-reduce of the
+    per-point accumulators per iteration)."""
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import _lib, datasets as D
+    from paper_1003_3272_b200.mds import PackedMdsProblem, _GpuMdsTri, tile_count
+    from paper_1003_3272_b200.parallel import nccl_comm_ptr, tile_range
+    W = WORKLOADS[args.workload]
+    n, dim = W["n"], W["dim"]
+    be = M.Backend(dtype="fp32", device=dev.index, mds_kernel="tri")
+    nt = tile_count(n)
+    t0, t1 = tile_range(nt, world, rank)
+    prob = PackedMdsProblem.from_rows(D.distance_rows(n, seed=0), n, dim, be, tiles=(t0, t1))
+    comm = nccl_comm_ptr() if world > 1 else None
+    mm = _GpuMdsTri(prob, be, comm=comm)
+    g = torch.Generator(device=dev)
+    g.manual_seed(2)
+    th = [torch.rand(dim, n, generator=g, device=dev) * 2 - 1, None]
+    th[1] = torch.empty_like(th[0])
+    cur = [0]
+
+    def step():
+        a = cur[0]
+        mm._iterate(th[a], th[1 - a], mm.status.f_ptr, mm.status.err_ptr)
+        cur[0] = 1 - a
+
+    timing = time_steps(args, torch, dev, step, world)
+    lib = _lib.load()
+    lib.mmk_prof_enable(1)
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize(dev)
+    lib.mmk_prof_enable(0)
+    prof = _lib.prof_report()
+    alg = {"mds_tri": (t1 - t0) * 128 * 128 * 4 + 2 * dim * n * 4}
+    launches = sum(c for c, _ in prof.values()) // 2
+    roof = roofline(prof, alg, "hbm", "dominant")
+    kernels = {k: {"launches_per_step": c // 2, "avg_ms": ms / c} for k, (c, ms) in prof.items()}
+    mm._check_error()
+    e2e = None
+    return timing, roof, launches, e2e, {
+        "kernels": kernels, "e2e_note": "not measured for mds-large this round",
+        "data": "synthetic (Y_ij = ||z_i - z_j||(1 + 0.05 e_ij), z ~ N(0, I_10), e from a "
+                "symmetric pair hash; theta0 uniform[-1,1]; datasets.distance_rows)"}
+
+
 def time_steps(args, torch, dev, step, world):
     import torch.distributed as dist
     for _ in range(args.warmup):
@@ -403,9 +450,12 @@ def run_ours(args):
     from paper_1003_3272_b200 import build as B
     B.build()
     W = WORKLOADS[args.workload]
-    if W["solver"] != "nnmf" or not args.workload.endswith("large"):
-        raise SystemExit(f"workload {args.workload} not wired into the headline bench yet")
-    timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
+    if args.workload == "nnmf-large":
+        timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
+    elif args.workload == "mds-large":
+        timing, roof, launches, e2e, extra = bench_mds_large(args, torch, world, rank, dev)
+    else:
+        raise SystemExit(f"workload {args.workload} runs inside the suite (see --workload help)")
     extra = extra or {}
     ms = timing["ms_total"]
     value = args.steps / (ms / 1000.0)
@@ -423,7 +473,8 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
-            "data": "synthetic (uniform [0,1) X, uniform start; torch.Generator seeded)",
+            "data": extra.get("data", "synthetic (uniform [0,1) X, uniform start; "
+                                      "torch.Generator seeded)"),
             "config": workload_config(args, W),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps, "clocks": timing["clocks"],

@@ -149,6 +149,42 @@ int mmk_mds_iter(int dtype, const void *Y, const void *Wt, int64_t ldy, const do
                  double *f_dev, int64_t *err_dev, void *stream);
 
 /* ------------------------------------------------------------------------
+ * MDS for large unit-weight problems (W = 1 - I, cli.py:181) over a PACKED
+ * UPPER TRIANGLE of Y: 128 x 128 tiles (I <= J) stored row-major over the
+ * triangle, 64 KB each (fp32 only, dim <= 3).  Every unordered pair is
+ * visited once per iteration (half the bytes of a full-row pass).
+ * Replaces stress / mds_update / _coincidence_error (mds.py:92-144) for the
+ * BASELINE config-5 shape.  [t0, t1) is this rank's range of linear tile
+ * indices (all tiles on one GPU; a balanced split when sharded).
+ *
+ *   pack   : tiles of [t0, t1) whose tile row lies in full rows
+ *            [row0, row0 + rows) of Y (leading dim ldy) -> packed
+ *            (packed[u] = tile t0 + u); validate != 0 also checks finite,
+ *            nonnegative, zero diagonal and exact symmetry (DOMAIN sites
+ *            2, 3, 5, 4) where the transposed row is inside the block.
+ *   iter_a : red = [ per point C_i[dim] = sum_j z_ij (theta_j - theta_i) |
+ *            stress partial | S = sum_i theta_i (from the rank holding
+ *            tile 0 only) ] (fp64, n*dim + 1 + dim); the sharded caller
+ *            all-reduces it.
+ *   iter_b : theta_out = MM update from red, f_dev = stress.
+ * Coupled coincident points set NUMERICS with index i*n + j (site 1).
+ * ---------------------------------------------------------------------- */
+int64_t mmk_mds_tri_ntiles(int64_t n);
+int64_t mmk_mds_tri_reduce_len(int64_t n, int64_t dim);
+int mmk_mds_tri_ws_bytes(int64_t n, int64_t dim, int64_t t0, int64_t t1, size_t *out);
+int mmk_mds_tri_pack(const float *Y, int64_t ldy, int64_t n, int64_t row0, int64_t rows,
+                     float *packed, int64_t t0, int64_t t1, int validate, int64_t *err_dev,
+                     void *stream);
+int mmk_mds_tri_iter_a(const float *packed, int64_t t0, int64_t t1, const float *theta,
+                       int64_t dim, int64_t n, void *ws, size_t ws_bytes, double *red,
+                       int64_t *err_dev, void *stream);
+int mmk_mds_tri_iter_b(const float *theta, float *theta_out, int64_t dim, int64_t n,
+                       const double *red, double *f_dev, void *stream);
+int mmk_mds_tri_iter(const float *packed, int64_t t0, int64_t t1, const float *theta,
+                     float *theta_out, int64_t dim, int64_t n, void *ws, size_t ws_bytes,
+                     double *red, double *f_dev, int64_t *err_dev, void *stream);
+
+/* ------------------------------------------------------------------------
  * Sharded-layout helper: gathered [G][dim][rows_pad] -> theta [dim][n]
  * (the coordinate all-gather of the row-sharded MDS path).
  * ---------------------------------------------------------------------- */
@@ -224,6 +260,10 @@ int mmk_mds_engine_create(int dtype, const void *Y, const void *Wt, int64_t ldy,
                           int64_t rows_pad, void *ws, size_t ws_bytes, void *comm,
                           const mmk_stop_rule *rule, double *trace, int64_t *tstamp,
                           int64_t *ctl, int64_t *err_dev, void **engine);
+int mmk_mds_tri_engine_create(const float *packed, int64_t t0, int64_t t1, float *thetaA,
+                              float *thetaB, int64_t dim, int64_t n, void *ws, size_t ws_bytes,
+                              double *red, void *comm, const mmk_stop_rule *rule, double *trace,
+                              int64_t *tstamp, int64_t *ctl, int64_t *err_dev, void **engine);
 int mmk_engine_run(void *engine, void *stream);
 void mmk_engine_destroy(void *engine);
 

@@ -17,7 +17,7 @@ from .driver import MmConfig, MmProblem, MmTrace, relative_change, run_mm
 from .errors import (DeviceError, DomainError, InputError, MatrixFormatError, MmkitError,
                      MonotonicityError, NonFiniteError, NumericsError, ShapeError)
 from .kernels import elementwise, matmul, matvec, tree_reduce_sum
-from .mds import (MdsProblem, anchor_configuration, mds_run, mds_update, stress,
+from .mds import (MdsProblem, PackedMdsProblem, anchor_configuration, mds_run, mds_update, stress,
                   stress_gradient)
 from .nnmf import (FactorPair, NnmfProblem, nnmf_gradient, nnmf_objective, nnmf_run,
                    nnmf_surrogate, nnmf_update_v, nnmf_update_w)

@@ -57,6 +57,16 @@ _SIGS = {
     "mmk_mds_iter": ([_i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i32,
                       _vp, _sz, _vp, _vp, _vp], _i32),
     "mmk_mds_unpack": ([_i32, _vp, _vp, _i64, _i64, _i64, _vp], _i32),
+    "mmk_mds_tri_ntiles": ([_i64], _i64),
+    "mmk_mds_tri_reduce_len": ([_i64, _i64], _i64),
+    "mmk_mds_tri_ws_bytes": ([_i64, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
+    "mmk_mds_tri_pack": ([_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp], _i32),
+    "mmk_mds_tri_iter_a": ([_vp, _i64, _i64, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp], _i32),
+    "mmk_mds_tri_iter_b": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _i32),
+    "mmk_mds_tri_iter": ([_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp, _vp],
+                         _i32),
+    "mmk_mds_tri_engine_create": ([_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp,
+                                   _vp, _vp, _vp, _vp, _vp], _i32),
     "mmk_nccl_available": ([], _i32),
     "mmk_allreduce_f64": ([_vp, _i64, _vp, _vp], _i32),
     "mmk_allgather": ([_vp, _vp, _i64, _i32, _vp, _vp], _i32),

@@ -18,6 +18,11 @@ deterministic run to run) and is otherwise ignored.
 ``fused`` lets ``run_mm`` hand whole runs to the device engine (CUDA graphs,
 stopping rule on the device; see ``_engine.py``).  ``fused=False`` keeps the
 plain one-iteration-per-host-round-trip loop.
+
+``mds_kernel`` picks the MDS pairwise kernel: ``"rows"`` (full-row tiling,
+any weights, fp32/fp64), ``"tri"`` (packed upper triangle, unit weights,
+fp32, p <= 3: every pair read once) or ``"auto"`` (tri from
+``mds.TRI_MIN_POINTS`` points when it applies).
 """
 
 from dataclasses import dataclass
@@ -34,12 +39,15 @@ class Backend:
     dtype: str = "fp64"
     device: Optional[int] = None
     fused: bool = True
+    mds_kernel: str = "auto"
 
     def __post_init__(self):
         if self.threads < 1:
             raise ShapeError(f"backend needs at least 1 thread, got {self.threads}")
         if self.dtype not in ("fp32", "fp64"):
             raise ShapeError(f"dtype must be 'fp32' or 'fp64', got {self.dtype!r}")
+        if self.mds_kernel not in ("auto", "rows", "tri"):
+            raise ShapeError(f"mds_kernel must be 'auto', 'rows' or 'tri', got {self.mds_kernel!r}")
 
     @staticmethod
     def serial(dtype="fp64", device=None):

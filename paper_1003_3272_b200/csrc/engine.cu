@@ -305,3 +305,24 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
     std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * esize(dtype)}};
     return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
 }
+
+extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_t t1,
+                                         float* thetaA, float* thetaB, int64_t dim, int64_t n,
+                                         void* ws, size_t ws_bytes, double* red, void* comm,
+                                         const mmk_stop_rule* rule, double* trace,
+                                         int64_t* tstamp, int64_t* ctl, int64_t* err_dev,
+                                         void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    const int64_t rl = mmk_mds_tri_reduce_len(n, dim);
+    auto iter = [=](cudaStream_t s) -> int {
+        int rc = mmk_mds_tri_iter_a(packed, t0, t1, thetaA, dim, n, ws, ws_bytes, red, err_dev, s);
+        if (rc) return rc;
+        if (comm) {
+            rc = mmk_allreduce_f64(red, rl, comm, s);
+            if (rc) return rc;
+        }
+        return mmk_mds_tri_iter_b(thetaA, thetaB, dim, n, red, f_dev, s);
+    };
+    std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * sizeof(float)}};
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}

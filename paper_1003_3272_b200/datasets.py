@@ -32,7 +32,7 @@ log = logging.getLogger(__name__)
 
 __all__ = ["PetGeometry", "build_system_matrix", "build_neighborhoods",
            "default_phantom", "simulate_counts", "votes_to_dissimilarity",
-           "synthetic_votes", "cbcl_preprocess", "tree_row_sums"]
+           "synthetic_votes", "cbcl_preprocess", "tree_row_sums", "distance_rows"]
 
 
 # ---------------------------------------------------------------------------
@@ -239,3 +239,32 @@ def cbcl_preprocess(raw):
     if frac > 0.0:
         log.info("cbcl_preprocess clamped %.3f%% of entries into [0, 1]", 100.0 * frac)
     return out
+
+
+# ---------------------------------------------------------------------------
+def distance_rows(n, seed=0, latent_dim=10, noise=0.05, device="cuda"):
+    """Device generator of large synthetic MDS dissimilarities (BASELINE
+    config 5): latent points z ~ N(0, I_latent) (torch
+    generator ``seed``), Y_ij = ||z_i - z_j|| (1 + noise * e_ij) with e_ij in
+    [-1, 1) from an integer hash of the unordered pair (exactly symmetric),
+    zero diagonal.  Returns ``rows(r0, r1)`` -> fp32 tensor of rows [r0, r1);
+    nothing n x n is ever materialised at once (feed it to
+    ``PackedMdsProblem.from_rows``).  The n = 65536 matrix does not fit a
+    numpy PCG64 recipe in host memory, hence a device hash instead of
+    ``default_rng(1)``."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    z = torch.randn(n, latent_dim, generator=g, device=device, dtype=torch.float32)
+    jj = torch.arange(n, device=device, dtype=torch.int64)
+
+    def rows(r0, r1):
+        d = torch.cdist(z[r0:r1], z)
+        ii = torch.arange(r0, r1, device=device, dtype=torch.int64)[:, None]
+        lo, hi = torch.minimum(ii, jj), torch.maximum(ii, jj)
+        h = (lo * 0x9E3779B1 + hi * 0x85EBCA77 + seed) & 0xFFFFFF
+        e = h.to(torch.float32) / float(1 << 23) - 1.0
+        y = d * (1.0 + noise * e)
+        y[torch.arange(r1 - r0, device=device), torch.arange(r0, r1, device=device)] = 0.0
+        return y
+    return rows

@@ -13,7 +13,10 @@ coordinate k of every point, which is also the coalesced layout the pairwise
 kernel wants.  Stress and update are computed by ``csrc/mds.cu`` directly
 from coordinate differences; no n x n matrix is ever formed on the device.
 Unit weights (W = 1 - I, what the CLI always builds) are detected once and
-never uploaded.  ``stress_gradient`` / ``mds_surrogate`` are host fp64
+never uploaded.  Large unit-weight fp32 problems (and ``PackedMdsProblem``,
+a device-resident problem built straight into the packed layout) run on
+``csrc/mds_tri.cu``: Y stored once as the packed upper triangle of 128 x 128
+tiles and every unordered pair visited once per iteration.  ``stress_gradient`` / ``mds_surrogate`` are host fp64
 property-test helpers.
 """
 
@@ -31,7 +34,7 @@ from .datasets import votes_to_dissimilarity  # noqa: F401  (re-export)
 from .driver import run_mm
 from .errors import DomainError, InputError, NumericsError, ShapeError
 
-__all__ = ["MdsProblem", "stress", "stress_gradient", "mds_update", "mds_run",
+__all__ = ["MdsProblem", "PackedMdsProblem", "stress", "stress_gradient", "mds_update", "mds_run",
            "mds_surrogate", "anchor_configuration", "votes_to_dissimilarity"]
 
 
@@ -106,6 +109,125 @@ class MdsProblem:
         return d
 
 
+TRI_MIN_POINTS = 4096   # Backend(mds_kernel="auto") uses the packed kernel from here
+TILE = 128
+
+_DOMAIN_MSGS = {
+    2: "dissimilarities contain non-finite entries",
+    3: "dissimilarities must be nonnegative",
+    4: "dissimilarities must be exactly symmetric",
+    5: "dissimilarities must have a zero diagonal",
+}
+
+
+def tile_count(n):
+    """Tiles of the packed upper triangle for n points."""
+    t = -(-n // TILE)
+    return t * (t + 1) // 2
+
+
+class PackedMdsProblem:
+    """Unit-weight MDS problem (W = 1 - I, ``cli.py:181``) whose
+    dissimilarities live on one GPU as the packed upper triangle of 128 x 128
+    fp32 tiles (``csrc/mds_tri.cu``) -- the form BASELINE config 5
+    (n = 65536) takes: 8.6 GB instead of 17.2 GB for full rows (and 34 GB
+    for the reference's fp64 n x n, ``mds.py:60-63``).
+
+    ``tiles = (t0, t1)`` is the range of linear tile indices held here: all of
+    them for one GPU, a balanced slice per rank when sharded
+    (``parallel.tile_range``).  Build with ``from_rows`` (a generator of fp32
+    row blocks on the device) or ``from_dense`` (a full matrix, validated on
+    the device like ``MdsProblem``, ``mds.py:40-58``)."""
+
+    unit_weights = True
+
+    def __init__(self, packed, n, p, tiles, device):
+        if p < 1:
+            raise InputError(f"embedding dimension must be >= 1, got {p}")
+        if n < 2:
+            raise DomainError("object 0 has zero total weight; its position is undefined")
+        self.packed, self.n, self.p = packed, int(n), int(p)
+        self.t0, self.t1 = int(tiles[0]), int(tiles[1])
+        self.device = device
+
+    @property
+    def q(self):
+        return self.n
+
+    @classmethod
+    def from_rows(cls, rows_fn, n, p, backend=SERIAL, tiles=None, block=4096, validate=False):
+        """``rows_fn(r0, r1)`` returns rows [r0, r1) of Y as an fp32 CUDA
+        tensor (n columns); blocks are multiples of 128 rows."""
+        torch = _lib.torch_mod()
+        dev = backend.torch_device()
+        t0, t1 = tiles if tiles is not None else (0, tile_count(n))
+        packed = torch.empty((t1 - t0) * TILE * TILE, dtype=torch.float32, device=dev)
+        status = _lib.StatusBlock(torch, dev)
+        status.clear_error()
+        block = max(TILE, -(-block // TILE) * TILE)
+        st = _lib.stream_handle(torch, dev)
+        for r0 in range(0, n, block):
+            r1 = min(n, r0 + block)
+            yb = rows_fn(r0, r1)
+            if yb.dtype != torch.float32 or yb.device != dev or yb.shape != (r1 - r0, n):
+                raise ShapeError(f"row block [{r0}, {r1}) must be fp32 ({r1 - r0}, {n}) on {dev}")
+            if yb.stride(1) != 1:
+                yb = yb.contiguous()
+            _lib.call("mmk_mds_tri_pack", _lib.ptr(yb), yb.stride(0), n, r0, r1 - r0,
+                      _lib.ptr(packed), t0, t1, 1 if validate else 0, status.err_ptr, st)
+        _, code, idx = status.read()
+        _lib.raise_device_error(code, idx, {k: (lambda i, m=m: m) for k, m in _DOMAIN_MSGS.items()})
+        return cls(packed, n, p, (t0, t1), dev)
+
+    @classmethod
+    def from_dense(cls, y, p, backend=SERIAL, tiles=None, validate=True):
+        """Full n x n dissimilarities (numpy or torch), checked on the device
+        for finiteness, sign, zero diagonal and exact symmetry."""
+        torch = _lib.torch_mod()
+        dev = backend.torch_device()
+        shp = tuple(A.shape_of(y))
+        if len(shp) != 2 or shp[0] != shp[1]:
+            raise ShapeError(f"dissimilarities must be square, got {shp}")
+        yt = (y if A.is_torch(y) else torch.from_numpy(np.ascontiguousarray(y)))
+        yt = yt.to(device=dev, dtype=torch.float32).contiguous()
+        n = shp[0]
+        return cls.from_rows(lambda r0, r1: yt[r0:r1], n, p, backend, tiles, block=n,
+                             validate=validate)
+
+
+def _use_tri(problem, backend):
+    ok = problem.unit_weights and backend.dtype == "fp32" and problem.p <= 3
+    if backend.mds_kernel == "tri":
+        if not ok:
+            raise ShapeError("the packed-triangle MDS kernel needs unit weights, fp32 and p <= 3")
+        return True
+    return backend.mds_kernel == "auto" and ok and problem.q >= TRI_MIN_POINTS
+
+
+def _packed_of(problem, backend):
+    """The packed form of a host MdsProblem (cached per device)."""
+    key = (str(backend.torch_device()), "tri")
+    pk = problem._dev.get(key)
+    if pk is None:
+        torch = _lib.torch_mod()
+        dev = backend.torch_device()
+        y = problem.dissimilarities
+        pk = PackedMdsProblem.from_rows(
+            lambda r0, r1: torch.from_numpy(np.ascontiguousarray(y[r0:r1], dtype=np.float32)
+                                            ).to(dev),
+            problem.q, problem.p, backend, block=2048)
+        problem._dev[key] = pk
+    return pk
+
+
+def _make_mm(problem, backend):
+    if isinstance(problem, PackedMdsProblem):
+        return _GpuMdsTri(problem, backend)
+    if _use_tri(problem, backend):
+        return _GpuMdsTri(_packed_of(problem, backend), backend)
+    return _GpuMds(problem, backend)
+
+
 def _check_theta(theta, problem):
     shp = tuple(A.shape_of(theta))
     if len(shp) != 2 or shp != (problem.p, problem.q):
@@ -171,10 +293,90 @@ class _GpuMds(DeviceMm):
         return mds_surrogate(state, anchor, self.problem)
 
 
+class _GpuMdsTri(DeviceMm):
+    """Packed-triangle MDS (``csrc/mds_tri.cu``); sharded when ``comm`` (an
+    NCCL communicator) or ``group`` (a torch process group) is set and the
+    problem holds a slice of the tiles: phase A leaves [zs_i, A_i | stress]
+    per point, one all-reduce combines the ranks, phase B updates every
+    point redundantly."""
+
+    direction = "minimize"
+
+    def __init__(self, packed, backend, comm=None, group=None):
+        if backend.dtype != "fp32":
+            raise ShapeError("the packed-triangle MDS kernel runs in fp32")
+        super().__init__(backend)
+        torch = self.torch
+        self.problem = packed
+        self.pk, self.n, self.dim = packed.packed, packed.n, packed.p
+        self.t0, self.t1 = packed.t0, packed.t1
+        self.comm, self.group = comm, group
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_mds_tri_ws_bytes", self.n, self.dim, self.t0,
+                                            self.t1), dtype=torch.uint8, device=self.device)
+        self.red = torch.zeros(_lib.load().mmk_mds_tri_reduce_len(self.n, self.dim),
+                               dtype=torch.float64, device=self.device)
+
+    def device_state(self, theta):
+        return A.to_device(theta, self.backend, self.torch)
+
+    def _alloc_like(self, s):
+        return self.torch.empty_like(s)
+
+    def _copy_into(self, dst, src):
+        dst.copy_(src)
+
+    def _bytes_per_iter(self):
+        return float((self.t1 - self.t0) * TILE * TILE * 4)
+
+    def _messages(self):
+        return {1: _coincide_msg(self.n)}
+
+    def _iterate(self, theta, out, f_ptr, err_ptr):
+        st = self.stream()
+        L = _lib
+        if self.group is None and self.comm is None:
+            L.call("mmk_mds_tri_iter", L.ptr(self.pk), self.t0, self.t1, L.ptr(theta), L.ptr(out),
+                   self.dim, self.n, L.ptr(self.ws), self.ws.numel(), L.ptr(self.red), f_ptr,
+                   err_ptr, st)
+            return
+        L.call("mmk_mds_tri_iter_a", L.ptr(self.pk), self.t0, self.t1, L.ptr(theta), self.dim,
+               self.n, L.ptr(self.ws), self.ws.numel(), L.ptr(self.red), err_ptr, st)
+        if self.comm is not None:
+            L.call("mmk_allreduce_f64", L.ptr(self.red), self.red.numel(),
+                   ctypes.c_void_p(self.comm), st)
+        else:
+            import torch.distributed as dist
+            dist.all_reduce(self.red, group=self.group)
+        L.call("mmk_mds_tri_iter_b", L.ptr(theta), L.ptr(out), self.dim, self.n, L.ptr(self.red),
+               f_ptr, st)
+
+    def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
+        self._keep = (a, b)
+        comm = ctypes.c_void_p(self.comm) if self.comm is not None else None
+        _lib.call("mmk_mds_tri_engine_create", _lib.ptr(self.pk), self.t0, self.t1, _lib.ptr(a),
+                  _lib.ptr(b), self.dim, self.n, _lib.ptr(self.ws), self.ws.numel(),
+                  _lib.ptr(self.red), comm, ctypes.byref(rule), _lib.ptr(trace),
+                  _lib.ptr(stamp), _lib.ptr(ctl), self.status.err_ptr, ctypes.byref(eng))
+
+    def stress_only(self, theta):
+        out = self.torch.empty_like(theta)
+        self._iterate(theta, out, self.status.f_ptr, self.status.err_ptr)
+        return self._check_error()
+
+    def update_only(self, theta):
+        out = self.torch.empty_like(theta)
+        self._iterate(theta, out, self.status.f_ptr, self.status.err_ptr)
+        self._check_error()
+        return out
+
+    def surrogate(self, state, anchor):
+        raise NotImplementedError("surrogate is a host helper of dense MdsProblem instances")
+
+
 def stress(theta, problem, backend=SERIAL):
     """Weighted squared mismatch over unordered pairs."""
     _check_theta(theta, problem)
-    mm = _GpuMds(problem, backend)
+    mm = _make_mm(problem, backend)
     return mm.stress_only(mm.device_state(theta))
 
 
@@ -182,7 +384,7 @@ def mds_update(theta, problem, backend=SERIAL):
     """One parallel stress-majorization step (every point moves given the
     previous configuration)."""
     _check_theta(theta, problem)
-    mm = _GpuMds(problem, backend)
+    mm = _make_mm(problem, backend)
     return A.to_user(mm.update_only(mm.device_state(theta)), theta)
 
 
@@ -220,9 +422,9 @@ def mds_run(problem, config, backend=SERIAL, anchor=False, theta0=None):
     if theta0 is None:
         theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
                                                             size=(problem.p, problem.q))
-    mm = _GpuMds(problem, backend)
+    mm = _make_mm(problem, backend)
     state, trace = run_mm(mm, mm.device_state(theta0), config)
-    theta = A.to_user(state, problem.weights if not A.is_torch(theta0) else theta0)
+    theta = A.to_user(state, theta0)
     if anchor:
         theta = anchor_configuration(theta)
     return theta, trace

@@ -7,9 +7,13 @@ SURVEY.md section 8(e): the paths shard where the math does --
   ``mmk_nnmf_iter_a`` leaves this rank's [P | G_V | f] partials in a fp64
   buffer, one NCCL all-reduce (sum) combines them, and phase B finishes W'
   redundantly on every rank (no broadcast).
-* MDS: points (rows of Y) are split; each rank updates its own points from
-  the full previous configuration, then the coordinates are all-gathered and
-  the stress partials all-reduced.
+* MDS (rows kernel): points (rows of Y) are split; each rank updates its own
+  points from the full previous configuration, then the coordinates are
+  all-gathered and the stress partials all-reduced.
+* MDS (packed triangle, large unit-weight problems): the TILES of the packed
+  upper triangle are split evenly (``tile_range``); phase A leaves per-point
+  [zs_i, A_i] partials and the stress partial, one all-reduce combines them
+  and every rank applies the (cheap, O(n dim)) update to all points.
 * PET: rays are split; the back-projection vector and loglik partial (the
   phase-A buffer) are all-reduced before the pixel update.
 
@@ -29,6 +33,13 @@ def shard_rows(n, world, rank):
     lo = rank * base + min(rank, extra)
     hi = lo + base + (1 if rank < extra else 0)
     return lo, hi
+
+
+def tile_range(ntiles, world, rank):
+    """Contiguous balanced slice [t0, t1) of the packed-triangle MDS tiles
+    (``csrc/mds_tri.cu``) held and processed by ``rank``: every rank gets
+    the same number of 64 KB tiles (+-1), i.e. the same HBM traffic."""
+    return ntiles * rank // world, ntiles * (rank + 1) // world
 
 
 def padded_rows(n, world):
