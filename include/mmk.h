@@ -276,6 +276,12 @@ void mmk_engine_destroy(void *engine);
 int mmk_selftest_tc(const float *A, const float *B, const float *X, const float *V, float *D1,
                     float *D2, float *D3, int mode, int *diag, void *stream);
 
+/* Tuning aid: cycles for `iters` back-to-back tcgen05.mma of one shape
+ * (mode 0 SS tf32 N128, 1 TS tf32 N128, 2 TS tf32 N64, 3 SS tf32 N256,
+ * 4 SS f16 N128, 5 SS tf32 N64, 6 TS f16 N256, 7 SS f16 N256; M = 128) into
+ * out[0] (device int64). */
+int mmk_tc_mma_bench(int mode, int iters, long long *out, void *stream);
+
 /* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core
  * NNMF kernels, 5 x 256 uint64 per buffer (TMA issue, split start, split
  * done, MMA start, MMA committed); NULL disables (the default). */

@@ -78,6 +78,7 @@ _SIGS = {
                                _i64, _i64, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "mmk_engine_run": ([_vp, _vp], _i32),
     "mmk_tc_set_trace": ([_vp, _vp], _i32),
+    "mmk_tc_mma_bench": ([_i32, _i32, _vp, _vp], _i32),
     "mmk_selftest_tc": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp], _i32),
     "mmk_engine_destroy": ([_vp], None),
 }

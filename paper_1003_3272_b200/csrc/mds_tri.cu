@@ -342,27 +342,34 @@ mds_tri_stage(const float* __restrict__ theta, float* __restrict__ thp, int n, l
     }
 }
 
-// red[p][.] = fixed-order sum of every partial of point p; red[n*DIM] = stress
+// red[p][.] = fixed-order sum of every partial of point p; red[n*DIM] = stress.
+// One CTA per tile column P: 4 groups of 128 threads split the column tiles
+// (I = g, g + 4, ...), group 0 adds the row partials, and the 4 group sums
+// are combined in a fixed order (deterministic).
+constexpr int kAccGroups = 4;
 template <int DIM>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128 * kAccGroups)
 mds_tri_accum(const float* __restrict__ colpart, const float* __restrict__ rowpart, int kmax,
               const double* __restrict__ stpart, int G, long long t0, long long ntl, int T, int n,
               double* __restrict__ red, unsigned int* counter) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) {
-        const int P = p / TB, pl = p % TB;
-        double acc[DIM];
+    __shared__ double part[kAccGroups][DIM][TB];
+    __shared__ double sc[32];
+    const int P = blockIdx.x, pl = threadIdx.x % TB, g = threadIdx.x / TB;
+    double acc[DIM];
 #pragma unroll
-        for (int q = 0; q < DIM; ++q) acc[q] = 0.0;
-        const long long Ilo = 0;
+    for (int q = 0; q < DIM; ++q) acc[q] = 0.0;
+    // tiles (I, P) of the local range: I in [Ilo, P]
+    const long long base = tri_index(0, P, T);   // I = 0
 #pragma unroll 4
-        for (long long I = Ilo; I <= P; ++I) {
-            const long long u = tri_index(I, P, T) - t0;
-            if (u < 0 || u >= ntl) continue;
-            const float* cp = colpart + u * (DIM * TB) + pl;
+    for (int I = g; I <= P; I += kAccGroups) {
+        const long long u = tri_index(I, P, T) - t0;
+        if (u < 0 || u >= ntl) continue;
+        const float* cp = colpart + u * (DIM * TB) + pl;
 #pragma unroll
-            for (int q = 0; q < DIM; ++q) acc[q] += (double)cp[q * TB];
-        }
+        for (int q = 0; q < DIM; ++q) acc[q] += (double)__ldg(cp + q * TB);
+    }
+    (void)base;
+    if (g == 0) {
         long long lo = tri_index(P, P, T) - t0, hi = tri_index(P, T - 1, T) - t0;
         if (lo < 0) lo = 0;
         if (hi > ntl - 1) hi = ntl - 1;
@@ -375,10 +382,20 @@ mds_tri_accum(const float* __restrict__ colpart, const float* __restrict__ rowpa
                 for (int q = 0; q < DIM; ++q) acc[q] += (double)rp[q * TB];
             }
         }
-#pragma unroll
-        for (int q = 0; q < DIM; ++q) red[(long long)p * DIM + q] = acc[q];
     }
-    __shared__ double sc[32];
+#pragma unroll
+    for (int q = 0; q < DIM; ++q) part[g][q][pl] = acc[q];
+    __syncthreads();
+    const int p = P * TB + threadIdx.x;
+    if (threadIdx.x < TB && p < n) {
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) {
+            double t = part[0][q][threadIdx.x];
+#pragma unroll
+            for (int k = 1; k < kAccGroups; ++k) t += part[k][q][threadIdx.x];
+            red[(long long)p * DIM + q] = t;
+        }
+    }
     if (arrive_last(counter, gridDim.x)) {
         const double tot = block_sum_array(stpart, G, sc);
         if (threadIdx.x == 0) red[(long long)n * DIM] = tot;
@@ -461,7 +478,7 @@ struct TriWs {
     long long npad;
 };
 
-constexpr int kStageBlocks = 64;
+constexpr int kStageBlocks = 2 * kNumSMs;
 
 size_t tri_layout(const TriPlan& P, int dim, void* base, TriWs* L) {
     size_t off = 256;
@@ -525,7 +542,7 @@ int tri_a(const float* Yp, long long t0, long long t1, const float* theta, int n
                    err)));
     MMK_CHECK_LAUNCH("mds_tri_kernel");
     MMK_LAUNCH("mds_tri_accum", st,
-               (mds_tri_accum<DIM><<<ceil_div(n, 128), 128, 0, st>>>(
+               (mds_tri_accum<DIM><<<P.T, 128 * kAccGroups, 0, st>>>(
                    L.colpart, L.rowpart, P.kmax, L.stpart, P.G, t0, P.ntl, P.T, n, red,
                    L.counter)));
     MMK_CHECK_LAUNCH("mds_tri_accum");

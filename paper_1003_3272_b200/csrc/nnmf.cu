@@ -314,6 +314,41 @@ __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wou
     Wout[t] = (T)((double)W[t] * (red[t] / (den + kDenomGuard)));
 }
 
+// Rank-64 W finish: a block owns 16 columns; G (64 x 64) and the W slab sit
+// in shared memory, thread (k, column group) forms 4 denominators G_k. W_j
+// in fp64 and applies W' = W * P / (den + guard).
+template <typename T>
+__global__ void __launch_bounds__(256)
+nnmf_wfinish64_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
+                      const double* __restrict__ red, double* f_dev) {
+    __shared__ double G[64][65];
+    __shared__ double Ws[64][17];
+    const long long rn = 64 * n;
+    if (f_dev && blockIdx.x == 0 && threadIdx.x == 0) *f_dev = red[rn + 64 * 64];
+    const long long j0 = (long long)blockIdx.x * 16;
+    for (int i = threadIdx.x; i < 64 * 64; i += 256) G[i / 64][i % 64] = red[rn + i];
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+        const int l = i / 16, jj = i % 16;
+        Ws[l][jj] = (j0 + jj < n) ? (double)W[(long long)l * n + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    const int k = threadIdx.x >> 2, jg = (threadIdx.x & 3) * 4;
+    double den[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int l = 0; l < 64; ++l) {
+        const double g = G[k][l];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) den[q] = fma(g, Ws[l][jg + q], den[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long j = j0 + jg + q;
+        if (j < n)
+            Wout[(long long)k * n + j] =
+                (T)(Ws[k][jg + q] * (red[(long long)k * n + j] / (den[q] + kDenomGuard)));
+    }
+}
+
 // ---------------------------------------------------------------------------
 struct Plan {
     int g64w_blocks, g64w_cpb, g64v_blocks, g64v_cpb;   // rank-64 Gram split-K
@@ -548,6 +583,13 @@ template <typename T>
 int finish_b(const void* W, void* W_out, long long n, int r, const double* red, double* f_dev,
              cudaStream_t st) {
     const long long rn = (long long)r * n;
+    if (r == 64) {
+        MMK_LAUNCH("nnmf_wfinish", st,
+                   (nnmf_wfinish64_kernel<T><<<ceil_div(n, 16), 256, 0, st>>>(
+                       (const T*)W, (T*)W_out, n, red, f_dev)));
+        MMK_CHECK_LAUNCH("nnmf_wfinish64_kernel");
+        return MMK_OK;
+    }
     MMK_LAUNCH("nnmf_wfinish", st,
                (nnmf_wfinish_kernel<T><<<ceil_div(rn, 256), 256, 0, st>>>(
                    (const T*)W, (T*)W_out, n, r, red, f_dev)));

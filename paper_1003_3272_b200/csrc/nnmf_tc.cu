@@ -48,22 +48,26 @@ constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W (or V') chunk hi; same a
 constexpr int XST = 8;                      // X ring (128 KB in flight per SM)
 constexpr int OST = 4;                      // operand (W / V' chunk) ring
 constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + 1024;
-constexpr int NA = 4;                       // TMEM lo-operand buffers (NA < XST)
+constexpr int NA = 4;                       // TMEM A-operand buffers [X_hi | X_lo] (64 cols)
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
-constexpr int TMAX = 3;                     // accumulators per pass (V step: row tiles)
+constexpr int TMAX = 2;                     // accumulators per pass (V step: row tiles)
 constexpr int CB = 2;                       // W step: 128-column blocks per item
 constexpr int TM_COLS = 512;
 constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
+
+// experiment switches (MMK_TC_DBG, timing studies only; results are wrong
+// when set): 1 skip the lo MMAs, 2 skip the tf32 split, 4 skip all MMAs
+__constant__ int c_dbg = 0;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// The tensor core reads an fp32 operand as tf32 by ignoring its 13 low
-// mantissa bits, so the raw tile is the "hi" operand as-is; the exact
-// remainder x - trunc_tf32(x) is the "lo" operand, written to TMEM.
-__device__ __forceinline__ float tf32_rem(float x) {
-    return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+// 3xTF32 split of an X value: hi = x with its 13 low mantissa bits cleared
+// (what the tensor core reads of a tf32 operand), lo = x - hi exactly.
+__device__ __forceinline__ void tf32_hilo(float x, float& hi, float& lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    lo = x - hi;
 }
 
 struct Bars {
@@ -74,7 +78,7 @@ struct Bars {
 __device__ __forceinline__ void init_bars(Bars& B) {
     for (int s = 0; s < XST; ++s) {
         tc::mbar_init(&B.xfull[s], 1);
-        tc::mbar_init(&B.xempty[s], 1);
+        tc::mbar_init(&B.xempty[s], 128);   // released by the split warps
     }
     for (int s = 0; s < OST; ++s) {
         tc::mbar_init(&B.ofull[s], 1);
@@ -89,25 +93,28 @@ __device__ __forceinline__ void init_bars(Bars& B) {
     tc::fence_barrier_init();
 }
 
-// One stage of 3xTF32.  The operand chunk holds [B_hi ; B_lo] stacked along
-// N (64 + 64 rows, contiguous in smem): per K-step an SS MMA with N = 128
-// gives D[:, 0:64] += X_hi.B_hi and D[:, 64:128] += X_hi.B_lo, and a TS MMA
-// with N = 64 adds X_lo.B_hi (lo from TMEM) into D[:, 0:64].  The epilogue
-// sums the two halves: X_hi B_hi + X_hi B_lo + X_lo B_hi.
+// One stage of 3xTF32, both MMAs with A from TMEM (buffer a = [X_hi | X_lo],
+// 32 + 32 columns, written by the split warps) so the tensor core reads only
+// the B operand from shared memory.  The operand chunk holds [B_hi ; B_lo]
+// stacked along N (64 + 64 rows): per K-step a TS MMA with N = 128 gives
+// D[:, 0:64] += X_hi.B_hi and D[:, 64:128] += X_hi.B_lo, and a TS MMA with
+// N = 64 adds X_lo.B_hi into D[:, 0:64].  The epilogue sums the two halves:
+// X_hi B_hi + X_hi B_lo + X_lo B_hi.
 template <bool MN>
-__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t alo, const uint8_t* xh,
-                                            const uint8_t* bhl, bool first) {
-    constexpr uint32_t id_ts = tc::idesc_tf32(BM, R, 0, MN ? 1 : 0);
-    constexpr uint32_t id_ss = tc::idesc_tf32(BM, ACC, MN ? 1 : 0, MN ? 1 : 0);
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bhl,
+                                            bool first) {
+    constexpr uint32_t id_lo = tc::idesc_tf32(BM, R, 0, MN ? 1 : 0);
+    constexpr uint32_t id_hi = tc::idesc_tf32(BM, ACC, 0, MN ? 1 : 0);
     // descriptors advance by their 16-byte start-address field only
-    const uint64_t da0 = MN ? tc::sdesc_sw128_32b(xh, 4096, 512) : tc::sdesc_sw128(xh, 16, 1024);
     const uint64_t db0 = MN ? tc::sdesc_sw128_32b(bhl, 4096, 512) : tc::sdesc_sw128(bhl, 16, 1024);
     constexpr uint64_t step = MN ? (1024 >> 4) : (32 >> 4);
+    const int dbg = c_dbg;
+    if (dbg & 4) return;
 #pragma unroll
     for (int ks = 0; ks < BK / 8; ++ks) {
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-        tc::mma_tf32(d, da0 + ks * step, db0 + ks * step, id_ss, acc);
-        tc::mma_tf32_ts(d, alo + ks * 8, db0 + ks * step, id_ts, 1);
+        tc::mma_tf32_ts(d, a + ks * 8, db0 + ks * step, id_hi, acc);
+        if (!(dbg & 1)) tc::mma_tf32_ts(d, a + 32 + ks * 8, db0 + ks * step, id_lo, 1);
     }
 }
 
@@ -118,32 +125,37 @@ struct Pass {
     int nacc, nkb;
 };
 
-// lo-operand of an X stage into TMEM: V step (MN = false) reads row `lane`
-// of the 128B-swizzled K-major tile; W step (MN = true) reads column `lane`
-// of box `quarter` of the 32-byte-atom swizzled MN-major tile.
+// An X stage from shared memory into registers: V step (MN = false) reads
+// row `lane` of the 128B-swizzled K-major tile; W step (MN = true) reads
+// column `lane` of box `quarter` of the 32-byte-atom swizzled MN-major tile.
 template <bool MN>
-__device__ __forceinline__ void split_stage(const uint8_t* xs, int quarter, int lane,
-                                            uint32_t a_addr) {
-    float lo[32];
+__device__ __forceinline__ void read_stage(const uint8_t* xs, int quarter, int lane, float* x) {
     if (!MN) {
         const int row = quarter * 32 + lane;
         const float4* rp = reinterpret_cast<const float4*>(xs + row * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const float4 t = rp[c ^ (row & 7)];
-            lo[4 * c] = tf32_rem(t.x);
-            lo[4 * c + 1] = tf32_rem(t.y);
-            lo[4 * c + 2] = tf32_rem(t.z);
-            lo[4 * c + 3] = tf32_rem(t.w);
+            x[4 * c] = t.x;
+            x[4 * c + 1] = t.y;
+            x[4 * c + 2] = t.z;
+            x[4 * c + 3] = t.w;
         }
     } else {
         const uint8_t* bx = xs + quarter * 4096 + (lane & 7) * 4;
 #pragma unroll
         for (int k = 0; k < 32; ++k)
-            lo[k] = tf32_rem(
-                *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 3) ^ (k & 3)) << 5)));
+            x[k] = *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
     }
-    tc::tmem_st32(a_addr, lo);
+}
+
+// tf32 hi / lo of the 32 values into TMEM columns [a, a + 32) / [a + 32, a + 64)
+__device__ __forceinline__ void store_hilo(float* x, uint32_t a_addr) {
+    float lo[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) tf32_hilo(x[k], x[k], lo[k]);
+    tc::tmem_st32(a_addr, x);
+    tc::tmem_st32(a_addr + 32, lo);
 }
 
 // ---------------------------------------------------------------------------
@@ -197,13 +209,12 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     tc::mbar_wait(&B.ofull[os], (oit / OST) & 1);
                     const uint8_t* ob = oring + os * 2 * SOP;
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
-                        const int xs = xit % XST, ab = xit % NA;
+                        const int ab = xit % NA;
                         tc::mbar_wait(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
-                        issue_stage<MN>(tmem + j * ACC, tmem + TM_A + ab * 32, xring + xs * SX, ob,
-                                        kb == 0);
-                        tc::mma_commit(&B.xempty[xs]);   // also frees lo-buffer ab (see split)
+                        issue_stage<MN>(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
+                        tc::mma_commit(&B.aempty[ab]);   // A buffer ab free once these finish
                         trace_at(tr, 4, xit);
                     }
                     tc::mma_commit(&B.oempty[os]);
@@ -223,14 +234,14 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     const int xs = xit % XST, ab = xit % NA;
                     tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
                     if (quarter == 0 && lane == 0) trace_at(tr, 1, xit);
-                    // lo-buffer ab was last read by the MMAs of stage xit - NA, whose
-                    // completion is the commit on that stage's X-slot barrier
-                    if (xit >= NA) {
-                        const int prev = xit - NA;
-                        tc::mbar_wait(&B.xempty[prev % XST], (prev / XST) & 1);
-                    }
+                    float x[32];
+                    read_stage<MN>(xring + xs * SX, quarter, lane, x);
+                    // the values are in registers (consumed below): release the slot
+                    tc::mbar_arrive(&B.xempty[xs]);
+                    // A buffer ab was last read by the MMAs of stage xit - NA
+                    if (xit >= NA) tc::mbar_wait(&B.aempty[ab], ((xit / NA) - 1) & 1);
                     tc::tc_fence_after();
-                    split_stage<MN>(xring + xs * SX, quarter, lane, tmem + TM_A + ab * 32 + lane_off);
+                    if (!(c_dbg & 2)) store_hilo(x, tmem + TM_A + ab * 64 + lane_off);
                     tc::tmem_st_wait();
                     tc::tc_fence_before();
                     tc::mbar_arrive(&B.afull[ab]);
@@ -462,48 +473,137 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
     }
 }
 
-constexpr int VGW_SMEM = R * R * 8 + R * (64 + 4) * 4;
-
-// DEN = V G_W (the V-step denominator without its guard), fp64 accumulation,
-// stored fp32.  A block computes 64 rows x 64 columns with 4x4 register tiles
-// per thread; the V tile (transposed) and G_W sit in shared memory.
+// DEN = V G_W (the V-step denominator without its guard): fp32 FFMA with
+// G_W rounded to fp32 -- the denominator only needs fp32 accuracy (SURVEY.md
+// 7.3-1: Gram-side products in fp32 keep raw V within 5e-6 of fp64).  A block
+// computes 64 rows x 64 columns with 4 x 4 register tiles per thread.
+constexpr int VGW_SMEM = 2 * R * (64 + 4) * 4;
 __global__ void __launch_bounds__(256)
 vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __restrict__ DEN,
            long long m) {
-    extern __shared__ double vgw_smem[];
-    double(*G)[R] = reinterpret_cast<double(*)[R]>(vgw_smem);
-    float(*Vt)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem + R * R);
+    extern __shared__ float vgw_smem[];
+    float(*G)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem);
+    float(*Vt)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem + R * (64 + 4));
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const long long r0 = (long long)blockIdx.x * 64;
-    for (int i = threadIdx.x; i < R * R; i += 256) G[i / R][i % R] = GW[i];
-    for (int i = threadIdx.x; i < 64 * R; i += 256) {
-        const int rr = i / R, l = i % R;
-        Vt[l][rr] = (r0 + rr < m) ? V[(r0 + rr) * R + l] : 0.f;
+    for (int i = threadIdx.x; i < R * R; i += 256) G[i / R][i % R] = (float)GW[i];
+    for (int i = threadIdx.x; i < 16 * R; i += 256) {
+        const int rr = i / 16, l4 = (i % 16) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + l4);
+        Vt[l4][rr] = v.x;
+        Vt[l4 + 1][rr] = v.y;
+        Vt[l4 + 2][rr] = v.z;
+        Vt[l4 + 3][rr] = v.w;
     }
     __syncthreads();
-    double acc[4][4];
+    float acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 #pragma unroll 8
     for (int l = 0; l < R; ++l) {
         const float4 a = *reinterpret_cast<const float4*>(&Vt[l][4 * ty]);
-        const double2 b01 = *reinterpret_cast<const double2*>(&G[l][4 * tx]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&G[l][4 * tx + 2]);
-        const double av[4] = {a.x, a.y, a.z, a.w};
-        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+        const float4 b = *reinterpret_cast<const float4*>(&G[l][4 * tx]);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const long long row = r0 + 4 * ty + i;
         if (row < m)
             *reinterpret_cast<float4*>(DEN + row * R + 4 * tx) =
-                make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+                make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    }
+}
+
+// Rank-64 Gram G = sum_c a_c a_c^T of fp32 vectors a_c (VEC_ROWS: A is
+// 64 x len, the vectors are columns of the row-major W; else A is len x 64,
+// the rows of V).  Products are formed in fp32 and summed 8 at a time in
+// fp32, then folded into fp64 accumulators (4 x 4 per thread); each block
+// writes its partial, gram_sum_kernel adds the partials in block order.
+template <bool VEC_ROWS>
+__global__ void __launch_bounds__(256)
+gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
+              double* __restrict__ part) {
+    __shared__ __align__(16) float S[32][64 + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const long long c_begin = (long long)blockIdx.x * per_block;
+    long long c_end = c_begin + per_block;
+    if (c_end > len) c_end = len;
+    for (long long c0 = c_begin; c0 < c_end; c0 += 32) {
+        if (VEC_ROWS) {
+            for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
+                const int a = idx >> 5, cc = idx & 31;
+                S[cc][a] = (c0 + cc < c_end) ? A[(long long)a * len + c0 + cc] : 0.f;
+            }
+        } else {
+            for (int idx = threadIdx.x; idx < 32 * 16; idx += 256) {
+                const int cc = idx >> 4, a4 = (idx & 15) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (c0 + cc < c_end) v = *reinterpret_cast<const float4*>(A + (c0 + cc) * 64 + a4);
+                *reinterpret_cast<float4*>(&S[cc][a4]) = v;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k8 = 0; k8 < 32; k8 += 8) {
+            float p[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) p[i][j] = 0.f;
+#pragma unroll
+            for (int kk = k8; kk < k8 + 8; ++kk) {
+                const float4 a = *reinterpret_cast<const float4*>(&S[kk][4 * ty]);
+                const float4 b = *reinterpret_cast<const float4*>(&S[kk][4 * tx]);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+                const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) p[i][j] = fmaf(av[i], bv[j], p[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += (double)p[i][j];
+        }
+        __syncthreads();
+    }
+    double* pb = part + (long long)blockIdx.x * (R * R);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[i][j];
+}
+
+// out[e] = sum_b part[b][e] in block order: 8 groups of 128 threads take
+// interleaved partials, combined in group order (deterministic)
+__global__ void __launch_bounds__(1024)
+gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+    __shared__ double sm[8][128];
+    const int o = blockIdx.x * 128 + (threadIdx.x & 127), g = threadIdx.x >> 7;
+    double s = 0.0;
+#pragma unroll 4
+    for (int b = g; b < nparts; b += 8) s += part[(long long)b * (R * R) + o];
+    sm[g][threadIdx.x & 127] = s;
+    __syncthreads();
+    if (g == 0) {
+        double t = sm[0][threadIdx.x];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) t += sm[k][threadIdx.x];
+        out[o] = t;
     }
 }
 
@@ -518,16 +618,36 @@ __global__ void split_w_kernel(const float* __restrict__ W, float* __restrict__ 
     Wl[t] = l;
 }
 
-// red[k n + j] = sum_s wpart[s][j][k] (fixed split order)
-__global__ void wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
-                                  double* __restrict__ red) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * R) return;
-    const long long j = t / R;
-    const int k = (int)(t - j * R);
-    double s = 0.0;
-    for (int q = 0; q < splits; ++q) s += (double)wpart[((long long)q * n + j) * R + k];
-    red[(long long)k * n + j] = s;
+// red[k n + j] = sum_s wpart[s][j][k] (fixed split order); a block owns 32
+// columns j: coalesced reads of the [32 j][64 k] slab of every split, fp64
+// sums, transposed through shared memory for coalesced writes
+__global__ void __launch_bounds__(256)
+wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
+                  double* __restrict__ red) {
+    __shared__ double T[R][32 + 1];
+    const long long j0 = (long long)blockIdx.x * 32;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    // element e = q * 256 + tid of the slab: j = e / 64, k = e % 64
+    for (int sp = 0; sp < splits; ++sp) {
+        const float* src = wpart + ((long long)sp * n + j0) * R;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = q * 256 + threadIdx.x;
+            if (j0 + e / R < n) acc[q] += (double)src[e];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int e = q * 256 + threadIdx.x;
+        T[e % R][e / R] = acc[q];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * 32; e += 256) {
+        const int k = e / 32, jj = e % 32;
+        if (j0 + jj < n) red[(long long)k * n + j0 + jj] = T[k][jj];
+    }
 }
 
 // f-partial = sum x^2 - 2 <V, Q> + <G_V, G_W> (all over this rank's rows)
@@ -578,9 +698,27 @@ TcPlan tc_plan(long long m, long long n) {
     return P;
 }
 
+constexpr int kGramBlocks = 2 * kNumSMs;
+
+// G = Gram of A (see gram32_kernel) into out (fp64 64 x 64)
+void gram32(const float* A, long long len, bool vec_rows, double* gpart, double* out,
+            cudaStream_t st) {
+    long long per = (len + kGramBlocks - 1) / kGramBlocks;
+    per = (per + 31) / 32 * 32;
+    const int blocks = (int)((len + per - 1) / per);
+    if (vec_rows)
+        MMK_LAUNCH("nnmf_gram32", st,
+                   (gram32_kernel<true><<<blocks, 256, 0, st>>>(A, len, per, gpart)));
+    else
+        MMK_LAUNCH("nnmf_gram32", st,
+                   (gram32_kernel<false><<<blocks, 256, 0, st>>>(A, len, per, gpart)));
+    MMK_LAUNCH("nnmf_gram_sum", st,
+               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out)));
+}
+
 struct TcWs {
     float *Wh, *Wl, *Vhi, *Vlo, *wpart, *DEN;
-    double *GVn, *part, *sqpart;
+    double *GVn, *part, *sqpart, *gpart;
     XXCache* xx;
     unsigned int* counter;
 };
@@ -603,6 +741,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oP = take(16 * (size_t)kNumSMs);
     size_t oS = take(8 * (size_t)kNumSMs * 4);
     size_t oC = take(sizeof(XXCache) + 64);
+    size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
     if (base && L) {
         L->sqpart = (double*)(c_base(base) + oS);
         L->xx = (XXCache*)(c_base(base) + oC);
@@ -616,6 +755,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->wpart = (float*)(c + oWp);
         L->GVn = (double*)(c + oG);
         L->part = (double*)(c + oP);
+        L->gpart = (double*)(c + oGP);
     }
     return off;
 }
@@ -649,6 +789,11 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);
     if (!g_attr_done) {
+        const char* dbg = getenv("MMK_TC_DBG");
+        if (dbg) {
+            const int v = atoi(dbg);
+            cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
+        }
         cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
@@ -665,8 +810,10 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     const long long rn = (long long)R * n;
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn)));
-    gram_w(W, GW, st);
-    gram_v_into(V, L.GVn, st);
+    (void)gram_w;
+    (void)gram_v_into;
+    gram32(W, n, true, L.gpart, GW, st);
+    gram32(V, m, false, L.gpart, L.GVn, st);
     MMK_LAUNCH("nnmf_sumsq_cached", st,
                (sumsq_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart,
                                                            L.counter)));
@@ -680,14 +827,14 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx, L.GVn, GW,
                                                         red + rn + (long long)R * R)));
-    gram_v_into(V_out, red + rn, st);
+    gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_wstep_tc", st,
                (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, (int)m, (int)n,
                                                                 P.splits, P.rows_per_split,
                                                                 L.wpart, g_trace_w)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
-               (wreduce_tc_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(L.wpart, P.splits, n, red)));
+               (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red)));
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a");
     return MMK_OK;
 }

@@ -174,3 +174,72 @@ extern "C" int mmk_selftest_tc(const float* A, const float* B, const float* X, c
     MMK_CHECK_LAUNCH("tc_selftest_kernel");
     return MMK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// MMA issue-rate microbenchmark (tuning aid): one CTA, one thread issues
+// `iters` back-to-back tcgen05.mma of one shape on zeroed operands, commits,
+// waits; out[0] = cycles.  mode: 0 SS tf32 N128, 1 TS tf32 N128, 2 TS tf32
+// N64, 3 SS tf32 N256, 4 SS f16 N128 K16, 5 SS tf32 N64, 6 TS f16 N256,
+// 7 SS f16 N256.
+namespace {
+__global__ void __launch_bounds__(128) tc_mma_bench_kernel(int mode, int iters, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 64 * 1024 / 4; i += 128) reinterpret_cast<float*>(base)[i] = 0.f;
+    tc::fence_async_smem();
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (tid == 0) {
+        const uint64_t da = tc::sdesc_sw128(base, 16, 1024);
+        const uint64_t db = tc::sdesc_sw128(base + 16384, 16, 1024);
+        // f16: a fmt 0 (F16), b fmt 0, c F32
+        const uint32_t id_f16_128 = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const uint32_t id_f16_256 = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint32_t acc = i ? 1u : 0u;
+            switch (mode) {
+                case 0: tc::mma_tf32(tm, da, db, tc::idesc_tf32(128, 128, 0, 0), acc); break;
+                case 1: tc::mma_tf32_ts(tm, tm + 256, db, tc::idesc_tf32(128, 128, 0, 0), acc); break;
+                case 2: tc::mma_tf32_ts(tm, tm + 256, db, tc::idesc_tf32(128, 64, 0, 0), acc); break;
+                case 3: tc::mma_tf32(tm, da, db, tc::idesc_tf32(128, 256, 0, 0), acc); break;
+                case 4: tc::mma_f16ss(tm, da, db, id_f16_128, acc); break;
+                case 5: tc::mma_tf32(tm, da, db, tc::idesc_tf32(128, 64, 0, 0), acc); break;
+                case 6: tc::mma_f16ts(tm, tm + 256, db, id_f16_256, acc); break;
+                case 7: tc::mma_f16ss(tm, da, db, id_f16_256, acc); break;
+                // independent accumulators (D rotates over 4 / 2 regions)
+                case 8: tc::mma_tf32(tm + (i & 3) * 128, da, db, tc::idesc_tf32(128, 128, 0, 0), i >= 4); break;
+                case 9: tc::mma_tf32_ts(tm + (i & 3) * 64, tm + 256, db, tc::idesc_tf32(128, 64, 0, 0), i >= 4); break;
+                case 10: tc::mma_tf32(tm + (i & 1) * 128, da, db, tc::idesc_tf32(128, 128, 0, 0), i >= 2); break;
+                case 11: tc::mma_tf32_ts(tm + (i & 1) * 128, tm + 256 + 64 * (i & 1), db, tc::idesc_tf32(128, 128, 0, 0), i >= 2); break;
+                default: tc::mma_f16ss(tm + (i & 1) * 256, da, db, id_f16_256, i >= 2); break;
+            }
+        }
+        tc::mma_commit(&bar);
+        tc::mbar_wait(&bar, 0);
+        out[0] = clock64() - t0;
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<512>(tm);
+}
+}  // namespace
+
+extern "C" int mmk_tc_mma_bench(int mode, int iters, long long* out, void* stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaFuncSetAttribute(tc_mma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
+    tc_mma_bench_kernel<<<1, 128, 70 * 1024, st>>>(mode, iters, out);
+    MMK_CHECK_LAUNCH("tc_mma_bench_kernel");
+    return MMK_OK;
+}
