@@ -109,6 +109,9 @@ bool prof_on();
 // 2-D fp32 row-major TMA map: box = 32 columns (128 B) x box_rows, 128B swizzle
 int make_map_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                  uint64_t row_stride_elems, uint32_t box_rows, int swizzle = 128);
+// 2-D fp16 row-major TMA map: box = 64 columns (128 B) x box_rows, 128B swizzle
+int make_map_f16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                 uint64_t row_stride_elems, uint32_t box_rows);
 void prof_start(const char* name, cudaStream_t s);
 void prof_stop(cudaStream_t s);
 }  // namespace mmk_host

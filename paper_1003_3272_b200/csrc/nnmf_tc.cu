@@ -1,34 +1,45 @@
-// nnmf_tc.cu -- tensor-core (tcgen05, kind::tf32, 3xTF32) path of the NNMF
-// MM iteration for large fp32 problems with rank 64 (BASELINE config 4).
+// nnmf_tc.cu -- tensor-core (tcgen05, kind::f16) path of the NNMF MM
+// iteration for large fp32 problems with rank 64 (BASELINE config 4).
 //
 // The two contractions with X are the whole cost (4mnr of
-// 5.5e11 flops); both run on the 5th-gen tensor cores in split-precision
-// "3xTF32": every fp32 operand is split into tf32 hi + lo (hi = round-to-
-// nearest tf32, lo = exact remainder) and a*b ~ hi*hi + hi*lo + lo*hi,
-// accumulated in fp32 in TMEM -- fp32-faithful products.
-// The O((m+n) r^2) Gram side stays in fp64 on the CUDA cores.
+// 5.5e11 flops).  Both run on the 5th-gen tensor cores as fp32-faithful
+// split products: every fp32 operand x is scaled by a power of two 2^e
+// (exact) so the largest |x 2^e| lies in [2^14, 2^15), then split into two
+// fp16 values hi = rn(x 2^e), lo = rn(x 2^e - hi) -- 22 significant bits.
+// x w ~ hi_x hi_w + hi_x lo_w + lo_x hi_w, accumulated in fp32 in TMEM and
+// scaled back by 2^-(e_x + e_w).  Elements within 2^18 of the scaled maximum
+// keep the full 22 bits; smaller ones lose low bits at an absolute level of
+// max * 2^-40, far below fp32 rounding of the dot products they enter.
 //
-//   nnmf_vstep_tc  (persistent, one CTA per SM, 10 warps)
-//     warp 0   TMA producer: X tile [128 rows x 32 cols] + W_hi/W_lo chunks
-//              [64 x 32] per stage (128-byte swizzle, K-major), 4 stages
-//     warps 2-5 split X in shared memory into hi (in place) / lo, and
-//              accumulate sum x^2 (fp64) for the objective
-//     warp 1   one thread issues 12 tcgen05.mma (M128 N64 K8) per stage into
-//              a double-buffered fp32 accumulator Q = X W^T in TMEM
-//     warps 6-9 epilogue: tcgen05.ld Q rows, V' = V * Q / (V G_W + 1e-300),
-//              <V, Q> (fp64); writes V' and its tf32 split for the W step
+// Why fp16 and not 3xTF32: a tcgen05.mma with M = 128 costs ~130-170 cycles
+// per 32 bytes of K whatever N is (measured, scripts/mma_bench.py), so the
+// MMA time per X element is set by the bytes of the A operand.  tf32 hi + lo
+// are 8 bytes per element (8 MMAs per 128 x 32 stage, ~900 cycles -- slower
+// than HBM delivers the stage); fp16 hi + lo are 4 bytes (4 MMAs).
+//
+//   nnmf_vstep_tc  (persistent, one CTA per SM, 14 warps)
+//     warp 0   TMA producer: X tile [128 rows x 64 cols] fp32 (two 128B-
+//              swizzled boxes) + [W_hi ; W_lo] fp16 chunk [128 x 64] per stage
+//     warps 2-9 split warps: read X rows from smem, release the slot, write
+//              fp16 hi / lo to a TMEM A-buffer (32 + 32 columns)
+//     warp 1   one thread issues 4 x (TS MMA hi, N = 128; TS MMA lo, N = 64)
+//              (M128 K16) per stage into an fp32 accumulator Q = X W^T
+//     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300), <V, Q> (fp64),
+//              max(V') for the W step's scale
+//   nnmf_vprep     V' -> V'^T hi / lo fp16 [64][m] (scaled): the W-step B operand
 //   nnmf_wstep_tc  P^T = X^T V' (M = 128 columns of X, N = 64, K = rows),
-//              split-K over row ranges; both operands MN-major (32-byte-atom
-//              128B swizzle, the only MN-major tf32 layout); per-split
-//              partials reduced in fixed order -> deterministic.
+//              split-K over row ranges; per-split partials reduced in fixed
+//              order -> deterministic.
 //
 // Objective f(V, W) = sum x^2 - 2 <V, X W^T> + <V^T V, W W^T> in fp64: every
 // term is a by-product of the pass (no extra X traffic).  Its conditioning
-// is ||X||^2 / f times the 3xTF32 accumulation error;
-// tests/test_nnmf_tc_gpu.py checks it against the explicit residual.
+// is ||X||^2 / f times the split-product accumulation error (SURVEY.md
+// 7.3-2); tests/test_nnmf_tc_gpu.py checks it against the explicit residual.
 //
 // HBM roofline: each kernel streams X once (m n 4 bytes) -> two passes per
 // iteration; tensor work 3 x 2mnr per kernel.
+#include <cuda_fp16.h>
+
 #include "mmk_common.cuh"
 #include "nnmf_tc.h"
 #include "tc_common.cuh"
@@ -37,16 +48,16 @@ namespace {
 
 using namespace mmk;
 
-constexpr int R = 64;            // rank of the tensor-core path (UMMA N)
+constexpr int R = 64;            // rank of the tensor-core path
 constexpr int BM = 128;          // UMMA M: rows of X (V step) / columns of X (W step)
-constexpr int BK = 32;           // K per stage: one 128-byte row of fp32
+constexpr int BK = 64;           // K per stage (fp32 X values; one 128-byte fp16 operand row)
 constexpr int NCONV = 8;         // split warps: groups of 4 take X stages round-robin
 constexpr int NGROUP = NCONV / 4;
 constexpr int kThreads = 32 * (2 + NCONV + 4);   // TMA, MMA, split x8, epilogue x4
-constexpr uint32_t SX = BM * BK * 4;        // 16 KB  raw X tile (the hi operand)
-constexpr uint32_t SOP = R * BK * 4;        //  8 KB  W (or V') chunk hi; same again for lo
-constexpr int XST = 8;                      // X ring (128 KB in flight per SM)
-constexpr int OST = 4;                      // operand (W / V' chunk) ring
+constexpr uint32_t SX = BM * BK * 4;        // 32 KB  fp32 X stage
+constexpr uint32_t SOP = R * BK * 2;        //  8 KB  fp16 operand chunk hi; same again for lo
+constexpr int XST = 4;                      // X ring (128 KB in flight per SM)
+constexpr int OST = 4;                      // operand ring
 constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + 1024;
 constexpr int NA = 4;                       // TMEM A-operand buffers [X_hi | X_lo] (64 cols)
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
@@ -56,18 +67,35 @@ constexpr int TM_COLS = 512;
 constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
 
 // experiment switches (MMK_TC_DBG, timing studies only; results are wrong
-// when set): 1 skip the lo MMAs, 2 skip the tf32 split, 4 skip all MMAs
+// when set): 1 skip the lo MMAs, 2 skip the split, 4 skip all MMAs
 __constant__ int c_dbg = 0;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// 3xTF32 split of an X value: hi = x with its 13 low mantissa bits cleared
-// (what the tensor core reads of a tf32 operand), lo = x - hi exactly.
-__device__ __forceinline__ void tf32_hilo(float x, float& hi, float& lo) {
-    hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
-    lo = x - hi;
+// power-of-two exponent e with max * 2^e in [2^14, 2^15) (0 for max == 0)
+__host__ __device__ inline int scale_exp(float mx) {
+    if (!(mx > 0.f)) return 0;
+    int E;
+    frexpf(mx, &E);   // mx = f 2^E, f in [0.5, 1)
+    int e = 15 - E;
+    return e < -120 ? -120 : (e > 120 ? 120 : e);
+}
+
+// fp16 hi / lo of an already-scaled value, packed pairwise (even K in the
+// low half of the 32-bit word)
+__device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// kind::f16 instruction descriptor: fp16 A/B (K-major), fp32 D
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 struct Bars {
@@ -93,28 +121,24 @@ __device__ __forceinline__ void init_bars(Bars& B) {
     tc::fence_barrier_init();
 }
 
-// One stage of 3xTF32, both MMAs with A from TMEM (buffer a = [X_hi | X_lo],
-// 32 + 32 columns, written by the split warps) so the tensor core reads only
-// the B operand from shared memory.  The operand chunk holds [B_hi ; B_lo]
-// stacked along N (64 + 64 rows): per K-step a TS MMA with N = 128 gives
-// D[:, 0:64] += X_hi.B_hi and D[:, 64:128] += X_hi.B_lo, and a TS MMA with
-// N = 64 adds X_lo.B_hi into D[:, 0:64].  The epilogue sums the two halves:
-// X_hi B_hi + X_hi B_lo + X_lo B_hi.
-template <bool MN>
+// One stage (K = 64) of the split product, both MMAs with A from TMEM
+// (buffer a = [X_hi | X_lo], 32 + 32 columns of fp16 pairs).  The operand
+// chunk holds [B_hi ; B_lo] stacked along N (64 + 64 rows, K-major fp16): per
+// K16 step a TS MMA with N = 128 gives D[:, 0:64] += X_hi.B_hi and
+// D[:, 64:128] += X_hi.B_lo, and a TS MMA with N = 64 adds X_lo.B_hi into
+// D[:, 0:64].  The epilogue sums the two halves.
 __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bhl,
                                             bool first) {
-    constexpr uint32_t id_lo = tc::idesc_tf32(BM, R, 0, MN ? 1 : 0);
-    constexpr uint32_t id_hi = tc::idesc_tf32(BM, ACC, 0, MN ? 1 : 0);
-    // descriptors advance by their 16-byte start-address field only
-    const uint64_t db0 = MN ? tc::sdesc_sw128_32b(bhl, 4096, 512) : tc::sdesc_sw128(bhl, 16, 1024);
-    constexpr uint64_t step = MN ? (1024 >> 4) : (32 >> 4);
+    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
+    constexpr uint32_t id_lo = idesc_f16(BM, R);
+    const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const int dbg = c_dbg;
     if (dbg & 4) return;
 #pragma unroll
-    for (int ks = 0; ks < BK / 8; ++ks) {
+    for (int ks = 0; ks < BK / 16; ++ks) {
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-        tc::mma_tf32_ts(d, a + ks * 8, db0 + ks * step, id_hi, acc);
-        if (!(dbg & 1)) tc::mma_tf32_ts(d, a + 32 + ks * 8, db0 + ks * step, id_lo, 1);
+        tc::mma_f16ts(d, a + ks * 8, db0 + ks * 2, id_hi, acc);
+        if (!(dbg & 1)) tc::mma_f16ts(d, a + 32 + ks * 8, db0 + ks * 2, id_lo, 1);
     }
 }
 
@@ -125,36 +149,47 @@ struct Pass {
     int nacc, nkb;
 };
 
-// An X stage from shared memory into registers: V step (MN = false) reads
-// row `lane` of the 128B-swizzled K-major tile; W step (MN = true) reads
-// column `lane` of box `quarter` of the 32-byte-atom swizzled MN-major tile.
+// The 64 X values of this thread's lane in an X stage, scaled by 2^e:
+// V step (MN = false): row `quarter*32 + lane` of two 128B-swizzled K-major
+// boxes [128 rows x 32 cols]; W step (MN = true): column `lane` of box
+// `quarter` [64 rows x 32 cols] (all 64 rows).
 template <bool MN>
-__device__ __forceinline__ void read_stage(const uint8_t* xs, int quarter, int lane, float* x) {
+__device__ __forceinline__ void read_stage(const uint8_t* xs, int quarter, int lane, float sc,
+                                           float* x) {
     if (!MN) {
         const int row = quarter * 32 + lane;
-        const float4* rp = reinterpret_cast<const float4*>(xs + row * 128);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const float4 t = rp[c ^ (row & 7)];
-            x[4 * c] = t.x;
-            x[4 * c + 1] = t.y;
-            x[4 * c + 2] = t.z;
-            x[4 * c + 3] = t.w;
+        for (int h = 0; h < 2; ++h) {
+            const float4* rp = reinterpret_cast<const float4*>(xs + h * (BM * 128) + row * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float4 t = rp[c ^ (row & 7)];
+                x[32 * h + 4 * c] = t.x * sc;
+                x[32 * h + 4 * c + 1] = t.y * sc;
+                x[32 * h + 4 * c + 2] = t.z * sc;
+                x[32 * h + 4 * c + 3] = t.w * sc;
+            }
         }
     } else {
-        const uint8_t* bx = xs + quarter * 4096 + (lane & 7) * 4;
+        const uint8_t* bx = xs + quarter * (BK * 128) + (lane & 3) * 4;
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-            x[k] = *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
+        for (int k = 0; k < BK; ++k)
+            x[k] = *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 2) ^ (k & 7)) << 4)) *
+                   sc;
     }
 }
 
-// tf32 hi / lo of the 32 values into TMEM columns [a, a + 32) / [a + 32, a + 64)
-__device__ __forceinline__ void store_hilo(float* x, uint32_t a_addr) {
-    float lo[32];
+// fp16 hi / lo pairs of the 64 values into TMEM columns [a, a+32) / [a+32, a+64)
+__device__ __forceinline__ void store_hilo(const float* x, uint32_t a_addr) {
+    float hi[32], lo[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) tf32_hilo(x[k], x[k], lo[k]);
-    tc::tmem_st32(a_addr, x);
+    for (int w = 0; w < 32; ++w) {
+        uint32_t h, l;
+        split_pair(x[2 * w], x[2 * w + 1], h, l);
+        hi[w] = __uint_as_float(h);
+        lo[w] = __uint_as_float(l);
+    }
+    tc::tmem_st32(a_addr, hi);
     tc::tmem_st32(a_addr + 32, lo);
 }
 
@@ -171,9 +206,9 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int x
 
 template <bool MN, class PassOf, class LoadX, class LoadOp, class Epi>
 __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tmem, int npass,
-                                             const PassOf& pass_of, const LoadX& load_x,
-                                             const LoadOp& load_op, const Epi& epilogue,
-                                             unsigned long long* tr) {
+                                             float xscale, const PassOf& pass_of,
+                                             const LoadX& load_x, const LoadOp& load_op,
+                                             const Epi& epilogue, unsigned long long* tr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* xring = base;
     uint8_t* oring = base + XST * SX;
@@ -213,7 +248,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                         tc::mbar_wait(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
-                        issue_stage<MN>(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
+                        issue_stage(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
                         tc::mma_commit(&B.aempty[ab]);   // A buffer ab free once these finish
                         trace_at(tr, 4, xit);
                     }
@@ -234,8 +269,8 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     const int xs = xit % XST, ab = xit % NA;
                     tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
                     if (quarter == 0 && lane == 0) trace_at(tr, 1, xit);
-                    float x[32];
-                    read_stage<MN>(xring + xs * SX, quarter, lane, x);
+                    float x[BK];
+                    read_stage<MN>(xring + xs * SX, quarter, lane, xscale, x);
                     // the values are in registers (consumed below): release the slot
                     tc::mbar_arrive(&B.xempty[xs]);
                     // A buffer ab was last read by the MMAs of stage xit - NA
@@ -264,18 +299,25 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
     }
 }
 
+// Scales shared by the kernels of one iteration (device, in the workspace):
+// exponents of X (cached with sum x^2), W and V'; maxima as float bits.
+struct Scales {
+    int ex, ew, ev, pad_;
+    unsigned int wmax_bits, vmax_bits, pad2_, pad3_;
+};
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
-              const float* __restrict__ DEN, float* __restrict__ Vout, float* __restrict__ Vhi,
-              float* __restrict__ Vlo, int m, int n, double* __restrict__ part,
-              unsigned long long* tr) {
+              const float* __restrict__ DEN, float* __restrict__ Vout, Scales* sc, int m, int n,
+              double* __restrict__ part, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     __shared__ Bars B;
     __shared__ uint32_t tmem_base;
     __shared__ double red[kThreads / 32];
+    __shared__ float vmx[kThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
     const int mine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -291,7 +333,10 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
+    const float xscale = exp2f((float)sc->ex);
+    const double qscale = exp2(-(double)(sc->ex + sc->ew));
     double acc = 0.0;
+    float vmax = 0.f;
     auto tile_of = [&](int p, int j) { return (int)blockIdx.x + (p * TMAX + j) * (int)gridDim.x; };
     auto pass_of = [&](int p) {
         const int left = mine - p * TMAX;
@@ -303,6 +348,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     };
     auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
         tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
+        tc::tma_load_2d(dst + BM * 128, &mX, bar, kb * BK + 32, tile_of(p, j) * BM);
     };
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool) {
         const long long row = (long long)tile_of(p, j) * BM + quarter * 32 + ln;
@@ -311,57 +357,62 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             float q[32], q2[32];
             tc::tmem_ld32(ta + h * 32, q);
             tc::tmem_ld32(ta + R + h * 32, q2);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) q[i] += q2[i];
             if (row >= m) continue;
             const float4* v4 = reinterpret_cast<const float4*>(V + row * R + h * 32);
             const float4* d4 = reinterpret_cast<const float4*>(DEN + row * R + h * 32);
             float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
-            float4* oh = reinterpret_cast<float4*>(Vhi + row * R + h * 32);
-            float4* ol = reinterpret_cast<float4*>(Vlo + row * R + h * 32);
 #pragma unroll
             for (int k4 = 0; k4 < 8; ++k4) {
                 const float4 vv = v4[k4], dd = d4[k4];
                 const float va[4] = {vv.x, vv.y, vv.z, vv.w};
                 const float da[4] = {dd.x, dd.y, dd.z, dd.w};
-                float nv[4], hh[4], ll[4];
+                float nv[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const double vk = (double)va[i];
-                    const double qk = (double)q[4 * k4 + i];
+                    const double qk = ((double)q[4 * k4 + i] + (double)q2[4 * k4 + i]) * qscale;
                     acc = fma(vk, qk, acc);
                     nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
-                    tc::split_tf32(nv[i], hh[i], ll[i]);
+                    vmax = fmaxf(vmax, nv[i]);
                 }
                 o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
-                oh[k4] = make_float4(hh[0], hh[1], hh[2], hh[3]);
-                ol[k4] = make_float4(ll[0], ll[1], ll[2], ll[3]);
             }
         }
     };
-    run_pipeline<false>(base, B, tmem, npass, pass_of, load_x, load_op, epilogue, tr);
-    // per-CTA partial <V, Q> (epilogue warps)
+    run_pipeline<false>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue, tr);
+    // per-CTA partial <V, Q> and max(V') (epilogue warps)
     acc = warp_sum(acc);
-    if (lane == 0) red[warp] = acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if (lane == 0) {
+        red[warp] = acc;
+        vmx[warp] = vmax;
+    }
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
         double c = 0.0;
-        for (int w = 2 + NCONV; w < kThreads / 32; ++w) c += red[w];
+        float mx = 0.f;
+        for (int w = 2 + NCONV; w < kThreads / 32; ++w) {
+            c += red[w];
+            mx = fmaxf(mx, vmx[w]);
+        }
         part[blockIdx.x] = c;
+        atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
     }
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------
 // P^T partials: item (row split s, column super-block cs of CB x 128 columns)
-// D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; V' chunks are shared
-// by the CB column blocks of an item.  X tiles arrive MN-major (4 boxes of
-// 32 rows x 32 columns, 32-byte-atom swizzle) and serve as the hi operand.
+// D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; V'^T chunks (fp16
+// hi / lo, K-major along rows) are shared by the CB column blocks of an item.
+// X tiles arrive as 4 boxes of [64 rows x 32 columns] (128B swizzle); split
+// thread `lane` of warp quarter q owns column 32 q + lane of the block.
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mVh,
-              const __grid_constant__ CUtensorMap mVl, int m, int n, int splits,
-              int rows_per_split, float* __restrict__ wpart, unsigned long long* tr) {
+              const __grid_constant__ CUtensorMap mVl, const Scales* sc, int m, int n,
+              int splits, int rows_per_split, float* __restrict__ wpart, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     __shared__ Bars B;
@@ -382,6 +433,7 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
+    const float xscale = exp2f((float)sc->ex);
     auto item_of = [&](int p) { return (int)blockIdx.x + p * (int)gridDim.x; };
     auto pass_of = [&](int p) {
         const int item = item_of(p), s = item / ncs, cs = item % ncs;
@@ -393,18 +445,16 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     };
     auto load_op = [&](int p, int kb, uint8_t* dst, uint64_t* bar) {
         const int row = (item_of(p) / ncs) * rows_per_split + kb * BK;
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            tc::tma_load_2d(dst + jj * 4096, &mVh, bar, 32 * jj, row);
-            tc::tma_load_2d(dst + SOP + jj * 4096, &mVl, bar, 32 * jj, row);
-        }
+        tc::tma_load_2d(dst, &mVh, bar, row, 0);
+        tc::tma_load_2d(dst + SOP, &mVl, bar, row, 0);
     };
     auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
         const int item = item_of(p);
         const int row = (item / ncs) * rows_per_split + kb * BK;
         const int col0 = ((item % ncs) * CB + j) * BM;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) tc::tma_load_2d(dst + jj * 4096, &mX, bar, col0 + 32 * jj, row);
+        for (int jj = 0; jj < 4; ++jj)
+            tc::tma_load_2d(dst + jj * (BK * 128), &mX, bar, col0 + 32 * jj, row);
     };
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool any) {
         const int item = item_of(p), s = item / ncs;
@@ -418,7 +468,7 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::tmem_ld32(ta + h * 32, v);
                 tc::tmem_ld32(ta + R + h * 32, v2);
 #pragma unroll
-                for (int k = 0; k < 32; ++k) v[k] += v2[k];
+                for (int k = 0; k < 32; ++k) v[k] += v2[k];   // scaled units (see wreduce)
             } else {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) v[k] = 0.f;
@@ -430,40 +480,61 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     };
-    run_pipeline<true>(base, B, tmem, npass, pass_of, load_x, load_op, epilogue, tr);
+    run_pipeline<true>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue, tr);
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
-// sum of x^2 over X, cached in the workspace and keyed by (X, m, n, ldx):
-// X is constant over a run, so after the first call this is a no-op launch.
+// sum of x^2 and max(x) over X, cached in the workspace and keyed by
+// (X, m, n, ldx): X is constant over a run, so after the first call this is
+// a no-op launch.  The X scale exponent goes to sc->ex.
 struct XXCache {
     double xx;
     unsigned long long key[4];
+    int ex, pad_;
 };
 
 __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
-                             XXCache* cache, double* __restrict__ part, unsigned int* counter) {
+                             XXCache* cache, double* __restrict__ part, float* __restrict__ mpart,
+                             unsigned int* counter, Scales* sc) {
     const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
     if (cache->key[0] == k0 && cache->key[1] == (unsigned long long)m &&
-        cache->key[2] == (unsigned long long)n && cache->key[3] == (unsigned long long)ldx)
+        cache->key[2] == (unsigned long long)n && cache->key[3] == (unsigned long long)ldx) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) sc->ex = cache->ex;
         return;   // uniform across the grid: every block exits, the counter is untouched
-    __shared__ double sc[32];
+    }
+    __shared__ double sd[32];
+    __shared__ float sf[32];
     double s = 0.0;
+    float mx = 0.f;
     for (long long i = blockIdx.x; i < m; i += gridDim.x) {
         const float* row = X + i * ldx;
         for (long long j = threadIdx.x; j < n; j += blockDim.x) {
-            const double v = row[j];
+            const float x = row[j];
+            const double v = x;
             s = fma(v, v, s);
+            mx = fmaxf(mx, fabsf(x));
         }
     }
-    s = block_sum(s, sc);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    s = block_sum(s, sd);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, sf[w]);
+        part[blockIdx.x] = s;
+        mpart[blockIdx.x] = mx;
+    }
     if (arrive_last(counter, gridDim.x)) {
-        const double tot = block_sum_array(part, gridDim.x, sc);
+        const double tot = block_sum_array(part, gridDim.x, sd);
         if (threadIdx.x == 0) {
+            float g = 0.f;
+            for (unsigned int b = 0; b < gridDim.x; ++b) g = fmaxf(g, mpart[b]);
             cache->xx = tot;
+            cache->ex = scale_exp(g);
+            sc->ex = cache->ex;
             cache->key[1] = (unsigned long long)m;
             cache->key[2] = (unsigned long long)n;
             cache->key[3] = (unsigned long long)ldx;
@@ -608,14 +679,80 @@ gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-__global__ void split_w_kernel(const float* __restrict__ W, float* __restrict__ Wh,
-                               float* __restrict__ Wl, long long len) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// max |W| -> sc->ew (last block), and reset the V' maximum for this iteration
+__global__ void __launch_bounds__(256)
+wmax_kernel(const float* __restrict__ W, long long len, float* __restrict__ mpart,
+            unsigned int* counter, Scales* sc) {
+    __shared__ float sf[8];
+    float mx = 0.f;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < len;
+         t += (long long)gridDim.x * blockDim.x)
+        mx = fmaxf(mx, fabsf(W[t]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < 8; ++w) mx = fmaxf(mx, sf[w]);
+        mpart[blockIdx.x] = mx;
+    }
+    if (arrive_last(counter, gridDim.x) && threadIdx.x == 0) {
+        float g = 0.f;
+        for (unsigned int b = 0; b < gridDim.x; ++b) g = fmaxf(g, mpart[b]);
+        sc->ew = scale_exp(g);
+        sc->wmax_bits = __float_as_uint(g);
+        sc->vmax_bits = 0u;
+    }
+}
+
+// W (64 x n fp32) -> W_hi / W_lo (64 x n fp16), scaled by 2^ew
+__global__ void split_w_kernel(const float* __restrict__ W, __half* __restrict__ Wh,
+                               __half* __restrict__ Wl, long long len, const Scales* sc) {
+    const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
     if (t >= len) return;
-    float h, l;
-    tc::split_tf32(W[t], h, l);
-    Wh[t] = h;
-    Wl[t] = l;
+    const float s = exp2f((float)sc->ew);
+    uint32_t h, l;
+    split_pair(W[t] * s, (t + 1 < len ? W[t + 1] : 0.f) * s, h, l);
+    if (t + 1 < len) {
+        *reinterpret_cast<uint32_t*>(Wh + t) = h;
+        *reinterpret_cast<uint32_t*>(Wl + t) = l;
+    } else {
+        Wh[t] = __ushort_as_half((unsigned short)(h & 0xffffu));
+        Wl[t] = __ushort_as_half((unsigned short)(l & 0xffffu));
+    }
+}
+
+// V' (m x 64 fp32) -> V'^T hi / lo (64 x m fp16), scaled by 2^ev where ev
+// comes from max(V') of the V step; a block transposes 64 rows through smem
+__global__ void __launch_bounds__(256)
+vprep_kernel(const float* __restrict__ V, __half* __restrict__ Vth, __half* __restrict__ Vtl,
+             long long m, Scales* sc) {
+    __shared__ float T[R][64 + 1];
+    const long long r0 = (long long)blockIdx.x * 64;
+    const int ev = scale_exp(__uint_as_float(sc->vmax_bits));
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->ev = ev;
+    const float s = exp2f((float)ev);
+    for (int i = threadIdx.x; i < 64 * R; i += 256) {
+        const int rr = i / R, k = i % R;
+        T[k][rr] = (r0 + rr < m) ? V[(r0 + rr) * R + k] * s : 0.f;
+    }
+    __syncthreads();
+    // thread: rank k = tid / 4, 16 consecutive rows (8 pairs)
+    const int k = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 16;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const long long row = r0 + c0 + 2 * q;
+        if (row >= m) break;
+        uint32_t h, l;
+        split_pair(T[k][c0 + 2 * q], T[k][c0 + 2 * q + 1], h, l);
+        if (row + 1 < m) {
+            *reinterpret_cast<uint32_t*>(Vth + (long long)k * m + row) = h;
+            *reinterpret_cast<uint32_t*>(Vtl + (long long)k * m + row) = l;
+        } else {
+            Vth[(long long)k * m + row] = __ushort_as_half((unsigned short)(h & 0xffffu));
+            Vtl[(long long)k * m + row] = __ushort_as_half((unsigned short)(l & 0xffffu));
+        }
+    }
 }
 
 // red[k n + j] = sum_s wpart[s][j][k] (fixed split order); a block owns 32
@@ -623,8 +760,10 @@ __global__ void split_w_kernel(const float* __restrict__ W, float* __restrict__ 
 // sums, transposed through shared memory for coalesced writes
 __global__ void __launch_bounds__(256)
 wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
-                  double* __restrict__ red) {
+                  double* __restrict__ red, const Scales* sc) {
     __shared__ double T[R][32 + 1];
+    // partials are in the scaled units of the split products: X 2^ex, V' 2^ev
+    const double pscale = exp2(-(double)(sc->ex + sc->ev));
     const long long j0 = (long long)blockIdx.x * 32;
     double acc[8];
 #pragma unroll
@@ -641,7 +780,7 @@ wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int e = q * 256 + threadIdx.x;
-        T[e % R][e / R] = acc[q];
+        T[e % R][e / R] = acc[q] * pscale;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < R * 32; e += 256) {
@@ -717,10 +856,12 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
 }
 
 struct TcWs {
-    float *Wh, *Wl, *Vhi, *Vlo, *wpart, *DEN;
+    __half *Wh, *Wl, *Vth, *Vtl;
+    float *wpart, *DEN, *mpart;
     double *GVn, *part, *sqpart, *gpart;
     XXCache* xx;
-    unsigned int* counter;
+    Scales* sc;
+    unsigned int* counter;   // [0] sumsq, [1] wmax
 };
 
 inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
@@ -733,24 +874,27 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    size_t oWh = take(4 * (size_t)R * n), oWl = take(4 * (size_t)R * n);
-    size_t oVh = take(4 * (size_t)R * m), oVl = take(4 * (size_t)R * m);
+    size_t oWh = take(2 * (size_t)R * n), oWl = take(2 * (size_t)R * n);
+    size_t oVh = take(2 * (size_t)R * m), oVl = take(2 * (size_t)R * m);
     size_t oD = take(4 * (size_t)R * m);
     size_t oWp = take(4 * (size_t)P.splits * n * R);
     size_t oG = take(8 * (size_t)R * R);
     size_t oP = take(16 * (size_t)kNumSMs);
     size_t oS = take(8 * (size_t)kNumSMs * 4);
-    size_t oC = take(sizeof(XXCache) + 64);
+    size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) sumsq, then wmax
+    size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
     if (base && L) {
-        L->sqpart = (double*)(c_base(base) + oS);
-        L->xx = (XXCache*)(c_base(base) + oC);
-        L->counter = (unsigned int*)(c_base(base) + oC + sizeof(XXCache));
-        char* c = reinterpret_cast<char*>(base);
-        L->Wh = (float*)(c + oWh);
-        L->Wl = (float*)(c + oWl);
-        L->Vhi = (float*)(c + oVh);
-        L->Vlo = (float*)(c + oVl);
+        char* c = c_base(base);
+        L->sqpart = (double*)(c + oS);
+        L->mpart = (float*)(c + oM);
+        L->xx = (XXCache*)(c + oC);
+        L->sc = (Scales*)(c + oC + sizeof(XXCache));
+        L->counter = (unsigned int*)(c + oC + sizeof(XXCache) + sizeof(Scales));
+        L->Wh = (__half*)(c + oWh);
+        L->Wl = (__half*)(c + oWl);
+        L->Vth = (__half*)(c + oVh);
+        L->Vtl = (__half*)(c + oVl);
         L->DEN = (float*)(c + oD);
         L->wpart = (float*)(c + oWp);
         L->GVn = (double*)(c + oG);
@@ -770,7 +914,8 @@ namespace mmk_tc {
 
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X) {
     if (dtype != MMK_F32 || r != R) return false;
-    if ((n & 3) || (ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
+    // 16-byte TMA row strides: fp32 X (ldx % 4), fp16 W^ (n % 8) and V'^T (m % 8)
+    if ((n & 7) || (m & 7) || (ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
     if (m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
     const char* env = getenv("MMK_NNMF_TC");
@@ -780,11 +925,13 @@ bool eligible(int dtype, long long m, long long n, long long r, long long ldx, c
 
 size_t ws_bytes(long long m, long long n) { return tc_layout(m, n, nullptr, nullptr); }
 
-// Phase A of one iteration on the tensor cores.  `gram` callbacks run the
-// CUDA-core fp64 Gram kernels of nnmf.cu.  Writes V_out and red = [P | G_V | f].
+// Phase A of one iteration on the tensor cores; writes V_out and
+// red = [P | G_V' | f-partial].
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
            long long m, long long n, void* tcws, double* GW, double* red,
            const GramFn& gram_w, const GramFn& gram_v_into, cudaStream_t st) {
+    (void)gram_w;
+    (void)gram_v_into;
     TcWs L;
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);
@@ -802,39 +949,44 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     CUtensorMap mX, mWh, mWl, mXt, mVh, mVl;
     int rc;
     if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mWh, L.Wh, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mWl, L.Wl, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK, 32))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mVh, L.Vhi, m, R, R, BK, 32))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mVl, L.Vlo, m, R, R, BK, 32))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, R, n, n, R))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, R, n, n, R))) return rc;
+    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, R, m, m, R))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, R, m, m, R))) return rc;
     const long long rn = (long long)R * n;
+    MMK_LAUNCH("nnmf_sumsq_cached", st,
+               (sumsq_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
+                                                           L.counter, L.sc)));
+    MMK_LAUNCH("nnmf_wmax", st,
+               (wmax_kernel<<<kNumSMs, 256, 0, st>>>(W, rn, L.mpart + 4 * kNumSMs,
+                                                     L.counter + 1, L.sc)));
     MMK_LAUNCH("nnmf_split_w", st,
-               (split_w_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn)));
-    (void)gram_w;
-    (void)gram_v_into;
+               (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
+                                                                            L.sc)));
     gram32(W, n, true, L.gpart, GW, st);
     gram32(V, m, false, L.gpart, L.GVn, st);
-    MMK_LAUNCH("nnmf_sumsq_cached", st,
-               (sumsq_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart,
-                                                           L.counter)));
-    MMK_LAUNCH("nnmf_vgw", st,
-               (vgw_kernel<<<ceil_div(m, 64), 256, VGW_SMEM, st>>>(V, GW, L.DEN, m)));
+    MMK_LAUNCH("nnmf_vgw",
+               st, (vgw_kernel<<<ceil_div(m, 64), 256, VGW_SMEM, st>>>(V, GW, L.DEN, m)));
     MMK_LAUNCH("nnmf_vstep_tc", st,
-               (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, L.DEN, V_out, L.Vhi,
-                                                                L.Vlo, (int)m, (int)n, L.part,
+               (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, L.DEN, V_out, L.sc,
+                                                                (int)m, (int)n, L.part,
                                                                 g_trace_v)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx, L.GVn, GW,
                                                         red + rn + (long long)R * R)));
     gram32(V_out, m, false, L.gpart, red + rn, st);
+    MMK_LAUNCH("nnmf_vprep", st,
+               (vprep_kernel<<<ceil_div(m, 64), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
     MMK_LAUNCH("nnmf_wstep_tc", st,
-               (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, (int)m, (int)n,
+               (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, L.sc, (int)m, (int)n,
                                                                 P.splits, P.rows_per_split,
                                                                 L.wpart, g_trace_w)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
-               (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red)));
+               (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
+                                                                    L.sc)));
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a");
     return MMK_OK;
 }

@@ -1,6 +1,8 @@
-"""Tensor-core (tcgen05 3xTF32) NNMF path vs the fp64 CUDA-core path on the
-same inputs: one iteration (V', W', objective) and a 30-iteration run, on
-tile-aligned and ragged shapes (TMA out-of-bounds fill on both edges)."""
+"""Tensor-core (tcgen05 kind::f16, scaled fp16 hi/lo split products) NNMF
+path vs fp64 on the same inputs: one iteration (V', W', objective) and a
+30-iteration run, on tile-aligned and ragged shapes (TMA out-of-bounds fill
+on both edges), with inputs far from unit scale and with a wide per-row
+dynamic range (the power-of-two scaling of csrc/nnmf_tc.cu)."""
 
 import os
 
@@ -48,13 +50,28 @@ def reference_iter(x, v, w):
     return v2, w2, f
 
 
-@pytest.mark.parametrize("m,n", [(1024, 512), (1000, 1000), (4100, 388)])
-def test_tc_iteration_matches_fp64(m, n):
+def tc_launched(fn):
+    """Run fn with the launch profiler on; True if the tcgen05 kernels ran."""
+    lib = _lib.load()
+    lib.mmk_prof_enable(1)
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+    finally:
+        lib.mmk_prof_enable(0)
+    prof = _lib.prof_report()
+    return out, "nnmf_vstep_tc" in prof and "nnmf_wstep_tc" in prof
+
+
+@pytest.mark.parametrize("m,n,scale", [(1024, 512, 1.0), (1000, 1000, 1.0), (4104, 392, 1.0),
+                                       (1024, 512, 1e-6), (1024, 512, 3e6)])
+def test_tc_iteration_matches_fp64(m, n, scale):
     g = torch.Generator(device="cuda").manual_seed(m + n)
-    x = torch.rand(m, n, device="cuda", generator=g)
+    x = torch.rand(m, n, device="cuda", generator=g) * scale
     v = torch.rand(m, 64, device="cuda", generator=g)
     w = torch.rand(64, n, device="cuda", generator=g)
-    vt, wt, ft = one_iter(x, v, w, force_simt=False)
+    (vt, wt, ft), used = tc_launched(lambda: one_iter(x, v, w, force_simt=False))
+    assert used, "tensor-core path did not run"
     vr, wr, fr = reference_iter(x, v, w)
     rel = lambda a, b: float((a.double() - b).norm() / b.norm())  # noqa: E731
     assert abs(ft - fr) / fr < 2e-6, (ft, fr)
@@ -87,3 +104,22 @@ def test_tc_deterministic():
     a = one_iter(x, v, w, False)
     b = one_iter(x, v, w, False)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and a[2] == b[2]
+
+
+def test_tc_wide_row_dynamic_range():
+    """Rows of X scaled by 2^u, u uniform in [-12, 12], and W entries spread
+    over 2^[-6, 6]: one scaled split per operand still gives fp32-level
+    agreement."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, n = 2048, 768
+    rs = torch.exp2(torch.randint(-12, 13, (m, 1), device="cuda", generator=g).float())
+    x = torch.rand(m, n, device="cuda", generator=g) * rs
+    v = torch.rand(m, 64, device="cuda", generator=g) / rs.sqrt()
+    w = torch.rand(64, n, device="cuda", generator=g) * torch.exp2(
+        torch.randint(-6, 7, (64, n), device="cuda", generator=g).float())
+    (vt, wt, ft), used = tc_launched(lambda: one_iter(x, v, w, force_simt=False))
+    assert used
+    vr, wr, fr = reference_iter(x, v, w)
+    rel = lambda a, b: float((a.double() - b).norm() / b.norm())  # noqa: E731
+    assert abs(ft - fr) / fr < 1e-5, (ft, fr)
+    assert rel(vt, vr) < 5e-5 and rel(wt, wr) < 5e-5, (rel(vt, vr), rel(wt, wr))
