@@ -723,34 +723,43 @@ __global__ void split_w_kernel(const float* __restrict__ W, __half* __restrict__
 }
 
 // V' (m x 64 fp32) -> V'^T hi / lo (64 x m fp16), scaled by 2^ev where ev
-// comes from max(V') of the V step; a block transposes 64 rows through smem
+// comes from max(V') of the V step; a block transposes 128 rows through
+// shared memory and writes 16-byte chunks (8 rows) of both outputs
 __global__ void __launch_bounds__(256)
 vprep_kernel(const float* __restrict__ V, __half* __restrict__ Vth, __half* __restrict__ Vtl,
              long long m, Scales* sc) {
-    __shared__ float T[R][64 + 1];
-    const long long r0 = (long long)blockIdx.x * 64;
+    __shared__ float T[R][128 + 4];
+    const long long r0 = (long long)blockIdx.x * 128;
     const int ev = scale_exp(__uint_as_float(sc->vmax_bits));
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->ev = ev;
     const float s = exp2f((float)ev);
-    for (int i = threadIdx.x; i < 64 * R; i += 256) {
-        const int rr = i / R, k = i % R;
-        T[k][rr] = (r0 + rr < m) ? V[(r0 + rr) * R + k] * s : 0.f;
+    for (int i = threadIdx.x; i < 128 * (R / 4); i += 256) {
+        const int rr = i / (R / 4), k4 = (i % (R / 4)) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + k4);
+        T[k4][rr] = v.x * s;
+        T[k4 + 1][rr] = v.y * s;
+        T[k4 + 2][rr] = v.z * s;
+        T[k4 + 3][rr] = v.w * s;
     }
     __syncthreads();
-    // thread: rank k = tid / 4, 16 consecutive rows (8 pairs)
-    const int k = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 16;
+    // chunk c of rank k: rows r0 + 8c .. r0 + 8c + 7 (16 bytes of fp16)
+    for (int e = threadIdx.x; e < R * 16; e += 256) {
+        const int k = e / 16, c = e % 16;
+        const long long row = r0 + 8 * c;
+        if (row >= m) continue;
+        uint32_t h[4], l[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const long long row = r0 + c0 + 2 * q;
-        if (row >= m) break;
-        uint32_t h, l;
-        split_pair(T[k][c0 + 2 * q], T[k][c0 + 2 * q + 1], h, l);
-        if (row + 1 < m) {
-            *reinterpret_cast<uint32_t*>(Vth + (long long)k * m + row) = h;
-            *reinterpret_cast<uint32_t*>(Vtl + (long long)k * m + row) = l;
+        for (int q = 0; q < 4; ++q) split_pair(T[k][8 * c + 2 * q], T[k][8 * c + 2 * q + 1], h[q], l[q]);
+        if (row + 8 <= m) {
+            *reinterpret_cast<uint4*>(Vth + (long long)k * m + row) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(Vtl + (long long)k * m + row) = make_uint4(l[0], l[1], l[2], l[3]);
         } else {
-            Vth[(long long)k * m + row] = __ushort_as_half((unsigned short)(h & 0xffffu));
-            Vtl[(long long)k * m + row] = __ushort_as_half((unsigned short)(l & 0xffffu));
+            for (int q = 0; q < 8 && row + q < m; ++q) {
+                const uint32_t hw = h[q / 2] >> (16 * (q & 1)), lw = l[q / 2] >> (16 * (q & 1));
+                Vth[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(hw & 0xffffu));
+                Vtl[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(lw & 0xffffu));
+            }
         }
     }
 }
@@ -813,20 +822,22 @@ TcPlan tc_plan(long long m, long long n) {
     P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
     const int ncb = (int)((n + BM - 1) / BM);
     const int ncs = (ncb + CB - 1) / CB;
-    // smallest split count whose item count fills whole waves of SMs
-    // (ncs * S a multiple of 148 when possible), rows per split >= 4 K-blocks
+    // split count minimising (wave quantisation loss) + (split-K partial
+    // traffic: S fp32 partials of n x 64 written and read back, relative to
+    // one pass over X); rows per split >= 4 K-blocks
     const int max_splits = (int)((m + 4 * BK - 1) / (4 * BK));
     int best = 1;
-    double best_eff = 0.0;
+    double best_cost = 1e300;
     for (int S = 1; S <= max_splits && S <= 4 * kNumSMs; ++S) {
         const int items = ncs * S;
         const int waves = (items + kNumSMs - 1) / kNumSMs;
         const double eff = (double)items / ((double)waves * kNumSMs);
-        if (eff > best_eff + 1e-9) {
-            best_eff = eff;
+        const double partial = 2.0 * S * (double)n * R * 4.0 / ((double)m * n * 4.0);
+        const double cost = 1.0 / eff + partial;
+        if (cost < best_cost - 1e-12) {
+            best_cost = cost;
             best = S;
         }
-        if (eff > 0.999) break;
     }
     long long rps = (m + best - 1) / best;
     rps = (rps + BK - 1) / BK * BK;
@@ -978,7 +989,7 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                                                         red + rn + (long long)R * R)));
     gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
-               (vprep_kernel<<<ceil_div(m, 64), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
+               (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
     MMK_LAUNCH("nnmf_wstep_tc", st,
                (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, L.sc, (int)m, (int)n,
                                                                 P.splits, P.rows_per_split,

@@ -119,3 +119,41 @@ def phase_b_model(w, red, n, r):
     p = red[:r * n].reshape(r, n)
     g = red[r * n:r * n + r * r].reshape(r, r)
     return w * (p / (g @ w + 1e-300)), red[-1]
+
+
+def tri_tiles(n, tile=128):
+    """(I, J) of every packed-triangle tile in linear order (csrc/mds_tri.cu)."""
+    t = -(-n // tile)
+    return [(i, j) for i in range(t) for j in range(i, t)]
+
+
+def tri_phase_a_model(y, theta, t0, t1, tile=128):
+    """Host fp64 model of ``mmk_mds_tri_iter_a`` for tiles [t0, t1) (tests
+    only): red = [C (n x dim, row-major) | stress partial | S if t0 == 0]."""
+    dim, n = theta.shape
+    c = np.zeros((n, dim))
+    stress = 0.0
+    for (bi, bj) in tri_tiles(n, tile)[t0:t1]:
+        i = np.arange(bi * tile, min(n, (bi + 1) * tile))
+        j = np.arange(bj * tile, min(n, (bj + 1) * tile))
+        ii, jj = np.meshgrid(i, j, indexing="ij")
+        keep = jj > ii
+        ii, jj = ii[keep], jj[keep]
+        g = theta[:, jj] - theta[:, ii]
+        d = np.sqrt((g * g).sum(0))
+        yy = y[ii, jj]
+        z = np.where(yy > 0.0, yy / np.where(d > 0.0, d, 1.0), 0.0)
+        stress += float(((yy - d) ** 2).sum())
+        np.add.at(c, ii, (z * g).T)
+        np.add.at(c, jj, -(z * g).T)
+    s = theta.sum(1) if t0 == 0 else np.zeros(dim)
+    return np.concatenate([c.ravel(), [stress], s])
+
+
+def tri_phase_b_model(theta, red):
+    """Host model of ``mmk_mds_tri_iter_b``: the unit-weight MM update."""
+    dim, n = theta.shape
+    c = red[:n * dim].reshape(n, dim).T
+    s = red[n * dim + 1:n * dim + 1 + dim]
+    w = n - 1.0
+    return (theta * (w - 1.0) + s[:, None] - c) / (2.0 * w), red[n * dim]

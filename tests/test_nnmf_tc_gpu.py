@@ -12,6 +12,7 @@ import torch
 
 import paper_1003_3272_b200 as M
 from paper_1003_3272_b200 import _lib
+from paper_1003_3272_b200 import parallel as P
 
 pytestmark = pytest.mark.gpu
 
@@ -123,3 +124,36 @@ def test_tc_wide_row_dynamic_range():
     rel = lambda a, b: float((a.double() - b).norm() / b.norm())  # noqa: E731
     assert abs(ft - fr) / fr < 1e-5, (ft, fr)
     assert rel(vt, vr) < 5e-5 and rel(wt, wr) < 5e-5, (rel(vt, vr), rel(wt, wr))
+
+
+def test_row_shards_sum_to_the_whole():
+    """The multi-GPU NNMF decomposition on one device: 3 row shards run phase
+    A on their own rows, the NCCL all-reduce is replaced by a sum of the
+    fp64 reduction buffers, phase B once; equals the unsharded iteration."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, n = 3072, 1024
+    x = torch.rand(m, n, device="cuda", generator=g)
+    v = torch.rand(m, 64, device="cuda", generator=g)
+    w = torch.rand(64, n, device="cuda", generator=g)
+    vw, ww, fw = one_iter(x, v, w, force_simt=False)
+    code, st = _lib.MMK_F32, _lib.stream_handle(torch, x.device)
+    rl = _lib.load().mmk_nnmf_reduce_len(n, 64)
+    total = torch.zeros(rl, dtype=torch.float64, device="cuda")
+    vs = torch.empty_like(v)
+    err = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for lo, hi in (P.shard_rows(m, 3, r) for r in range(3)):
+        ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_ws_bytes", code, hi - lo, n, 64),
+                         dtype=torch.uint8, device="cuda")
+        red = torch.zeros(rl, dtype=torch.float64, device="cuda")
+        _lib.call("mmk_nnmf_iter_a", code, _lib.ptr(x[lo:hi]), n, _lib.ptr(v[lo:hi]),
+                  _lib.ptr(w), _lib.ptr(vs[lo:hi]), hi - lo, n, 64, _lib.ptr(ws), ws.numel(),
+                  _lib.ptr(red), _lib.ptr(err), st)
+        total += red
+    wo = torch.empty_like(w)
+    f = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("mmk_nnmf_iter_b", code, _lib.ptr(w), _lib.ptr(wo), n, 64, _lib.ptr(total),
+              _lib.ptr(f), _lib.ptr(err), st)
+    torch.cuda.synchronize()
+    rel = lambda a, b: float((a - b).norm() / b.norm())  # noqa: E731
+    assert torch.equal(vs, vw)            # the V step is row-local: bitwise
+    assert rel(wo, ww) < 1e-6 and abs(float(f) - fw) / fw < 1e-9
