@@ -45,7 +45,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="nnmf-large", choices=sorted(WORKLOADS))
@@ -310,15 +310,17 @@ def bench_mds_large(args, torch, world, rank, dev):
     import paper_1003_3272_b200 as M
     from paper_1003_3272_b200 import _lib, datasets as D
     from paper_1003_3272_b200.mds import PackedMdsProblem, _GpuMdsTri, tile_count
-    from paper_1003_3272_b200.parallel import nccl_comm_ptr, tile_range
+    from paper_1003_3272_b200.parallel import tile_range
     W = WORKLOADS[args.workload]
     n, dim = W["n"], W["dim"]
     be = M.Backend(dtype="fp32", device=dev.index, mds_kernel="tri")
     nt = tile_count(n)
     t0, t1 = tile_range(nt, world, rank)
     prob = PackedMdsProblem.from_rows(D.distance_rows(n, seed=0), n, dim, be, tiles=(t0, t1))
-    comm = nccl_comm_ptr() if world > 1 else None
-    mm = _GpuMdsTri(prob, be, comm=comm)
+    # sharded: one all-reduce of the per-point accumulators per iteration,
+    # issued through torch.distributed (NCCL) on the compute stream
+    import torch.distributed as dist
+    mm = _GpuMdsTri(prob, be, group=dist.group.WORLD if world > 1 else None)
     g = torch.Generator(device=dev)
     g.manual_seed(2)
     th = [torch.rand(dim, n, generator=g, device=dev) * 2 - 1, None]
