@@ -314,38 +314,56 @@ __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wou
     Wout[t] = (T)((double)W[t] * (red[t] / (den + kDenomGuard)));
 }
 
-// Rank-64 W finish: a block owns 16 columns; G (64 x 64) and the W slab sit
-// in shared memory, thread (k, column group) forms 4 denominators G_k. W_j
-// in fp64 and applies W' = W * P / (den + guard).
+// Rank-64 W finish: a block owns 64 columns; G^T and the W slab (fp64) sit in
+// shared memory and each thread forms a 4 x 4 register tile of denominators
+// (G_V W)[k][j] in fp64, then W' = W * P / (den + guard).
+constexpr int kWf64Smem = 2 * 64 * 64 * 8;
 template <typename T>
 __global__ void __launch_bounds__(256)
 nnmf_wfinish64_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
                       const double* __restrict__ red, double* f_dev) {
-    __shared__ double G[64][65];
-    __shared__ double Ws[64][17];
+    extern __shared__ double wf_smem[];
+    double(*Gt)[64] = reinterpret_cast<double(*)[64]>(wf_smem);            // Gt[l][k] = G[k][l]
+    double(*Ws)[64] = reinterpret_cast<double(*)[64]>(wf_smem + 64 * 64);  // Ws[l][j]
     const long long rn = 64 * n;
     if (f_dev && blockIdx.x == 0 && threadIdx.x == 0) *f_dev = red[rn + 64 * 64];
-    const long long j0 = (long long)blockIdx.x * 16;
-    for (int i = threadIdx.x; i < 64 * 64; i += 256) G[i / 64][i % 64] = red[rn + i];
-    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-        const int l = i / 16, jj = i % 16;
-        Ws[l][jj] = (j0 + jj < n) ? (double)W[(long long)l * n + j0 + jj] : 0.0;
+    const long long j0 = (long long)blockIdx.x * 64;
+    for (int i = threadIdx.x; i < 64 * 64; i += 256) {
+        const int k = i / 64, l = i % 64;
+        Gt[l][k] = red[rn + i];
+        const int jj = i % 64, r = i / 64;
+        Ws[r][jj] = (j0 + jj < n) ? (double)W[(long long)r * n + j0 + jj] : 0.0;
     }
     __syncthreads();
-    const int k = threadIdx.x >> 2, jg = (threadIdx.x & 3) * 4;
-    double den[4] = {0.0, 0.0, 0.0, 0.0};
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
 #pragma unroll 8
     for (int l = 0; l < 64; ++l) {
-        const double g = G[k][l];
+        const double2 a01 = *reinterpret_cast<const double2*>(&Gt[l][4 * ty]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&Gt[l][4 * ty + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&Ws[l][4 * tx]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Ws[l][4 * tx + 2]);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) den[q] = fma(g, Ws[l][jg + q], den[q]);
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const long long j = j0 + jg + q;
-        if (j < n)
-            Wout[(long long)k * n + j] =
-                (T)(Ws[k][jg + q] * (red[(long long)k * n + j] / (den[q] + kDenomGuard)));
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * ty + i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long col = j0 + 4 * tx + j;
+            if (col < n)
+                Wout[(long long)k * n + col] =
+                    (T)(Ws[k][4 * tx + j] * (red[(long long)k * n + col] / (acc[i][j] + kDenomGuard)));
+        }
     }
 }
 
@@ -584,8 +602,14 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
              cudaStream_t st) {
     const long long rn = (long long)r * n;
     if (r == 64) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(nnmf_wfinish64_kernel<T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kWf64Smem);
+            attr = true;
+        }
         MMK_LAUNCH("nnmf_wfinish", st,
-                   (nnmf_wfinish64_kernel<T><<<ceil_div(n, 16), 256, 0, st>>>(
+                   (nnmf_wfinish64_kernel<T><<<ceil_div(n, 64), 256, kWf64Smem, st>>>(
                        (const T*)W, (T*)W_out, n, red, f_dev)));
         MMK_CHECK_LAUNCH("nnmf_wfinish64_kernel");
         return MMK_OK;

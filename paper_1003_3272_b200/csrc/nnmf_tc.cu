@@ -680,20 +680,24 @@ gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict_
 
 // ---------------------------------------------------------------------------
 // max |W| -> sc->ew (last block), and reset the V' maximum for this iteration
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 wmax_kernel(const float* __restrict__ W, long long len, float* __restrict__ mpart,
             unsigned int* counter, Scales* sc) {
-    __shared__ float sf[8];
+    __shared__ float sf[32];
     float mx = 0.f;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < len;
-         t += (long long)gridDim.x * blockDim.x)
-        mx = fmaxf(mx, fabsf(W[t]));
+    const long long len4 = len / 4;   // W rows are n % 8 == 0 long (eligible()): len % 4 == 0
+    const float4* W4 = reinterpret_cast<const float4*>(W);
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < len4;
+         t += (long long)gridDim.x * blockDim.x) {
+        const float4 v = W4[t];
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 0; w < 8; ++w) mx = fmaxf(mx, sf[w]);
+        for (int w = 0; w < 32; ++w) mx = fmaxf(mx, sf[w]);
         mpart[blockIdx.x] = mx;
     }
     if (arrive_last(counter, gridDim.x) && threadIdx.x == 0) {
@@ -967,10 +971,10 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, R, m, m, R))) return rc;
     const long long rn = (long long)R * n;
     MMK_LAUNCH("nnmf_sumsq_cached", st,
-               (sumsq_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
+               (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
                                                            L.counter, L.sc)));
     MMK_LAUNCH("nnmf_wmax", st,
-               (wmax_kernel<<<kNumSMs, 256, 0, st>>>(W, rn, L.mpart + 4 * kNumSMs,
+               (wmax_kernel<<<kNumSMs, 1024, 0, st>>>(W, rn, L.mpart + 4 * kNumSMs,
                                                      L.counter + 1, L.sc)));
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
