@@ -201,7 +201,7 @@ mds_tri_kernel(const float* __restrict__ Yp, long long t0, long long ntl, int T,
                const float* __restrict__ thp, long long npad, float* __restrict__ colpart,
                float* __restrict__ rowpart, int kmax, double* __restrict__ stpart, int64_t* err) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    float* red = reinterpret_cast<float*>(smem_raw + STAGES * STAGE_BYTES);   // [warp][DIM][TB]
+    float* red = reinterpret_cast<float*>(smem_raw + STAGES * STAGE_BYTES);   // 2 x [warp][DIM][TB]
     __shared__ uint64_t full[STAGES];
     __shared__ double sred[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -282,25 +282,27 @@ mds_tri_kernel(const float* __restrict__ Yp, long long t0, long long ntl, int T,
                 CJ[p][k2].x += __shfl_xor_sync(0xffffffffu, CJ[p][k2].x, 16);
                 CJ[p][k2].y += __shfl_xor_sync(0xffffffffu, CJ[p][k2].y, 16);
             }
-        __syncthreads();   // every thread is done with slot s and with red of the last tile
-        if (tid == 0 && k + STAGES < cnt) {
-            issue(k + STAGES, pI, pJ);
-            if (++pJ == T) pJ = ++pI;
-        }
+        // red is double-buffered: the readers of this buffer (tile k - 2) are
+        // behind the barrier of tile k - 1, so one barrier per tile suffices
+        float* rb = red + (k & 1) * (kWarps * kMaxTriDim * TB);
         if (lane < 16) {
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
                 for (int k2 = 0; k2 < DIM; ++k2)
-                    *reinterpret_cast<float2*>(red + (warp * DIM + k2) * TB + jcol(tx, p, 0)) =
+                    *reinterpret_cast<float2*>(rb + (warp * DIM + k2) * TB + jcol(tx, p, 0)) =
                         CJ[p][k2];
         }
-        __syncthreads();
+        __syncthreads();   // slot s consumed by every thread; rb complete
+        if (tid == 0 && k + STAGES < cnt) {
+            issue(k + STAGES, pI, pJ);
+            if (++pJ == T) pJ = ++pI;
+        }
         float* cp = colpart + (u0 + k) * (long long)(DIM * TB);
         for (int o = tid; o < DIM * TB; o += kThreads) {
             float sum = 0.f;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) sum += red[w * DIM * TB + o];
+            for (int w = 0; w < kWarps; ++w) sum += rb[w * DIM * TB + o];
             cp[o] = -sum;
         }
         if (++J == T) J = ++I;
@@ -506,7 +508,7 @@ size_t tri_layout(const TriPlan& P, int dim, void* base, TriWs* L) {
     return off;
 }
 
-constexpr uint32_t kTriSmem = STAGES * STAGE_BYTES + kWarps * kMaxTriDim * TB * 4;
+constexpr uint32_t kTriSmem = STAGES * STAGE_BYTES + 2 * kWarps * kMaxTriDim * TB * 4;
 
 int check_tri(long long n, long long dim, long long t0, long long t1) {
     const long long T = (n + TB - 1) / TB;
