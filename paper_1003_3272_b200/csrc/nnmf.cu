@@ -159,13 +159,16 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nparts, 
 }
 
 // ---------------------------------------------------------------------------
-template <typename T, int RMAX, int RPW>
+template <typename T, int RMAX, int RPW, bool WFULL>
 __global__ void __launch_bounds__(kThreads)
 nnmf_vstep_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                   const T* __restrict__ W, const double* __restrict__ GW, T* __restrict__ Vout,
                   long long m, long long n, int r, int flags, double* __restrict__ respart,
                   unsigned int* counter, double* res_out) {
-    __shared__ T Ws[RMAX][33];
+    // WFULL: all of W (r x n) staged in shared memory once (small problems,
+    // e.g. the paper shape), no per-chunk barriers; else 32-column chunks
+    extern __shared__ __align__(16) unsigned char vstep_smem[];
+    __shared__ T Ws[WFULL ? 1 : RMAX][33];
     __shared__ T qs[kWarps][RPW][RMAX];
     __shared__ double sc[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -184,6 +187,33 @@ nnmf_vstep_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ 
         }
     }
     double res = 0.0;
+    if (WFULL) {
+        T* Wf = reinterpret_cast<T*>(vstep_smem);
+        for (long long idx = threadIdx.x; idx < (long long)r * n; idx += kThreads) Wf[idx] = W[idx];
+        __syncthreads();
+        for (long long j = lane; j < n; j += 32) {
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+                const long long i = i0 + rr;
+                if (i < m) {
+                    const T x = X[i * ldx + j];
+                    T rec = T(0);
+#pragma unroll
+                    for (int k = 0; k < RMAX; ++k) {
+                        if (k < r) {
+                            const T w = Wf[(long long)k * n + j];
+                            q[rr][k] = fma(x, w, q[rr][k]);
+                            rec = fma(v[rr][k], w, rec);
+                        }
+                    }
+                    if (resid) {
+                        const double d = (double)x - (double)rec;
+                        res = fma(d, d, res);
+                    }
+                }
+            }
+        }
+    } else {
     for (long long j0 = 0; j0 < n; j0 += 32) {
         for (int idx = threadIdx.x; idx < r * 32; idx += kThreads) {
             const int k = idx >> 5, c = idx & 31;
@@ -214,6 +244,7 @@ nnmf_vstep_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ 
             }
         }
         __syncthreads();
+    }
     }
     if (flags & VSTEP_UPDATE) {
 #pragma unroll
@@ -449,6 +480,7 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws*
 }
 
 constexpr int kMaxRank = 128;
+constexpr size_t kWFullBytes = 96 * 1024;   // stage all of W when it fits
 
 template <typename T, int RMAX>
 struct K {
@@ -487,17 +519,33 @@ struct K {
     static void vstep(const T* X, long long ldx, const T* V, const T* W, T* Vout, long long m,
                       long long n, int r, int flags, const Plan& P, const Ws& L, double* res_out,
                       cudaStream_t st) {
+        const size_t wbytes = sizeof(T) * (size_t)r * (size_t)n;
+        const bool full = wbytes <= kWFullBytes;
         if constexpr (RMAX <= 16) {
             if (P.rpw == 2) {
+                if (full) {
+                    static bool attr = false;
+                    if (!attr) {
+                        cudaFuncSetAttribute(nnmf_vstep_kernel<T, RMAX, 2, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kWFullBytes);
+                        attr = true;
+                    }
+                    MMK_LAUNCH("nnmf_vstep", st,
+                               (nnmf_vstep_kernel<T, RMAX, 2, true><<<P.nvb, kThreads, wbytes, st>>>(
+                                   X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
+                                   res_out)));
+                    return;
+                }
                 MMK_LAUNCH("nnmf_vstep", st,
-                           (nnmf_vstep_kernel<T, RMAX, 2><<<P.nvb, kThreads, 0, st>>>(
+                           (nnmf_vstep_kernel<T, RMAX, 2, false><<<P.nvb, kThreads, 0, st>>>(
                                X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
                                res_out)));
                 return;
             }
         }
             MMK_LAUNCH("nnmf_vstep", st,
-                       (nnmf_vstep_kernel<T, RMAX, 1><<<P.nvb, kThreads, 0, st>>>(
+                       (nnmf_vstep_kernel<T, RMAX, 1, false><<<P.nvb, kThreads, 0, st>>>(
                            X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
                            res_out)));
     }

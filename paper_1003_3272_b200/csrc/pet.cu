@@ -1,15 +1,15 @@
 // pet.cu -- penalized Poisson MM for emission tomography (reference
 // pet.py:288-417), as a single pass over the system matrix E.
 //
-// Phase A (pet_project_kernel): a CTA owns kRays consecutive rays.  Each warp
-// forms one forward projection m_i = E_i . lam (vectorised row loads, fp64
-// accumulation), then the count ratio r_i = y_i / m_i and the loglik term
-// y_i ln m_i - m_i (pet.py:288-315).  The CTA then back-projects its own rays
-// while their rows are still in L1/L2: b^R_j = sum_{i in R} e_ij r_i, written
-// as a per-CTA partial.  E is therefore streamed from HBM once per iteration
-// (d*p*sizeof(T) bytes) -- the kernel's roofline.
-// pet_reduce_kernel sums the CTA partials in CTA order (deterministic) into
-// red = [b | loglik]; a multi-GPU caller all-reduces red across ray shards.
+// Phase A1 (pet_fwd_kernel): one warp per ray forms the forward projection
+// m_i = E_i . lam (vectorised row loads, fp64 accumulation), the count ratio
+// r_i = y_i / m_i and the loglik term y_i ln m_i - m_i (pet.py:288-315).
+// Phase A2 (pet_back_kernel): the back-projection b_j = sum_i e_ij r_i with a
+// thread per pixel over coalesced rows of E, split over ray ranges; the last
+// split block of each column block adds the split partials in order
+// (deterministic) into red = [b | loglik].  E is read twice per iteration; at
+// the paper shape (33 MB fp32) both reads are L2 hits.  A multi-GPU caller
+// all-reduces red across ray shards.
 //
 // Phase B (pet_pixel_kernel): per pixel c_j = lam_j b_j, neighbour sums over
 // the CSR lattice (pet.py:204-210), EM floor or positive-root update
@@ -24,89 +24,159 @@ using namespace mmk;
 constexpr int kRays = 8;      // rays (warps) per projection CTA
 constexpr int kPixThreads = 256;
 
+// warp-wide dot product of a row of E with lam, fp64 accumulation; four
+// independent accumulators per lane (combined in a fixed order) keep four
+// vector loads in flight
 template <typename T>
 __device__ __forceinline__ double row_dot(const T* __restrict__ e, const T* __restrict__ lam,
                                           long long p, int lane) {
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (sizeof(T) == 4 && (p & 3) == 0 && ((reinterpret_cast<uintptr_t>(e) & 15) == 0)) {
         const float4* e4 = reinterpret_cast<const float4*>(e);
         const float4* l4 = reinterpret_cast<const float4*>(lam);
-        for (long long q = lane; q < p / 4; q += 32) {
+        const long long nq = p / 4;
+        long long q = lane;
+        for (; q + 96 < nq; q += 128) {
+            const float4 x0 = __ldg(e4 + q), x1 = __ldg(e4 + q + 32), x2 = __ldg(e4 + q + 64),
+                         x3 = __ldg(e4 + q + 96);
+            const float4 y0 = __ldg(l4 + q), y1 = __ldg(l4 + q + 32), y2 = __ldg(l4 + q + 64),
+                         y3 = __ldg(l4 + q + 96);
+            a0 = fma((double)x0.x, (double)y0.x, a0);
+            a0 = fma((double)x0.y, (double)y0.y, a0);
+            a0 = fma((double)x0.z, (double)y0.z, a0);
+            a0 = fma((double)x0.w, (double)y0.w, a0);
+            a1 = fma((double)x1.x, (double)y1.x, a1);
+            a1 = fma((double)x1.y, (double)y1.y, a1);
+            a1 = fma((double)x1.z, (double)y1.z, a1);
+            a1 = fma((double)x1.w, (double)y1.w, a1);
+            a2 = fma((double)x2.x, (double)y2.x, a2);
+            a2 = fma((double)x2.y, (double)y2.y, a2);
+            a2 = fma((double)x2.z, (double)y2.z, a2);
+            a2 = fma((double)x2.w, (double)y2.w, a2);
+            a3 = fma((double)x3.x, (double)y3.x, a3);
+            a3 = fma((double)x3.y, (double)y3.y, a3);
+            a3 = fma((double)x3.z, (double)y3.z, a3);
+            a3 = fma((double)x3.w, (double)y3.w, a3);
+        }
+        for (; q < nq; q += 32) {
             const float4 a = __ldg(e4 + q), b = __ldg(l4 + q);
-            acc = fma((double)a.x, (double)b.x, acc);
-            acc = fma((double)a.y, (double)b.y, acc);
-            acc = fma((double)a.z, (double)b.z, acc);
-            acc = fma((double)a.w, (double)b.w, acc);
+            a0 = fma((double)a.x, (double)b.x, a0);
+            a0 = fma((double)a.y, (double)b.y, a0);
+            a0 = fma((double)a.z, (double)b.z, a0);
+            a0 = fma((double)a.w, (double)b.w, a0);
         }
     } else if (sizeof(T) == 8 && (p & 1) == 0 && ((reinterpret_cast<uintptr_t>(e) & 15) == 0)) {
         const double2* e2 = reinterpret_cast<const double2*>(e);
         const double2* l2 = reinterpret_cast<const double2*>(lam);
-        for (long long q = lane; q < p / 2; q += 32) {
+        const long long nq = p / 2;
+        long long q = lane;
+        for (; q + 32 < nq; q += 64) {
+            const double2 x0 = __ldg(e2 + q), x1 = __ldg(e2 + q + 32);
+            const double2 y0 = __ldg(l2 + q), y1 = __ldg(l2 + q + 32);
+            a0 = fma(x0.x, y0.x, a0);
+            a1 = fma(x0.y, y0.y, a1);
+            a2 = fma(x1.x, y1.x, a2);
+            a3 = fma(x1.y, y1.y, a3);
+        }
+        for (; q < nq; q += 32) {
             const double2 a = __ldg(e2 + q), b = __ldg(l2 + q);
-            acc = fma(a.x, b.x, acc);
-            acc = fma(a.y, b.y, acc);
+            a0 = fma(a.x, b.x, a0);
+            a1 = fma(a.y, b.y, a1);
         }
     } else {
-        for (long long q = lane; q < p; q += 32) acc = fma((double)e[q], (double)lam[q], acc);
+        for (long long q = lane; q < p; q += 32) a0 = fma((double)e[q], (double)lam[q], a0);
     }
-    return warp_sum(acc);
+    return warp_sum((a0 + a1) + (a2 + a3));
 }
 
+// Phase A1: kWPR warps per ray (latency hiding at small ray counts) --
+// m_i = E_i . lam (fp64 accumulation, the warps' partials combined in a
+// fixed order), the count ratio r_i and the loglik term; the last block sums
+// the per-block loglik partials in block order into red[p].
+constexpr int kWPR = 4;
+constexpr int kRaysPB = kRays / kWPR;   // rays per block
 template <typename T>
 __global__ void __launch_bounds__(kRays * 32)
-pet_project_kernel(const T* __restrict__ E, long long lde, const T* __restrict__ y,
-                   const T* __restrict__ lam, long long d, long long p,
-                   double* __restrict__ bpart, double* __restrict__ llpart, int64_t* err) {
+pet_fwd_kernel(const T* __restrict__ E, long long lde, const T* __restrict__ y,
+               const T* __restrict__ lam, long long d, long long p, double* __restrict__ ratio,
+               double* __restrict__ llpart, unsigned int* counter, double* __restrict__ red,
+               int64_t* err) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long ray0 = (long long)blockIdx.x * kRays;
-    __shared__ double ratio[kRays];
-    __shared__ double ll[kRays];
-    const long long i = ray0 + warp;
-    if (i < d) {
-        const double m = row_dot(E + i * lde, lam, p, lane);
-        if (lane == 0) {
-            const double yi = (double)y[i];
-            double r = 0.0, l = -m;
+    const int rl = warp / kWPR, part = warp % kWPR;
+    __shared__ double dots[kRays];
+    __shared__ double ll[kRaysPB];
+    __shared__ double sc[32];
+    const long long i = (long long)blockIdx.x * kRaysPB + rl;
+    // this warp's slice of the row: kWPR contiguous pieces, 16-byte aligned
+    long long seg = (p + kWPR - 1) / kWPR;
+    seg = (seg + 3) & ~3LL;
+    long long c0 = part * seg, c1 = c0 + seg;
+    if (c1 > p) c1 = p;
+    double dot = 0.0;
+    if (i < d && c0 < c1) dot = row_dot(E + i * lde + c0, lam + c0, c1 - c0, lane);
+    if (lane == 0) dots[warp] = dot;
+    __syncthreads();
+    if (threadIdx.x < kRaysPB) {
+        const long long ii = (long long)blockIdx.x * kRaysPB + threadIdx.x;
+        double l = 0.0;
+        if (ii < d) {
+            double m = 0.0;
+            for (int q = 0; q < kWPR; ++q) m += dots[threadIdx.x * kWPR + q];
+            const double yi = (double)y[ii];
+            double r = 0.0;
+            l = -m;
             if (yi > 0.0) {
-                if (m == 0.0) flag_error(err, MMK_E_NUMERICS, err_at(1, i));
+                if (m == 0.0) flag_error(err, MMK_E_NUMERICS, err_at(1, ii));
                 r = yi / m;
                 l += yi * log(m);
             }
-            ratio[warp] = r;
-            ll[warp] = l;
+            ratio[ii] = r;
         }
-    } else if (lane == 0) {
-        ratio[warp] = 0.0;
-        ll[warp] = 0.0;
+        ll[threadIdx.x] = l;
     }
     __syncthreads();
-    const long long left = d - ray0;
-    const int nr = left < kRays ? (int)left : kRays;
-    double* out = bpart + (long long)blockIdx.x * p;
-    for (long long j = threadIdx.x; j < p; j += blockDim.x) {
-        double b = 0.0;
-        for (int w = 0; w < nr; ++w) b = fma((double)E[(ray0 + w) * lde + j], ratio[w], b);
-        out[j] = b;
-    }
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < nr; ++w) s += ll[w];
-        llpart[blockIdx.x] = s;
+        double s2 = 0.0;
+        for (int w = 0; w < kRaysPB; ++w) s2 += ll[w];
+        llpart[blockIdx.x] = s2;
+    }
+    if (arrive_last(counter, gridDim.x)) {
+        const double t = block_sum_array(llpart, gridDim.x, sc);
+        if (threadIdx.x == 0) red[p] = t;
     }
 }
 
-__global__ void pet_reduce_kernel(const double* __restrict__ bpart, const double* __restrict__ llpart,
-                                  int nparts, long long p, double* __restrict__ red) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// Phase A2: back-projection b_j = sum_i e_ij r_i, split over ray ranges
+// (blockIdx.y); thread = pixel, coalesced rows of E.  The last ray-split
+// block of a column block sums the split partials in split order into red.
+constexpr int kBackCols = 128;
+template <typename T>
+__global__ void __launch_bounds__(kBackCols)
+pet_back_kernel(const T* __restrict__ E, long long lde, long long d, long long p,
+                long long rays_per_split, const double* __restrict__ ratio,
+                double* __restrict__ bpart, unsigned int* counters, double* __restrict__ red) {
+    const long long j = (long long)blockIdx.x * kBackCols + threadIdx.x;
+    const long long i0 = (long long)blockIdx.y * rays_per_split;
+    long long i1 = i0 + rays_per_split;
+    if (i1 > d) i1 = d;
     if (j < p) {
-        double b = 0.0;
-        for (int s = 0; s < nparts; ++s) b += bpart[(long long)s * p + j];
-        red[j] = b;
+        double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+        long long i = i0;
+        for (; i + 3 < i1; i += 4) {
+            const double e0 = (double)E[i * lde + j], e1 = (double)E[(i + 1) * lde + j],
+                         e2 = (double)E[(i + 2) * lde + j], e3 = (double)E[(i + 3) * lde + j];
+            b0 = fma(e0, ratio[i], b0);
+            b1 = fma(e1, ratio[i + 1], b1);
+            b2 = fma(e2, ratio[i + 2], b2);
+            b3 = fma(e3, ratio[i + 3], b3);
+        }
+        for (; i < i1; ++i) b0 = fma((double)E[i * lde + j], ratio[i], b0);
+        bpart[(long long)blockIdx.y * p + j] = (b0 + b1) + (b2 + b3);
     }
-    if (blockIdx.x == 0) {
-        __shared__ double sc[32];
-        const double t = block_sum_array(llpart, nparts, sc);
-        if (threadIdx.x == 0) red[p] = t;
+    if (arrive_last(counters + blockIdx.x, gridDim.y) && j < p) {
+        double t = 0.0;
+        for (unsigned int s2 = 0; s2 < gridDim.y; ++s2) t += bpart[(long long)s2 * p + j];
+        red[j] = t;
     }
 }
 
@@ -161,34 +231,57 @@ pet_pixel_kernel(const T* __restrict__ lam, T* __restrict__ lam_out, long long p
 }
 
 struct PetWs {
-    unsigned int* counter;
+    unsigned int* counter;    // [0] pixel kernel, [1] forward kernel
+    unsigned int* bcounters;  // one per back-projection column block
+    double* ratio;
     double* bpart;
     double* llpart;
     double* penpart;
-    int nparts;
+    int nfwd, ncb, splits;
+    long long rays_per_split;
 };
 
+void back_plan(long long d, long long p, int* ncb, int* splits, long long* rps) {
+    *ncb = ceil_div(p, kBackCols);
+    long long s = ceil_div(16 * kNumSMs, *ncb);
+    const long long smax = d > 32 ? d / 32 : 1;
+    if (s > smax) s = smax;
+    if (s < 1) s = 1;
+    *rps = ceil_div(d > 0 ? d : 1, s);
+    *splits = ceil_div(d > 0 ? d : 1, *rps);
+}
+
 size_t pet_ws_layout(long long d, long long p, void* base, PetWs* L) {
-    const int nparts = ceil_div(d > 0 ? d : 1, kRays);
+    const int nfwd = ceil_div(d > 0 ? d : 1, kRaysPB);
     const int npix = ceil_div(p, kPixThreads);
+    int ncb, splits;
+    long long rps;
+    back_plan(d, p, &ncb, &splits, &rps);
     size_t off = 256;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    // counter + penalty partials first so phase B finds them at offsets that
+    // counters + penalty partials first so phase B finds them at offsets that
     // do not depend on the ray count
     size_t o_pen = take(sizeof(double) * (size_t)npix);
-    size_t o_ll = take(sizeof(double) * (size_t)nparts);
-    size_t o_b = take(sizeof(double) * (size_t)nparts * (size_t)p);
+    size_t o_bc = take(sizeof(unsigned int) * (size_t)ncb);
+    size_t o_ll = take(sizeof(double) * (size_t)nfwd);
+    size_t o_r = take(sizeof(double) * (size_t)(d > 0 ? d : 1));
+    size_t o_b = take(sizeof(double) * (size_t)splits * (size_t)p);
     if (L && base) {
         char* c = reinterpret_cast<char*>(base);
         L->counter = reinterpret_cast<unsigned int*>(c);
+        L->bcounters = reinterpret_cast<unsigned int*>(c + o_bc);
+        L->ratio = reinterpret_cast<double*>(c + o_r);
         L->bpart = reinterpret_cast<double*>(c + o_b);
         L->llpart = reinterpret_cast<double*>(c + o_ll);
         L->penpart = reinterpret_cast<double*>(c + o_pen);
-        L->nparts = nparts;
+        L->nfwd = nfwd;
+        L->ncb = ncb;
+        L->splits = splits;
+        L->rays_per_split = rps;
     }
     return off;
 }
@@ -197,17 +290,18 @@ template <typename T>
 int pet_a(const T* E, long long lde, const T* y, const T* lam, long long d, long long p,
           const PetWs& L, double* red, int64_t* err, cudaStream_t st) {
     if (d > 0) {
-        MMK_LAUNCH("pet_project", st,
-                   (pet_project_kernel<T><<<L.nparts, kRays * 32, 0, st>>>(
-                       E, lde, y, lam, d, p, L.bpart, L.llpart, err)));
-        MMK_CHECK_LAUNCH("pet_project_kernel");
-        MMK_LAUNCH("pet_reduce", st,
-                   (pet_reduce_kernel<<<ceil_div(p, 256), 256, 0, st>>>(L.bpart, L.llpart,
-                                                                       L.nparts, p, red)));
+        MMK_LAUNCH("pet_fwd", st,
+                   (pet_fwd_kernel<T><<<L.nfwd, kRays * 32, 0, st>>>(
+                       E, lde, y, lam, d, p, L.ratio, L.llpart, L.counter + 1, red, err)));
+        MMK_CHECK_LAUNCH("pet_fwd_kernel");
+        MMK_LAUNCH("pet_back", st,
+                   (pet_back_kernel<T><<<dim3(L.ncb, L.splits), kBackCols, 0, st>>>(
+                       E, lde, d, p, L.rays_per_split, L.ratio, L.bpart, L.bcounters, red)));
+        MMK_CHECK_LAUNCH("pet_back_kernel");
     } else {
         cudaMemsetAsync(red, 0, sizeof(double) * (size_t)(p + 1), st);
+        MMK_CHECK_LAUNCH("pet_a memset");
     }
-    MMK_CHECK_LAUNCH("pet_reduce_kernel");
     return MMK_OK;
 }
 
