@@ -37,6 +37,8 @@ WORKLOADS = {
     "nnmf-large": dict(solver="nnmf", m=131072, n=16384, r=64, label="BASELINE config 4"),
     "mds-large": dict(solver="mds", n=65536, dim=3, label="BASELINE config 5"),
     "nnmf-c1": dict(solver="nnmf", m=2429, n=361, r=10, label="BASELINE config 1"),
+    "poisson-c1": dict(solver="poisson", m=2429, n=361, r=10,
+                       label="Poisson NNMF at the config-1 shape (SURVEY 8f)"),
     "pet-c2": dict(solver="pet", grid=64, detectors=64, mu=1e-5, label="BASELINE config 2"),
     "mds-c3": dict(solver="mds", n=401, dim=3, label="BASELINE config 3"),
 }
@@ -152,6 +154,20 @@ def cpu_sample(workload, seconds):
             f"{iters} oracle MM iteration(s) (objective + V,W update) on {rows} of {m} rows "
             f"(n={n}, r={r}, fp64 tree-summed); per-iteration time scaled linearly in rows"
             if rows < m else f"{iters} oracle MM iterations at full size (fp64)")
+    if W["solver"] == "poisson":
+        x = np.floor(rng.random((W["m"], W["n"])) * 6.0)
+        v = rng.random((W["m"], W["r"]))
+        w = rng.random((W["r"], W["n"]))
+        t0 = time.perf_counter()
+        iters = 0
+        while True:
+            O.nnmf_poisson_objective(x, v, w, threads)
+            v, w = O.nnmf_poisson_update(x, v, w, threads)
+            iters += 1
+            if time.perf_counter() - t0 > seconds or iters >= 50:
+                break
+        dt = (time.perf_counter() - t0) / iters
+        return 1.0 / dt, threads, f"{iters} oracle Poisson MM iterations at full size (fp64)"
     if W["solver"] == "mds":
         n, dim = W["n"], W["dim"]
         ns = n if n <= 2048 else 1024
@@ -423,6 +439,14 @@ def suite(args, torch, dev):
     cpu, thr, _ = cpu_sample("nnmf-c1", 3.0)
     out["nnmf-c1"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
                       "speedup": tr.iters / dt / cpu}
+    xc = np.floor(np.random.default_rng(21).random((2429, 361)) * 6.0)
+    g = np.random.default_rng(22)
+    sc0 = M.FactorPair(g.random((2429, 10)), g.random((10, 361)))
+    cprob = M.NnmfProblem(x=xc, rank=10)
+    (_, tr), dt = timed(lambda: M.nnmf_poisson_run(cprob, cfg, be, state0=sc0))
+    cpu, thr, _ = cpu_sample("poisson-c1", 3.0)
+    out["poisson-c1"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
+                         "speedup": tr.iters / dt / cpu}
     e = D.build_system_matrix(D.PetGeometry(64, 64))
     y = D.simulate_counts(D.default_phantom(64), e, 20260811)
     pprob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=D.build_neighborhoods(64))

@@ -100,6 +100,29 @@ int mmk_nnmf_update_w(int dtype, const void *X, int64_t ldx, const void *V, cons
                       double *red, int64_t *err_dev, void *stream);
 
 /* ------------------------------------------------------------------------
+ * NNMF, Poisson log fit (nnmf.py:178-265), rank <= 64.  Square-root
+ * multiplicative MM: V' = V sqrt((R W^T) / (rowsum W + guard)) with
+ * R = X / (VW) masked to x > 0, then W' = W sqrt((V'^T R') / (colsum V' +
+ * guard)) with R' = X / (V'W).
+ *   iter_a : f-partial(V, W) = sum x ln(VW) - VW (fp64) over the local rows,
+ *            V -> V_out, red = [ V'^T R' (r x n) | colsum V' (r) | f-partial ]
+ *   iter_b : W' from the (all-reduced) red -> W_out, f_dev = red[f]
+ * A positive count over a zero reconstruction sets NUMERICS at site 1
+ * (state's objective / V half) or 2 (W half), index i * n + j.
+ * ---------------------------------------------------------------------- */
+int mmk_nnmf_poisson_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
+int64_t mmk_nnmf_poisson_reduce_len(int64_t n, int64_t r);
+int mmk_nnmf_poisson_iter_a(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
+                            void *V_out, int64_t m, int64_t n, int64_t r, void *ws,
+                            size_t ws_bytes, double *red, int64_t *err_dev, void *stream);
+int mmk_nnmf_poisson_iter_b(int dtype, const void *W, void *W_out, int64_t n, int64_t r,
+                            const double *red, double *f_dev, int64_t *err_dev, void *stream);
+int mmk_nnmf_poisson_iter(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
+                          void *V_out, void *W_out, int64_t m, int64_t n, int64_t r, void *ws,
+                          size_t ws_bytes, double *red, double *f_dev, int64_t *err_dev,
+                          void *stream);
+
+/* ------------------------------------------------------------------------
  * PET penalized Poisson MM.  E is d x p (leading dim lde), y d, lam p.
  * Neighbourhoods as int32 CSR (nbr_ptr p+1, nbr_idx).  Replaces
  * pet_update / pet_penalized_objective / pet_loglik (pet.py:288-417) with the
@@ -249,6 +272,11 @@ int mmk_nnmf_engine_create(int dtype, const void *X, int64_t ldx, void *VA, void
                            void *WB, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,
                            double *red, void *comm, const mmk_stop_rule *rule, double *trace,
                            int64_t *tstamp, int64_t *ctl, int64_t *err_dev, void **engine);
+int mmk_nnmf_poisson_engine_create(int dtype, const void *X, int64_t ldx, void *VA, void *WA,
+                                   void *VB, void *WB, int64_t m, int64_t n, int64_t r, void *ws,
+                                   size_t ws_bytes, double *red, void *comm,
+                                   const mmk_stop_rule *rule, double *trace, int64_t *tstamp,
+                                   int64_t *ctl, int64_t *err_dev, void **engine);
 int mmk_pet_engine_create(int dtype, const void *E, int64_t lde, const void *y, void *lamA,
                           void *lamB, int64_t d, int64_t p, const int32_t *nbr_ptr,
                           const int32_t *nbr_idx, double mu, void *ws, size_t ws_bytes,

@@ -149,6 +149,49 @@ def nnmf_step(x, v, w, threads=1):                    # nnmf.py:153-156
 
 
 # --------------------------------------------------------------------------
+# NNMF (Poisson log fit), nnmf.py:178-265
+def _masked_ratio(x, b):                              # nnmf.py:178-190
+    if np.any((x > 0.0) & (b == 0.0)):
+        raise OracleError("NumericsError",
+                          "reconstruction has zero mean where data is positive")
+    out = np.zeros_like(x)
+    m = x > 0.0
+    out[m] = x[m] / b[m]
+    return out
+
+
+def nnmf_poisson_objective(x, v, w, threads=1):       # nnmf.py:193-209
+    b = matmul(v, w, threads=threads)
+    x = _f64(x)
+    if np.any((x > 0.0) & (b == 0.0)):
+        raise OracleError("NumericsError", "zero reconstruction mean at a positive data entry")
+    out = -b.copy()
+    m = x > 0.0
+    out[m] += x[m] * np.log(b[m])
+    return tree_sum(out)
+
+
+def nnmf_poisson_update(x, v, w, threads=1):          # nnmf.py:212-242
+    for name, m in (("x", x), ("v", v), ("w", w)):
+        _require_nonneg(name, m)
+    x, v, w = _f64(x), _f64(v), _f64(w)
+    p, q = x.shape
+    b = matmul(v, w, threads=threads)
+    ratio = _masked_ratio(x, b)
+    numer_v = matmul(ratio, w, tb=True, threads=threads)
+    w_sums = matvec(w, np.ones(q), threads=threads)
+    v_next = v * np.sqrt(numer_v / (np.broadcast_to(w_sums, (p, len(w_sums))) +
+                                    NNMF_DENOM_GUARD))
+    b = matmul(v_next, w, threads=threads)
+    ratio = _masked_ratio(x, b)
+    numer_w = matmul(v_next, ratio, ta=True, threads=threads)
+    v_sums = matvec(v_next, np.ones(p), ta=True, threads=threads)
+    w_next = w * np.sqrt(numer_w / (np.broadcast_to(v_sums[:, None], (len(v_sums), q)) +
+                                    NNMF_DENOM_GUARD))
+    return v_next, w_next
+
+
+# --------------------------------------------------------------------------
 # PET, pet.py
 class PetData:
     """The arrays ``PetProblem`` derives (pet.py:231-277)."""
@@ -331,6 +374,14 @@ def nnmf_run(x, v0, w0, max_iters, threads=1, **kw):
     return run(lambda s: nnmf_objective(x, s[0], s[1], threads),
                lambda s: nnmf_step(x, s[0], s[1], threads),
                (_f64(v0), _f64(w0)), "minimize", max_iters, **kw)
+
+
+def nnmf_poisson_run(x, v0, w0, max_iters, threads=1, **kw):
+    """_PoissonNnmf under run_mm (nnmf.py:245-265) from a given start."""
+    x = _f64(x)
+    return run(lambda s: nnmf_poisson_objective(x, s[0], s[1], threads),
+               lambda s: nnmf_poisson_update(x, s[0], s[1], threads),
+               (_f64(v0), _f64(w0)), "maximize", max_iters, **kw)
 
 
 def pet_run(pd, max_iters, threads=1, lam0=None, **kw):

@@ -19,7 +19,8 @@ from .errors import (DeviceError, DomainError, InputError, MatrixFormatError, Mm
 from .kernels import elementwise, matmul, matvec, tree_reduce_sum
 from .mds import (MdsProblem, PackedMdsProblem, anchor_configuration, mds_run, mds_update, stress,
                   stress_gradient)
-from .nnmf import (FactorPair, NnmfProblem, nnmf_gradient, nnmf_objective, nnmf_run,
+from .nnmf import (FactorPair, NnmfProblem, nnmf_gradient, nnmf_objective,
+                   nnmf_poisson_objective, nnmf_poisson_run, nnmf_poisson_update, nnmf_run,
                    nnmf_surrogate, nnmf_update_v, nnmf_update_w)
 from .pet import (PetProblem, pet_loglik, pet_penalized_gradient, pet_penalized_objective,
                   pet_run, pet_surrogate, pet_update)

@@ -46,6 +46,15 @@ _SIGS = {
                            _vp], _i32),
     "mmk_nnmf_update_w": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp,
                            _vp], _i32),
+    "mmk_nnmf_poisson_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
+    "mmk_nnmf_poisson_reduce_len": ([_i64, _i64], _i64),
+    "mmk_nnmf_poisson_iter_a": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp,
+                                 _vp, _vp], _i32),
+    "mmk_nnmf_poisson_iter_b": ([_i32, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp], _i32),
+    "mmk_nnmf_poisson_iter": ([_i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz,
+                               _vp, _vp, _vp, _vp], _i32),
+    "mmk_nnmf_poisson_engine_create": ([_i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                        _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "mmk_pet_ws_bytes": ([_i32, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_pet_reduce_len": ([_i64], _i64),
     "mmk_pet_iter_a": ([_i32, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp], _i32),

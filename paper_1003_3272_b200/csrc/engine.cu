@@ -326,3 +326,27 @@ extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_
     std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * sizeof(float)}};
     return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
 }
+
+extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t ldx, void* VA,
+                                              void* WA, void* VB, void* WB, int64_t m, int64_t n,
+                                              int64_t r, void* ws, size_t ws_bytes, double* red,
+                                              void* comm, const mmk_stop_rule* rule,
+                                              double* trace, int64_t* tstamp, int64_t* ctl,
+                                              int64_t* err_dev, void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    const int64_t rl = mmk_nnmf_poisson_reduce_len(n, r);
+    auto iter = [=](cudaStream_t s) -> int {
+        int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, VA, WA, VB, m, n, r, ws, ws_bytes, red,
+                                         err_dev, s);
+        if (rc) return rc;
+        if (comm) {
+            rc = mmk_allreduce_f64(red, rl, comm, s);
+            if (rc) return rc;
+        }
+        return mmk_nnmf_poisson_iter_b(dtype, WA, WB, n, r, red, f_dev, err_dev, s);
+    };
+    std::vector<Copy> copies = {{VA, VB, (size_t)(m * r) * esize(dtype)},
+                                {WA, WB, (size_t)(r * n) * esize(dtype)}};
+    if (m == 0) copies.erase(copies.begin());
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}

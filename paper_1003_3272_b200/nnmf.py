@@ -10,11 +10,16 @@ Drop-in for the reference's Frobenius path (``pkg/src/mmkit/nnmf.py``):
   nnmf_run         nnmf.py:170-177 uniform(0,1) start from default_rng(seed)
   _initial_factors nnmf.py:162-167 same PCG64 draw order
 
-Every update and objective runs in libmmk.so (``csrc/nnmf.cu``); one MM
-iteration is one fused device pass (see ``_engine.DeviceMm``).  The Poisson
-variant and ``cbcl_preprocess`` are outside this round's hot-path scope
-(SURVEY.md section 8f); ``cbcl_preprocess`` is provided host-side in
-``datasets``.  ``nnmf_gradient`` / ``nnmf_surrogate`` are host-side fp64
+Poisson log fit (the first "next" row):
+
+  nnmf_poisson_objective nnmf.py:193-209  sum x ln(VW) - VW, 0 ln 0 = 0
+  nnmf_poisson_update    nnmf.py:212-242  joint square-root update (V, then W)
+  nnmf_poisson_run       nnmf.py:262-265  maximize from the uniform(0,1) start
+
+Every update and objective runs in libmmk.so (``csrc/nnmf.cu``,
+``csrc/nnmf_tc.cu``, ``csrc/nnmf_poisson.cu``); one MM iteration is one fused
+device pass (see ``_engine.DeviceMm``).  ``cbcl_preprocess`` is provided
+host-side in ``datasets``.  ``nnmf_gradient`` / ``nnmf_surrogate`` are host-side fp64
 property-test helpers, not part of the iteration.
 """
 
@@ -33,7 +38,8 @@ from .driver import run_mm
 from .errors import DomainError, ShapeError
 
 __all__ = ["NnmfProblem", "FactorPair", "nnmf_objective", "nnmf_update_v", "nnmf_update_w",
-           "nnmf_run", "nnmf_gradient", "nnmf_surrogate"]
+           "nnmf_run", "nnmf_gradient", "nnmf_surrogate", "nnmf_poisson_objective",
+           "nnmf_poisson_update", "nnmf_poisson_run"]
 
 DENOM_GUARD = 1e-300
 
@@ -229,6 +235,93 @@ def nnmf_run(problem, config, backend=SERIAL, state0=None):
     tensor X."""
     start = _initial_factors(problem, config.seed) if state0 is None else state0
     mm = _GpuNnmf(problem, backend)
+    state, trace = run_mm(mm, mm.device_state(start), config)
+    return FactorPair(A.to_user(state.v, problem.x), A.to_user(state.w, problem.x)), trace
+
+
+# ---------------------------------------------------------------------------
+# Poisson log fit (nnmf.py:178-265)
+def _poisson_messages(n):
+    def at(text):
+        return lambda idx: text
+    return {1: at("zero reconstruction mean at a positive data entry"),
+            2: at("reconstruction has zero mean where data is positive")}
+
+
+class _GpuPoissonNnmf(_GpuNnmf):
+    """``_PoissonNnmf`` (nnmf.py:245-259) on the device: objective(state)
+    runs one fused pass giving f(state) and the next state."""
+
+    direction = "maximize"
+
+    def __init__(self, problem, backend, x_dev=None):
+        DeviceMm.__init__(self, backend)
+        torch = self.torch
+        self.x = problem.device_x(backend, torch) if x_dev is None else x_dev
+        self.m, self.n = self.x.shape
+        self.r = problem.rank
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_poisson_ws_bytes", self.code, self.m,
+                                            self.n, self.r), dtype=torch.uint8,
+                              device=self.device)
+        self.red = torch.zeros(_lib.load().mmk_nnmf_poisson_reduce_len(self.n, self.r),
+                               dtype=torch.float64, device=self.device)
+        self._problem = problem
+
+    def _messages(self):
+        return _poisson_messages(self.n)
+
+    def _iterate(self, s, out, f_ptr, err_ptr):
+        _lib.call("mmk_nnmf_poisson_iter", self.code, _lib.ptr(self.x), self.x.stride(0),
+                  _lib.ptr(s.v), _lib.ptr(s.w), _lib.ptr(out.v), _lib.ptr(out.w), self.m, self.n,
+                  self.r, _lib.ptr(self.ws), self.ws.numel(), _lib.ptr(self.red), f_ptr, err_ptr,
+                  self.stream())
+
+    def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
+        self._keep = (a, b)
+        _lib.call("mmk_nnmf_poisson_engine_create", self.code, _lib.ptr(self.x),
+                  self.x.stride(0), _lib.ptr(a.v), _lib.ptr(a.w), _lib.ptr(b.v), _lib.ptr(b.w),
+                  self.m, self.n, self.r, _lib.ptr(self.ws), self.ws.numel(), _lib.ptr(self.red),
+                  self.comm, ctypes.byref(rule), _lib.ptr(trace), _lib.ptr(stamp), _lib.ptr(ctl),
+                  self.status.err_ptr, ctypes.byref(eng))
+
+    def surrogate(self, state, anchor):
+        raise NotImplementedError("the reference defines no Poisson surrogate")
+
+
+def _poisson_pass(x, v, w, backend):
+    """One fused device pass: (f(V, W), V', W') as device tensors."""
+    m, n, r = _conform(x, v, w)
+    prob = NnmfProblem.__new__(NnmfProblem)
+    object.__setattr__(prob, "x", x)
+    object.__setattr__(prob, "rank", r)
+    object.__setattr__(prob, "_dev", {})
+    mm = _GpuPoissonNnmf(prob, backend)
+    s = mm.device_state(FactorPair(v, w))
+    out = mm._alloc_like(s)
+    mm._iterate(s, out, mm.status.f_ptr, mm.status.err_ptr)
+    return mm._check_error(), out
+
+
+def nnmf_poisson_objective(x, v, w, backend=SERIAL):
+    """Poisson-model log fit: sum of x*ln(VW) - VW, with 0 ln 0 = 0."""
+    f, _ = _poisson_pass(x, v, w, backend)
+    return f
+
+
+def nnmf_poisson_update(x, v, w, backend=SERIAL):
+    """One joint square-root multiplicative update of (V, W): V first, then W
+    against the recomputed reconstruction (nnmf.py:212-242)."""
+    for name, mat in (("x", x), ("v", v), ("w", w)):
+        _require_nonneg(name, mat)
+    _, out = _poisson_pass(x, v, w, backend)
+    return A.to_user(out.v, v), A.to_user(out.w, w)
+
+
+def nnmf_poisson_run(problem, config, backend=SERIAL, state0=None):
+    """Factorize under the Poisson log fit from a uniform(0,1) start drawn
+    with ``config.seed`` (or from ``state0``); returns (FactorPair, MmTrace)."""
+    start = _initial_factors(problem, config.seed) if state0 is None else state0
+    mm = _GpuPoissonNnmf(problem, backend)
     state, trace = run_mm(mm, mm.device_state(start), config)
     return FactorPair(A.to_user(state.v, problem.x), A.to_user(state.w, problem.x)), trace
 

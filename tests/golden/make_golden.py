@@ -150,7 +150,34 @@ def gen_mds_small():
     save("mds_small", y=y, trace=tr.objective_values, theta=theta, anchored=anchored)
 
 
+def poisson_c1_inputs():
+    """Count data of the CBCL shape (2429 x 361), rank 10 start; fp32-exact."""
+    x = np.floor(np.random.default_rng(21).random((2429, 361)) * 6.0)
+    g = np.random.default_rng(22)
+    return x, f32(g.random((2429, 10))), f32(g.random((10, 361)))
+
+
+def gen_poisson_small():
+    rng = np.random.default_rng(12)
+    x = np.floor(rng.random((12, 9)) * 6.0)
+    problem = R.NnmfProblem(x=x, rank=3)
+    state, tr = R.nnmf_poisson_run(problem, R.MmConfig(max_iters=40, seed=4))
+    save("poisson_small", x=x, trace=tr.objective_values, v=state.v, w=state.w)
+
+
+def gen_poisson_c1():
+    x, v0, w0 = poisson_c1_inputs()
+    problem = R.NnmfProblem(x=x, rank=10)
+    import importlib
+    nn = importlib.import_module("mmkit_ref.nnmf")
+    mm = nn._PoissonNnmf(problem, R.Backend.parallel(THREADS))
+    state, tr = R.run_mm(mm, nn.FactorPair(v0, w0), R.MmConfig(max_iters=100, epsilon=1e-300))
+    save("poisson_c1", trace=tr.objective_values, v=state.v, w=state.w,
+         x_digest=digest(x), v0_digest=digest(v0), w0_digest=digest(w0))
+
+
 GENERATORS = {
+    "poisson_small": gen_poisson_small, "poisson_c1": gen_poisson_c1,
     "nnmf_small": gen_nnmf_small, "pet_small": gen_pet_small, "mds_small": gen_mds_small,
     "mds_c3": gen_mds_c3, "pet_c2": gen_pet_c2, "nnmf_c1": gen_nnmf_c1,
     "pet_c2_converge": gen_pet_c2_converge,

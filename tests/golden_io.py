@@ -29,6 +29,13 @@ def c1_inputs():
     return x, f32(g.random((2429, 10))), f32(g.random((10, 361)))
 
 
+def poisson_c1_inputs():
+    """Count data of the CBCL shape, rank 10 (tests/golden/make_golden.py)."""
+    x = np.floor(np.random.default_rng(21).random((2429, 361)) * 6.0)
+    g = np.random.default_rng(22)
+    return x, f32(g.random((2429, 10))), f32(g.random((10, 361)))
+
+
 _C2 = {}
 
 

@@ -29,6 +29,36 @@ def test_nnmf_c1_prefix_bitwise():
     assert np.array_equal(trace, g["trace"][:3])
 
 
+def test_poisson_small_run_bitwise():
+    g = G.load("poisson_small")
+    x = g["x"]
+    rng = np.random.default_rng(4)          # nnmf_poisson_run's init, nnmf.py:262-265
+    v0, w0 = rng.random((12, 3)), rng.random((3, 9))
+    (v, w), trace, _ = O.nnmf_poisson_run(x, v0, w0, 40, threads=3, epsilon=1e-9)
+    assert np.array_equal(trace, g["trace"])
+    assert np.array_equal(v, g["v"]) and np.array_equal(w, g["w"])
+
+
+def test_poisson_c1_prefix_bitwise():
+    g = G.load("poisson_c1")
+    x, v0, w0 = G.poisson_c1_inputs()
+    assert G.digest(x) == str(g["x_digest"]) and G.digest(v0) == str(g["v0_digest"])
+    _, trace, _ = O.nnmf_poisson_run(x, v0, w0, 2, threads=8)
+    assert np.array_equal(trace, g["trace"][:3])
+
+
+def test_poisson_kats():
+    """test_nnmf.py:146-158: X = VW is a fixed point; 1x1 square-root update."""
+    rng = np.random.default_rng(8)
+    v = rng.random((5, 2)) + 0.1
+    w = rng.random((2, 6)) + 0.1
+    x = O.matmul(v, w)
+    v2, w2 = O.nnmf_poisson_update(x, v, w)
+    assert np.array_equal(v2, v) and np.array_equal(w2, w)
+    v2, _ = O.nnmf_poisson_update(np.array([[4.0]]), np.array([[1.0]]), np.array([[1.0]]))
+    assert v2[0, 0] == 2.0
+
+
 @pytest.mark.parametrize("mu", [0.0, 1e-7, 1e-6, 1e-5])
 def test_pet_small_run_bitwise(mu):
     g = G.load("pet_small")
@@ -91,6 +121,11 @@ def test_oracle_matches_live_reference_random():
         assert np.array_equal(O.nnmf_update_v(x, v, w, 3), R.nnmf_update_v(x, v, w))
         assert np.array_equal(O.nnmf_update_w(x, v, w, 2), R.nnmf_update_w(x, v, w))
         assert O.nnmf_objective(x, v, w) == R.nnmf_objective(x, v, w)
+        xc = np.floor(x * 3.0)
+        v2o, w2o = O.nnmf_poisson_update(xc, v, w, 2)
+        v2r, w2r = R.nnmf_poisson_update(xc, v, w)
+        assert np.array_equal(v2o, v2r) and np.array_equal(w2o, w2r)
+        assert O.nnmf_poisson_objective(xc, v, w) == R.nnmf_poisson_objective(xc, v, w)
         y = rng.random((q + 2, q + 2))
         y = (y + y.T) / 2.0
         np.fill_diagonal(y, 0.0)
