@@ -150,6 +150,23 @@ int mmk_pet_iter(int dtype, const void *E, int64_t lde, const void *y, const voi
                  const int32_t *nbr_idx, double mu, int flags, void *ws, size_t ws_bytes,
                  double *red, double *f_dev, int64_t *err_dev, void *stream);
 
+/* Sparse system matrix variant (the Siddon matrix is ~1 % nonzero): E as
+ * CSR by rays (rptr d+1, ridx, rval) for the forward projection and CSC by
+ * pixels (cptr p+1, cidx, cval) for the back-projection, int32 indices,
+ * values in `dtype`.  Same red layout and phase B as the dense path (a
+ * sharded caller passes its rays' CSR rows and the CSC of its ray block). */
+int mmk_pet_sparse_ws_bytes(int dtype, int64_t d, int64_t p, size_t *out);
+int mmk_pet_sparse_iter_a(int dtype, const int32_t *rptr, const int32_t *ridx, const void *rval,
+                          const int32_t *cptr, const int32_t *cidx, const void *cval,
+                          const void *y, const void *lam, int64_t d, int64_t p, void *ws,
+                          size_t ws_bytes, double *red, int64_t *err_dev, void *stream);
+int mmk_pet_sparse_iter(int dtype, const int32_t *rptr, const int32_t *ridx, const void *rval,
+                        const int32_t *cptr, const int32_t *cidx, const void *cval, const void *y,
+                        const void *lam, void *lam_out, int64_t d, int64_t p,
+                        const int32_t *nbr_ptr, const int32_t *nbr_idx, double mu, int flags,
+                        void *ws, size_t ws_bytes, double *red, double *f_dev, int64_t *err_dev,
+                        void *stream);
+
 /* ------------------------------------------------------------------------
  * MDS stress majorization, full-row tiling.  theta is dim x n (SoA: row k =
  * coordinate k of every point).  Y/Wt point at row `row0` of the n x n
@@ -282,6 +299,14 @@ int mmk_pet_engine_create(int dtype, const void *E, int64_t lde, const void *y, 
                           const int32_t *nbr_idx, double mu, void *ws, size_t ws_bytes,
                           double *red, void *comm, const mmk_stop_rule *rule, double *trace,
                           int64_t *tstamp, int64_t *ctl, int64_t *err_dev, void **engine);
+int mmk_pet_sparse_engine_create(int dtype, const int32_t *rptr, const int32_t *ridx,
+                                 const void *rval, const int32_t *cptr, const int32_t *cidx,
+                                 const void *cval, const void *y, void *lamA, void *lamB,
+                                 int64_t d, int64_t p, const int32_t *nbr_ptr,
+                                 const int32_t *nbr_idx, double mu, void *ws, size_t ws_bytes,
+                                 double *red, void *comm, const mmk_stop_rule *rule,
+                                 double *trace, int64_t *tstamp, int64_t *ctl, int64_t *err_dev,
+                                 void **engine);
 int mmk_mds_engine_create(int dtype, const void *Y, const void *Wt, int64_t ldy,
                           const double *wsum, void *thetaA, void *thetaB, void *local_out,
                           void *gathered, int64_t dim, int64_t n, int64_t row0, int64_t rows,

@@ -23,6 +23,10 @@ plain one-iteration-per-host-round-trip loop.
 any weights, fp32/fp64), ``"tri"`` (packed upper triangle, unit weights,
 fp32, p <= 3: every pair read once) or ``"auto"`` (tri from
 ``mds.TRI_MIN_POINTS`` points when it applies).
+
+``pet_kernel`` picks the PET projector: ``"dense"`` (stream E), ``"sparse"``
+(CSR/CSC of E's nonzeros) or ``"auto"`` (sparse when E is under
+``pet.SPARSE_DENSITY`` nonzero -- the Siddon matrix is ~1 %).
 """
 
 from dataclasses import dataclass
@@ -40,12 +44,16 @@ class Backend:
     device: Optional[int] = None
     fused: bool = True
     mds_kernel: str = "auto"
+    pet_kernel: str = "auto"
 
     def __post_init__(self):
         if self.threads < 1:
             raise ShapeError(f"backend needs at least 1 thread, got {self.threads}")
         if self.dtype not in ("fp32", "fp64"):
             raise ShapeError(f"dtype must be 'fp32' or 'fp64', got {self.dtype!r}")
+        if self.pet_kernel not in ("auto", "dense", "sparse"):
+            raise ShapeError(f"pet_kernel must be 'auto', 'dense' or 'sparse', got "
+                             f"{self.pet_kernel!r}")
         if self.mds_kernel not in ("auto", "rows", "tri"):
             raise ShapeError(f"mds_kernel must be 'auto', 'rows' or 'tri', got {self.mds_kernel!r}")
 

@@ -350,3 +350,30 @@ extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t 
     if (m == 0) copies.erase(copies.begin());
     return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
 }
+
+extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, const int32_t* ridx,
+                                            const void* rval, const int32_t* cptr,
+                                            const int32_t* cidx, const void* cval, const void* y,
+                                            void* lamA, void* lamB, int64_t d, int64_t p,
+                                            const int32_t* nbr_ptr, const int32_t* nbr_idx,
+                                            double mu, void* ws, size_t ws_bytes, double* red,
+                                            void* comm, const mmk_stop_rule* rule, double* trace,
+                                            int64_t* tstamp, int64_t* ctl, int64_t* err_dev,
+                                            void** engine) {
+    double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
+    const int64_t rl = mmk_pet_reduce_len(p);
+    auto iter = [=](cudaStream_t s) -> int {
+        int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lamA, d, p,
+                                       ws, ws_bytes, red, err_dev, s);
+        if (rc) return rc;
+        if (comm) {
+            rc = mmk_allreduce_f64(red, rl, comm, s);
+            if (rc) return rc;
+        }
+        return mmk_pet_iter_b(dtype, lamA, lamB, p, nbr_ptr, nbr_idx, mu,
+                              MMK_PET_UPDATE | MMK_PET_OBJECTIVE, red, ws, ws_bytes, f_dev,
+                              err_dev, s);
+    };
+    std::vector<Copy> copies = {{lamA, lamB, (size_t)p * esize(dtype)}};
+    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+}

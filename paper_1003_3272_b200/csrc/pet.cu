@@ -327,6 +327,125 @@ int check_ws(long long d, long long p, void* ws, size_t ws_bytes, PetWs* L) {
     return MMK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Sparse system matrix (the Siddon matrix of build_system_matrix is ~1 %
+// nonzero, pet.py:69-132): E by rays as CSR (forward projection) and by
+// pixels as CSC (back-projection), int32 indices.  The back-projection then
+// writes red[j] directly -- no partials, deterministic by construction.
+
+// warp per ray: m_i over the CSR row, ratio, loglik; last block -> red[p]
+template <typename T>
+__global__ void __launch_bounds__(kRays * 32)
+pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+                const T* __restrict__ rval, const T* __restrict__ y, const T* __restrict__ lam,
+                long long d, long long p, double* __restrict__ ratio, double* __restrict__ llpart,
+                unsigned int* counter, double* __restrict__ red, int64_t* err) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double ll[kRays];
+    __shared__ double sc[32];
+    const long long i = (long long)blockIdx.x * kRays + warp;
+    double l = 0.0;
+    if (i < d) {
+        double m = 0.0;
+        for (int t = rptr[i] + lane; t < rptr[i + 1]; t += 32)
+            m = fma((double)rval[t], (double)lam[ridx[t]], m);
+        m = warp_sum(m);
+        if (lane == 0) {
+            const double yi = (double)y[i];
+            double r = 0.0;
+            l = -m;
+            if (yi > 0.0) {
+                if (m == 0.0) flag_error(err, MMK_E_NUMERICS, err_at(1, i));
+                r = yi / m;
+                l += yi * log(m);
+            }
+            ratio[i] = r;
+        }
+    }
+    if (lane == 0) ll[warp] = l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s2 = 0.0;
+        for (int w = 0; w < kRays; ++w) s2 += ll[w];
+        llpart[blockIdx.x] = s2;
+    }
+    if (arrive_last(counter, gridDim.x)) {
+        const double t = block_sum_array(llpart, gridDim.x, sc);
+        if (threadIdx.x == 0) red[p] = t;
+    }
+}
+
+// thread per pixel: b_j over the CSC column -> red[j]
+template <typename T>
+__global__ void __launch_bounds__(256)
+pet_sback_kernel(const int32_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
+                 const T* __restrict__ cval, long long p, const double* __restrict__ ratio,
+                 double* __restrict__ red) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p) return;
+    double b0 = 0.0, b1 = 0.0;
+    int t = cptr[j];
+    const int t1 = cptr[j + 1];
+    for (; t + 1 < t1; t += 2) {
+        b0 = fma((double)cval[t], ratio[cidx[t]], b0);
+        b1 = fma((double)cval[t + 1], ratio[cidx[t + 1]], b1);
+    }
+    if (t < t1) b0 = fma((double)cval[t], ratio[cidx[t]], b0);
+    red[j] = b0 + b1;
+}
+
+struct SparseWs {
+    unsigned int* counter;   // [0] pixel kernel, [1] forward kernel
+    double* llpart;
+    double* ratio;
+    int nfwd;
+};
+
+// phase B (shared with the dense path) finds the counter and the penalty
+// partials at the same offsets as pet_ws_layout
+size_t sparse_ws_layout(long long d, long long p, void* base, SparseWs* L) {
+    const int nfwd = ceil_div(d > 0 ? d : 1, kRays);
+    const int npix = ceil_div(p, kPixThreads);
+    size_t off = 256;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    take(sizeof(double) * (size_t)npix);   // penalty partials (phase B)
+    size_t o_ll = take(sizeof(double) * (size_t)nfwd);
+    size_t o_r = take(sizeof(double) * (size_t)(d > 0 ? d : 1));
+    if (L && base) {
+        char* c = reinterpret_cast<char*>(base);
+        L->counter = reinterpret_cast<unsigned int*>(c);
+        L->llpart = reinterpret_cast<double*>(c + o_ll);
+        L->ratio = reinterpret_cast<double*>(c + o_r);
+        L->nfwd = nfwd;
+    }
+    return off;
+}
+
+template <typename T>
+int pet_sparse_a(const int32_t* rptr, const int32_t* ridx, const T* rval, const int32_t* cptr,
+                 const int32_t* cidx, const T* cval, const T* y, const T* lam, long long d,
+                 long long p, const SparseWs& L, double* red, int64_t* err, cudaStream_t st) {
+    if (d > 0) {
+        MMK_LAUNCH("pet_sfwd", st,
+                   (pet_sfwd_kernel<T><<<L.nfwd, kRays * 32, 0, st>>>(
+                       rptr, ridx, rval, y, lam, d, p, L.ratio, L.llpart, L.counter + 1, red,
+                       err)));
+        MMK_CHECK_LAUNCH("pet_sfwd_kernel");
+        MMK_LAUNCH("pet_sback", st,
+                   (pet_sback_kernel<T><<<ceil_div(p, 256), 256, 0, st>>>(cptr, cidx, cval, p,
+                                                                          L.ratio, red)));
+        MMK_CHECK_LAUNCH("pet_sback_kernel");
+    } else {
+        cudaMemsetAsync(red, 0, sizeof(double) * (size_t)(p + 1), st);
+        MMK_CHECK_LAUNCH("pet_sparse_a memset");
+    }
+    return MMK_OK;
+}
+
 }  // namespace
 
 extern "C" int mmk_pet_ws_bytes(int dtype, int64_t d, int64_t p, size_t* out) {
@@ -387,6 +506,56 @@ extern "C" int mmk_pet_iter(int dtype, const void* E, int64_t lde, const void* y
                             size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                             void* stream) {
     int rc = mmk_pet_iter_a(dtype, E, lde, y, lam, d, p, ws, ws_bytes, red, err_dev, stream);
+    if (rc) return rc;
+    return mmk_pet_iter_b(dtype, lam, lam_out, p, nbr_ptr, nbr_idx, mu, flags, red, ws, ws_bytes,
+                          f_dev, err_dev, stream);
+}
+
+extern "C" int mmk_pet_sparse_ws_bytes(int dtype, int64_t d, int64_t p, size_t* out) {
+    (void)dtype;
+    const size_t a = sparse_ws_layout(d, p, nullptr, nullptr);
+    const size_t b = pet_ws_layout(0, p, nullptr, nullptr);   // phase B needs
+    *out = a > b ? a : b;
+    return MMK_OK;
+}
+
+extern "C" int mmk_pet_sparse_iter_a(int dtype, const int32_t* rptr, const int32_t* ridx,
+                                     const void* rval, const int32_t* cptr, const int32_t* cidx,
+                                     const void* cval, const void* y, const void* lam, int64_t d,
+                                     int64_t p, void* ws, size_t ws_bytes, double* red,
+                                     int64_t* err_dev, void* stream) {
+    if (p < 1 || d < 0) {
+        mmk_host::set_error("bad sparse PET shape d=%lld p=%lld", (long long)d, (long long)p);
+        return MMK_E_SHAPE;
+    }
+    const size_t need = sparse_ws_layout(d, p, nullptr, nullptr);
+    if (ws_bytes < need) {
+        mmk_host::set_error("sparse PET workspace too small: %zu < %zu", ws_bytes, need);
+        return MMK_E_SHAPE;
+    }
+    SparseWs L;
+    sparse_ws_layout(d, p, ws, &L);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == MMK_F32)
+        return pet_sparse_a<float>(rptr, ridx, (const float*)rval, cptr, cidx, (const float*)cval,
+                                   (const float*)y, (const float*)lam, d, p, L, red, err_dev, st);
+    if (dtype == MMK_F64)
+        return pet_sparse_a<double>(rptr, ridx, (const double*)rval, cptr, cidx,
+                                    (const double*)cval, (const double*)y, (const double*)lam, d, p,
+                                    L, red, err_dev, st);
+    mmk_host::set_error("unknown dtype %d", dtype);
+    return MMK_E_SHAPE;
+}
+
+extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t* ridx,
+                                   const void* rval, const int32_t* cptr, const int32_t* cidx,
+                                   const void* cval, const void* y, const void* lam,
+                                   void* lam_out, int64_t d, int64_t p, const int32_t* nbr_ptr,
+                                   const int32_t* nbr_idx, double mu, int flags, void* ws,
+                                   size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
+                                   void* stream) {
+    int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lam, d, p, ws,
+                                   ws_bytes, red, err_dev, stream);
     if (rc) return rc;
     return mmk_pet_iter_b(dtype, lam, lam_out, p, nbr_ptr, nbr_idx, mu, flags, red, ws, ws_bytes,
                           f_dev, err_dev, stream);

@@ -125,13 +125,13 @@ class PetProblem:
         kernels back-project from E directly)."""
         return self.e.T
 
-    def device_arrays(self, backend, torch):
-        key = (str(backend.torch_device()), backend.dtype)
+    def device_arrays(self, backend, torch, dense=True):
+        key = (str(backend.torch_device()), backend.dtype, dense)
         d = self._dev.get(key)
         if d is None:
             dev = backend.torch_device()
             d = {
-                "e": A.to_device(self.e, backend, torch),
+                "e": A.to_device(self.e, backend, torch) if dense else None,
                 "y": A.to_device(self.y, backend, torch),
                 "ptr": torch.from_numpy(self.nbr_indptr.astype(np.int32)).to(dev),
                 "idx": torch.from_numpy(self.nbr_indices.astype(np.int32)).to(dev),
@@ -142,6 +142,36 @@ class PetProblem:
         return d
 
 
+SPARSE_DENSITY = 0.25   # Backend(pet_kernel="auto") switches to CSR/CSC below this
+
+
+def _use_sparse(problem, backend):
+    if backend.pet_kernel != "auto":
+        return backend.pet_kernel == "sparse"
+    if A.is_torch(problem.e):
+        return False
+    return np.count_nonzero(problem.e) < SPARSE_DENSITY * problem.e.size
+
+
+def _sparse_arrays(e_rows, backend, torch):
+    """CSR (by ray) and CSC (by pixel) of a host E block, on the device."""
+    import scipy.sparse as sp
+    dev, dt = backend.torch_device(), backend.torch_dtype()
+    csr = sp.csr_matrix(e_rows)
+    csc = csr.tocsc()
+    if csr.nnz >= 2 ** 31:
+        raise ShapeError("system matrix has too many nonzeros for int32 indices")
+
+    def put(a, dtype):
+        a = np.ascontiguousarray(a)
+        if a.size == 0:
+            a = np.zeros(1, dtype=a.dtype)
+        return torch.from_numpy(a.astype(dtype)).to(dev)
+    return {"rptr": put(csr.indptr, np.int32), "ridx": put(csr.indices, np.int32),
+            "rval": put(csr.data, np.float64).to(dt), "cptr": put(csc.indptr, np.int32),
+            "cidx": put(csc.indices, np.int32), "cval": put(csc.data, np.float64).to(dt)}
+
+
 class _GpuPet(DeviceMm):
     direction = "maximize"
 
@@ -149,14 +179,25 @@ class _GpuPet(DeviceMm):
         super().__init__(backend)
         torch = self.torch
         self.problem = problem
-        d = problem.device_arrays(backend, torch)
+        self.sparse = _use_sparse(problem, backend)
+        lo, hi = rows if rows is not None else (0, problem.n_rays)   # ray shard
+        if self.sparse:
+            key = (str(backend.torch_device()), backend.dtype, "sparse", lo, hi)
+            sa = problem._dev.get(key)
+            if sa is None:
+                e = problem.e if not A.is_torch(problem.e) else problem.e.cpu().numpy()
+                sa = _sparse_arrays(np.asarray(e, dtype=np.float64)[lo:hi], backend, torch)
+                problem._dev[key] = sa
+            self.sa = sa
+        d = problem.device_arrays(backend, torch, dense=not self.sparse)
         self.e, self.y, self.ptr, self.idx = d["e"], d["y"], d["ptr"], d["idx"]
-        if rows is not None:          # ray shard [lo, hi) of a distributed run
-            lo, hi = rows
-            self.e, self.y = self.e[lo:hi], self.y[lo:hi]
-        self.d, self.p = self.e.shape
+        self.y = self.y[lo:hi]
+        if self.e is not None:
+            self.e = self.e[lo:hi]
+        self.d, self.p = hi - lo, problem.n_pixels
         self.mu = float(problem.mu)
-        self.ws = torch.zeros(_lib.ws_bytes("mmk_pet_ws_bytes", self.code, max(self.d, 1), self.p),
+        name = "mmk_pet_sparse_ws_bytes" if self.sparse else "mmk_pet_ws_bytes"
+        self.ws = torch.zeros(_lib.ws_bytes(name, self.code, max(self.d, 1), self.p),
                               dtype=torch.uint8, device=self.device)
         self.red = torch.zeros(_lib.load().mmk_pet_reduce_len(self.p), dtype=torch.float64,
                                device=self.device)
@@ -171,12 +212,21 @@ class _GpuPet(DeviceMm):
         dst.copy_(src)
 
     def _bytes_per_iter(self):
+        if self.sparse:
+            return float(2 * self.sa["rval"].numel() * (self.sa["rval"].element_size() + 4))
         return float(self.d * self.p * self.e.element_size())
 
     def _messages(self):
         return _MSG
 
     def _iterate(self, lam, out, f_ptr, err_ptr, flags=_lib.MMK_PET_UPDATE | _lib.MMK_PET_OBJECTIVE):
+        if self.sparse:
+            sa, P = self.sa, _lib.ptr
+            _lib.call("mmk_pet_sparse_iter", self.code, P(sa["rptr"]), P(sa["ridx"]),
+                      P(sa["rval"]), P(sa["cptr"]), P(sa["cidx"]), P(sa["cval"]), P(self.y),
+                      P(lam), P(out), self.d, self.p, P(self.ptr), P(self.idx), self.mu, flags,
+                      P(self.ws), self.ws.numel(), P(self.red), f_ptr, err_ptr, self.stream())
+            return
         _lib.call("mmk_pet_iter", self.code, _lib.ptr(self.e), self.e.stride(0), _lib.ptr(self.y),
                   _lib.ptr(lam), _lib.ptr(out), self.d, self.p, _lib.ptr(self.ptr),
                   _lib.ptr(self.idx), self.mu, flags, _lib.ptr(self.ws), self.ws.numel(),
@@ -184,6 +234,14 @@ class _GpuPet(DeviceMm):
 
     def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
         self._keep = (a, b)
+        if self.sparse:
+            sa, P = self.sa, _lib.ptr
+            _lib.call("mmk_pet_sparse_engine_create", self.code, P(sa["rptr"]), P(sa["ridx"]),
+                      P(sa["rval"]), P(sa["cptr"]), P(sa["cidx"]), P(sa["cval"]), P(self.y),
+                      P(a), P(b), self.d, self.p, P(self.ptr), P(self.idx), self.mu, P(self.ws),
+                      self.ws.numel(), P(self.red), self.comm, ctypes.byref(rule), P(trace),
+                      P(stamp), P(ctl), self.status.err_ptr, ctypes.byref(eng))
+            return
         _lib.call("mmk_pet_engine_create", self.code, _lib.ptr(self.e), self.e.stride(0),
                   _lib.ptr(self.y), _lib.ptr(a), _lib.ptr(b), self.d, self.p, _lib.ptr(self.ptr),
                   _lib.ptr(self.idx), self.mu, _lib.ptr(self.ws), self.ws.numel(),
@@ -242,6 +300,8 @@ class _LooseProblem:
         self.nbr_indices = np.zeros(0, dtype=np.int64)
 
     device_arrays = PetProblem.device_arrays
+    n_pixels = PetProblem.n_pixels
+    n_rays = PetProblem.n_rays
 
 
 def pet_update(lam, problem, backend=SERIAL, mean_counts=None):

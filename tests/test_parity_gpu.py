@@ -153,7 +153,7 @@ def test_pet_c2_1000_iters(mu, dtype):
     prob = M.PetProblem(e=e, y=y, mu=mu, neighborhoods=nbrs)
     cfg = FIXED if dtype == "fp64" else MmConfig(max_iters=1000, epsilon=1e-300,
                                                  monotone_tol=1e-6)
-    lam, tr = M.pet_run(prob, cfg, Backend(dtype=dtype))
+    lam, tr = M.pet_run(prob, cfg, Backend(dtype=dtype, pet_kernel="dense"))
     tol = TOL[dtype]
     assert trace_err(tr.objective_values, g[f"trace_{mu:g}"]) <= tol
     assert G.rel(lam, g[f"lam_{mu:g}"]) <= tol
@@ -359,3 +359,23 @@ def test_run_to_run_bitwise_determinism():
     a, ta = M.mds_run(prob, cfg, FP32, theta0=theta0)
     b, tb = M.mds_run(prob, cfg, FP32, theta0=theta0)
     assert np.array_equal(a, b) and np.array_equal(ta.objective_values, tb.objective_values)
+
+
+# ----------------------------------------------------------------------------- sparse PET
+@pytest.mark.parametrize("mu", [0.0, 1e-5])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_pet_c2_sparse_projector(mu, dtype):
+    """CSR/CSC projector against the same golden traces as
+    the dense path (BASELINE config 2, 1000 iterations)."""
+    g = G.load("pet_c2")
+    e, y, nbrs = G.c2_inputs()
+    prob = M.PetProblem(e=e, y=y, mu=mu, neighborhoods=nbrs)
+    cfg = FIXED if dtype == "fp64" else MmConfig(max_iters=1000, epsilon=1e-300,
+                                                 monotone_tol=1e-6)
+    be = Backend(dtype=dtype, pet_kernel="sparse")
+    lam, tr = M.pet_run(prob, cfg, be)
+    tol = TOL[dtype]
+    assert trace_err(tr.objective_values, g[f"trace_{mu:g}"]) <= tol
+    assert G.rel(lam, g[f"lam_{mu:g}"]) <= tol
+    # the auto switch picks the sparse kernels for the ~1 % dense Siddon matrix
+    assert M.pet._use_sparse(prob, Backend(dtype=dtype))
