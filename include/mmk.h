@@ -167,6 +167,14 @@ int mmk_pet_sparse_iter(int dtype, const int32_t *rptr, const int32_t *ridx, con
                         void *ws, size_t ws_bytes, double *red, double *f_dev, int64_t *err_dev,
                         void *stream);
 
+/* Siddon system matrix on the device (pet.py:69-132): detector positions
+ * det (n_det x 2 fp64, detector_positions()), grid lines (side + 1 fp64,
+ * np.linspace(-1, 1, side + 1)); one row per detector pair in the
+ * reference's loop order, written as ELL: idx / val [n_rays][cap] (cap >=
+ * 2 side + 3), cnt[n_rays].  Unnormalised chord lengths. */
+int mmk_pet_siddon(const double *det, int n_det, int side, const double *lines, int cap,
+                   int *idx, double *val, int *cnt, void *stream);
+
 /* ------------------------------------------------------------------------
  * MDS stress majorization, full-row tiling.  theta is dim x n (SoA: row k =
  * coordinate k of every point).  Y/Wt point at row `row0` of the n x n

@@ -22,7 +22,7 @@ from .mds import (MdsProblem, PackedMdsProblem, anchor_configuration, mds_run, m
 from .nnmf import (FactorPair, NnmfProblem, nnmf_gradient, nnmf_objective,
                    nnmf_poisson_objective, nnmf_poisson_run, nnmf_poisson_update, nnmf_run,
                    nnmf_surrogate, nnmf_update_v, nnmf_update_w)
-from .pet import (PetProblem, pet_loglik, pet_penalized_gradient, pet_penalized_objective,
+from .pet import (PetProblem, SparsePetProblem, pet_loglik, system_matrix_device, pet_penalized_gradient, pet_penalized_objective,
                   pet_run, pet_surrogate, pet_update)
 
 __version__ = "0.1.0"

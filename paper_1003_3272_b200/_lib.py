@@ -70,6 +70,7 @@ _SIGS = {
     "mmk_pet_sparse_engine_create": ([_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                                       _i64, _vp, _vp, _dbl, _vp, _sz, _vp, _vp, _vp, _vp, _vp,
                                       _vp, _vp, _vp], _i32),
+    "mmk_pet_siddon": ([_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp], _i32),
     "mmk_mds_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_mds_iter": ([_i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i32,
                       _vp, _sz, _vp, _vp, _vp], _i32),

@@ -29,9 +29,9 @@ from .backend import SERIAL
 from .datasets import (PetGeometry, build_neighborhoods, build_system_matrix,  # noqa: F401
                        default_phantom, simulate_counts)
 from .driver import run_mm
-from .errors import DomainError, NumericsError, ShapeError
+from .errors import DomainError, InputError, NumericsError, ShapeError
 
-__all__ = ["PetGeometry", "PetProblem", "build_system_matrix", "build_neighborhoods",
+__all__ = ["PetGeometry", "PetProblem", "SparsePetProblem", "system_matrix_device", "build_system_matrix", "build_neighborhoods",
            "simulate_counts", "default_phantom", "pet_loglik", "pet_penalized_objective",
            "pet_penalized_gradient", "pet_update", "pet_run", "pet_surrogate"]
 
@@ -145,7 +145,110 @@ class PetProblem:
 SPARSE_DENSITY = 0.25   # Backend(pet_kernel="auto") switches to CSR/CSC below this
 
 
+def system_matrix_device(geometry, backend=SERIAL):
+    """The Siddon system matrix of ``geometry`` built on the GPU
+    (``csrc/pet_siddon.cu``; the reference's Python loop is pet.py:69-132),
+    columns scaled to unit l1 norm, as device CSR (by ray) and CSC (by pixel)
+    arrays in fp64: {rptr, ridx, rval, cptr, cidx, cval, n_rays, n_pixels}.
+    Raises the reference's DomainError for a pixel no ray crosses."""
+    from .datasets import PetGeometry
+    if not isinstance(geometry, PetGeometry):
+        raise InputError("system_matrix_device needs a PetGeometry")
+    torch = _lib.torch_mod()
+    dev = backend.torch_device()
+    side, nd = geometry.grid_side, geometry.n_detectors
+    nr, npx = geometry.n_rays, geometry.n_pixels
+    det = torch.from_numpy(np.ascontiguousarray(geometry.detector_positions())).to(dev)
+    lines = torch.from_numpy(np.linspace(-1.0, 1.0, side + 1)).to(dev)
+    cap = 2 * side + 3
+    idx = torch.empty((nr, cap), dtype=torch.int32, device=dev)
+    val = torch.empty((nr, cap), dtype=torch.float64, device=dev)
+    cnt = torch.empty(nr, dtype=torch.int32, device=dev)
+    _lib.call("mmk_pet_siddon", _lib.ptr(det), nd, side, _lib.ptr(lines), cap, _lib.ptr(idx),
+              _lib.ptr(val), _lib.ptr(cnt), _lib.stream_handle(torch, dev))
+    keep = torch.arange(cap, device=dev)[None, :] < cnt[:, None]
+    ridx = idx[keep]
+    rval = val[keep]
+    rows = torch.arange(nr, device=dev, dtype=torch.int32)[:, None].expand(nr, cap)[keep]
+    # canonical CSR: pixels ascending within each ray (rays emit in path order)
+    key = rows.to(torch.int64) * npx + ridx.to(torch.int64)
+    srt = torch.sort(key).indices
+    ridx, rval, rows = ridx[srt], rval[srt], rows[srt]
+    rptr = torch.zeros(nr + 1, dtype=torch.int64, device=dev)
+    rptr[1:] = torch.cumsum(cnt.to(torch.int64), 0)
+    order = torch.sort(ridx, stable=True).indices      # by pixel, ray order kept
+    cidx = rows[order]
+    cval = rval[order]
+    ccnt = torch.bincount(ridx.to(torch.int64), minlength=npx)
+    cptr = torch.zeros(npx + 1, dtype=torch.int64, device=dev)
+    cptr[1:] = torch.cumsum(ccnt, 0)
+    col = torch.zeros(npx, dtype=torch.float64, device=dev)
+    col.index_add_(0, ridx.to(torch.int64), rval)
+    empty = torch.nonzero(col == 0.0)
+    if empty.numel():
+        raise DomainError(f"pixel {int(empty[0, 0])} is intersected by no ray; its intensity "
+                          "is unidentifiable (add detectors or shrink the grid)")
+    rval = rval / col[ridx.to(torch.int64)]
+    cval = cval / col[torch.repeat_interleave(torch.arange(npx, device=dev), ccnt)]
+    i32 = torch.int32
+    return {"rptr": rptr.to(i32), "ridx": ridx, "rval": rval, "cptr": cptr.to(i32),
+            "cidx": cidx, "cval": cval, "n_rays": nr, "n_pixels": npx}
+
+
+class SparsePetProblem:
+    """A PET problem whose system matrix lives on the GPU in sparse form --
+    built by ``system_matrix_device`` for geometries whose dense matrix would
+    not fit host memory (a 256 x 256 image with 256 detectors is 32,640 x
+    65,536: 17 GB dense in fp64, ~100 MB as CSR + CSC).  Same solver
+    semantics as ``PetProblem`` (pet.py:213-285); counts y and the penalty
+    lattice as there."""
+
+    def __init__(self, sparse, y, mu, neighborhoods):
+        self.sa = sparse
+        self.y = y if A.is_torch(y) else np.asarray(y, dtype=np.float64)
+        if tuple(A.shape_of(self.y)) != (sparse["n_rays"],):
+            raise ShapeError(f"counts shape {tuple(A.shape_of(self.y))} does not match "
+                             f"{sparse['n_rays']} rays")
+        if A.min_value(self.y) < 0.0:
+            raise DomainError("counts must be nonnegative")
+        if mu < 0.0:
+            raise DomainError(f"penalty constant must be >= 0, got {mu}")
+        self.mu = float(mu)
+        p = sparse["n_pixels"]
+        if len(neighborhoods) != p:
+            raise ShapeError(f"{len(neighborhoods)} neighborhoods for {p} pixels")
+        indptr = np.zeros(p + 1, dtype=np.int64)
+        indptr[1:] = np.cumsum([len(a) for a in neighborhoods])
+        self.nbr_indptr = indptr
+        self.nbr_indices = np.fromiter((k for a in neighborhoods for k in a), dtype=np.int64,
+                                       count=int(indptr[-1]))
+        self.e = None
+        self._dev = {}
+
+    @property
+    def n_pixels(self):
+        return self.sa["n_pixels"]
+
+    @property
+    def n_rays(self):
+        return self.sa["n_rays"]
+
+    def forward(self, lam):
+        """E lam (fp64) on the device -- e.g. for simulating counts."""
+        torch = _lib.torch_mod()
+        sa = self.sa
+        e = torch.sparse_csr_tensor(sa["rptr"].to(torch.int64), sa["ridx"].to(torch.int64),
+                                    sa["rval"], (sa["n_rays"], sa["n_pixels"]),
+                                    check_invariants=True)
+        lam_t = lam if A.is_torch(lam) else torch.from_numpy(np.asarray(lam, dtype=np.float64))
+        return (e @ lam_t.to(sa["rval"].device, torch.float64)[:, None])[:, 0]
+
+    device_arrays = PetProblem.device_arrays
+
+
 def _use_sparse(problem, backend):
+    if isinstance(problem, SparsePetProblem):
+        return True
     if backend.pet_kernel != "auto":
         return backend.pet_kernel == "sparse"
     if A.is_torch(problem.e):
@@ -185,8 +288,17 @@ class _GpuPet(DeviceMm):
             key = (str(backend.torch_device()), backend.dtype, "sparse", lo, hi)
             sa = problem._dev.get(key)
             if sa is None:
-                e = problem.e if not A.is_torch(problem.e) else problem.e.cpu().numpy()
-                sa = _sparse_arrays(np.asarray(e, dtype=np.float64)[lo:hi], backend, torch)
+                if isinstance(problem, SparsePetProblem):
+                    if (lo, hi) != (0, problem.n_rays):
+                        raise ShapeError("ray shards of a device-built system matrix are "
+                                         "not supported")
+                    dt = backend.torch_dtype()
+                    sa = {k: (v.to(dt) if k in ("rval", "cval") else v)
+                          for k, v in problem.sa.items() if k in ("rptr", "ridx", "rval",
+                                                                  "cptr", "cidx", "cval")}
+                else:
+                    e = problem.e if not A.is_torch(problem.e) else problem.e.cpu().numpy()
+                    sa = _sparse_arrays(np.asarray(e, dtype=np.float64)[lo:hi], backend, torch)
                 problem._dev[key] = sa
             self.sa = sa
         d = problem.device_arrays(backend, torch, dense=not self.sparse)

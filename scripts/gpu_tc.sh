@@ -1,3 +1,2 @@
 python -c "from paper_1003_3272_b200 import build; build.build()"
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -15
-python scripts/suite_probe.py 2>&1 | grep -A4 pet
+timeout 600 python bench.py --workload pet-large --steps 50 --warmup 3 --no-suite --cpu-seconds 5 2>&1 | tail -c 2500
