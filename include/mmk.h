@@ -217,6 +217,16 @@ int mmk_mds_iter(int dtype, const void *Y, const void *Wt, int64_t ldy, const do
  *   iter_b : theta_out = MM update from red, f_dev = stress.
  * Coupled coincident points set NUMERICS with index i*n + j (site 1).
  * ---------------------------------------------------------------------- */
+/* Roll-call votes (q x m, entries 1 / -1 / 0, fp32 or fp64 `dtype`) straight
+ * into packed-triangle fp32 dissimilarity tiles [t0, t1) on the tensor cores
+ * (votes_to_dissimilarity, mds.py:260-283: D = (S - N) / (2 S) with S = P P^T,
+ * N = V V^T, exact in fp16 x fp16 -> fp32).  ws >= mmk_mds_votes_bytes.
+ * DOMAIN errors: site 6 bad vote entry (index i*m + k), site 7 a pair sharing
+ * no roll call (index i*q + j, i < j). */
+int mmk_mds_votes_bytes(int64_t q, int64_t m, size_t *out);
+int mmk_mds_votes_tri(int dtype, const void *votes, int64_t q, int64_t m, float *packed,
+                      int64_t t0, int64_t t1, void *ws, size_t ws_bytes, int64_t *err_dev,
+                      void *stream);
 int64_t mmk_mds_tri_ntiles(int64_t n);
 int64_t mmk_mds_tri_reduce_len(int64_t n, int64_t dim);
 int mmk_mds_tri_ws_bytes(int64_t n, int64_t dim, int64_t t0, int64_t t1, size_t *out);

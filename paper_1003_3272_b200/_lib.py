@@ -75,6 +75,8 @@ _SIGS = {
     "mmk_mds_iter": ([_i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i32,
                       _vp, _sz, _vp, _vp, _vp], _i32),
     "mmk_mds_unpack": ([_i32, _vp, _vp, _i64, _i64, _i64, _vp], _i32),
+    "mmk_mds_votes_bytes": ([_i64, _i64, _c.POINTER(_sz)], _i32),
+    "mmk_mds_votes_tri": ([_i32, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _sz, _vp, _vp], _i32),
     "mmk_mds_tri_ntiles": ([_i64], _i64),
     "mmk_mds_tri_reduce_len": ([_i64, _i64], _i64),
     "mmk_mds_tri_ws_bytes": ([_i64, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),

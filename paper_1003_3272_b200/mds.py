@@ -180,6 +180,41 @@ class PackedMdsProblem:
         return cls(packed, n, p, (t0, t1), dev)
 
     @classmethod
+    def from_votes(cls, votes, p, backend=SERIAL, tiles=None):
+        """Dissimilarities of a q x m roll-call matrix (1 yea, -1 nay, 0
+        absent) computed on the tensor cores straight into the packed tiles
+        (``csrc/mds_votes.cu``; reference votes_to_dissimilarity,
+        mds.py:260-283) -- no q x q matrix on the host or the device."""
+        torch = _lib.torch_mod()
+        dev = backend.torch_device()
+        shp = tuple(A.shape_of(votes))
+        if len(shp) != 2:
+            raise ShapeError(f"vote matrix must be 2-D, got {shp}")
+        q, m = shp
+        vt = votes if A.is_torch(votes) else torch.from_numpy(np.ascontiguousarray(votes))
+        if vt.dtype not in (torch.float32, torch.float64):
+            vt = vt.to(torch.float64)
+        vt = vt.to(dev).contiguous()
+        t0, t1 = tiles if tiles is not None else (0, tile_count(q))
+        packed = torch.empty((t1 - t0) * TILE * TILE, dtype=torch.float32, device=dev)
+        ws = torch.empty(_lib.ws_bytes("mmk_mds_votes_bytes", q, m), dtype=torch.uint8,
+                         device=dev)
+        status = _lib.StatusBlock(torch, dev)
+        status.clear_error()
+        _lib.call("mmk_mds_votes_tri", _lib.dtype_code(vt.dtype), _lib.ptr(vt), q, m,
+                  _lib.ptr(packed), t0, t1, _lib.ptr(ws), ws.numel(), status.err_ptr,
+                  _lib.stream_handle(torch, dev))
+        _, code, idx = status.read()
+
+        def pair(i):
+            a, b = divmod(i, q)
+            return (f"voters {a} and {b} share no roll call; their dissimilarity "
+                    "is undefined")
+        _lib.raise_device_error(code, idx, {
+            6: lambda i: "votes must be 1 (yea), -1 (nay) or 0 (absent)", 7: pair})
+        return cls(packed, q, p, (t0, t1), dev)
+
+    @classmethod
     def from_dense(cls, y, p, backend=SERIAL, tiles=None, validate=True):
         """Full n x n dissimilarities (numpy or torch), checked on the device
         for finiteness, sign, zero diagonal and exact symmetry."""

@@ -1,2 +1,2 @@
 python -c "from paper_1003_3272_b200 import build; build.build()"
-timeout 600 python bench.py --workload pet-large --steps 50 --warmup 3 --no-suite --cpu-seconds 5 2>&1 | tail -c 2500
+timeout 900 python -m pytest tests/test_mds_tri_gpu.py -x -q -p no:cacheprovider -k votes 2>&1 | tail -30

@@ -217,3 +217,30 @@ def test_c5_full_shape_properties():
                                                                        device="cuda")[:, None]
         s += float((((yb - d) ** 2) * mask).sum())
     assert abs(v[0] - s) / s <= 1e-5
+
+
+@pytest.mark.parametrize("q,m", [(401, 671), (300, 57), (1000, 130)])
+def test_votes_to_packed_tiles_match_reference(q, m):
+    """Roll calls -> packed dissimilarity tiles on the tensor cores equal the
+    fp32 rounding of the reference's votes_to_dissimilarity bit for bit."""
+    votes = M.datasets.synthetic_votes(q, m, q + m)
+    want = PackedMdsProblem.from_dense(G.f32(M.votes_to_dissimilarity(votes)), 2, TRI,
+                                       validate=False)
+    got = PackedMdsProblem.from_votes(votes, 2, TRI)
+    import torch
+    assert torch.equal(got.packed, want.packed)
+    half = PackedMdsProblem.from_votes(votes.astype(np.float32), 2, TRI,
+                                       tiles=tile_range(tile_count(q), 2, 1))
+    assert torch.equal(half.packed, want.packed[half.t0 * 16384:half.t1 * 16384])
+
+
+def test_votes_errors():
+    v = M.datasets.synthetic_votes(200, 40, 1)
+    v[3, 5] = 2.0
+    with pytest.raises(M.DomainError, match="votes must be 1"):
+        PackedMdsProblem.from_votes(v, 2, TRI)
+    v = M.datasets.synthetic_votes(200, 40, 1)
+    v[7, :20] = 0.0
+    v[150, 20:] = 0.0
+    with pytest.raises(M.DomainError, match="voters 7 and 150 share no roll call"):
+        PackedMdsProblem.from_votes(v, 2, TRI)
