@@ -335,7 +335,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const uint32_t tmem = tmem_base;
     const float xscale = exp2f((float)sc->ex);
     const double qscale = exp2(-(double)(sc->ex + sc->ew));
-    double acc = 0.0;
+    double acc = 0.0, gacc = 0.0;
     float vmax = 0.f;
     auto tile_of = [&](int p, int j) { return (int)blockIdx.x + (p * TMAX + j) * (int)gridDim.x; };
     auto pass_of = [&](int p) {
@@ -372,6 +372,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     const double vk = (double)va[i];
                     const double qk = ((double)q[4 * k4 + i] + (double)q2[4 * k4 + i]) * qscale;
                     acc = fma(vk, qk, acc);
+                    gacc = fma(vk, (double)da[i], gacc);   // <V, V G_W> = <V^T V, G_W>
                     nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
                     vmax = fmaxf(vmax, nv[i]);
                 }
@@ -380,24 +381,29 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         }
     };
     run_pipeline<false>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue, tr);
-    // per-CTA partial <V, Q> and max(V') (epilogue warps)
+    // per-CTA partials <V, Q>, <V, V G_W> and max(V') (epilogue warps)
+    __shared__ double gred[kThreads / 32];
     acc = warp_sum(acc);
+    gacc = warp_sum(gacc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     if (lane == 0) {
         red[warp] = acc;
+        gred[warp] = gacc;
         vmx[warp] = vmax;
     }
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        double c = 0.0;
+        double c = 0.0, gg = 0.0;
         float mx = 0.f;
         for (int w = 2 + NCONV; w < kThreads / 32; ++w) {
             c += red[w];
+            gg += gred[w];
             mx = fmaxf(mx, vmx[w]);
         }
         part[blockIdx.x] = c;
+        part[gridDim.x + blockIdx.x] = gg;
         atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
     }
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
@@ -549,6 +555,7 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
 // 7.3-1: Gram-side products in fp32 keep raw V within 5e-6 of fp64).  A block
 // computes 64 rows x 64 columns with 4 x 4 register tiles per thread.
 constexpr int VGW_SMEM = 2 * R * (64 + 4) * 4;
+constexpr int VGW_CHUNKS = 4;   // 64-row chunks per block (amortise the G_W load)
 __global__ void __launch_bounds__(256)
 vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __restrict__ DEN,
            long long m) {
@@ -556,40 +563,44 @@ vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __
     float(*G)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem);
     float(*Vt)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem + R * (64 + 4));
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const long long r0 = (long long)blockIdx.x * 64;
     for (int i = threadIdx.x; i < R * R; i += 256) G[i / R][i % R] = (float)GW[i];
-    for (int i = threadIdx.x; i < 16 * R; i += 256) {
-        const int rr = i / 16, l4 = (i % 16) * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + l4);
-        Vt[l4][rr] = v.x;
-        Vt[l4 + 1][rr] = v.y;
-        Vt[l4 + 2][rr] = v.z;
-        Vt[l4 + 3][rr] = v.w;
-    }
-    __syncthreads();
-    float acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 8
-    for (int l = 0; l < R; ++l) {
-        const float4 a = *reinterpret_cast<const float4*>(&Vt[l][4 * ty]);
-        const float4 b = *reinterpret_cast<const float4*>(&G[l][4 * tx]);
-        const float av[4] = {a.x, a.y, a.z, a.w};
-        const float bv[4] = {b.x, b.y, b.z, b.w};
+    for (int ch = 0; ch < VGW_CHUNKS; ++ch) {
+        const long long r0 = ((long long)blockIdx.x * VGW_CHUNKS + ch) * 64;
+        if (r0 >= m) break;
+        __syncthreads();   // G ready / previous chunk's Vt consumed
+        for (int i = threadIdx.x; i < 16 * R; i += 256) {
+            const int rr = i / 16, l4 = (i % 16) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + l4);
+            Vt[l4][rr] = v.x;
+            Vt[l4 + 1][rr] = v.y;
+            Vt[l4 + 2][rr] = v.z;
+            Vt[l4 + 3][rr] = v.w;
+        }
+        __syncthreads();
+        float acc[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 8
+        for (int l = 0; l < R; ++l) {
+            const float4 a = *reinterpret_cast<const float4*>(&Vt[l][4 * ty]);
+            const float4 b = *reinterpret_cast<const float4*>(&G[l][4 * tx]);
+            const float av[4] = {a.x, a.y, a.z, a.w};
+            const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const long long row = r0 + 4 * ty + i;
-        if (row < m)
-            *reinterpret_cast<float4*>(DEN + row * R + 4 * tx) =
-                make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const long long row = r0 + 4 * ty + i;
+            if (row < m)
+                *reinterpret_cast<float4*>(DEN + row * R + 4 * tx) =
+                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        }
     }
 }
 
@@ -802,15 +813,17 @@ wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
     }
 }
 
-// f-partial = sum x^2 - 2 <V, Q> + <G_V, G_W> (all over this rank's rows)
+// f-partial = sum x^2 - 2 <V, Q> + <G_V, G_W> (all over this rank's rows);
+// <G_V, G_W> = sum_i v_i . (v_i G_W) comes from the V-step epilogue, which
+// holds V and DEN = V G_W row by row (no Gram of the old V needed)
 __global__ void tc_objective_kernel(const double* __restrict__ part, int nparts,
-                                    const XXCache* __restrict__ cache,
-                                    const double* __restrict__ GV, const double* __restrict__ GW,
-                                    double* __restrict__ out) {
+                                    const XXCache* __restrict__ cache, double* __restrict__ out) {
     __shared__ double sc[32];
     double cr = 0.0, gg = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) cr += part[i];
-    for (int i = threadIdx.x; i < R * R; i += blockDim.x) gg = fma(GV[i], GW[i], gg);
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+        cr += part[i];
+        gg += part[nparts + i];
+    }
     cr = block_sum(cr, sc);
     gg = block_sum(gg, sc);
     if (threadIdx.x == 0) *out = cache->xx - 2.0 * cr + gg;
@@ -980,16 +993,16 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
     gram32(W, n, true, L.gpart, GW, st);
-    gram32(V, m, false, L.gpart, L.GVn, st);
     MMK_LAUNCH("nnmf_vgw",
-               st, (vgw_kernel<<<ceil_div(m, 64), 256, VGW_SMEM, st>>>(V, GW, L.DEN, m)));
+               st, (vgw_kernel<<<ceil_div(m, 64 * VGW_CHUNKS), 256, VGW_SMEM, st>>>(V, GW, L.DEN,
+                                                                                m)));
     MMK_LAUNCH("nnmf_vstep_tc", st,
                (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, L.DEN, V_out, L.sc,
                                                                 (int)m, (int)n, L.part,
                                                                 g_trace_v)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
-               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx, L.GVn, GW,
+               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx,
                                                         red + rn + (long long)R * R)));
     gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
