@@ -157,3 +157,81 @@ def tri_phase_b_model(theta, red):
     s = red[n * dim + 1:n * dim + 1 + dim]
     w = n - 1.0
     return (theta * (w - 1.0) + s[:, None] - c) / (2.0 * w), red[n * dim]
+
+
+# ---------------------------------------------------------------------------
+# Public sharded solvers (one process per GPU, torch.distributed NCCL group).
+# Each iteration: phase A on this rank's rows / tiles, ONE all-reduce of the
+# fp64 reduction buffer (plus the device error record, so every rank raises
+# together), phase B redundantly on every rank; run_mm's per-iteration
+# protocol drives it (the objective is the all-reduced value).
+def _allreduce_status(status, group):
+    import torch.distributed as dist
+    rec = status.dev[1:3].clone()
+    code, idx = rec[0:1].clone(), rec[1:2].clone()
+    dist.all_reduce(code, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
+    status.dev[1:2].copy_(code)
+    status.dev[2:3].copy_(idx)
+
+
+def _make_sharded_nnmf(base_cls, iter_a, iter_b):
+    class _Sharded(base_cls):
+        def __init__(self, problem, backend, group):
+            super().__init__(problem, backend)
+            self.__dict__.pop("run_fused", None)     # per-iteration protocol
+            self.group = group
+
+        def _iterate(self, s, out, f_ptr, err_ptr):
+            from . import _lib as L
+            st = self.stream()
+            L.call(iter_a, self.code, L.ptr(self.x), self.x.stride(0), L.ptr(s.v), L.ptr(s.w),
+                   L.ptr(out.v), self.m, self.n, self.r, L.ptr(self.ws), self.ws.numel(),
+                   L.ptr(self.red), err_ptr, st)
+            allreduce_sum_(self.red, self.group)
+            _allreduce_status(self.status, self.group)
+            L.call(iter_b, self.code, L.ptr(s.w), L.ptr(out.w), self.n, self.r, L.ptr(self.red),
+                   f_ptr, err_ptr, st)
+    return _Sharded
+
+
+def nnmf_run_sharded(x_local, rank, config, backend, group=None, state0=None, poisson=False):
+    """Row-sharded NNMF (Frobenius, or the Poisson fit with ``poisson=True``):
+    this rank holds rows ``x_local`` of X (a CUDA tensor or array) and the
+    matching rows of V; W is replicated.  ``state0`` = (V_local, W) (required:
+    the ranks must agree on W and on the split of V).  Returns
+    (FactorPair(V_local, W), MmTrace); every rank gets the same trace."""
+    from . import nnmf as N
+    from .driver import run_mm
+    if state0 is None:
+        raise ValueError("nnmf_run_sharded needs state0 = (V_local, W)")
+    prob = N.NnmfProblem(x=x_local, rank=rank)
+    if poisson:
+        cls = _make_sharded_nnmf(N._GpuPoissonNnmf, "mmk_nnmf_poisson_iter_a",
+                                 "mmk_nnmf_poisson_iter_b")
+    else:
+        cls = _make_sharded_nnmf(N._GpuNnmf, "mmk_nnmf_iter_a", "mmk_nnmf_iter_b")
+    mm = cls(prob, backend, group)
+    state, trace = run_mm(mm, mm.device_state(N.FactorPair(state0[0], state0[1])), config)
+    return state, trace
+
+
+def mds_run_sharded(problem, config, backend, group=None, theta0=None):
+    """Tile-sharded packed-triangle MDS: ``problem`` is this rank's
+    ``PackedMdsProblem`` (tiles ``tile_range(ntiles, world, rank)``), theta is
+    replicated.  One all-reduce of the per-point accumulators per iteration;
+    every rank returns the same configuration and trace."""
+    from . import mds as D
+    from .driver import run_mm
+    if theta0 is None:
+        theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
+                                                            size=(problem.p, problem.q))
+    mm = D._GpuMdsTri(problem, backend, group=group)
+    mm.__dict__.pop("run_fused", None)
+    base_iter = mm._iterate
+
+    def _iterate(theta, out, f_ptr, err_ptr):
+        base_iter(theta, out, f_ptr, err_ptr)
+        _allreduce_status(mm.status, group)
+    mm._iterate = _iterate
+    return run_mm(mm, mm.device_state(theta0), config)
