@@ -603,14 +603,8 @@ struct RunA {
         if constexpr (std::is_same<T, float>::value && RMAX == 64) {
             if (a.mode == 0 && tc_shape(a.m, a.n, a.r) &&
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
-                auto gw = [&](const float* Wp, double* out, cudaStream_t s) {
-                    K<float, 64>::gram64(Wp, a.n, true, P.g64w_blocks, P.g64w_cpb, L, out, s);
-                };
-                auto gv = [&](const float* Vp, double* out, cudaStream_t s) {
-                    K<float, 64>::gram64(Vp, a.m, false, P.g64v_blocks, P.g64v_cpb, L, out, s);
-                };
                 return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
-                                      a.red, gw, gv, a.st);
+                                      a.red, a.st);
             }
         }
         if (a.mode == 0 || a.mode == 1 || a.mode == 2) {

@@ -957,9 +957,7 @@ size_t ws_bytes(long long m, long long n) { return tc_layout(m, n, nullptr, null
 // red = [P | G_V' | f-partial].
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
            long long m, long long n, void* tcws, double* GW, double* red,
-           const GramFn& gram_w, const GramFn& gram_v_into, cudaStream_t st) {
-    (void)gram_w;
-    (void)gram_v_into;
+           cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);

@@ -3,17 +3,12 @@
 
 #include <cuda_runtime.h>
 
-#include <functional>
-
 namespace mmk_tc {
-
-// (input matrix, fp64 r x r Gram output, stream)
-using GramFn = std::function<void(const float*, double*, cudaStream_t)>;
 
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X);
 size_t ws_bytes(long long m, long long n);
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
            long long m, long long n, void* tcws, double* GW, double* red,
-           const GramFn& gram_w, const GramFn& gram_v_into, cudaStream_t st);
+           cudaStream_t st);
 
 }  // namespace mmk_tc

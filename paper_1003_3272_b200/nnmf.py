@@ -77,6 +77,15 @@ class NnmfProblem:
     def shape(self):
         return tuple(self.x.shape)
 
+    @classmethod
+    def _unchecked(cls, x, rank):
+        """A problem around already-validated data (single-op entry points)."""
+        prob = cls.__new__(cls)
+        object.__setattr__(prob, "x", x)
+        object.__setattr__(prob, "rank", rank)
+        object.__setattr__(prob, "_dev", {})
+        return prob
+
     def device_x(self, backend, torch):
         key = (str(backend.torch_device()), backend.dtype)
         t = self._dev.get(key)
@@ -291,11 +300,7 @@ class _GpuPoissonNnmf(_GpuNnmf):
 def _poisson_pass(x, v, w, backend):
     """One fused device pass: (f(V, W), V', W') as device tensors."""
     m, n, r = _conform(x, v, w)
-    prob = NnmfProblem.__new__(NnmfProblem)
-    object.__setattr__(prob, "x", x)
-    object.__setattr__(prob, "rank", r)
-    object.__setattr__(prob, "_dev", {})
-    mm = _GpuPoissonNnmf(prob, backend)
+    mm = _GpuPoissonNnmf(NnmfProblem._unchecked(x, r), backend)
     s = mm.device_state(FactorPair(v, w))
     out = mm._alloc_like(s)
     mm._iterate(s, out, mm.status.f_ptr, mm.status.err_ptr)
