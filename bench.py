@@ -284,14 +284,9 @@ def bench_nnmf_large(args, torch, world, rank, dev):
         sh.iterate(world)
 
     timing = time_steps(args, torch, dev, step, world)
-    # dominant kernel via the launch profiler (events on the launch stream)
-    lib = _lib.load()
-    lib.mmk_prof_enable(1)
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    lib.mmk_prof_enable(0)
-    prof = _lib.prof_report()
+    # dominant kernel via the launch profiler (events on the launch stream,
+    # recorded over the timed region)
+    prof = timing["prof"]
     es = x.element_size()
     ml = hi - lo
     alg = {  # algorithmic HBM bytes per launch
@@ -302,12 +297,13 @@ def bench_nnmf_large(args, torch, world, rank, dev):
         # X once + V'_hi/V'_lo read + fp32 split-K partials written
         "nnmf_wstep_tc": ml * n * 4 + 2 * ml * r * 4,
     }
-    launches = sum(c for c, _ in prof.values()) // 2
+    launches = sum(c for c, _ in prof.values()) // args.steps
     roof = roofline(prof, alg, "hbm", "dominant")
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = nnmf_e2e(args, torch, be, x, v0, w0, r)
-    kernels = {k: {"launches_per_step": c // 2, "avg_ms": ms / c} for k, (c, ms) in prof.items()}
+    kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
+               for k, (c, ms) in prof.items()}
     return timing, roof, launches, e2e, {"kernels": kernels}
 
 
@@ -362,17 +358,12 @@ def bench_mds_large(args, torch, world, rank, dev):
         cur[0] = 1 - a
 
     timing = time_steps(args, torch, dev, step, world)
-    lib = _lib.load()
-    lib.mmk_prof_enable(1)
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    lib.mmk_prof_enable(0)
-    prof = _lib.prof_report()
+    prof = timing["prof"]
     alg = {"mds_tri": (t1 - t0) * 128 * 128 * 4 + 2 * dim * n * 4}
-    launches = sum(c for c, _ in prof.values()) // 2
+    launches = sum(c for c, _ in prof.values()) // args.steps
     roof = roofline(prof, alg, "hbm", "dominant")
-    kernels = {k: {"launches_per_step": c // 2, "avg_ms": ms / c} for k, (c, ms) in prof.items()}
+    kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
+               for k, (c, ms) in prof.items()}
     mm._check_error()
     e2e = None
     return timing, roof, launches, e2e, {
@@ -410,21 +401,16 @@ def bench_pet_large(args, torch, world, rank, dev):
         cur[0] = 1 - a
 
     timing = time_steps(args, torch, dev, step, world)
-    lib = _lib.load()
-    lib.mmk_prof_enable(1)
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    lib.mmk_prof_enable(0)
-    prof = _lib.prof_report()
+    prof = timing["prof"]
     nnz = int(sa["rval"].numel())
     # streamed bytes of each projector (values fp32 + int32 indices + the
     # row/column pointers); the gathers of lam / ratio hit L2 and are excluded
     alg = {"pet_sfwd": nnz * 8 + (geo.n_rays + 1) * 4 + geo.n_rays * 12,
            "pet_sback": nnz * 8 + (geo.n_pixels + 1) * 4 + geo.n_pixels * 8}
-    launches = sum(c for c, _ in prof.values()) // 2
+    launches = sum(c for c, _ in prof.values()) // args.steps
     roof = roofline(prof, alg, "hbm", "dominant")
-    kernels = {k: {"launches_per_step": c // 2, "avg_ms": ms / c} for k, (c, ms) in prof.items()}
+    kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
+               for k, (c, ms) in prof.items()}
     mm._check_error()
     return timing, roof, launches, None, {
         "kernels": kernels, "e2e_note": "not measured for pet-large this round",
@@ -433,7 +419,14 @@ def bench_pet_large(args, torch, world, rank, dev):
 
 
 def time_steps(args, torch, dev, step, world):
+    """Warm-up, then exactly args.steps timed steps between CUDA events on the
+    compute stream (barrier + synchronize on both sides, max over ranks).
+    The library's launch profiler records an event pair around every kernel
+    launch of the timed region on its launch stream; ``prof`` holds
+    {kernel: (launches, total ms)} for the roofline of the dominant kernel."""
     import torch.distributed as dist
+    from paper_1003_3272_b200 import _lib
+    lib = _lib.load()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -442,19 +435,23 @@ def time_steps(args, torch, dev, step, world):
     stream = torch.cuda.current_stream(dev)
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    _lib.prof_report()                     # drop anything recorded earlier
     with Clocks(dev.index) as clk:
+        lib.mmk_prof_enable(1)
         start.record(stream)
         for _ in range(args.steps):
             step()
         end.record(stream)
         torch.cuda.synchronize(dev)
+        lib.mmk_prof_enable(0)
+    prof = _lib.prof_report()
     ms = start.elapsed_time(end)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         ms = float(t.item())
-    return {"ms_total": ms, "clocks": clk.summary()}
+    return {"ms_total": ms, "clocks": clk.summary(), "prof": prof}
 
 
 def roofline(prof, alg, bound, _label):
@@ -582,6 +579,9 @@ def run_ours(args):
             "config": workload_config(args, W),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps, "clocks": timing["clocks"],
+            "timing_note": "kernel times from CUDA events around every launch of the timed "
+                           "region (library launch profiler); value from events bracketing "
+                           "the region",
             "suite": suite_res,
             "kernels": extra.get("kernels"),
         }

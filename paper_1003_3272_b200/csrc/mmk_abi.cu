@@ -36,6 +36,18 @@ struct ProfRec {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_pool;   // recycled events (no create/destroy per launch)
+
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
 }  // namespace
 
 namespace mmk_host {
@@ -44,11 +56,9 @@ void prof_start(const char* name, cudaStream_t s) {
     if (!g_prof_on) return;
     cudaStreamCaptureStatus cs;
     if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
-    ProfRec r{name, nullptr, nullptr};
-    cudaEventCreate(&r.a);
-    cudaEventCreate(&r.b);
-    cudaEventRecord(r.a, s);
     std::lock_guard<std::mutex> lk(g_prof_mu);
+    ProfRec r{name, take_event(), take_event()};
+    cudaEventRecord(r.a, s);
     g_prof.push_back(r);
 }
 void prof_stop(cudaStream_t s) {
@@ -80,8 +90,8 @@ extern "C" int mmk_prof_report(char* buf, size_t len) {
                 found = true;
             }
         if (!found) agg.push_back({r.name, {1, (double)ms}});
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
     }
     g_prof.clear();
     std::string out;

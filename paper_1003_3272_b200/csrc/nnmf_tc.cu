@@ -568,8 +568,10 @@ vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __
         const long long r0 = ((long long)blockIdx.x * VGW_CHUNKS + ch) * 64;
         if (r0 >= m) break;
         __syncthreads();   // G ready / previous chunk's Vt consumed
+        // consecutive threads take consecutive rows: conflict-free transposed
+        // smem stores (the row's 16-byte pieces are read by 16 warps, L1 hits)
         for (int i = threadIdx.x; i < 16 * R; i += 256) {
-            const int rr = i / 16, l4 = (i % 16) * 4;
+            const int rr = i % 64, l4 = (i / 64) * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + l4);
             Vt[l4][rr] = v.x;
