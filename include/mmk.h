@@ -264,13 +264,15 @@ int mmk_allgather(const void *send, void *recv, int64_t count, int dtype, void *
  * Device-side MM loop (replaces the host loop of run_mm, driver.py:101-149,
  * with identical stopping / monotonicity / non-finite semantics).
  *
- * An engine is ONE CUDA graph: a conditional WHILE node whose body copies
- * state slot B into slot A, runs one fused iteration A -> B (f(A) into
- * ctl[MMK_CTL_FCUR]), and a control kernel that applies the stopping rule.
- * Each mmk_engine_run() launch advances until the run stops or `batch`
- * iterations were recorded.  trace[k] / tstamp[k] (k = it - batch start)
- * receive f(S_it) and the device globaltimer (ns).  When the run stops at
- * iteration `it`, slot A holds S_it.  ctl (16 int64, zeroed by the caller
+ * An engine is ONE CUDA graph: a conditional WHILE node whose body runs one
+ * fused iteration A -> B (f(A) into ctl[MMK_CTL_FCUR]) and a control kernel
+ * that applies the stopping rule, then -- inside a conditional IF node --
+ * the iteration B -> A and its control kernel: two iterations per body,
+ * no state copies.  Each mmk_engine_run() launch advances until the run
+ * stops or `batch` (even) iterations were recorded.  trace[k] / tstamp[k]
+ * (k = it - batch start) receive f(S_it) and the device globaltimer (ns).
+ * When the run stops at iteration `it`, S_it is in slot A if
+ * ctl[MMK_CTL_SLOT] == 0, else in slot B; after a pause it is in slot A.  ctl (16 int64, zeroed by the caller
  * before the first launch) holds the loop state.  With comm != NULL the
  * body also all-reduces the phase-A buffer (NNMF, PET) or the stress
  * partial + coordinate all-gather (MDS) over NCCL.
@@ -292,6 +294,7 @@ enum {
     MMK_CTL_FPREV = 3,       /* fp64 bits */
     MMK_CTL_FCUR = 4,        /* fp64 bits: f_dev of the iteration kernels */
     MMK_CTL_REL = 5,         /* fp64 bits: last relative change */
+    MMK_CTL_SLOT = 6,        /* after a stop: 0 -> state in slot A, 1 -> slot B */
     MMK_CTL_LEN = 16
 };
 enum {

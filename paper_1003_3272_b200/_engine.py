@@ -11,10 +11,11 @@ Two ways to drive a solver, identical results:
   iteration (the pattern of the reference's ``_PetMm._means`` cache,
   ``pet.py:454-471``).
 * **Fused** (``run_fused``, picked up by ``run_mm`` when the backend allows
-  it): the whole loop runs on the device as one CUDA graph with a
-  conditional WHILE node (``csrc/engine.cu``); the control kernel applies the
-  same stopping rule, monotonicity slack and non-finite checks, and the host
-  only drains the objective trace every ``batch`` iterations.
+  it): the whole loop runs on the device as one CUDA graph with conditional
+  WHILE / IF nodes, two iterations per body on ping-pong state slots
+  (``csrc/engine.cu``); the control kernels apply the same stopping rule,
+  monotonicity slack and non-finite checks, and the host only drains the
+  objective trace every ``batch`` iterations.
 """
 
 import ctypes
@@ -27,7 +28,8 @@ from . import _lib
 from .driver import MmProblem, MmTrace
 from .errors import MonotonicityError, NonFiniteError
 
-CTL_IT, CTL_REASON, CTL_BATCH_START, CTL_FPREV, CTL_FCUR, CTL_REL, CTL_LEN = 0, 1, 2, 3, 4, 5, 16
+CTL_IT, CTL_REASON, CTL_BATCH_START, CTL_FPREV, CTL_FCUR, CTL_REL, CTL_SLOT, CTL_LEN = (
+    0, 1, 2, 3, 4, 5, 6, 16)
 STOP_CONVERGED, STOP_CAP, STOP_NONFINITE, STOP_MONOTONE, STOP_DEVICE_ERROR = 1, 2, 3, 4, 5
 
 
@@ -93,7 +95,8 @@ class DeviceMm(MmProblem):
     def _batch(self, config):
         t_iter = self._bytes_per_iter() / 4.0e12 + 8e-6
         batch = int(min(4096, max(8, 0.05 / t_iter)))
-        return int(min(batch, config.max_iters + 1))
+        batch = int(min(batch, config.max_iters + 2))
+        return batch + (batch & 1)            # even: pauses fall after the B -> A half
 
     def _run_fused(self, state0, config):
         torch = self.torch
@@ -145,6 +148,7 @@ class DeviceMm(MmProblem):
             raise NonFiniteError(f"objective became non-finite at iteration {it}: {values[-1]!r}")
         if reason == STOP_MONOTONE:
             raise MonotonicityError(it, values[-2], values[-1], self.direction)
+        final = b if int(c[CTL_SLOT]) == 1 else a
         ts = np.asarray(stamps, dtype=np.float64)
         trace_obj = MmTrace(
             objective_values=np.array(values),
@@ -154,4 +158,4 @@ class DeviceMm(MmProblem):
             wall_time=time.perf_counter() - started,
             final_relative_change=_as_f64(c[CTL_REL]) if it > 0 else math.inf,
         )
-        return a, trace_obj
+        return final, trace_obj

@@ -5,10 +5,11 @@
 // whole iteration is a few microseconds of GPU work, so a host round trip per
 // iteration would dominate.  The engine instead records ONE CUDA graph
 //
-//     WHILE (cond) {  A <- B  (state copy) ;  iteration(A -> B, f(A)) ;
-//                     control(f) }
+//     WHILE (w) {  iteration(A -> B, f(A)) ; control(f)  ->  w, i
+//                  IF (i) { iteration(B -> A, f(B)) ; control(f) -> w } }
 //
-// using a conditional WHILE node.  The control kernel applies exactly the
+// using conditional WHILE and IF nodes: two iterations per body with the
+// state slots swapped, so no state copy is needed.  The control kernel applies exactly the
 // reference's rules -- non-finite check, monotone slack
 // monotone_tol * (1 + |f_prev|), relative change |f - f_prev| / (|f_prev| + 1)
 // < epsilon, the max_iters cap -- records the objective trace and a device
@@ -32,12 +33,6 @@ namespace {
 
 using namespace mmk;
 
-struct Copy {
-    void* dst;
-    const void* src;
-    size_t bytes;
-};
-
 struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -47,8 +42,13 @@ struct Engine {
 __device__ __forceinline__ double as_f64(long long b) { return __longlong_as_double(b); }
 __device__ __forceinline__ long long as_bits(double d) { return __double_as_longlong(d); }
 
-__global__ void control_kernel(cudaGraphConditionalHandle h, long long* ctl, double* trace,
-                               long long* tstamp, const long long* err, mmk_stop_rule rule) {
+// half 0 follows iteration A -> B (its objective is f(A)), half 1 follows
+// B -> A.  A stop records which slot holds the returned state (the input of
+// the last recorded objective, as run_mm returns it); batch pauses happen only
+// after half 1, so every launch starts from slot A.
+__global__ void control_kernel(cudaGraphConditionalHandle h, cudaGraphConditionalHandle hif,
+                               int half, long long* ctl, double* trace, long long* tstamp,
+                               const long long* err, mmk_stop_rule rule) {
     if (threadIdx.x != 0) return;
     const long long it = ctl[MMK_CTL_IT];
     const double f = as_f64(ctl[MMK_CTL_FCUR]);
@@ -75,12 +75,16 @@ __global__ void control_kernel(cudaGraphConditionalHandle h, long long* ctl, dou
     if (!reason && it >= rule.max_iters) reason = MMK_STOP_CAP;
     if (reason) {
         ctl[MMK_CTL_REASON] = reason;
+        ctl[MMK_CTL_SLOT] = half;
         cudaGraphSetConditional(h, 0);
+        if (half == 0) cudaGraphSetConditional(hif, 0);
         return;
     }
     ctl[MMK_CTL_FPREV] = as_bits(f);
     ctl[MMK_CTL_IT] = it + 1;
-    if (it + 1 - ctl[MMK_CTL_BATCH_START] >= rule.batch) {
+    if (half == 0) {
+        cudaGraphSetConditional(hif, 1);
+    } else if (it + 1 - ctl[MMK_CTL_BATCH_START] >= rule.batch) {
         ctl[MMK_CTL_BATCH_START] = it + 1;
         cudaGraphSetConditional(h, 0);
     }
@@ -95,53 +99,75 @@ __global__ void control_kernel(cudaGraphConditionalHandle h, long long* ctl, dou
         }                                                              \
     } while (0)
 
-int build(const std::function<int(cudaStream_t)>& iter, const std::vector<Copy>& copies,
-          const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
-          int64_t* err, void** out) {
+using IterFn = std::function<int(cudaStream_t, int /* 0: A -> B, 1: B -> A */)>;
+
+// capture `iter(dir)` + control(half = dir) into `g`; returns the last node
+int capture_half(Engine* e, cudaGraph_t g, const IterFn& iter, int dir,
+                 cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi,
+                 const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+                 int64_t* err, cudaGraphNode_t* last) {
     int rc = MMK_OK;
-    Engine* e = new Engine();
-    cudaGraphConditionalHandle h;
-    cudaGraphNodeParams np = {};
-    cudaGraphNode_t node;
-    cudaGraph_t body, captured;
-    if (rule->batch < 1) {
-        mmk_host::set_error("engine batch must be >= 1");
-        rc = MMK_E_SHAPE;
-        goto fail;
-    }
-    ENG_CHECK(cudaGraphCreate(&e->graph, 0), "cudaGraphCreate");
-    ENG_CHECK(cudaGraphConditionalHandleCreate(&h, e->graph, 1, cudaGraphCondAssignDefault),
-              "cudaGraphConditionalHandleCreate");
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    ENG_CHECK(cudaGraphAddNode(&node, e->graph, nullptr, 0, &np), "cudaGraphAddNode(while)");
-    body = np.conditional.phGraph_out[0];
-    ENG_CHECK(cudaStreamCreateWithFlags(&e->cap, cudaStreamNonBlocking), "cudaStreamCreate");
-    ENG_CHECK(cudaStreamBeginCaptureToGraph(e->cap, body, nullptr, nullptr, 0,
-                                            cudaStreamCaptureModeThreadLocal),
-              "cudaStreamBeginCaptureToGraph");
-    for (const Copy& c : copies) {
-        cudaError_t ce = cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, e->cap);
-        if (ce != cudaSuccess) {
-            cudaStreamEndCapture(e->cap, &captured);
-            rc = mmk_host::cuda_status(ce, "engine state copy");
-            goto fail;
-        }
-    }
-    rc = iter(e->cap);
+    cudaGraph_t captured;
+    cudaError_t ce = cudaStreamBeginCaptureToGraph(e->cap, g, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "cudaStreamBeginCaptureToGraph");
+    rc = iter(e->cap, dir);
     if (rc == MMK_OK) {
-        control_kernel<<<1, 32, 0, e->cap>>>(h, reinterpret_cast<long long*>(ctl), trace,
+        control_kernel<<<1, 32, 0, e->cap>>>(hw, hi, dir, reinterpret_cast<long long*>(ctl), trace,
                                              reinterpret_cast<long long*>(tstamp),
                                              reinterpret_cast<const long long*>(err), *rule);
         cudaError_t le = cudaGetLastError();
         if (le != cudaSuccess) rc = mmk_host::cuda_status(le, "control_kernel");
     }
-    {
-        cudaError_t ee = cudaStreamEndCapture(e->cap, &captured);
-        if (rc == MMK_OK && ee != cudaSuccess) rc = mmk_host::cuda_status(ee, "EndCapture");
+    if (rc == MMK_OK && last) {
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        ce = cudaStreamGetCaptureInfo(e->cap, &cs, nullptr, nullptr, &deps, &nd);
+        if (ce != cudaSuccess || nd != 1) rc = mmk_host::cuda_status(
+            ce != cudaSuccess ? ce : cudaErrorInvalidValue, "cudaStreamGetCaptureInfo");
+        else
+            *last = deps[0];
     }
+    ce = cudaStreamEndCapture(e->cap, &captured);
+    if (rc == MMK_OK && ce != cudaSuccess) rc = mmk_host::cuda_status(ce, "EndCapture");
+    return rc;
+}
+
+int build(const IterFn& iter, const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
+          int64_t* ctl, int64_t* err, void** out) {
+    int rc = MMK_OK;
+    Engine* e = new Engine();
+    cudaGraphConditionalHandle hw, hi;
+    cudaGraphNodeParams np = {}, ip = {};
+    cudaGraphNode_t node, ifnode, last = nullptr;
+    cudaGraph_t body;
+    if (rule->batch < 2 || (rule->batch & 1)) {
+        mmk_host::set_error("engine batch must be an even number >= 2");
+        rc = MMK_E_SHAPE;
+        goto fail;
+    }
+    ENG_CHECK(cudaGraphCreate(&e->graph, 0), "cudaGraphCreate");
+    ENG_CHECK(cudaGraphConditionalHandleCreate(&hw, e->graph, 1, cudaGraphCondAssignDefault),
+              "cudaGraphConditionalHandleCreate(while)");
+    ENG_CHECK(cudaGraphConditionalHandleCreate(&hi, e->graph, 0, 0),
+              "cudaGraphConditionalHandleCreate(if)");
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hw;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    ENG_CHECK(cudaGraphAddNode(&node, e->graph, nullptr, 0, &np), "cudaGraphAddNode(while)");
+    body = np.conditional.phGraph_out[0];
+    ENG_CHECK(cudaStreamCreateWithFlags(&e->cap, cudaStreamNonBlocking), "cudaStreamCreate");
+    rc = capture_half(e, body, iter, 0, hw, hi, rule, trace, tstamp, ctl, err, &last);
+    if (rc != MMK_OK) goto fail;
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    ENG_CHECK(cudaGraphAddNode(&ifnode, body, &last, 1, &ip), "cudaGraphAddNode(if)");
+    rc = capture_half(e, ip.conditional.phGraph_out[0], iter, 1, hw, hi, rule, trace, tstamp, ctl,
+                      err, nullptr);
     if (rc != MMK_OK) goto fail;
     ENG_CHECK(cudaGraphInstantiate(&e->exec, e->graph, 0), "cudaGraphInstantiate");
     *out = e;
@@ -237,19 +263,17 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
                                       int64_t* ctl, int64_t* err_dev, void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_reduce_len(n, r);
-    auto iter = [=](cudaStream_t s) -> int {
-        int rc = mmk_nnmf_iter_a(dtype, X, ldx, VA, WA, VB, m, n, r, ws, ws_bytes, red, err_dev, s);
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        void *Vi = dir ? VB : VA, *Vo = dir ? VA : VB, *Wi = dir ? WB : WA, *Wo = dir ? WA : WB;
+        int rc = mmk_nnmf_iter_a(dtype, X, ldx, Vi, Wi, Vo, m, n, r, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
         if (comm) {
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_nnmf_iter_b(dtype, WA, WB, n, r, red, f_dev, err_dev, s);
+        return mmk_nnmf_iter_b(dtype, Wi, Wo, n, r, red, f_dev, err_dev, s);
     };
-    std::vector<Copy> copies = {{VA, VB, (size_t)(m * r) * esize(dtype)},
-                                {WA, WB, (size_t)(r * n) * esize(dtype)}};
-    if (m == 0) copies.erase(copies.begin());
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
 
 extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, const void* y,
@@ -260,19 +284,19 @@ extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, cons
                                      int64_t* ctl, int64_t* err_dev, void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
-    auto iter = [=](cudaStream_t s) -> int {
-        int rc = mmk_pet_iter_a(dtype, E, lde, y, lamA, d, p, ws, ws_bytes, red, err_dev, s);
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        void *Li = dir ? lamB : lamA, *Lo = dir ? lamA : lamB;
+        int rc = mmk_pet_iter_a(dtype, E, lde, y, Li, d, p, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
         if (comm) {
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_pet_iter_b(dtype, lamA, lamB, p, nbr_ptr, nbr_idx, mu,
+        return mmk_pet_iter_b(dtype, Li, Lo, p, nbr_ptr, nbr_idx, mu,
                               MMK_PET_UPDATE | MMK_PET_OBJECTIVE, red, ws, ws_bytes, f_dev,
                               err_dev, s);
     };
-    std::vector<Copy> copies = {{lamA, lamB, (size_t)p * esize(dtype)}};
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
 
 extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, int64_t ldy,
@@ -283,16 +307,17 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
                                      double* trace, int64_t* tstamp, int64_t* ctl,
                                      int64_t* err_dev, void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
-    auto iter = [=](cudaStream_t s) -> int {
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        void *Ti = dir ? thetaB : thetaA, *To = dir ? thetaA : thetaB;
         if (!comm) {
-            return mmk_mds_iter(dtype, Y, Wt, ldy, wsum, thetaA, thetaB, n, dim, n, 0, n,
+            return mmk_mds_iter(dtype, Y, Wt, ldy, wsum, Ti, To, n, dim, n, 0, n,
                                 MMK_MDS_UPDATE | MMK_MDS_OBJECTIVE, ws, ws_bytes, f_dev, err_dev,
                                 s);
         }
         // sharded: own rows -> local_out [dim x rows_pad]; all-gather into
-        // gathered [rank][dim][rows_pad]; unpack to thetaB [dim x n]; the
-        // stress partial is all-reduced in place
-        int rc = mmk_mds_iter(dtype, Y, Wt, ldy, wsum, thetaA, local_out, rows_pad, dim, n, row0,
+        // gathered [rank][dim][rows_pad]; unpack to the output slot [dim x n];
+        // the stress partial is all-reduced in place
+        int rc = mmk_mds_iter(dtype, Y, Wt, ldy, wsum, Ti, local_out, rows_pad, dim, n, row0,
                               rows, MMK_MDS_UPDATE | MMK_MDS_OBJECTIVE, ws, ws_bytes, f_dev,
                               err_dev, s);
         if (rc) return rc;
@@ -300,10 +325,9 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
         if (rc) return rc;
         rc = mmk_allgather(local_out, gathered, dim * rows_pad, dtype, comm, s);
         if (rc) return rc;
-        return mmk_mds_unpack(dtype, gathered, thetaB, dim, n, rows_pad, s);
+        return mmk_mds_unpack(dtype, gathered, To, dim, n, rows_pad, s);
     };
-    std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * esize(dtype)}};
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
 
 extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_t t1,
@@ -314,17 +338,17 @@ extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_
                                          void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_mds_tri_reduce_len(n, dim);
-    auto iter = [=](cudaStream_t s) -> int {
-        int rc = mmk_mds_tri_iter_a(packed, t0, t1, thetaA, dim, n, ws, ws_bytes, red, err_dev, s);
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        float *Ti = dir ? thetaB : thetaA, *To = dir ? thetaA : thetaB;
+        int rc = mmk_mds_tri_iter_a(packed, t0, t1, Ti, dim, n, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
         if (comm) {
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_mds_tri_iter_b(thetaA, thetaB, dim, n, red, f_dev, s);
+        return mmk_mds_tri_iter_b(Ti, To, dim, n, red, f_dev, s);
     };
-    std::vector<Copy> copies = {{thetaA, thetaB, (size_t)(dim * n) * sizeof(float)}};
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
 
 extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t ldx, void* VA,
@@ -335,20 +359,18 @@ extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t 
                                               int64_t* err_dev, void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_poisson_reduce_len(n, r);
-    auto iter = [=](cudaStream_t s) -> int {
-        int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, VA, WA, VB, m, n, r, ws, ws_bytes, red,
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        void *Vi = dir ? VB : VA, *Vo = dir ? VA : VB, *Wi = dir ? WB : WA, *Wo = dir ? WA : WB;
+        int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, Vi, Wi, Vo, m, n, r, ws, ws_bytes, red,
                                          err_dev, s);
         if (rc) return rc;
         if (comm) {
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_nnmf_poisson_iter_b(dtype, WA, WB, n, r, red, f_dev, err_dev, s);
+        return mmk_nnmf_poisson_iter_b(dtype, Wi, Wo, n, r, red, f_dev, err_dev, s);
     };
-    std::vector<Copy> copies = {{VA, VB, (size_t)(m * r) * esize(dtype)},
-                                {WA, WB, (size_t)(r * n) * esize(dtype)}};
-    if (m == 0) copies.erase(copies.begin());
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
 
 extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, const int32_t* ridx,
@@ -362,18 +384,18 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
                                             void** engine) {
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
-    auto iter = [=](cudaStream_t s) -> int {
-        int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lamA, d, p,
+    auto iter = [=](cudaStream_t s, int dir) -> int {
+        void *Li = dir ? lamB : lamA, *Lo = dir ? lamA : lamB;
+        int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, Li, d, p,
                                        ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
         if (comm) {
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_pet_iter_b(dtype, lamA, lamB, p, nbr_ptr, nbr_idx, mu,
+        return mmk_pet_iter_b(dtype, Li, Lo, p, nbr_ptr, nbr_idx, mu,
                               MMK_PET_UPDATE | MMK_PET_OBJECTIVE, red, ws, ws_bytes, f_dev,
                               err_dev, s);
     };
-    std::vector<Copy> copies = {{lamA, lamB, (size_t)p * esize(dtype)}};
-    return build(iter, copies, rule, trace, tstamp, ctl, err_dev, engine);
+    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }

@@ -21,7 +21,10 @@ using namespace mmk;
 
 constexpr int kWarps = 8;
 
-template <typename T, int DIM, int RPW>
+// SPLIT > 1 (small problems): SPLIT warps share a row, each sweeping every
+// SPLIT-th 32-column slice; their sums are combined through shared memory in
+// warp order (deterministic) before the update.
+template <typename T, int DIM, int RPW, int SPLIT>
 __global__ void __launch_bounds__(kWarps * 32)
 mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy,
                 const double* __restrict__ wsum, const T* __restrict__ theta,
@@ -31,7 +34,8 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
     const int dim = DIM > 0 ? DIM : dim_rt;
     constexpr int DM = DIM > 0 ? DIM : 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long lbase = ((long long)blockIdx.x * kWarps + warp) * RPW;  // local row
+    const int seg = warp % SPLIT, rw = warp / SPLIT;
+    const long long lbase = ((long long)blockIdx.x * (kWarps / SPLIT) + rw) * RPW;  // local row
     const bool do_update = flags & MMK_MDS_UPDATE;
     const bool do_obj = flags & MMK_MDS_OBJECTIVE;
 
@@ -52,7 +56,7 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
         st[rr] = 0.0;
     }
 
-    for (long long j = lane; j < n; j += 32) {
+    for (long long j = lane + 32 * seg; j < n; j += 32 * SPLIT) {
         T tj[DM];
 #pragma unroll
         for (int k = 0; k < DM; ++k) tj[k] = (k < dim) ? __ldg(theta + (long long)k * n + j) : T(0);
@@ -90,14 +94,45 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
     }
 
     double blk = 0.0;
+    double sst[RPW];
 #pragma unroll
     for (int rr = 0; rr < RPW; ++rr) {
-        const long long li = lbase + rr;
         zs[rr] = warp_sum(zs[rr]);
 #pragma unroll
         for (int k = 0; k < DM; ++k) acc[rr][k] = warp_sum(acc[rr][k]);
-        const double s = warp_sum(st[rr]);
-        if (li < rows) {
+        sst[rr] = warp_sum(st[rr]);
+    }
+    if (SPLIT > 1) {
+        __shared__ double sh[kWarps][DM + 2];
+        if (lane == 0) {
+            sh[warp][0] = (double)zs[0];
+            sh[warp][1] = sst[0];
+#pragma unroll
+            for (int k = 0; k < DM; ++k) sh[warp][2 + k] = (double)acc[0][k];
+        }
+        __syncthreads();
+        if (seg == 0 && lane == 0) {
+            double z = sh[warp][0], t = sh[warp][1];
+            double a[DM];
+#pragma unroll
+            for (int k = 0; k < DM; ++k) a[k] = sh[warp][2 + k];
+            for (int q = 1; q < SPLIT; ++q) {
+                z += sh[warp + q][0];
+                t += sh[warp + q][1];
+#pragma unroll
+                for (int k = 0; k < DM; ++k) a[k] += sh[warp + q][2 + k];
+            }
+            zs[0] = (T)z;
+            sst[0] = t;
+#pragma unroll
+            for (int k = 0; k < DM; ++k) acc[0][k] = (T)a[k];
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const long long li = lbase + rr;
+        const double s = sst[rr];
+        if (li < rows && seg == 0) {
             blk += s;
             if (do_update && lane == 0) {
                 const long long gi = row0 + li;
@@ -130,18 +165,18 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
 
 constexpr int kMaxDim = 32;
 
-template <typename T, int RPW>
+template <typename T, int RPW, int SPLIT = 1>
 int launch_rows(const T* Y, const T* Wt, long long ldy, const double* wsum, const T* theta,
                 T* out, long long ldo, int dim, long long n, long long row0, long long rows,
                 int flags, void* ws, double* f_dev, int64_t* err, cudaStream_t st) {
-    const int rows_per_block = kWarps * RPW;
+    const int rows_per_block = kWarps / SPLIT * RPW;
     const int grid = ceil_div(rows, rows_per_block);
     unsigned int* counter = reinterpret_cast<unsigned int*>(ws);
     double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + 256);
 #define MMK_MDS_CASE(D)                                                                     \
     case D:                                                                                 \
         MMK_LAUNCH("mds_rows", st,                                                          \
-                   (mds_rows_kernel<T, D, RPW><<<grid, kWarps * 32, 0, st>>>(               \
+                   (mds_rows_kernel<T, D, RPW, SPLIT><<<grid, kWarps * 32, 0, st>>>(               \
                        Y, Wt, ldy, wsum, theta, out, ldo, dim, n, row0, rows, flags,        \
                        partials, counter, f_dev, err)));                                    \
         break;
@@ -150,7 +185,7 @@ int launch_rows(const T* Y, const T* Wt, long long ldy, const double* wsum, cons
         MMK_MDS_CASE(6) MMK_MDS_CASE(7) MMK_MDS_CASE(8) MMK_MDS_CASE(9) MMK_MDS_CASE(10)
         default:
             MMK_LAUNCH("mds_rows", st,
-                       (mds_rows_kernel<T, 0, RPW><<<grid, kWarps * 32, 0, st>>>(
+                       (mds_rows_kernel<T, 0, RPW, SPLIT><<<grid, kWarps * 32, 0, st>>>(
                            Y, Wt, ldy, wsum, theta, out, ldo, dim, n, row0, rows, flags,
                            partials, counter, f_dev, err)));
     }
@@ -160,7 +195,7 @@ int launch_rows(const T* Y, const T* Wt, long long ldy, const double* wsum, cons
 }
 
 size_t mds_ws(long long rows) {
-    const int grid = ceil_div(rows, kWarps);  // worst case RPW = 1
+    const int grid = ceil_div(rows, 1);   // worst case: SPLIT = kWarps, one row per block
     return 256 + sizeof(double) * (size_t)grid;
 }
 
@@ -219,14 +254,19 @@ extern "C" int mmk_mds_iter(int dtype, const void* Y, const void* Wt, int64_t ld
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // small problems: one point per warp (more CTAs); large: 4 points per warp
+    // small problems: split every row over 8 (4) warps for parallelism;
+    // large: 4 points per warp
     const bool big = rows >= 4096;
+    const bool tiny = rows <= 1024;
     if (dtype == MMK_F32) {
-        auto f = big ? launch_rows<float, 4> : launch_rows<float, 1>;
+        auto f = big ? launch_rows<float, 4> : tiny ? launch_rows<float, 1, 8>
+                                                    : launch_rows<float, 1, 4>;
         return f((const float*)Y, (const float*)Wt, ldy, wsum, (const float*)theta,
                  (float*)theta_out, ldo, (int)dim, n, row0, rows, flags, ws, f_dev, err_dev, st);
     }
     if (dtype == MMK_F64) {
-        auto f = big ? launch_rows<double, 4> : launch_rows<double, 1>;
+        auto f = big ? launch_rows<double, 4> : tiny ? launch_rows<double, 1, 8>
+                                                     : launch_rows<double, 1, 4>;
         return f((const double*)Y, (const double*)Wt, ldy, wsum, (const double*)theta,
                  (double*)theta_out, ldo, (int)dim, n, row0, rows, flags, ws, f_dev, err_dev, st);
     }

@@ -237,9 +237,9 @@ class SparsePetProblem:
         """E lam (fp64) on the device -- e.g. for simulating counts."""
         torch = _lib.torch_mod()
         sa = self.sa
-        e = torch.sparse_csr_tensor(sa["rptr"].to(torch.int64), sa["ridx"].to(torch.int64),
-                                    sa["rval"], (sa["n_rays"], sa["n_pixels"]),
-                                    check_invariants=True)
+        with torch.sparse.check_sparse_tensor_invariants():
+            e = torch.sparse_csr_tensor(sa["rptr"].to(torch.int64), sa["ridx"].to(torch.int64),
+                                        sa["rval"], (sa["n_rays"], sa["n_pixels"]))
         lam_t = lam if A.is_torch(lam) else torch.from_numpy(np.asarray(lam, dtype=np.float64))
         return (e @ lam_t.to(sa["rval"].device, torch.float64)[:, None])[:, 0]
 

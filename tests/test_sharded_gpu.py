@@ -55,3 +55,25 @@ def test_mds_sharded_equals_unsharded(group):
     ref, rtr = M.mds_run(prob, cfg, be, theta0=th0)
     assert np.array_equal(tr.objective_values, rtr.objective_values)
     assert np.array_equal(np.asarray(th.cpu() if hasattr(th, "cpu") else th), ref)
+
+
+def test_in_graph_nccl_engine(group):
+    """The fused device engine with the all-reduce captured inside its CUDA
+    graph (ncclAllReduce of torch's communicator, resolved with dlsym):
+    equal to the engine without the collective."""
+    from paper_1003_3272_b200 import _lib
+    comm = P.nccl_comm_ptr()
+    assert comm, "no NCCL communicator pointer"
+    assert _lib.load().mmk_nccl_available() == 1
+    rng = np.random.default_rng(6)
+    x = rng.random((512, 192))
+    v0, w0 = rng.random((512, 8)), rng.random((8, 192))
+    be = Backend(dtype="fp64")
+    cfg = MmConfig(max_iters=12, epsilon=1e-300)
+    prob = M.NnmfProblem(x=x, rank=8)
+    mm = M.nnmf._GpuNnmf(prob, be)
+    mm.comm = comm
+    st, tr = M.run_mm(mm, mm.device_state(M.FactorPair(v0, w0)), cfg)
+    ref, rtr = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
+    assert np.array_equal(tr.objective_values, rtr.objective_values)
+    assert np.array_equal(st.v.cpu().numpy(), ref.v)
