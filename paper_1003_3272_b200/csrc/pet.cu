@@ -375,23 +375,25 @@ pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ri
     }
 }
 
-// thread per pixel: b_j over the CSC column -> red[j]
+// kSubW lanes per pixel: b_j over the CSC column (lane q takes entries
+// q, q + kSubW, ...), combined by a fixed xor-shuffle tree -> red[j]
+constexpr int kSubW = 8;
 template <typename T>
 __global__ void __launch_bounds__(256)
 pet_sback_kernel(const int32_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
                  const T* __restrict__ cval, long long p, const double* __restrict__ ratio,
                  double* __restrict__ red) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= p) return;
-    double b0 = 0.0, b1 = 0.0;
-    int t = cptr[j];
-    const int t1 = cptr[j + 1];
-    for (; t + 1 < t1; t += 2) {
-        b0 = fma((double)cval[t], ratio[cidx[t]], b0);
-        b1 = fma((double)cval[t + 1], ratio[cidx[t + 1]], b1);
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long j = g / kSubW;
+    const int q = (int)(g % kSubW);
+    double b = 0.0;
+    if (j < p) {
+        const int t1 = cptr[j + 1];
+        for (int t = cptr[j] + q; t < t1; t += kSubW) b = fma((double)cval[t], ratio[cidx[t]], b);
     }
-    if (t < t1) b0 = fma((double)cval[t], ratio[cidx[t]], b0);
-    red[j] = b0 + b1;
+#pragma unroll
+    for (int o = kSubW / 2; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (j < p && q == 0) red[j] = b;
 }
 
 struct SparseWs {
@@ -436,8 +438,8 @@ int pet_sparse_a(const int32_t* rptr, const int32_t* ridx, const T* rval, const 
                        err)));
         MMK_CHECK_LAUNCH("pet_sfwd_kernel");
         MMK_LAUNCH("pet_sback", st,
-                   (pet_sback_kernel<T><<<ceil_div(p, 256), 256, 0, st>>>(cptr, cidx, cval, p,
-                                                                          L.ratio, red)));
+                   (pet_sback_kernel<T><<<ceil_div(p * kSubW, 256), 256, 0, st>>>(
+                       cptr, cidx, cval, p, L.ratio, red)));
         MMK_CHECK_LAUNCH("pet_sback_kernel");
     } else {
         cudaMemsetAsync(red, 0, sizeof(double) * (size_t)(p + 1), st);
