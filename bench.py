@@ -406,7 +406,7 @@ def bench_pet_large(args, torch, world, rank, dev):
     # streamed bytes of each projector (values fp32 + int32 indices + the
     # row/column pointers); the gathers of lam / ratio hit L2 and are excluded
     alg = {"pet_sfwd": nnz * 8 + (geo.n_rays + 1) * 4 + geo.n_rays * 12,
-           "pet_sback": nnz * 8 + (geo.n_pixels + 1) * 4 + geo.n_pixels * 8}
+           "pet_sback_pixel": nnz * 8 + (geo.n_pixels + 1) * 4 + geo.n_pixels * 8}
     launches = sum(c for c, _ in prof.values()) // args.steps
     roof = roofline(prof, alg, "hbm", "dominant")
     kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}

@@ -386,6 +386,11 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
     const int64_t rl = mmk_pet_reduce_len(p);
     auto iter = [=](cudaStream_t s, int dir) -> int {
         void *Li = dir ? lamB : lamA, *Lo = dir ? lamA : lamB;
+        if (!comm)   // one GPU: fused back-projection + pixel update
+            return mmk_pet_sparse_iter(dtype, rptr, ridx, rval, cptr, cidx, cval, y, Li, Lo, d,
+                                       p, nbr_ptr, nbr_idx, mu,
+                                       MMK_PET_UPDATE | MMK_PET_OBJECTIVE, ws, ws_bytes, red,
+                                       f_dev, err_dev, s);
         int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, Li, d, p,
                                        ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;

@@ -180,6 +180,106 @@ pet_back_kernel(const T* __restrict__ E, long long lde, long long d, long long p
     }
 }
 
+// sparse gather-dot over entries t0, t0 + S, ... < t1: sum val[t] * x[idx[t]]
+// in that order (one fp64 chain), with the index/value/gather loads of four
+// consecutive entries issued before their fmas so four gathers are in flight
+template <int S, typename T, typename X>
+__device__ __forceinline__ double gather_dot(const int32_t* __restrict__ idx,
+                                             const T* __restrict__ val,
+                                             const X* __restrict__ x, int t0, int t1) {
+    double m = 0.0;
+    int t = t0;
+    for (; t + 3 * S < t1; t += 4 * S) {
+        const int i0 = idx[t], i1 = idx[t + S], i2 = idx[t + 2 * S], i3 = idx[t + 3 * S];
+        const T v0 = val[t], v1 = val[t + S], v2 = val[t + 2 * S], v3 = val[t + 3 * S];
+        const X x0 = x[i0], x1 = x[i1], x2 = x[i2], x3 = x[i3];
+        m = fma((double)v0, (double)x0, m);
+        m = fma((double)v1, (double)x1, m);
+        m = fma((double)v2, (double)x2, m);
+        m = fma((double)v3, (double)x3, m);
+    }
+    for (; t < t1; t += S) m = fma((double)val[t], (double)x[idx[t]], m);
+    return m;
+}
+
+constexpr int kSubW = 8;   // lanes per pixel of the sparse back-projection
+constexpr int kFusedPix = kPixThreads / kSubW;   // pixels per fused CTA
+
+// pixel j of the MM update given its back-projection bj (pet.py:388-417):
+// c_j = lam_j b_j, neighbour sum, EM floor or positive root -> lam_out[j];
+// returns this pixel's share of the roughness penalty at lam (each lattice
+// pair once, from its lower index; pet.py:326-331)
+template <typename T>
+__device__ __forceinline__ double pixel_update(const T* __restrict__ lam, T* __restrict__ lam_out,
+                                               const int32_t* __restrict__ nptr,
+                                               const int32_t* __restrict__ nidx, double mu,
+                                               int flags, long long j, double bj, int64_t* err) {
+    double pen = 0.0;
+    const double lj = (double)lam[j];
+    if ((flags & MMK_PET_CHECK_POSITIVE) && !(lj > 0.0)) flag_error(err, MMK_E_DOMAIN, err_at(3, j));
+    const int k0 = nptr[j], k1 = nptr[j + 1];
+    double nbr = 0.0;
+    // neighbours in batches of four: indices, then values, then the in-order
+    // sums (same order as one at a time)
+    for (int t0 = k0; t0 < k1; t0 += 4) {
+        int kk[4];
+        double lk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kk[u] = (t0 + u < k1) ? nidx[t0 + u] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lk[u] = (kk[u] >= 0) ? (double)lam[kk[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (kk[u] < 0) break;
+            nbr += lk[u];
+            if (kk[u] > j) pen += (lj - lk[u]) * (lj - lk[u]);
+        }
+    }
+    if (flags & MMK_PET_UPDATE) {
+        const double c = lj * bj;
+        double out;
+        if (mu == 0.0) {
+            out = c;
+        } else {
+            const double deg = (double)(k1 - k0);
+            const double a = -2.0 * mu * deg;
+            const double b = mu * (deg * lj + nbr) - 1.0;
+            const double disc = b * b - 4.0 * a * c;
+            if (disc < 0.0) flag_error(err, MMK_E_NUMERICS, err_at(2, j));
+            const double sq = sqrt(disc);
+            out = (b < 0.0) ? 2.0 * c / (sq - b) : (-b - sq) / ((a < 0.0) ? 2.0 * a : -1.0);
+        }
+        lam_out[j] = (T)fmax(out, num<T>::floor());
+    }
+    return pen;
+}
+
+// f = loglik - mu/2 * penalty, assembled by the last CTA from the per-CTA
+// penalty partials (fixed order).  The loglik is red[p], or -- when the
+// forward kernel skipped its own final reduction (llpart != nullptr) -- the
+// same fixed-order sum of its nll per-CTA partials, formed here.
+__device__ __forceinline__ void pixel_objective(double pen_block, double mu,
+                                                const double* __restrict__ red, long long p,
+                                                double* __restrict__ penpart,
+                                                unsigned int* counter, double* f_dev,
+                                                double* sc, const double* llpart = nullptr,
+                                                int nll = 0) {
+    if (threadIdx.x == 0) penpart[blockIdx.x] = pen_block;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(penpart, gridDim.x, sc);
+        double ll = 0.0;
+        if (llpart) {
+            __syncthreads();   // sc reuse
+            ll = block_sum_array(llpart, nll, sc);
+        }
+        if (threadIdx.x == 0) {
+            double f = llpart ? ll : red[p];
+            if (mu > 0.0) f -= 0.5 * mu * tot;
+            *f_dev = f;
+        }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPixThreads)
 pet_pixel_kernel(const T* __restrict__ lam, T* __restrict__ lam_out, long long p,
@@ -188,46 +288,49 @@ pet_pixel_kernel(const T* __restrict__ lam, T* __restrict__ lam_out, long long p
                  unsigned int* counter, double* f_dev, int64_t* err) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double pen = 0.0;
-    if (j < p) {
-        const double lj = (double)lam[j];
-        if ((flags & MMK_PET_CHECK_POSITIVE) && !(lj > 0.0)) flag_error(err, MMK_E_DOMAIN, err_at(3, j));
-        const int k0 = nptr[j], k1 = nptr[j + 1];
-        double nbr = 0.0;
-        for (int t = k0; t < k1; ++t) {
-            const int k = nidx[t];
-            const double lk = (double)lam[k];
-            nbr += lk;
-            if (k > j) pen += (lj - lk) * (lj - lk);
-        }
-        if (flags & MMK_PET_UPDATE) {
-            const double c = lj * red[j];
-            double out;
-            if (mu == 0.0) {
-                out = c;
-            } else {
-                const double deg = (double)(k1 - k0);
-                const double a = -2.0 * mu * deg;
-                const double b = mu * (deg * lj + nbr) - 1.0;
-                const double disc = b * b - 4.0 * a * c;
-                if (disc < 0.0) flag_error(err, MMK_E_NUMERICS, err_at(2, j));
-                const double sq = sqrt(disc);
-                out = (b < 0.0) ? 2.0 * c / (sq - b) : (-b - sq) / ((a < 0.0) ? 2.0 * a : -1.0);
-            }
-            lam_out[j] = (T)fmax(out, num<T>::floor());
-        }
-    }
+    if (j < p)
+        pen = pixel_update(lam, lam_out, nptr, nidx, mu, flags, j,
+                           (flags & MMK_PET_UPDATE) ? red[j] : 0.0, err);
     if (!(flags & MMK_PET_OBJECTIVE)) return;
     __shared__ double sc[32];
-    const double bs = block_sum(pen, sc);
-    if (threadIdx.x == 0) penpart[blockIdx.x] = bs;
-    if (arrive_last(counter, gridDim.x)) {
-        const double tot = block_sum_array(penpart, gridDim.x, sc);
-        if (threadIdx.x == 0) {
-            double f = red[p];
-            if (mu > 0.0) f -= 0.5 * mu * tot;
-            *f_dev = f;
-        }
+    pixel_objective(block_sum(pen, sc), mu, red, p, penpart, counter, f_dev, sc);
+}
+
+// single-GPU sparse phase B: a CTA back-projects kFusedPix pixels (kSubW
+// lanes per CSC column, the order of pet_sback_kernel, so b_j is bitwise that
+// kernel's) into shared memory, then warp 0 applies their pixel updates --
+// b never goes through memory
+template <typename T>
+__global__ void __launch_bounds__(kPixThreads)
+pet_sback_pixel_kernel(const int32_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
+                       const T* __restrict__ cval, const double* __restrict__ ratio,
+                       const T* __restrict__ lam, T* __restrict__ lam_out, long long p,
+                       const int32_t* __restrict__ nptr, const int32_t* __restrict__ nidx,
+                       double mu, int flags, const double* __restrict__ red,
+                       double* __restrict__ penpart, unsigned int* counter, double* f_dev,
+                       int64_t* err, const double* __restrict__ llpart, int nll) {
+    __shared__ double bsh[kFusedPix];
+    __shared__ double sc[32];
+    const int q = threadIdx.x % kSubW;
+    const int slot = threadIdx.x / kSubW;
+    const long long j0 = (long long)blockIdx.x * kFusedPix;
+    const long long jj = j0 + slot;
+    double b = 0.0;
+    if (jj < p && (flags & MMK_PET_UPDATE))
+        b = gather_dot<kSubW>(cidx, cval, ratio, cptr[jj] + q, cptr[jj + 1]);
+#pragma unroll
+    for (int o = kSubW / 2; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (q == 0) bsh[slot] = b;
+    __syncthreads();
+    double pen = 0.0;
+    if (threadIdx.x < kFusedPix) {
+        const long long j = j0 + threadIdx.x;
+        if (j < p) pen = pixel_update(lam, lam_out, nptr, nidx, mu, flags, j, bsh[threadIdx.x], err);
     }
+    if (!(flags & MMK_PET_OBJECTIVE)) return;
+    static_assert(kFusedPix == 32, "one warp of pixel updates");
+    if (threadIdx.x < 32) pen = warp_sum(pen);
+    pixel_objective(pen, mu, red, p, penpart, counter, f_dev, sc, llpart, nll);
 }
 
 struct PetWs {
@@ -253,7 +356,7 @@ void back_plan(long long d, long long p, int* ncb, int* splits, long long* rps) 
 
 size_t pet_ws_layout(long long d, long long p, void* base, PetWs* L) {
     const int nfwd = ceil_div(d > 0 ? d : 1, kRaysPB);
-    const int npix = ceil_div(p, kPixThreads);
+    const int npix = ceil_div(p, kFusedPix);   // penalty partials (>= pixel CTAs)
     int ncb, splits;
     long long rps;
     back_plan(d, p, &ncb, &splits, &rps);
@@ -334,7 +437,9 @@ int check_ws(long long d, long long p, void* ws, size_t ws_bytes, PetWs* L) {
 // writes red[j] directly -- no partials, deterministic by construction.
 
 // warp per ray: m_i over the CSR row, ratio, loglik; last block -> red[p]
-template <typename T>
+// TAIL: the last CTA sums the loglik partials into red[p]; without it the
+// partials stay in llpart for the fused phase-B kernel
+template <typename T, bool TAIL = true>
 __global__ void __launch_bounds__(kRays * 32)
 pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
                 const T* __restrict__ rval, const T* __restrict__ y, const T* __restrict__ lam,
@@ -346,9 +451,7 @@ pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ri
     const long long i = (long long)blockIdx.x * kRays + warp;
     double l = 0.0;
     if (i < d) {
-        double m = 0.0;
-        for (int t = rptr[i] + lane; t < rptr[i + 1]; t += 32)
-            m = fma((double)rval[t], (double)lam[ridx[t]], m);
+        double m = gather_dot<32>(ridx, rval, lam, rptr[i] + lane, rptr[i + 1]);
         m = warp_sum(m);
         if (lane == 0) {
             const double yi = (double)y[i];
@@ -369,6 +472,7 @@ pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ri
         for (int w = 0; w < kRays; ++w) s2 += ll[w];
         llpart[blockIdx.x] = s2;
     }
+    if (!TAIL) return;
     if (arrive_last(counter, gridDim.x)) {
         const double t = block_sum_array(llpart, gridDim.x, sc);
         if (threadIdx.x == 0) red[p] = t;
@@ -377,7 +481,6 @@ pet_sfwd_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ ri
 
 // kSubW lanes per pixel: b_j over the CSC column (lane q takes entries
 // q, q + kSubW, ...), combined by a fixed xor-shuffle tree -> red[j]
-constexpr int kSubW = 8;
 template <typename T>
 __global__ void __launch_bounds__(256)
 pet_sback_kernel(const int32_t* __restrict__ cptr, const int32_t* __restrict__ cidx,
@@ -387,10 +490,7 @@ pet_sback_kernel(const int32_t* __restrict__ cptr, const int32_t* __restrict__ c
     const long long j = g / kSubW;
     const int q = (int)(g % kSubW);
     double b = 0.0;
-    if (j < p) {
-        const int t1 = cptr[j + 1];
-        for (int t = cptr[j] + q; t < t1; t += kSubW) b = fma((double)cval[t], ratio[cidx[t]], b);
-    }
+    if (j < p) b = gather_dot<kSubW>(cidx, cval, ratio, cptr[j] + q, cptr[j + 1]);
 #pragma unroll
     for (int o = kSubW / 2; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
     if (j < p && q == 0) red[j] = b;
@@ -407,7 +507,7 @@ struct SparseWs {
 // partials at the same offsets as pet_ws_layout
 size_t sparse_ws_layout(long long d, long long p, void* base, SparseWs* L) {
     const int nfwd = ceil_div(d > 0 ? d : 1, kRays);
-    const int npix = ceil_div(p, kPixThreads);
+    const int npix = ceil_div(p, kFusedPix);
     size_t off = 256;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -549,6 +649,10 @@ extern "C" int mmk_pet_sparse_iter_a(int dtype, const int32_t* rptr, const int32
     return MMK_E_SHAPE;
 }
 
+// single-GPU sparse iteration: the forward projection, then ONE kernel that
+// back-projects each pixel's CSC column and applies the pixel update (the
+// per-pixel b_j never goes through memory; results bitwise equal to
+// iter_a + iter_b, which a sharded caller uses to all-reduce b in between)
 extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t* ridx,
                                    const void* rval, const int32_t* cptr, const int32_t* cidx,
                                    const void* cval, const void* y, const void* lam,
@@ -556,9 +660,42 @@ extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t
                                    const int32_t* nbr_idx, double mu, int flags, void* ws,
                                    size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                                    void* stream) {
-    int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lam, d, p, ws,
-                                   ws_bytes, red, err_dev, stream);
-    if (rc) return rc;
-    return mmk_pet_iter_b(dtype, lam, lam_out, p, nbr_ptr, nbr_idx, mu, flags, red, ws, ws_bytes,
-                          f_dev, err_dev, stream);
+    if (d == 0 || (dtype != MMK_F32 && dtype != MMK_F64)) {
+        int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lam, d, p,
+                                       ws, ws_bytes, red, err_dev, stream);
+        if (rc) return rc;
+        return mmk_pet_iter_b(dtype, lam, lam_out, p, nbr_ptr, nbr_idx, mu, flags, red, ws,
+                              ws_bytes, f_dev, err_dev, stream);
+    }
+    if (p < 1 || d < 0) {
+        mmk_host::set_error("bad sparse PET shape d=%lld p=%lld", (long long)d, (long long)p);
+        return MMK_E_SHAPE;
+    }
+    size_t need = 0;
+    mmk_pet_sparse_ws_bytes(dtype, d, p, &need);
+    if (ws_bytes < need) {
+        mmk_host::set_error("sparse PET workspace too small: %zu < %zu", ws_bytes, need);
+        return MMK_E_SHAPE;
+    }
+    SparseWs L;
+    sparse_ws_layout(d, p, ws, &L);
+    PetWs Lb;
+    pet_ws_layout(0, p, ws, &Lb);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto run = [&](auto tag) -> int {
+        using T = decltype(tag);
+        MMK_LAUNCH("pet_sfwd", st,
+                   (pet_sfwd_kernel<T, false><<<L.nfwd, kRays * 32, 0, st>>>(
+                       rptr, ridx, (const T*)rval, (const T*)y, (const T*)lam, d, p, L.ratio,
+                       L.llpart, L.counter + 1, red, err_dev)));
+        MMK_CHECK_LAUNCH("pet_sfwd_kernel");
+        MMK_LAUNCH("pet_sback_pixel", st,
+                   (pet_sback_pixel_kernel<T><<<ceil_div(p, kFusedPix), kPixThreads, 0, st>>>(
+                       cptr, cidx, (const T*)cval, L.ratio, (const T*)lam, (T*)lam_out, p,
+                       nbr_ptr, nbr_idx, mu, flags, red, Lb.penpart, Lb.counter, f_dev,
+                       err_dev, L.llpart, L.nfwd)));
+        MMK_CHECK_LAUNCH("pet_sback_pixel");
+        return MMK_OK;
+    };
+    return dtype == MMK_F32 ? run(float{}) : run(double{});
 }
