@@ -341,6 +341,11 @@ int mmk_mds_tri_engine_create(const float *packed, int64_t t0, int64_t t1, float
 int mmk_engine_run(void *engine, void *stream);
 void mmk_engine_destroy(void *engine);
 
+/* MMX1 loader (replaces the host decode of io.py:90-106 `_load_binary` for
+ * device runs): narrow n landed fp64 values to fp32, round-to-nearest-even
+ * (numpy astype(float32)); src/dst 16-byte aligned device buffers. */
+int mmk_f64_to_f32(const double *src, float *dst, int64_t n, void *stream);
+
 /* Known-answer self-test of the tcgen05 building blocks (TMA 128B-swizzle
  * tiles, K-/MN-major UMMA descriptors, kind::tf32 MMA, TMEM loads):
  *   D1[128x64] = A[128x64] B[64x64]^T,  D2[128x32] = A B[:, :32],

@@ -16,6 +16,7 @@ from .datasets import (PetGeometry, build_neighborhoods, build_system_matrix,
 from .driver import MmConfig, MmProblem, MmTrace, relative_change, run_mm
 from .errors import (DeviceError, DomainError, InputError, MatrixFormatError, MmkitError,
                      MonotonicityError, NonFiniteError, NumericsError, ShapeError)
+from .io import load_matrix_device, read_mmx_header
 from .kernels import elementwise, matmul, matvec, tree_reduce_sum
 from .mds import (MdsProblem, PackedMdsProblem, anchor_configuration, mds_run, mds_update, stress,
                   stress_gradient)

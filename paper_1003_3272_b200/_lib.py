@@ -33,6 +33,7 @@ _SIGS = {
     "mmk_last_error": ([], _c.c_char_p),
     "mmk_prof_enable": ([_i32], _i32),
     "mmk_prof_report": ([_c.c_char_p, _sz], _i32),
+    "mmk_f64_to_f32": ([_vp, _vp, _i64, _vp], _i32),
     "mmk_nnmf_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_nnmf_reduce_len": ([_i64, _i64], _i64),
     "mmk_nnmf_iter_a": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp,
