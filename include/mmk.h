@@ -98,6 +98,12 @@ int mmk_nnmf_update_v(int dtype, const void *X, int64_t ldx, const void *V, cons
 int mmk_nnmf_update_w(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
                       void *W_out, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,
                       double *red, int64_t *err_dev, void *stream);
+/* Gradient of ||X - VW||^2 (nnmf_gradient, nnmf.py:113-119):
+ * GV = 2 (V W - X) W^T (m x r), GW = 2 V^T (V W - X) (r x n); red as for
+ * mmk_nnmf_update_w (reduce_len doubles). */
+int mmk_nnmf_gradient(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
+                      void *GV, void *GW, int64_t m, int64_t n, int64_t r, void *ws,
+                      size_t ws_bytes, double *red, int64_t *err_dev, void *stream);
 
 /* ------------------------------------------------------------------------
  * NNMF, Poisson log fit (nnmf.py:178-265), rank <= 64.  Square-root
@@ -149,6 +155,13 @@ int mmk_pet_iter(int dtype, const void *E, int64_t lde, const void *y, const voi
                  void *lam_out, int64_t d, int64_t p, const int32_t *nbr_ptr,
                  const int32_t *nbr_idx, double mu, int flags, void *ws, size_t ws_bytes,
                  double *red, double *f_dev, int64_t *err_dev, void *stream);
+/* Gradient of the penalized loglikelihood (pet_penalized_gradient,
+ * pet.py:349-360) from red = [b | loglik] left by mmk_pet_iter_a /
+ * mmk_pet_sparse_iter_a at lam:  grad_j = b_j - colsum_j
+ * - mu (deg_j lam_j - sum_{k in N(j)} lam_k);  colsum fp64 (p). */
+int mmk_pet_gradient(int dtype, const void *lam, void *grad, int64_t p, const int32_t *nbr_ptr,
+                     const int32_t *nbr_idx, double mu, const double *colsum, const double *red,
+                     void *stream);
 
 /* Sparse system matrix variant (the Siddon matrix is ~1 % nonzero): E as
  * CSR by rays (rptr d+1, ridx, rval) for the forward projection and CSC by
@@ -188,8 +201,11 @@ int mmk_pet_siddon(const double *det, int n_det, int side, const double *lines, 
  *   f_dev = sum_{i in rows, j > i} w_ij (y_ij - d_ij)^2   (stress partial)
  * flags: MMK_MDS_UPDATE, MMK_MDS_OBJECTIVE.  Coupled coincident points
  * (d_ij = 0, w_ij y_ij > 0) set NUMERICS with index i*n + j.
+ * MMK_MDS_GRADIENT instead writes the stress gradient (stress_gradient,
+ * mds.py:147-167) 2 (theta_i (w_i. - z_i.) - sum_j (w_ij - z_ij) theta_j)
+ * to theta_out; coincident points with w_ij > 0 set NUMERICS.
  * ---------------------------------------------------------------------- */
-enum { MMK_MDS_UPDATE = 1, MMK_MDS_OBJECTIVE = 2 };
+enum { MMK_MDS_UPDATE = 1, MMK_MDS_OBJECTIVE = 2, MMK_MDS_GRADIENT = 4 };
 int mmk_mds_ws_bytes(int dtype, int64_t n, int64_t dim, int64_t rows, size_t *out);
 int mmk_mds_iter(int dtype, const void *Y, const void *Wt, int64_t ldy, const double *wsum,
                  const void *theta, void *theta_out, int64_t ldo, int64_t dim, int64_t n,

@@ -342,6 +342,22 @@ def mds_update(theta, md, threads=1):                 # mds.py:114-144
     return (theta * (md.wsum + z_sums)[None, :] + spread) / (2.0 * md.wsum)[None, :]
 
 
+def mds_stress_gradient(theta, md, threads=1):         # mds.py:147-167
+    theta = _f64(theta)
+    d2 = _pair_d2(theta, threads)
+    w_off = md.w * ~np.eye(md.n, dtype=bool)
+    bad = np.nonzero((d2 <= 0.0) & (w_off > 0.0))
+    if bad[0].size:
+        raise OracleError("NumericsError",
+                          f"objects {int(bad[0][0])} and {int(bad[1][0])} coincide")
+    coef = np.zeros_like(w_off)
+    m = w_off > 0.0
+    coef[m] = w_off[m] * (1.0 - md.y[m] / np.sqrt(d2[m]))
+    row = matvec(coef, np.ones(md.n), threads=threads)
+    pulled = matmul(theta, coef, threads=threads)
+    return 2.0 * (theta * row[None, :] - pulled)
+
+
 # --------------------------------------------------------------------------
 # driver restatement (driver.py:101-149) for fixed-count parity runs
 def run(objective, step, state0, direction, max_iters, epsilon=1e-300,

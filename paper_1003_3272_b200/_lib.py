@@ -20,7 +20,7 @@ ABI_VERSION = 1
 
 MMK_F32, MMK_F64 = 0, 1
 MMK_PET_UPDATE, MMK_PET_OBJECTIVE, MMK_PET_CHECK_POSITIVE = 1, 2, 4
-MMK_MDS_UPDATE, MMK_MDS_OBJECTIVE = 1, 2
+MMK_MDS_UPDATE, MMK_MDS_OBJECTIVE, MMK_MDS_GRADIENT = 1, 2, 4
 ERR_SITE_SHIFT = 48   # include/mmk.h: err index = site << 48 | offending index
 
 _lock = threading.Lock()
@@ -34,6 +34,9 @@ _SIGS = {
     "mmk_prof_enable": ([_i32], _i32),
     "mmk_prof_report": ([_c.c_char_p, _sz], _i32),
     "mmk_f64_to_f32": ([_vp, _vp, _i64, _vp], _i32),
+    "mmk_nnmf_gradient": ([_i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp,
+                           _vp, _vp], _i32),
+    "mmk_pet_gradient": ([_i32, _vp, _vp, _i64, _vp, _vp, _dbl, _vp, _vp, _vp], _i32),
     "mmk_nnmf_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_nnmf_reduce_len": ([_i64, _i64], _i64),
     "mmk_nnmf_iter_a": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp,

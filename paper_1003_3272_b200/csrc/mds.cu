@@ -36,7 +36,8 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int seg = warp % SPLIT, rw = warp / SPLIT;
     const long long lbase = ((long long)blockIdx.x * (kWarps / SPLIT) + rw) * RPW;  // local row
-    const bool do_update = flags & MMK_MDS_UPDATE;
+    const bool do_update = flags & (MMK_MDS_UPDATE | MMK_MDS_GRADIENT);
+    const bool do_grad = flags & MMK_MDS_GRADIENT;
     const bool do_obj = flags & MMK_MDS_OBJECTIVE;
 
     T ti[RPW][DM];
@@ -75,13 +76,11 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
             }
             const T wy = w * y;
             T z = T(0);
-            if (wy > T(0)) {
-                if (d2 <= T(0)) {
-                    if (do_update) flag_error(err, MMK_E_NUMERICS, err_at(1, gi * n + j));
-                } else {
-                    z = wy / sqrt(d2);
-                }
-            }
+            // the update needs d > 0 where w y > 0 (mds.py:127-128), the
+            // gradient wherever w > 0 (stress_gradient mds.py:154-156)
+            if (d2 <= T(0) && (do_grad ? w > T(0) : (do_update && wy > T(0))))
+                flag_error(err, MMK_E_NUMERICS, err_at(1, gi * n + j));
+            if (wy > T(0) && d2 > T(0)) z = wy / sqrt(d2);
             zs[rr] += z;
             const T c = w - z;
 #pragma unroll
@@ -137,6 +136,15 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
             if (do_update && lane == 0) {
                 const long long gi = row0 + li;
                 const double ws = wsum[gi];
+                if (do_grad) {   // 2 (theta_i (w_i. - z_i.) - sum_j (w_ij - z_ij) theta_j)
+                    const double row = ws - (double)zs[rr];
+#pragma unroll
+                    for (int k = 0; k < DM; ++k)
+                        if (k < dim)
+                            theta_out[(long long)k * ldo + li] =
+                                (T)(2.0 * ((double)ti[rr][k] * row - (double)acc[rr][k]));
+                    continue;
+                }
                 const double scale = ws + (double)zs[rr];
                 const double inv = 2.0 * ws;
 #pragma unroll

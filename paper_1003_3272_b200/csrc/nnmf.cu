@@ -30,7 +30,7 @@ using namespace mmk;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-enum { VSTEP_UPDATE = 1, VSTEP_RESID = 2 };
+enum { VSTEP_UPDATE = 1, VSTEP_RESID = 2, VSTEP_GRAD = 4 };
 
 // ---------------------------------------------------------------------------
 // G[a][b] = sum_c A(a, c) A(b, c); VEC_ROWS: A is r x len (vectors are rows,
@@ -267,6 +267,10 @@ nnmf_vstep_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ 
 #pragma unroll
                 for (int l = 0; l < RMAX; ++l)
                     if (l < r) den = fma((double)v[rr][l], GW[l * r + k], den);
+                if (flags & VSTEP_GRAD) {   // 2 (V G_W - X W^T) = 2 (V W - X) W^T
+                    Vout[i * r + k] = (T)(2.0 * (den - (double)qs[warp][rr][k]));
+                    continue;
+                }
                 const double vk = (double)V[i * r + k];
                 Vout[i * r + k] = (T)(vk * ((double)qs[warp][rr][k] / (den + kDenomGuard)));
             }
@@ -330,7 +334,8 @@ __global__ void nnmf_wreduce_kernel(const double* __restrict__ part, int S, long
     red[t] = s;
 }
 
-template <typename T>
+// GRAD: write 2 (G_V W - V^T X) = 2 V^T (V W - X) instead of the update
+template <typename T, bool GRAD = false>
 __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
                                     int r, const double* __restrict__ red, double* f_dev) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -342,7 +347,10 @@ __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wou
     const double* G = red + rn + (long long)k * r;
     double den = 0.0;
     for (int l = 0; l < r; ++l) den = fma(G[l], (double)W[(long long)l * n + j], den);
-    Wout[t] = (T)((double)W[t] * (red[t] / (den + kDenomGuard)));
+    if (GRAD)
+        Wout[t] = (T)(2.0 * (den - red[t]));
+    else
+        Wout[t] = (T)((double)W[t] * (red[t] / (den + kDenomGuard)));
 }
 
 // Rank-64 W finish: a block owns 64 columns; G^T and the W slab (fp64) sit in
@@ -586,7 +594,7 @@ struct Args {
     double* f_dev;
     int64_t* err;
     cudaStream_t st;
-    int mode;  // 0 iter_a, 1 update_v, 2 objective, 3 update_w (a + b)
+    int mode;  // 0 iter_a, 1 update_v, 2 objective, 3 update_w (a + b), 4 gradient
 };
 
 template <typename T, int RMAX>
@@ -607,11 +615,13 @@ struct RunA {
                                       a.red, a.st);
             }
         }
-        if (a.mode == 0 || a.mode == 1 || a.mode == 2) {
+        if (a.mode == 0 || a.mode == 1 || a.mode == 2 || a.mode == 4) {
             if (a.m > 0) {
                 if (a.mode != 2) KK::gram_w(W, a.n, a.r, P, L, a.st);
-                int flags = (a.mode == 0) ? (VSTEP_UPDATE | VSTEP_RESID)
-                                          : (a.mode == 1 ? VSTEP_UPDATE : VSTEP_RESID);
+                int flags = (a.mode == 0)   ? (VSTEP_UPDATE | VSTEP_RESID)
+                            : a.mode == 1 ? VSTEP_UPDATE
+                            : a.mode == 4 ? (VSTEP_UPDATE | VSTEP_GRAD)
+                                          : VSTEP_RESID;
                 double* res_out = a.mode == 0 ? a.red + rn + (long long)a.r * a.r : a.f_dev;
                 KK::vstep(X, a.ldx, V, W, (T*)a.V_out, a.m, a.n, a.r, flags, P, L, res_out, a.st);
             } else if (a.mode == 0) {
@@ -621,8 +631,8 @@ struct RunA {
             }
             MMK_CHECK_LAUNCH("nnmf_vstep");
         }
-        if (a.mode == 0 || a.mode == 3) {
-            // W step uses the new V for iter_a, the given V for update_w
+        if (a.mode == 0 || a.mode == 3 || a.mode == 4) {
+            // W step uses the new V for iter_a, the given V for update_w / gradient
             const T* Vn = a.mode == 0 ? (const T*)a.V_out : V;
             if (a.m > 0) {
                 KK::gram_v(Vn, a.m, a.r, P, L, a.red + rn, a.st);
@@ -631,7 +641,7 @@ struct RunA {
                 cudaMemsetAsync(a.red, 0, sizeof(double) * (size_t)(rn + (long long)a.r * a.r),
                                 a.st);
             }
-            if (a.mode == 3)
+            if (a.mode == 3 || a.mode == 4)
                 cudaMemsetAsync(a.red + rn + (long long)a.r * a.r, 0, sizeof(double), a.st);
             MMK_CHECK_LAUNCH("nnmf_wstep");
         }
@@ -641,8 +651,15 @@ struct RunA {
 
 template <typename T>
 int finish_b(const void* W, void* W_out, long long n, int r, const double* red, double* f_dev,
-             cudaStream_t st) {
+             cudaStream_t st, bool grad = false) {
     const long long rn = (long long)r * n;
+    if (grad) {
+        MMK_LAUNCH("nnmf_wgrad", st,
+                   (nnmf_wfinish_kernel<T, true><<<ceil_div(rn, 256), 256, 0, st>>>(
+                       (const T*)W, (T*)W_out, n, r, red, f_dev)));
+        MMK_CHECK_LAUNCH("nnmf_wfinish_kernel<grad>");
+        return MMK_OK;
+    }
     if (r == 64) {
         static bool attr = false;
         if (!attr) {
@@ -768,4 +785,21 @@ extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const vo
     rc = run_a(dtype, a);
     if (rc) return rc;
     return mmk_nnmf_iter_b(dtype, W, W_out, n, r, red, nullptr, err_dev, stream);
+}
+
+// grad_V = 2 (V W - X) W^T, grad_W = 2 V^T (V W - X) (reference nnmf_gradient
+// nnmf.py:113-119) in the Gram form 2 (V G_W - X W^T), 2 (G_V W - V^T X):
+// products accumulated as in the update kernels, differences in fp64
+extern "C" int mmk_nnmf_gradient(int dtype, const void* X, int64_t ldx, const void* V,
+                                 const void* W, void* GV, void* GW, int64_t m, int64_t n,
+                                 int64_t r, void* ws, size_t ws_bytes, double* red,
+                                 int64_t* err_dev, void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    if (rc) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Args a{X, V, W, GV, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev, st, 4};
+    rc = run_a(dtype, a);
+    if (rc) return rc;
+    return dtype == MMK_F32 ? finish_b<float>(W, GW, n, (int)r, red, nullptr, st, true)
+                            : finish_b<double>(W, GW, n, (int)r, red, nullptr, st, true);
 }

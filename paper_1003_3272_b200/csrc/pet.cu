@@ -333,6 +333,24 @@ pet_sback_pixel_kernel(const int32_t* __restrict__ cptr, const int32_t* __restri
     pixel_objective(pen, mu, red, p, penpart, counter, f_dev, sc, llpart, nll);
 }
 
+// grad_j = b_j - colsum_j - mu (deg_j lam_j - nbr_j)   (pet.py:349-360)
+template <typename T>
+__global__ void __launch_bounds__(kPixThreads)
+pet_grad_kernel(const T* __restrict__ lam, T* __restrict__ grad, long long p,
+                const int32_t* __restrict__ nptr, const int32_t* __restrict__ nidx, double mu,
+                const double* __restrict__ colsum, const double* __restrict__ red) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p) return;
+    double g = red[j] - colsum[j];
+    if (mu > 0.0) {
+        const int k0 = nptr[j], k1 = nptr[j + 1];
+        double nbr = 0.0;
+        for (int t = k0; t < k1; ++t) nbr += (double)lam[nidx[t]];
+        g -= mu * ((double)(k1 - k0) * (double)lam[j] - nbr);
+    }
+    grad[j] = (T)g;
+}
+
 struct PetWs {
     unsigned int* counter;    // [0] pixel kernel, [1] forward kernel
     unsigned int* bcounters;  // one per back-projection column block
@@ -698,4 +716,24 @@ extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t
         return MMK_OK;
     };
     return dtype == MMK_F32 ? run(float{}) : run(double{});
+}
+
+extern "C" int mmk_pet_gradient(int dtype, const void* lam, void* grad, int64_t p,
+                                const int32_t* nbr_ptr, const int32_t* nbr_idx, double mu,
+                                const double* colsum, const double* red, void* stream) {
+    if (p < 1 || (dtype != MMK_F32 && dtype != MMK_F64)) {
+        mmk_host::set_error("bad PET gradient call: dtype %d p=%lld", dtype, (long long)p);
+        return MMK_E_SHAPE;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == MMK_F32)
+        MMK_LAUNCH("pet_grad", st,
+                   (pet_grad_kernel<float><<<ceil_div(p, kPixThreads), kPixThreads, 0, st>>>(
+                       (const float*)lam, (float*)grad, p, nbr_ptr, nbr_idx, mu, colsum, red)));
+    else
+        MMK_LAUNCH("pet_grad", st,
+                   (pet_grad_kernel<double><<<ceil_div(p, kPixThreads), kPixThreads, 0, st>>>(
+                       (const double*)lam, (double*)grad, p, nbr_ptr, nbr_idx, mu, colsum, red)));
+    MMK_CHECK_LAUNCH("pet_grad_kernel");
+    return MMK_OK;
 }

@@ -477,20 +477,18 @@ def _host_d2(theta):
 
 
 def stress_gradient(theta, problem, backend=SERIAL):
-    """Analytic stress gradient (host fp64 helper)."""
+    """Analytic stress gradient (mds.py:147-167), on the device: the rows
+    kernel with MMK_MDS_GRADIENT.  Coincident points with positive weight
+    raise the reference's NumericsError."""
     _check_theta(theta, problem)
-    t = _host(theta)
-    d2 = _host_d2(t)
-    w_off = problem.weights * ~np.eye(problem.q, dtype=bool)
-    bad = np.argwhere((d2 <= 0.0) & (w_off > 0.0))
-    if bad.size:
-        raise NumericsError(f"objects {bad[0][0]} and {bad[0][1]} coincide but are coupled "
-                            "with positive weight * dissimilarity; the surrogate is undefined "
-                            "there")
-    coef = np.zeros_like(w_off)
-    m = w_off > 0.0
-    coef[m] = w_off[m] * (1.0 - problem.dissimilarities[m] / np.sqrt(d2[m]))
-    return 2.0 * (t * coef.sum(axis=1)[None, :] - t @ coef)
+    if isinstance(problem, PackedMdsProblem):
+        raise ShapeError("stress_gradient takes a dense MdsProblem")
+    mm = _GpuMds(problem, backend)
+    th = mm.device_state(theta)
+    out = mm.torch.empty_like(th)
+    mm._iterate(th, out, mm.status.f_ptr, mm.status.err_ptr, _lib.MMK_MDS_GRADIENT)
+    mm._check_error()
+    return A.to_user(out, theta)
 
 
 def mds_surrogate(theta, theta_n, problem):

@@ -331,15 +331,21 @@ def nnmf_poisson_run(problem, config, backend=SERIAL, state0=None):
     return FactorPair(A.to_user(state.v, problem.x), A.to_user(state.w, problem.x)), trace
 
 
-# ---------------------------------------------------------------------------
-# host-side fp64 helpers for property tests (not on the iteration path)
 def nnmf_gradient(x, v, w, backend=SERIAL):
-    """Gradient of ||X - VW||^2 with respect to (V, W)."""
-    x, v, w = (np.asarray(a, dtype=np.float64) for a in (x, v, w))
-    resid = v @ w - x
-    return 2.0 * resid @ w.T, 2.0 * v.T @ resid
+    """Gradient of ||X - VW||^2 with respect to (V, W) (nnmf.py:113-119):
+    (2 (VW - X) W^T, 2 V^T (VW - X)), on the device (``mmk_nnmf_gradient``)."""
+    m, n, r = _conform(x, v, w)
+    ops = _Ops(backend, m, n, r)
+    xd, vd, wd = ops.put(x), ops.put(v), ops.put(w)
+    gv, gw = ops.torch.empty_like(vd), ops.torch.empty_like(wd)
+    _lib.call("mmk_nnmf_gradient", ops.code, _lib.ptr(xd), xd.stride(0), _lib.ptr(vd),
+              _lib.ptr(wd), _lib.ptr(gv), _lib.ptr(gw), m, n, r, _lib.ptr(ops.ws),
+              ops.ws.numel(), _lib.ptr(ops.red), ops.status.err_ptr, ops.stream())
+    return A.to_user(gv, v), A.to_user(gw, w)
 
 
+# ---------------------------------------------------------------------------
+# host-side fp64 helper for majorization property tests (not on the iteration path)
 def nnmf_surrogate(x, v, w, v_n, w_n):
     """Separable majorizer of the Frobenius loss at anchor (v_n, w_n)."""
     x, v, w, v_n, w_n = (np.asarray(A.to_user(a, np.empty(0)) if A.is_torch(a) else a,

@@ -445,17 +445,43 @@ def _host(a):
 
 
 def pet_penalized_gradient(lam, problem, backend=SERIAL):
-    """Analytic gradient of the penalized objective (host fp64)."""
-    lam, e, y = _host(lam), _host(problem.e), _host(problem.y)
-    means = e @ lam
-    if np.any((y > 0.0) & (means == 0.0)):
-        raise NumericsError("a ray with positive counts has zero expected counts")
-    ratio = np.where(y > 0.0, y / np.where(y > 0.0, means, 1.0), 0.0)
-    grad = e.T @ ratio - problem.col_sums
-    if problem.mu > 0.0:
-        nbr = np.array([lam[a].sum() if len(a) else 0.0 for a in problem.neighborhoods])
-        grad -= problem.mu * (problem.degrees * lam - nbr)
-    return grad
+    """Analytic gradient of the penalized objective (pet.py:349-360) on the
+    device: the projection phase (dense or sparse) leaves b = E^T (y / E lam),
+    then ``mmk_pet_gradient`` forms b - colsum - mu (deg lam - nbr)."""
+    _check_lam(lam, problem)
+    mm = _GpuPet(problem, backend)
+    ld = mm.device_state(lam)
+    st, P = mm.stream(), _lib.ptr
+    if mm.sparse:
+        sa = mm.sa
+        _lib.call("mmk_pet_sparse_iter_a", mm.code, P(sa["rptr"]), P(sa["ridx"]), P(sa["rval"]),
+                  P(sa["cptr"]), P(sa["cidx"]), P(sa["cval"]), P(mm.y), P(ld), mm.d, mm.p,
+                  P(mm.ws), mm.ws.numel(), P(mm.red), mm.status.err_ptr, st)
+    else:
+        _lib.call("mmk_pet_iter_a", mm.code, P(mm.e), mm.e.stride(0), P(mm.y), P(ld), mm.d,
+                  mm.p, P(mm.ws), mm.ws.numel(), P(mm.red), mm.status.err_ptr, st)
+    grad = mm.torch.empty_like(ld)
+    _lib.call("mmk_pet_gradient", mm.code, P(ld), P(grad), mm.p, P(mm.ptr), P(mm.idx), mm.mu,
+              P(_col_sums_device(problem, mm)), P(mm.red), st)
+    mm._check_error()
+    return A.to_user(grad, lam)
+
+
+def _col_sums_device(problem, mm):
+    """Column sums of E in fp64 on the device (cached on the problem)."""
+    key = (str(mm.device), "colsum")
+    cs = problem._dev.get(key)
+    if cs is None:
+        torch = mm.torch
+        if isinstance(problem, SparsePetProblem):
+            sa = problem.sa
+            cs = torch.zeros(problem.n_pixels, dtype=torch.float64, device=mm.device)
+            cs.index_add_(0, sa["ridx"].to(mm.device).long(),
+                          sa["rval"].to(device=mm.device, dtype=torch.float64))
+        else:
+            cs = torch.from_numpy(np.ascontiguousarray(problem.col_sums)).to(mm.device)
+        problem._dev[key] = cs
+    return cs
 
 
 def pet_surrogate(lam, lam_n, problem):

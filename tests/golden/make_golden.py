@@ -176,7 +176,36 @@ def gen_poisson_c1():
          x_digest=digest(x), v0_digest=digest(v0), w0_digest=digest(w0))
 
 
+def gen_gradients():
+    """Analytic gradients (nnmf.py:113-119, pet.py:349-360, mds.py:147-167) at
+    the config starts and at the 1000-iteration goldens (near-stationary)."""
+    import importlib
+    out = {}
+    nn = importlib.import_module("mmkit_ref.nnmf")
+    pt = importlib.import_module("mmkit_ref.pet")
+    x, v0, w0 = c1_inputs()
+    c1 = np.load(os.path.join(HERE, "nnmf_c1.npz"))
+    for tag, (v, w) in (("start", (v0, w0)), ("it1000", (c1["v"], c1["w"]))):
+        gv, gw = nn.nnmf_gradient(x, v, w, backend=R.Backend.parallel(THREADS))
+        out[f"nnmf_gv_{tag}"], out[f"nnmf_gw_{tag}"] = gv, gw
+    e, y, nbrs = c2_inputs()
+    c2 = np.load(os.path.join(HERE, "pet_c2.npz"))
+    for mu in (0.0, 1e-5):
+        problem = R.PetProblem(e=e, y=y, mu=mu, neighborhoods=nbrs)
+        for tag, lam in (("start", np.ones(4096)), ("it1000", c2[f"lam_{mu:g}"])):
+            out[f"pet_g_{mu:g}_{tag}"] = pt.pet_penalized_gradient(
+                lam, problem, backend=R.Backend.parallel(THREADS))
+    md = importlib.import_module("mmkit_ref.mds")
+    c3 = np.load(os.path.join(HERE, "mds_c3.npz"))
+    diss, theta0 = c3_inputs(3)
+    problem = R.MdsProblem(weights=1.0 - np.eye(401), dissimilarities=diss, p=3)
+    for tag, th in (("start", theta0), ("it1000", c3["theta_3"])):
+        out[f"mds_g_{tag}"] = md.stress_gradient(th, problem, backend=R.Backend.parallel(THREADS))
+    save("gradients", **out)
+
+
 GENERATORS = {
+    "gradients": gen_gradients,
     "poisson_small": gen_poisson_small, "poisson_c1": gen_poisson_c1,
     "nnmf_small": gen_nnmf_small, "pet_small": gen_pet_small, "mds_small": gen_mds_small,
     "mds_c3": gen_mds_c3, "pet_c2": gen_pet_c2, "nnmf_c1": gen_nnmf_c1,

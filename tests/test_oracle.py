@@ -135,3 +135,26 @@ def test_oracle_matches_live_reference_random():
         prob = R.MdsProblem(weights=1.0 - np.eye(n), dissimilarities=y, p=r)
         assert np.array_equal(O.mds_update(theta, md), R.mds_update(theta, prob))
         assert O.mds_stress(theta, md) == R.stress(theta, prob)
+
+
+def test_gradients_bitwise():
+    """The oracle's gradient restatements equal the reference's analytic
+    gradients (nnmf.py:113-119, pet.py:349-360, mds.py:147-167) bitwise at the
+    config starts and the 1000-iteration goldens."""
+    g = G.load("gradients")
+    x, v0, w0 = G.c1_inputs()
+    c1 = G.load("nnmf_c1")
+    for tag, (v, w) in (("start", (v0, w0)), ("it1000", (c1["v"], c1["w"]))):
+        gv, gw = O.nnmf_gradient(x, v, w, threads=8)
+        assert np.array_equal(gv, g[f"nnmf_gv_{tag}"]) and np.array_equal(gw, g[f"nnmf_gw_{tag}"])
+    e, y, nbrs = G.c2_inputs()
+    c2 = G.load("pet_c2")
+    for mu in (0.0, 1e-5):
+        pd = O.PetData(e, y, mu, nbrs)
+        for tag, lam in (("start", np.ones(4096)), ("it1000", c2[f"lam_{mu:g}"])):
+            assert np.array_equal(O.pet_gradient(lam, pd, threads=8), g[f"pet_g_{mu:g}_{tag}"])
+    diss, theta0 = G.c3_inputs(3)
+    md = O.MdsData(1.0 - np.eye(401), diss, 3)
+    c3 = G.load("mds_c3")
+    for tag, th in (("start", theta0), ("it1000", c3["theta_3"])):
+        assert np.array_equal(O.mds_stress_gradient(th, md, threads=8), g[f"mds_g_{tag}"])
