@@ -315,17 +315,30 @@ def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
     wh = w0_dev.cpu().pin_memory()
     prob = M.NnmfProblem(x=xh, rank=r)   # validation outside the timed region
     cfg = M.MmConfig(max_iters=args.steps, epsilon=1e-300, monotone_tol=1e-6)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    st, tr = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(vh, wh))
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+
+    def run():
+        prob._dev.clear()                   # no cached device copy: X is uploaded in the run
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st, tr = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(vh, wh))
+        torch.cuda.synchronize()
+        return st, tr, time.perf_counter() - t0
+
+    # one untimed warm-up run (first-touch of the caching allocators, host and
+    # device), then the timed run -- the steady state of a serving process
+    st, tr, dt0 = run()
+    del st, tr
+    st, tr, dt = run()
     K = tr.iters
     h2d = xh.numel() * xh.element_size() + vh.numel() * 4 + wh.numel() * 4
     d2h = (st.v.numel() + st.w.numel()) * st.v.element_size() + 8 * (K + 1)
     return {"value": K / dt, "unit": "iterations/s", "h2d_bytes_per_step": h2d // max(K, 1),
             "d2h_bytes_per_step": d2h // max(K, 1), "iters": K,
-            "path": "nnmf_run(NnmfProblem(pinned host X), fused device loop) -> host factors"}
+            "phases_ms": {"total": 1e3 * dt, "device_loop": 1e3 * tr.wall_time,
+                          "upload_setup_readback": 1e3 * (dt - tr.wall_time),
+                          "warmup_run_total": 1e3 * dt0},
+            "path": "nnmf_run(NnmfProblem(pinned host X), fused device loop) -> host factors; "
+                    "second of two runs (the first warms the allocators)"}
 
 
 def bench_mds_large(args, torch, world, rank, dev):
