@@ -27,7 +27,8 @@
 #include <functional>
 #include <vector>
 
-#include "mmk_common.cuh"
+#include "mm_control.cuh"
+#include "small_engine.h"
 
 namespace {
 
@@ -37,10 +38,8 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cap = nullptr;
+    mmk_small::Launch persistent;   // set: one persistent-kernel launch per batch
 };
-
-__device__ __forceinline__ double as_f64(long long b) { return __longlong_as_double(b); }
-__device__ __forceinline__ long long as_bits(double d) { return __double_as_longlong(d); }
 
 // half 0 follows iteration A -> B (its objective is f(A)), half 1 follows
 // B -> A.  A stop records which slot holds the returned state (the input of
@@ -50,42 +49,13 @@ __global__ void control_kernel(cudaGraphConditionalHandle h, cudaGraphConditiona
                                int half, long long* ctl, double* trace, long long* tstamp,
                                const long long* err, mmk_stop_rule rule) {
     if (threadIdx.x != 0) return;
-    const long long it = ctl[MMK_CTL_IT];
-    const double f = as_f64(ctl[MMK_CTL_FCUR]);
-    const long long k = it - ctl[MMK_CTL_BATCH_START];
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    trace[k] = f;
-    tstamp[k] = (long long)now;
-    int reason = 0;
-    if (err[0] != 0) {
-        reason = MMK_STOP_DEVICE_ERROR;
-    } else if (!isfinite(f)) {
-        reason = MMK_STOP_NONFINITE;
-    } else if (it > 0) {
-        const double fp = as_f64(ctl[MMK_CTL_FPREV]);
-        if (rule.check_monotone && rule.sign * (f - fp) < -rule.monotone_tol * (1.0 + fabs(fp))) {
-            reason = MMK_STOP_MONOTONE;
-        } else {
-            const double rel = fabs(f - fp) / (fabs(fp) + 1.0);
-            ctl[MMK_CTL_REL] = as_bits(rel);
-            if (rel < rule.epsilon) reason = MMK_STOP_CONVERGED;
-        }
-    }
-    if (!reason && it >= rule.max_iters) reason = MMK_STOP_CAP;
-    if (reason) {
-        ctl[MMK_CTL_REASON] = reason;
-        ctl[MMK_CTL_SLOT] = half;
+    const int d = mm_control(half, ctl, trace, tstamp, err, rule, ctl_f64(ctl[MMK_CTL_FCUR]));
+    if (d == kMmStop) {
         cudaGraphSetConditional(h, 0);
         if (half == 0) cudaGraphSetConditional(hif, 0);
-        return;
-    }
-    ctl[MMK_CTL_FPREV] = as_bits(f);
-    ctl[MMK_CTL_IT] = it + 1;
-    if (half == 0) {
+    } else if (half == 0) {
         cudaGraphSetConditional(hif, 1);
-    } else if (it + 1 - ctl[MMK_CTL_BATCH_START] >= rule.batch) {
-        ctl[MMK_CTL_BATCH_START] = it + 1;
+    } else if (d == kMmPause) {
         cudaGraphSetConditional(h, 0);
     }
 }
@@ -240,6 +210,7 @@ extern "C" int mmk_engine_run(void* eng, void* stream) {
         mmk_host::set_error("null engine");
         return MMK_E_SHAPE;
     }
+    if (e->persistent.fn) return e->persistent.fn(reinterpret_cast<cudaStream_t>(stream));
     cudaError_t ce = cudaGraphLaunch(e->exec, reinterpret_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "cudaGraphLaunch");
     return MMK_OK;
@@ -251,6 +222,7 @@ extern "C" void mmk_engine_destroy(void* eng) {
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     if (e->cap) cudaStreamDestroy(e->cap);
+    if (e->persistent.scratch) cudaFree(e->persistent.scratch);
     delete e;
 }
 
@@ -261,6 +233,19 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
                                       void* ws, size_t ws_bytes, double* red, void* comm,
                                       const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
                                       int64_t* ctl, int64_t* err_dev, void** engine) {
+    if (!comm && mmk_small::nnmf_eligible(dtype, m, n, r, ldx)) {
+        // small problems: the whole loop in one persistent kernel per batch
+        Engine* e = new Engine();
+        int rc = mmk_small::nnmf_prepare(dtype, X, ldx, VA, WA, VB, WB, m, n, (int)r, rule, trace,
+                                         tstamp, ctl, err_dev, &e->persistent);
+        if (rc) {
+            delete e;
+            *engine = nullptr;
+            return rc;
+        }
+        *engine = e;
+        return MMK_OK;
+    }
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_reduce_len(n, r);
     auto iter = [=](cudaStream_t s, int dir) -> int {

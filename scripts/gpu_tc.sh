@@ -1,2 +1,4 @@
 python -c "from paper_1003_3272_b200 import build; build.build()"
-timeout 900 ncu --metrics gpu__time_duration.sum,sm__cycles_active.max --cache-control none --clock-control none -s 400 -c 60 --csv --log-file gpurun_out/warm_c1.csv python scripts/suite_probe.py > gpurun_out/ncu_warm.log 2>&1; echo ncu rc=$?
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+for k in 1 2; do python scripts/suite_probe.py 2>&1 | grep fused; done
+MMK_SMALL_ENGINE=0 python scripts/suite_probe.py 2>&1 | grep "nnmf-c1"

@@ -134,14 +134,48 @@ def test_nnmf_restartability_bitwise(fused):
                           tj.objective_values)
 
 
-def test_fused_and_per_iteration_paths_bitwise():
+@pytest.mark.parametrize("engine", ["graph", "persistent"])
+def test_fused_and_per_iteration_paths(engine, monkeypatch):
+    """The graph engine replays the per-iteration kernels: bitwise equal.  The
+    persistent small-problem engine (csrc/nnmf_small.cu) has its own fixed
+    reduction order: equal to rounding (fp64)."""
+    if engine == "graph":
+        monkeypatch.setenv("MMK_SMALL_ENGINE", "0")
     x, v0, w0 = G.c1_inputs()
     prob = M.NnmfProblem(x=x, rank=10)
     cfg = MmConfig(max_iters=50, epsilon=1e-300)
     a, ta = M.nnmf_run(prob, cfg, Backend(fused=True), state0=M.FactorPair(v0, w0))
     b, tb = M.nnmf_run(prob, cfg, Backend(fused=False), state0=M.FactorPair(v0, w0))
-    assert np.array_equal(ta.objective_values, tb.objective_values)
-    assert np.array_equal(a.v, b.v) and np.array_equal(a.w, b.w)
+    if engine == "graph":
+        assert np.array_equal(ta.objective_values, tb.objective_values)
+        assert np.array_equal(a.v, b.v) and np.array_equal(a.w, b.w)
+    else:
+        assert G.rel(ta.objective_values, tb.objective_values) <= 1e-13
+        assert G.rel(a.v, b.v) <= 1e-12 and G.rel(a.w, b.w) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp64"])
+def test_persistent_engine_pauses_and_restarts(dtype, monkeypatch):
+    """Batches (host drains of the trace) and restarts do not change the
+    persistent engine's results: 9000 iterations in 3 batches of 4096, and two
+    runs of 4500 from the first's end state, equal one run bitwise; the graph
+    engine agrees to rounding."""
+    x, v0, w0 = G.c1_inputs()
+    prob = M.NnmfProblem(x=x, rank=10)
+    be = Backend(dtype=dtype)
+    cfg = MmConfig(max_iters=9000, epsilon=1e-300, monotone_tol=1e-6)
+    full, tf = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
+    half = MmConfig(max_iters=4500, epsilon=1e-300, monotone_tol=1e-6)
+    s1, t1 = M.nnmf_run(prob, half, be, state0=M.FactorPair(v0, w0))
+    s2, t2 = M.nnmf_run(prob, half, be, state0=s1)
+    assert np.array_equal(s2.v, full.v) and np.array_equal(s2.w, full.w)
+    assert np.array_equal(np.concatenate([t1.objective_values, t2.objective_values[1:]]),
+                          tf.objective_values)
+    monkeypatch.setenv("MMK_SMALL_ENGINE", "0")
+    g, tg = M.nnmf_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
+    tol = 1e-3 if dtype == "fp32" else 1e-10
+    assert G.rel(tg.objective_values, tf.objective_values) <= tol
+    assert G.rel(g.v @ g.w, full.v @ full.w) <= tol
 
 
 # ----------------------------------------------------------------------------- PET

@@ -57,11 +57,14 @@ def test_mds_sharded_equals_unsharded(group):
     assert np.array_equal(np.asarray(th.cpu() if hasattr(th, "cpu") else th), ref)
 
 
-def test_in_graph_nccl_engine(group):
+def test_in_graph_nccl_engine(group, monkeypatch):
     """The fused device engine with the all-reduce captured inside its CUDA
     graph (ncclAllReduce of torch's communicator, resolved with dlsym):
-    equal to the engine without the collective."""
+    equal to the graph engine without the collective (the persistent
+    small-problem engine, which a single-GPU run of this size would pick,
+    is switched off for the reference run)."""
     from paper_1003_3272_b200 import _lib
+    monkeypatch.setenv("MMK_SMALL_ENGINE", "0")
     comm = P.nccl_comm_ptr()
     assert comm, "no NCCL communicator pointer"
     assert _lib.load().mmk_nccl_available() == 1
