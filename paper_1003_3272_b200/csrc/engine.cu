@@ -25,6 +25,7 @@
 #include <dlfcn.h>
 
 #include <functional>
+#include <mutex>
 #include <vector>
 
 #include "mm_control.cuh"
@@ -222,7 +223,7 @@ extern "C" void mmk_engine_destroy(void* eng) {
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
     if (e->cap) cudaStreamDestroy(e->cap);
-    if (e->persistent.scratch) cudaFree(e->persistent.scratch);
+    if (e->persistent.scratch) mmk_small::scratch_give(e->persistent.scratch);
     delete e;
 }
 
@@ -291,6 +292,19 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
                                      size_t ws_bytes, void* comm, const mmk_stop_rule* rule,
                                      double* trace, int64_t* tstamp, int64_t* ctl,
                                      int64_t* err_dev, void** engine) {
+    if (!comm && row0 == 0 && rows == n && mmk_small::mds_eligible(dtype, n, dim, Wt != nullptr)) {
+        // small problems: the whole loop in one persistent kernel per batch
+        Engine* e = new Engine();
+        int rc = mmk_small::mds_prepare(dtype, Y, Wt, ldy, wsum, thetaA, thetaB, dim, n, rule,
+                                        trace, tstamp, ctl, err_dev, &e->persistent);
+        if (rc) {
+            delete e;
+            *engine = nullptr;
+            return rc;
+        }
+        *engine = e;
+        return MMK_OK;
+    }
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     auto iter = [=](cudaStream_t s, int dir) -> int {
         void *Ti = dir ? thetaB : thetaA, *To = dir ? thetaA : thetaB;
@@ -367,6 +381,20 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
                                             void* comm, const mmk_stop_rule* rule, double* trace,
                                             int64_t* tstamp, int64_t* ctl, int64_t* err_dev,
                                             void** engine) {
+    if (!comm && mmk_small::pet_eligible(dtype, d, p)) {
+        // small problems: the whole loop in one persistent kernel per batch
+        Engine* e = new Engine();
+        int rc = mmk_small::pet_prepare(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lamA, lamB,
+                                        d, p, nbr_ptr, nbr_idx, mu, rule, trace, tstamp, ctl,
+                                        err_dev, &e->persistent);
+        if (rc) {
+            delete e;
+            *engine = nullptr;
+            return rc;
+        }
+        *engine = e;
+        return MMK_OK;
+    }
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
     auto iter = [=](cudaStream_t s, int dir) -> int {
@@ -389,3 +417,57 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
     };
     return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
+
+namespace mmk_small {
+
+namespace {
+struct Pooled {
+    void* p;
+    size_t bytes;
+};
+std::mutex g_pool_mu;
+std::vector<Pooled> g_free, g_live;
+constexpr size_t kPoolKeep = 8;
+}  // namespace
+
+void* scratch_take(size_t bytes, size_t zero_bytes) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    void* p = nullptr;
+    size_t got = 0;
+    for (size_t i = 0; i < g_free.size(); ++i) {
+        if (g_free[i].bytes >= bytes) {
+            p = g_free[i].p;
+            got = g_free[i].bytes;
+            g_free.erase(g_free.begin() + i);
+            break;
+        }
+    }
+    if (!p) {
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+        got = bytes;
+    }
+    g_live.push_back({p, got});
+    if (zero_bytes) {
+        // barrier slots must read 0 before the first launch on any stream
+        cudaMemset(p, 0, zero_bytes);
+        cudaDeviceSynchronize();
+    }
+    return p;
+}
+
+void scratch_give(void* p) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_live.size(); ++i) {
+        if (g_live[i].p == p) {
+            g_free.push_back(g_live[i]);
+            g_live.erase(g_live.begin() + i);
+            break;
+        }
+    }
+    while (g_free.size() > kPoolKeep) {
+        cudaFree(g_free.front().p);
+        g_free.erase(g_free.begin());
+    }
+}
+
+}  // namespace mmk_small

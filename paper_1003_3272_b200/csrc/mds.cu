@@ -13,7 +13,10 @@
 // Roofline: HBM-bound on Y (n*rows*sizeof(T) bytes per call; W adds the same
 // when weights are explicit).  The packed-triangle variant for large unit-
 // weight problems lives in mds_tri.cu.
-#include "mmk_common.cuh"
+#include <memory>
+
+#include "mm_control.cuh"
+#include "small_engine.h"
 
 namespace {
 
@@ -217,6 +220,187 @@ __global__ void mds_unpack_kernel(const T* __restrict__ g, T* __restrict__ theta
     theta[t] = g[(rank * dim + k) * rows_pad + c];
 }
 
+// ---------------------------------------------------------------------------
+// Persistent small-problem engine (BASELINE config 3: n = 401, dim 2..10):
+// whole batches of MM iterations in one cooperative kernel.  CTA c owns rows
+// [c n / G, (c + 1) n / G) with their rows of Y (and W) resident in shared
+// memory; per iteration
+//   stage theta_k (dim x n) in shared memory
+//   for each of my rows (the whole CTA sweeps its columns, fixed-order
+//   block reduction): zs_i, A_i, the stress partial (j > i), the update
+//   (the arithmetic of mds_rows_kernel) -> theta_k+1 in slot s^1
+//   barrier
+//   every CTA sums the stress partials in the same order and applies the
+//   stopping rule itself (mm_step); CTA 0 records the trace.
+// One grid barrier per iteration.
+constexpr int kMdsSmallThr = 256;
+
+template <typename T>
+struct MdsSmall {
+    const T *Y, *Wt;
+    long long ldy;
+    const double* wsum;
+    T* theta[2];
+    int n, rpc;
+    double* part;          // [G] stress partials
+    unsigned int* flags;   // [32 G]
+    unsigned int epoch0;
+    long long* ctl;
+    double* trace;
+    long long* tstamp;
+    int64_t* err;
+    mmk_stop_rule rule;
+};
+
+template <typename T, int DIM>
+__global__ void __launch_bounds__(kMdsSmallThr) mds_small_kernel(MdsSmall<T> a) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int n = a.n, rpc = a.rpc;
+    T* const th = reinterpret_cast<T*>(sm_raw);     // DIM x n
+    T* const ys = th + DIM * n;                     // rpc x n: my rows of Y
+    T* const wts = ys + rpc * n;                    // rpc x n: my rows of W (if explicit)
+    __shared__ double red[kMdsSmallThr / 32][DIM + 2];
+    __shared__ int decision;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x, G = gridDim.x;
+    const int r0 = (int)((long long)c * n / G), r1 = (int)((long long)(c + 1) * n / G);
+    for (int t = tid; t < (r1 - r0) * n; t += kMdsSmallThr) {
+        const int i = t / n, j = t - i * n;
+        ys[t] = a.Y[(long long)(r0 + i) * a.ldy + j];
+        if (a.Wt) wts[t] = a.Wt[(long long)(r0 + i) * a.ldy + j];
+    }
+    MmState st = mm_load(a.ctl);
+    unsigned int epoch = a.epoch0;
+    int slot = 0;
+    for (;;) {
+        {
+            const T* tg = a.theta[slot];
+            for (int t0 = 0; t0 < DIM * n; t0 += kMdsSmallThr * 8) {
+                T v8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = t0 + u * kMdsSmallThr + tid;
+                    v8[u] = t < DIM * n ? __ldcg(tg + t) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = t0 + u * kMdsSmallThr + tid;
+                    if (t < DIM * n) th[t] = v8[u];
+                }
+            }
+        }
+        __syncthreads();
+        double stress = 0.0;
+        T* out = a.theta[slot ^ 1];
+        for (int i = r0; i < r1; ++i) {
+            const T* yr = ys + (i - r0) * n;
+            const T* wr = wts + (i - r0) * n;
+            T ti[DIM], acc[DIM];
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                ti[k] = th[k * n + i];
+                acc[k] = T(0);
+            }
+            T zs = T(0);
+            double sti = 0.0;
+            for (int j = tid; j < n; j += kMdsSmallThr) {
+                const T y = yr[j];
+                const T w = a.Wt ? wr[j] : (i == j ? T(0) : T(1));
+                T d2 = T(0);
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) {
+                    const T g = ti[k] - th[k * n + j];
+                    d2 = fma(g, g, d2);
+                }
+                const T wy = w * y;
+                T z = T(0);
+                if (wy > T(0)) {
+                    if (d2 <= T(0))
+                        flag_error(a.err, MMK_E_NUMERICS, err_at(1, (long long)i * n + j));
+                    else
+                        z = wy / sqrt(d2);
+                }
+                zs += z;
+                const T cw = w - z;
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) acc[k] = fma(cw, th[k * n + j], acc[k]);
+                if (j > i) {
+                    const double rr = (double)y - sqrt((double)d2);
+                    sti += (double)w * rr * rr;
+                }
+            }
+            // fixed-order block reduction of (zs, acc, stress)
+            double v[DIM + 2];
+            v[0] = (double)warp_sum(zs);
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) v[1 + k] = (double)warp_sum(acc[k]);
+            v[DIM + 1] = warp_sum(sti);
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < DIM + 2; ++q) red[warp][q] = v[q];
+            __syncthreads();
+            if (tid == 0) {
+                double z = 0.0, s2 = 0.0, A[DIM];
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) A[k] = 0.0;
+                for (int w = 0; w < kMdsSmallThr / 32; ++w) {
+                    z += red[w][0];
+                    s2 += red[w][DIM + 1];
+#pragma unroll
+                    for (int k = 0; k < DIM; ++k) A[k] += red[w][1 + k];
+                }
+                stress += s2;
+                const double ws = a.wsum[i];
+                const double scale = ws + (double)(T)z;
+                const double inv = 2.0 * ws;
+#pragma unroll
+                for (int k = 0; k < DIM; ++k)
+                    out[(long long)k * n + i] = (T)(((double)ti[k] * scale + (double)(T)A[k]) / inv);
+            }
+            __syncthreads();
+        }
+        if (tid == 0) a.part[c] = stress;
+        grid_sync_flags(a.flags, ++epoch);
+        if (warp == 0) {
+            double s2 = 0.0;
+            for (int b = lane; b < G; b += 32) s2 += __ldcg(a.part + b);
+            s2 = warp_sum(s2);
+            if (lane == 0) {
+                const MmState before = st;
+                int reason = 0;
+                const int dcs =
+                    mm_step(st, slot, s2, *(volatile int64_t*)a.err != 0, a.rule, &reason);
+                if (c == 0) mm_record(a.ctl, a.trace, a.tstamp, before, st, slot, s2, dcs, reason);
+                decision = dcs;
+            }
+        }
+        __syncthreads();
+        const int dcs = decision;
+        if (dcs != kMmContinue) return;
+        slot ^= 1;
+    }
+}
+
+template <typename T>
+size_t mds_small_smem(long long n, int dim, bool weighted) {
+    const long long rpc = (n + kNumSMs - 1) / kNumSMs + 1;
+    return sizeof(T) * (size_t)(dim * n + (weighted ? 2 : 1) * rpc * n);
+}
+
+template <typename T>
+const void* mds_small_kernel_for(int dim) {
+    switch (dim) {
+#define MMK_MDS_SMALL(D) \
+    case D:              \
+        return reinterpret_cast<const void*>(&mds_small_kernel<T, D>);
+        MMK_MDS_SMALL(1) MMK_MDS_SMALL(2) MMK_MDS_SMALL(3) MMK_MDS_SMALL(4) MMK_MDS_SMALL(5)
+        MMK_MDS_SMALL(6) MMK_MDS_SMALL(7) MMK_MDS_SMALL(8) MMK_MDS_SMALL(9) MMK_MDS_SMALL(10)
+#undef MMK_MDS_SMALL
+        default:
+            return nullptr;
+    }
+}
+
 }  // namespace
 
 extern "C" int mmk_mds_unpack(int dtype, const void* gathered, void* theta, int64_t dim, int64_t n,
@@ -281,3 +465,86 @@ extern "C" int mmk_mds_iter(int dtype, const void* Y, const void* Wt, int64_t ld
     mmk_host::set_error("unknown dtype %d", dtype);
     return MMK_E_SHAPE;
 }
+
+namespace mmk_small {
+
+bool mds_eligible(int dtype, long long n, long long dim, bool weighted) {
+    const char* env = getenv("MMK_SMALL_ENGINE");
+    if (env && env[0] == '0') return false;
+    if ((dtype != MMK_F32 && dtype != MMK_F64) || dim < 1 || dim > 10 || n < 2 || n > 8192)
+        return false;
+    const size_t smem = dtype == MMK_F32 ? mds_small_smem<float>(n, (int)dim, weighted)
+                                         : mds_small_smem<double>(n, (int)dim, weighted);
+    return smem <= 160 * 1024;
+}
+
+template <typename T>
+static int mds_prepare_t(const void* Y, const void* Wt, long long ldy, const double* wsum,
+                         void* thetaA, void* thetaB, long long dim, long long n,
+                         const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+                         int64_t* err, Launch* out) {
+    MdsSmall<T> a;
+    a.Y = (const T*)Y;
+    a.Wt = (const T*)Wt;
+    a.ldy = ldy;
+    a.wsum = wsum;
+    a.theta[0] = (T*)thetaA;
+    a.theta[1] = (T*)thetaB;
+    a.n = (int)n;
+    const int G = kNumSMs;
+    a.rpc = (int)((n + G - 1) / G) + 1;
+    const void* kern = mds_small_kernel_for<T>((int)dim);
+    const size_t smem = mds_small_smem<T>(n, (int)dim, Wt != nullptr);
+    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem);
+    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "mds_small smem attribute");
+    int per_sm = 0;
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMdsSmallThr, smem);
+    if (ce != cudaSuccess || per_sm < 1) {
+        mmk_host::set_error("mds_small: kernel does not fit an SM (smem %zu)", smem);
+        return MMK_E_SHAPE;
+    }
+    const size_t fbytes = (sizeof(unsigned int) * 32 * G + 255) / 256 * 256;
+    void* scratch = scratch_take(fbytes + sizeof(double) * G, fbytes);
+    if (!scratch) return mmk_host::cuda_status(cudaErrorMemoryAllocation, "mds_small scratch");
+    a.flags = reinterpret_cast<unsigned int*>(scratch);
+    a.part = reinterpret_cast<double*>(reinterpret_cast<char*>(scratch) + fbytes);
+    a.epoch0 = 0;
+    a.ctl = reinterpret_cast<long long*>(ctl);
+    a.trace = trace;
+    a.tstamp = reinterpret_cast<long long*>(tstamp);
+    a.err = err;
+    a.rule = *rule;
+    out->scratch = scratch;
+    auto seq = std::make_shared<unsigned int>(0);
+    out->fn = [a, G, smem, kern, seq](cudaStream_t s) -> int {
+        MdsSmall<T> arg = a;
+        arg.epoch0 = (++*seq) << 20;
+        void* args[] = {&arg};
+        const bool pr = mmk_host::prof_on();
+        if (pr) mmk_host::prof_start("mds_small", s);
+        cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kMdsSmallThr), args,
+                                                    smem, s);
+        if (pr) mmk_host::prof_stop(s);
+        if (e != cudaSuccess) return mmk_host::cuda_status(e, "mds_small_kernel");
+        return MMK_OK;
+    };
+    return MMK_OK;
+}
+
+int mds_prepare(int dtype, const void* Y, const void* Wt, long long ldy, const double* wsum,
+                void* thetaA, void* thetaB, long long dim, long long n,
+                const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+                int64_t* err, Launch* out) {
+    if (rule->batch < 2 || (rule->batch & 1)) {
+        mmk_host::set_error("engine batch must be an even number >= 2");
+        return MMK_E_SHAPE;
+    }
+    if (dtype == MMK_F32)
+        return mds_prepare_t<float>(Y, Wt, ldy, wsum, thetaA, thetaB, dim, n, rule, trace,
+                                    tstamp, ctl, err, out);
+    return mds_prepare_t<double>(Y, Wt, ldy, wsum, thetaA, thetaB, dim, n, rule, trace, tstamp,
+                                 ctl, err, out);
+}
+
+}  // namespace mmk_small

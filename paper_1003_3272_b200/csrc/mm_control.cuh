@@ -17,49 +17,93 @@ enum { kMmContinue = 0, kMmStop = 1, kMmPause = 2 };
 __device__ __forceinline__ double ctl_f64(long long b) { return __longlong_as_double(b); }
 __device__ __forceinline__ long long ctl_bits(double d) { return __double_as_longlong(d); }
 
-// Records f of iteration ctl[IT] (trace + device timestamp) and decides:
-// non-finite, monotone slack monotone_tol * (1 + |f_prev|), relative change
-// |f - f_prev| / (|f_prev| + 1) < epsilon, the max_iters cap -> kMmStop with
-// ctl[REASON] and ctl[SLOT] = half (the slot holding the returned state);
-// otherwise advances ctl[IT]; after half 1 pauses every rule.batch iterations
-// (-> kMmPause) so the host can drain the trace.  Single thread.
-__device__ __forceinline__ int mm_control(int half, long long* ctl, double* trace,
-                                          long long* tstamp, const long long* err,
-                                          const mmk_stop_rule& rule, double f) {
-    const long long it = ctl[MMK_CTL_IT];
-    const long long k = it - ctl[MMK_CTL_BATCH_START];
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    trace[k] = f;
-    tstamp[k] = (long long)now;
-    int reason = 0;
-    if (*(volatile const long long*)err != 0) {
-        reason = MMK_STOP_DEVICE_ERROR;
+// Loop state of the stopping rule (the ctl fields it reads and advances).
+struct MmState {
+    long long it, bstart;
+    double fprev, rel;
+    bool has_rel;
+};
+
+// The stopping rule proper: non-finite, monotone slack
+// monotone_tol * (1 + |f_prev|), relative change |f - f_prev| / (|f_prev| + 1)
+// < epsilon, the max_iters cap -> kMmStop (reason in *reason); otherwise
+// advances the state and, after half 1, pauses every rule.batch iterations
+// (-> kMmPause) so the host can drain the trace.  Pure function of its
+// inputs, so every CTA of a persistent kernel can evaluate it redundantly.
+__device__ __forceinline__ int mm_step(MmState& st, int half, double f, bool err,
+                                       const mmk_stop_rule& rule, int* reason) {
+    int why = 0;
+    st.has_rel = false;
+    if (err) {
+        why = MMK_STOP_DEVICE_ERROR;
     } else if (!isfinite(f)) {
-        reason = MMK_STOP_NONFINITE;
-    } else if (it > 0) {
-        const double fp = ctl_f64(ctl[MMK_CTL_FPREV]);
+        why = MMK_STOP_NONFINITE;
+    } else if (st.it > 0) {
+        const double fp = st.fprev;
         if (rule.check_monotone && rule.sign * (f - fp) < -rule.monotone_tol * (1.0 + fabs(fp))) {
-            reason = MMK_STOP_MONOTONE;
+            why = MMK_STOP_MONOTONE;
         } else {
-            const double rel = fabs(f - fp) / (fabs(fp) + 1.0);
-            ctl[MMK_CTL_REL] = ctl_bits(rel);
-            if (rel < rule.epsilon) reason = MMK_STOP_CONVERGED;
+            st.rel = fabs(f - fp) / (fabs(fp) + 1.0);
+            st.has_rel = true;
+            if (st.rel < rule.epsilon) why = MMK_STOP_CONVERGED;
         }
     }
-    if (!reason && it >= rule.max_iters) reason = MMK_STOP_CAP;
-    if (reason) {
-        ctl[MMK_CTL_REASON] = reason;
-        ctl[MMK_CTL_SLOT] = half;
-        return kMmStop;
-    }
-    ctl[MMK_CTL_FPREV] = ctl_bits(f);
-    ctl[MMK_CTL_IT] = it + 1;
-    if (half == 1 && it + 1 - ctl[MMK_CTL_BATCH_START] >= rule.batch) {
-        ctl[MMK_CTL_BATCH_START] = it + 1;
+    if (!why && st.it >= rule.max_iters) why = MMK_STOP_CAP;
+    *reason = why;
+    if (why) return kMmStop;
+    st.fprev = f;
+    st.it += 1;
+    if (half == 1 && st.it - st.bstart >= rule.batch) {
+        st.bstart = st.it;
         return kMmPause;
     }
     return kMmContinue;
+}
+
+__device__ __forceinline__ MmState mm_load(const long long* ctl) {
+    MmState st;
+    st.it = ctl[MMK_CTL_IT];
+    st.bstart = ctl[MMK_CTL_BATCH_START];
+    st.fprev = ctl_f64(ctl[MMK_CTL_FPREV]);
+    st.rel = 0.0;
+    st.has_rel = false;
+    return st;
+}
+
+// Records f of iteration st.it (trace + device timestamp) and writes the
+// outcome of mm_step back to ctl: ctl[REASON] and ctl[SLOT] = half (the slot
+// holding the returned state) on a stop.  `st` is the state BEFORE the step.
+__device__ __forceinline__ void mm_record(long long* ctl, double* trace, long long* tstamp,
+                                          const MmState& before, const MmState& after, int half,
+                                          double f, int decision, int reason) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    const long long k = before.it - before.bstart;
+    trace[k] = f;
+    tstamp[k] = (long long)now;
+    ctl[MMK_CTL_FCUR] = ctl_bits(f);
+    if (after.has_rel) ctl[MMK_CTL_REL] = ctl_bits(after.rel);
+    if (decision == kMmStop) {
+        ctl[MMK_CTL_REASON] = reason;
+        ctl[MMK_CTL_SLOT] = half;
+        return;
+    }
+    ctl[MMK_CTL_FPREV] = ctl_bits(after.fprev);
+    ctl[MMK_CTL_IT] = after.it;
+    ctl[MMK_CTL_BATCH_START] = after.bstart;
+}
+
+// Single-thread form used by the graph engine's control kernel and the NNMF
+// persistent kernel: state from ctl, step, record.
+__device__ __forceinline__ int mm_control(int half, long long* ctl, double* trace,
+                                          long long* tstamp, const long long* err,
+                                          const mmk_stop_rule& rule, double f) {
+    const MmState before = mm_load(ctl);
+    MmState after = before;
+    int reason = 0;
+    const int d = mm_step(after, half, f, *(volatile const long long*)err != 0, rule, &reason);
+    mm_record(ctl, trace, tstamp, before, after, half, f, d, reason);
+    return d;
 }
 
 // Flag barrier: CTA b publishes `epoch` in its own 128-byte slot

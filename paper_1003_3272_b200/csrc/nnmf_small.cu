@@ -386,10 +386,8 @@ static int prepare_t(const void* X, long long ldx, void* VA, void* WA, void* VB,
     constexpr int kHead = 32;   // bar words before the flag slots
     const size_t bar_bytes = (sizeof(unsigned int) * (kHead + 32 * G) + 255) / 256 * 256;
     const size_t bytes = bar_bytes + sizeof(double) * ((size_t)G * a.E + a.E);
-    void* scratch = nullptr;
-    ce = cudaMalloc(&scratch, bytes);
-    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "nnmf_small scratch");
-    cudaMemset(scratch, 0, bar_bytes);
+    void* scratch = scratch_take(bytes, bar_bytes);
+    if (!scratch) return mmk_host::cuda_status(cudaErrorMemoryAllocation, "nnmf_small scratch");
     a.bar = reinterpret_cast<unsigned int*>(scratch);
     a.flags = a.bar + kHead;
     a.epoch0 = 0;

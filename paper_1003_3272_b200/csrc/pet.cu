@@ -15,7 +15,10 @@
 // the CSR lattice (pet.py:204-210), EM floor or positive-root update
 // (pet.py:390-417), and the roughness penalty at lam (pet.py:326-338); the
 // last CTA assembles f = loglik - mu/2 * penalty.
-#include "mmk_common.cuh"
+#include <memory>
+
+#include "mm_control.cuh"
+#include "small_engine.h"
 
 namespace {
 
@@ -566,6 +569,187 @@ int pet_sparse_a(const int32_t* rptr, const int32_t* ridx, const T* rval, const 
     return MMK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent small-problem engine for the sparse projector (BASELINE config 2:
+// 2016 rays x 4096 pixels, 84,512 nonzeros): whole batches of MM iterations
+// in one cooperative kernel.  Per iteration, state lam_k in slot s:
+//   stage lam_k in shared memory (every CTA)
+//   phase 1  my rays (warp per ray): m_i, ratio_i, loglik partial  -> global
+//   barrier
+//   stage the ratios in shared memory
+//   phase 2  my pixels (8 lanes per CSC column): b_j, the pixel update
+//            (pixel_update, the same code as the graph path) -> lam_k+1 in
+//            slot s^1; penalty partial at lam_k
+//   barrier
+//   every CTA sums the loglik / penalty partials in the same fixed order,
+//   forms f_k and evaluates the stopping rule (mm_step) itself -- no third
+//   barrier; CTA 0 records the trace and ctl.
+// The projections gather from shared memory, in the order of pet_sfwd /
+// pet_sback, so lam is bitwise the graph path's; f differs from it only in
+// the grouping of the partial sums.
+constexpr int kPetSmallThr = 256;
+
+template <typename T>
+struct PetSmall {
+    const int32_t *rptr, *ridx, *cptr, *cidx, *nptr, *nidx;
+    const T *rval, *cval, *y;
+    T* lam[2];
+    int d, p;
+    double mu;
+    double* ratio;          // [d]
+    double* part;           // [2][G]: loglik, penalty partials
+    unsigned int* flags;    // [32 G] barrier slots
+    unsigned int epoch0;
+    long long* ctl;
+    double* trace;
+    long long* tstamp;
+    int64_t* err;
+    mmk_stop_rule rule;
+    long long* dbg;         // optional: CTA 0 phase stamps (MMK_SMALL_TRACE)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kPetSmallThr) pet_small_kernel(PetSmall<T> a) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    double* const rs = reinterpret_cast<double*>(sm_raw);   // d ratios
+    T* const ls = reinterpret_cast<T*>(rs + a.d);           // p intensities
+    __shared__ double wsum[kPetSmallThr / 32];
+    __shared__ int decision;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x, G = gridDim.x;
+    const int i0 = (int)((long long)c * a.d / G), i1 = (int)((long long)(c + 1) * a.d / G);
+    const int j0 = (int)((long long)c * a.p / G), j1 = (int)((long long)(c + 1) * a.p / G);
+    MmState st = mm_load(a.ctl);
+    unsigned int epoch = a.epoch0;
+    int slot = 0;
+    int iter_local = 0;
+    auto stamp = [&](int ph) {
+        if (a.dbg && c == 0 && tid == 0 && iter_local < 64) a.dbg[iter_local * 12 + ph] = clock64();
+    };
+    for (;;) {
+        stamp(0);
+        // ---- lam_k into shared memory ------------------------------------------
+        {
+            const T* lg = a.lam[slot];
+            for (int t0 = 0; t0 < a.p; t0 += kPetSmallThr * 8) {
+                T v8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = t0 + u * kPetSmallThr + tid;
+                    v8[u] = t < a.p ? __ldcg(lg + t) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = t0 + u * kPetSmallThr + tid;
+                    if (t < a.p) ls[t] = v8[u];
+                }
+            }
+        }
+        __syncthreads();
+        stamp(1);
+        // ---- phase 1: rays ------------------------------------------------------
+        double ll = 0.0;
+        for (int i = i0 + warp; i < i1; i += kPetSmallThr / 32) {
+            double m = gather_dot<32>(a.ridx, a.rval, ls, a.rptr[i] + lane, a.rptr[i + 1]);
+            m = warp_sum(m);
+            if (lane == 0) {
+                const double yi = (double)a.y[i];
+                double r = 0.0;
+                ll -= m;
+                if (yi > 0.0) {
+                    if (m == 0.0) flag_error(a.err, MMK_E_NUMERICS, err_at(1, i));
+                    r = yi / m;
+                    ll += yi * log(m);
+                }
+                a.ratio[i] = r;
+            }
+        }
+        if (lane == 0) wsum[warp] = ll;
+        __syncthreads();
+        if (tid == 0) {
+            double s2 = 0.0;
+            for (int w = 0; w < kPetSmallThr / 32; ++w) s2 += wsum[w];
+            a.part[c] = s2;
+        }
+        stamp(2);
+        grid_sync_flags(a.flags, ++epoch);
+        stamp(3);
+        // ---- ratios into shared memory ------------------------------------------
+        for (int t0 = 0; t0 < a.d; t0 += kPetSmallThr * 8) {
+            double v8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * kPetSmallThr + tid;
+                v8[u] = t < a.d ? __ldcg(a.ratio + t) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * kPetSmallThr + tid;
+                if (t < a.d) rs[t] = v8[u];
+            }
+        }
+        __syncthreads();
+        stamp(4);
+        // ---- phase 2: pixels ----------------------------------------------------
+        double pen = 0.0;
+        {
+            const int g = tid / kSubW, q = tid % kSubW;
+            T* lo = a.lam[slot ^ 1];
+            for (int base = j0; base < j1; base += kPetSmallThr / kSubW) {
+                const int j = base + g;
+                double b = 0.0;
+                if (j < j1) b = gather_dot<kSubW>(a.cidx, a.cval, rs, a.cptr[j] + q, a.cptr[j + 1]);
+#pragma unroll
+                for (int o = kSubW / 2; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+                if (q == 0 && j < j1)
+                    pen += pixel_update(ls, lo, a.nptr, a.nidx, a.mu,
+                                        MMK_PET_UPDATE | MMK_PET_OBJECTIVE, j, b, a.err);
+            }
+        }
+        pen = warp_sum(pen);
+        if (lane == 0) wsum[warp] = pen;
+        __syncthreads();
+        if (tid == 0) {
+            double s2 = 0.0;
+            for (int w = 0; w < kPetSmallThr / 32; ++w) s2 += wsum[w];
+            a.part[G + c] = s2;
+        }
+        stamp(5);
+        grid_sync_flags(a.flags, ++epoch);
+        stamp(6);
+        // ---- f_k and the stopping rule, redundantly in every CTA -----------------
+        if (warp == 0) {
+            double l2 = 0.0, p2 = 0.0;
+            for (int b = lane; b < G; b += 32) {
+                l2 += __ldcg(a.part + b);
+                p2 += __ldcg(a.part + G + b);
+            }
+            l2 = warp_sum(l2);
+            p2 = warp_sum(p2);
+            if (lane == 0) {
+                double f = l2;
+                if (a.mu > 0.0) f -= 0.5 * a.mu * p2;
+                const MmState before = st;
+                int reason = 0;
+                const int dcs = mm_step(st, slot, f, *(volatile int64_t*)a.err != 0, a.rule, &reason);
+                if (c == 0) mm_record(a.ctl, a.trace, a.tstamp, before, st, slot, f, dcs, reason);
+                decision = dcs;
+            }
+        }
+        __syncthreads();
+        stamp(7);
+        ++iter_local;
+        const int dcs = decision;
+        if (dcs != kMmContinue) return;
+        slot ^= 1;
+    }
+}
+
+template <typename T>
+size_t pet_small_smem(long long d, long long p) {
+    return sizeof(double) * (size_t)d + sizeof(T) * (size_t)p;
+}
+
 }  // namespace
 
 extern "C" int mmk_pet_ws_bytes(int dtype, int64_t d, int64_t p, size_t* out) {
@@ -737,3 +921,98 @@ extern "C" int mmk_pet_gradient(int dtype, const void* lam, void* grad, int64_t 
     MMK_CHECK_LAUNCH("pet_grad_kernel");
     return MMK_OK;
 }
+
+namespace mmk_small {
+
+bool pet_eligible(int dtype, long long d, long long p) {
+    const char* env = getenv("MMK_SMALL_ENGINE");
+    if (env && env[0] == '0') return false;
+    if ((dtype != MMK_F32 && dtype != MMK_F64) || d < 1 || p < 1) return false;
+    const size_t smem = dtype == MMK_F32 ? pet_small_smem<float>(d, p) : pet_small_smem<double>(d, p);
+    return smem <= 160 * 1024 && d * 1.0 * p <= (double)(1LL << 26);
+}
+
+template <typename T>
+static int pet_prepare_t(const int32_t* rptr, const int32_t* ridx, const void* rval,
+                         const int32_t* cptr, const int32_t* cidx, const void* cval,
+                         const void* y, void* lamA, void* lamB, long long d, long long p,
+                         const int32_t* nbr_ptr, const int32_t* nbr_idx, double mu,
+                         const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+                         int64_t* err, Launch* out) {
+    PetSmall<T> a;
+    a.rptr = rptr;
+    a.ridx = ridx;
+    a.cptr = cptr;
+    a.cidx = cidx;
+    a.nptr = nbr_ptr;
+    a.nidx = nbr_idx;
+    a.rval = (const T*)rval;
+    a.cval = (const T*)cval;
+    a.y = (const T*)y;
+    a.lam[0] = (T*)lamA;
+    a.lam[1] = (T*)lamB;
+    a.d = (int)d;
+    a.p = (int)p;
+    a.mu = mu;
+    const int G = kNumSMs;
+    const size_t smem = pet_small_smem<T>(d, p);
+    cudaError_t ce = cudaFuncSetAttribute(pet_small_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "pet_small smem attribute");
+    int per_sm = 0;
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pet_small_kernel<T>,
+                                                       kPetSmallThr, smem);
+    if (ce != cudaSuccess || per_sm < 1) {
+        mmk_host::set_error("pet_small: kernel does not fit an SM (smem %zu)", smem);
+        return MMK_E_SHAPE;
+    }
+    const size_t fbytes = (sizeof(unsigned int) * 32 * G + 255) / 256 * 256;
+    const size_t bytes = fbytes + sizeof(double) * ((size_t)d + 2 * (size_t)G);
+    void* scratch = scratch_take(bytes, fbytes);
+    if (!scratch) return mmk_host::cuda_status(cudaErrorMemoryAllocation, "pet_small scratch");
+    a.flags = reinterpret_cast<unsigned int*>(scratch);
+    a.ratio = reinterpret_cast<double*>(reinterpret_cast<char*>(scratch) + fbytes);
+    a.part = a.ratio + d;
+    a.epoch0 = 0;
+    a.ctl = reinterpret_cast<long long*>(ctl);
+    a.trace = trace;
+    a.tstamp = reinterpret_cast<long long*>(tstamp);
+    a.err = err;
+    a.rule = *rule;
+    a.dbg = nullptr;
+    if (const char* tr = getenv("MMK_SMALL_TRACE"))
+        a.dbg = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
+    out->scratch = scratch;
+    auto seq = std::make_shared<unsigned int>(0);
+    out->fn = [a, G, smem, seq](cudaStream_t s) -> int {
+        PetSmall<T> arg = a;
+        arg.epoch0 = (++*seq) << 20;
+        void* args[] = {&arg};
+        const bool pr = mmk_host::prof_on();
+        if (pr) mmk_host::prof_start("pet_small", s);
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)pet_small_kernel<T>, dim3(G),
+                                                    dim3(kPetSmallThr), args, smem, s);
+        if (pr) mmk_host::prof_stop(s);
+        if (e != cudaSuccess) return mmk_host::cuda_status(e, "pet_small_kernel");
+        return MMK_OK;
+    };
+    return MMK_OK;
+}
+
+int pet_prepare(int dtype, const int32_t* rptr, const int32_t* ridx, const void* rval,
+                const int32_t* cptr, const int32_t* cidx, const void* cval, const void* y,
+                void* lamA, void* lamB, long long d, long long p, const int32_t* nbr_ptr,
+                const int32_t* nbr_idx, double mu, const mmk_stop_rule* rule, double* trace,
+                int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out) {
+    if (rule->batch < 2 || (rule->batch & 1)) {
+        mmk_host::set_error("engine batch must be an even number >= 2");
+        return MMK_E_SHAPE;
+    }
+    if (dtype == MMK_F32)
+        return pet_prepare_t<float>(rptr, ridx, rval, cptr, cidx, cval, y, lamA, lamB, d, p,
+                                    nbr_ptr, nbr_idx, mu, rule, trace, tstamp, ctl, err, out);
+    return pet_prepare_t<double>(rptr, ridx, rval, cptr, cidx, cval, y, lamA, lamB, d, p, nbr_ptr,
+                                 nbr_idx, mu, rule, trace, tstamp, ctl, err, out);
+}
+
+}  // namespace mmk_small

@@ -24,9 +24,31 @@ struct Launch {
 
 // Frobenius NNMF (nnmf.py:84-110, 143-159): r <= 16, small m x n.
 // MMK_SMALL_ENGINE=0 in the environment disables the persistent engines.
+// Scratch buffers of destroyed persistent engines are kept for reuse:
+// cudaFree synchronises the device and costs milliseconds, which is most of
+// a short run.  scratch_take returns a zeroed-header buffer of >= bytes.
+void* scratch_take(size_t bytes, size_t zero_bytes);
+void scratch_give(void* p);
+
 bool nnmf_eligible(int dtype, long long m, long long n, long long r, long long ldx);
 int nnmf_prepare(int dtype, const void* X, long long ldx, void* VA, void* WA, void* VB, void* WB,
                  long long m, long long n, int r, const mmk_stop_rule* rule, double* trace,
                  int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out);
+
+// Penalized PET with the sparse projector (pet.py:363-417 on CSR + CSC):
+// ratios and intensities staged in shared memory (d doubles + p values).
+bool pet_eligible(int dtype, long long d, long long p);
+int pet_prepare(int dtype, const int32_t* rptr, const int32_t* ridx, const void* rval,
+                const int32_t* cptr, const int32_t* cidx, const void* cval, const void* y,
+                void* lamA, void* lamB, long long d, long long p, const int32_t* nbr_ptr,
+                const int32_t* nbr_idx, double mu, const mmk_stop_rule* rule, double* trace,
+                int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out);
+
+// MDS stress majorization, full rows (mds.py:114-144), n <= 8192, dim <= 10.
+bool mds_eligible(int dtype, long long n, long long dim, bool weighted);
+int mds_prepare(int dtype, const void* Y, const void* Wt, long long ldy, const double* wsum,
+                void* thetaA, void* thetaB, long long dim, long long n,
+                const mmk_stop_rule* rule, double* trace, int64_t* tstamp, int64_t* ctl,
+                int64_t* err, Launch* out);
 
 }  // namespace mmk_small

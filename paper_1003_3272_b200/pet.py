@@ -253,7 +253,10 @@ def _use_sparse(problem, backend):
         return backend.pet_kernel == "sparse"
     if A.is_torch(problem.e):
         return False
-    return np.count_nonzero(problem.e) < SPARSE_DENSITY * problem.e.size
+    nnz = problem._dev.get("nnz")          # E is immutable: count its nonzeros once
+    if nnz is None:
+        nnz = problem._dev["nnz"] = int(np.count_nonzero(problem.e))
+    return nnz < SPARSE_DENSITY * problem.e.size
 
 
 def _sparse_arrays(e_rows, backend, torch):

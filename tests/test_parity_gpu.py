@@ -413,3 +413,34 @@ def test_pet_c2_sparse_projector(mu, dtype):
     assert G.rel(lam, g[f"lam_{mu:g}"]) <= tol
     # the auto switch picks the sparse kernels for the ~1 % dense Siddon matrix
     assert M.pet._use_sparse(prob, Backend(dtype=dtype))
+
+
+@pytest.mark.parametrize("solver", ["mds", "pet"])
+def test_persistent_engines_match_graph_engine(solver, monkeypatch):
+    """The persistent MDS (rows) and sparse-PET engines against the graph
+    engine: traces and states equal to rounding; 9000 MDS iterations cross two
+    batch pauses and equal two restarted runs of 4500 bitwise."""
+    be = Backend(dtype="fp64")
+    if solver == "mds":
+        diss, theta0 = G.c3_inputs(3)
+        prob = M.MdsProblem(weights=1.0 - np.eye(401), dissimilarities=diss, p=3)
+        run = lambda cfg, t0=theta0: M.mds_run(prob, cfg, be, theta0=t0)
+        iters = 9000
+    else:
+        e, y, nbrs = G.c2_inputs()
+        prob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=nbrs)
+        run = lambda cfg: M.pet_run(prob, cfg, Backend(dtype="fp64", pet_kernel="sparse"))
+        iters = 2000
+    cfg = MmConfig(max_iters=iters, epsilon=1e-300)
+    s_p, t_p = run(cfg)
+    if solver == "mds":
+        half = MmConfig(max_iters=iters // 2, epsilon=1e-300)
+        s1, t1 = run(half)
+        s2, t2 = run(half, s1)
+        assert np.array_equal(s2, s_p)
+        assert np.array_equal(np.concatenate([t1.objective_values, t2.objective_values[1:]]),
+                              t_p.objective_values)
+    monkeypatch.setenv("MMK_SMALL_ENGINE", "0")
+    s_g, t_g = run(cfg)
+    assert G.rel(t_p.objective_values, t_g.objective_values) <= 1e-12
+    assert G.rel(s_p, s_g) <= 1e-9
