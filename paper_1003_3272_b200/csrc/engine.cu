@@ -356,6 +356,18 @@ extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t 
                                               void* comm, const mmk_stop_rule* rule,
                                               double* trace, int64_t* tstamp, int64_t* ctl,
                                               int64_t* err_dev, void** engine) {
+    if (!comm && mmk_small::nnmf_eligible(dtype, m, n, r, ldx)) {
+        Engine* e = new Engine();
+        int rc = mmk_small::nnmf_prepare(dtype, X, ldx, VA, WA, VB, WB, m, n, (int)r, rule, trace,
+                                         tstamp, ctl, err_dev, &e->persistent, true);
+        if (rc) {
+            delete e;
+            *engine = nullptr;
+            return rc;
+        }
+        *engine = e;
+        return MMK_OK;
+    }
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_poisson_reduce_len(n, r);
     auto iter = [=](cudaStream_t s, int dir) -> int {

@@ -59,14 +59,18 @@ struct SmallNnmf {
     long long* ctl;
     double* trace;
     long long* tstamp;
-    const long long* err;
+    int64_t* err;
     mmk_stop_rule rule;
     long long* dbg;         // optional: CTA 0 phase timestamps (MMK_SMALL_TRACE)
     unsigned int* flags;    // [32 * G] barrier slots
     unsigned int epoch0;    // first barrier epoch of this launch
 };
 
-template <typename T, int R>
+// POIS: the Poisson log fit (nnmf.py:178-242) instead of the Frobenius loss:
+// V' = V sqrt((R W^T) / (1 W^T)), W' = W sqrt((V'^T R') / (V'^T 1)) with
+// R = X / (V W) masked to x > 0, objective sum x ln b - b (fp64); the
+// reduction entries are [P (r x n) | colsum V' (r) | f].
+template <typename T, int R, bool POIS>
 __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     constexpr int r = R;
@@ -113,6 +117,30 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
         __syncthreads();
         stamp(0);
         // ---- phase 1 ---------------------------------------------------------
+        if constexpr (POIS) {
+            // ws_k = sum_j w_kj (fp64): kWsSeg column segments per k, combined in order
+            constexpr int SEG = kThr / R >= 16 ? 16 : kThr / R;
+            for (int t = tid; t < R * SEG; t += kThr) {
+                const int k = t / SEG, sg = t % SEG;
+                const int j0 = (int)((long long)sg * n / SEG), j1 = (int)((long long)(sg + 1) * n / SEG);
+                const double* Wd = Wd0 + wcur * r * n;
+                double s0 = 0.0, s1 = 0.0;
+                int j = j0;
+                for (; j + 1 < j1; j += 2) {
+                    s0 += Wd[k * n + j];
+                    s1 += Wd[k * n + j + 1];
+                }
+                if (j < j1) s0 += Wd[k * n + j];
+                Gv[t] = s0 + s1;
+            }
+            __syncthreads();
+            for (int k = tid; k < R; k += kThr) {
+                double s = 0.0;
+                for (int sg = 0; sg < SEG; ++sg) s += Gv[k * SEG + sg];
+                Gw[k] = s;
+            }
+            __syncthreads();
+        } else {
         // G_W = W W^T: the r(r+1)/2 entries x kGwSeg column segments over the
         // threads, segments combined in order (fp64)
         {
@@ -147,6 +175,7 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
             }
             __syncthreads();
         }
+        }
         stamp(1);
         const T* Vc = slot ? Vs1 : Vs0;
         T* Vn = slot ? Vs0 : Vs1;
@@ -162,17 +191,34 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
             const T* xr = Xs + i * n;
             for (int j = lane; j < n; j += 32) {
                 const T x = xr[j];
-                T rec = T(0);
+                if constexpr (POIS) {
+                    T b = T(0);
 #pragma unroll
-                for (int k = 0; k < kSmallR; ++k) {
-                    if (k < r) {
-                        const T w = Ws[k * n + j];
-                        q[k] = fma(x, w, q[k]);
-                        rec = fma(v[k], w, rec);
+                    for (int k = 0; k < R; ++k) b = fma(v[k], Ws[k * n + j], b);
+                    res -= (double)b;
+                    if (x > T(0)) {
+                        if (b == T(0)) {
+                            flag_error(a.err, MMK_E_NUMERICS, err_at(1, (long long)(row0 + i) * n + j));
+                            continue;
+                        }
+                        res = fma((double)x, log((double)b), res);
+                        const T ratio = x / b;
+#pragma unroll
+                        for (int k = 0; k < R; ++k) q[k] = fma(ratio, Ws[k * n + j], q[k]);
                     }
+                } else {
+                    T rec = T(0);
+#pragma unroll
+                    for (int k = 0; k < kSmallR; ++k) {
+                        if (k < r) {
+                            const T w = Ws[k * n + j];
+                            q[k] = fma(x, w, q[k]);
+                            rec = fma(v[k], w, rec);
+                        }
+                    }
+                    const double d = (double)x - (double)rec;
+                    res = fma(d, d, res);
                 }
-                const double d = (double)x - (double)rec;
-                res = fma(d, d, res);
             }
             T qk = T(0), vk = T(0);
             double den = 0.0;
@@ -184,11 +230,12 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
                         qk = t;
                         vk = v[k];
                     }
-                    if (lane < r) den = fma((double)v[k], Gw[k * r + lane], den);
+                    if (!POIS && lane < r) den = fma((double)v[k], Gw[k * r + lane], den);
                 }
             }
             if (lane < r) {
-                const T nv = (T)((double)vk * ((double)qk / (den + kDenomGuard)));
+                const T nv = POIS ? (T)((double)vk * sqrt((double)qk / (Gw[lane] + kDenomGuard)))
+                                  : (T)((double)vk * ((double)qk / (den + kDenomGuard)));
                 Vo[(long long)(row0 + i) * r + lane] = nv;
                 Vn[i * r + lane] = nv;
             }
@@ -202,21 +249,50 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
             T acc[kSmallR];
 #pragma unroll
             for (int k = 0; k < kSmallR; ++k) acc[k] = T(0);
-            for (int i = 0; i < nrows; ++i) {
-                const T x = Xs[i * n + j];
+            if constexpr (POIS) {
+                T wj[R];
 #pragma unroll
-                for (int k = 0; k < kSmallR; ++k)
-                    if (k < r) acc[k] = fma(Vn[i * r + k], x, acc[k]);
+                for (int k = 0; k < R; ++k) wj[k] = Ws[k * n + j];
+                for (int i = 0; i < nrows; ++i) {
+                    const T x = Xs[i * n + j];
+                    if (!(x > T(0))) continue;
+                    T b = T(0);
+#pragma unroll
+                    for (int k = 0; k < R; ++k) b = fma(Vn[i * r + k], wj[k], b);
+                    if (b == T(0)) {
+                        flag_error(a.err, MMK_E_NUMERICS, err_at(2, (long long)(row0 + i) * n + j));
+                        continue;
+                    }
+                    const T ratio = x / b;
+#pragma unroll
+                    for (int k = 0; k < R; ++k) acc[k] = fma(Vn[i * r + k], ratio, acc[k]);
+                }
+            } else {
+                for (int i = 0; i < nrows; ++i) {
+                    const T x = Xs[i * n + j];
+#pragma unroll
+                    for (int k = 0; k < kSmallR; ++k)
+                        if (k < r) acc[k] = fma(Vn[i * r + k], x, acc[k]);
+                }
             }
 #pragma unroll
             for (int k = 0; k < kSmallR; ++k)
                 if (k < r) pc[(long long)k * n + j] = (double)acc[k];
         }
-        for (int t = tid; t < r * r; t += kThr) {
-            const int p = t / r, q = t - p * r;
-            double s = 0.0;
-            for (int i = 0; i < nrows; ++i) s = fma((double)Vn[i * r + p], (double)Vn[i * r + q], s);
-            pc[(long long)r * n + t] = s;
+        if constexpr (POIS) {
+            for (int k = tid; k < R; k += kThr) {
+                double s = 0.0;
+                for (int i = 0; i < nrows; ++i) s += (double)Vn[i * r + k];
+                pc[(long long)r * n + k] = s;
+            }
+        } else {
+            for (int t = tid; t < r * r; t += kThr) {
+                const int p = t / r, q = t - p * r;
+                double s = 0.0;
+                for (int i = 0; i < nrows; ++i)
+                    s = fma((double)Vn[i * r + p], (double)Vn[i * r + q], s);
+                pc[(long long)r * n + t] = s;
+            }
         }
         const double bres = block_sum(res, sc);
         if (tid == 0) pc[E - 1] = bres;
@@ -245,7 +321,8 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
                     a.tot[e] = s;
                     if (e == E - 1) {
                         a.ctl[MMK_CTL_FCUR] = ctl_bits(s);
-                        a.bar[2] = (unsigned int)mm_control(slot, a.ctl, a.trace, a.tstamp, a.err,
+                        a.bar[2] = (unsigned int)mm_control(slot, a.ctl, a.trace, a.tstamp,
+                                                            reinterpret_cast<const long long*>(a.err),
                                                             a.rule, s);
                     }
                 }
@@ -261,22 +338,23 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
         // ---- phase 3 ---------------------------------------------------------
         // all totals into shared memory at once (one L2 round trip)
         stamp(8);
-        for (int t0 = 0; t0 < r * n + r * r; t0 += kThr * 8) {
+        constexpr int kSide = POIS ? R : R * R;   // colsum V' (Poisson) or G_V
+        for (int t0 = 0; t0 < r * n + kSide; t0 += kThr * 8) {
             double v8[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int t = t0 + u * kThr + tid;
-                v8[u] = t < r * n + r * r ? __ldcg(a.tot + t) : 0.0;
+                v8[u] = t < r * n + kSide ? __ldcg(a.tot + t) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int t = t0 + u * kThr + tid;
-                if (t < r * n + r * r) Pt[t] = v8[u];
+                if (t < r * n + kSide) Pt[t] = v8[u];
             }
         }
         __syncthreads();
         stamp(9);
-        for (int t = tid; t < r * r; t += kThr) Gv[t] = Pt[r * n + t];
+        for (int t = tid; t < kSide; t += kThr) Gv[t] = Pt[r * n + t];
         __syncthreads();
         stamp(10);
         T* Wo = a.W[slot ^ 1];
@@ -291,10 +369,15 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
                 const bool mine = j >= jlo && j < jhi;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
-                    double den = 0.0;
+                    T nw;
+                    if constexpr (POIS) {
+                        nw = (T)(wc[k] * sqrt(Pt[k * n + j] / (Gv[k] + kDenomGuard)));
+                    } else {
+                        double den = 0.0;
 #pragma unroll
-                    for (int l = 0; l < R; ++l) den = fma(Gv[k * R + l], wc[l], den);
-                    const T nw = (T)(wc[k] * (Pt[k * n + j] * __drcp_rn(den + kDenomGuard)));
+                        for (int l = 0; l < R; ++l) den = fma(Gv[k * R + l], wc[l], den);
+                        nw = (T)(wc[k] * (Pt[k * n + j] / (den + kDenomGuard)));
+                    }
                     Wd0[wr + k * n + j] = (double)nw;
                     Ws[k * n + j] = nw;
                     if (mine) Wo[(long long)k * n + j] = nw;
@@ -310,12 +393,12 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
     }
 }
 
-template <typename T>
+template <typename T, bool POIS>
 void* kernel_for(int r) {
     switch (r) {
 #define MMK_SMALL_R(R) \
     case R:            \
-        return reinterpret_cast<void*>(&nnmf_small_kernel<T, R>);
+        return reinterpret_cast<void*>(&nnmf_small_kernel<T, R, POIS>);
         MMK_SMALL_R(1) MMK_SMALL_R(2) MMK_SMALL_R(3) MMK_SMALL_R(4) MMK_SMALL_R(5) MMK_SMALL_R(6)
         MMK_SMALL_R(7) MMK_SMALL_R(8) MMK_SMALL_R(9) MMK_SMALL_R(10) MMK_SMALL_R(11)
         MMK_SMALL_R(12) MMK_SMALL_R(13) MMK_SMALL_R(14) MMK_SMALL_R(15) MMK_SMALL_R(16)
@@ -351,7 +434,7 @@ bool nnmf_eligible(int dtype, long long m, long long n, long long r, long long l
     return smem <= 200 * 1024;
 }
 
-template <typename T>
+template <typename T, bool POIS>
 static int prepare_t(const void* X, long long ldx, void* VA, void* WA, void* VB, void* WB,
                      long long m, long long n, int r, const mmk_stop_rule* rule, double* trace,
                      int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out) {
@@ -367,9 +450,9 @@ static int prepare_t(const void* X, long long ldx, void* VA, void* WA, void* VB,
     a.r = r;
     const int G = grid_of(m);
     a.rpc = (int)((m + G - 1) / G);
-    a.E = (int)(r * n + r * r + 1);
+    a.E = (int)(r * n + (POIS ? r : r * r) + 1);
     const size_t smem = smem_of<T>(m, n, r);
-    const void* kern = kernel_for<T>(r);
+    const void* kern = kernel_for<T, POIS>(r);
     if (!kern) {
         mmk_host::set_error("nnmf_small: rank %d out of range", r);
         return MMK_E_SHAPE;
@@ -396,7 +479,7 @@ static int prepare_t(const void* X, long long ldx, void* VA, void* WA, void* VB,
     a.ctl = reinterpret_cast<long long*>(ctl);
     a.trace = trace;
     a.tstamp = reinterpret_cast<long long*>(tstamp);
-    a.err = reinterpret_cast<const long long*>(err);
+    a.err = err;
     a.rule = *rule;
     a.dbg = nullptr;
     if (const char* tr = getenv("MMK_SMALL_TRACE")) {
@@ -422,15 +505,20 @@ static int prepare_t(const void* X, long long ldx, void* VA, void* WA, void* VB,
 
 int nnmf_prepare(int dtype, const void* X, long long ldx, void* VA, void* WA, void* VB, void* WB,
                  long long m, long long n, int r, const mmk_stop_rule* rule, double* trace,
-                 int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out) {
+                 int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out, bool poisson) {
     if (rule->batch < 2 || (rule->batch & 1)) {
         mmk_host::set_error("engine batch must be an even number >= 2");
         return MMK_E_SHAPE;
     }
     if (dtype == MMK_F32)
-        return prepare_t<float>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace, tstamp, ctl, err,
-                                out);
-    return prepare_t<double>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace, tstamp, ctl, err, out);
+        return poisson ? prepare_t<float, true>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace,
+                                                tstamp, ctl, err, out)
+                       : prepare_t<float, false>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace,
+                                                 tstamp, ctl, err, out);
+    return poisson ? prepare_t<double, true>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace, tstamp,
+                                             ctl, err, out)
+                   : prepare_t<double, false>(X, ldx, VA, WA, VB, WB, m, n, r, rule, trace, tstamp,
+                                              ctl, err, out);
 }
 
 }  // namespace mmk_small

@@ -22,7 +22,8 @@ struct Launch {
     void* scratch = nullptr;               // cudaMalloc'd, freed by mmk_engine_destroy
 };
 
-// Frobenius NNMF (nnmf.py:84-110, 143-159): r <= 16, small m x n.
+// Frobenius NNMF (nnmf.py:84-110, 143-159) or, with poisson, the Poisson
+// log fit (nnmf.py:178-265): r <= 16, small m x n.
 // MMK_SMALL_ENGINE=0 in the environment disables the persistent engines.
 // Scratch buffers of destroyed persistent engines are kept for reuse:
 // cudaFree synchronises the device and costs milliseconds, which is most of
@@ -33,7 +34,7 @@ void scratch_give(void* p);
 bool nnmf_eligible(int dtype, long long m, long long n, long long r, long long ldx);
 int nnmf_prepare(int dtype, const void* X, long long ldx, void* VA, void* WA, void* VB, void* WB,
                  long long m, long long n, int r, const mmk_stop_rule* rule, double* trace,
-                 int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out);
+                 int64_t* tstamp, int64_t* ctl, int64_t* err, Launch* out, bool poisson = false);
 
 // Penalized PET with the sparse projector (pet.py:363-417 on CSR + CSC):
 // ratios and intensities staged in shared memory (d doubles + p values).

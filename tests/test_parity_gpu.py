@@ -415,7 +415,7 @@ def test_pet_c2_sparse_projector(mu, dtype):
     assert M.pet._use_sparse(prob, Backend(dtype=dtype))
 
 
-@pytest.mark.parametrize("solver", ["mds", "pet"])
+@pytest.mark.parametrize("solver", ["mds", "pet", "poisson"])
 def test_persistent_engines_match_graph_engine(solver, monkeypatch):
     """The persistent MDS (rows) and sparse-PET engines against the graph
     engine: traces and states equal to rounding; 9000 MDS iterations cross two
@@ -426,21 +426,31 @@ def test_persistent_engines_match_graph_engine(solver, monkeypatch):
         prob = M.MdsProblem(weights=1.0 - np.eye(401), dissimilarities=diss, p=3)
         run = lambda cfg, t0=theta0: M.mds_run(prob, cfg, be, theta0=t0)
         iters = 9000
-    else:
+    elif solver == "pet":
         e, y, nbrs = G.c2_inputs()
         prob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=nbrs)
         run = lambda cfg: M.pet_run(prob, cfg, Backend(dtype="fp64", pet_kernel="sparse"))
         iters = 2000
+    else:
+        x, v0, w0 = G.poisson_c1_inputs()
+        prob = M.NnmfProblem(x=x, rank=10)
+        run = lambda cfg, s0=M.FactorPair(v0, w0): M.nnmf_poisson_run(prob, cfg, be, state0=s0)
+        iters = 9000
     cfg = MmConfig(max_iters=iters, epsilon=1e-300)
     s_p, t_p = run(cfg)
-    if solver == "mds":
+    flat = (lambda s: np.concatenate([s.v.ravel(), s.w.ravel()])) if solver == "poisson" \
+        else (lambda s: np.asarray(s))
+    if solver in ("mds", "poisson"):
         half = MmConfig(max_iters=iters // 2, epsilon=1e-300)
         s1, t1 = run(half)
         s2, t2 = run(half, s1)
-        assert np.array_equal(s2, s_p)
+        assert np.array_equal(flat(s2), flat(s_p))
         assert np.array_equal(np.concatenate([t1.objective_values, t2.objective_values[1:]]),
                               t_p.objective_values)
     monkeypatch.setenv("MMK_SMALL_ENGINE", "0")
     s_g, t_g = run(cfg)
     assert G.rel(t_p.objective_values, t_g.objective_values) <= 1e-12
-    assert G.rel(s_p, s_g) <= 1e-9
+    if solver == "poisson":
+        assert G.rel(s_p.v @ s_p.w, s_g.v @ s_g.w) <= 1e-9
+    else:
+        assert G.rel(s_p, s_g) <= 1e-9
