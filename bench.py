@@ -488,7 +488,10 @@ def roofline(prof, alg, bound, _label):
 
 def suite(args, torch, dev):
     """Paper shapes (BASELINE configs 1-3) through the public API with host
-    numpy inputs, 1000 fixed iterations each, next to the CPU oracle."""
+    numpy inputs, 1000 fixed iterations each, next to the CPU oracle; plus the
+    time to the reference's default tolerance (epsilon 1e-9, at most 100,000
+    iterations) for C1 / C2 / C3, the CPU time estimated from the oracle's
+    iteration rate."""
     import numpy as np
 
     import paper_1003_3272_b200 as M
@@ -542,6 +545,15 @@ def suite(args, torch, dev):
     cpu, thr, _ = cpu_sample("mds-c3", 3.0)
     out["mds-c3"] = {"gpu_it_s": tr.iters / dt, "cpu_it_s": cpu, "cpu_threads": thr,
                      "speedup": tr.iters / dt / cpu}
+    (_, tr), dt = timed(lambda: M.mds_run(mprob, conv, be, theta0=th0))
+    out["mds-c3-to-tolerance"] = {"iters": tr.iters, "converged": bool(tr.converged),
+                                  "gpu_s": dt, "cpu_s_est": tr.iters / cpu,
+                                  "speedup": tr.iters / cpu / dt}
+    cpu_n = out["nnmf-c1"]["cpu_it_s"]
+    (_, tr), dt = timed(lambda: M.nnmf_run(prob, conv, be, state0=s0))
+    out["nnmf-c1-to-tolerance"] = {"iters": tr.iters, "converged": bool(tr.converged),
+                                   "gpu_s": dt, "cpu_s_est": tr.iters / cpu_n,
+                                   "speedup": tr.iters / cpu_n / dt}
     return out
 
 
