@@ -527,11 +527,9 @@ int tri_a(const float* Yp, long long t0, long long t1, const float* theta, int n
     const TriPlan P = tri_plan(n, t0, t1);
     TriWs L;
     tri_layout(P, DIM, ws, &L);
-    static bool attr = false;
-    if (!attr) {
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(mds_tri_kernel<DIM>))) {
         cudaFuncSetAttribute(mds_tri_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kTriSmem);
-        attr = true;
     }
     MMK_LAUNCH("mds_tri_stage", st,
                (mds_tri_stage<<<kStageBlocks, 256, 0, st>>>(theta, L.thp, n, L.npad, DIM, L.spart,

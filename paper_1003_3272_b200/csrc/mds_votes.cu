@@ -261,11 +261,9 @@ extern "C" int mmk_mds_votes_tri(int dtype, const void* votes, int64_t q, int64_
     int rc;
     if ((rc = mmk_host::make_map_f16(&mA, A, qpad, K2, K2, TB))) return rc;
     if ((rc = mmk_host::make_map_f16(&mB, Bm, 2 * qpad, K2, K2, 2 * TB))) return rc;
-    static bool attr = false;
-    if (!attr) {
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(mds_votes_tri_kernel))) {
         cudaFuncSetAttribute(mds_votes_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM);
-        attr = true;
     }
     const long long ntl = t1 - t0;
     const int G = (int)(ntl < kNumSMs ? ntl : kNumSMs);

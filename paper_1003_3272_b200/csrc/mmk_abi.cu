@@ -51,6 +51,17 @@ cudaEvent_t take_event() {
 }  // namespace
 
 namespace mmk_host {
+bool first_on_device(const void* key) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : seen)
+        if (e.first == key && e.second == dev) return false;
+    seen.emplace_back(key, dev);
+    return true;
+}
 bool prof_on() { return g_prof_on; }
 void prof_start(const char* name, cudaStream_t s) {
     if (!g_prof_on) return;

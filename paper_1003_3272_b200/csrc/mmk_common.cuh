@@ -114,6 +114,9 @@ int make_map_f16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t col
                  uint64_t row_stride_elems, uint32_t box_rows);
 void prof_start(const char* name, cudaStream_t s);
 void prof_stop(cudaStream_t s);
+// true the first time `key` (e.g. a kernel's address) is seen on the current
+// device -- for once-per-device kernel attributes (thread-safe)
+bool first_on_device(const void* key);
 }  // namespace mmk_host
 
 // Bracket one kernel launch for the opt-in profiler (mmk_prof_enable).

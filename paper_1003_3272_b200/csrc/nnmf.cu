@@ -532,12 +532,11 @@ struct K {
         if constexpr (RMAX <= 16) {
             if (P.rpw == 2) {
                 if (full) {
-                    static bool attr = false;
-                    if (!attr) {
+                    if (mmk_host::first_on_device(
+                            reinterpret_cast<const void*>(nnmf_vstep_kernel<T, RMAX, 2, true>))) {
                         cudaFuncSetAttribute(nnmf_vstep_kernel<T, RMAX, 2, true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kWFullBytes);
-                        attr = true;
                     }
                     MMK_LAUNCH("nnmf_vstep", st,
                                (nnmf_vstep_kernel<T, RMAX, 2, true><<<P.nvb, kThreads, wbytes, st>>>(
@@ -661,11 +660,9 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
         return MMK_OK;
     }
     if (r == 64) {
-        static bool attr = false;
-        if (!attr) {
+        if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wfinish64_kernel<T>))) {
             cudaFuncSetAttribute(nnmf_wfinish64_kernel<T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kWf64Smem);
-            attr = true;
         }
         MMK_LAUNCH("nnmf_wfinish", st,
                    (nnmf_wfinish64_kernel<T><<<ceil_div(n, 64), 256, kWf64Smem, st>>>(

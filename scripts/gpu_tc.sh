@@ -1,19 +1,11 @@
 python -c "from paper_1003_3272_b200 import build; build.build()"
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-cat > /tmp/pois_probe.py <<'PY'
-import sys, time
-sys.path.insert(0, '.')
-sys.path.insert(0, 'tests')
-import numpy as np, torch
-import paper_1003_3272_b200 as M
-import golden_io as G
-x, v0, w0 = G.poisson_c1_inputs()
-prob = M.NnmfProblem(x=x, rank=10)
-be = M.Backend(dtype="fp32")
-cfg = M.MmConfig(max_iters=1000, epsilon=1e-300, monotone_tol=1e-6)
-M.nnmf_poisson_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
-torch.cuda.synchronize(); t = time.perf_counter()
-_, tr = M.nnmf_poisson_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
-torch.cuda.synchronize(); print(f"poisson-c1: {1e6*(time.perf_counter()-t)/1000:.1f} us/iter")
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'gram|vgw' --csv --log-file gpurun_out/lh.csv python bench.py --steps 3 --warmup 1 --no-e2e --no-suite --cpu-seconds 0 > /dev/null 2>&1
+python - <<'PY'
+import csv
+rows=list(csv.reader(open('gpurun_out/lh.csv')))
+for i,r in enumerate(rows):
+    if 'Kernel Name' in r: h=r; start=i; break
+ik=h.index('Kernel Name'); iv=h.index('Metric Value')
+for r in rows[start+1:][-6:]: print(r[ik][:30], float(r[iv].replace(',',''))/1000, 'us')
 PY
-python /tmp/pois_probe.py; MMK_SMALL_ENGINE=0 python /tmp/pois_probe.py
