@@ -934,7 +934,6 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     return off;
 }
 
-bool g_attr_done = false;
 unsigned long long* g_trace_v = nullptr;   // debug: mmk_tc_set_trace
 unsigned long long* g_trace_w = nullptr;
 
@@ -963,7 +962,7 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     TcWs L;
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);
-    if (!g_attr_done) {
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc))) {
         const char* dbg = getenv("MMK_TC_DBG");
         if (dbg) {
             const int v = atoi(dbg);
@@ -972,7 +971,6 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
         cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
-        g_attr_done = true;
     }
     CUtensorMap mX, mWh, mWl, mXt, mVh, mVl;
     int rc;
