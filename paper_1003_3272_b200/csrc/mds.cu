@@ -233,7 +233,7 @@ __global__ void mds_unpack_kernel(const T* __restrict__ g, T* __restrict__ theta
 //   every CTA sums the stress partials in the same order and applies the
 //   stopping rule itself (mm_step); CTA 0 records the trace.
 // One grid barrier per iteration.
-constexpr int kMdsSmallThr = 256;
+constexpr int kMdsSmallThr = 512;
 
 template <typename T>
 struct MdsSmall {

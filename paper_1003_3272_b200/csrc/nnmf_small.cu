@@ -38,7 +38,7 @@ namespace {
 
 using namespace mmk;
 
-constexpr int kThr = 256;
+constexpr int kThr = 512;
 constexpr int kWarps = kThr / 32;
 constexpr int kSmallR = 16;
 constexpr int kSub = 16;                // lanes per reduced entry in phase 2
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
         // ---- phase 1 ---------------------------------------------------------
         if constexpr (POIS) {
             // ws_k = sum_j w_kj (fp64): kWsSeg column segments per k, combined in order
-            constexpr int SEG = kThr / R >= 16 ? 16 : kThr / R;
+            constexpr int SEG = 256 / R >= 16 ? 16 : 256 / R;   // scratch (Gv) <= 256
             for (int t = tid; t < R * SEG; t += kThr) {
                 const int k = t / SEG, sg = t % SEG;
                 const int j0 = (int)((long long)sg * n / SEG), j1 = (int)((long long)(sg + 1) * n / SEG);
@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
         // threads, segments combined in order (fp64)
         {
             constexpr int NE = r * (r + 1) / 2;
-            constexpr int SEG = (NE * 4 <= kThr) ? 4 : ((NE * 2 <= kThr) ? 2 : 1);
+            // segments per entry: enough tasks for the block, scratch (Gv) <= 256
+            constexpr int SEG = (NE * 4 <= kThr && NE * 4 <= 256) ? 4
+                                : ((NE * 2 <= kThr && NE * 2 <= 256) ? 2 : 1);
             for (int t = tid; t < NE * SEG; t += kThr) {
                 const int e = t / SEG, sg = t % SEG;
                 int p = 0, rem = e;

@@ -587,7 +587,7 @@ int pet_sparse_a(const int32_t* rptr, const int32_t* ridx, const T* rval, const 
 // The projections gather from shared memory, in the order of pet_sfwd /
 // pet_sback, so lam is bitwise the graph path's; f differs from it only in
 // the grouping of the partial sums.
-constexpr int kPetSmallThr = 256;
+constexpr int kPetSmallThr = 512;
 
 template <typename T>
 struct PetSmall {
