@@ -223,6 +223,10 @@ def mds_run_sharded(problem, config, backend, group=None, theta0=None):
     every rank returns the same configuration and trace."""
     from . import mds as D
     from .driver import run_mm
+    if group is None:   # the default process group, as torch.distributed collectives use it
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            group = dist.group.WORLD
     if theta0 is None:
         theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
                                                             size=(problem.p, problem.q))
