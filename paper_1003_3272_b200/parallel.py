@@ -239,3 +239,47 @@ def mds_run_sharded(problem, config, backend, group=None, theta0=None):
         _allreduce_status(mm.status, group)
     mm._iterate = _iterate
     return run_mm(mm, mm.device_state(theta0), config)
+
+
+def pet_run_sharded(problem, config, backend, group=None):
+    """Ray-sharded penalized PET: rank r holds the rays
+    shard_rows(n_rays, world, r) of a host-matrix ``PetProblem`` (dense or
+    sparse projector); lam is replicated.  Per iteration: the projection phase
+    on the local rays leaves [b | loglik] (p + 1 doubles), one all-reduce,
+    then every rank applies the same pixel update and objective.  Returns
+    (lam, MmTrace) on every rank, from the flat start lam = 1 as pet_run."""
+    import torch.distributed as dist
+
+    from . import _arrays as A
+    from . import _lib as L
+    from . import pet as PT
+    from .driver import run_mm
+    if group is None and dist.is_available() and dist.is_initialized():
+        group = dist.group.WORLD
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if group is not None else 0
+    lo, hi = shard_rows(problem.n_rays, world, rank)
+
+    class _Sharded(PT._GpuPet):
+        def _iterate(self, lam, out, f_ptr, err_ptr,
+                     flags=L.MMK_PET_UPDATE | L.MMK_PET_OBJECTIVE):
+            st, P = self.stream(), L.ptr
+            if self.sparse:
+                sa = self.sa
+                L.call("mmk_pet_sparse_iter_a", self.code, P(sa["rptr"]), P(sa["ridx"]),
+                       P(sa["rval"]), P(sa["cptr"]), P(sa["cidx"]), P(sa["cval"]), P(self.y),
+                       P(lam), self.d, self.p, P(self.ws), self.ws.numel(), P(self.red),
+                       err_ptr, st)
+            else:
+                L.call("mmk_pet_iter_a", self.code, P(self.e), self.e.stride(0), P(self.y),
+                       P(lam), self.d, self.p, P(self.ws), self.ws.numel(), P(self.red), err_ptr,
+                       st)
+            allreduce_sum_(self.red, group)
+            _allreduce_status(self.status, group)
+            L.call("mmk_pet_iter_b", self.code, P(lam), P(out), self.p, P(self.ptr), P(self.idx),
+                   self.mu, flags, P(self.red), P(self.ws), self.ws.numel(), f_ptr, err_ptr, st)
+
+    mm = _Sharded(problem, backend, rows=(lo, hi))
+    mm.__dict__.pop("run_fused", None)     # per-iteration protocol
+    state, trace = run_mm(mm, mm.device_state(np.ones(problem.n_pixels)), config)
+    return A.to_user(state, problem.e), trace

@@ -122,3 +122,35 @@ def test_mds_tri_two_ranks():
                          theta0=th0)
     assert G.rel(t0, rtr.objective_values) <= 1e-6
     assert G.rel(th0s, np.asarray(ref)) <= 1e-5
+
+
+def _pet_worker(rank, world, port, kernel, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import parallel as P
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        e, y, nbrs = G.c2_inputs()
+        prob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=nbrs)
+        lam, tr = P.pet_run_sharded(prob, M.MmConfig(max_iters=50, epsilon=1e-300),
+                                    M.Backend(dtype="fp64", pet_kernel=kernel))
+        q.put((rank, tr.objective_values, np.asarray(lam), None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e), None, None))
+
+
+@pytest.mark.parametrize("kernel", ["dense", "sparse"])
+def test_pet_two_ranks(kernel):
+    """Ray shards (1008 rays each at C2) with the all-reduce of [b | loglik]."""
+    import paper_1003_3272_b200 as M
+    out = _run_ranks(_pet_worker, kernel)
+    (_, t0, l0, _), (_, t1, l1, _) = out
+    assert np.array_equal(t0, t1) and np.array_equal(l0, l1)
+    e, y, nbrs = G.c2_inputs()
+    prob = M.PetProblem(e=e, y=y, mu=1e-5, neighborhoods=nbrs)
+    ref, rtr = M.pet_run(prob, M.MmConfig(max_iters=50, epsilon=1e-300),
+                         M.Backend(dtype="fp64", pet_kernel=kernel))
+    assert G.rel(t0, rtr.objective_values) <= 1e-12
+    assert G.rel(l0, ref) <= 1e-11
