@@ -217,16 +217,25 @@ def nnmf_run_sharded(x_local, rank, config, backend, group=None, state0=None, po
 
 
 def mds_run_sharded(problem, config, backend, group=None, theta0=None):
-    """Tile-sharded packed-triangle MDS: ``problem`` is this rank's
-    ``PackedMdsProblem`` (tiles ``tile_range(ntiles, world, rank)``), theta is
-    replicated.  One all-reduce of the per-point accumulators per iteration;
-    every rank returns the same configuration and trace."""
+    """Sharded MDS; every rank returns the same configuration and trace.
+
+    * ``PackedMdsProblem`` (unit weights, packed triangle): ``problem`` is this
+      rank's tile slice (``tile_range(ntiles, world, rank)``); one all-reduce
+      of the per-point accumulators per iteration.
+    * dense ``MdsProblem`` (any weights): rank r owns the points
+      ``shard_rows(n, world, r)`` and uploads only their rows of Y (and W);
+      per iteration it updates its points (``mmk_mds_iter`` on its row block),
+      all-gathers the new coordinates and all-reduces the stress partial
+      (SURVEY.md 8(e)).
+    theta is replicated."""
     from . import mds as D
     from .driver import run_mm
     if group is None:   # the default process group, as torch.distributed collectives use it
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():
             group = dist.group.WORLD
+    if not isinstance(problem, D.PackedMdsProblem):
+        return _mds_rows_sharded(problem, config, backend, group, theta0)
     if theta0 is None:
         theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
                                                             size=(problem.p, problem.q))
@@ -238,6 +247,78 @@ def mds_run_sharded(problem, config, backend, group=None, theta0=None):
         base_iter(theta, out, f_ptr, err_ptr)
         _allreduce_status(mm.status, group)
     mm._iterate = _iterate
+    return run_mm(mm, mm.device_state(theta0), config)
+
+
+def _mds_rows_sharded(problem, config, backend, group, theta0):
+    import torch
+    import torch.distributed as dist
+
+    from . import _arrays as A
+    from . import _lib as L
+    from . import mds as D
+    from ._engine import DeviceMm
+    from .driver import run_mm
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if group is not None else 0
+    n, dim = problem.q, problem.p
+    bounds = [shard_rows(n, world, r) for r in range(world)]
+    lo, hi = bounds[rank]
+    pad = max(b - a for a, b in bounds)
+    if theta0 is None:
+        theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0, size=(dim, n))
+
+    class _RowsMm(DeviceMm):
+        direction = "minimize"
+
+        def __init__(self):
+            super().__init__(backend)
+            t = self.torch
+            self.y = A.to_device(problem.dissimilarities[lo:hi], backend, t)
+            self.w = None if problem.unit_weights else A.to_device(problem.weights[lo:hi],
+                                                                   backend, t)
+            self.wsum = t.from_numpy(np.ascontiguousarray(problem.weight_sums)).to(self.device)
+            self.ws = t.zeros(L.ws_bytes("mmk_mds_ws_bytes", self.code, n, dim, max(hi - lo, 1)),
+                              dtype=t.uint8, device=self.device)
+            self.local = t.zeros((dim, pad), dtype=self.dtype, device=self.device)
+            self.parts = [t.zeros((dim, pad), dtype=self.dtype, device=self.device)
+                          for _ in range(world)]
+
+        def device_state(self, theta):
+            return A.to_device(theta, backend, self.torch)
+
+        def _alloc_like(self, s):
+            return self.torch.empty_like(s)
+
+        def _copy_into(self, dst, src):
+            dst.copy_(src)
+
+        def _bytes_per_iter(self):
+            return float((1 if self.w is None else 2) * (hi - lo) * n * self.y.element_size())
+
+        def _messages(self):
+            return {1: D._coincide_msg(n)}
+
+        def _iterate(self, theta, out, f_ptr, err_ptr):
+            P = L.ptr
+            if hi > lo:
+                L.call("mmk_mds_iter", self.code, P(self.y), P(self.w) if self.w is not None
+                       else None, n, P(self.wsum), P(theta), P(self.local), pad, dim, n, lo,
+                       hi - lo, L.MMK_MDS_UPDATE | L.MMK_MDS_OBJECTIVE, P(self.ws),
+                       self.ws.numel(), f_ptr, err_ptr, self.stream())
+            else:
+                self.status.dev[0:1].zero_()
+            if group is not None:
+                dist.all_reduce(self.status.dev[0:1].view(self.torch.float64), group=group)
+                dist.all_gather(self.parts, self.local, group=group)
+                _allreduce_status(self.status, group)
+            else:
+                self.parts[0].copy_(self.local)
+            for r, (a, b) in enumerate(bounds):
+                out[:, a:b].copy_(self.parts[r][:, :b - a])
+
+    mm = _RowsMm()
+    mm.__dict__.pop("run_fused", None)     # per-iteration protocol
     return run_mm(mm, mm.device_state(theta0), config)
 
 

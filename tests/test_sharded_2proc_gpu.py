@@ -154,3 +154,47 @@ def test_pet_two_ranks(kernel):
                          M.Backend(dtype="fp64", pet_kernel=kernel))
     assert G.rel(t0, rtr.objective_values) <= 1e-12
     assert G.rel(l0, ref) <= 1e-11
+
+
+def _mds_rows_worker(rank, world, port, weighted, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import parallel as P
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        prob, th0 = _mds_rows_problem(weighted)
+        th, tr = P.mds_run_sharded(prob, M.MmConfig(max_iters=40, epsilon=1e-300),
+                                   M.Backend(dtype="fp64"), theta0=th0)
+        th = th.cpu().numpy() if hasattr(th, "cpu") else np.asarray(th)
+        q.put((rank, tr.objective_values, th, None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e), None, None))
+
+
+def _mds_rows_problem(weighted):
+    import paper_1003_3272_b200 as M
+    diss, th0 = G.c3_inputs(3)
+    w = 1.0 - np.eye(401)
+    if weighted:
+        rng = np.random.default_rng(9)
+        w = rng.random((401, 401)) + 0.5
+        w = np.triu(w, 1) + np.triu(w, 1).T
+    return M.MdsProblem(weights=w, dissimilarities=diss, p=3), th0
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_mds_rows_two_ranks(weighted):
+    """Dense MDS, points split over the ranks: each rank updates its points from
+    its rows of Y (and W), then all-gather of theta' and all-reduce of the
+    stress partial."""
+    import paper_1003_3272_b200 as M
+    out = _run_ranks(_mds_rows_worker, weighted)
+    (_, t0, th0s, _), (_, t1, th1s, _) = out
+    assert np.array_equal(t0, t1) and np.array_equal(th0s, th1s)
+    prob, th0 = _mds_rows_problem(weighted)
+    ref, rtr = M.mds_run(prob, M.MmConfig(max_iters=40, epsilon=1e-300), M.Backend(dtype="fp64"),
+                         theta0=th0)
+    assert G.rel(t0, rtr.objective_values) <= 1e-12
+    assert G.rel(th0s, np.asarray(ref)) <= 1e-10
