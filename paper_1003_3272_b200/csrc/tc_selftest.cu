@@ -264,3 +264,92 @@ extern "C" int mmk_tc_mma_bench(int mode, int iters, long long* out, void* strea
     MMK_CHECK_LAUNCH("tc_mma_bench_kernel");
     return MMK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// 2-CTA (cta_group::2) issue-rate microbenchmark: a cluster of two CTAs (one
+// TPC), the leader issues `iters` back-to-back kind::f16 MMAs of M = 256
+// (128 rows per SM) x N x K16, all SS from zeroed shared memory, then one
+// multicast commit; cycles of the leader into out[0], a timeout flag into
+// out[1] (bounded waits: a wrong encoding cannot hang the GPU).
+namespace {
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
+tc_mma2_bench_kernel(int ncols, int iters, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t rank = cluster_rank();
+    for (int i = tid; i < 64 * 1024 / 4; i += 128) reinterpret_cast<float*>(base)[i] = 0.f;
+    tc::fence_async_smem();
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            tc::smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc::tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (rank == 0 && tid == 0) {
+        const uint64_t da = tc::sdesc_sw128(base, 16, 1024);
+        const uint64_t db = tc::sdesc_sw128(base + 32768, 16, 1024);
+        // kind::f16: a/b F16, c F32; N >> 3 at bit 17, M >> 4 at bit 24 (M = 256)
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
+                "l"(da), "l"(db), "r"(idesc), "r"(i ? 1u : 0u)
+                : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+            "[%0], %1;" ::"r"(tc::smem_u32(&bar)),
+            "h"((unsigned short)3)
+            : "memory");
+        const bool ok = tc::mbar_wait_bounded(&bar, 0);
+        out[0] = clock64() - t0;
+        out[1] = ok ? 0 : 1;
+    }
+    if (rank == 1 && tid == 0) {
+        if (!tc::mbar_wait_bounded(&bar, 0)) out[2] = 1;
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+}  // namespace
+
+extern "C" int mmk_tc_mma2_bench(int ncols, int iters, long long* out, void* stream) {
+    if (ncols < 16 || ncols > 256 || (ncols % 16)) {
+        mmk_host::set_error("mma2 bench: N must be a multiple of 16 in [16, 256]");
+        return MMK_E_SHAPE;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaFuncSetAttribute(tc_mma2_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         70 * 1024);
+    tc_mma2_bench_kernel<<<2, 128, 70 * 1024, st>>>(ncols, iters, out);
+    MMK_CHECK_LAUNCH("tc_mma2_bench_kernel");
+    return MMK_OK;
+}
