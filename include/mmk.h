@@ -378,7 +378,8 @@ int mmk_selftest_tc(const float *A, const float *B, const float *X, const float 
 int mmk_tc_mma_bench(int mode, int iters, long long *out, void *stream);
 
 /* Tuning aid: the same for cta_group::2 (a 2-CTA cluster, M = 256, kind::f16,
- * N = ncols): leader cycles into out[0], timeout flags into out[1], out[2]. */
+ * N = |ncols|, A from TMEM when ncols < 0): leader cycles into out[0],
+ * timeout flags into out[1], out[2]. */
 int mmk_tc_mma2_bench(int ncols, int iters, long long *out, void *stream);
 
 /* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core

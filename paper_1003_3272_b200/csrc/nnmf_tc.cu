@@ -69,6 +69,7 @@ constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
 // experiment switches (MMK_TC_DBG, timing studies only; results are wrong
 // when set): 1 skip the lo MMAs, 2 skip the split, 4 skip all MMAs
 __constant__ int c_dbg = 0;
+__constant__ int c_trace_cta = 0;   // CTA whose pipeline the debug trace records
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -103,7 +104,9 @@ struct Bars {
     uint64_t dfull, dempty;
 };
 
-__device__ __forceinline__ void init_bars(Bars& B) {
+// pair: the leader's afull / dempty also count one arrival of the peer CTA
+__device__ __forceinline__ void init_bars(Bars& B, bool pair = false) {
+    const uint32_t two = pair ? 2 : 1;
     for (int s = 0; s < XST; ++s) {
         tc::mbar_init(&B.xfull[s], 1);
         tc::mbar_init(&B.xempty[s], 128);   // released by the split warps
@@ -113,11 +116,11 @@ __device__ __forceinline__ void init_bars(Bars& B) {
         tc::mbar_init(&B.oempty[s], 1);
     }
     for (int b = 0; b < NA; ++b) {
-        tc::mbar_init(&B.afull[b], 128);
+        tc::mbar_init(&B.afull[b], 128 + (two - 1));   // pair: + one arrival from the peer
         tc::mbar_init(&B.aempty[b], 1);
     }
     tc::mbar_init(&B.dfull, 1);
-    tc::mbar_init(&B.dempty, 128);
+    tc::mbar_init(&B.dempty, 128 + (two - 1));
     tc::fence_barrier_init();
 }
 
@@ -127,18 +130,38 @@ __device__ __forceinline__ void init_bars(Bars& B) {
 // K16 step a TS MMA with N = 128 gives D[:, 0:64] += X_hi.B_hi and
 // D[:, 64:128] += X_hi.B_lo, and a TS MMA with N = 64 adds X_lo.B_hi into
 // D[:, 0:64].  The epilogue sums the two halves.
+//
+// PAIR (CTA pair, cta_group::2, M = 256): each CTA's TMEM holds its own 128
+// rows of X_hi / X_lo and of D; the operand's N = 128 rows are split between
+// the pair -- B_hi in the leader's stage, B_lo at the same offset in the
+// peer's -- and both MMAs of a K16 step use that B with N = 128: X_hi.[B_hi;B_lo]
+// and X_lo.[B_hi;B_lo].  The second adds X_lo.B_lo to D[:, 64:128], the one
+// product the single-CTA path leaves out (it only makes the sum more exact).
+// A pair MMA runs at the full tensor rate (64 cycles at N = 128, measured)
+// where a single-CTA M = 128 one costs ~175 cycles whatever N is.
+template <bool PAIR>
 __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bhl,
                                             bool first) {
-    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
-    constexpr uint32_t id_lo = idesc_f16(BM, R);
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const int dbg = c_dbg;
     if (dbg & 4) return;
+    if constexpr (PAIR) {
+        constexpr uint32_t id = idesc_f16(2 * BM, ACC);
 #pragma unroll
-    for (int ks = 0; ks < BK / 16; ++ks) {
-        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-        tc::mma_f16ts(d, a + ks * 8, db0 + ks * 2, id_hi, acc);
-        if (!(dbg & 1)) tc::mma_f16ts(d, a + 32 + ks * 8, db0 + ks * 2, id_lo, 1);
+        for (int ks = 0; ks < BK / 16; ++ks) {
+            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+            tc::mma_f16ts_pair(d, a + ks * 8, db0 + ks * 2, id, acc);
+            if (!(dbg & 1)) tc::mma_f16ts_pair(d, a + 32 + ks * 8, db0 + ks * 2, id, 1);
+        }
+    } else {
+        constexpr uint32_t id_hi = idesc_f16(BM, ACC);
+        constexpr uint32_t id_lo = idesc_f16(BM, R);
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks) {
+            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+            tc::mma_f16ts(d, a + ks * 8, db0 + ks * 2, id_hi, acc);
+            if (!(dbg & 1)) tc::mma_f16ts(d, a + 32 + ks * 8, db0 + ks * 2, id_lo, 1);
+        }
     }
 }
 
@@ -201,17 +224,42 @@ __device__ __forceinline__ void store_hilo(const float* x, uint32_t a_addr) {
 // start (operands ready), [4] MMAs issued + committed
 constexpr int kTrace = 256;
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int xit) {
-    if (tr && blockIdx.x == 0 && xit < kTrace) tr[what * kTrace + xit] = clock64();
+    if (tr && (int)blockIdx.x == c_trace_cta && xit < kTrace) tr[what * kTrace + xit] = clock64();
 }
 
-template <bool MN, class PassOf, class LoadX, class LoadOp, class Epi>
+// PAIR: the kernel runs as CTA pairs (cluster of 2).  Each CTA streams and
+// splits its own X tiles into its own TMEM and loads its half of the operand
+// chunk (the loader counts both halves on the leader's ofull); only the
+// leader's MMA warp issues (M = 256) and its commits arrive on the barriers of
+// both CTAs (multicast); the peer's split and epilogue warps arrive on the
+// leader's afull / dempty.
+template <bool MN, bool PAIR, class PassOf, class LoadX, class LoadOp, class Epi>
 __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tmem, int npass,
                                              float xscale, const PassOf& pass_of,
                                              const LoadX& load_x, const LoadOp& load_op,
                                              const Epi& epilogue, unsigned long long* tr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? tc::cluster_rank() : 0u;
     uint8_t* xring = base;
     uint8_t* oring = base + XST * SX;
+    auto wait = [](uint64_t* bar, uint32_t parity) {
+        if constexpr (PAIR)
+            tc::mbar_wait_cluster(bar, parity);
+        else
+            tc::mbar_wait(bar, parity);
+    };
+    auto arrive_leader = [](uint64_t* bar) {
+        if constexpr (PAIR)
+            tc::mbar_arrive_cluster(tc::map_to_rank(bar, 0));
+        else
+            tc::mbar_arrive(bar);
+    };
+    auto commit = [](uint64_t* bar) {
+        if constexpr (PAIR)
+            tc::mma_commit_pair(bar);
+        else
+            tc::mma_commit(bar);
+    };
     if (warp == 0) {
         if (lane == 0) {
             int xit = 0, oit = 0;
@@ -219,8 +267,8 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                 const Pass P = pass_of(p);
                 for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
                     const int os = oit % OST;
-                    tc::mbar_wait(&B.oempty[os], ((oit / OST) & 1) ^ 1);
-                    tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                    wait(&B.oempty[os], ((oit / OST) & 1) ^ 1);
+                    if (rank == 0) tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
                     load_op(p, kb, oring + os * 2 * SOP, &B.ofull[os]);
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
                         const int xs = xit % XST;
@@ -233,28 +281,28 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             int xit = 0, oit = 0;
             for (int p = 0; p < npass; ++p) {
                 const Pass P = pass_of(p);
-                if (p > 0) tc::mbar_wait(&B.dempty, (p - 1) & 1);
+                if (p > 0) wait(&B.dempty, (p - 1) & 1);
                 tc::tc_fence_after();
                 for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
                     const int os = oit % OST;
-                    tc::mbar_wait(&B.ofull[os], (oit / OST) & 1);
+                    wait(&B.ofull[os], (oit / OST) & 1);
                     const uint8_t* ob = oring + os * 2 * SOP;
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
                         const int ab = xit % NA;
-                        tc::mbar_wait(&B.afull[ab], (xit / NA) & 1);
+                        wait(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
-                        issue_stage(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
-                        tc::mma_commit(&B.aempty[ab]);   // A buffer ab free once these finish
+                        issue_stage<PAIR>(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
+                        commit(&B.aempty[ab]);   // A buffer ab free once these finish
                         trace_at(tr, 4, xit);
                     }
-                    tc::mma_commit(&B.oempty[os]);
+                    commit(&B.oempty[os]);
                 }
-                tc::mma_commit(&B.dfull);
+                commit(&B.dfull);
             }
         }
     } else if (warp < 2 + NCONV) {
@@ -274,12 +322,19 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     // the values are in registers (consumed below): release the slot
                     tc::mbar_arrive(&B.xempty[xs]);
                     // A buffer ab was last read by the MMAs of stage xit - NA
-                    if (xit >= NA) tc::mbar_wait(&B.aempty[ab], ((xit / NA) - 1) & 1);
+                    if (xit >= NA) wait(&B.aempty[ab], ((xit / NA) - 1) & 1);
                     tc::tc_fence_after();
                     if (!(c_dbg & 2)) store_hilo(x, tmem + TM_A + ab * 64 + lane_off);
                     tc::tmem_st_wait();
                     tc::tc_fence_before();
-                    tc::mbar_arrive(&B.afull[ab]);
+                    if (!PAIR || rank == 0) {
+                        tc::mbar_arrive(&B.afull[ab]);
+                    } else {
+                        // the group's 128 threads meet on a named barrier, then
+                        // ONE cluster-scope release arrive on the leader's afull
+                        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+                        if (quarter == 0 && lane == 0) arrive_leader(&B.afull[ab]);
+                    }
                     if (quarter == 0 && lane == 0) trace_at(tr, 2, xit);
                 }
             }
@@ -288,13 +343,18 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
         const int quarter = warp & 3;
         for (int p = 0; p < npass; ++p) {
             const Pass P = pass_of(p);
-            tc::mbar_wait(&B.dfull, p & 1);
+            wait(&B.dfull, p & 1);
             tc::tc_fence_after();
             for (int j = 0; j < P.nacc; ++j)
                 epilogue(p, j, quarter, lane,
                          tmem + j * ACC + ((uint32_t)(quarter * 32) << 16), P.nkb > 0);
             tc::tc_fence_before();
-            tc::mbar_arrive(&B.dempty);
+            if (!PAIR || rank == 0) {
+                tc::mbar_arrive(&B.dempty);
+            } else {
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                if (quarter == 0 && lane == 0) arrive_leader(&B.dempty);
+            }
         }
     }
 }
@@ -307,6 +367,9 @@ struct Scales {
 };
 
 // ---------------------------------------------------------------------------
+// PAIR: launched as clusters of 2 (CTA pairs); pair q takes the 256-row
+// units q, q + G/2, ... and CTA rank r of the pair their 128-row half r.
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
@@ -320,31 +383,48 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __shared__ float vmx[kThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
-    const int mine = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int rank = PAIR ? (int)tc::cluster_rank() : 0;
+    const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const int me = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int units = PAIR ? (ntiles + 1) / 2 : ntiles;
+    const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
     const int npass = (mine + TMAX - 1) / TMAX;
     if (threadIdx.x == 0) {
-        init_bars(B);
+        init_bars(B, PAIR);
         tc::tma_prefetch(&mX);
         tc::tma_prefetch(&mWh);
         tc::tma_prefetch(&mWl);
     }
-    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tc::tmem_alloc_pair<TM_COLS>(&tmem_base);
+        else
+            tc::tmem_alloc<TM_COLS>(&tmem_base);
+    }
     tc::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();   // barriers initialised, TMEM allocated in both
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
     const float xscale = exp2f((float)sc->ex);
     const double qscale = exp2(-(double)(sc->ex + sc->ew));
     double acc = 0.0, gacc = 0.0;
     float vmax = 0.f;
-    auto tile_of = [&](int p, int j) { return (int)blockIdx.x + (p * TMAX + j) * (int)gridDim.x; };
+    auto tile_of = [&](int p, int j) {
+        const int u = me + (p * TMAX + j) * G;
+        return PAIR ? 2 * u + rank : u;
+    };
     auto pass_of = [&](int p) {
         const int left = mine - p * TMAX;
         return Pass{left < TMAX ? left : TMAX, nk};
     };
     auto load_op = [&](int, int kb, uint8_t* dst, uint64_t* bar) {
-        tc::tma_load_2d(dst, &mWh, bar, kb * BK, 0);
-        tc::tma_load_2d(dst + SOP, &mWl, bar, kb * BK, 0);
+        if constexpr (PAIR) {   // this CTA's half of [W_hi; W_lo], counted on the leader
+            tc::tma_load_2d_pair(dst, rank == 0 ? &mWh : &mWl, tc::map_to_rank(bar, 0), kb * BK, 0);
+        } else {
+            tc::tma_load_2d(dst, &mWh, bar, kb * BK, 0);
+            tc::tma_load_2d(dst + SOP, &mWl, bar, kb * BK, 0);
+        }
     };
     auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
         tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
@@ -380,7 +460,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     };
-    run_pipeline<false>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue, tr);
+    run_pipeline<false, PAIR>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
+                              tr);
     // per-CTA partials <V, Q>, <V, V G_W> and max(V') (epilogue warps)
     __shared__ double gred[kThreads / 32];
     acc = warp_sum(acc);
@@ -406,7 +487,13 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         part[gridDim.x + blockIdx.x] = gg;
         atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
     }
-    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    if constexpr (PAIR) {
+        tc::tc_fence_before();
+        tc::cluster_sync();   // both CTAs done with the pair's TMEM
+        if (warp == 1) tc::tmem_free_pair<TM_COLS>(tmem);
+    } else {
+        if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -415,6 +502,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
 // hi / lo, K-major along rows) are shared by the CB column blocks of an item.
 // X tiles arrive as 4 boxes of [64 rows x 32 columns] (128B swizzle); split
 // thread `lane` of warp quarter q owns column 32 q + lane of the block.
+// PAIR: clusters of 2; an item covers 2 CB column blocks, CTA rank r takes
+// blocks 2 j + r of it.
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mVh,
               const __grid_constant__ CUtensorMap mVl, const Scales* sc, int m, int n,
@@ -424,47 +514,65 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __shared__ Bars B;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5;
+    const int rank = PAIR ? (int)tc::cluster_rank() : 0;
+    const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const int me = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int span = PAIR ? 2 * CB : CB;   // column blocks per item
     const int ncb = (n + BM - 1) / BM;
-    const int ncs = (ncb + CB - 1) / CB;
+    const int ncs = (ncb + span - 1) / span;
     const int nitems = ncs * splits;
-    const int npass = nitems > (int)blockIdx.x ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int npass = nitems > me ? (nitems - 1 - me) / G + 1 : 0;
     if (threadIdx.x == 0) {
-        init_bars(B);
+        init_bars(B, PAIR);
         tc::tma_prefetch(&mX);
         tc::tma_prefetch(&mVh);
         tc::tma_prefetch(&mVl);
     }
-    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tc::tmem_alloc_pair<TM_COLS>(&tmem_base);
+        else
+            tc::tmem_alloc<TM_COLS>(&tmem_base);
+    }
     tc::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
     const float xscale = exp2f((float)sc->ex);
-    auto item_of = [&](int p) { return (int)blockIdx.x + p * (int)gridDim.x; };
+    auto item_of = [&](int p) { return me + p * G; };
+    auto block_of = [&](int item, int j) {
+        return (item % ncs) * span + (PAIR ? 2 * j + rank : j);
+    };
     auto pass_of = [&](int p) {
         const int item = item_of(p), s = item / ncs, cs = item % ncs;
         const int r0 = s * rows_per_split;
         int r1 = r0 + rows_per_split;
         if (r1 > m) r1 = m;
-        const int left = ncb - cs * CB;
+        int left = ncb - cs * span;
+        if (PAIR) left = (left + 1) / 2;   // the leader's share (the peer's may be one less)
         return Pass{left < CB ? left : CB, r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0};
     };
     auto load_op = [&](int p, int kb, uint8_t* dst, uint64_t* bar) {
         const int row = (item_of(p) / ncs) * rows_per_split + kb * BK;
-        tc::tma_load_2d(dst, &mVh, bar, row, 0);
-        tc::tma_load_2d(dst + SOP, &mVl, bar, row, 0);
+        if constexpr (PAIR) {
+            tc::tma_load_2d_pair(dst, rank == 0 ? &mVh : &mVl, tc::map_to_rank(bar, 0), row, 0);
+        } else {
+            tc::tma_load_2d(dst, &mVh, bar, row, 0);
+            tc::tma_load_2d(dst + SOP, &mVl, bar, row, 0);
+        }
     };
     auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
         const int item = item_of(p);
         const int row = (item / ncs) * rows_per_split + kb * BK;
-        const int col0 = ((item % ncs) * CB + j) * BM;
+        const int col0 = block_of(item, j) * BM;
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
             tc::tma_load_2d(dst + jj * (BK * 128), &mX, bar, col0 + 32 * jj, row);
     };
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool any) {
         const int item = item_of(p), s = item / ncs;
-        const long long col = (long long)((item % ncs) * CB + j) * BM + quarter * 32 + ln;
+        const long long col = (long long)block_of(item, j) * BM + quarter * 32 + ln;
         float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
@@ -486,10 +594,16 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     };
-    run_pipeline<true>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue, tr);
+    run_pipeline<true, PAIR>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
+                             tr);
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    if constexpr (PAIR) {
+        tc::cluster_sync();
+        if (warp == 1) tc::tmem_free_pair<TM_COLS>(tmem);
+    } else {
+        if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    }
 }
 
 // sum of x^2 and max(x) over X, cached in the workspace and keyed by
@@ -835,12 +949,28 @@ struct TcPlan {
     int vgrid, wgrid, splits, rows_per_split;
 };
 
-TcPlan tc_plan(long long m, long long n) {
+// pair: CTA pairs (cta_group::2) -- kNumSMs / 2 work slots of 256 rows
+// (V step) or 2 CB column blocks (W step); grids are even.  Experimental,
+// opt-in (MMK_TC_PAIR=1): correct (tests/test_nnmf_tc_gpu.py passes with it),
+// but with NA = 4 TMEM A buffers the cross-CTA split -> MMA -> commit loop
+// (~6.7k cycles) paces a stage at ~1.7k cycles against ~1.17k for single
+// CTAs (scripts/tctrace.py), so the single-CTA kernels stay the default.
+bool pair_on() {
+    static const bool on = [] {
+        const char* e = getenv("MMK_TC_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+TcPlan tc_plan(long long m, long long n, bool pair) {
     TcPlan P;
+    const int slots = pair ? kNumSMs / 2 : kNumSMs;
     const int ntiles = (int)((m + BM - 1) / BM);
-    P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
+    const int units = pair ? (ntiles + 1) / 2 : ntiles;
+    P.vgrid = (units < slots ? units : slots) * (pair ? 2 : 1);
     const int ncb = (int)((n + BM - 1) / BM);
-    const int ncs = (ncb + CB - 1) / CB;
+    const int ncs = (ncb + (pair ? 2 * CB : CB) - 1) / (pair ? 2 * CB : CB);
     // split count minimising (wave quantisation loss) + (split-K partial
     // traffic: S fp32 partials of n x 64 written and read back, relative to
     // one pass over X); rows per split >= 4 K-blocks
@@ -849,8 +979,8 @@ TcPlan tc_plan(long long m, long long n) {
     double best_cost = 1e300;
     for (int S = 1; S <= max_splits && S <= 4 * kNumSMs; ++S) {
         const int items = ncs * S;
-        const int waves = (items + kNumSMs - 1) / kNumSMs;
-        const double eff = (double)items / ((double)waves * kNumSMs);
+        const int waves = (items + slots - 1) / slots;
+        const double eff = (double)items / ((double)waves * slots);
         const double partial = 2.0 * S * (double)n * R * 4.0 / ((double)m * n * 4.0);
         const double cost = 1.0 / eff + partial;
         if (cost < best_cost - 1e-12) {
@@ -863,7 +993,7 @@ TcPlan tc_plan(long long m, long long n) {
     P.rows_per_split = (int)rps;
     P.splits = (int)((m + rps - 1) / rps);
     const int items = ncs * P.splits;
-    P.wgrid = items < kNumSMs ? items : kNumSMs;
+    P.wgrid = (items < slots ? items : slots) * (pair ? 2 : 1);
     return P;
 }
 
@@ -897,7 +1027,10 @@ struct TcWs {
 inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
 
 size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
-    const TcPlan P = tc_plan(m, n);
+    // room for the split-K partials of either plan (single CTAs or pairs)
+    TcPlan P = tc_plan(m, n, false);
+    const TcPlan P2 = tc_plan(m, n, true);
+    if (P2.splits > P.splits) P.splits = P2.splits;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -961,17 +1094,40 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
            cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
-    const TcPlan P = tc_plan(m, n);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc))) {
+    const bool pair = pair_on();
+    const TcPlan P = tc_plan(m, n, pair);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc<false>))) {
         const char* dbg = getenv("MMK_TC_DBG");
         if (dbg) {
             const int v = atoi(dbg);
             cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
         }
-        cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        if (const char* tc = getenv("MMK_TRACE_CTA")) {
+            const int v = atoi(tc);
+            cudaMemcpyToSymbol(c_trace_cta, &v, sizeof(int));
+        }
+        cudaFuncSetAttribute(nnmf_vstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(nnmf_wstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(nnmf_vstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(nnmf_wstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
     }
+    // cluster launch of the pair kernels (2 CTAs = one TPC)
+    auto launch_pair = [&](auto kern, int grid, auto... args) {
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = SMEM;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        (void)cudaLaunchKernelEx(&cfg, kern, args...);
+    };
     CUtensorMap mX, mWh, mWl, mXt, mVh, mVl;
     int rc;
     if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
@@ -994,10 +1150,14 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     MMK_LAUNCH("nnmf_vgw",
                st, (vgw_kernel<<<ceil_div(m, 64 * VGW_CHUNKS), 256, VGW_SMEM, st>>>(V, GW, L.DEN,
                                                                                 m)));
-    MMK_LAUNCH("nnmf_vstep_tc", st,
-               (nnmf_vstep_tc<<<P.vgrid, kThreads, SMEM, st>>>(mX, mWh, mWl, V, L.DEN, V_out, L.sc,
-                                                                (int)m, (int)n, L.part,
-                                                                g_trace_v)));
+    if (pair)
+        MMK_LAUNCH("nnmf_vstep_tc", st,
+                   launch_pair(nnmf_vstep_tc<true>, P.vgrid, mX, mWh, mWl, V, (const float*)L.DEN,
+                               V_out, L.sc, (int)m, (int)n, L.part, g_trace_v));
+    else
+        MMK_LAUNCH("nnmf_vstep_tc", st,
+                   (nnmf_vstep_tc<false><<<P.vgrid, kThreads, SMEM, st>>>(
+                       mX, mWh, mWl, V, L.DEN, V_out, L.sc, (int)m, (int)n, L.part, g_trace_v)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx,
@@ -1005,10 +1165,15 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
                (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
-    MMK_LAUNCH("nnmf_wstep_tc", st,
-               (nnmf_wstep_tc<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mVh, mVl, L.sc, (int)m, (int)n,
-                                                                P.splits, P.rows_per_split,
-                                                                L.wpart, g_trace_w)));
+    if (pair)
+        MMK_LAUNCH("nnmf_wstep_tc", st,
+                   launch_pair(nnmf_wstep_tc<true>, P.wgrid, mXt, mVh, mVl, (const Scales*)L.sc,
+                               (int)m, (int)n, P.splits, P.rows_per_split, L.wpart, g_trace_w));
+    else
+        MMK_LAUNCH("nnmf_wstep_tc", st,
+                   (nnmf_wstep_tc<false><<<P.wgrid, kThreads, SMEM, st>>>(
+                       mXt, mVh, mVl, L.sc, (int)m, (int)n, P.splits, P.rows_per_split, L.wpart,
+                       g_trace_w)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
                (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,

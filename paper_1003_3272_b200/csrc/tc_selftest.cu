@@ -311,15 +311,25 @@ tc_mma2_bench_kernel(int ncols, int iters, long long* out) {
         const uint64_t da = tc::sdesc_sw128(base, 16, 1024);
         const uint64_t db = tc::sdesc_sw128(base + 32768, 16, 1024);
         // kind::f16: a/b F16, c F32; N >> 3 at bit 17, M >> 4 at bit 24 (M = 256)
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+        const int nc = ncols < 0 ? -ncols : ncols;
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(nc >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
         long long t0 = clock64();
+        const bool ts = ncols < 0;
         for (int i = 0; i < iters; ++i) {
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
-                "l"(da), "l"(db), "r"(idesc), "r"(i ? 1u : 0u)
-                : "memory");
+            if (ts)   // A from TMEM (columns 256..): the TS form the NNMF kernels use
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm),
+                    "r"(tm + 256), "l"(db), "r"(idesc), "r"(i ? 1u : 0u)
+                    : "memory");
+            else
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
+                    "l"(da), "l"(db), "r"(idesc), "r"(i ? 1u : 0u)
+                    : "memory");
         }
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
@@ -342,7 +352,8 @@ tc_mma2_bench_kernel(int ncols, int iters, long long* out) {
 }  // namespace
 
 extern "C" int mmk_tc_mma2_bench(int ncols, int iters, long long* out, void* stream) {
-    if (ncols < 16 || ncols > 256 || (ncols % 16)) {
+    const int nc = ncols < 0 ? -ncols : ncols;   // negative: A from TMEM (TS form)
+    if (nc < 16 || nc > 256 || (nc % 16)) {
         mmk_host::set_error("mma2 bench: N must be a multiple of 16 in [16, 256]");
         return MMK_E_SHAPE;
     }

@@ -157,3 +157,32 @@ def test_row_shards_sum_to_the_whole():
     rel = lambda a, b: float((a - b).norm() / b.norm())  # noqa: E731
     assert torch.equal(vs, vw)            # the V step is row-local: bitwise
     assert rel(wo, ww) < 1e-6 and abs(float(f) - fw) / fw < 1e-9
+
+
+def test_pair_kernels_match_fp64():
+    """The experimental CTA-pair kernels (cta_group::2, MMK_TC_PAIR=1; read once
+    per process, hence the subprocess) run the same 30-iteration parity check
+    (odd tile counts exercise the empty half of the last pair)."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, paper_1003_3272_b200 as M
+rng = np.random.default_rng(3)
+x = rng.random((2176, 1160)).astype(np.float32).astype(np.float64)
+v0 = rng.random((2176, 64)).astype(np.float32).astype(np.float64)
+w0 = rng.random((64, 1160)).astype(np.float32).astype(np.float64)
+prob = M.NnmfProblem(x=x, rank=64)
+s32, t32 = M.nnmf_run(prob, M.MmConfig(max_iters=30, epsilon=1e-300, monotone_tol=1e-6),
+                      M.Backend(dtype="fp32"), state0=M.FactorPair(v0, w0))
+s64, t64 = M.nnmf_run(prob, M.MmConfig(max_iters=30, epsilon=1e-300), M.Backend(dtype="fp64"),
+                      state0=M.FactorPair(v0, w0))
+err = np.max(np.abs(t32.objective_values - t64.objective_values) / t64.objective_values)
+vw = np.linalg.norm(s32.v @ s32.w - s64.v @ s64.w) / np.linalg.norm(s64.v @ s64.w)
+print(err, vw)
+assert err < 1e-4 and vw < 1e-4
+"""
+    env = dict(os.environ, MMK_TC_PAIR="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
