@@ -383,7 +383,7 @@ int mmk_tc_mma_bench(int mode, int iters, long long *out, void *stream);
 int mmk_tc_mma2_bench(int ncols, int iters, long long *out, void *stream);
 
 /* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core
- * NNMF kernels, 5 x 256 uint64 per buffer (TMA issue, split start, split
+ * NNMF kernels, 6 x 256 uint64 per buffer (TMA issue, split start, split
  * done, MMA start, MMA committed); NULL disables (the default). */
 int mmk_tc_set_trace(unsigned long long *vstep, unsigned long long *wstep);
 

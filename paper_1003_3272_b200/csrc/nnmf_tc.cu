@@ -222,7 +222,7 @@ __device__ __forceinline__ void store_hilo(const float* x, uint32_t a_addr) {
 // trace (debug): CTA 0 records clock64 per X stage for the first kTrace stages:
 // [0] TMA issued, [1] split start (data landed), [2] split done, [3] MMA
 // start (operands ready), [4] MMAs issued + committed
-constexpr int kTrace = 256;
+constexpr int kTrace = 256;   // slots: 0-4 as above, 5 = operand chunk ready (MMA warp)
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int xit) {
     if (tr && (int)blockIdx.x == c_trace_cta && xit < kTrace) tr[what * kTrace + xit] = clock64();
 }
@@ -293,6 +293,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     const uint8_t* ob = oring + os * 2 * SOP;
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
                         const int ab = xit % NA;
+                        trace_at(tr, 5, xit);
                         wait(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
@@ -1184,7 +1185,7 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 
 }  // namespace mmk_tc
 
-// Debug hook: per-stage pipeline timestamps of CTA 0 (5 x 256 uint64 each, or
+// Debug hook: per-stage pipeline timestamps of CTA 0 (6 x 256 uint64 each, or
 // NULL to disable).  Not part of the solver ABI contract.
 extern "C" int mmk_tc_set_trace(unsigned long long* vstep, unsigned long long* wstep) {
     g_trace_v = vstep;

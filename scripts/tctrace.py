@@ -9,13 +9,13 @@ g = torch.Generator(device='cuda'); g.manual_seed(1)
 x = torch.rand(m, n, device='cuda', generator=g)
 v = torch.rand(m, r, device='cuda', generator=g); w = torch.rand(r, n, device='cuda', generator=g)
 sh = ShardedNnmf(x, v, w, r, M.Backend(dtype='fp32'))
-tv = torch.zeros(5 * 256, dtype=torch.int64, device='cuda'); tw = torch.zeros_like(tv)
+tv = torch.zeros(6 * 256, dtype=torch.int64, device='cuda'); tw = torch.zeros_like(tv)
 sh.iterate(1); torch.cuda.synchronize()
 _lib.load().mmk_tc_set_trace(_lib.ptr(tv), _lib.ptr(tw))
 sh.iterate(1); torch.cuda.synchronize()
 _lib.load().mmk_tc_set_trace(None, None)
 for name, t in (("vstep", tv), ("wstep", tw)):
-    a = t.cpu().numpy().reshape(5, 256).astype(np.int64)
+    a = t.cpu().numpy().reshape(6, 256).astype(np.int64)
     t0 = a[0, 0]
     a = a - t0
     print(name, "cols: tma_issue split_start split_done mma_start mma_done  (cycles rel. to first TMA issue)")
@@ -26,4 +26,6 @@ for name, t in (("vstep", tv), ("wstep", tw)):
           " split latency (start->done) mean %.0f" % (a[2, 20:250] - a[1, 20:250]).mean(),
           " TMA issue->split start mean %.0f" % (a[1, 20:250] - a[0, 20:250]).mean(),
           " split done->mma start %.0f" % (a[3, 20:250] - a[2, 20:250]).mean(),
-          " mma issue time %.0f" % (a[4, 20:250] - a[3, 20:250]).mean())
+          " mma issue time %.0f" % (a[4, 20:250] - a[3, 20:250]).mean(),
+          " operand ready->A ready (afull wait) %.0f" % (a[3, 20:250] - a[5, 20:250]).mean(),
+          " prev MMA issued->operand ready %.0f" % (a[5, 21:251] - a[4, 20:250]).mean())
