@@ -242,7 +242,11 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
     const uint32_t rank = PAIR ? tc::cluster_rank() : 0u;
     uint8_t* xring = base;
     uint8_t* oring = base + XST * SX;
-    auto wait = [](uint64_t* bar, uint32_t parity) {
+    // cluster-scope acquire only where another CTA's threads arrive (the
+    // leader's afull / dempty); commit arrivals (aempty, oempty, dfull) and
+    // TMA completions need no more than the CTA-scope wait
+    auto wait = [](uint64_t* bar, uint32_t parity) { tc::mbar_wait(bar, parity); };
+    auto wait_peer = [](uint64_t* bar, uint32_t parity) {
         if constexpr (PAIR)
             tc::mbar_wait_cluster(bar, parity);
         else
@@ -285,7 +289,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
             int xit = 0, oit = 0;
             for (int p = 0; p < npass; ++p) {
                 const Pass P = pass_of(p);
-                if (p > 0) wait(&B.dempty, (p - 1) & 1);
+                if (p > 0) wait_peer(&B.dempty, (p - 1) & 1);
                 tc::tc_fence_after();
                 for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
                     const int os = oit % OST;
@@ -294,7 +298,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
                         const int ab = xit % NA;
                         trace_at(tr, 5, xit);
-                        wait(&B.afull[ab], (xit / NA) & 1);
+                        wait_peer(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
                         issue_stage<PAIR>(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
