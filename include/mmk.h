@@ -382,6 +382,11 @@ int mmk_tc_mma_bench(int mode, int iters, long long *out, void *stream);
  * timeout flags into out[1], out[2]. */
 int mmk_tc_mma2_bench(int ncols, int iters, long long *out, void *stream);
 
+/* Tuning aid: cross-CTA hand-off latency in a CTA pair: out[0] cycles per
+ * remote-arrive round trip, out[1] per commit-multicast + remote-arrive round
+ * trip, out[2..3] timeout flags. */
+int mmk_tc_pingpong(int iters, long long *out, void *stream);
+
 /* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core
  * NNMF kernels, 6 x 256 uint64 per buffer (TMA issue, split start, split
  * done, MMA start, MMA committed); NULL disables (the default). */

@@ -35,6 +35,7 @@ _SIGS = {
     "mmk_prof_report": ([_c.c_char_p, _sz], _i32),
     "mmk_f64_to_f32": ([_vp, _vp, _i64, _vp], _i32),
     "mmk_tc_mma2_bench": ([_i32, _i32, _vp, _vp], _i32),
+    "mmk_tc_pingpong": ([_i32, _vp, _vp], _i32),
     "mmk_nnmf_gradient": ([_i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp,
                            _vp, _vp], _i32),
     "mmk_pet_gradient": ([_i32, _vp, _vp, _i64, _vp, _vp, _dbl, _vp, _vp, _vp], _i32),

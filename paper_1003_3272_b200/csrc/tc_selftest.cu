@@ -364,3 +364,75 @@ extern "C" int mmk_tc_mma2_bench(int ncols, int iters, long long* out, void* str
     MMK_CHECK_LAUNCH("tc_mma2_bench_kernel");
     return MMK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Cross-CTA hand-off latency in a CTA pair: `iters` round trips in which CTA 0
+// arrives (release.cluster) on CTA 1's mbarrier and waits on its own, and
+// CTA 1 answers in kind; out[0] = CTA 0 cycles per round trip.  A second
+// phase measures a commit-multicast round trip: CTA 0 issues an empty
+// tcgen05.commit.cta_group::2 multicast to both barriers and CTA 1 answers
+// with a remote arrive; out[1] = cycles per round trip.
+namespace {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32)
+tc_pingpong_kernel(int iters, long long* out) {
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const uint32_t rank = tc::cluster_rank();
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_barrier_init();
+    }
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        tc::smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    __syncwarp();
+    tc::cluster_sync();
+    if (threadIdx.x == 0) {
+        const uint32_t peer = tc::map_to_rank(&bar, rank ^ 1u);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            if (rank == 0) {
+                tc::mbar_arrive_cluster(peer);
+                if (!tc::mbar_wait_bounded(&bar, i & 1)) { out[2] = 1; break; }
+            } else {
+                if (!tc::mbar_wait_bounded(&bar, i & 1)) { out[3] = 1; break; }
+                tc::mbar_arrive_cluster(peer);
+            }
+        }
+        if (rank == 0) out[0] = (clock64() - t0) / iters;
+    }
+    __syncwarp();
+    tc::cluster_sync();
+    // phase 2: commit multicast (leader) -> both barriers; peer answers
+    if (threadIdx.x == 0) {
+        const uint32_t leader = tc::map_to_rank(&bar, 0);
+        uint32_t ph = (uint32_t)iters;   // phases completed in phase 1 (both barriers)
+        const int rounds = iters / 2 > 0 ? iters / 2 : 1;
+        long long t0 = clock64();
+        for (int r = 0; r < rounds; ++r) {
+            if (rank == 0) {
+                tc::mma_commit_pair(&bar);   // arrives on both CTAs' barriers
+                if (!tc::mbar_wait_bounded(&bar, ph & 1)) { out[2] = 2; break; }
+                ++ph;
+                if (!tc::mbar_wait_bounded(&bar, ph & 1)) { out[2] = 3; break; }
+                ++ph;
+            } else {
+                if (!tc::mbar_wait_bounded(&bar, ph & 1)) { out[3] = 2; break; }
+                ++ph;
+                tc::mbar_arrive_cluster(leader);
+            }
+        }
+        if (rank == 0) out[1] = (clock64() - t0) / rounds;
+    }
+    __syncwarp();
+    tc::cluster_sync();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(tmem_base));
+}
+}  // namespace
+
+extern "C" int mmk_tc_pingpong(int iters, long long* out, void* stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    tc_pingpong_kernel<<<2, 32, 0, st>>>(iters, out);
+    MMK_CHECK_LAUNCH("tc_pingpong_kernel");
+    return MMK_OK;
+}
