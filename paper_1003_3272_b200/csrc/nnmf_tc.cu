@@ -38,6 +38,17 @@
 //
 // HBM roofline: each kernel streams X once (m n 4 bytes) -> two passes per
 // iteration; tensor work 3 x 2mnr per kernel.
+//
+// Pre-split X (PS, the default while the copy fits, see presplit_on): X is
+// constant over a run, so its fp16 hi / lo pair -- exactly what the split
+// warps compute -- is made ONCE (presplit_kernel, row-major for the V step and
+// transposed for the W step) and the kernels stream [X_hi | X_lo] tiles (the
+// same 4 bytes per element) straight from TMA into SS MMAs: no split warps,
+// no TMEM A buffers, the MMA commit releases the X slot.  Same products from
+// the same values (bitwise-equal traces, tests/test_nnmf_tc_gpu.py); measured
+// 1.39 / 1.29 ms per half step at C4 against 1.51 / 1.45 for the split-warp
+// kernels, i.e. HBM-bound at the power-capped clocks where the split-warp
+// pipeline is MMA-issue bound.
 #include <cuda_fp16.h>
 
 #include "mmk_common.cuh"
@@ -104,12 +115,13 @@ struct Bars {
     uint64_t dfull, dempty;
 };
 
-// pair: the leader's afull / dempty also count one arrival of the peer CTA
-__device__ __forceinline__ void init_bars(Bars& B, bool pair = false) {
+// pair: the leader's afull / dempty also count one arrival of the peer CTA;
+// pre-split X: the X slots are released by an MMA commit, not the split warps
+__device__ __forceinline__ void init_bars(Bars& B, bool pair, bool presplit) {
     const uint32_t two = pair ? 2 : 1;
     for (int s = 0; s < XST; ++s) {
         tc::mbar_init(&B.xfull[s], 1);
-        tc::mbar_init(&B.xempty[s], 128);   // released by the split warps
+        tc::mbar_init(&B.xempty[s], presplit ? 1 : 128);   // split warps / MMA commit
     }
     for (int s = 0; s < OST; ++s) {
         tc::mbar_init(&B.ofull[s], 1);
@@ -139,13 +151,39 @@ __device__ __forceinline__ void init_bars(Bars& B, bool pair = false) {
 // product the single-CTA path leaves out (it only makes the sum more exact).
 // A pair MMA runs at the full tensor rate (64 cycles at N = 128, measured)
 // where a single-CTA M = 128 one costs ~175 cycles whatever N is.
-template <bool PAIR>
-__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* bhl,
-                                            bool first) {
+//
+// PS (pre-split X): A comes from shared memory instead -- the X stage holds
+// [X_hi | X_lo] as two 128-row x 64-K fp16 tiles (128B swizzle) loaded by TMA
+// from the pre-split copy of X, so no split warps sit between the load and
+// the MMA (SS MMAs, same products).
+template <bool PAIR, bool PS>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* xs,
+                                            const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const int dbg = c_dbg;
     if (dbg & 4) return;
-    if constexpr (PAIR) {
+    if constexpr (PS) {
+        const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
+        const uint64_t al = tc::sdesc_sw128(xs + SX / 2, 16, 1024);
+        if constexpr (PAIR) {
+            constexpr uint32_t id = idesc_f16(2 * BM, ACC);
+#pragma unroll
+            for (int ks = 0; ks < BK / 16; ++ks) {
+                const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                tc::mma_f16ss_pair(d, ah + ks * 2, db0 + ks * 2, id, acc);
+                if (!(dbg & 1)) tc::mma_f16ss_pair(d, al + ks * 2, db0 + ks * 2, id, 1);
+            }
+        } else {
+            constexpr uint32_t id_hi = idesc_f16(BM, ACC);
+            constexpr uint32_t id_lo = idesc_f16(BM, R);
+#pragma unroll
+            for (int ks = 0; ks < BK / 16; ++ks) {
+                const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                tc::mma_f16ss(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
+                if (!(dbg & 1)) tc::mma_f16ss(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
+            }
+        }
+    } else if constexpr (PAIR) {
         constexpr uint32_t id = idesc_f16(2 * BM, ACC);
 #pragma unroll
         for (int ks = 0; ks < BK / 16; ++ks) {
@@ -233,7 +271,10 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int x
 // leader's MMA warp issues (M = 256) and its commits arrive on the barriers of
 // both CTAs (multicast); the peer's split and epilogue warps arrive on the
 // leader's afull / dempty.
-template <bool MN, bool PAIR, class PassOf, class LoadX, class LoadOp, class Epi>
+// PS: pre-split X (see issue_stage): the TMA warp loads [X_hi | X_lo] stages
+// that the MMA warp consumes directly (pair: both CTAs' loads are counted on
+// the leader's xfull) and the MMA commit releases the slot; no split warps.
+template <bool MN, bool PAIR, bool PS, class PassOf, class LoadX, class LoadOp, class Epi>
 __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tmem, int npass,
                                              float xscale, const PassOf& pass_of,
                                              const LoadX& load_x, const LoadOp& load_op,
@@ -277,7 +318,10 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
                         const int xs = xit % XST;
                         tc::mbar_wait(&B.xempty[xs], ((xit / XST) & 1) ^ 1);
-                        tc::mbar_expect_tx(&B.xfull[xs], SX);
+                        if (!(PS && PAIR))
+                            tc::mbar_expect_tx(&B.xfull[xs], SX);
+                        else if (rank == 0)
+                            tc::mbar_expect_tx(&B.xfull[xs], 2 * SX);
                         load_x(p, kb, j, xring + xs * SX, &B.xfull[xs]);
                         trace_at(tr, 0, xit);
                     }
@@ -296,13 +340,18 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     wait(&B.ofull[os], (oit / OST) & 1);
                     const uint8_t* ob = oring + os * 2 * SOP;
                     for (int j = 0; j < P.nacc; ++j, ++xit) {
-                        const int ab = xit % NA;
+                        const int ab = xit % NA, xs = xit % XST;
                         trace_at(tr, 5, xit);
-                        wait_peer(&B.afull[ab], (xit / NA) & 1);
+                        if constexpr (PS)
+                            wait(&B.xfull[xs], (xit / XST) & 1);
+                        else
+                            wait_peer(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
-                        issue_stage<PAIR>(tmem + j * ACC, tmem + TM_A + ab * 64, ob, kb == 0);
-                        commit(&B.aempty[ab]);   // A buffer ab free once these finish
+                        issue_stage<PAIR, PS>(tmem + j * ACC, tmem + TM_A + ab * 64,
+                                              xring + xs * SX, ob, kb == 0);
+                        // X slot xs (pre-split) / A buffer ab free once these finish
+                        commit(PS ? &B.xempty[xs] : &B.aempty[ab]);
                         trace_at(tr, 4, xit);
                     }
                     commit(&B.oempty[os]);
@@ -311,6 +360,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
             }
         }
     } else if (warp < 2 + NCONV) {
+        if constexpr (PS) return;   // pre-split X: nothing to split
         const int g = (warp - 2) >> 2, quarter = warp & 3;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         int xit = 0;
@@ -374,9 +424,11 @@ struct Scales {
 // ---------------------------------------------------------------------------
 // PAIR: launched as clusters of 2 (CTA pairs); pair q takes the 256-row
 // units q, q + G/2, ... and CTA rank r of the pair their 128-row half r.
-template <bool PAIR>
+// PS: mX / mX2 are the fp16 hi / lo maps of the pre-split X (m x n).
+template <bool PAIR, bool PS>
 __global__ void __launch_bounds__(kThreads, 1)
-nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mWh,
+nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
+              const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
               const float* __restrict__ DEN, float* __restrict__ Vout, Scales* sc, int m, int n,
               double* __restrict__ part, unsigned long long* tr) {
@@ -395,8 +447,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
     const int npass = (mine + TMAX - 1) / TMAX;
     if (threadIdx.x == 0) {
-        init_bars(B, PAIR);
+        init_bars(B, PAIR, PS);
         tc::tma_prefetch(&mX);
+        if (PS) tc::tma_prefetch(&mX2);
         tc::tma_prefetch(&mWh);
         tc::tma_prefetch(&mWl);
     }
@@ -432,8 +485,17 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         }
     };
     auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
-        tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
-        tc::tma_load_2d(dst + BM * 128, &mX, bar, kb * BK + 32, tile_of(p, j) * BM);
+        if constexpr (PS && PAIR) {
+            const uint32_t lb = tc::map_to_rank(bar, 0);
+            tc::tma_load_2d_pair(dst, &mX, lb, kb * BK, tile_of(p, j) * BM);
+            tc::tma_load_2d_pair(dst + SX / 2, &mX2, lb, kb * BK, tile_of(p, j) * BM);
+        } else if constexpr (PS) {
+            tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
+            tc::tma_load_2d(dst + SX / 2, &mX2, bar, kb * BK, tile_of(p, j) * BM);
+        } else {
+            tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
+            tc::tma_load_2d(dst + BM * 128, &mX, bar, kb * BK + 32, tile_of(p, j) * BM);
+        }
     };
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool) {
         const long long row = (long long)tile_of(p, j) * BM + quarter * 32 + ln;
@@ -465,7 +527,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     };
-    run_pipeline<false, PAIR>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
+    run_pipeline<false, PAIR, PS>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
                               tr);
     // per-CTA partials <V, Q>, <V, V G_W> and max(V') (epilogue warps)
     __shared__ double gred[kThreads / 32];
@@ -509,9 +571,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
 // thread `lane` of warp quarter q owns column 32 q + lane of the block.
 // PAIR: clusters of 2; an item covers 2 CB column blocks, CTA rank r takes
 // blocks 2 j + r of it.
-template <bool PAIR>
+// PS: mX / mX2 are the fp16 hi / lo maps of the pre-split X^T (n x m).
+template <bool PAIR, bool PS>
 __global__ void __launch_bounds__(kThreads, 1)
-nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mVh,
+nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
+              const __grid_constant__ CUtensorMap mVh,
               const __grid_constant__ CUtensorMap mVl, const Scales* sc, int m, int n,
               int splits, int rows_per_split, float* __restrict__ wpart, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
@@ -528,8 +592,9 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const int nitems = ncs * splits;
     const int npass = nitems > me ? (nitems - 1 - me) / G + 1 : 0;
     if (threadIdx.x == 0) {
-        init_bars(B, PAIR);
+        init_bars(B, PAIR, PS);
         tc::tma_prefetch(&mX);
+        if (PS) tc::tma_prefetch(&mX2);
         tc::tma_prefetch(&mVh);
         tc::tma_prefetch(&mVl);
     }
@@ -571,9 +636,18 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         const int item = item_of(p);
         const int row = (item / ncs) * rows_per_split + kb * BK;
         const int col0 = block_of(item, j) * BM;
+        if constexpr (PS && PAIR) {
+            const uint32_t lb = tc::map_to_rank(bar, 0);
+            tc::tma_load_2d_pair(dst, &mX, lb, row, col0);
+            tc::tma_load_2d_pair(dst + SX / 2, &mX2, lb, row, col0);
+        } else if constexpr (PS) {
+            tc::tma_load_2d(dst, &mX, bar, row, col0);
+            tc::tma_load_2d(dst + SX / 2, &mX2, bar, row, col0);
+        } else {
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-            tc::tma_load_2d(dst + jj * (BK * 128), &mX, bar, col0 + 32 * jj, row);
+            for (int jj = 0; jj < 4; ++jj)
+                tc::tma_load_2d(dst + jj * (BK * 128), &mX, bar, col0 + 32 * jj, row);
+        }
     };
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool any) {
         const int item = item_of(p), s = item / ncs;
@@ -599,7 +673,7 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     };
-    run_pipeline<true, PAIR>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
+    run_pipeline<true, PAIR, PS>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
                              tr);
     tc::tc_fence_before();
     __syncthreads();
@@ -618,6 +692,7 @@ struct XXCache {
     double xx;
     unsigned long long key[4];
     int ex, pad_;
+    unsigned long long pkey[4];   // X the pre-split copy was made from (presplit_kernel)
 };
 
 __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
@@ -666,6 +741,67 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
             __threadfence();
             cache->key[0] = k0;
         }
+    }
+}
+
+// Pre-split copy of X for the PS kernels: X_hi = rn(x 2^ex), X_lo = rn(x 2^ex
+// - X_hi) in fp16 -- the values the split warps would compute every pass --
+// both row-major (m x n, V step) and transposed (n x m, W step), i.e. 8 bytes
+// per element of X in HBM, 4 of them read per half step as before.  Made once
+// per X (keyed like the sum-of-squares cache; runs after sumsq_kernel, whose
+// exponent it uses); later launches exit at the key check.
+constexpr int PS_TILE = 64;
+__global__ void __launch_bounds__(256)
+presplit_kernel(const float* __restrict__ X, long long ldx, int m, int n, XXCache* cache,
+                __half* __restrict__ Xh, __half* __restrict__ Xl, __half* __restrict__ XTh,
+                __half* __restrict__ XTl, unsigned int* counter) {
+    const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
+    if (cache->pkey[0] == k0 && cache->pkey[1] == (unsigned long long)m &&
+        cache->pkey[2] == (unsigned long long)n && cache->pkey[3] == (unsigned long long)ldx)
+        return;   // uniform across the grid
+    __shared__ float t[PS_TILE][PS_TILE + 1];
+    const float sc = exp2f((float)cache->ex);
+    const int tr = (m + PS_TILE - 1) / PS_TILE, tcn = (n + PS_TILE - 1) / PS_TILE;
+    const long long ntiles = (long long)tr * tcn;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int r0 = (int)(tile / tcn) * PS_TILE, c0 = (int)(tile % tcn) * PS_TILE;
+        // row-major copy: 64 rows x 32 column pairs (m, n are multiples of 8)
+        for (int i = threadIdx.x; i < PS_TILE * PS_TILE / 2; i += blockDim.x) {
+            const int r = i >> 5, cp = i & 31, row = r0 + r, col = c0 + 2 * cp;
+            float a = 0.f, b = 0.f;
+            if (row < m && col < n) {
+                const float2 v = *reinterpret_cast<const float2*>(X + (long long)row * ldx + col);
+                a = v.x * sc;
+                b = v.y * sc;
+                uint32_t h, l;
+                split_pair(a, b, h, l);
+                const long long o = ((long long)row * n + col) / 2;
+                reinterpret_cast<uint32_t*>(Xh)[o] = h;
+                reinterpret_cast<uint32_t*>(Xl)[o] = l;
+            }
+            t[r][2 * cp] = a;
+            t[r][2 * cp + 1] = b;
+        }
+        __syncthreads();
+        // transposed copy: 64 columns x 32 row pairs
+        for (int i = threadIdx.x; i < PS_TILE * PS_TILE / 2; i += blockDim.x) {
+            const int c = i >> 5, rp = i & 31, col = c0 + c, row = r0 + 2 * rp;
+            if (col < n && row < m) {
+                uint32_t h, l;
+                split_pair(t[2 * rp][c], t[2 * rp + 1][c], h, l);
+                const long long o = ((long long)col * m + row) / 2;
+                reinterpret_cast<uint32_t*>(XTh)[o] = h;
+                reinterpret_cast<uint32_t*>(XTl)[o] = l;
+            }
+        }
+        __syncthreads();
+    }
+    if (arrive_last(counter, gridDim.x) && threadIdx.x == 0) {
+        cache->pkey[1] = (unsigned long long)m;
+        cache->pkey[2] = (unsigned long long)n;
+        cache->pkey[3] = (unsigned long long)ldx;
+        __threadfence();
+        cache->pkey[0] = k0;
     }
 }
 
@@ -968,6 +1104,19 @@ bool pair_on() {
     return on;
 }
 
+// pre-split X (PS kernels): on unless MMK_TC_PRESPLIT=0, or the copy (8 bytes
+// per element of X: fp16 hi + lo, row-major and transposed) would pass 48 GiB;
+// MMK_TC_PRESPLIT=1 forces it.  A function of (m, n) only, so ws_bytes and
+// iter_a agree.
+bool presplit_on(long long m, long long n) {
+    static const int mode = [] {
+        const char* e = getenv("MMK_TC_PRESPLIT");
+        return e ? (e[0] == '1' ? 1 : (e[0] == '0' ? 0 : -1)) : -1;
+    }();
+    if (mode >= 0) return mode == 1;
+    return 8.0 * (double)m * (double)n <= 48.0 * (1ull << 30);
+}
+
 TcPlan tc_plan(long long m, long long n, bool pair) {
     TcPlan P;
     const int slots = pair ? kNumSMs / 2 : kNumSMs;
@@ -1022,6 +1171,7 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
 
 struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl;
+    __half *Xh, *Xl, *XTh, *XTl;   // pre-split X (presplit_on(m, n) only)
     float *wpart, *DEN, *mpart;
     double *GVn, *part, *sqpart, *gpart;
     XXCache* xx;
@@ -1052,7 +1202,13 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) sumsq, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
+    const size_t xe = presplit_on(m, n) ? (size_t)m * n : 0;
+    size_t oXh = take(2 * xe), oXl = take(2 * xe), oXTh = take(2 * xe), oXTl = take(2 * xe);
     if (base && L) {
+        L->Xh = (__half*)(c_base(base) + oXh);
+        L->Xl = (__half*)(c_base(base) + oXl);
+        L->XTh = (__half*)(c_base(base) + oXTh);
+        L->XTl = (__half*)(c_base(base) + oXTl);
         char* c = c_base(base);
         L->sqpart = (double*)(c + oS);
         L->mpart = (float*)(c + oM);
@@ -1099,9 +1255,9 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
            cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
-    const bool pair = pair_on();
+    const bool pair = pair_on(), ps = presplit_on(m, n);
     const TcPlan P = tc_plan(m, n, pair);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc<false>))) {
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc<false, false>))) {
         const char* dbg = getenv("MMK_TC_DBG");
         if (dbg) {
             const int v = atoi(dbg);
@@ -1111,10 +1267,17 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
             const int v = atoi(tc);
             cudaMemcpyToSymbol(c_trace_cta, &v, sizeof(int));
         }
-        cudaFuncSetAttribute(nnmf_vstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(nnmf_wstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(nnmf_vstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(nnmf_wstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        auto big = [](auto f) {
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        };
+        big(nnmf_vstep_tc<false, false>);
+        big(nnmf_wstep_tc<false, false>);
+        big(nnmf_vstep_tc<true, false>);
+        big(nnmf_wstep_tc<true, false>);
+        big(nnmf_vstep_tc<false, true>);
+        big(nnmf_wstep_tc<false, true>);
+        big(nnmf_vstep_tc<true, true>);
+        big(nnmf_wstep_tc<true, true>);
         cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
     }
     // cluster launch of the pair kernels (2 CTAs = one TPC)
@@ -1133,18 +1296,32 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
         cfg.numAttrs = 1;
         (void)cudaLaunchKernelEx(&cfg, kern, args...);
     };
-    CUtensorMap mX, mWh, mWl, mXt, mVh, mVl;
+    CUtensorMap mX, mX2, mWh, mWl, mXt, mXt2, mVh, mVl;
     int rc;
-    if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
+    if (ps) {   // fp16 hi / lo maps of the pre-split X and X^T (made below)
+        if ((rc = mmk_host::make_map_f16(&mX, L.Xh, m, n, n, BM))) return rc;
+        if ((rc = mmk_host::make_map_f16(&mX2, L.Xl, m, n, n, BM))) return rc;
+        if ((rc = mmk_host::make_map_f16(&mXt, L.XTh, n, m, m, BM))) return rc;
+        if ((rc = mmk_host::make_map_f16(&mXt2, L.XTl, n, m, m, BM))) return rc;
+    } else {
+        if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
+        if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK))) return rc;
+        mX2 = mX;
+        mXt2 = mXt;
+    }
     if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK))) return rc;
     if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, R, m, m, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, R, m, m, R))) return rc;
     const long long rn = (long long)R * n;
     MMK_LAUNCH("nnmf_sumsq_cached", st,
                (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
                                                            L.counter, L.sc)));
+    if (ps)
+        MMK_LAUNCH("nnmf_presplit_cached", st,
+                   (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
+                                                                 L.Xl, L.XTh, L.XTl,
+                                                                 L.counter + 2)));
     MMK_LAUNCH("nnmf_wmax", st,
                (wmax_kernel<<<kNumSMs, 1024, 0, st>>>(W, rn, L.mpart + 4 * kNumSMs,
                                                      L.counter + 1, L.sc)));
@@ -1155,14 +1332,18 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     MMK_LAUNCH("nnmf_vgw",
                st, (vgw_kernel<<<ceil_div(m, 64 * VGW_CHUNKS), 256, VGW_SMEM, st>>>(V, GW, L.DEN,
                                                                                 m)));
-    if (pair)
-        MMK_LAUNCH("nnmf_vstep_tc", st,
-                   launch_pair(nnmf_vstep_tc<true>, P.vgrid, mX, mWh, mWl, V, (const float*)L.DEN,
-                               V_out, L.sc, (int)m, (int)n, L.part, g_trace_v));
-    else
-        MMK_LAUNCH("nnmf_vstep_tc", st,
-                   (nnmf_vstep_tc<false><<<P.vgrid, kThreads, SMEM, st>>>(
-                       mX, mWh, mWl, V, L.DEN, V_out, L.sc, (int)m, (int)n, L.part, g_trace_v)));
+    {
+        auto vk = pair ? (ps ? nnmf_vstep_tc<true, true> : nnmf_vstep_tc<true, false>)
+                       : (ps ? nnmf_vstep_tc<false, true> : nnmf_vstep_tc<false, false>);
+        if (pair)
+            MMK_LAUNCH("nnmf_vstep_tc", st,
+                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const float*)L.DEN, V_out,
+                                   L.sc, (int)m, (int)n, L.part, g_trace_v));
+        else
+            MMK_LAUNCH("nnmf_vstep_tc", st,
+                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, L.DEN, V_out, L.sc,
+                                                            (int)m, (int)n, L.part, g_trace_v)));
+    }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx,
@@ -1170,15 +1351,19 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
                (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
-    if (pair)
-        MMK_LAUNCH("nnmf_wstep_tc", st,
-                   launch_pair(nnmf_wstep_tc<true>, P.wgrid, mXt, mVh, mVl, (const Scales*)L.sc,
-                               (int)m, (int)n, P.splits, P.rows_per_split, L.wpart, g_trace_w));
-    else
-        MMK_LAUNCH("nnmf_wstep_tc", st,
-                   (nnmf_wstep_tc<false><<<P.wgrid, kThreads, SMEM, st>>>(
-                       mXt, mVh, mVl, L.sc, (int)m, (int)n, P.splits, P.rows_per_split, L.wpart,
-                       g_trace_w)));
+    {
+        auto wk = pair ? (ps ? nnmf_wstep_tc<true, true> : nnmf_wstep_tc<true, false>)
+                       : (ps ? nnmf_wstep_tc<false, true> : nnmf_wstep_tc<false, false>);
+        if (pair)
+            MMK_LAUNCH("nnmf_wstep_tc", st,
+                       launch_pair(wk, P.wgrid, mXt, mXt2, mVh, mVl, (const Scales*)L.sc, (int)m,
+                                   (int)n, P.splits, P.rows_per_split, L.wpart, g_trace_w));
+        else
+            MMK_LAUNCH("nnmf_wstep_tc", st,
+                       (wk<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mXt2, mVh, mVl, L.sc, (int)m,
+                                                            (int)n, P.splits, P.rows_per_split,
+                                                            L.wpart, g_trace_w)));
+    }
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
                (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,

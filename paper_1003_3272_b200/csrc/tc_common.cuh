@@ -238,6 +238,16 @@ __device__ __forceinline__ void mma_f16ts_pair(uint32_t d_tmem, uint32_t a_tmem,
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// SS form of the pair MMA: A's 256 rows are 128 in each CTA's smem (same offset)
+__device__ __forceinline__ void mma_f16ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // arrive on the mbarrier at the same offset in both CTAs once the pair's MMAs finish
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
     asm volatile(

@@ -159,14 +159,8 @@ def test_row_shards_sum_to_the_whole():
     assert rel(wo, ww) < 1e-6 and abs(float(f) - fw) / fw < 1e-9
 
 
-def test_pair_kernels_match_fp64():
-    """The experimental CTA-pair kernels (cta_group::2, MMK_TC_PAIR=1; read once
-    per process, hence the subprocess) run the same 30-iteration parity check
-    (odd tile counts exercise the empty half of the last pair)."""
-    import subprocess
-    import sys
-    code = r"""
-import numpy as np, paper_1003_3272_b200 as M
+_VARIANT_CODE = r"""
+import json, numpy as np, paper_1003_3272_b200 as M
 rng = np.random.default_rng(3)
 x = rng.random((2176, 1160)).astype(np.float32).astype(np.float64)
 v0 = rng.random((2176, 64)).astype(np.float32).astype(np.float64)
@@ -178,11 +172,35 @@ s64, t64 = M.nnmf_run(prob, M.MmConfig(max_iters=30, epsilon=1e-300), M.Backend(
                       state0=M.FactorPair(v0, w0))
 err = np.max(np.abs(t32.objective_values - t64.objective_values) / t64.objective_values)
 vw = np.linalg.norm(s32.v @ s32.w - s64.v @ s64.w) / np.linalg.norm(s64.v @ s64.w)
-print(err, vw)
-assert err < 1e-4 and vw < 1e-4
+assert err < 1e-4 and vw < 1e-4, (err, vw)
+print(json.dumps([float(v) for v in t32.objective_values]))
 """
-    env = dict(os.environ, MMK_TC_PAIR="1")
+
+
+def _variant_trace(**env):
+    import json
+    import subprocess
+    import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
-                       text=True, timeout=600)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_CODE], env=dict(os.environ, **env),
+                       cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+    return np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+
+
+@pytest.mark.parametrize("env", [{"MMK_TC_PAIR": "1", "MMK_TC_PRESPLIT": "0"},
+                                 {"MMK_TC_PRESPLIT": "0"},
+                                 {"MMK_TC_PAIR": "1", "MMK_TC_PRESPLIT": "1"}],
+                         ids=["pair-split-warps", "split-warps", "pair-presplit"])
+def test_kernel_variants_match_fp64(env):
+    """The kernel variants (read once per process, hence the subprocess) run the
+    same 30-iteration parity check against fp64 (odd tile counts exercise the
+    empty half of the last pair): MMK_TC_PAIR=1 -- CTA pairs (cta_group::2);
+    MMK_TC_PRESPLIT=0 -- the split-warp kernels instead of the default
+    pre-split X (fp16 hi / lo made once, SS MMAs from TMA tiles).  The
+    single-CTA kernels of both kinds form the same products from the same fp16
+    values: their traces must be equal."""
+    t = _variant_trace(**env)
+    if env == {"MMK_TC_PRESPLIT": "0"}:
+        base = _variant_trace(MMK_TC_PRESPLIT="1", MMK_TC_PAIR="0")
+        assert np.array_equal(t, base), np.max(np.abs(t - base) / base)
