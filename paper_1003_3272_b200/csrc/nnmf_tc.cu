@@ -76,6 +76,7 @@ constexpr int TMAX = 2;                     // accumulators per pass (V step: ro
 constexpr int CB = 2;                       // W step: 128-column blocks per item
 constexpr int TM_COLS = 512;
 constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
+static_assert(2 * TMAX * ACC <= TM_COLS, "two accumulator sets (pre-split X) must fit in TMEM");
 
 // experiment switches (MMK_TC_DBG, timing studies only; results are wrong
 // when set): 1 skip the lo MMAs, 2 skip the split, 4 skip all MMAs
@@ -112,7 +113,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
 
 struct Bars {
     uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST], afull[NA], aempty[NA];
-    uint64_t dfull, dempty;
+    uint64_t dfull[2], dempty[2];   // accumulator sets (pre-split X: two, else one)
 };
 
 // pair: the leader's afull / dempty also count one arrival of the peer CTA;
@@ -131,8 +132,10 @@ __device__ __forceinline__ void init_bars(Bars& B, bool pair, bool presplit) {
         tc::mbar_init(&B.afull[b], 128 + (two - 1));   // pair: + one arrival from the peer
         tc::mbar_init(&B.aempty[b], 1);
     }
-    tc::mbar_init(&B.dfull, 1);
-    tc::mbar_init(&B.dempty, 128 + (two - 1));
+    for (int b = 0; b < 2; ++b) {
+        tc::mbar_init(&B.dfull[b], 1);
+        tc::mbar_init(&B.dempty[b], 128 + (two - 1));
+    }
     tc::fence_barrier_init();
 }
 
@@ -281,6 +284,9 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                                              const Epi& epilogue, unsigned long long* tr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? tc::cluster_rank() : 0u;
+    // accumulator sets: with pre-split X the TMEM A buffers are free, so pass
+    // p + 1 accumulates into the other set while the epilogue drains pass p
+    constexpr int NBUF = PS ? 2 : 1;
     uint8_t* xring = base;
     uint8_t* oring = base + XST * SX;
     // cluster-scope acquire only where another CTA's threads arrive (the
@@ -333,7 +339,8 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
             int xit = 0, oit = 0;
             for (int p = 0; p < npass; ++p) {
                 const Pass P = pass_of(p);
-                if (p > 0) wait_peer(&B.dempty, (p - 1) & 1);
+                const int b = p % NBUF;
+                if (p >= NBUF) wait_peer(&B.dempty[b], ((p / NBUF) - 1) & 1);
                 tc::tc_fence_after();
                 for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
                     const int os = oit % OST;
@@ -348,7 +355,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                             wait_peer(&B.afull[ab], (xit / NA) & 1);
                         trace_at(tr, 3, xit);
                         tc::tc_fence_after();
-                        issue_stage<PAIR, PS>(tmem + j * ACC, tmem + TM_A + ab * 64,
+                        issue_stage<PAIR, PS>(tmem + (b * TMAX + j) * ACC, tmem + TM_A + ab * 64,
                                               xring + xs * SX, ob, kb == 0);
                         // X slot xs (pre-split) / A buffer ab free once these finish
                         commit(PS ? &B.xempty[xs] : &B.aempty[ab]);
@@ -356,7 +363,7 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
                     }
                     commit(&B.oempty[os]);
                 }
-                commit(&B.dfull);
+                commit(&B.dfull[b]);
             }
         }
     } else if (warp < 2 + NCONV) {
@@ -398,17 +405,19 @@ __device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tm
         const int quarter = warp & 3;
         for (int p = 0; p < npass; ++p) {
             const Pass P = pass_of(p);
-            wait(&B.dfull, p & 1);
+            const int b = p % NBUF;
+            wait(&B.dfull[b], (p / NBUF) & 1);
             tc::tc_fence_after();
             for (int j = 0; j < P.nacc; ++j)
                 epilogue(p, j, quarter, lane,
-                         tmem + j * ACC + ((uint32_t)(quarter * 32) << 16), P.nkb > 0);
+                         tmem + (b * TMAX + j) * ACC + ((uint32_t)(quarter * 32) << 16),
+                         P.nkb > 0);
             tc::tc_fence_before();
             if (!PAIR || rank == 0) {
-                tc::mbar_arrive(&B.dempty);
+                tc::mbar_arrive(&B.dempty[b]);
             } else {
                 asm volatile("bar.sync 3, 128;" ::: "memory");
-                if (quarter == 0 && lane == 0) arrive_leader(&B.dempty);
+                if (quarter == 0 && lane == 0) arrive_leader(&B.dempty[b]);
             }
         }
     }
