@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+# tuning experiments only (e.g. MMK_NVCC_EXTRA="-DMMK_TC_XST=5"); empty by default
+FLAGS += os.environ.get("MMK_NVCC_EXTRA", "").split()
 
 
 def _sources():

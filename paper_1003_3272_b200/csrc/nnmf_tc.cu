@@ -67,9 +67,16 @@ constexpr int NGROUP = NCONV / 4;
 constexpr int kThreads = 32 * (2 + NCONV + 4);   // TMA, MMA, split x8, epilogue x4
 constexpr uint32_t SX = BM * BK * 4;        // 32 KB  fp32 X stage
 constexpr uint32_t SOP = R * BK * 2;        //  8 KB  fp16 operand chunk hi; same again for lo
-constexpr int XST = 4;                      // X ring (128 KB in flight per SM)
-constexpr int OST = 4;                      // operand ring
-constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + 1024;
+#ifndef MMK_TC_XST
+#define MMK_TC_XST 4
+#endif
+#ifndef MMK_TC_OST
+#define MMK_TC_OST 4
+#endif
+constexpr int XST = MMK_TC_XST;             // X ring (128 KB in flight per SM)
+constexpr int OST = MMK_TC_OST;             // operand ring
+constexpr uint32_t SGW = R * R * 4;         // 16 KB  G_W (fp32) for the V-step epilogue
+constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + SGW + 1024;
 constexpr int NA = 4;                       // TMEM A-operand buffers [X_hi | X_lo] (64 cols)
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
 constexpr int TMAX = 2;                     // accumulators per pass (V step: row tiles)
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
-              const float* __restrict__ DEN, float* __restrict__ Vout, Scales* sc, int m, int n,
+              const double* __restrict__ GW, float* __restrict__ Vout, Scales* sc, int m, int n,
               double* __restrict__ part, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
@@ -455,6 +462,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const int units = PAIR ? (ntiles + 1) / 2 : ntiles;
     const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
     const int npass = (mine + TMAX - 1) / TMAX;
+    // G_W rounded to fp32 for the epilogue's denominator rows (V G_W)_i
+    float* gws = reinterpret_cast<float*>(base + XST * SX + OST * 2 * SOP);
+    for (int i = threadIdx.x; i < R * R; i += kThreads) gws[i] = (float)GW[i];
     if (threadIdx.x == 0) {
         init_bars(B, PAIR, PS);
         tc::tma_prefetch(&mX);
@@ -515,24 +525,52 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::tmem_ld32(ta + R + h * 32, q2);
             if (row >= m) continue;
             const float4* v4 = reinterpret_cast<const float4*>(V + row * R + h * 32);
-            const float4* d4 = reinterpret_cast<const float4*>(DEN + row * R + h * 32);
+            const float4* vr = reinterpret_cast<const float4*>(V + row * R);
             float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
 #pragma unroll
-            for (int k4 = 0; k4 < 8; ++k4) {
-                const float4 vv = v4[k4], dd = d4[k4];
-                const float va[4] = {vv.x, vv.y, vv.z, vv.w};
-                const float da[4] = {dd.x, dd.y, dd.z, dd.w};
-                float nv[4];
+            for (int hh = 0; hh < 2; ++hh) {
+                // denominator columns h*32 + hh*16 .. +16 of this row: (V G_W) in
+                // fp32, l ascending (the row is this thread's: no separate pass)
+                float den[16];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const double vk = (double)va[i];
-                    const double qk = ((double)q[4 * k4 + i] + (double)q2[4 * k4 + i]) * qscale;
-                    acc = fma(vk, qk, acc);
-                    gacc = fma(vk, (double)da[i], gacc);   // <V, V G_W> = <V^T V, G_W>
-                    nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
-                    vmax = fmaxf(vmax, nv[i]);
+                for (int c = 0; c < 16; ++c) den[c] = 0.f;
+#pragma unroll 2
+                for (int l4 = 0; l4 < R / 4; ++l4) {
+                    const float4 vv = vr[l4];
+                    const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float4* g4 = reinterpret_cast<const float4*>(
+                            gws + (4 * l4 + e) * R + h * 32 + hh * 16);
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const float4 g = g4[c4];
+                            den[4 * c4] = fmaf(va[e], g.x, den[4 * c4]);
+                            den[4 * c4 + 1] = fmaf(va[e], g.y, den[4 * c4 + 1]);
+                            den[4 * c4 + 2] = fmaf(va[e], g.z, den[4 * c4 + 2]);
+                            den[4 * c4 + 3] = fmaf(va[e], g.w, den[4 * c4 + 3]);
+                        }
+                    }
                 }
-                o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+#pragma unroll
+                for (int kq = 0; kq < 4; ++kq) {
+                    const int k4 = hh * 4 + kq;
+                    const float4 vv = v4[k4];
+                    const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+                    const float da[4] = {den[4 * kq], den[4 * kq + 1], den[4 * kq + 2],
+                                         den[4 * kq + 3]};
+                    float nv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double vk = (double)va[i];
+                        const double qk = ((double)q[4 * k4 + i] + (double)q2[4 * k4 + i]) * qscale;
+                        acc = fma(vk, qk, acc);
+                        gacc = fma(vk, (double)da[i], gacc);   // <V, V G_W> = <V^T V, G_W>
+                        nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
+                        vmax = fmaxf(vmax, nv[i]);
+                    }
+                    o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+                }
             }
         }
     };
@@ -814,62 +852,6 @@ presplit_kernel(const float* __restrict__ X, long long ldx, int m, int n, XXCach
     }
 }
 
-// DEN = V G_W (the V-step denominator without its guard): fp32 FFMA with
-// G_W rounded to fp32 -- the denominator only needs fp32 accuracy (SURVEY.md
-// 7.3-1: Gram-side products in fp32 keep raw V within 5e-6 of fp64).  A block
-// computes 64 rows x 64 columns with 4 x 4 register tiles per thread.
-constexpr int VGW_SMEM = 2 * R * (64 + 4) * 4;
-constexpr int VGW_CHUNKS = 4;   // 64-row chunks per block (amortise the G_W load)
-__global__ void __launch_bounds__(256)
-vgw_kernel(const float* __restrict__ V, const double* __restrict__ GW, float* __restrict__ DEN,
-           long long m) {
-    extern __shared__ float vgw_smem[];
-    float(*G)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem);
-    float(*Vt)[64 + 4] = reinterpret_cast<float(*)[64 + 4]>(vgw_smem + R * (64 + 4));
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    for (int i = threadIdx.x; i < R * R; i += 256) G[i / R][i % R] = (float)GW[i];
-    for (int ch = 0; ch < VGW_CHUNKS; ++ch) {
-        const long long r0 = ((long long)blockIdx.x * VGW_CHUNKS + ch) * 64;
-        if (r0 >= m) break;
-        __syncthreads();   // G ready / previous chunk's Vt consumed
-        // consecutive threads take consecutive rows: conflict-free transposed
-        // smem stores (the row's 16-byte pieces are read by 16 warps, L1 hits)
-        for (int i = threadIdx.x; i < 16 * R; i += 256) {
-            const int rr = i % 64, l4 = (i / 64) * 4;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + l4);
-            Vt[l4][rr] = v.x;
-            Vt[l4 + 1][rr] = v.y;
-            Vt[l4 + 2][rr] = v.z;
-            Vt[l4 + 3][rr] = v.w;
-        }
-        __syncthreads();
-        float acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 8
-        for (int l = 0; l < R; ++l) {
-            const float4 a = *reinterpret_cast<const float4*>(&Vt[l][4 * ty]);
-            const float4 b = *reinterpret_cast<const float4*>(&G[l][4 * tx]);
-            const float av[4] = {a.x, a.y, a.z, a.w};
-            const float bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const long long row = r0 + 4 * ty + i;
-            if (row < m)
-                *reinterpret_cast<float4*>(DEN + row * R + 4 * tx) =
-                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        }
-    }
-}
-
 // Rank-64 Gram G = sum_c a_c a_c^T of fp32 vectors a_c (VEC_ROWS: A is
 // 64 x len, the vectors are columns of the row-major W; else A is len x 64,
 // the rows of V).  Products are formed in fp32 and summed 8 at a time in
@@ -1100,11 +1082,12 @@ struct TcPlan {
 };
 
 // pair: CTA pairs (cta_group::2) -- kNumSMs / 2 work slots of 256 rows
-// (V step) or 2 CB column blocks (W step); grids are even.  Experimental,
-// opt-in (MMK_TC_PAIR=1): correct (tests/test_nnmf_tc_gpu.py passes with it),
-// but with NA = 4 TMEM A buffers the cross-CTA split -> MMA -> commit loop
-// (~6.7k cycles) paces a stage at ~1.7k cycles against ~1.17k for single
-// CTAs (scripts/tctrace.py), so the single-CTA kernels stay the default.
+// (V step) or 2 CB column blocks (W step); grids are even.  Opt-in
+// (MMK_TC_PAIR=1), correct (tests/test_nnmf_tc_gpu.py).  With the split warps
+// the cross-CTA split -> MMA -> commit loop (~6.7k cycles) paced a stage at
+// ~1.7k cycles against ~1.17k for single CTAs (scripts/tctrace.py); with
+// pre-split X that loop is gone and pairs run within 1-2 % of single CTAs
+// (both HBM-bound), so single CTAs stay the default.
 bool pair_on() {
     static const bool on = [] {
         const char* e = getenv("MMK_TC_PAIR");
@@ -1287,7 +1270,6 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
         big(nnmf_wstep_tc<false, true>);
         big(nnmf_vstep_tc<true, true>);
         big(nnmf_wstep_tc<true, true>);
-        cudaFuncSetAttribute(vgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VGW_SMEM);
     }
     // cluster launch of the pair kernels (2 CTAs = one TPC)
     auto launch_pair = [&](auto kern, int grid, auto... args) {
@@ -1338,19 +1320,16 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
     gram32(W, n, true, L.gpart, GW, st);
-    MMK_LAUNCH("nnmf_vgw",
-               st, (vgw_kernel<<<ceil_div(m, 64 * VGW_CHUNKS), 256, VGW_SMEM, st>>>(V, GW, L.DEN,
-                                                                                m)));
     {
         auto vk = pair ? (ps ? nnmf_vstep_tc<true, true> : nnmf_vstep_tc<true, false>)
                        : (ps ? nnmf_vstep_tc<false, true> : nnmf_vstep_tc<false, false>);
         if (pair)
             MMK_LAUNCH("nnmf_vstep_tc", st,
-                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const float*)L.DEN, V_out,
+                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const double*)GW, V_out,
                                    L.sc, (int)m, (int)n, L.part, g_trace_v));
         else
             MMK_LAUNCH("nnmf_vstep_tc", st,
-                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, L.DEN, V_out, L.sc,
+                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, GW, V_out, L.sc,
                                                             (int)m, (int)n, L.part, g_trace_v)));
     }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");

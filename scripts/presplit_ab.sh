@@ -1,6 +1,6 @@
 # A/B of the NNMF tensor-core variants at C4 (one GPU), interleaved; pass the
 # env settings to compare as arguments (default: pre-split X vs split warps)
-B="python bench.py --steps 30 --warmup 3 --no-e2e --no-suite --cpu-seconds 0"
+B="python bench.py --steps ${STEPS:-30} --warmup 3 --no-e2e --no-suite --cpu-seconds 0"
 [ $# -eq 0 ] && set -- "" "MMK_TC_PRESPLIT=0"
 for rep in 1 2; do
   for v in "$@"; do
