@@ -71,12 +71,16 @@ constexpr uint32_t SOP = R * BK * 2;        //  8 KB  fp16 operand chunk hi; sam
 #define MMK_TC_XST 4
 #endif
 #ifndef MMK_TC_OST
-#define MMK_TC_OST 4
+#define MMK_TC_OST 3
 #endif
 constexpr int XST = MMK_TC_XST;             // X ring (128 KB in flight per SM)
-constexpr int OST = MMK_TC_OST;             // operand ring
+constexpr int OST = MMK_TC_OST;             // operand ring (3: 2 hold X back, measured)
+// V' tile for the fused Gram (pre-split X): 128 rows x 16 float4, float4 c of
+// row r at slot c ^ (r & 7) (conflict-free row-per-thread writes)
+constexpr uint32_t SGB = BM * R * 4;        // 32 KB
 constexpr uint32_t SGW = R * R * 4;         // 16 KB  G_W (fp32) for the V-step epilogue
-constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + SGW + 1024;
+constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + SGB + SGW + 1024;
+static_assert(SMEM + 2048 <= 232448, "dynamic + static shared memory per CTA");
 constexpr int NA = 4;                       // TMEM A-operand buffers [X_hi | X_lo] (64 cols)
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
 constexpr int TMAX = 2;                     // accumulators per pass (V step: row tiles)
@@ -121,6 +125,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
 struct Bars {
     uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST], afull[NA], aempty[NA];
     uint64_t dfull[2], dempty[2];   // accumulator sets (pre-split X: two, else one)
+    uint64_t gfull, gempty;         // V' tile buffer (V step, pre-split X): epilogue -> Gram warps
 };
 
 // pair: the leader's afull / dempty also count one arrival of the peer CTA;
@@ -143,6 +148,8 @@ __device__ __forceinline__ void init_bars(Bars& B, bool pair, bool presplit) {
         tc::mbar_init(&B.dfull[b], 1);
         tc::mbar_init(&B.dempty[b], 128 + (two - 1));
     }
+    tc::mbar_init(&B.gfull, 128);             // the epilogue threads (one row each)
+    tc::mbar_init(&B.gempty, 32 * NCONV);     // the Gram warps
     tc::fence_barrier_init();
 }
 
@@ -446,8 +453,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh,
               const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
-              const double* __restrict__ GW, float* __restrict__ Vout, Scales* sc, int m, int n,
-              double* __restrict__ part, unsigned long long* tr) {
+              const float* __restrict__ GWf, float* __restrict__ Vout, Scales* sc, int m, int n,
+              double* __restrict__ part, double* __restrict__ gpart, unsigned long long* tr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     __shared__ Bars B;
@@ -462,9 +469,12 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const int units = PAIR ? (ntiles + 1) / 2 : ntiles;
     const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
     const int npass = (mine + TMAX - 1) / TMAX;
-    // G_W rounded to fp32 for the epilogue's denominator rows (V G_W)_i
-    float* gws = reinterpret_cast<float*>(base + XST * SX + OST * 2 * SOP);
-    for (int i = threadIdx.x; i < R * R; i += kThreads) gws[i] = (float)GW[i];
+    // GWf: G_W rounded to fp32 (gram_sum_kernel), staged in smem for the
+    // epilogue's denominator rows (V G_W)_i
+    float4* gbuf = reinterpret_cast<float4*>(base + XST * SX + OST * 2 * SOP);
+    float* gws = reinterpret_cast<float*>(base + XST * SX + OST * 2 * SOP + SGB);
+    for (int i = threadIdx.x; i < R * R / 4; i += kThreads)
+        reinterpret_cast<float4*>(gws)[i] = __ldg(reinterpret_cast<const float4*>(GWf) + i);
     if (threadIdx.x == 0) {
         init_bars(B, PAIR, PS);
         tc::tma_prefetch(&mX);
@@ -516,14 +526,27 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::tma_load_2d(dst + BM * 128, &mX, bar, kb * BK + 32, tile_of(p, j) * BM);
         }
     };
+    // PS: the epilogue also copies the V' tile into gbuf, where the (otherwise
+    // idle) split warps form its Gram V'^T V' -- no separate pass over V'
     auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool) {
         const long long row = (long long)tile_of(p, j) * BM + quarter * 32 + ln;
+        const int git = p * TMAX + j;   // this CTA's tile sequence number
+        const int grr = quarter * 32 + ln;
+        float4* grow = gbuf + grr * (R / 4);
+        if (PS && git > 0) tc::mbar_wait(&B.gempty, (git - 1) & 1);
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             float q[32], q2[32];
             tc::tmem_ld32(ta + h * 32, q);
             tc::tmem_ld32(ta + R + h * 32, q2);
-            if (row >= m) continue;
+            if (row >= m) {
+                if (PS) {   // rows past m count as zero in the Gram
+#pragma unroll
+                    for (int k4 = 0; k4 < 8; ++k4)
+                        grow[(h * 8 + k4) ^ (grr & 7)] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                continue;
+            }
             const float4* v4 = reinterpret_cast<const float4*>(V + row * R + h * 32);
             const float4* vr = reinterpret_cast<const float4*>(V + row * R);
             float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
@@ -570,12 +593,59 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         vmax = fmaxf(vmax, nv[i]);
                     }
                     o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+                    if (PS) grow[(h * 8 + k4) ^ (grr & 7)] = make_float4(nv[0], nv[1], nv[2], nv[3]);
                 }
             }
         }
+        if (PS) tc::mbar_arrive(&B.gfull);   // release: this row of gbuf is written
     };
     run_pipeline<false, PAIR, PS>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
                               tr);
+    if constexpr (PS) {
+        // Gram warps (the split warps, idle with pre-split X): thread t owns the
+        // 4 x 4 block (4 (t / 16), 4 (t % 16)) of V'^T V' over this CTA's tiles;
+        // fp32 products summed 8 rows at a time, folded into fp64 (as gram32)
+        if (warp >= 2 && warp < 2 + NCONV) {
+            const int t = threadIdx.x - 64, ka = 4 * (t >> 4), kb = 4 * (t & 15);
+            double g[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) g[i][q] = 0.0;
+            for (int it = 0; it < mine; ++it) {
+                tc::mbar_wait(&B.gfull, it & 1);
+#pragma unroll 1
+                for (int r0 = 0; r0 < BM; r0 += 8) {
+                    float pr[4][4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) pr[i][q] = 0.f;
+#pragma unroll
+                    for (int r = r0; r < r0 + 8; ++r) {
+                        const float4 a = gbuf[r * (R / 4) + ((ka >> 2) ^ (r & 7))];
+                        const float4 b = gbuf[r * (R / 4) + ((kb >> 2) ^ (r & 7))];
+                        const float av[4] = {a.x, a.y, a.z, a.w};
+                        const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) pr[i][q] = fmaf(av[i], bv[q], pr[i][q]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) g[i][q] += (double)pr[i][q];
+                }
+                tc::mbar_arrive(&B.gempty);
+            }
+            double* pb = gpart + (long long)blockIdx.x * (R * R);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) pb[(ka + i) * R + kb + q] = g[i][q];
+        }
+    }
     // per-CTA partials <V, Q>, <V, V G_W> and max(V') (epilogue warps)
     __shared__ double gred[kThreads / 32];
     acc = warp_sum(acc);
@@ -921,7 +991,8 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
 // out[e] = sum_b part[b][e] in block order: 8 groups of 128 threads take
 // interleaved partials, combined in group order (deterministic)
 __global__ void __launch_bounds__(1024)
-gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out,
+                float* __restrict__ outf) {
     __shared__ double sm[8][128];
     const int o = blockIdx.x * 128 + (threadIdx.x & 127), g = threadIdx.x >> 7;
     double s = 0.0;
@@ -934,6 +1005,7 @@ gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict_
 #pragma unroll
         for (int k = 1; k < 8; ++k) t += sm[k][threadIdx.x];
         out[o] = t;
+        if (outf) outf[o] = (float)t;   // fp32 copy (G_W for the V-step epilogue)
     }
 }
 
@@ -1147,7 +1219,7 @@ constexpr int kGramBlocks = 2 * kNumSMs;
 
 // G = Gram of A (see gram32_kernel) into out (fp64 64 x 64)
 void gram32(const float* A, long long len, bool vec_rows, double* gpart, double* out,
-            cudaStream_t st) {
+            cudaStream_t st, float* outf = nullptr) {
     long long per = (len + kGramBlocks - 1) / kGramBlocks;
     per = (per + 31) / 32 * 32;
     const int blocks = (int)((len + per - 1) / per);
@@ -1158,13 +1230,13 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
         MMK_LAUNCH("nnmf_gram32", st,
                    (gram32_kernel<false><<<blocks, 256, 0, st>>>(A, len, per, gpart)));
     MMK_LAUNCH("nnmf_gram_sum", st,
-               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out)));
+               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out, outf)));
 }
 
 struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl;
     __half *Xh, *Xl, *XTh, *XTl;   // pre-split X (presplit_on(m, n) only)
-    float *wpart, *DEN, *mpart;
+    float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
     double *GVn, *part, *sqpart, *gpart;
     XXCache* xx;
     Scales* sc;
@@ -1186,7 +1258,6 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     };
     size_t oWh = take(2 * (size_t)R * n), oWl = take(2 * (size_t)R * n);
     size_t oVh = take(2 * (size_t)R * m), oVl = take(2 * (size_t)R * m);
-    size_t oD = take(4 * (size_t)R * m);
     size_t oWp = take(4 * (size_t)P.splits * n * R);
     size_t oG = take(8 * (size_t)R * R);
     size_t oP = take(16 * (size_t)kNumSMs);
@@ -1194,6 +1265,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) sumsq, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
+    size_t oGF = take(4 * (size_t)R * R);
     const size_t xe = presplit_on(m, n) ? (size_t)m * n : 0;
     size_t oXh = take(2 * xe), oXl = take(2 * xe), oXTh = take(2 * xe), oXTl = take(2 * xe);
     if (base && L) {
@@ -1211,11 +1283,11 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->Wl = (__half*)(c + oWl);
         L->Vth = (__half*)(c + oVh);
         L->Vtl = (__half*)(c + oVl);
-        L->DEN = (float*)(c + oD);
         L->wpart = (float*)(c + oWp);
         L->GVn = (double*)(c + oG);
         L->part = (double*)(c + oP);
         L->gpart = (double*)(c + oGP);
+        L->GWf = (float*)(c + oGF);
     }
     return off;
 }
@@ -1319,24 +1391,30 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
-    gram32(W, n, true, L.gpart, GW, st);
+    gram32(W, n, true, L.gpart, GW, st, L.GWf);
     {
         auto vk = pair ? (ps ? nnmf_vstep_tc<true, true> : nnmf_vstep_tc<true, false>)
                        : (ps ? nnmf_vstep_tc<false, true> : nnmf_vstep_tc<false, false>);
         if (pair)
             MMK_LAUNCH("nnmf_vstep_tc", st,
-                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const double*)GW, V_out,
-                                   L.sc, (int)m, (int)n, L.part, g_trace_v));
+                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const float*)L.GWf, V_out,
+                                   L.sc, (int)m, (int)n, L.part, L.gpart, g_trace_v));
         else
             MMK_LAUNCH("nnmf_vstep_tc", st,
-                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, GW, V_out, L.sc,
-                                                            (int)m, (int)n, L.part, g_trace_v)));
+                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, L.GWf, V_out, L.sc,
+                                                            (int)m, (int)n, L.part, L.gpart,
+                                                            g_trace_v)));
     }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx,
                                                         red + rn + (long long)R * R)));
-    gram32(V_out, m, false, L.gpart, red + rn, st);
+    if (ps)   // V'^T V' partials came from the V step (one per CTA)
+        MMK_LAUNCH("nnmf_gram_sum", st,
+                   (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(L.gpart, P.vgrid, red + rn,
+                                                                   nullptr)));
+    else
+        gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
                (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
     {

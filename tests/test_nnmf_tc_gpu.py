@@ -198,9 +198,11 @@ def test_kernel_variants_match_fp64(env):
     empty half of the last pair): MMK_TC_PAIR=1 -- CTA pairs (cta_group::2);
     MMK_TC_PRESPLIT=0 -- the split-warp kernels instead of the default
     pre-split X (fp16 hi / lo made once, SS MMAs from TMA tiles).  The
-    single-CTA kernels of both kinds form the same products from the same fp16
-    values: their traces must be equal."""
+    single-CTA kernels of both kinds form the same X products from the same
+    fp16 values; only the Gram V'^T V' is summed in a different grouping (fused
+    into the pre-split V step vs the separate gram32 pass), so their traces
+    agree to fp32-Gram rounding."""
     t = _variant_trace(**env)
     if env == {"MMK_TC_PRESPLIT": "0"}:
         base = _variant_trace(MMK_TC_PRESPLIT="1", MMK_TC_PAIR="0")
-        assert np.array_equal(t, base), np.max(np.abs(t - base) / base)
+        assert np.max(np.abs(t - base) / base) < 1e-6, np.max(np.abs(t - base) / base)
