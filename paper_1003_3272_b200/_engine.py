@@ -61,8 +61,15 @@ class DeviceMm(MmProblem):
         self.status.clear_error()
         self._cache = None
         self.launches_per_iter = 0
-        if backend.fused:
-            self.run_fused = self._run_fused
+        self._fused = bool(backend.fused)
+
+    @property
+    def run_fused(self):
+        """The fused device loop when the backend allows it (``driver.run_mm``
+        picks it up), else None.  A property, not an instance attribute holding
+        the bound method: that would be a reference cycle keeping X and the
+        workspace alive until the garbage collector happens to run."""
+        return self._run_fused if self._fused else None
 
     # ---- plumbing -----------------------------------------------------------
     def stream(self):

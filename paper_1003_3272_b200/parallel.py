@@ -179,7 +179,7 @@ def _make_sharded_nnmf(base_cls, iter_a, iter_b):
     class _Sharded(base_cls):
         def __init__(self, problem, backend, group):
             super().__init__(problem, backend)
-            self.__dict__.pop("run_fused", None)     # per-iteration protocol
+            self._fused = False     # per-iteration protocol
             self.group = group
 
         def _iterate(self, s, out, f_ptr, err_ptr):
@@ -240,7 +240,7 @@ def mds_run_sharded(problem, config, backend, group=None, theta0=None):
         theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
                                                             size=(problem.p, problem.q))
     mm = D._GpuMdsTri(problem, backend, group=group)
-    mm.__dict__.pop("run_fused", None)
+    mm._fused = False
     base_iter = mm._iterate
 
     def _iterate(theta, out, f_ptr, err_ptr):
@@ -318,7 +318,7 @@ def _mds_rows_sharded(problem, config, backend, group, theta0):
                 out[:, a:b].copy_(self.parts[r][:, :b - a])
 
     mm = _RowsMm()
-    mm.__dict__.pop("run_fused", None)     # per-iteration protocol
+    mm._fused = False     # per-iteration protocol
     return run_mm(mm, mm.device_state(theta0), config)
 
 
@@ -361,6 +361,6 @@ def pet_run_sharded(problem, config, backend, group=None):
                    self.mu, flags, P(self.red), P(self.ws), self.ws.numel(), f_ptr, err_ptr, st)
 
     mm = _Sharded(problem, backend, rows=(lo, hi))
-    mm.__dict__.pop("run_fused", None)     # per-iteration protocol
+    mm._fused = False     # per-iteration protocol
     state, trace = run_mm(mm, mm.device_state(np.ones(problem.n_pixels)), config)
     return A.to_user(state, problem.e), trace
