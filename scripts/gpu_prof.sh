@@ -3,7 +3,7 @@ set -x
 python -c "import __graft_entry__ as g; g.build()"
 timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench rc=$?
 B="python bench.py --steps 3 --warmup 1 --no-e2e --no-suite --cpu-seconds 0"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'nnmf|pois|gram|vgw|vprep|wreduce|wmax|split_w|sumsq|objective' --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'nnmf|pois|gram|presplit|vprep|wreduce|wmax|split_w|sumsq|objective' --csv \
   --log-file gpurun_out/launches_nnmf_large.csv $B > gpurun_out/launches.log 2>&1; echo l1 rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'mds' --csv \
   --log-file gpurun_out/launches_mds_large.csv $B --workload mds-large > gpurun_out/launches2.log 2>&1; echo l2 rc=$?
