@@ -52,3 +52,28 @@ def test_sass_has_no_legacy_fallback_symbols():
     # the product library is CUDA-only: no host compute entry points
     lib = _lib.load()
     assert not hasattr(lib, "ora_matmul")
+
+
+@pytest.mark.parametrize("env,presplit", [(None, True), ("0", False), ("1", True)])
+def test_nnmf_tc_presplit_workspace_policy(env, presplit):
+    """The tensor-core NNMF workspace holds the pre-split copy of X (fp16 hi / lo,
+    row-major + transposed: 8 bytes per element) unless MMK_TC_PRESPLIT=0, and by
+    default only while that copy stays within 48 GiB (read once per process,
+    hence the subprocess)."""
+    import subprocess
+    import sys
+    code = ("from paper_1003_3272_b200 import _lib\n"
+            "print(_lib.ws_bytes('mmk_nnmf_ws_bytes', 0, 131072, 16384, 64),"
+            " _lib.ws_bytes('mmk_nnmf_ws_bytes', 0, 262144, 65536, 64))")
+    e = dict(os.environ)
+    e.pop("MMK_TC_PRESPLIT", None)
+    if env is not None:
+        e["MMK_TC_PRESPLIT"] = env
+    out = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    c4, big = (int(v) for v in out.stdout.split())
+    copy = 8 * 131072 * 16384
+    assert (c4 >= copy) == presplit and c4 < copy + (1 << 30)
+    # 262144 x 65536: the copy would be 128 GiB -- only when forced
+    assert (big >= 8 * 262144 * 65536) == (env == "1")
