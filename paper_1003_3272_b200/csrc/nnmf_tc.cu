@@ -21,11 +21,14 @@
 //     warp 0   TMA producer: X tile [128 rows x 64 cols] fp32 (two 128B-
 //              swizzled boxes) + [W_hi ; W_lo] fp16 chunk [128 x 64] per stage
 //     warps 2-9 split warps: read X rows from smem, release the slot, write
-//              fp16 hi / lo to a TMEM A-buffer (32 + 32 columns)
+//              fp16 hi / lo to a TMEM A-buffer (32 + 32 columns); with
+//              pre-split X (below) there is nothing to split and they form
+//              the Gram V'^T V' of each finished V' tile instead
 //     warp 1   one thread issues 4 x (TS MMA hi, N = 128; TS MMA lo, N = 64)
 //              (M128 K16) per stage into an fp32 accumulator Q = X W^T
-//     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300), <V, Q> (fp64),
-//              max(V') for the W step's scale
+//     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300) with the row of
+//              V G_W formed here (fp32), <V, Q> (fp64), max(V') for the
+//              W step's scale
 //   nnmf_vprep     V' -> V'^T hi / lo fp16 [64][m] (scaled): the W-step B operand
 //   nnmf_wstep_tc  P^T = X^T V' (M = 128 columns of X, N = 64, K = rows),
 //              split-K over row ranges; per-split partials reduced in fixed
