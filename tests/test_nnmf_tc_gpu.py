@@ -107,6 +107,23 @@ def test_tc_deterministic():
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and a[2] == b[2]
 
 
+def test_tc_strided_x_equals_contiguous():
+    """X given as a column slice of a wider matrix (row stride ldx > n): the
+    scale pass and the pre-split copy follow ldx, so V', W' and f equal the
+    contiguous copy's bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(21)
+    m, n = 1536, 640
+    wide = torch.rand(m, n + 64, device="cuda", generator=g)
+    v = torch.rand(m, 64, device="cuda", generator=g)
+    w = torch.rand(64, n, device="cuda", generator=g)
+    xs = wide[:, :n]
+    assert xs.stride(0) == n + 64
+    (a, used) = tc_launched(lambda: one_iter(xs, v, w, force_simt=False))
+    assert used
+    b = one_iter(xs.contiguous(), v, w, force_simt=False)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and a[2] == b[2]
+
+
 def test_tc_wide_row_dynamic_range():
     """Rows of X scaled by 2^u, u uniform in [-12, 12], and W entries spread
     over 2^[-6, 6]: one scaled split per operand still gives fp32-level
