@@ -76,6 +76,11 @@ int mmk_prof_report(char *buf, size_t len);
  *            f_dev = red[f]
  * The row range is the caller's shard of X/V (rows are independent in the
  * V step; the W step is a sum over rows, hence the all-reduce of `red`).
+ * The workspace (zero-filled by the caller before first use) caches per-X
+ * data of the fp32 tensor-core path -- sum x^2, the scale exponent and the
+ * pre-split fp16 hi / lo copy of X (8 bytes per element unless
+ * MMK_TC_PRESPLIT=0, or while it would pass 48 GiB) -- keyed by (X, m, n, ldx):
+ * zero it again, or use a fresh one, if the contents of X change in place.
  * ---------------------------------------------------------------------- */
 int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
 int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r);
