@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "mm_control.cuh"
+#include "nnmf_tc.h"
 #include "small_engine.h"
 
 namespace {
@@ -40,6 +41,8 @@ struct Engine {
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cap = nullptr;
     mmk_small::Launch persistent;   // set: one persistent-kernel launch per batch
+    std::function<int(cudaStream_t)> prologue;   // once, before the first batch
+    bool prologue_done = false;
 };
 
 // half 0 follows iteration A -> B (its objective is f(A)), half 1 follows
@@ -212,6 +215,11 @@ extern "C" int mmk_engine_run(void* eng, void* stream) {
         return MMK_E_SHAPE;
     }
     if (e->persistent.fn) return e->persistent.fn(reinterpret_cast<cudaStream_t>(stream));
+    if (e->prologue && !e->prologue_done) {
+        const int rc = e->prologue(reinterpret_cast<cudaStream_t>(stream));
+        if (rc) return rc;
+        e->prologue_done = true;
+    }
     cudaError_t ce = cudaGraphLaunch(e->exec, reinterpret_cast<cudaStream_t>(stream));
     if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "cudaGraphLaunch");
     return MMK_OK;
@@ -259,7 +267,19 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
         }
         return mmk_nnmf_iter_b(dtype, Wi, Wo, n, r, red, f_dev, err_dev, s);
     };
-    return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
+    // tensor-core path: the per-X preparation runs once (engine prologue, on
+    // the run's stream) instead of as a key check in every captured iteration
+    void* tcws = mmk_tc::engine_tc_ws(dtype, X, ldx, m, n, r, ws);
+    if (tcws) mmk_tc::set_x_prepared(true);
+    const int rc = build(iter, rule, trace, tstamp, ctl, err_dev, engine);
+    mmk_tc::set_x_prepared(false);
+    if (rc == MMK_OK && tcws) {
+        const float* Xf = reinterpret_cast<const float*>(X);
+        reinterpret_cast<Engine*>(*engine)->prologue = [=](cudaStream_t s) {
+            return mmk_tc::prepare_x(Xf, ldx, m, n, tcws, s);
+        };
+    }
+    return rc;
 }
 
 extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, const void* y,

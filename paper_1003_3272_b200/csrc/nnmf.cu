@@ -703,6 +703,15 @@ int run_a(int dtype, Args a) {
 
 }  // namespace
 
+void* mmk_tc::engine_tc_ws(int dtype, const void* X, long long ldx, long long m, long long n,
+                          long long r, void* ws) {
+    if (dtype != MMK_F32 || !tc_shape(m, n, (int)r) || !eligible(MMK_F32, m, n, r, ldx, X))
+        return nullptr;
+    Ws L;
+    ws_layout(make_plan(m, n, (int)r), m, n, (int)r, ws, &L);
+    return L.tc;
+}
+
 extern "C" int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t* out) {
     (void)dtype;
     if (r < 1 || r > kMaxRank || n < 1) {

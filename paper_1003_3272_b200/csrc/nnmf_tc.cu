@@ -1296,6 +1296,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
 }
 
 unsigned long long* g_trace_v = nullptr;   // debug: mmk_tc_set_trace
+thread_local bool t_x_prepared = false;      // set while an engine captures its loop
 unsigned long long* g_trace_w = nullptr;
 
 }  // namespace
@@ -1314,6 +1315,24 @@ bool eligible(int dtype, long long m, long long n, long long r, long long ldx, c
 }
 
 size_t ws_bytes(long long m, long long n) { return tc_layout(m, n, nullptr, nullptr); }
+
+void set_x_prepared(bool on) { t_x_prepared = on; }
+
+int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
+              cudaStream_t st) {
+    TcWs L;
+    tc_layout(m, n, tcws, &L);
+    MMK_LAUNCH("nnmf_sumsq_cached", st,
+               (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
+                                                           L.counter, L.sc)));
+    if (presplit_on(m, n))
+        MMK_LAUNCH("nnmf_presplit_cached", st,
+                   (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
+                                                                 L.Xl, L.XTh, L.XTl,
+                                                                 L.counter + 2)));
+    MMK_CHECK_LAUNCH("nnmf_prepare_x");
+    return MMK_OK;
+}
 
 // Phase A of one iteration on the tensor cores; writes V_out and
 // red = [P | G_V' | f-partial].
@@ -1380,14 +1399,10 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
     if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, R, m, m, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, R, m, m, R))) return rc;
     const long long rn = (long long)R * n;
-    MMK_LAUNCH("nnmf_sumsq_cached", st,
-               (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
-                                                           L.counter, L.sc)));
-    if (ps)
-        MMK_LAUNCH("nnmf_presplit_cached", st,
-                   (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
-                                                                 L.Xl, L.XTh, L.XTl,
-                                                                 L.counter + 2)));
+    if (!t_x_prepared) {
+        int prc = prepare_x(X, ldx, m, n, tcws, st);
+        if (prc) return prc;
+    }
     MMK_LAUNCH("nnmf_wmax", st,
                (wmax_kernel<<<kNumSMs, 1024, 0, st>>>(W, rn, L.mpart + 4 * kNumSMs,
                                                      L.counter + 1, L.sc)));

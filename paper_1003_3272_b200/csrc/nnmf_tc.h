@@ -11,4 +11,16 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
            long long m, long long n, void* tcws, double* GW, double* red,
            cudaStream_t st);
 
+// Per-X preparation (sum x^2 / scale exponent, the pre-split copy): iter_a
+// launches it every iteration (a key check after the first); a device-loop
+// engine runs it once before its first batch (prepare_x) and captures its
+// loop with set_x_prepared(true), which leaves those launches out.
+int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
+              cudaStream_t st);
+void set_x_prepared(bool on);
+// the NNMF workspace's tensor-core part for (dtype, m, n, r), or nullptr when
+// the tensor-core path does not apply (nnmf.cu)
+void* engine_tc_ws(int dtype, const void* X, long long ldx, long long m, long long n, long long r,
+                   void* ws);
+
 }  // namespace mmk_tc
