@@ -223,3 +223,19 @@ def test_kernel_variants_match_fp64(env):
     if env == {"MMK_TC_PRESPLIT": "0"}:
         base = _variant_trace(MMK_TC_PRESPLIT="1", MMK_TC_PAIR="0")
         assert np.max(np.abs(t - base) / base) < 1e-6, np.max(np.abs(t - base) / base)
+
+
+def test_engine_prologue_equals_per_iteration_path():
+    """The device-loop engine prepares X once (engine prologue) and leaves the
+    per-X launches out of its graph; the per-iteration path launches them
+    every iteration (key check).  Same trace and factors, bit for bit."""
+    rng = np.random.default_rng(12)
+    x = rng.random((1280, 896)).astype(np.float32)
+    v0 = rng.random((1280, 64)).astype(np.float32)
+    w0 = rng.random((64, 896)).astype(np.float32)
+    prob = M.NnmfProblem(x=x, rank=64)
+    cfg = M.MmConfig(max_iters=12, epsilon=1e-300, monotone_tol=1e-6)
+    a, ta = M.nnmf_run(prob, cfg, M.Backend(dtype="fp32", fused=True), state0=M.FactorPair(v0, w0))
+    b, tb = M.nnmf_run(prob, cfg, M.Backend(dtype="fp32", fused=False), state0=M.FactorPair(v0, w0))
+    assert np.array_equal(ta.objective_values, tb.objective_values)
+    assert np.array_equal(a.v, b.v) and np.array_equal(a.w, b.w)
