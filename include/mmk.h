@@ -77,12 +77,16 @@ int mmk_prof_report(char *buf, size_t len);
  * The row range is the caller's shard of X/V (rows are independent in the
  * V step; the W step is a sum over rows, hence the all-reduce of `red`).
  * The workspace (zero-filled by the caller before first use) caches per-X
- * data of the fp32 tensor-core path -- sum x^2, the scale exponent and the
- * pre-split fp16 hi / lo copy of X (8 bytes per element unless
- * MMK_TC_PRESPLIT=0, or while it would pass 48 GiB) -- keyed by (X, m, n, ldx):
- * zero it again, or use a fresh one, if the contents of X change in place.
+ * data of the fp32 tensor-core path (rank 64) -- the scale exponent and the
+ * pre-split fp16 hi / lo copy of X (8 bytes per element; shapes whose copy
+ * would pass 96 GiB take the SIMT path) -- keyed by (X, m, n, ldx): zero it
+ * again, or use a fresh one, if the contents of X change in place.
+ * mmk_nnmf_ws_bytes sizes the workspace of iter / iter_a / the engine;
+ * mmk_nnmf_op_ws_bytes the smaller one of the single operations below (they
+ * run the SIMT kernels and never touch the tensor-core region).
  * ---------------------------------------------------------------------- */
 int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
+int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
 int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r);
 int mmk_nnmf_iter_a(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
                     void *V_out, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,
@@ -366,36 +370,6 @@ void mmk_engine_destroy(void *engine);
  * device runs): narrow n landed fp64 values to fp32, round-to-nearest-even
  * (numpy astype(float32)); src/dst 16-byte aligned device buffers. */
 int mmk_f64_to_f32(const double *src, float *dst, int64_t n, void *stream);
-
-/* Known-answer self-test of the tcgen05 building blocks (TMA 128B-swizzle
- * tiles, K-/MN-major UMMA descriptors, kind::tf32 MMA, TMEM loads):
- *   D1[128x64] = A[128x64] B[64x64]^T,  D2[128x32] = A B[:, :32],
- *   D3[128x64] = X[32x128]^T V[32x64]   (device fp32, row-major).
- * mode bits: 1 dump the raw swizzled A tile into D1, 2/4/8 run D1/D2/D3;
- * diag (device int) gets bit 1 if the TMA barrier timed out, 2 for MMA. */
-int mmk_selftest_tc(const float *A, const float *B, const float *X, const float *V, float *D1,
-                    float *D2, float *D3, int mode, int *diag, void *stream);
-
-/* Tuning aid: cycles for `iters` back-to-back tcgen05.mma of one shape
- * (mode 0 SS tf32 N128, 1 TS tf32 N128, 2 TS tf32 N64, 3 SS tf32 N256,
- * 4 SS f16 N128, 5 SS tf32 N64, 6 TS f16 N256, 7 SS f16 N256; M = 128) into
- * out[0] (device int64). */
-int mmk_tc_mma_bench(int mode, int iters, long long *out, void *stream);
-
-/* Tuning aid: the same for cta_group::2 (a 2-CTA cluster, M = 256, kind::f16,
- * N = |ncols|, A from TMEM when ncols < 0): leader cycles into out[0],
- * timeout flags into out[1], out[2]. */
-int mmk_tc_mma2_bench(int ncols, int iters, long long *out, void *stream);
-
-/* Tuning aid: cross-CTA hand-off latency in a CTA pair: out[0] cycles per
- * remote-arrive round trip, out[1] per commit-multicast + remote-arrive round
- * trip, out[2..3] timeout flags. */
-int mmk_tc_pingpong(int iters, long long *out, void *stream);
-
-/* Debug: per-stage pipeline timestamps (clock64) of CTA 0 of the tensor-core
- * NNMF kernels, 6 x 256 uint64 per buffer (TMA issue, split start, split
- * done, MMA start, MMA committed); NULL disables (the default). */
-int mmk_tc_set_trace(unsigned long long *vstep, unsigned long long *wstep);
 
 #ifdef __cplusplus
 }

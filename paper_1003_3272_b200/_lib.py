@@ -16,6 +16,9 @@ from .errors import DeviceError, DomainError, NumericsError, raise_for_status
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libmmk.so")
+# tcgen05 self-test and tuning microbenchmarks (include/mmk_diag.h): a separate
+# library, not part of the solver ABI
+DIAG_PATH = os.path.join(_PKG, "libmmk_diag.so")
 ABI_VERSION = 1
 
 MMK_F32, MMK_F64 = 0, 1
@@ -34,12 +37,11 @@ _SIGS = {
     "mmk_prof_enable": ([_i32], _i32),
     "mmk_prof_report": ([_c.c_char_p, _sz], _i32),
     "mmk_f64_to_f32": ([_vp, _vp, _i64, _vp], _i32),
-    "mmk_tc_mma2_bench": ([_i32, _i32, _vp, _vp], _i32),
-    "mmk_tc_pingpong": ([_i32, _vp, _vp], _i32),
     "mmk_nnmf_gradient": ([_i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp,
                            _vp, _vp], _i32),
     "mmk_pet_gradient": ([_i32, _vp, _vp, _i64, _vp, _vp, _dbl, _vp, _vp, _vp], _i32),
     "mmk_nnmf_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
+    "mmk_nnmf_op_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_nnmf_reduce_len": ([_i64, _i64], _i64),
     "mmk_nnmf_iter_a": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp,
                          _vp], _i32),
@@ -103,11 +105,40 @@ _SIGS = {
     "mmk_mds_engine_create": ([_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                _i64, _i64, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "mmk_engine_run": ([_vp, _vp], _i32),
-    "mmk_tc_set_trace": ([_vp, _vp], _i32),
-    "mmk_tc_mma_bench": ([_i32, _i32, _vp, _vp], _i32),
-    "mmk_selftest_tc": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp], _i32),
     "mmk_engine_destroy": ([_vp], None),
 }
+
+
+_DIAG_SIGS = {
+    "mmk_selftest_tc": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp], _i32),
+    "mmk_tc_mma_bench": ([_i32, _i32, _vp, _vp], _i32),
+    "mmk_tc_mma2_bench": ([_i32, _i32, _vp, _vp], _i32),
+    "mmk_tc_pingpong": ([_i32, _vp, _vp], _i32),
+}
+_diag = None
+
+
+def load_diag(path=DIAG_PATH):
+    """The diagnostics library (self-test, MMA microbenchmarks)."""
+    global _diag
+    with _lock:
+        if _diag is None:
+            if not os.path.exists(path):
+                raise DeviceError(f"{path} is missing; build it with "
+                                  "`python -m paper_1003_3272_b200.build`")
+            lib = ctypes.CDLL(path)
+            for name, (args, res) in _DIAG_SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _diag = lib
+        return _diag
+
+
+def call_diag(name, *args):
+    rc = getattr(load_diag(), name)(*args)
+    if rc != 0:
+        raise_for_status(rc, f"{name}: {load_diag().mmk_last_error().decode(errors='replace')}")
 
 
 def exported_symbols():

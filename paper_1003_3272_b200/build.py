@@ -18,6 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libmmk.so")
+DIAG = os.path.join(PKG, "libmmk_diag.so")   # self-test + microbenchmarks (include/mmk_diag.h)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -30,20 +31,25 @@ def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _diag_sources():
+    return sorted(glob.glob(os.path.join(CSRC, "diag", "*.cu")))
+
+
 def _deps():
-    return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+    return _sources() + _diag_sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
 
 
 def _up_to_date():
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(DIAG)):
         return False
-    t = os.path.getmtime(LIB)
+    t = min(os.path.getmtime(LIB), os.path.getmtime(DIAG))
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
 def _compile(src):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    sub = "diag_" if os.path.basename(os.path.dirname(src)) == "diag" else ""
+    obj = os.path.join(OBJ, sub + os.path.basename(src)[:-3] + ".o")
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
@@ -56,14 +62,17 @@ def build(force=False, verbose=False):
     if not force and _up_to_date():
         return LIB
     os.makedirs(OBJ, exist_ok=True)
+    srcs, dsrcs = _sources(), _diag_sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        results = list(ex.map(_compile, _sources()))
+        results = list(ex.map(_compile, srcs + dsrcs))
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
-    objs = [o for o, _ in results]
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
-    subprocess.run(cmd, check=True)
+    objs = [o for o, _ in results[:len(srcs)]]
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], check=True)
+    # the diagnostics library reuses the host helpers of mmk_abi.cu and tma_maps.cu
+    dobjs = [o for o, _ in results[len(srcs):]] + [o for o in objs if o.endswith(("mmk_abi.o", "tma_maps.o"))]
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", DIAG, *dobjs], check=True)
     return LIB
 
 

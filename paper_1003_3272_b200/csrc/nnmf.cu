@@ -427,8 +427,13 @@ struct Ws {
     void* tc;                // tensor-core path scratch (fp32 rank 64 only)
 };
 
-// the tensor-core region is reserved whenever the path could apply
-bool tc_shape(long long m, long long n, int r) { return r == 64 && (n & 3) == 0 && m >= 128 && n >= 128; }
+// the tensor-core region (pre-split X, operand copies) is reserved only for
+// workspaces of a full iteration (iter_a) whose dtype / shape can take the
+// tensor-core path; single ops (update_v/w, objective, gradient) run the SIMT
+// kernels and size their workspace without it (mmk_nnmf_op_ws_bytes)
+bool tc_region(int dtype, long long m, long long n, int r, bool iter) {
+    return iter && mmk_tc::shape_ok(dtype, m, n, r);
+}
 
 Plan make_plan(long long m, long long n, int r) {
     Plan P;
@@ -457,7 +462,7 @@ Plan make_plan(long long m, long long n, int r) {
     return P;
 }
 
-size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws* L) {
+size_t ws_layout(const Plan& P, long long m, long long n, int r, bool tc, void* base, Ws* L) {
     size_t off = 256;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -473,7 +478,7 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, void* base, Ws*
     size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
     size_t o_f = take(sizeof(double) * 4);
     size_t o_wp = take(P.S > 1 ? sizeof(double) * (size_t)P.S * r * (size_t)n : 0);
-    size_t o_tc = take(tc_shape(m, n, r) ? mmk_tc::ws_bytes(m, n) : 0);
+    size_t o_tc = take(tc ? mmk_tc::ws_bytes(m, n) : 0);
     if (base && L) {
         L->tc = reinterpret_cast<char*>(base) + o_tc;
         char* c = reinterpret_cast<char*>(base);
@@ -601,14 +606,15 @@ struct RunA {
     static int run(const Args& a) {
         const Plan P = make_plan(a.m, a.n, a.r);
         Ws L;
-        ws_layout(P, a.m, a.n, a.r, a.ws, &L);
+        const int dt = std::is_same<T, float>::value ? MMK_F32 : MMK_F64;
+        ws_layout(P, a.m, a.n, a.r, tc_region(dt, a.m, a.n, a.r, a.mode == 0), a.ws, &L);
         using KK = K<T, RMAX>;
         const T* X = (const T*)a.X;
         const T* V = (const T*)a.V;
         const T* W = (const T*)a.W;
         const long long rn = (long long)a.r * a.n;
         if constexpr (std::is_same<T, float>::value && RMAX == 64) {
-            if (a.mode == 0 && tc_shape(a.m, a.n, a.r) &&
+            if (a.mode == 0 && tc_region(MMK_F32, a.m, a.n, a.r, true) &&
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
                 return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
                                       a.red, a.st);
@@ -677,7 +683,8 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
     return MMK_OK;
 }
 
-int check(int dtype, long long m, long long n, long long r, long long ldx, size_t ws_bytes) {
+int check(int dtype, long long m, long long n, long long r, long long ldx, size_t ws_bytes,
+          bool iter) {
     if (dtype != MMK_F32 && dtype != MMK_F64) {
         mmk_host::set_error("unknown dtype %d", dtype);
         return MMK_E_SHAPE;
@@ -688,7 +695,8 @@ int check(int dtype, long long m, long long n, long long r, long long ldx, size_
         return MMK_E_SHAPE;
     }
     const Plan P = make_plan(m, n, (int)r);
-    const size_t need = ws_layout(P, m, n, (int)r, nullptr, nullptr);
+    const size_t need = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr,
+                                  nullptr);
     if (ws_bytes < need) {
         mmk_host::set_error("NNMF workspace too small: %zu < %zu", ws_bytes, need);
         return MMK_E_SHAPE;
@@ -705,22 +713,29 @@ int run_a(int dtype, Args a) {
 
 void* mmk_tc::engine_tc_ws(int dtype, const void* X, long long ldx, long long m, long long n,
                           long long r, void* ws) {
-    if (dtype != MMK_F32 || !tc_shape(m, n, (int)r) || !eligible(MMK_F32, m, n, r, ldx, X))
+    if (!tc_region(dtype, m, n, (int)r, true) || !eligible(MMK_F32, m, n, r, ldx, X))
         return nullptr;
     Ws L;
-    ws_layout(make_plan(m, n, (int)r), m, n, (int)r, ws, &L);
+    ws_layout(make_plan(m, n, (int)r), m, n, (int)r, true, ws, &L);
     return L.tc;
 }
 
-extern "C" int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t* out) {
-    (void)dtype;
+static int ws_bytes_for(int dtype, int64_t m, int64_t n, int64_t r, bool iter, size_t* out) {
     if (r < 1 || r > kMaxRank || n < 1) {
         mmk_host::set_error("unsupported NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
     }
     const Plan P = make_plan(m, n, (int)r);
-    *out = ws_layout(P, m, n, (int)r, nullptr, nullptr);
+    *out = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr, nullptr);
     return MMK_OK;
+}
+
+extern "C" int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t* out) {
+    return ws_bytes_for(dtype, m, n, r, true, out);
+}
+
+extern "C" int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t* out) {
+    return ws_bytes_for(dtype, m, n, r, false, out);
 }
 
 extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 1; }
@@ -729,7 +744,7 @@ extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void
                                const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
                                void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
                                void* stream) {
-    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, true);
     if (rc) return rc;
     Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 0};
@@ -763,7 +778,7 @@ extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* 
 extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const void* V,
                                   const void* W, int64_t m, int64_t n, int64_t r, void* ws,
                                   size_t ws_bytes, double* f_dev, int64_t* err_dev, void* stream) {
-    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, nullptr, f_dev, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 2};
@@ -773,7 +788,7 @@ extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const v
 extern "C" int mmk_nnmf_update_v(int dtype, const void* X, int64_t ldx, const void* V,
                                  const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
                                  void* ws, size_t ws_bytes, int64_t* err_dev, void* stream) {
-    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, nullptr, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 1};
@@ -784,7 +799,7 @@ extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const vo
                                  const void* W, void* W_out, int64_t m, int64_t n, int64_t r,
                                  void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
                                  void* stream) {
-    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 3};
@@ -800,7 +815,7 @@ extern "C" int mmk_nnmf_gradient(int dtype, const void* X, int64_t ldx, const vo
                                  const void* W, void* GV, void* GW, int64_t m, int64_t n,
                                  int64_t r, void* ws, size_t ws_bytes, double* red,
                                  int64_t* err_dev, void* stream) {
-    int rc = check(dtype, m, n, r, ldx, ws_bytes);
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Args a{X, V, W, GV, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev, st, 4};

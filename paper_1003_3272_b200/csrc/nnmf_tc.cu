@@ -1,57 +1,61 @@
 // nnmf_tc.cu -- tensor-core (tcgen05, kind::f16) path of the NNMF MM
 // iteration for large fp32 problems with rank 64 (BASELINE config 4).
+// Reference: nnmf_objective / nnmf_update_v / nnmf_update_w (nnmf.py:75-110)
+// and the V-then-W step of _FrobeniusNnmf (nnmf.py:153-156).
 //
-// The two contractions with X are the whole cost (4mnr of
-// 5.5e11 flops).  Both run on the 5th-gen tensor cores as fp32-faithful
-// split products: every fp32 operand x is scaled by a power of two 2^e
-// (exact) so the largest |x 2^e| lies in [2^14, 2^15), then split into two
-// fp16 values hi = rn(x 2^e), lo = rn(x 2^e - hi) -- 22 significant bits.
-// x w ~ hi_x hi_w + hi_x lo_w + lo_x hi_w, accumulated in fp32 in TMEM and
-// scaled back by 2^-(e_x + e_w).  Elements within 2^18 of the scaled maximum
-// keep the full 22 bits; smaller ones lose low bits at an absolute level of
-// max * 2^-40, far below fp32 rounding of the dot products they enter.
+// Split products.  The two contractions with X are the whole cost (SURVEY.md
+// 8(d): 4mnr of 5.5e11 flops).  Both run on the 5th-gen tensor cores as
+// fp32-faithful split products: every fp32 operand x is scaled by a power of
+// two 2^e (exact) so the largest |x 2^e| lies in [2^14, 2^15), then split
+// into two fp16 values hi = rn(x 2^e), lo = rn(x 2^e - hi) -- 22 significant
+// bits.  x w ~ hi_x hi_w + hi_x lo_w + lo_x hi_w, accumulated in fp32 in TMEM
+// and scaled back by 2^-(e_x + e_w) in fp64.  fp16 and not 3xTF32: a
+// single-CTA tcgen05.mma costs ~110-175 cycles per 32 bytes of K of its A
+// operand (measured), so the A bytes per X element set the MMA time; tf32
+// hi + lo are 8 bytes, fp16 hi + lo are 4.
 //
-// Why fp16 and not 3xTF32: a tcgen05.mma with M = 128 costs ~130-170 cycles
-// per 32 bytes of K whatever N is (measured, scripts/mma_bench.py), so the
-// MMA time per X element is set by the bytes of the A operand.  tf32 hi + lo
-// are 8 bytes per element (8 MMAs per 128 x 32 stage, ~900 cycles -- slower
-// than HBM delivers the stage); fp16 hi + lo are 4 bytes (4 MMAs).
+// Pre-split X.  X is constant over a run, so its scaled fp16 hi / lo pair is
+// made ONCE per X (presplit_kernel): row-major for the V step, transposed for
+// the W step (8 bytes per element of X in HBM, 4 of them read per half step,
+// as many as the fp32 X itself).  Both kernels stream [X_hi | X_lo] tiles
+// from TMA straight into SS MMAs.
 //
-//   nnmf_vstep_tc  (persistent, one CTA per SM, 14 warps)
-//     warp 0   TMA producer: X tile [128 rows x 64 cols] fp32 (two 128B-
-//              swizzled boxes) + [W_hi ; W_lo] fp16 chunk [128 x 64] per stage
-//     warps 2-9 split warps: read X rows from smem, release the slot, write
-//              fp16 hi / lo to a TMEM A-buffer (32 + 32 columns); with
-//              pre-split X (below) there is nothing to split and they form
-//              the Gram V'^T V' of each finished V' tile instead
-//     warp 1   one thread issues 4 x (TS MMA hi, N = 128; TS MMA lo, N = 64)
-//              (M128 K16) per stage into an fp32 accumulator Q = X W^T
-//     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300) with the row of
-//              V G_W formed here (fp32), <V, Q> (fp64), max(V') for the
-//              W step's scale
+// Objective.  f(V, W) = sum_ij (x_ij - v_i . w_j)^2 is an EXPLICIT residual
+// (the Gram-trace identity sum x^2 - 2<V, X W^T> +
+// <V^T V, W W^T> cancels catastrophically in fp32 when ||X||^2 / f is large),
+// evaluated inside the V step's X stream with no extra HBM traffic:
+//   * per 128 x 64 X stage the MMA warp also issues R' = V_h [W_hi | W_lo]
+//     (4 MMAs, N = 128, B = the W chunk already in shared memory read as an
+//     MN-major operand), V_h = fp16 of V scaled per row by 2^ev_i;
+//   * eight residual warps read R' from TMEM and the X stage from shared
+//     memory and accumulate F' = sum (x - v_h.w)^2 (fp32 squares of 8 terms
+//     folded into fp64);
+//   * the exact correction for V's rounding E = V - V_h,
+//       f = F' - 2 <(X - V W) W^T, E> - sum_i e_i G_W e_i^T,
+//     comes from the V-update epilogue, which holds Q = X W^T, V G_W and V
+//     for its row: (X - VW)W^T = Q - V G_W.  E is ~2^-12 V, so these terms
+//     are small and well conditioned; F' is a sum of squares (no
+//     cancellation).  tests/test_nnmf_tc_gpu.py checks f against the fp64
+//     residual on well-fit data (||X||^2 / f ~ 1e4).
+//
+//   nnmf_vstep_tc  (persistent, one CTA per SM, 14 warps, one 128-row tile
+//                  per pass, two accumulator sets so pass p's epilogue
+//                  overlaps pass p + 1's MMAs)
+//     warp 0     TMA: V_h tile per pass; per 64-column stage the W chunk
+//                [W_hi ; W_lo] and the X stage [X_hi | X_lo]
+//     warp 1     one thread issues per stage 4 x (SS MMA N = 128 X_hi.[W_hi;
+//                W_lo] + SS MMA N = 64 X_lo.W_hi) into Q, then 4 x SS MMA
+//                N = 128 V_h.[W_hi | W_lo] into the residual buffer
+//     warps 2-9  residual (two groups of 4 alternate stages)
+//     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300), max(V'), the
+//                correction terms above
 //   nnmf_vprep     V' -> V'^T hi / lo fp16 [64][m] (scaled): the W-step B operand
 //   nnmf_wstep_tc  P^T = X^T V' (M = 128 columns of X, N = 64, K = rows),
-//              split-K over row ranges; per-split partials reduced in fixed
-//              order -> deterministic.
-//
-// Objective f(V, W) = sum x^2 - 2 <V, X W^T> + <V^T V, W W^T> in fp64: every
-// term is a by-product of the pass (no extra X traffic).  Its conditioning
-// is ||X||^2 / f times the split-product accumulation error (SURVEY.md
-// 7.3-2); tests/test_nnmf_tc_gpu.py checks it against the explicit residual.
+//                split-K over row ranges; per-split partials reduced in fixed
+//                order -> deterministic.
 //
 // HBM roofline: each kernel streams X once (m n 4 bytes) -> two passes per
-// iteration; tensor work 3 x 2mnr per kernel.
-//
-// Pre-split X (PS, the default while the copy fits, see presplit_on): X is
-// constant over a run, so its fp16 hi / lo pair -- exactly what the split
-// warps compute -- is made ONCE (presplit_kernel, row-major for the V step and
-// transposed for the W step) and the kernels stream [X_hi | X_lo] tiles (the
-// same 4 bytes per element) straight from TMA into SS MMAs: no split warps,
-// no TMEM A buffers, the MMA commit releases the X slot.  Same products from
-// the same values (bitwise-equal traces, tests/test_nnmf_tc_gpu.py); measured
-// 1.39 / 1.29 ms per half step at C4 against 1.51 / 1.45 for the split-warp
-// kernels, i.e. HBM-bound at the power-capped clocks where the split-warp
-// pipeline is MMA-issue bound.
+// iteration; tensor work 3 x 2mnr per kernel plus 2 x 2mnr for R'.
 #include <cuda_fp16.h>
 
 #include "mmk_common.cuh"
@@ -64,38 +68,33 @@ using namespace mmk;
 
 constexpr int R = 64;            // rank of the tensor-core path
 constexpr int BM = 128;          // UMMA M: rows of X (V step) / columns of X (W step)
-constexpr int BK = 64;           // K per stage (fp32 X values; one 128-byte fp16 operand row)
-constexpr int NCONV = 8;         // split warps: groups of 4 take X stages round-robin
-constexpr int NGROUP = NCONV / 4;
-constexpr int kThreads = 32 * (2 + NCONV + 4);   // TMA, MMA, split x8, epilogue x4
-constexpr uint32_t SX = BM * BK * 4;        // 32 KB  fp32 X stage
+constexpr int BK = 64;           // K per stage (one 128-byte fp16 operand row)
+constexpr uint32_t SXH = BM * BK * 2;       // 16 KB  fp16 X tile [128 x 64]
+constexpr uint32_t SX = 2 * SXH;            // 32 KB  X stage [X_hi | X_lo]
 constexpr uint32_t SOP = R * BK * 2;        //  8 KB  fp16 operand chunk hi; same again for lo
-#ifndef MMK_TC_XST
-#define MMK_TC_XST 4
-#endif
+constexpr uint32_t SGW = R * R * 4;         // 16 KB  G_W (fp32) for the V-step epilogue
+constexpr int XST = 4;                      // X ring (128 KB in flight per SM)
 #ifndef MMK_TC_OST
 #define MMK_TC_OST 3
 #endif
-constexpr int XST = MMK_TC_XST;             // X ring (128 KB in flight per SM)
-constexpr int OST = MMK_TC_OST;             // operand ring (3: 2 hold X back, measured)
-// V' tile for the fused Gram (pre-split X): 128 rows x 16 float4, float4 c of
-// row r at slot c ^ (r & 7) (conflict-free row-per-thread writes)
-constexpr uint32_t SGB = BM * R * 4;        // 32 KB
-constexpr uint32_t SGW = R * R * 4;         // 16 KB  G_W (fp32) for the V-step epilogue
-constexpr uint32_t SMEM = XST * SX + OST * 2 * SOP + SGB + SGW + 1024;
-static_assert(SMEM + 2048 <= 232448, "dynamic + static shared memory per CTA");
-constexpr int NA = 4;                       // TMEM A-operand buffers [X_hi | X_lo] (64 cols)
+constexpr int OST = MMK_TC_OST;             // operand ring (V step: one W chunk per X stage,
+                                            // held until the residual MMAs finish)
+constexpr int NRES = 8;                     // residual warps (two groups of 4)
+constexpr int kVThreads = 32 * (2 + NRES + 4);   // TMA, MMA, residual x8, epilogue x4
+constexpr int kWThreads = 32 * (2 + 4);          // TMA, MMA, epilogue x4
+constexpr uint32_t SVH = BM * R * 2;        // 16 KB  V_h tile [128 rows x 64 ranks]
+constexpr uint32_t SMEM_V = XST * SX + OST * 2 * SOP + 2 * SVH + SGW + 1024;
+constexpr int OSTW = 3;                     // W step operand ring (a V'^T chunk feeds CB stages)
+constexpr uint32_t SMEM_W = XST * SX + OSTW * 2 * SOP + 1024;
+static_assert(SMEM_V + 2048 <= 232448, "dynamic + static shared memory per CTA");
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
-constexpr int TMAX = 2;                     // accumulators per pass (V step: row tiles)
 constexpr int CB = 2;                       // W step: 128-column blocks per item
 constexpr int TM_COLS = 512;
-constexpr uint32_t TM_A = TMAX * ACC;       // A buffers after the accumulators
-static_assert(2 * TMAX * ACC <= TM_COLS, "two accumulator sets (pre-split X) must fit in TMEM");
-
-// experiment switches (MMK_TC_DBG, timing studies only; results are wrong
-// when set): 1 skip the lo MMAs, 2 skip the split, 4 skip all MMAs
-__constant__ int c_dbg = 0;
-__constant__ int c_trace_cta = 0;   // CTA whose pipeline the debug trace records
+// V step TMEM: two Q sets [0, 256), two residual buffers [W_hi | W_lo] columns
+constexpr int NRB = 2;
+constexpr uint32_t TM_RES = 2 * ACC;
+static_assert(TM_RES + NRB * ACC <= TM_COLS, "V-step TMEM budget");
+static_assert(2 * CB * ACC <= TM_COLS, "W step: two accumulator sets");
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -120,323 +119,30 @@ __device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint3
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// kind::f16 instruction descriptor: fp16 A/B (K-major), fp32 D
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
-    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::f16 instruction descriptor: fp16 A/B, fp32 D; b_mn = 1 for an
+// MN-major B operand
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn = 0) {
+    return (1u << 4) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
 }
 
-struct Bars {
-    uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST], afull[NA], aempty[NA];
-    uint64_t dfull[2], dempty[2];   // accumulator sets (pre-split X: two, else one)
-    uint64_t gfull, gempty;         // V' tile buffer (V step, pre-split X): epilogue -> Gram warps
-};
-
-// pair: the leader's afull / dempty also count one arrival of the peer CTA;
-// pre-split X: the X slots are released by an MMA commit, not the split warps
-__device__ __forceinline__ void init_bars(Bars& B, bool pair, bool presplit) {
-    const uint32_t two = pair ? 2 : 1;
-    for (int s = 0; s < XST; ++s) {
-        tc::mbar_init(&B.xfull[s], 1);
-        tc::mbar_init(&B.xempty[s], presplit ? 1 : 128);   // split warps / MMA commit
-    }
-    for (int s = 0; s < OST; ++s) {
-        tc::mbar_init(&B.ofull[s], 1);
-        tc::mbar_init(&B.oempty[s], 1);
-    }
-    for (int b = 0; b < NA; ++b) {
-        tc::mbar_init(&B.afull[b], 128 + (two - 1));   // pair: + one arrival from the peer
-        tc::mbar_init(&B.aempty[b], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-        tc::mbar_init(&B.dfull[b], 1);
-        tc::mbar_init(&B.dempty[b], 128 + (two - 1));
-    }
-    tc::mbar_init(&B.gfull, 128);             // the epilogue threads (one row each)
-    tc::mbar_init(&B.gempty, 32 * NCONV);     // the Gram warps
-    tc::fence_barrier_init();
-}
-
-// One stage (K = 64) of the split product, both MMAs with A from TMEM
-// (buffer a = [X_hi | X_lo], 32 + 32 columns of fp16 pairs).  The operand
-// chunk holds [B_hi ; B_lo] stacked along N (64 + 64 rows, K-major fp16): per
-// K16 step a TS MMA with N = 128 gives D[:, 0:64] += X_hi.B_hi and
-// D[:, 64:128] += X_hi.B_lo, and a TS MMA with N = 64 adds X_lo.B_hi into
-// D[:, 0:64].  The epilogue sums the two halves.
-//
-// PAIR (CTA pair, cta_group::2, M = 256): each CTA's TMEM holds its own 128
-// rows of X_hi / X_lo and of D; the operand's N = 128 rows are split between
-// the pair -- B_hi in the leader's stage, B_lo at the same offset in the
-// peer's -- and both MMAs of a K16 step use that B with N = 128: X_hi.[B_hi;B_lo]
-// and X_lo.[B_hi;B_lo].  The second adds X_lo.B_lo to D[:, 64:128], the one
-// product the single-CTA path leaves out (it only makes the sum more exact).
-// A pair MMA runs at the full tensor rate (64 cycles at N = 128, measured)
-// where a single-CTA M = 128 one costs ~175 cycles whatever N is.
-//
-// PS (pre-split X): A comes from shared memory instead -- the X stage holds
-// [X_hi | X_lo] as two 128-row x 64-K fp16 tiles (128B swizzle) loaded by TMA
-// from the pre-split copy of X, so no split warps sit between the load and
-// the MMA (SS MMAs, same products).
-template <bool PAIR, bool PS>
-__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t a, const uint8_t* xs,
-                                            const uint8_t* bhl, bool first) {
+// One 64-column stage of Q += X W^T with A = [X_hi | X_lo] (two 128-row x
+// 64-K fp16 tiles, 128B swizzle) and the operand chunk [B_hi ; B_lo] stacked
+// along N (64 + 64 rows, K-major): per K16 step an SS MMA with N = 128 gives
+// D[:, 0:64] += X_hi.B_hi, D[:, 64:128] += X_hi.B_lo, and one with N = 64
+// adds X_lo.B_hi into D[:, 0:64].  The epilogue sums the two halves.
+__device__ __forceinline__ void issue_split_stage(uint32_t d, const uint8_t* xs,
+                                                  const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
-    const int dbg = c_dbg;
-    if (dbg & 4) return;
-    if constexpr (PS) {
-        const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
-        const uint64_t al = tc::sdesc_sw128(xs + SX / 2, 16, 1024);
-        if constexpr (PAIR) {
-            constexpr uint32_t id = idesc_f16(2 * BM, ACC);
+    const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
+    const uint64_t al = tc::sdesc_sw128(xs + SXH, 16, 1024);
+    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
+    constexpr uint32_t id_lo = idesc_f16(BM, R);
 #pragma unroll
-            for (int ks = 0; ks < BK / 16; ++ks) {
-                const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                tc::mma_f16ss_pair(d, ah + ks * 2, db0 + ks * 2, id, acc);
-                if (!(dbg & 1)) tc::mma_f16ss_pair(d, al + ks * 2, db0 + ks * 2, id, 1);
-            }
-        } else {
-            constexpr uint32_t id_hi = idesc_f16(BM, ACC);
-            constexpr uint32_t id_lo = idesc_f16(BM, R);
-#pragma unroll
-            for (int ks = 0; ks < BK / 16; ++ks) {
-                const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                tc::mma_f16ss(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
-                if (!(dbg & 1)) tc::mma_f16ss(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
-            }
-        }
-    } else if constexpr (PAIR) {
-        constexpr uint32_t id = idesc_f16(2 * BM, ACC);
-#pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks) {
-            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-            tc::mma_f16ts_pair(d, a + ks * 8, db0 + ks * 2, id, acc);
-            if (!(dbg & 1)) tc::mma_f16ts_pair(d, a + 32 + ks * 8, db0 + ks * 2, id, 1);
-        }
-    } else {
-        constexpr uint32_t id_hi = idesc_f16(BM, ACC);
-        constexpr uint32_t id_lo = idesc_f16(BM, R);
-#pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks) {
-            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-            tc::mma_f16ts(d, a + ks * 8, db0 + ks * 2, id_hi, acc);
-            if (!(dbg & 1)) tc::mma_f16ts(d, a + 32 + ks * 8, db0 + ks * 2, id_lo, 1);
-        }
-    }
-}
-
-// Work of one CTA pass: `nacc` accumulators (row tiles or column blocks),
-// `nkb` K-blocks; stage (kb, j) streams X block j of K-block kb while the
-// operand chunk of kb is shared by all j.
-struct Pass {
-    int nacc, nkb;
-};
-
-// The 64 X values of this thread's lane in an X stage, scaled by 2^e:
-// V step (MN = false): row `quarter*32 + lane` of two 128B-swizzled K-major
-// boxes [128 rows x 32 cols]; W step (MN = true): column `lane` of box
-// `quarter` [64 rows x 32 cols] (all 64 rows).
-template <bool MN>
-__device__ __forceinline__ void read_stage(const uint8_t* xs, int quarter, int lane, float sc,
-                                           float* x) {
-    if (!MN) {
-        const int row = quarter * 32 + lane;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float4* rp = reinterpret_cast<const float4*>(xs + h * (BM * 128) + row * 128);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const float4 t = rp[c ^ (row & 7)];
-                x[32 * h + 4 * c] = t.x * sc;
-                x[32 * h + 4 * c + 1] = t.y * sc;
-                x[32 * h + 4 * c + 2] = t.z * sc;
-                x[32 * h + 4 * c + 3] = t.w * sc;
-            }
-        }
-    } else {
-        const uint8_t* bx = xs + quarter * (BK * 128) + (lane & 3) * 4;
-#pragma unroll
-        for (int k = 0; k < BK; ++k)
-            x[k] = *reinterpret_cast<const float*>(bx + k * 128 + (((lane >> 2) ^ (k & 7)) << 4)) *
-                   sc;
-    }
-}
-
-// fp16 hi / lo pairs of the 64 values into TMEM columns [a, a+32) / [a+32, a+64)
-__device__ __forceinline__ void store_hilo(const float* x, uint32_t a_addr) {
-    float hi[32], lo[32];
-#pragma unroll
-    for (int w = 0; w < 32; ++w) {
-        uint32_t h, l;
-        split_pair(x[2 * w], x[2 * w + 1], h, l);
-        hi[w] = __uint_as_float(h);
-        lo[w] = __uint_as_float(l);
-    }
-    tc::tmem_st32(a_addr, hi);
-    tc::tmem_st32(a_addr + 32, lo);
-}
-
-// ---------------------------------------------------------------------------
-// The pipeline shared by both steps.  Role functions get (pass index p, j)
-// and must agree on the iteration order: for p: for kb: [operand], for j: [X].
-// trace (debug): CTA 0 records clock64 per X stage for the first kTrace stages:
-// [0] TMA issued, [1] split start (data landed), [2] split done, [3] MMA
-// start (operands ready), [4] MMAs issued + committed
-constexpr int kTrace = 256;   // slots: 0-4 as above, 5 = operand chunk ready (MMA warp)
-__device__ __forceinline__ void trace_at(unsigned long long* tr, int what, int xit) {
-    if (tr && (int)blockIdx.x == c_trace_cta && xit < kTrace) tr[what * kTrace + xit] = clock64();
-}
-
-// PAIR: the kernel runs as CTA pairs (cluster of 2).  Each CTA streams and
-// splits its own X tiles into its own TMEM and loads its half of the operand
-// chunk (the loader counts both halves on the leader's ofull); only the
-// leader's MMA warp issues (M = 256) and its commits arrive on the barriers of
-// both CTAs (multicast); the peer's split and epilogue warps arrive on the
-// leader's afull / dempty.
-// PS: pre-split X (see issue_stage): the TMA warp loads [X_hi | X_lo] stages
-// that the MMA warp consumes directly (pair: both CTAs' loads are counted on
-// the leader's xfull) and the MMA commit releases the slot; no split warps.
-template <bool MN, bool PAIR, bool PS, class PassOf, class LoadX, class LoadOp, class Epi>
-__device__ __forceinline__ void run_pipeline(uint8_t* base, Bars& B, uint32_t tmem, int npass,
-                                             float xscale, const PassOf& pass_of,
-                                             const LoadX& load_x, const LoadOp& load_op,
-                                             const Epi& epilogue, unsigned long long* tr) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = PAIR ? tc::cluster_rank() : 0u;
-    // accumulator sets: with pre-split X the TMEM A buffers are free, so pass
-    // p + 1 accumulates into the other set while the epilogue drains pass p
-    constexpr int NBUF = PS ? 2 : 1;
-    uint8_t* xring = base;
-    uint8_t* oring = base + XST * SX;
-    // cluster-scope acquire only where another CTA's threads arrive (the
-    // leader's afull / dempty); commit arrivals (aempty, oempty, dfull) and
-    // TMA completions need no more than the CTA-scope wait
-    auto wait = [](uint64_t* bar, uint32_t parity) { tc::mbar_wait(bar, parity); };
-    auto wait_peer = [](uint64_t* bar, uint32_t parity) {
-        if constexpr (PAIR)
-            tc::mbar_wait_cluster(bar, parity);
-        else
-            tc::mbar_wait(bar, parity);
-    };
-    auto arrive_leader = [](uint64_t* bar) {
-        if constexpr (PAIR)
-            tc::mbar_arrive_cluster(tc::map_to_rank(bar, 0));
-        else
-            tc::mbar_arrive(bar);
-    };
-    auto commit = [](uint64_t* bar) {
-        if constexpr (PAIR)
-            tc::mma_commit_pair(bar);
-        else
-            tc::mma_commit(bar);
-    };
-    if (warp == 0) {
-        if (lane == 0) {
-            int xit = 0, oit = 0;
-            for (int p = 0; p < npass; ++p) {
-                const Pass P = pass_of(p);
-                for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
-                    const int os = oit % OST;
-                    wait(&B.oempty[os], ((oit / OST) & 1) ^ 1);
-                    if (rank == 0) tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
-                    load_op(p, kb, oring + os * 2 * SOP, &B.ofull[os]);
-                    for (int j = 0; j < P.nacc; ++j, ++xit) {
-                        const int xs = xit % XST;
-                        tc::mbar_wait(&B.xempty[xs], ((xit / XST) & 1) ^ 1);
-                        if (!(PS && PAIR))
-                            tc::mbar_expect_tx(&B.xfull[xs], SX);
-                        else if (rank == 0)
-                            tc::mbar_expect_tx(&B.xfull[xs], 2 * SX);
-                        load_x(p, kb, j, xring + xs * SX, &B.xfull[xs]);
-                        trace_at(tr, 0, xit);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            int xit = 0, oit = 0;
-            for (int p = 0; p < npass; ++p) {
-                const Pass P = pass_of(p);
-                const int b = p % NBUF;
-                if (p >= NBUF) wait_peer(&B.dempty[b], ((p / NBUF) - 1) & 1);
-                tc::tc_fence_after();
-                for (int kb = 0; kb < P.nkb; ++kb, ++oit) {
-                    const int os = oit % OST;
-                    wait(&B.ofull[os], (oit / OST) & 1);
-                    const uint8_t* ob = oring + os * 2 * SOP;
-                    for (int j = 0; j < P.nacc; ++j, ++xit) {
-                        const int ab = xit % NA, xs = xit % XST;
-                        trace_at(tr, 5, xit);
-                        if constexpr (PS)
-                            wait(&B.xfull[xs], (xit / XST) & 1);
-                        else
-                            wait_peer(&B.afull[ab], (xit / NA) & 1);
-                        trace_at(tr, 3, xit);
-                        tc::tc_fence_after();
-                        issue_stage<PAIR, PS>(tmem + (b * TMAX + j) * ACC, tmem + TM_A + ab * 64,
-                                              xring + xs * SX, ob, kb == 0);
-                        // X slot xs (pre-split) / A buffer ab free once these finish
-                        commit(PS ? &B.xempty[xs] : &B.aempty[ab]);
-                        trace_at(tr, 4, xit);
-                    }
-                    commit(&B.oempty[os]);
-                }
-                commit(&B.dfull[b]);
-            }
-        }
-    } else if (warp < 2 + NCONV) {
-        if constexpr (PS) return;   // pre-split X: nothing to split
-        const int g = (warp - 2) >> 2, quarter = warp & 3;
-        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        int xit = 0;
-        for (int p = 0; p < npass; ++p) {
-            const Pass P = pass_of(p);
-            for (int kb = 0; kb < P.nkb; ++kb) {
-                for (int j = 0; j < P.nacc; ++j, ++xit) {
-                    if (xit % NGROUP != g) continue;
-                    const int xs = xit % XST, ab = xit % NA;
-                    tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
-                    if (quarter == 0 && lane == 0) trace_at(tr, 1, xit);
-                    float x[BK];
-                    read_stage<MN>(xring + xs * SX, quarter, lane, xscale, x);
-                    // the values are in registers (consumed below): release the slot
-                    tc::mbar_arrive(&B.xempty[xs]);
-                    // A buffer ab was last read by the MMAs of stage xit - NA
-                    if (xit >= NA) wait(&B.aempty[ab], ((xit / NA) - 1) & 1);
-                    tc::tc_fence_after();
-                    if (!(c_dbg & 2)) store_hilo(x, tmem + TM_A + ab * 64 + lane_off);
-                    tc::tmem_st_wait();
-                    tc::tc_fence_before();
-                    if (!PAIR || rank == 0) {
-                        tc::mbar_arrive(&B.afull[ab]);
-                    } else {
-                        // the group's 128 threads meet on a named barrier, then
-                        // ONE cluster-scope release arrive on the leader's afull
-                        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-                        if (quarter == 0 && lane == 0) arrive_leader(&B.afull[ab]);
-                    }
-                    if (quarter == 0 && lane == 0) trace_at(tr, 2, xit);
-                }
-            }
-        }
-    } else {
-        const int quarter = warp & 3;
-        for (int p = 0; p < npass; ++p) {
-            const Pass P = pass_of(p);
-            const int b = p % NBUF;
-            wait(&B.dfull[b], (p / NBUF) & 1);
-            tc::tc_fence_after();
-            for (int j = 0; j < P.nacc; ++j)
-                epilogue(p, j, quarter, lane,
-                         tmem + (b * TMAX + j) * ACC + ((uint32_t)(quarter * 32) << 16),
-                         P.nkb > 0);
-            tc::tc_fence_before();
-            if (!PAIR || rank == 0) {
-                tc::mbar_arrive(&B.dempty[b]);
-            } else {
-                asm volatile("bar.sync 3, 128;" ::: "memory");
-                if (quarter == 0 && lane == 0) arrive_leader(&B.dempty[b]);
-            }
-        }
+    for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+        tc::mma_f16ss(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
+        tc::mma_f16ss(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
     }
 }
 
@@ -448,361 +154,498 @@ struct Scales {
 };
 
 // ---------------------------------------------------------------------------
-// PAIR: launched as clusters of 2 (CTA pairs); pair q takes the 256-row
-// units q, q + G/2, ... and CTA rank r of the pair their 128-row half r.
-// PS: mX / mX2 are the fp16 hi / lo maps of the pre-split X (m x n).
-template <bool PAIR, bool PS>
-__global__ void __launch_bounds__(kThreads, 1)
+// V step.  mX / mX2: fp16 hi / lo maps of the pre-split X (m x n); mWh / mWl:
+// W_hi / W_lo (64 x n).  part[b] = this CTA's share of f(V, W); the V'
+// maximum goes to sc->vmax_bits.
+//
+// Pipeline per 64-column stage `it` of a 128-row tile (pass p = tile):
+//   TMA      V_h tile of the pass (split_v_kernel's fp16 V, per-row scale);
+//            per stage the W chunk [W_hi ; W_lo] -> operand slot it % OST and
+//            the X stage [X_hi | X_lo] -> slot it % XST
+//   MMA      Q(it) += X_hi [W_hi ; W_lo] + X_lo W_hi (8 SS MMAs), commit ->
+//            xempty; R'(it) = V_h [W_hi | W_lo] (4 SS MMAs N = 128, B = the W
+//            chunk read MN-major: rows = ranks = K, W_hi and W_lo two 64-column
+//            atoms), commit -> rfull, oempty
+//   residual group (it % 2) reads its rows of X(it) into registers as soon
+//            as the stage lands (release -> xempty), then R'(it) from TMEM
+//   epilogue V' of the tile from Q (two accumulator sets: pass p's epilogue
+//            overlaps pass p + 1)
+// A single-CTA M = 128 MMA costs ~60-150 cycles whatever N is (measured), so
+// the 12 MMAs of a stage make this kernel tensor-issue bound (~1.75 ms at C4,
+// against ~1.3 ms for the 8 Q MMAs alone); DESIGN.md has the measurements.
+struct VBars {
+    uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST];
+    uint64_t vfull[2], vempty[2];       // V_h tiles of a pass (TMA -> MMA)
+    uint64_t dfull[2], dempty[2];       // Q accumulator sets: MMA -> epilogue
+    uint64_t rfull[NRB], rempty[NRB];   // residual buffers: MMA -> residual warps
+};
+
+// per-row exponent of V_h: max_k |v_ik| * 2^ev in [2^14, 2^15)
+__device__ __forceinline__ int row_exp(const float4* vr) {
+    float mx = 0.f;
+#pragma unroll
+    for (int l4 = 0; l4 < R / 4; ++l4) {
+        const float4 v = vr[l4];
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    return scale_exp(mx);
+}
+
+__global__ void __launch_bounds__(kVThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
-              const __grid_constant__ CUtensorMap mWh,
-              const __grid_constant__ CUtensorMap mWl, const float* __restrict__ V,
+              const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
+              const __grid_constant__ CUtensorMap mVh, const float* __restrict__ V,
               const float* __restrict__ GWf, float* __restrict__ Vout, Scales* sc, int m, int n,
-              double* __restrict__ part, double* __restrict__ gpart, unsigned long long* tr) {
+              double* __restrict__ part) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
-    __shared__ Bars B;
+    uint8_t* xring = base;
+    uint8_t* oring = base + XST * SX;
+    uint8_t* vbuf = oring + OST * 2 * SOP;
+    float* gws = reinterpret_cast<float*>(vbuf + 2 * SVH);
+    __shared__ VBars B;
     __shared__ uint32_t tmem_base;
-    __shared__ double red[kThreads / 32];
-    __shared__ float vmx[kThreads / 32];
+    __shared__ double red[kVThreads / 32];
+    __shared__ float vmx[kVThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
-    const int rank = PAIR ? (int)tc::cluster_rank() : 0;
-    const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
-    const int me = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
-    const int units = PAIR ? (ntiles + 1) / 2 : ntiles;
-    const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
-    const int npass = (mine + TMAX - 1) / TMAX;
-    // GWf: G_W rounded to fp32 (gram_sum_kernel), staged in smem for the
-    // epilogue's denominator rows (V G_W)_i
-    float4* gbuf = reinterpret_cast<float4*>(base + XST * SX + OST * 2 * SOP);
-    float* gws = reinterpret_cast<float*>(base + XST * SX + OST * 2 * SOP + SGB);
-    for (int i = threadIdx.x; i < R * R / 4; i += kThreads)
+    const int G = (int)gridDim.x, me = (int)blockIdx.x;
+    const int mine = ntiles > me ? (ntiles - 1 - me) / G + 1 : 0;
+    // G_W rounded to fp32 (gram_sum_kernel), staged for the denominator rows
+    for (int i = threadIdx.x; i < R * R / 4; i += kVThreads)
         reinterpret_cast<float4*>(gws)[i] = __ldg(reinterpret_cast<const float4*>(GWf) + i);
     if (threadIdx.x == 0) {
-        init_bars(B, PAIR, PS);
+        for (int s = 0; s < XST; ++s) {
+            tc::mbar_init(&B.xfull[s], 1);
+            tc::mbar_init(&B.xempty[s], 5);   // the residual group's 4 warps + the Q MMAs' commit
+        }
+        for (int s = 0; s < OST; ++s) {
+            tc::mbar_init(&B.ofull[s], 1);
+            tc::mbar_init(&B.oempty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&B.vfull[b], 1);
+            tc::mbar_init(&B.vempty[b], 1);
+            tc::mbar_init(&B.dfull[b], 1);
+            tc::mbar_init(&B.dempty[b], 4);   // epilogue warps
+        }
+        for (int b = 0; b < NRB; ++b) {
+            tc::mbar_init(&B.rfull[b], 1);
+            tc::mbar_init(&B.rempty[b], 4);   // the residual group that read it
+        }
+        tc::fence_barrier_init();
         tc::tma_prefetch(&mX);
-        if (PS) tc::tma_prefetch(&mX2);
+        tc::tma_prefetch(&mX2);
         tc::tma_prefetch(&mWh);
         tc::tma_prefetch(&mWl);
+        tc::tma_prefetch(&mVh);
     }
-    if (warp == 1) {
-        if constexpr (PAIR)
-            tc::tmem_alloc_pair<TM_COLS>(&tmem_base);
-        else
-            tc::tmem_alloc<TM_COLS>(&tmem_base);
-    }
+    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
-    if constexpr (PAIR) tc::cluster_sync();   // barriers initialised, TMEM allocated in both
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
-    const float xscale = exp2f((float)sc->ex);
-    const double qscale = exp2(-(double)(sc->ex + sc->ew));
-    double acc = 0.0, gacc = 0.0;
+    double acc = 0.0;   // residual warps: F'; epilogue warps: the correction terms
     float vmax = 0.f;
-    auto tile_of = [&](int p, int j) {
-        const int u = me + (p * TMAX + j) * G;
-        return PAIR ? 2 * u + rank : u;
-    };
-    auto pass_of = [&](int p) {
-        const int left = mine - p * TMAX;
-        return Pass{left < TMAX ? left : TMAX, nk};
-    };
-    auto load_op = [&](int, int kb, uint8_t* dst, uint64_t* bar) {
-        if constexpr (PAIR) {   // this CTA's half of [W_hi; W_lo], counted on the leader
-            tc::tma_load_2d_pair(dst, rank == 0 ? &mWh : &mWl, tc::map_to_rank(bar, 0), kb * BK, 0);
-        } else {
-            tc::tma_load_2d(dst, &mWh, bar, kb * BK, 0);
-            tc::tma_load_2d(dst + SOP, &mWl, bar, kb * BK, 0);
-        }
-    };
-    auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
-        if constexpr (PS && PAIR) {
-            const uint32_t lb = tc::map_to_rank(bar, 0);
-            tc::tma_load_2d_pair(dst, &mX, lb, kb * BK, tile_of(p, j) * BM);
-            tc::tma_load_2d_pair(dst + SX / 2, &mX2, lb, kb * BK, tile_of(p, j) * BM);
-        } else if constexpr (PS) {
-            tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
-            tc::tma_load_2d(dst + SX / 2, &mX2, bar, kb * BK, tile_of(p, j) * BM);
-        } else {
-            tc::tma_load_2d(dst, &mX, bar, kb * BK, tile_of(p, j) * BM);
-            tc::tma_load_2d(dst + BM * 128, &mX, bar, kb * BK + 32, tile_of(p, j) * BM);
-        }
-    };
-    // PS: the epilogue also copies the V' tile into gbuf, where the (otherwise
-    // idle) split warps form its Gram V'^T V' -- no separate pass over V'
-    auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool) {
-        const long long row = (long long)tile_of(p, j) * BM + quarter * 32 + ln;
-        const int git = p * TMAX + j;   // this CTA's tile sequence number
-        const int grr = quarter * 32 + ln;
-        float4* grow = gbuf + grr * (R / 4);
-        if (PS && git > 0) tc::mbar_wait(&B.gempty, (git - 1) & 1);
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            float q[32], q2[32];
-            tc::tmem_ld32(ta + h * 32, q);
-            tc::tmem_ld32(ta + R + h * 32, q2);
-            if (row >= m) {
-                if (PS) {   // rows past m count as zero in the Gram
-#pragma unroll
-                    for (int k4 = 0; k4 < 8; ++k4)
-                        grow[(h * 8 + k4) ^ (grr & 7)] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (warp == 0) {
+        if (lane == 0) {   // TMA producer
+            int it = 0;
+            for (int p = 0; p < mine; ++p) {
+                const int tile = me + p * G, vb = p & 1;
+                tc::mbar_wait(&B.vempty[vb], ((p >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&B.vfull[vb], SVH);
+                tc::tma_load_2d(vbuf + vb * SVH, &mVh, &B.vfull[vb], 0, tile * BM);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int os = it % OST, xs = it % XST;
+                    tc::mbar_wait(&B.oempty[os], ((it / OST) & 1) ^ 1);
+                    tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                    tc::tma_load_2d(oring + os * 2 * SOP, &mWh, &B.ofull[os], kb * BK, 0);
+                    tc::tma_load_2d(oring + os * 2 * SOP + SOP, &mWl, &B.ofull[os], kb * BK, 0);
+                    tc::mbar_wait(&B.xempty[xs], ((it / XST) & 1) ^ 1);
+                    tc::mbar_expect_tx(&B.xfull[xs], SX);
+                    tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], kb * BK, tile * BM);
+                    tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], kb * BK, tile * BM);
                 }
-                continue;
             }
-            const float4* v4 = reinterpret_cast<const float4*>(V + row * R + h * 32);
-            const float4* vr = reinterpret_cast<const float4*>(V + row * R);
-            float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // MMA issuer
+            constexpr uint32_t id_res = idesc_f16(BM, ACC, 1);
+            int it = 0;
+            for (int p = 0; p < mine; ++p) {
+                const int b = p & 1;
+                tc::mbar_wait(&B.dempty[b], ((p >> 1) & 1) ^ 1);
+                tc::mbar_wait(&B.vfull[b], (p >> 1) & 1);
+                tc::tc_fence_after();
+                const uint64_t va = tc::sdesc_sw128(vbuf + b * SVH, 16, 1024);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int os = it % OST, xs = it % XST, rb = it % NRB;
+                    tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
+                    tc::mbar_wait(&B.xfull[xs], (it / XST) & 1);
+                    tc::tc_fence_after();
+                    const uint8_t* ob = oring + os * 2 * SOP;
+                    issue_split_stage(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                    tc::mma_commit(&B.xempty[xs]);
+                    tc::mbar_wait(&B.rempty[rb], ((it / NRB) & 1) ^ 1);
+                    tc::tc_fence_after();
+                    const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major, 2 atoms
+                    const uint32_t dr = tmem + TM_RES + rb * ACC;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                // denominator columns h*32 + hh*16 .. +16 of this row: (V G_W) in
-                // fp32, l ascending (the row is this thread's: no separate pass)
-                float den[16];
+                    for (int ks = 0; ks < R / 16; ++ks)
+                        tc::mma_f16ss(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res, ks ? 1u : 0u);
+                    tc::mma_commit(&B.rfull[rb]);
+                    tc::mma_commit(&B.oempty[os]);
+                }
+                tc::mma_commit(&B.dfull[b]);
+                tc::mma_commit(&B.vempty[b]);
+            }
+        }
+    } else if (warp < 2 + NRES) {
+        // residual group g takes the stages with it % 2 == g; thread = row
+        // `quarter * 32 + lane` of the tile.  X-scaled units: d 2^ex = x_s -
+        // R' 2^(ex - ev_i - ew) (powers of two, exact), squares of 16 terms in
+        // fp32 (packed fp32x2) folded into fp64, times 2^-2ex at the end
+        const int g = (warp - 2) >> 2, quarter = warp & 3, r = quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const int ex = sc->ex, ew = sc->ew;
+        int it = 0;
+        for (int p = 0; p < mine; ++p) {
+            const long long row = (long long)(me + p * G) * BM + r;
+            int ke = ex - (row < m ? row_exp(reinterpret_cast<const float4*>(V + row * R)) : 0) - ew;
+            ke = ke < -126 ? -126 : (ke > 127 ? 127 : ke);
+            const float nk2 = -exp2f((float)ke);
+            const float2 nkk = make_float2(nk2, nk2);
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                if ((it & 1) != g) continue;
+                // this row's 64 X values of the stage into registers, then release
+                // the slot (its other user is the Q MMA, which commits on xempty)
+                const int xs = it % XST, rb = it % NRB;
+                tc::mbar_wait(&B.xfull[xs], (it / XST) & 1);
+                const uint32_t xh = tc::smem_u32(xring + xs * SX) + r * 128;
+                uint4 hv[8], lv[8];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) den[c] = 0.f;
-#pragma unroll 2
-                for (int l4 = 0; l4 < R / 4; ++l4) {
-                    const float4 vv = vr[l4];
-                    const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+                for (int cc = 0; cc < 8; ++cc) {
+                    hv[cc] = tc::lds128(xh + ((cc ^ (r & 7)) * 16));
+                    lv[cc] = tc::lds128(xh + SXH + ((cc ^ (r & 7)) * 16));
+                }
+                // the slot's next writer is the TMA (async proxy): order these
+                // generic-proxy reads before it
+                tc::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&B.xempty[xs]);
+                tc::mbar_wait(&B.rfull[rb], (it / NRB) & 1);
+                tc::tc_fence_after();
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float4* g4 = reinterpret_cast<const float4*>(
-                            gws + (4 * l4 + e) * R + h * 32 + hh * 16);
+                for (int q = 0; q < 4; ++q) {   // 16 columns at a time
+                    float dh[16], dl[16];
+                    tc::tmem_ld16x2(tmem + TM_RES + rb * ACC + q * 16 + lane_off,
+                                    tmem + TM_RES + rb * ACC + R + q * 16 + lane_off, dh, dl);
+                    float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-                        for (int c4 = 0; c4 < 4; ++c4) {
-                            const float4 g = g4[c4];
-                            den[4 * c4] = fmaf(va[e], g.x, den[4 * c4]);
-                            den[4 * c4 + 1] = fmaf(va[e], g.y, den[4 * c4 + 1]);
-                            den[4 * c4 + 2] = fmaf(va[e], g.z, den[4 * c4 + 2]);
-                            den[4 * c4 + 3] = fmaf(va[e], g.w, den[4 * c4 + 3]);
+                    for (int half = 0; half < 2; ++half) {
+                        const uint4 hq = hv[2 * q + half], lq = lv[2 * q + half];
+                        const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
+                        const uint32_t lw[4] = {lq.x, lq.y, lq.z, lq.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int k = half * 8 + 2 * e;
+                            const float2 xs2 = __fadd2_rn(
+                                __half22float2(*reinterpret_cast<const __half2*>(&hw[e])),
+                                __half22float2(*reinterpret_cast<const __half2*>(&lw[e])));
+                            const float2 rr = __fadd2_rn(make_float2(dh[k], dh[k + 1]),
+                                                         make_float2(dl[k], dl[k + 1]));
+                            const float2 d = __ffma2_rn(rr, nkk, xs2);
+                            s2 = __ffma2_rn(d, d, s2);
                         }
                     }
+                    acc += (double)(s2.x + s2.y);
                 }
-#pragma unroll
-                for (int kq = 0; kq < 4; ++kq) {
-                    const int k4 = hh * 4 + kq;
-                    const float4 vv = v4[k4];
-                    const float va[4] = {vv.x, vv.y, vv.z, vv.w};
-                    const float da[4] = {den[4 * kq], den[4 * kq + 1], den[4 * kq + 2],
-                                         den[4 * kq + 3]};
-                    float nv[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double vk = (double)va[i];
-                        const double qk = ((double)q[4 * k4 + i] + (double)q2[4 * k4 + i]) * qscale;
-                        acc = fma(vk, qk, acc);
-                        gacc = fma(vk, (double)da[i], gacc);   // <V, V G_W> = <V^T V, G_W>
-                        nv[i] = (float)(vk * (qk / ((double)da[i] + kDenomGuard)));
-                        vmax = fmaxf(vmax, nv[i]);
-                    }
-                    o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
-                    if (PS) grow[(h * 8 + k4) ^ (grr & 7)] = make_float4(nv[0], nv[1], nv[2], nv[3]);
-                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&B.rempty[rb]);
             }
         }
-        if (PS) tc::mbar_arrive(&B.gfull);   // release: this row of gbuf is written
-    };
-    run_pipeline<false, PAIR, PS>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
-                              tr);
-    if constexpr (PS) {
-        // Gram warps (the split warps, idle with pre-split X): thread t owns the
-        // 4 x 4 block (4 (t / 16), 4 (t % 16)) of V'^T V' over this CTA's tiles;
-        // fp32 products summed 8 rows at a time, folded into fp64 (as gram32)
-        if (warp >= 2 && warp < 2 + NCONV) {
-            const int t = threadIdx.x - 64, ka = 4 * (t >> 4), kb = 4 * (t & 15);
-            double g[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) g[i][q] = 0.0;
-            for (int it = 0; it < mine; ++it) {
-                tc::mbar_wait(&B.gfull, it & 1);
+        acc *= exp2(-2.0 * ex);
+    } else {
+        // epilogue: thread = row.  V' = V Q / (V G_W + 1e-300) with the row
+        // of V G_W formed here (fp32, l ascending), plus the correction terms
+        // -2 (Q - V G_W)_ik e_ik - e_ik (e G_W)_ik of f (fp64)
+        const int quarter = warp & 3;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const double qscale = exp2(-(double)(sc->ex + sc->ew));
+        const uint32_t gws_s = tc::smem_u32(gws);
+        auto row_of = [&](int p) { return (long long)(me + p * G) * BM + quarter * 32 + lane; };
+        for (int p = 0; p < mine; ++p) {
+            const int b = p & 1;
+            tc::mbar_wait(&B.dfull[b], (p >> 1) & 1);
+            tc::tc_fence_after();
+            const long long row = row_of(p);
+            const uint32_t ta = tmem + b * ACC + lane_off;
+            const float4* vr = reinterpret_cast<const float4*>(V + (row < m ? row : 0) * R);
+            const int ev = row < m ? row_exp(vr) : 0;
+            const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
 #pragma unroll 1
-                for (int r0 = 0; r0 < BM; r0 += 8) {
-                    float pr[4][4];
+            for (int h = 0; h < 2; ++h) {
+                float q[32], q2[32];
+                tc::tmem_ld32(ta + h * 32, q);   // warp-collective: before the row guard
+                tc::tmem_ld32(ta + R + h * 32, q2);
+                if (row >= m) continue;
+                float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                for (int hh = 0; hh < 4; ++hh) {
+                    // columns h*32 + hh*8 .. +8: (V G_W) and (E G_W) in fp32
+                    float den[8], eg[8];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) pr[i][q] = 0.f;
+                    for (int c = 0; c < 8; ++c) den[c] = eg[c] = 0.f;
+#pragma unroll 2
+                    for (int l4 = 0; l4 < R / 4; ++l4) {
+                        const float4 vv = vr[l4];
+                        const float va[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-                    for (int r = r0; r < r0 + 8; ++r) {
-                        const float4 a = gbuf[r * (R / 4) + ((ka >> 2) ^ (r & 7))];
-                        const float4 b = gbuf[r * (R / 4) + ((kb >> 2) ^ (r & 7))];
-                        const float av[4] = {a.x, a.y, a.z, a.w};
-                        const float bv[4] = {b.x, b.y, b.z, b.w};
+                        for (int e = 0; e < 4; ++e) {
+                            const float el = va[e] - __half2float(__float2half_rn(va[e] * vs)) * vsi;
+                            const uint32_t g4 =
+                                gws_s + 4u * (uint32_t)((4 * l4 + e) * R + h * 32 + hh * 8);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) pr[i][q] = fmaf(av[i], bv[q], pr[i][q]);
+                            for (int c4 = 0; c4 < 2; ++c4) {
+                                const float4 gg = tc::lds128f(g4 + 16u * c4);
+                                den[4 * c4] = fmaf(va[e], gg.x, den[4 * c4]);
+                                den[4 * c4 + 1] = fmaf(va[e], gg.y, den[4 * c4 + 1]);
+                                den[4 * c4 + 2] = fmaf(va[e], gg.z, den[4 * c4 + 2]);
+                                den[4 * c4 + 3] = fmaf(va[e], gg.w, den[4 * c4 + 3]);
+                                eg[4 * c4] = fmaf(el, gg.x, eg[4 * c4]);
+                                eg[4 * c4 + 1] = fmaf(el, gg.y, eg[4 * c4 + 1]);
+                                eg[4 * c4 + 2] = fmaf(el, gg.z, eg[4 * c4 + 2]);
+                                eg[4 * c4 + 3] = fmaf(el, gg.w, eg[4 * c4 + 3]);
+                            }
+                        }
                     }
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int kq = 0; kq < 2; ++kq) {
+                        const int k4 = h * 8 + hh * 2 + kq;   // float4 index in the row
+                        const float4 vv = vr[k4];
+                        const float va[4] = {vv.x, vv.y, vv.z, vv.w};
+                        float nv[4];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) g[i][q] += (double)pr[i][q];
+                        for (int i = 0; i < 4; ++i) {
+                            const int c = 4 * kq + i, kk = hh * 8 + c;   // column within the half
+                            const double vk = (double)va[i];
+                            const double qk = ((double)q[kk] + (double)q2[kk]) * qscale;
+                            const double dk = (double)den[c];
+                            const double ek =
+                                (double)(va[i] - __half2float(__float2half_rn(va[i] * vs)) * vsi);
+                            acc = fma(-2.0 * (qk - dk), ek, acc);
+                            acc = fma(-ek, (double)eg[c], acc);
+                            nv[i] = (float)(vk * (qk / (dk + kDenomGuard)));
+                            vmax = fmaxf(vmax, nv[i]);
+                        }
+                        o[hh * 2 + kq] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+                    }
                 }
-                tc::mbar_arrive(&B.gempty);
             }
-            double* pb = gpart + (long long)blockIdx.x * (R * R);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) pb[(ka + i) * R + kb + q] = g[i][q];
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&B.dempty[b]);
         }
     }
-    // per-CTA partials <V, Q>, <V, V G_W> and max(V') (epilogue warps)
-    __shared__ double gred[kThreads / 32];
+    // per-CTA share of f (residual + correction terms, fixed warp order) and max(V')
     acc = warp_sum(acc);
-    gacc = warp_sum(gacc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     if (lane == 0) {
         red[warp] = acc;
-        gred[warp] = gacc;
         vmx[warp] = vmax;
     }
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        double c = 0.0, gg = 0.0;
+        double c = 0.0;
         float mx = 0.f;
-        for (int w = 2 + NCONV; w < kThreads / 32; ++w) {
+        for (int w = 2; w < kVThreads / 32; ++w) {
             c += red[w];
-            gg += gred[w];
             mx = fmaxf(mx, vmx[w]);
         }
         part[blockIdx.x] = c;
-        part[gridDim.x + blockIdx.x] = gg;
         atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
     }
-    if constexpr (PAIR) {
-        tc::tc_fence_before();
-        tc::cluster_sync();   // both CTAs done with the pair's TMEM
-        if (warp == 1) tc::tmem_free_pair<TM_COLS>(tmem);
-    } else {
-        if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
-    }
+    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+}
+
+// V (m x 64 fp32) -> V_h = rn(V_i 2^ev_i) fp16 row-major (the A operand of
+// the residual MMAs), ev_i = scale_exp(max_k |v_ik|); 16 threads per row
+__global__ void __launch_bounds__(256)
+split_v_kernel(const float* __restrict__ V, __half* __restrict__ Vh, long long m) {
+    const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
+    const long long row = t >> 4;
+    const int c4 = (int)(t & 15);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < m) v = reinterpret_cast<const float4*>(V + row * R)[c4];
+    float mx = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (row >= m) return;
+    const float s = exp2f((float)scale_exp(mx));
+    const __half2 a = __floats2half2_rn(v.x * s, v.y * s);
+    const __half2 b = __floats2half2_rn(v.z * s, v.w * s);
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&a);
+    o.y = *reinterpret_cast<const uint32_t*>(&b);
+    reinterpret_cast<uint2*>(Vh + row * R)[c4] = o;
 }
 
 // ---------------------------------------------------------------------------
-// P^T partials: item (row split s, column super-block cs of CB x 128 columns)
-// D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; V'^T chunks (fp16
-// hi / lo, K-major along rows) are shared by the CB column blocks of an item.
-// X tiles arrive as 4 boxes of [64 rows x 32 columns] (128B swizzle); split
-// thread `lane` of warp quarter q owns column 32 q + lane of the block.
-// PAIR: clusters of 2; an item covers 2 CB column blocks, CTA rank r takes
-// blocks 2 j + r of it.
-// PS: mX / mX2 are the fp16 hi / lo maps of the pre-split X^T (n x m).
-template <bool PAIR, bool PS>
-__global__ void __launch_bounds__(kThreads, 1)
+// W step.  P^T partials: item (row split s, column super-block cs of CB x 128
+// columns) D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; the V'^T chunk
+// (fp16 hi / lo, K-major along rows) is shared by the CB column blocks of an
+// item.  mX / mX2: fp16 hi / lo maps of the pre-split X^T (n x m).
+struct WBars {
+    uint64_t xfull[XST], xempty[XST], ofull[OSTW], oempty[OSTW];
+    uint64_t dfull[2], dempty[2];
+};
+
+__global__ void __launch_bounds__(kWThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
-              const __grid_constant__ CUtensorMap mVh,
-              const __grid_constant__ CUtensorMap mVl, const Scales* sc, int m, int n,
-              int splits, int rows_per_split, float* __restrict__ wpart, unsigned long long* tr) {
+              const __grid_constant__ CUtensorMap mVh, const __grid_constant__ CUtensorMap mVl,
+              int m, int n, int splits, int rows_per_split, float* __restrict__ wpart) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
-    __shared__ Bars B;
+    uint8_t* xring = base;
+    uint8_t* oring = base + XST * SX;
+    __shared__ WBars B;
     __shared__ uint32_t tmem_base;
-    const int warp = threadIdx.x >> 5;
-    const int rank = PAIR ? (int)tc::cluster_rank() : 0;
-    const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
-    const int me = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
-    const int span = PAIR ? 2 * CB : CB;   // column blocks per item
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = (int)gridDim.x, me = (int)blockIdx.x;
     const int ncb = (n + BM - 1) / BM;
-    const int ncs = (ncb + span - 1) / span;
+    const int ncs = (ncb + CB - 1) / CB;
     const int nitems = ncs * splits;
     const int npass = nitems > me ? (nitems - 1 - me) / G + 1 : 0;
     if (threadIdx.x == 0) {
-        init_bars(B, PAIR, PS);
+        for (int s = 0; s < XST; ++s) {
+            tc::mbar_init(&B.xfull[s], 1);
+            tc::mbar_init(&B.xempty[s], 1);   // MMA commit
+        }
+        for (int s = 0; s < OSTW; ++s) {
+            tc::mbar_init(&B.ofull[s], 1);
+            tc::mbar_init(&B.oempty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&B.dfull[b], 1);
+            tc::mbar_init(&B.dempty[b], 4);
+        }
+        tc::fence_barrier_init();
         tc::tma_prefetch(&mX);
-        if (PS) tc::tma_prefetch(&mX2);
+        tc::tma_prefetch(&mX2);
         tc::tma_prefetch(&mVh);
         tc::tma_prefetch(&mVl);
     }
-    if (warp == 1) {
-        if constexpr (PAIR)
-            tc::tmem_alloc_pair<TM_COLS>(&tmem_base);
-        else
-            tc::tmem_alloc<TM_COLS>(&tmem_base);
-    }
+    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
     tc::tc_fence_before();
     __syncthreads();
-    if constexpr (PAIR) tc::cluster_sync();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
-    const float xscale = exp2f((float)sc->ex);
-    auto item_of = [&](int p) { return me + p * G; };
-    auto block_of = [&](int item, int j) {
-        return (item % ncs) * span + (PAIR ? 2 * j + rank : j);
-    };
-    auto pass_of = [&](int p) {
-        const int item = item_of(p), s = item / ncs, cs = item % ncs;
-        const int r0 = s * rows_per_split;
+    // pass p = item me + p G: (number of column blocks, K-blocks of rows, first row)
+    auto pass_of = [&](int p, int& nacc, int& nkb, int& r0) {
+        const int item = me + p * G, s = item / ncs, cs = item % ncs;
+        r0 = s * rows_per_split;
         int r1 = r0 + rows_per_split;
         if (r1 > m) r1 = m;
-        int left = ncb - cs * span;
-        if (PAIR) left = (left + 1) / 2;   // the leader's share (the peer's may be one less)
-        return Pass{left < CB ? left : CB, r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0};
+        const int left = ncb - cs * CB;
+        nacc = left < CB ? left : CB;
+        nkb = r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0;
     };
-    auto load_op = [&](int p, int kb, uint8_t* dst, uint64_t* bar) {
-        const int row = (item_of(p) / ncs) * rows_per_split + kb * BK;
-        if constexpr (PAIR) {
-            tc::tma_load_2d_pair(dst, rank == 0 ? &mVh : &mVl, tc::map_to_rank(bar, 0), row, 0);
-        } else {
-            tc::tma_load_2d(dst, &mVh, bar, row, 0);
-            tc::tma_load_2d(dst + SOP, &mVl, bar, row, 0);
+    if (warp == 0) {
+        if (lane == 0) {   // TMA producer
+            int xit = 0, oit = 0;
+            for (int p = 0; p < npass; ++p) {
+                int nacc, nkb, r0;
+                pass_of(p, nacc, nkb, r0);
+                const int col0 = ((me + p * G) % ncs) * CB * BM;
+                for (int kb = 0; kb < nkb; ++kb, ++oit) {
+                    const int os = oit % OSTW;
+                    tc::mbar_wait(&B.oempty[os], ((oit / OSTW) & 1) ^ 1);
+                    tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                    tc::tma_load_2d(oring + os * 2 * SOP, &mVh, &B.ofull[os], r0 + kb * BK, 0);
+                    tc::tma_load_2d(oring + os * 2 * SOP + SOP, &mVl, &B.ofull[os], r0 + kb * BK, 0);
+                    for (int j = 0; j < nacc; ++j, ++xit) {
+                        const int xs = xit % XST;
+                        tc::mbar_wait(&B.xempty[xs], ((xit / XST) & 1) ^ 1);
+                        tc::mbar_expect_tx(&B.xfull[xs], SX);
+                        tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], r0 + kb * BK,
+                                        col0 + j * BM);
+                        tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], r0 + kb * BK,
+                                        col0 + j * BM);
+                    }
+                }
+            }
         }
-    };
-    auto load_x = [&](int p, int kb, int j, uint8_t* dst, uint64_t* bar) {
-        const int item = item_of(p);
-        const int row = (item / ncs) * rows_per_split + kb * BK;
-        const int col0 = block_of(item, j) * BM;
-        if constexpr (PS && PAIR) {
-            const uint32_t lb = tc::map_to_rank(bar, 0);
-            tc::tma_load_2d_pair(dst, &mX, lb, row, col0);
-            tc::tma_load_2d_pair(dst + SX / 2, &mX2, lb, row, col0);
-        } else if constexpr (PS) {
-            tc::tma_load_2d(dst, &mX, bar, row, col0);
-            tc::tma_load_2d(dst + SX / 2, &mX2, bar, row, col0);
-        } else {
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-                tc::tma_load_2d(dst + jj * (BK * 128), &mX, bar, col0 + 32 * jj, row);
+    } else if (warp == 1) {
+        if (lane == 0) {   // MMA issuer
+            int xit = 0, oit = 0;
+            for (int p = 0; p < npass; ++p) {
+                int nacc, nkb, r0;
+                pass_of(p, nacc, nkb, r0);
+                const int b = p & 1;
+                tc::mbar_wait(&B.dempty[b], ((p >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++oit) {
+                    const int os = oit % OSTW;
+                    tc::mbar_wait(&B.ofull[os], (oit / OSTW) & 1);
+                    for (int j = 0; j < nacc; ++j, ++xit) {
+                        const int xs = xit % XST;
+                        tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
+                        tc::tc_fence_after();
+                        issue_split_stage(tmem + (b * CB + j) * ACC, xring + xs * SX,
+                                          oring + os * 2 * SOP, kb == 0);
+                        tc::mma_commit(&B.xempty[xs]);
+                    }
+                    tc::mma_commit(&B.oempty[os]);
+                }
+                tc::mma_commit(&B.dfull[b]);
+            }
         }
-    };
-    auto epilogue = [&](int p, int j, int quarter, int ln, uint32_t ta, bool any) {
-        const int item = item_of(p), s = item / ncs;
-        const long long col = (long long)block_of(item, j) * BM + quarter * 32 + ln;
-        float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
+    } else {
+        // epilogue: thread = column `quarter * 32 + lane` of each block
+        const int quarter = warp & 3;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        for (int p = 0; p < npass; ++p) {
+            int nacc, nkb, r0;
+            pass_of(p, nacc, nkb, r0);
+            const int item = me + p * G, s = item / ncs, b = p & 1;
+            tc::mbar_wait(&B.dfull[b], (p >> 1) & 1);
+            tc::tc_fence_after();
+            for (int j = 0; j < nacc; ++j) {
+                const long long col = (long long)((item % ncs) * CB + j) * BM + quarter * 32 + lane;
+                float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
+                const uint32_t ta = tmem + (b * CB + j) * ACC + lane_off;
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            float v[32];
-            if (any) {
-                float v2[32];
-                tc::tmem_ld32(ta + h * 32, v);
-                tc::tmem_ld32(ta + R + h * 32, v2);
+                for (int h = 0; h < 2; ++h) {
+                    float v[32];
+                    if (nkb > 0) {
+                        float v2[32];
+                        tc::tmem_ld32(ta + h * 32, v);
+                        tc::tmem_ld32(ta + R + h * 32, v2);
 #pragma unroll
-                for (int k = 0; k < 32; ++k) v[k] += v2[k];   // scaled units (see wreduce)
-            } else {
+                        for (int k = 0; k < 32; ++k) v[k] += v2[k];   // scaled units (see wreduce)
+                    } else {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) v[k] = 0.f;
+                        for (int k = 0; k < 32; ++k) v[k] = 0.f;
+                    }
+                    if (col < n) {
+#pragma unroll
+                        for (int k4 = 0; k4 < 8; ++k4)
+                            o[h * 8 + k4] =
+                                make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
+                    }
+                }
             }
-            if (col < n) {
-#pragma unroll
-                for (int k4 = 0; k4 < 8; ++k4)
-                    o[h * 8 + k4] = make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
-            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&B.dempty[b]);
         }
-    };
-    run_pipeline<true, PAIR, PS>(base, B, tmem, npass, xscale, pass_of, load_x, load_op, epilogue,
-                             tr);
+    }
     tc::tc_fence_before();
     __syncthreads();
-    if constexpr (PAIR) {
-        tc::cluster_sync();
-        if (warp == 1) tc::tmem_free_pair<TM_COLS>(tmem);
-    } else {
-        if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
-    }
+    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
 // sum of x^2 and max(x) over X, cached in the workspace and keyed by
@@ -864,10 +707,8 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
     }
 }
 
-// Pre-split copy of X for the PS kernels: X_hi = rn(x 2^ex), X_lo = rn(x 2^ex
-// - X_hi) in fp16 -- the values the split warps would compute every pass --
-// both row-major (m x n, V step) and transposed (n x m, W step), i.e. 8 bytes
-// per element of X in HBM, 4 of them read per half step as before.  Made once
+// Pre-split copy of X: X_hi = rn(x 2^ex), X_lo = rn(x 2^ex - X_hi) in fp16,
+// both row-major (m x n, V step) and transposed (n x m, W step).  Made once
 // per X (keyed like the sum-of-squares cache; runs after sumsq_kernel, whose
 // exponent it uses); later launches exit at the key check.
 constexpr int PS_TILE = 64;
@@ -1136,62 +977,24 @@ wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
     }
 }
 
-// f-partial = sum x^2 - 2 <V, Q> + <G_V, G_W> (all over this rank's rows);
-// <G_V, G_W> = sum_i v_i . (v_i G_W) comes from the V-step epilogue, which
-// holds V and DEN = V G_W row by row (no Gram of the old V needed)
+// f-partial (this rank's rows) = sum of the V step's per-CTA shares in CTA order
 __global__ void tc_objective_kernel(const double* __restrict__ part, int nparts,
-                                    const XXCache* __restrict__ cache, double* __restrict__ out) {
+                                    double* __restrict__ out) {
     __shared__ double sc[32];
-    double cr = 0.0, gg = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-        cr += part[i];
-        gg += part[nparts + i];
-    }
-    cr = block_sum(cr, sc);
-    gg = block_sum(gg, sc);
-    if (threadIdx.x == 0) *out = cache->xx - 2.0 * cr + gg;
+    const double f = block_sum_array(part, nparts, sc);
+    if (threadIdx.x == 0) *out = f;
 }
 
 struct TcPlan {
     int vgrid, wgrid, splits, rows_per_split;
 };
 
-// pair: CTA pairs (cta_group::2) -- kNumSMs / 2 work slots of 256 rows
-// (V step) or 2 CB column blocks (W step); grids are even.  Opt-in
-// (MMK_TC_PAIR=1), correct (tests/test_nnmf_tc_gpu.py).  With the split warps
-// the cross-CTA split -> MMA -> commit loop (~6.7k cycles) paced a stage at
-// ~1.7k cycles against ~1.17k for single CTAs (scripts/tctrace.py); with
-// pre-split X that loop is gone and pairs run within 1-2 % of single CTAs
-// (both HBM-bound), so single CTAs stay the default.
-bool pair_on() {
-    static const bool on = [] {
-        const char* e = getenv("MMK_TC_PAIR");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-// pre-split X (PS kernels): on unless MMK_TC_PRESPLIT=0, or the copy (8 bytes
-// per element of X: fp16 hi + lo, row-major and transposed) would pass 48 GiB;
-// MMK_TC_PRESPLIT=1 forces it.  A function of (m, n) only, so ws_bytes and
-// iter_a agree.
-bool presplit_on(long long m, long long n) {
-    static const int mode = [] {
-        const char* e = getenv("MMK_TC_PRESPLIT");
-        return e ? (e[0] == '1' ? 1 : (e[0] == '0' ? 0 : -1)) : -1;
-    }();
-    if (mode >= 0) return mode == 1;
-    return 8.0 * (double)m * (double)n <= 48.0 * (1ull << 30);
-}
-
-TcPlan tc_plan(long long m, long long n, bool pair) {
+TcPlan tc_plan(long long m, long long n) {
     TcPlan P;
-    const int slots = pair ? kNumSMs / 2 : kNumSMs;
     const int ntiles = (int)((m + BM - 1) / BM);
-    const int units = pair ? (ntiles + 1) / 2 : ntiles;
-    P.vgrid = (units < slots ? units : slots) * (pair ? 2 : 1);
+    P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
     const int ncb = (int)((n + BM - 1) / BM);
-    const int ncs = (ncb + (pair ? 2 * CB : CB) - 1) / (pair ? 2 * CB : CB);
+    const int ncs = (ncb + CB - 1) / CB;
     // split count minimising (wave quantisation loss) + (split-K partial
     // traffic: S fp32 partials of n x 64 written and read back, relative to
     // one pass over X); rows per split >= 4 K-blocks
@@ -1200,8 +1003,8 @@ TcPlan tc_plan(long long m, long long n, bool pair) {
     double best_cost = 1e300;
     for (int S = 1; S <= max_splits && S <= 4 * kNumSMs; ++S) {
         const int items = ncs * S;
-        const int waves = (items + slots - 1) / slots;
-        const double eff = (double)items / ((double)waves * slots);
+        const int waves = (items + kNumSMs - 1) / kNumSMs;
+        const double eff = (double)items / ((double)waves * kNumSMs);
         const double partial = 2.0 * S * (double)n * R * 4.0 / ((double)m * n * 4.0);
         const double cost = 1.0 / eff + partial;
         if (cost < best_cost - 1e-12) {
@@ -1214,7 +1017,7 @@ TcPlan tc_plan(long long m, long long n, bool pair) {
     P.rows_per_split = (int)rps;
     P.splits = (int)((m + rps - 1) / rps);
     const int items = ncs * P.splits;
-    P.wgrid = (items < slots ? items : slots) * (pair ? 2 : 1);
+    P.wgrid = items < kNumSMs ? items : kNumSMs;
     return P;
 }
 
@@ -1237,22 +1040,19 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
 }
 
 struct TcWs {
-    __half *Wh, *Wl, *Vth, *Vtl;
-    __half *Xh, *Xl, *XTh, *XTl;   // pre-split X (presplit_on(m, n) only)
+    __half *Wh, *Wl, *Vth, *Vtl, *Vh;
+    __half *Xh, *Xl, *XTh, *XTl;   // pre-split X
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
-    double *GVn, *part, *sqpart, *gpart;
+    double *part, *sqpart, *gpart;
     XXCache* xx;
     Scales* sc;
-    unsigned int* counter;   // [0] sumsq, [1] wmax
+    unsigned int* counter;   // [0] sumsq, [1] wmax, [2] presplit
 };
 
 inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
 
 size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
-    // room for the split-K partials of either plan (single CTAs or pairs)
-    TcPlan P = tc_plan(m, n, false);
-    const TcPlan P2 = tc_plan(m, n, true);
-    if (P2.splits > P.splits) P.splits = P2.splits;
+    const TcPlan P = tc_plan(m, n);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -1261,22 +1061,22 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     };
     size_t oWh = take(2 * (size_t)R * n), oWl = take(2 * (size_t)R * n);
     size_t oVh = take(2 * (size_t)R * m), oVl = take(2 * (size_t)R * m);
+    size_t oVr = take(2 * (size_t)R * m);
     size_t oWp = take(4 * (size_t)P.splits * n * R);
-    size_t oG = take(8 * (size_t)R * R);
-    size_t oP = take(16 * (size_t)kNumSMs);
+    size_t oP = take(8 * (size_t)kNumSMs);
     size_t oS = take(8 * (size_t)kNumSMs * 4);
     size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) sumsq, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
     size_t oGF = take(4 * (size_t)R * R);
-    const size_t xe = presplit_on(m, n) ? (size_t)m * n : 0;
+    const size_t xe = (size_t)m * n;
     size_t oXh = take(2 * xe), oXl = take(2 * xe), oXTh = take(2 * xe), oXTl = take(2 * xe);
     if (base && L) {
-        L->Xh = (__half*)(c_base(base) + oXh);
-        L->Xl = (__half*)(c_base(base) + oXl);
-        L->XTh = (__half*)(c_base(base) + oXTh);
-        L->XTl = (__half*)(c_base(base) + oXTl);
         char* c = c_base(base);
+        L->Xh = (__half*)(c + oXh);
+        L->Xl = (__half*)(c + oXl);
+        L->XTh = (__half*)(c + oXTh);
+        L->XTl = (__half*)(c + oXTl);
         L->sqpart = (double*)(c + oS);
         L->mpart = (float*)(c + oM);
         L->xx = (XXCache*)(c + oC);
@@ -1286,8 +1086,8 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->Wl = (__half*)(c + oWl);
         L->Vth = (__half*)(c + oVh);
         L->Vtl = (__half*)(c + oVl);
+        L->Vh = (__half*)(c + oVr);
         L->wpart = (float*)(c + oWp);
-        L->GVn = (double*)(c + oG);
         L->part = (double*)(c + oP);
         L->gpart = (double*)(c + oGP);
         L->GWf = (float*)(c + oGF);
@@ -1295,20 +1095,25 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     return off;
 }
 
-unsigned long long* g_trace_v = nullptr;   // debug: mmk_tc_set_trace
-thread_local bool t_x_prepared = false;      // set while an engine captures its loop
-unsigned long long* g_trace_w = nullptr;
+thread_local bool t_x_prepared = false;   // set while an engine captures its loop
 
 }  // namespace
 
 namespace mmk_tc {
 
-bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X) {
+// The tensor-core path needs the pre-split copy of X (8 bytes per element)
+// next to X itself; shapes whose copy would pass 96 GiB take the SIMT path.
+bool shape_ok(int dtype, long long m, long long n, long long r) {
     if (dtype != MMK_F32 || r != R) return false;
-    // 16-byte TMA row strides: fp32 X (ldx % 4), fp16 W^ (n % 8) and V'^T (m % 8)
-    if ((n & 7) || (m & 7) || (ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
-    if (m < BM || n < BM) return false;
+    if ((n & 7) || (m & 7) || m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
+    return 8.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
+}
+
+bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X) {
+    if (!shape_ok(dtype, m, n, r)) return false;
+    // 16-byte rows for the pre-split pass (ldx % 4) and a 16-byte aligned X
+    if ((ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 15)) return false;
     const char* env = getenv("MMK_NNMF_TC");
     if (env && env[0] == '0') return false;
     return true;
@@ -1325,11 +1130,9 @@ int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcw
     MMK_LAUNCH("nnmf_sumsq_cached", st,
                (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
                                                            L.counter, L.sc)));
-    if (presplit_on(m, n))
-        MMK_LAUNCH("nnmf_presplit_cached", st,
-                   (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
-                                                                 L.Xl, L.XTh, L.XTl,
-                                                                 L.counter + 2)));
+    MMK_LAUNCH("nnmf_presplit_cached", st,
+               (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
+                                                             L.Xl, L.XTh, L.XTl, L.counter + 2)));
     MMK_CHECK_LAUNCH("nnmf_prepare_x");
     return MMK_OK;
 }
@@ -1341,59 +1144,18 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
            cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
-    const bool pair = pair_on(), ps = presplit_on(m, n);
-    const TcPlan P = tc_plan(m, n, pair);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc<false, false>))) {
-        const char* dbg = getenv("MMK_TC_DBG");
-        if (dbg) {
-            const int v = atoi(dbg);
-            cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
-        }
-        if (const char* tc = getenv("MMK_TRACE_CTA")) {
-            const int v = atoi(tc);
-            cudaMemcpyToSymbol(c_trace_cta, &v, sizeof(int));
-        }
-        auto big = [](auto f) {
-            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        };
-        big(nnmf_vstep_tc<false, false>);
-        big(nnmf_wstep_tc<false, false>);
-        big(nnmf_vstep_tc<true, false>);
-        big(nnmf_wstep_tc<true, false>);
-        big(nnmf_vstep_tc<false, true>);
-        big(nnmf_wstep_tc<false, true>);
-        big(nnmf_vstep_tc<true, true>);
-        big(nnmf_wstep_tc<true, true>);
+    const TcPlan P = tc_plan(m, n);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc))) {
+        cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_V);
+        cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
     }
-    // cluster launch of the pair kernels (2 CTAs = one TPC)
-    auto launch_pair = [&](auto kern, int grid, auto... args) {
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = SMEM;
-        cfg.stream = st;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        (void)cudaLaunchKernelEx(&cfg, kern, args...);
-    };
-    CUtensorMap mX, mX2, mWh, mWl, mXt, mXt2, mVh, mVl;
+    CUtensorMap mX, mX2, mWh, mWl, mVr, mXt, mXt2, mVh, mVl;
     int rc;
-    if (ps) {   // fp16 hi / lo maps of the pre-split X and X^T (made below)
-        if ((rc = mmk_host::make_map_f16(&mX, L.Xh, m, n, n, BM))) return rc;
-        if ((rc = mmk_host::make_map_f16(&mX2, L.Xl, m, n, n, BM))) return rc;
-        if ((rc = mmk_host::make_map_f16(&mXt, L.XTh, n, m, m, BM))) return rc;
-        if ((rc = mmk_host::make_map_f16(&mXt2, L.XTl, n, m, m, BM))) return rc;
-    } else {
-        if ((rc = mmk_host::make_map_f32(&mX, X, m, n, ldx, BM))) return rc;
-        if ((rc = mmk_host::make_map_f32(&mXt, X, m, n, ldx, BK))) return rc;
-        mX2 = mX;
-        mXt2 = mXt;
-    }
+    if ((rc = mmk_host::make_map_f16(&mX, L.Xh, m, n, n, BM))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mX2, L.Xl, m, n, n, BM))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mXt, L.XTh, n, m, m, BM))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mXt2, L.XTl, n, m, m, BM))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mVr, L.Vh, m, R, R, BM))) return rc;
     if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, R, m, m, R))) return rc;
@@ -1410,44 +1172,23 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
     gram32(W, n, true, L.gpart, GW, st, L.GWf);
-    {
-        auto vk = pair ? (ps ? nnmf_vstep_tc<true, true> : nnmf_vstep_tc<true, false>)
-                       : (ps ? nnmf_vstep_tc<false, true> : nnmf_vstep_tc<false, false>);
-        if (pair)
-            MMK_LAUNCH("nnmf_vstep_tc", st,
-                       launch_pair(vk, P.vgrid, mX, mX2, mWh, mWl, V, (const float*)L.GWf, V_out,
-                                   L.sc, (int)m, (int)n, L.part, L.gpart, g_trace_v));
-        else
-            MMK_LAUNCH("nnmf_vstep_tc", st,
-                       (vk<<<P.vgrid, kThreads, SMEM, st>>>(mX, mX2, mWh, mWl, V, L.GWf, V_out, L.sc,
-                                                            (int)m, (int)n, L.part, L.gpart,
-                                                            g_trace_v)));
-    }
+    MMK_LAUNCH("nnmf_split_v", st,
+               (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
+    MMK_LAUNCH("nnmf_vstep_tc", st,
+               (nnmf_vstep_tc<<<P.vgrid, kVThreads, SMEM_V, st>>>(mX, mX2, mWh, mWl, mVr, V,
+                                                                  L.GWf, V_out, L.sc, (int)m,
+                                                                  (int)n, L.part)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
-               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid, L.xx,
+               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid,
                                                         red + rn + (long long)R * R)));
-    if (ps)   // V'^T V' partials came from the V step (one per CTA)
-        MMK_LAUNCH("nnmf_gram_sum", st,
-                   (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(L.gpart, P.vgrid, red + rn,
-                                                                   nullptr)));
-    else
-        gram32(V_out, m, false, L.gpart, red + rn, st);
+    gram32(V_out, m, false, L.gpart, red + rn, st);
     MMK_LAUNCH("nnmf_vprep", st,
                (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
-    {
-        auto wk = pair ? (ps ? nnmf_wstep_tc<true, true> : nnmf_wstep_tc<true, false>)
-                       : (ps ? nnmf_wstep_tc<false, true> : nnmf_wstep_tc<false, false>);
-        if (pair)
-            MMK_LAUNCH("nnmf_wstep_tc", st,
-                       launch_pair(wk, P.wgrid, mXt, mXt2, mVh, mVl, (const Scales*)L.sc, (int)m,
-                                   (int)n, P.splits, P.rows_per_split, L.wpart, g_trace_w));
-        else
-            MMK_LAUNCH("nnmf_wstep_tc", st,
-                       (wk<<<P.wgrid, kThreads, SMEM, st>>>(mXt, mXt2, mVh, mVl, L.sc, (int)m,
-                                                            (int)n, P.splits, P.rows_per_split,
-                                                            L.wpart, g_trace_w)));
-    }
+    MMK_LAUNCH("nnmf_wstep_tc", st,
+               (nnmf_wstep_tc<<<P.wgrid, kWThreads, SMEM_W, st>>>(mXt, mXt2, mVh, mVl, (int)m,
+                                                                  (int)n, P.splits,
+                                                                  P.rows_per_split, L.wpart)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
                (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
@@ -1457,11 +1198,3 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 }
 
 }  // namespace mmk_tc
-
-// Debug hook: per-stage pipeline timestamps of CTA 0 (6 x 256 uint64 each, or
-// NULL to disable).  Not part of the solver ABI contract.
-extern "C" int mmk_tc_set_trace(unsigned long long* vstep, unsigned long long* wstep) {
-    g_trace_v = vstep;
-    g_trace_w = wstep;
-    return 0;
-}

@@ -5,6 +5,10 @@
 
 namespace mmk_tc {
 
+// dtype / shape admit the tensor-core path (fp32, rank 64, m and n multiples
+// of 8, >= 128, the pre-split copy of X within its memory cap)
+bool shape_ok(int dtype, long long m, long long n, long long r);
+// ... and this X (row stride, alignment; MMK_NNMF_TC=0 disables the path)
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X);
 size_t ws_bytes(long long m, long long n);
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,

@@ -176,7 +176,7 @@ class _Ops:
         self.backend = backend
         self.dev = backend.torch_device()
         self.code = _lib.dtype_code(backend.torch_dtype())
-        self.ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_ws_bytes", self.code, m, n, r),
+        self.ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_op_ws_bytes", self.code, m, n, r),
                               dtype=torch.uint8, device=self.dev)
         self.red = torch.zeros(_lib.load().mmk_nnmf_reduce_len(n, r), dtype=torch.float64,
                                device=self.dev)

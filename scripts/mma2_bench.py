@@ -9,7 +9,7 @@ st = _lib.stream_handle(torch, torch.device("cuda", 0))
 for n in (64, 128, 192, 256, -64, -128, -256):
     for iters in (256, 4096):
         out.zero_()
-        _lib.call("mmk_tc_mma2_bench", n, iters, _lib.ptr(out), st)
+        _lib.call_diag("mmk_tc_mma2_bench", n, iters, _lib.ptr(out), st)
         torch.cuda.synchronize()
     o = out.cpu().tolist()
     cyc = o[0] / 4096

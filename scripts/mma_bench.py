@@ -11,7 +11,7 @@ flops = [2*128*128*8, 2*128*128*8, 2*128*64*8, 2*128*256*8, 2*128*128*16, 2*128*
          2*128*128*8, 2*128*64*8, 2*128*128*8, 2*128*128*8, 2*128*256*16]
 for mode in range(13):
     for iters in (256, 4096):
-        _lib.call("mmk_tc_mma_bench", mode, iters, _lib.ptr(out), st)
+        _lib.call_diag("mmk_tc_mma_bench", mode, iters, _lib.ptr(out), st)
         torch.cuda.synchronize()
     cyc = out.item() / 4096
     print(f"{names[mode]:18s} {cyc:7.1f} cycles/MMA  {flops[mode]/cyc:7.0f} flop/cycle")

@@ -8,7 +8,7 @@ out = torch.zeros(4, dtype=torch.int64, device="cuda")
 st = _lib.stream_handle(torch, torch.device("cuda", 0))
 for iters in (64, 1024):
     out.zero_()
-    _lib.call("mmk_tc_pingpong", iters, _lib.ptr(out), st)
+    _lib.call_diag("mmk_tc_pingpong", iters, _lib.ptr(out), st)
     torch.cuda.synchronize()
 o = out.cpu().tolist()
 print(f"remote arrive round trip: {o[0]} cycles; commit-multicast + remote arrive round trip: {o[1]} cycles; timeouts {o[2]},{o[3]}")

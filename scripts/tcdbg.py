@@ -15,7 +15,7 @@ for mode in (1, 2, 4, 8, 14):
     D2 = torch.full((128, 32), -7.0, device="cuda")
     D3 = torch.full((128, 64), -7.0, device="cuda")
     diag = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), mode, _lib.ptr(diag), st)
+    _lib.call_diag("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), mode, _lib.ptr(diag), st)
     torch.cuda.synchronize()
     print("mode", mode, "diag", diag.item(), flush=True)
     if mode == 1:
@@ -39,7 +39,7 @@ for mode in (1, 2, 4, 8, 14):
 # 32B-atom swizzle model check on the dumps from mode 1
 D1 = torch.zeros(128, 64, device="cuda"); D2 = torch.zeros(128, 32, device="cuda"); D3 = torch.zeros(128, 64, device="cuda")
 diag = torch.zeros(1, dtype=torch.int32, device="cuda")
-_lib.call("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), 1, _lib.ptr(diag), st)
+_lib.call_diag("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), 1, _lib.ptr(diag), st)
 torch.cuda.synchronize()
 raw = D3.reshape(-1).cpu()
 Xh, Bh = X.cpu(), B.cpu()

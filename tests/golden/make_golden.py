@@ -204,7 +204,55 @@ def gen_gradients():
     save("gradients", **out)
 
 
+def _outer_sum(a, b):
+    """a @ b as a fixed-order sum of outer products (BLAS summation order
+    depends on the machine's thread count; this does not)."""
+    out = np.zeros((a.shape[0], b.shape[1]))
+    for k in range(a.shape[1]):
+        out += np.outer(a[:, k], b[k])
+    return out
+
+
+def r64_inputs(kind):
+    """Rank-64 NNMF on a tensor-core-eligible shape (1024 x 2048: 8 row tiles,
+    16 column blocks, 32 K-blocks of the tcgen05 kernels), fp32-exact.
+    uniform : X, V0, W0 ~ U[0, 1) (SURVEY 8(d) C4 recipe at a reduced shape)
+    wellfit : X = (Vt Wt)(1 + 0.01 N(0, 1)) clipped at 0, a rank-64 product
+              with 1 % noise, started from Vt, Wt perturbed by up to 20 %:
+              ||X||^2 / f ~ 1e4 over the run, the regime where the Gram-trace
+              objective cancels."""
+    m, n, r = 1024, 2048, 64
+    if kind == "uniform":
+        g = np.random.default_rng(41)
+        return f32(g.random((m, n))), f32(g.random((m, r))), f32(g.random((r, n)))
+    g = np.random.default_rng(31)
+    vt, wt = g.random((m, r)), g.random((r, n))
+    x = f32(np.maximum(_outer_sum(vt, wt) * (1.0 + 0.01 * g.standard_normal((m, n))), 0.0))
+    g2 = np.random.default_rng(32)
+    return x, f32(vt * (1.0 + 0.2 * g2.random((m, r)))), f32(wt * (1.0 + 0.2 * g2.random((r, n))))
+
+
+def _gen_r64(kind, iters):
+    import importlib
+    nn = importlib.import_module("mmkit_ref.nnmf")
+    x, v0, w0 = r64_inputs(kind)
+    mm = nn._FrobeniusNnmf(R.NnmfProblem(x=x, rank=64), R.Backend.parallel(THREADS))
+    state, tr = R.run_mm(mm, nn.FactorPair(v0, w0),
+                         R.MmConfig(max_iters=iters, epsilon=1e-300))
+    save(f"nnmf_r64_{kind}", trace=tr.objective_values, v=state.v, w=state.w,
+         x_digest=digest(x), v0_digest=digest(v0), w0_digest=digest(w0))
+
+
+def gen_nnmf_r64_uniform():
+    _gen_r64("uniform", 500)
+
+
+def gen_nnmf_r64_wellfit():
+    _gen_r64("wellfit", 1000)
+
+
 GENERATORS = {
+    "nnmf_r64_uniform": gen_nnmf_r64_uniform, "nnmf_r64_wellfit": gen_nnmf_r64_wellfit,
     "gradients": gen_gradients,
     "poisson_small": gen_poisson_small, "poisson_c1": gen_poisson_c1,
     "nnmf_small": gen_nnmf_small, "pet_small": gen_pet_small, "mds_small": gen_mds_small,

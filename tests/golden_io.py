@@ -63,3 +63,27 @@ def rel_elem(a, b):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def _outer_sum(a, b):
+    """a @ b as a fixed-order sum of outer products (BLAS summation order
+    depends on the machine's thread count; this does not)."""
+    out = np.zeros((a.shape[0], b.shape[1]))
+    for k in range(a.shape[1]):
+        out += np.outer(a[:, k], b[k])
+    return out
+
+
+def r64_inputs(kind):
+    """Rank-64 tensor-core-eligible NNMF inputs (tests/golden/make_golden.py
+    r64_inputs): 'uniform' or 'wellfit' (rank-64 product with 1 % noise,
+    start within 20 % of the truth, ||X||^2 / f ~ 1e4)."""
+    m, n, r = 1024, 2048, 64
+    if kind == "uniform":
+        g = np.random.default_rng(41)
+        return f32(g.random((m, n))), f32(g.random((m, r))), f32(g.random((r, n)))
+    g = np.random.default_rng(31)
+    vt, wt = g.random((m, r)), g.random((r, n))
+    x = f32(np.maximum(_outer_sum(vt, wt) * (1.0 + 0.01 * g.standard_normal((m, n))), 0.0))
+    g2 = np.random.default_rng(32)
+    return x, f32(vt * (1.0 + 0.2 * g2.random((m, r)))), f32(wt * (1.0 + 0.2 * g2.random((r, n))))

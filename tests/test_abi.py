@@ -54,26 +54,33 @@ def test_sass_has_no_legacy_fallback_symbols():
     assert not hasattr(lib, "ora_matmul")
 
 
-@pytest.mark.parametrize("env,presplit", [(None, True), ("0", False), ("1", True)])
-def test_nnmf_tc_presplit_workspace_policy(env, presplit):
-    """The tensor-core NNMF workspace holds the pre-split copy of X (fp16 hi / lo,
-    row-major + transposed: 8 bytes per element) unless MMK_TC_PRESPLIT=0, and by
-    default only while that copy stays within 48 GiB (read once per process,
-    hence the subprocess)."""
-    import subprocess
-    import sys
-    code = ("from paper_1003_3272_b200 import _lib\n"
-            "print(_lib.ws_bytes('mmk_nnmf_ws_bytes', 0, 131072, 16384, 64),"
-            " _lib.ws_bytes('mmk_nnmf_ws_bytes', 0, 262144, 65536, 64))")
-    e = dict(os.environ)
-    e.pop("MMK_TC_PRESPLIT", None)
-    if env is not None:
-        e["MMK_TC_PRESPLIT"] = env
-    out = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True,
-                         text=True, timeout=300)
-    assert out.returncode == 0, out.stderr
-    c4, big = (int(v) for v in out.stdout.split())
+def test_nnmf_tc_workspace_policy():
+    """Only a full-iteration fp32 rank-64 workspace holds the tensor-core region
+    (the pre-split copy of X: fp16 hi / lo, row-major + transposed, 8 bytes per
+    element), and only while that copy stays within 96 GiB; fp64, other ranks
+    and the single operations (mmk_nnmf_op_ws_bytes) never reserve it
+    (a zero-filled 16 GiB region per single-op call)."""
+    ws = _lib.ws_bytes
     copy = 8 * 131072 * 16384
-    assert (c4 >= copy) == presplit and c4 < copy + (1 << 30)
-    # 262144 x 65536: the copy would be 128 GiB -- only when forced
-    assert (big >= 8 * 262144 * 65536) == (env == "1")
+    c4 = ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 64)
+    assert copy <= c4 < copy + (1 << 30)
+    for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 32)):
+        assert ws("mmk_nnmf_ws_bytes", *args) < (1 << 30)
+    assert ws("mmk_nnmf_op_ws_bytes", 0, 131072, 16384, 64) < (1 << 30)
+    # 262144 x 65536: the copy would be 128 GiB -- SIMT path, no region
+    assert ws("mmk_nnmf_ws_bytes", 0, 262144, 65536, 64) < (1 << 32)
+
+
+def test_diagnostics_live_outside_the_solver_library():
+    """The tcgen05 self-test and MMA microbenchmarks are in libmmk_diag.so
+    (include/mmk_diag.h), not in the product library."""
+    text = open(os.path.join(ROOT, "include", "mmk_diag.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    diag = sorted(set(re.findall(r"\b(mmk_[a-z0-9_]+)\s*\(", text)))
+    assert diag and not set(diag) & set(header_functions())
+    dl = _lib.load_diag()
+    for name in diag:
+        assert hasattr(dl, name), name
+    lib = _lib.load()
+    for name in diag + ["mmk_tc_set_trace"]:
+        assert not hasattr(lib, name), name

@@ -1,4 +1,4 @@
-"""Known-answer test of the tcgen05 building blocks (csrc/tc_selftest.cu)."""
+"""Known-answer test of the tcgen05 building blocks (csrc/diag/tc_selftest.cu, libmmk_diag.so)."""
 
 import pytest
 import torch
@@ -19,7 +19,7 @@ def test_tcgen05_tf32_descriptors():
     D2 = torch.zeros(128, 32, device="cuda")
     D3 = torch.zeros(128, 64, device="cuda")
     diag = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), 14,
+    _lib.call_diag("mmk_selftest_tc", *(_lib.ptr(t) for t in (A, B, X, V, D1, D2, D3)), 14,
               _lib.ptr(diag), _lib.stream_handle(torch, torch.device("cuda", 0)))
     torch.cuda.synchronize()
     assert diag.item() == 0
