@@ -2,7 +2,12 @@
 """MM iterations/sec on B200 (BASELINE.json metric), one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload nnmf-large|mds-large|pet-c2|nnmf-c1|mds-c3]
+                    [--workload nnmf-large|mds-large|pet-large|nnmf-mid]
+
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks on this node (one per GPU; on a box with
+fewer GPUs than N the ranks share devices over a gloo group -- a functional
+check of the sharded path, not a throughput number).
 
 A "step" is one MM iteration: the objective at the current state plus the
 full update (one fused device pass).  Default workload = BASELINE config 4,
@@ -11,8 +16,9 @@ NNMF 131072 x 16384, rank 64, fp32 (the largest single-GPU config; X is
 torchrun the rows of X are sharded across ranks (strong scaling of a fixed
 problem, NCCL all-reduce of the W-step partials).
 
-value    device-timed iterations/s of the whole job, inputs resident in HBM
-         (CUDA events on the compute stream, max over ranks)
+value    device-timed iterations/s of the whole job through the public API
+         (nnmf_run / nnmf_run_sharded, mds_run / mds_run_sharded), inputs
+         resident in HBM (CUDA events on the compute stream, max over ranks)
 e2e      the same metric through the public API (nnmf_run on a pinned host
          tensor: H2D of X and the start, K iterations with per-batch trace
          reads, D2H of the factors) -- the headline against --impl reference
@@ -35,6 +41,8 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     "nnmf-large": dict(solver="nnmf", m=131072, n=16384, r=64, label="BASELINE config 4"),
+    "nnmf-mid": dict(solver="nnmf", m=16384, n=4096, r=64,
+                     label="BASELINE config 4 at 1/32 of the size (CI of the sharded path)"),
     "mds-large": dict(solver="mds", n=65536, dim=3, label="BASELINE config 5"),
     "nnmf-c1": dict(solver="nnmf", m=2429, n=361, r=10, label="BASELINE config 1"),
     "poisson-c1": dict(solver="poisson", m=2429, n=361, r=10,
@@ -90,6 +98,11 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a moment to start: the timed region begins once
+            # it reports (a short region would otherwise go unsampled)
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
@@ -239,7 +252,7 @@ def run_reference(args):
         "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, W),
+        "config": workload_config(args, W, world),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
@@ -249,10 +262,11 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, W):
+def workload_config(args, W, world=1):
     cfg = {"workload": args.workload, "what": W["label"]}
     cfg.update({k: v for k, v in W.items() if k not in ("solver", "label")})
-    cfg["parallelism"] = f"rows-sharded x{args.gpus}" if args.gpus > 1 else "single-gpu"
+    kind = {"mds": "tiles-sharded", "pet": "replicas"}.get(W["solver"], "rows-sharded")
+    cfg["parallelism"] = f"{kind} x{world}" if world > 1 else "single-gpu"
     cfg["l2"] = ("inputs larger than L2" if args.workload in ("nnmf-large", "mds-large")
                  else "L2-resident (no flush: the solver re-reads a cache-sized matrix "
                       "every iteration by design)")
@@ -261,11 +275,16 @@ def workload_config(args, W):
 
 # ----------------------------------------------------------------------------- GPU arm
 def bench_nnmf_large(args, torch, world, rank, dev):
-    import numpy as np
+    """BASELINE config 4: rows of X (and V) sharded across ranks, W
+    replicated.  `value` times the public API on X resident in HBM --
+    nnmf_run at one rank, nnmf_run_sharded (the device-loop engine with the
+    NCCL all-reduce captured in its graph) across ranks; the per-kernel
+    breakdown and the roofline come from a separate launch-profiled loop of
+    the same iteration through the C ABI (phase A, all-reduce, phase B)."""
+    import torch.distributed as dist
 
     import paper_1003_3272_b200 as M
-    from paper_1003_3272_b200 import _lib
-    from paper_1003_3272_b200.parallel import ShardedNnmf, shard_rows
+    from paper_1003_3272_b200.parallel import ShardedNnmf, nnmf_run_sharded, shard_rows
     W = WORKLOADS[args.workload]
     m, n, r = W["m"], W["n"], W["r"]
     lo, hi = shard_rows(m, world, rank)
@@ -278,22 +297,31 @@ def bench_nnmf_large(args, torch, world, rank, dev):
     w0 = torch.rand(r, n, generator=g, device=dev, dtype=torch.float32).to(dt)
     g.manual_seed(2000 + rank)
     v0 = torch.rand(hi - lo, r, generator=g, device=dev, dtype=torch.float32).to(dt)
-    sh = ShardedNnmf(x, v0.clone(), w0.clone(), r, be)
 
-    def step():
-        sh.iterate(world)
+    # 1) the public API (the headline value)
+    group = dist.group.WORLD if world > 1 else None
+    prob = M.NnmfProblem(x=x, rank=r)
 
-    timing = time_steps(args, torch, dev, step, world)
-    # dominant kernel via the launch profiler (events on the launch stream,
-    # recorded over the timed region)
-    prof = timing["prof"]
+    def api_run(iters):
+        cfg = M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6)
+        if world > 1:
+            return nnmf_run_sharded(x, r, cfg, be, group=group, state0=(v0, w0))
+        return M.nnmf_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
+
+    timing = time_region(args, torch, dev, lambda: api_run(args.warmup),
+                         lambda: api_run(args.steps), world)
+
+    # 2) launch-profiled per-iteration loop (kernel breakdown, roofline)
+    sh = ShardedNnmf(x, v0.clone(), w0.clone(), r, be, group=group)
+    loop = time_steps(args, torch, dev, lambda: sh.iterate(world), world)
+    prof = loop["prof"]
     es = x.element_size()
     ml = hi - lo
     alg = {  # algorithmic HBM bytes per launch
         "nnmf_vstep": ml * n * es + 2 * ml * r * es + r * n * es,
         "nnmf_wpart": ml * n * es + ml * r * es,
-        # X once + V read + V', V'_hi, V'_lo written + W_hi/W_lo chunks (L2-resident)
-        "nnmf_vstep_tc": ml * n * 4 + 4 * ml * r * 4 + 2 * r * n * 4,
+        # X once (as X_hi + X_lo) + V read + V' written + V_h read + W_hi/W_lo chunks
+        "nnmf_vstep_tc": ml * n * 4 + 2 * ml * r * 4 + ml * r * 2 + 2 * r * n * 4,
         # X once + V'_hi/V'_lo read + fp32 split-K partials written
         "nnmf_wstep_tc": ml * n * 4 + 2 * ml * r * 4,
     }
@@ -304,7 +332,12 @@ def bench_nnmf_large(args, torch, world, rank, dev):
         e2e = nnmf_e2e(args, torch, be, x, v0, w0, r)
     kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
                for k, (c, ms) in prof.items()}
-    return timing, roof, launches, e2e, {"kernels": kernels}
+    return timing, roof, launches, e2e, {
+        "kernels": kernels, "kernel_loop_ms_per_step": loop["ms_total"] / args.steps,
+        "value_path": ("nnmf_run_sharded (device-loop engine, NCCL all-reduce in its graph)"
+                       if world > 1 else "nnmf_run (device-loop engine)") +
+                      " on X resident in HBM; one timed run of `steps` iterations after a "
+                      "`warmup`-iteration run"}
 
 
 def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
@@ -429,6 +462,33 @@ def bench_pet_large(args, torch, world, rank, dev):
         "kernels": kernels, "e2e_note": "not measured for pet-large this round",
         "data": f"synthetic (Poisson counts of 50 x E default_phantom(256), torch generator; "
                 f"E = device Siddon matrix, {nnz} nonzeros)"}
+
+
+def time_region(args, torch, dev, warm, run, world):
+    """Time ONE call of `run` (a whole public-API run of args.steps
+    iterations) between CUDA events on the compute stream, after `warm`
+    (args.warmup iterations through the same API); barrier + synchronize on
+    both sides, max over ranks; nvidia-smi clocks sampled meanwhile."""
+    import torch.distributed as dist
+    warm()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with Clocks(dev.index) as clk:
+        start.record(stream)
+        run()
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    return {"ms_total": ms, "clocks": clk.summary()}
 
 
 def time_steps(args, torch, dev, step, world):
@@ -557,19 +617,38 @@ def suite(args, torch, dev):
     return out
 
 
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks on this node (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     world, rank, local = dist_info()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+    ndev = torch.cuda.device_count()
+    # one rank per GPU over NCCL; more ranks than GPUs (a functional check of
+    # the sharded path on a small box) share devices over gloo
+    backend = "nccl" if world <= ndev else "gloo"
+    dev = torch.device("cuda", local % ndev if world > 1 else 0)
     torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     from paper_1003_3272_b200 import build as B
     B.build()
     W = WORKLOADS[args.workload]
-    if args.workload == "nnmf-large":
+    if args.workload in ("nnmf-large", "nnmf-mid"):
         timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
     elif args.workload == "mds-large":
         timing, roof, launches, e2e, extra = bench_mds_large(args, torch, world, rank, dev)
@@ -595,13 +674,14 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": "MM iterations/sec", "value": value, "unit": "iterations/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "devices": min(world, ndev), "collectives": backend,
+            "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak (replicas)" if replicas else "strong",
             "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
             "data": extra.get("data", "synthetic (uniform [0,1) X, uniform start; "
                                       "torch.Generator seeded)"),
-            "config": workload_config(args, W),
+            "config": workload_config(args, W, world),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps, "clocks": timing["clocks"],
             "timing_note": "kernel times from CUDA events around every launch of the timed "
@@ -610,6 +690,9 @@ def run_ours(args):
             "suite": suite_res,
             "kernels": extra.get("kernels"),
         }
+        for k in ("kernel_loop_ms_per_step", "value_path", "e2e_note"):
+            if k in extra:
+                line[k] = extra[k]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -617,6 +700,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -49,7 +49,9 @@ enum {
     MMK_E_DOMAIN = 2,    /* DomainError */
     MMK_E_NUMERICS = 3,  /* NumericsError */
     MMK_E_NONFINITE = 4, /* NonFiniteError */
-    MMK_E_CUDA = 5       /* DeviceError (launch / runtime failure) */
+    MMK_E_CUDA = 5,      /* DeviceError (launch / runtime failure) */
+    MMK_E_PEER = 6       /* error-record code only: another rank of a sharded run
+                            flagged a device error (its record names it) */
 };
 
 enum { MMK_F32 = 0, MMK_F64 = 1 };
@@ -262,7 +264,7 @@ int mmk_mds_tri_iter_a(const float *packed, int64_t t0, int64_t t1, const float 
                        int64_t dim, int64_t n, void *ws, size_t ws_bytes, double *red,
                        int64_t *err_dev, void *stream);
 int mmk_mds_tri_iter_b(const float *theta, float *theta_out, int64_t dim, int64_t n,
-                       const double *red, double *f_dev, void *stream);
+                       const double *red, double *f_dev, int64_t *err_dev, void *stream);
 int mmk_mds_tri_iter(const float *packed, int64_t t0, int64_t t1, const float *theta,
                      float *theta_out, int64_t dim, int64_t n, void *ws, size_t ws_bytes,
                      double *red, double *f_dev, int64_t *err_dev, void *stream);

@@ -90,7 +90,7 @@ _SIGS = {
     "mmk_mds_tri_ws_bytes": ([_i64, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_mds_tri_pack": ([_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp], _i32),
     "mmk_mds_tri_iter_a": ([_vp, _i64, _i64, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp], _i32),
-    "mmk_mds_tri_iter_b": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _i32),
+    "mmk_mds_tri_iter_b": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp], _i32),
     "mmk_mds_tri_iter": ([_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp, _vp],
                          _i32),
     "mmk_mds_tri_engine_create": ([_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _sz, _vp, _vp, _vp,

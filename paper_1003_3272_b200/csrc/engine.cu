@@ -258,6 +258,7 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_reduce_len(n, r);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         void *Vi = dir ? VB : VA, *Vo = dir ? VA : VB, *Wi = dir ? WB : WA, *Wo = dir ? WA : WB;
         int rc = mmk_nnmf_iter_a(dtype, X, ldx, Vi, Wi, Vo, m, n, r, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
@@ -291,6 +292,7 @@ extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, cons
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         void *Li = dir ? lamB : lamA, *Lo = dir ? lamA : lamB;
         int rc = mmk_pet_iter_a(dtype, E, lde, y, Li, d, p, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
@@ -327,6 +329,7 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
     }
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         void *Ti = dir ? thetaB : thetaA, *To = dir ? thetaA : thetaB;
         if (!comm) {
             return mmk_mds_iter(dtype, Y, Wt, ldy, wsum, Ti, To, n, dim, n, 0, n,
@@ -358,6 +361,7 @@ extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_mds_tri_reduce_len(n, dim);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         float *Ti = dir ? thetaB : thetaA, *To = dir ? thetaA : thetaB;
         int rc = mmk_mds_tri_iter_a(packed, t0, t1, Ti, dim, n, ws, ws_bytes, red, err_dev, s);
         if (rc) return rc;
@@ -365,7 +369,7 @@ extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_
             rc = mmk_allreduce_f64(red, rl, comm, s);
             if (rc) return rc;
         }
-        return mmk_mds_tri_iter_b(Ti, To, dim, n, red, f_dev, s);
+        return mmk_mds_tri_iter_b(Ti, To, dim, n, red, f_dev, err_dev, s);
     };
     return build(iter, rule, trace, tstamp, ctl, err_dev, engine);
 }
@@ -391,6 +395,7 @@ extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t 
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_nnmf_poisson_reduce_len(n, r);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         void *Vi = dir ? VB : VA, *Vo = dir ? VA : VB, *Wi = dir ? WB : WA, *Wo = dir ? WA : WB;
         int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, Vi, Wi, Vo, m, n, r, ws, ws_bytes, red,
                                          err_dev, s);
@@ -430,6 +435,7 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
     auto iter = [=](cudaStream_t s, int dir) -> int {
+        mmk_host::NoFlag one_gpu(comm == nullptr);   // error flag only around a collective
         void *Li = dir ? lamB : lamA, *Lo = dir ? lamA : lamB;
         if (!comm)   // one GPU: fused back-projection + pixel update
             return mmk_pet_sparse_iter(dtype, rptr, ridx, rval, cptr, cidx, cval, y, Li, Lo, d,

@@ -565,7 +565,8 @@ extern "C" int64_t mmk_mds_tri_ntiles(int64_t n) {
     return T * (T + 1) / 2;
 }
 
-extern "C" int64_t mmk_mds_tri_reduce_len(int64_t n, int64_t dim) { return n * dim + 1 + dim; }
+// [C (n dim) | stress | S (dim) | device-error flag]
+extern "C" int64_t mmk_mds_tri_reduce_len(int64_t n, int64_t dim) { return n * dim + 1 + dim + 1; }
 
 extern "C" int mmk_mds_tri_ws_bytes(int64_t n, int64_t dim, int64_t t0, int64_t t1, size_t* out) {
     int rc = check_tri(n, dim, t0, t1);
@@ -605,20 +606,25 @@ extern "C" int mmk_mds_tri_iter_a(const float* packed, int64_t t0, int64_t t1, c
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     switch (dim) {
-        case 1: return tri_a<1>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st);
-        case 2: return tri_a<2>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st);
-        default: return tri_a<3>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st);
+        case 1: rc = tri_a<1>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st); break;
+        case 2: rc = tri_a<2>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st); break;
+        default: rc = tri_a<3>(packed, t0, t1, theta, (int)n, ws, red, err_dev, st); break;
     }
+    if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_mds_tri_reduce_len(n, dim) - 1, st);
+    return MMK_OK;
 }
 
 extern "C" int mmk_mds_tri_iter_b(const float* theta, float* theta_out, int64_t dim, int64_t n,
-                                  const double* red, double* f_dev, void* stream) {
+                                  const double* red, double* f_dev, int64_t* err_dev,
+                                  void* stream) {
     if (dim < 1 || dim > kMaxTriDim || n < 2) {
         mmk_host::set_error("bad packed-triangle MDS shape: n=%lld dim=%lld", (long long)n,
                             (long long)dim);
         return MMK_E_SHAPE;
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    mmk_host::peer_err(red + mmk_mds_tri_reduce_len(n, dim) - 1, err_dev, st);
     switch (dim) {
         case 1: return tri_b<1>(theta, theta_out, (int)n, red, f_dev, st);
         case 2: return tri_b<2>(theta, theta_out, (int)n, red, f_dev, st);
@@ -630,7 +636,8 @@ extern "C" int mmk_mds_tri_iter(const float* packed, int64_t t0, int64_t t1, con
                                 float* theta_out, int64_t dim, int64_t n, void* ws,
                                 size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                                 void* stream) {
+    mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_mds_tri_iter_a(packed, t0, t1, theta, dim, n, ws, ws_bytes, red, err_dev, stream);
     if (rc) return rc;
-    return mmk_mds_tri_iter_b(theta, theta_out, dim, n, red, f_dev, stream);
+    return mmk_mds_tri_iter_b(theta, theta_out, dim, n, red, f_dev, err_dev, stream);
 }

@@ -19,6 +19,32 @@ int cuda_status(cudaError_t e, const char* what) {
 }
 }  // namespace mmk_host
 
+namespace {
+__global__ void err_flag_kernel(const int64_t* err, double* flag) {
+    *flag = (err != nullptr && err[0] != 0) ? 1.0 : 0.0;
+}
+__global__ void peer_err_kernel(const double* flag, int64_t* err) {
+    if (*flag > 0.5 && err[0] == 0) err[0] = MMK_E_PEER;   // index stays at its reset value
+}
+}  // namespace
+
+static thread_local bool t_no_flag = false;
+
+namespace mmk_host {
+NoFlag::NoFlag(bool active) : prev(t_no_flag) {
+    if (active) t_no_flag = true;
+}
+NoFlag::~NoFlag() { t_no_flag = prev; }
+void err_flag(const int64_t* err, double* flag, cudaStream_t st) {
+    if (t_no_flag) return;
+    MMK_LAUNCH("mmk_err_flag", st, (err_flag_kernel<<<1, 1, 0, st>>>(err, flag)));
+}
+void peer_err(const double* flag, int64_t* err, cudaStream_t st) {
+    if (t_no_flag || err == nullptr) return;
+    MMK_LAUNCH("mmk_peer_err", st, (peer_err_kernel<<<1, 1, 0, st>>>(flag, err)));
+}
+}  // namespace mmk_host
+
 // ---- opt-in launch profiler --------------------------------------------------
 // Off by default.  When enabled (bench.py), every kernel launch site brackets
 // its launch with CUDA events recorded on the launch stream; mmk_prof_report

@@ -117,6 +117,21 @@ void prof_stop(cudaStream_t s);
 // true the first time `key` (e.g. a kernel's address) is seen on the current
 // device -- for once-per-device kernel attributes (thread-safe)
 bool first_on_device(const void* key);
+// Device errors of sharded runs (one collective per iteration):
+// phase A writes 1.0 into the last slot of its all-reduce payload when this
+// rank's error record is set (err_flag); phase B, after the all-reduce, marks
+// a clean rank whose summed flag is > 0 with MMK_E_PEER (peer_err), so every
+// rank stops at the same iteration.  The host then recovers the first
+// offender with one (rare, slow-path) reduction of the records.
+void err_flag(const int64_t* err, double* flag, cudaStream_t st);
+void peer_err(const double* flag, int64_t* err, cudaStream_t st);
+// Single-GPU iterations (phases A and B back to back, no collective between
+// them) skip both launches: a NoFlag scope around them turns them off.
+struct NoFlag {
+    explicit NoFlag(bool active = true);
+    ~NoFlag();
+    bool prev;
+};
 }  // namespace mmk_host
 
 // Bracket one kernel launch for the opt-in profiler (mmk_prof_enable).

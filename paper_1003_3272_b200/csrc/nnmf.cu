@@ -738,7 +738,8 @@ extern "C" int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, 
     return ws_bytes_for(dtype, m, n, r, false, out);
 }
 
-extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 1; }
+// [P (r n) | G (r r) | f | device-error flag]
+extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 2; }
 
 extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void* V,
                                const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
@@ -748,17 +749,20 @@ extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void
     if (rc) return rc;
     Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 0};
-    return run_a(dtype, a);
+    rc = run_a(dtype, a);
+    if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_nnmf_reduce_len(n, r) - 1, a.st);
+    return MMK_OK;
 }
 
 extern "C" int mmk_nnmf_iter_b(int dtype, const void* W, void* W_out, int64_t n, int64_t r,
                                const double* red, double* f_dev, int64_t* err_dev, void* stream) {
-    (void)err_dev;
     if (r < 1 || n < 1) {
         mmk_host::set_error("bad NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    mmk_host::peer_err(red + mmk_nnmf_reduce_len(n, r) - 1, err_dev, st);
     if (dtype == MMK_F32) return finish_b<float>(W, W_out, n, (int)r, red, f_dev, st);
     if (dtype == MMK_F64) return finish_b<double>(W, W_out, n, (int)r, red, f_dev, st);
     mmk_host::set_error("unknown dtype %d", dtype);
@@ -769,6 +773,7 @@ extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* 
                              void* V_out, void* W_out, int64_t m, int64_t n, int64_t r, void* ws,
                              size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                              void* stream) {
+    mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_nnmf_iter_a(dtype, X, ldx, V, W, V_out, m, n, r, ws, ws_bytes, red, err_dev,
                              stream);
     if (rc) return rc;
@@ -805,6 +810,7 @@ extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const vo
            reinterpret_cast<cudaStream_t>(stream), 3};
     rc = run_a(dtype, a);
     if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_nnmf_reduce_len(n, r) - 1, a.st);
     return mmk_nnmf_iter_b(dtype, W, W_out, n, r, red, nullptr, err_dev, stream);
 }
 

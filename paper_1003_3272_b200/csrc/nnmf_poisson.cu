@@ -385,7 +385,8 @@ extern "C" int mmk_nnmf_poisson_ws_bytes(int dtype, int64_t m, int64_t n, int64_
     return MMK_OK;
 }
 
-extern "C" int64_t mmk_nnmf_poisson_reduce_len(int64_t n, int64_t r) { return r * n + r + 1; }
+// [P (r n) | column sums of V' (r) | f | device-error flag]
+extern "C" int64_t mmk_nnmf_poisson_reduce_len(int64_t n, int64_t r) { return r * n + r + 2; }
 
 extern "C" int mmk_nnmf_poisson_iter_a(int dtype, const void* X, int64_t ldx, const void* V,
                                        const void* W, void* V_out, int64_t m, int64_t n,
@@ -395,18 +396,21 @@ extern "C" int mmk_nnmf_poisson_iter_a(int dtype, const void* X, int64_t ldx, co
     if (rc) return rc;
     Args a{X, V, W, V_out, ldx, m, n, (int)r, ws, red, err_dev,
            reinterpret_cast<cudaStream_t>(stream)};
-    return dtype == MMK_F32 ? dispatch<float>(a) : dispatch<double>(a);
+    rc = dtype == MMK_F32 ? dispatch<float>(a) : dispatch<double>(a);
+    if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_nnmf_poisson_reduce_len(n, r) - 1, a.st);
+    return MMK_OK;
 }
 
 extern "C" int mmk_nnmf_poisson_iter_b(int dtype, const void* W, void* W_out, int64_t n,
                                        int64_t r, const double* red, double* f_dev,
                                        int64_t* err_dev, void* stream) {
-    (void)err_dev;
     if (r < 1 || r > kMaxPoisRank || n < 1) {
         mmk_host::set_error("bad Poisson NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    mmk_host::peer_err(red + mmk_nnmf_poisson_reduce_len(n, r) - 1, err_dev, st);
     const long long rn = r * n;
     if (dtype == MMK_F32)
         MMK_LAUNCH("pois_wfinish", st,
@@ -428,6 +432,7 @@ extern "C" int mmk_nnmf_poisson_iter(int dtype, const void* X, int64_t ldx, cons
                                      const void* W, void* V_out, void* W_out, int64_t m,
                                      int64_t n, int64_t r, void* ws, size_t ws_bytes, double* red,
                                      double* f_dev, int64_t* err_dev, void* stream) {
+    mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, V, W, V_out, m, n, r, ws, ws_bytes, red,
                                      err_dev, stream);
     if (rc) return rc;

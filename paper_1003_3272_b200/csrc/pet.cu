@@ -758,7 +758,8 @@ extern "C" int mmk_pet_ws_bytes(int dtype, int64_t d, int64_t p, size_t* out) {
     return MMK_OK;
 }
 
-extern "C" int64_t mmk_pet_reduce_len(int64_t p) { return p + 1; }
+// [b (p) | loglik | device-error flag]
+extern "C" int64_t mmk_pet_reduce_len(int64_t p) { return p + 2; }
 
 extern "C" int mmk_pet_iter_a(int dtype, const void* E, int64_t lde, const void* y,
                               const void* lam, int64_t d, int64_t p, void* ws, size_t ws_bytes,
@@ -773,13 +774,18 @@ extern "C" int mmk_pet_iter_a(int dtype, const void* E, int64_t lde, const void*
     if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == MMK_F32)
-        return pet_a<float>((const float*)E, lde, (const float*)y, (const float*)lam, d, p, L, red,
-                            err_dev, st);
-    if (dtype == MMK_F64)
-        return pet_a<double>((const double*)E, lde, (const double*)y, (const double*)lam, d, p, L,
-                             red, err_dev, st);
-    mmk_host::set_error("unknown dtype %d", dtype);
-    return MMK_E_SHAPE;
+        rc = pet_a<float>((const float*)E, lde, (const float*)y, (const float*)lam, d, p, L, red,
+                          err_dev, st);
+    else if (dtype == MMK_F64)
+        rc = pet_a<double>((const double*)E, lde, (const double*)y, (const double*)lam, d, p, L,
+                           red, err_dev, st);
+    else {
+        mmk_host::set_error("unknown dtype %d", dtype);
+        return MMK_E_SHAPE;
+    }
+    if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_pet_reduce_len(p) - 1, st);
+    return MMK_OK;
 }
 
 extern "C" int mmk_pet_iter_b(int dtype, const void* lam, void* lam_out, int64_t p,
@@ -794,6 +800,7 @@ extern "C" int mmk_pet_iter_b(int dtype, const void* lam, void* lam_out, int64_t
     int rc = check_ws(0, p, ws, ws_bytes, &L);
     if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    mmk_host::peer_err(red + mmk_pet_reduce_len(p) - 1, err_dev, st);
     if (dtype == MMK_F32)
         return pet_b<float>((const float*)lam, (float*)lam_out, p, nbr_ptr, nbr_idx, mu, flags, red,
                             L, f_dev, err_dev, st);
@@ -809,6 +816,7 @@ extern "C" int mmk_pet_iter(int dtype, const void* E, int64_t lde, const void* y
                             const int32_t* nbr_idx, double mu, int flags, void* ws,
                             size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                             void* stream) {
+    mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_pet_iter_a(dtype, E, lde, y, lam, d, p, ws, ws_bytes, red, err_dev, stream);
     if (rc) return rc;
     return mmk_pet_iter_b(dtype, lam, lam_out, p, nbr_ptr, nbr_idx, mu, flags, red, ws, ws_bytes,
@@ -840,15 +848,21 @@ extern "C" int mmk_pet_sparse_iter_a(int dtype, const int32_t* rptr, const int32
     SparseWs L;
     sparse_ws_layout(d, p, ws, &L);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int rc;
     if (dtype == MMK_F32)
-        return pet_sparse_a<float>(rptr, ridx, (const float*)rval, cptr, cidx, (const float*)cval,
-                                   (const float*)y, (const float*)lam, d, p, L, red, err_dev, st);
-    if (dtype == MMK_F64)
-        return pet_sparse_a<double>(rptr, ridx, (const double*)rval, cptr, cidx,
-                                    (const double*)cval, (const double*)y, (const double*)lam, d, p,
-                                    L, red, err_dev, st);
-    mmk_host::set_error("unknown dtype %d", dtype);
-    return MMK_E_SHAPE;
+        rc = pet_sparse_a<float>(rptr, ridx, (const float*)rval, cptr, cidx, (const float*)cval,
+                                 (const float*)y, (const float*)lam, d, p, L, red, err_dev, st);
+    else if (dtype == MMK_F64)
+        rc = pet_sparse_a<double>(rptr, ridx, (const double*)rval, cptr, cidx,
+                                  (const double*)cval, (const double*)y, (const double*)lam, d, p,
+                                  L, red, err_dev, st);
+    else {
+        mmk_host::set_error("unknown dtype %d", dtype);
+        return MMK_E_SHAPE;
+    }
+    if (rc) return rc;
+    mmk_host::err_flag(err_dev, red + mmk_pet_reduce_len(p) - 1, st);
+    return MMK_OK;
 }
 
 // single-GPU sparse iteration: the forward projection, then ONE kernel that
@@ -863,6 +877,7 @@ extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t
                                    size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                                    void* stream) {
     if (d == 0 || (dtype != MMK_F32 && dtype != MMK_F64)) {
+        mmk_host::NoFlag one_gpu;
         int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lam, d, p,
                                        ws, ws_bytes, red, err_dev, stream);
         if (rc) return rc;

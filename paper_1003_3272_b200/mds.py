@@ -383,7 +383,7 @@ class _GpuMdsTri(DeviceMm):
             import torch.distributed as dist
             dist.all_reduce(self.red, group=self.group)
         L.call("mmk_mds_tri_iter_b", L.ptr(theta), L.ptr(out), self.dim, self.n, L.ptr(self.red),
-               f_ptr, st)
+               f_ptr, err_ptr, st)
 
     def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
         self._keep = (a, b)

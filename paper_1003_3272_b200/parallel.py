@@ -106,19 +106,21 @@ class ShardedNnmf:
         return self.status.f_ptr
 
 
-def phase_a_model(x, v, w):
-    """Host fp64 model of phase A's buffer for one shard (tests only)."""
+def phase_a_model(x, v, w, error=False):
+    """Host fp64 model of phase A's buffer for one shard (tests only):
+    [P | G_V' | f | device-error flag]."""
     q = x @ w.T
     g_w = w @ w.T
     v2 = v * (q / (v @ g_w + 1e-300))
     f = float(np.sum((x - v @ w) ** 2))
-    return v2, np.concatenate([(v2.T @ x).ravel(), (v2.T @ v2).ravel(), [f]])
+    return v2, np.concatenate([(v2.T @ x).ravel(), (v2.T @ v2).ravel(), [f, float(error)]])
 
 
 def phase_b_model(w, red, n, r):
+    """W', f, and whether any rank flagged a device error (all ranks agree)."""
     p = red[:r * n].reshape(r, n)
     g = red[r * n:r * n + r * r].reshape(r, r)
-    return w * (p / (g @ w + 1e-300)), red[-1]
+    return w * (p / (g @ w + 1e-300)), red[r * n + r * r], red[r * n + r * r + 1] > 0.5
 
 
 def tri_tiles(n, tile=128):
@@ -129,7 +131,8 @@ def tri_tiles(n, tile=128):
 
 def tri_phase_a_model(y, theta, t0, t1, tile=128):
     """Host fp64 model of ``mmk_mds_tri_iter_a`` for tiles [t0, t1) (tests
-    only): red = [C (n x dim, row-major) | stress partial | S if t0 == 0]."""
+    only): red = [C (n x dim, row-major) | stress partial | S if t0 == 0 |
+    device-error flag]."""
     dim, n = theta.shape
     c = np.zeros((n, dim))
     stress = 0.0
@@ -147,7 +150,7 @@ def tri_phase_a_model(y, theta, t0, t1, tile=128):
         np.add.at(c, ii, (z * g).T)
         np.add.at(c, jj, -(z * g).T)
     s = theta.sum(1) if t0 == 0 else np.zeros(dim)
-    return np.concatenate([c.ravel(), [stress], s])
+    return np.concatenate([c.ravel(), [stress], s, [0.0]])
 
 
 def tri_phase_b_model(theta, red):
@@ -160,36 +163,78 @@ def tri_phase_b_model(theta, red):
 
 
 # ---------------------------------------------------------------------------
-# Public sharded solvers (one process per GPU, torch.distributed NCCL group).
-# Each iteration: phase A on this rank's rows / tiles, ONE all-reduce of the
-# fp64 reduction buffer (plus the device error record, so every rank raises
-# together), phase B redundantly on every rank; run_mm's per-iteration
-# protocol drives it (the objective is the all-reduced value).
-def _allreduce_status(status, group):
+# Public sharded solvers (one process per GPU, torch.distributed group).
+# Each iteration: phase A on this rank's rows / tiles / rays, ONE all-reduce
+# of the fp64 reduction buffer -- whose last slot carries the device-error
+# flag (csrc: mmk_host::err_flag / peer_err), so every rank stops at the same
+# iteration -- and phase B redundantly on every rank.
+#
+# With an NCCL group and Backend(fused=True) the whole run is the device
+# engine: the per-iteration kernels and the ncclAllReduce captured in ONE CUDA
+# graph with the stopping rule on the device (csrc/engine.cu).  Otherwise
+# (gloo, fused=False) run_mm's per-iteration protocol drives it with the
+# all-reduce issued through torch.distributed.  Either way the objective
+# trace is the all-reduced value and identical on every rank.
+MMK_E_PEER = 6   # include/mmk.h: error-record code "another rank flagged an error"
+
+
+def _combine_error_records(status, group):
+    """Slow path, only after a device error: every rank's record is nonzero
+    (its own error, or MMK_E_PEER); reduce them to the first real offender
+    (largest code, then smallest index) so all ranks raise the same error."""
+    import torch
     import torch.distributed as dist
     rec = status.dev[1:3].clone()
-    code, idx = rec[0:1].clone(), rec[1:2].clone()
+    code = rec[0:1].clone()
+    code[code == MMK_E_PEER] = 0
     dist.all_reduce(code, op=dist.ReduceOp.MAX, group=group)
+    idx = rec[1:2].clone()
+    idx[rec[0:1] != code] = torch.iinfo(torch.int64).max
     dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
     status.dev[1:2].copy_(code)
     status.dev[2:3].copy_(idx)
 
 
+def _shard(mm, group, iter_fns=None):
+    """Configure a DeviceMm for a sharded run (see the section comment)."""
+    mm.group = group
+    comm = nccl_comm_ptr(group) if group is not None else None
+    mm.comm = comm
+    mm._fused = bool(mm.backend.fused) and comm is not None
+    base_check = mm._check_error
+
+    def _check_error():
+        f, code, _ = mm.status.read()
+        if code == 0:
+            return f
+        if group is not None:
+            _combine_error_records(mm.status, group)
+        return base_check()
+    mm._check_error = _check_error
+    return mm
+
+
+def _default_group(group):
+    if group is None:   # the default process group, as torch.distributed collectives use it
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            group = dist.group.WORLD
+    return group
+
+
 def _make_sharded_nnmf(base_cls, iter_a, iter_b):
     class _Sharded(base_cls):
-        def __init__(self, problem, backend, group):
-            super().__init__(problem, backend)
-            self._fused = False     # per-iteration protocol
-            self.group = group
-
         def _iterate(self, s, out, f_ptr, err_ptr):
             from . import _lib as L
             st = self.stream()
             L.call(iter_a, self.code, L.ptr(self.x), self.x.stride(0), L.ptr(s.v), L.ptr(s.w),
                    L.ptr(out.v), self.m, self.n, self.r, L.ptr(self.ws), self.ws.numel(),
                    L.ptr(self.red), err_ptr, st)
-            allreduce_sum_(self.red, self.group)
-            _allreduce_status(self.status, self.group)
+            if self.comm is not None:
+                L.call("mmk_allreduce_f64", L.ptr(self.red), self.red.numel(),
+                       L.ctypes.c_void_p(self.comm), st)
+            elif self.group is not None:
+                allreduce_sum_(self.red, self.group)
             L.call(iter_b, self.code, L.ptr(s.w), L.ptr(out.w), self.n, self.r, L.ptr(self.red),
                    f_ptr, err_ptr, st)
     return _Sharded
@@ -205,13 +250,14 @@ def nnmf_run_sharded(x_local, rank, config, backend, group=None, state0=None, po
     from .driver import run_mm
     if state0 is None:
         raise ValueError("nnmf_run_sharded needs state0 = (V_local, W)")
+    group = _default_group(group)
     prob = N.NnmfProblem(x=x_local, rank=rank)
     if poisson:
         cls = _make_sharded_nnmf(N._GpuPoissonNnmf, "mmk_nnmf_poisson_iter_a",
                                  "mmk_nnmf_poisson_iter_b")
     else:
         cls = _make_sharded_nnmf(N._GpuNnmf, "mmk_nnmf_iter_a", "mmk_nnmf_iter_b")
-    mm = cls(prob, backend, group)
+    mm = _shard(cls(prob, backend), group)
     state, trace = run_mm(mm, mm.device_state(N.FactorPair(state0[0], state0[1])), config)
     return state, trace
 
@@ -230,23 +276,13 @@ def mds_run_sharded(problem, config, backend, group=None, theta0=None):
     theta is replicated."""
     from . import mds as D
     from .driver import run_mm
-    if group is None:   # the default process group, as torch.distributed collectives use it
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized():
-            group = dist.group.WORLD
+    group = _default_group(group)
     if not isinstance(problem, D.PackedMdsProblem):
         return _mds_rows_sharded(problem, config, backend, group, theta0)
     if theta0 is None:
         theta0 = np.random.default_rng(config.seed).uniform(-1.0, 1.0,
                                                             size=(problem.p, problem.q))
-    mm = D._GpuMdsTri(problem, backend, group=group)
-    mm._fused = False
-    base_iter = mm._iterate
-
-    def _iterate(theta, out, f_ptr, err_ptr):
-        base_iter(theta, out, f_ptr, err_ptr)
-        _allreduce_status(mm.status, group)
-    mm._iterate = _iterate
+    mm = _shard(D._GpuMdsTri(problem, backend, group=group), group)
     return run_mm(mm, mm.device_state(theta0), config)
 
 
@@ -311,7 +347,7 @@ def _mds_rows_sharded(problem, config, backend, group, theta0):
             if group is not None:
                 dist.all_reduce(self.status.dev[0:1].view(self.torch.float64), group=group)
                 dist.all_gather(self.parts, self.local, group=group)
-                _allreduce_status(self.status, group)
+                _combine_error_records(self.status, group)
             else:
                 self.parts[0].copy_(self.local)
             for r, (a, b) in enumerate(bounds):
@@ -335,8 +371,7 @@ def pet_run_sharded(problem, config, backend, group=None):
     from . import _lib as L
     from . import pet as PT
     from .driver import run_mm
-    if group is None and dist.is_available() and dist.is_initialized():
-        group = dist.group.WORLD
+    group = _default_group(group)
     world = dist.get_world_size(group) if group is not None else 1
     rank = dist.get_rank(group) if group is not None else 0
     lo, hi = shard_rows(problem.n_rays, world, rank)
@@ -355,12 +390,14 @@ def pet_run_sharded(problem, config, backend, group=None):
                 L.call("mmk_pet_iter_a", self.code, P(self.e), self.e.stride(0), P(self.y),
                        P(lam), self.d, self.p, P(self.ws), self.ws.numel(), P(self.red), err_ptr,
                        st)
-            allreduce_sum_(self.red, group)
-            _allreduce_status(self.status, group)
+            if self.comm is not None:
+                L.call("mmk_allreduce_f64", P(self.red), self.red.numel(),
+                       L.ctypes.c_void_p(self.comm), st)
+            elif group is not None:
+                allreduce_sum_(self.red, group)
             L.call("mmk_pet_iter_b", self.code, P(lam), P(out), self.p, P(self.ptr), P(self.idx),
                    self.mu, flags, P(self.red), P(self.ws), self.ws.numel(), f_ptr, err_ptr, st)
 
-    mm = _Sharded(problem, backend, rows=(lo, hi))
-    mm._fused = False     # per-iteration protocol
+    mm = _shard(_Sharded(problem, backend, rows=(lo, hi)), group)
     state, trace = run_mm(mm, mm.device_state(np.ones(problem.n_pixels)), config)
     return A.to_user(state, problem.e), trace

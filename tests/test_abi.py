@@ -38,8 +38,8 @@ def test_workspace_queries_are_host_only():
     assert _lib.ws_bytes("mmk_nnmf_ws_bytes", 0, 2429, 361, 10) > 0
     assert _lib.ws_bytes("mmk_pet_ws_bytes", 0, 2016, 4096) > 0
     assert _lib.ws_bytes("mmk_mds_ws_bytes", 0, 401, 3, 401) > 0
-    assert lib.mmk_nnmf_reduce_len(361, 10) == 3610 + 100 + 1
-    assert lib.mmk_pet_reduce_len(4096) == 4097
+    assert lib.mmk_nnmf_reduce_len(361, 10) == 3610 + 100 + 2   # [P | G | f | error flag]
+    assert lib.mmk_pet_reduce_len(4096) == 4098   # [b | loglik | error flag]
 
 
 def test_shape_errors_map_to_exceptions():

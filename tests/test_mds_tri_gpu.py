@@ -181,7 +181,7 @@ def test_tri_sharded_slices_sum_to_the_whole():
     out = torch.empty_like(theta)
     f = torch.zeros(1, dtype=torch.float64, device="cuda")
     _lib.call("mmk_mds_tri_iter_b", _lib.ptr(theta), _lib.ptr(out), dim, n, _lib.ptr(total),
-              _lib.ptr(f), mm.stream())
+              _lib.ptr(f), mm.status.err_ptr, mm.stream())
     torch.cuda.synchronize()
     assert abs(float(f) - f_ref) / f_ref <= 1e-6
     assert float((out - ref_out).norm() / ref_out.norm()) <= 1e-6

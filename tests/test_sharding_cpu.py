@@ -47,15 +47,15 @@ def test_tile_partition_covers_and_balances():
             assert max(sizes) - min(sizes) <= 1
 
 
-def _nnmf_worker(rank, world, port, x, v, w, out):
+def _nnmf_worker(rank, world, port, x, v, w, out, bad_rank=-1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = P.shard_rows(x.shape[0], world, rank)
-    v2, red = P.phase_a_model(x[lo:hi], v[lo:hi], w)
+    v2, red = P.phase_a_model(x[lo:hi], v[lo:hi], w, error=rank == bad_rank)
     t = torch.from_numpy(red)
     P.allreduce_sum_(t)
-    w2, f = P.phase_b_model(w, t.numpy(), x.shape[1], v.shape[1])
-    out[rank] = (lo, hi, v2, w2, f)
+    w2, f, err = P.phase_b_model(w, t.numpy(), x.shape[1], v.shape[1])
+    out[rank] = (lo, hi, v2, w2, f, err)
     dist.destroy_process_group()
 
 
@@ -74,6 +74,20 @@ def test_nnmf_row_sharding_gloo():
         np.testing.assert_allclose(res[r][3], w_ref, rtol=1e-12)
     np.testing.assert_allclose(v_sh, v_ref, rtol=1e-12)
     np.testing.assert_array_equal(res[0][3], res[1][3])   # W' replicated bitwise
+    assert not res[0][5] and not res[1][5]
+
+
+def test_device_error_flag_reaches_every_rank_gloo():
+    """The device-error flag rides in the one all-reduce of the phase-A buffer
+    (csrc: mmk_host::err_flag / peer_err): an error on rank 1 of 3 stops all
+    three at the same iteration."""
+    rng = np.random.default_rng(2)
+    x, v, w = rng.random((30, 11)), rng.random((30, 3)), rng.random((3, 11))
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_nnmf_worker, args=(3, _free_port(), x, v, w, out, 1), nprocs=3, join=True)
+        res = dict(out)
+    assert all(res[r][5] for r in range(3))
 
 
 def _mds_worker(rank, world, port, y, theta, out):
