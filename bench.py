@@ -140,6 +140,27 @@ def dist_info():
 
 
 # ----------------------------------------------------------------------------- CPU arm
+def host_cpu():
+    """lscpu model name, physical cores and logical CPUs of this host
+    (state the core count the CPU number was taken on)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        sockets = int(kv.get("Socket(s)", "1"))
+        cores = int(kv.get("Core(s) per socket", "0"))
+        info["physical_cores"] = sockets * cores or None
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return info
+
+
+
 def cpu_sample(workload, seconds):
     """Time the CPU oracle on a bounded sample of `workload`; returns the
     extrapolated full-size iterations/s plus a description."""
@@ -254,7 +275,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, W, world),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "host": host_cpu()},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": elapsed,
@@ -303,7 +324,10 @@ def bench_nnmf_large(args, torch, world, rank, dev):
     prob = M.NnmfProblem(x=x, rank=r)
 
     def api_run(iters):
-        cfg = M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6)
+        # (kernel timing experiments that disable parts of the objective turn
+        # the descent check off; they never produce a bench number)
+        cfg = M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6,
+                         check_monotone="MMK_TC_EXP" not in os.environ)
         if world > 1:
             return nnmf_run_sharded(x, r, cfg, be, group=group, state0=(v0, w0))
         return M.nnmf_run(prob, cfg, be, state0=M.FactorPair(v0, w0))
@@ -377,25 +401,38 @@ def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
 def bench_mds_large(args, torch, world, rank, dev):
     """BASELINE config 5: MDS n = 65536, dim 3, unit weights, packed upper
     triangle; tiles split evenly across ranks (one all-reduce of the
-    per-point accumulators per iteration)."""
+    per-point accumulators per iteration).  `value` times the public API
+    (mds_run / mds_run_sharded) with the tiles resident in HBM; the kernel
+    breakdown comes from a launch-profiled loop of the same iteration; `e2e`
+    uploads the packed tiles from pinned host memory inside the timed run."""
+    import torch.distributed as dist
+
     import paper_1003_3272_b200 as M
-    from paper_1003_3272_b200 import _lib, datasets as D
+    from paper_1003_3272_b200 import datasets as D
     from paper_1003_3272_b200.mds import PackedMdsProblem, _GpuMdsTri, tile_count
-    from paper_1003_3272_b200.parallel import tile_range
+    from paper_1003_3272_b200.parallel import mds_run_sharded, tile_range
     W = WORKLOADS[args.workload]
     n, dim = W["n"], W["dim"]
     be = M.Backend(dtype="fp32", device=dev.index, mds_kernel="tri")
     nt = tile_count(n)
     t0, t1 = tile_range(nt, world, rank)
     prob = PackedMdsProblem.from_rows(D.distance_rows(n, seed=0), n, dim, be, tiles=(t0, t1))
-    # sharded: one all-reduce of the per-point accumulators per iteration,
-    # issued through torch.distributed (NCCL) on the compute stream
-    import torch.distributed as dist
-    mm = _GpuMdsTri(prob, be, group=dist.group.WORLD if world > 1 else None)
+    group = dist.group.WORLD if world > 1 else None
     g = torch.Generator(device=dev)
     g.manual_seed(2)
-    th = [torch.rand(dim, n, generator=g, device=dev) * 2 - 1, None]
-    th[1] = torch.empty_like(th[0])
+    th0 = torch.rand(dim, n, generator=g, device=dev) * 2 - 1
+
+    def api_run(iters, problem=prob):
+        cfg = M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6)
+        if world > 1:
+            return mds_run_sharded(problem, cfg, be, group=group, theta0=th0)
+        return M.mds_run(problem, cfg, be, theta0=th0)
+
+    timing = time_region(args, torch, dev, lambda: api_run(args.warmup),
+                         lambda: api_run(args.steps), world)
+    # launch-profiled loop (kernel breakdown, roofline)
+    mm = _GpuMdsTri(prob, be, group=group)
+    th = [th0.clone(), torch.empty_like(th0)]
     cur = [0]
 
     def step():
@@ -403,8 +440,7 @@ def bench_mds_large(args, torch, world, rank, dev):
         mm._iterate(th[a], th[1 - a], mm.status.f_ptr, mm.status.err_ptr)
         cur[0] = 1 - a
 
-    timing = time_steps(args, torch, dev, step, world)
-    prof = timing["prof"]
+    prof = time_steps(args, torch, dev, step, world)["prof"]
     alg = {"mds_tri": (t1 - t0) * 128 * 128 * 4 + 2 * dim * n * 4}
     launches = sum(c for c, _ in prof.values()) // args.steps
     roof = roofline(prof, alg, "hbm", "dominant")
@@ -412,8 +448,37 @@ def bench_mds_large(args, torch, world, rank, dev):
                for k, (c, ms) in prof.items()}
     mm._check_error()
     e2e = None
+    if not args.no_e2e and world == 1:
+        host = torch.empty(prob.packed.numel(), dtype=torch.float32, pin_memory=True)
+        host.copy_(prob.packed)
+        del mm, th
+
+        def run():
+            torch.cuda.synchronize()
+            t_0 = time.perf_counter()
+            p2 = PackedMdsProblem.from_packed(host, n, dim, be, tiles=(t0, t1))
+            cfg = M.MmConfig(max_iters=args.steps, epsilon=1e-300, monotone_tol=1e-6)
+            th_out, tr = M.mds_run(p2, cfg, be, theta0=th0.cpu().numpy())
+            th_h = th_out.cpu() if hasattr(th_out, "cpu") else th_out
+            torch.cuda.synchronize()
+            return tr, th_h, time.perf_counter() - t_0
+
+        run()
+        tr, th_h, dt = run()
+        K = tr.iters
+        h2d = host.numel() * 4 + dim * n * 8
+        d2h = dim * n * 8 + 8 * (K + 1)
+        e2e = {"value": K / dt, "unit": "iterations/s", "h2d_bytes_per_step": h2d // max(K, 1),
+               "d2h_bytes_per_step": d2h // max(K, 1), "iters": K,
+               "phases_ms": {"total": 1e3 * dt, "device_loop": 1e3 * tr.wall_time,
+                             "upload_setup_readback": 1e3 * (dt - tr.wall_time)},
+               "path": "PackedMdsProblem.from_packed(pinned host tiles) + mds_run(host theta0) "
+                       "-> host theta; second of two runs"}
     return timing, roof, launches, e2e, {
-        "kernels": kernels, "e2e_note": "not measured for mds-large this round",
+        "kernels": kernels,
+        "value_path": ("mds_run_sharded (device-loop engine, NCCL all-reduce in its graph)"
+                       if world > 1 else "mds_run (device-loop engine)") +
+                      " on the packed tiles resident in HBM",
         "data": "synthetic (Y_ij = ||z_i - z_j||(1 + 0.05 e_ij), z ~ N(0, I_10), e from a "
                 "symmetric pair hash; theta0 uniform[-1,1]; datasets.distance_rows)"}
 
@@ -668,7 +733,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, thr, sample = cpu_sample(args.workload, args.cpu_seconds)
         cpu = {"value": v, "unit": "iterations/s", "cores": thr, "kind": "port",
-               "sample": sample}
+               "sample": sample, "host": host_cpu()}
         if not args.no_suite:
             suite_res = suite(args, torch, dev)
     if rank == 0:

@@ -73,7 +73,14 @@ constexpr uint32_t SXH = BM * BK * 2;       // 16 KB  fp16 X tile [128 x 64]
 constexpr uint32_t SX = 2 * SXH;            // 32 KB  X stage [X_hi | X_lo]
 constexpr uint32_t SOP = R * BK * 2;        //  8 KB  fp16 operand chunk hi; same again for lo
 constexpr uint32_t SGW = R * R * 4;         // 16 KB  G_W (fp32) for the V-step epilogue
-constexpr int XST = 4;                      // X ring (128 KB in flight per SM)
+constexpr int XST = 4;                      // W step X ring (128 KB in flight per SM)
+#ifndef MMK_TC_XSTV
+#define MMK_TC_XSTV 4
+#endif
+constexpr int XSTV = MMK_TC_XSTV;           // V step X ring
+#ifndef MMK_TC_GW_SMEM
+#define MMK_TC_GW_SMEM 1
+#endif
 #ifndef MMK_TC_OST
 #define MMK_TC_OST 3
 #endif
@@ -83,7 +90,7 @@ constexpr int NRES = 8;                     // residual warps (two groups of 4)
 constexpr int kVThreads = 32 * (2 + NRES + 4);   // TMA, MMA, residual x8, epilogue x4
 constexpr int kWThreads = 32 * (2 + 4);          // TMA, MMA, epilogue x4
 constexpr uint32_t SVH = BM * R * 2;        // 16 KB  V_h tile [128 rows x 64 ranks]
-constexpr uint32_t SMEM_V = XST * SX + OST * 2 * SOP + 2 * SVH + SGW + 1024;
+constexpr uint32_t SMEM_V = XSTV * SX + OST * 2 * SOP + 2 * SVH + (MMK_TC_GW_SMEM ? SGW : 0) + 1024;
 constexpr int OSTW = 3;                     // W step operand ring (a V'^T chunk feeds CB stages)
 constexpr uint32_t SMEM_W = XST * SX + OSTW * 2 * SOP + 1024;
 static_assert(SMEM_V + 2048 <= 232448, "dynamic + static shared memory per CTA");
@@ -161,7 +168,7 @@ struct Scales {
 // Pipeline per 64-column stage `it` of a 128-row tile (pass p = tile):
 //   TMA      V_h tile of the pass (split_v_kernel's fp16 V, per-row scale);
 //            per stage the W chunk [W_hi ; W_lo] -> operand slot it % OST and
-//            the X stage [X_hi | X_lo] -> slot it % XST
+//            the X stage [X_hi | X_lo] -> slot it % XSTV
 //   MMA      Q(it) += X_hi [W_hi ; W_lo] + X_lo W_hi (8 SS MMAs), commit ->
 //            xempty; R'(it) = V_h [W_hi | W_lo] (4 SS MMAs N = 128, B = the W
 //            chunk read MN-major: rows = ranks = K, W_hi and W_lo two 64-column
@@ -174,7 +181,7 @@ struct Scales {
 // the 12 MMAs of a stage make this kernel tensor-issue bound (~1.75 ms at C4,
 // against ~1.3 ms for the 8 Q MMAs alone); DESIGN.md has the measurements.
 struct VBars {
-    uint64_t xfull[XST], xempty[XST], ofull[OST], oempty[OST];
+    uint64_t xfull[XSTV], xempty[XSTV], ofull[OST], oempty[OST];
     uint64_t vfull[2], vempty[2];       // V_h tiles of a pass (TMA -> MMA)
     uint64_t dfull[2], dempty[2];       // Q accumulator sets: MMA -> epilogue
     uint64_t rfull[NRB], rempty[NRB];   // residual buffers: MMA -> residual warps
@@ -200,7 +207,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
-    uint8_t* oring = base + XST * SX;
+    uint8_t* oring = base + XSTV * SX;
     uint8_t* vbuf = oring + OST * 2 * SOP;
     float* gws = reinterpret_cast<float*>(vbuf + 2 * SVH);
     __shared__ VBars B;
@@ -212,10 +219,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     const int G = (int)gridDim.x, me = (int)blockIdx.x;
     const int mine = ntiles > me ? (ntiles - 1 - me) / G + 1 : 0;
     // G_W rounded to fp32 (gram_sum_kernel), staged for the denominator rows
-    for (int i = threadIdx.x; i < R * R / 4; i += kVThreads)
-        reinterpret_cast<float4*>(gws)[i] = __ldg(reinterpret_cast<const float4*>(GWf) + i);
+    if (MMK_TC_GW_SMEM)
+        for (int i = threadIdx.x; i < R * R / 4; i += kVThreads)
+            reinterpret_cast<float4*>(gws)[i] = __ldg(reinterpret_cast<const float4*>(GWf) + i);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < XST; ++s) {
+        for (int s = 0; s < XSTV; ++s) {
             tc::mbar_init(&B.xfull[s], 1);
             tc::mbar_init(&B.xempty[s], 5);   // the residual group's 4 warps + the Q MMAs' commit
         }
@@ -256,12 +264,12 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::mbar_expect_tx(&B.vfull[vb], SVH);
                 tc::tma_load_2d(vbuf + vb * SVH, &mVh, &B.vfull[vb], 0, tile * BM);
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XST;
+                    const int os = it % OST, xs = it % XSTV;
                     tc::mbar_wait(&B.oempty[os], ((it / OST) & 1) ^ 1);
                     tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
                     tc::tma_load_2d(oring + os * 2 * SOP, &mWh, &B.ofull[os], kb * BK, 0);
                     tc::tma_load_2d(oring + os * 2 * SOP + SOP, &mWl, &B.ofull[os], kb * BK, 0);
-                    tc::mbar_wait(&B.xempty[xs], ((it / XST) & 1) ^ 1);
+                    tc::mbar_wait(&B.xempty[xs], ((it / XSTV) & 1) ^ 1);
                     tc::mbar_expect_tx(&B.xfull[xs], SX);
                     tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], kb * BK, tile * BM);
                     tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], kb * BK, tile * BM);
@@ -279,9 +287,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::tc_fence_after();
                 const uint64_t va = tc::sdesc_sw128(vbuf + b * SVH, 16, 1024);
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XST, rb = it % NRB;
+                    const int os = it % OST, xs = it % XSTV, rb = it % NRB;
                     tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
-                    tc::mbar_wait(&B.xfull[xs], (it / XST) & 1);
+                    tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
                     tc::tc_fence_after();
                     const uint8_t* ob = oring + os * 2 * SOP;
                     issue_split_stage(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
@@ -319,8 +327,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 if ((it & 1) != g) continue;
                 // this row's 64 X values of the stage into registers, then release
                 // the slot (its other user is the Q MMA, which commits on xempty)
-                const int xs = it % XST, rb = it % NRB;
-                tc::mbar_wait(&B.xfull[xs], (it / XST) & 1);
+                const int xs = it % XSTV, rb = it % NRB;
+                tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
                 const uint32_t xh = tc::smem_u32(xring + xs * SX) + r * 128;
                 uint4 hv[8], lv[8];
 #pragma unroll
@@ -408,7 +416,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                 gws_s + 4u * (uint32_t)((4 * l4 + e) * R + h * 32 + hh * 8);
 #pragma unroll
                             for (int c4 = 0; c4 < 2; ++c4) {
-                                const float4 gg = tc::lds128f(g4 + 16u * c4);
+                                const float4 gg =
+                                    MMK_TC_GW_SMEM
+                                        ? tc::lds128f(g4 + 16u * c4)
+                                        : __ldg(reinterpret_cast<const float4*>(GWf) +
+                                                (((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4));
                                 den[4 * c4] = fmaf(va[e], gg.x, den[4 * c4]);
                                 den[4 * c4 + 1] = fmaf(va[e], gg.y, den[4 * c4 + 1]);
                                 den[4 * c4 + 2] = fmaf(va[e], gg.z, den[4 * c4 + 2]);

@@ -215,6 +215,21 @@ class PackedMdsProblem:
         return cls(packed, q, p, (t0, t1), dev)
 
     @classmethod
+    def from_packed(cls, packed, n, p, backend=SERIAL, tiles=None):
+        """Already-packed tiles (this layout, e.g. saved from ``packed`` of an
+        earlier problem) as a torch tensor of (t1 - t0) * 128 * 128 fp32
+        values, on the device or in (pinned) host memory -- uploaded as is,
+        no re-validation."""
+        torch = _lib.torch_mod()
+        dev = backend.torch_device()
+        t0, t1 = tiles if tiles is not None else (0, tile_count(n))
+        if not A.is_torch(packed) or packed.dtype != torch.float32 or \
+                packed.numel() != (t1 - t0) * TILE * TILE:
+            raise ShapeError(f"packed tiles must be an fp32 tensor of {(t1 - t0) * TILE * TILE} "
+                             f"values for n={n}, tiles=({t0}, {t1})")
+        return cls(packed.reshape(-1).to(dev, non_blocking=True), n, p, (t0, t1), dev)
+
+    @classmethod
     def from_dense(cls, y, p, backend=SERIAL, tiles=None, validate=True):
         """Full n x n dissimilarities (numpy or torch), checked on the device
         for finiteness, sign, zero diagonal and exact symmetry."""
