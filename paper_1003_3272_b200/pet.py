@@ -125,14 +125,18 @@ class PetProblem:
         kernels back-project from E directly)."""
         return self.e.T
 
-    def device_arrays(self, backend, torch, dense=True):
-        key = (str(backend.torch_device()), backend.dtype, dense)
+    def device_arrays(self, backend, torch, dense=True, rows=None):
+        """E (dense only), y, and the neighbour CSR on the device; with
+        ``rows = (lo, hi)`` (a ray shard) only those rows of E and y are
+        uploaded."""
+        lo, hi = rows if rows is not None else (0, self.n_rays)
+        key = (str(backend.torch_device()), backend.dtype, dense, lo, hi)
         d = self._dev.get(key)
         if d is None:
             dev = backend.torch_device()
             d = {
-                "e": A.to_device(self.e, backend, torch) if dense else None,
-                "y": A.to_device(self.y, backend, torch),
+                "e": A.to_device(self.e[lo:hi], backend, torch) if dense else None,
+                "y": A.to_device(self.y[lo:hi], backend, torch),
                 "ptr": torch.from_numpy(self.nbr_indptr.astype(np.int32)).to(dev),
                 "idx": torch.from_numpy(self.nbr_indices.astype(np.int32)).to(dev),
             }
@@ -278,6 +282,29 @@ def _sparse_arrays(e_rows, backend, torch):
             "cidx": put(csc.indices, np.int32), "cval": put(csc.data, np.float64).to(dt)}
 
 
+def _shard_device_sparse(sa, lo, hi, p, torch):
+    """Rays [lo, hi) of a device-built system matrix, built on the device:
+    the CSR rows (pointers rebased) and the CSC restricted to those rays (ray
+    indices rebased to lo).  Boolean selection keeps every pixel's entries in
+    ray order, so a shard's per-pixel sums run in the unsharded order."""
+    dev = sa["rptr"].device
+    rptr = sa["rptr"].to(torch.int64)
+    a, b = int(rptr[lo]), int(rptr[hi])
+    cidx = sa["cidx"].to(torch.int64)
+    cptr = sa["cptr"].to(torch.int64)
+    keep = (cidx >= lo) & (cidx < hi)
+    col = torch.repeat_interleave(torch.arange(p, device=dev), cptr[1:] - cptr[:-1])
+    cptr_s = torch.zeros(p + 1, dtype=torch.int64, device=dev)
+    cptr_s[1:] = torch.cumsum(torch.bincount(col[keep], minlength=p), 0)
+
+    def nonempty(t):
+        return t if t.numel() else torch.zeros(1, dtype=t.dtype, device=dev)
+    return {"rptr": (rptr[lo:hi + 1] - a).to(torch.int32),
+            "ridx": nonempty(sa["ridx"][a:b]), "rval": nonempty(sa["rval"][a:b]),
+            "cptr": cptr_s.to(torch.int32), "cidx": nonempty((cidx[keep] - lo).to(torch.int32)),
+            "cval": nonempty(sa["cval"][keep])}
+
+
 class _GpuPet(DeviceMm):
     direction = "maximize"
 
@@ -292,23 +319,19 @@ class _GpuPet(DeviceMm):
             sa = problem._dev.get(key)
             if sa is None:
                 if isinstance(problem, SparsePetProblem):
-                    if (lo, hi) != (0, problem.n_rays):
-                        raise ShapeError("ray shards of a device-built system matrix are "
-                                         "not supported")
                     dt = backend.torch_dtype()
                     sa = {k: (v.to(dt) if k in ("rval", "cval") else v)
                           for k, v in problem.sa.items() if k in ("rptr", "ridx", "rval",
                                                                   "cptr", "cidx", "cval")}
+                    if (lo, hi) != (0, problem.n_rays):
+                        sa = _shard_device_sparse(sa, lo, hi, problem.n_pixels, torch)
                 else:
                     e = problem.e if not A.is_torch(problem.e) else problem.e.cpu().numpy()
                     sa = _sparse_arrays(np.asarray(e, dtype=np.float64)[lo:hi], backend, torch)
                 problem._dev[key] = sa
             self.sa = sa
-        d = problem.device_arrays(backend, torch, dense=not self.sparse)
+        d = problem.device_arrays(backend, torch, dense=not self.sparse, rows=(lo, hi))
         self.e, self.y, self.ptr, self.idx = d["e"], d["y"], d["ptr"], d["idx"]
-        self.y = self.y[lo:hi]
-        if self.e is not None:
-            self.e = self.e[lo:hi]
         self.d, self.p = hi - lo, problem.n_pixels
         self.mu = float(problem.mu)
         name = "mmk_pet_sparse_ws_bytes" if self.sparse else "mmk_pet_ws_bytes"

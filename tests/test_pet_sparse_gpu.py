@@ -127,3 +127,37 @@ def test_fused_sparse_iteration_equals_split_phases(dtype, side, det, mu):
         fs.append(float(f.item()))
     assert torch.equal(outs[0], outs[1])
     assert abs(fs[0] - fs[1]) <= 1e-13 * abs(fs[1])
+
+
+def test_device_sparse_ray_shards_sum_to_the_whole():
+    """Ray shards of the device-built matrix (pet._shard_device_sparse): the
+    phase-A buffers [b | loglik] of three shards sum to the unsharded one,
+    and each shard's CSC holds exactly its rays' entries."""
+    import torch
+    from paper_1003_3272_b200 import _lib, parallel as P
+    from paper_1003_3272_b200.pet import _GpuPet
+    geo = M.PetGeometry(24, 32)
+    sa = M.system_matrix_device(geo)
+    y = M.simulate_counts(M.default_phantom(24) + 0.5, M.build_system_matrix(geo), 5)
+    prob = M.SparsePetProblem(sa, y, 1e-4, M.build_neighborhoods(24))
+    be = Backend(dtype="fp64", fused=False)
+    lam = torch.rand(geo.n_pixels, dtype=torch.float64, device="cuda") + 0.5
+
+    def phase_a(mm):
+        s = mm.sa
+        P_ = _lib.ptr
+        _lib.call("mmk_pet_sparse_iter_a", mm.code, P_(s["rptr"]), P_(s["ridx"]), P_(s["rval"]),
+                  P_(s["cptr"]), P_(s["cidx"]), P_(s["cval"]), P_(mm.y), P_(lam), mm.d, mm.p,
+                  P_(mm.ws), mm.ws.numel(), P_(mm.red), mm.status.err_ptr, mm.stream())
+        torch.cuda.synchronize()
+        return mm.red.clone()
+    whole = phase_a(_GpuPet(prob, be))
+    total = torch.zeros_like(whole)
+    nnz = 0
+    for r in range(3):
+        lo, hi = P.shard_rows(geo.n_rays, 3, r)
+        mm = _GpuPet(prob, be, rows=(lo, hi))
+        nnz += int(mm.sa["cptr"][-1])
+        total += phase_a(mm)
+    assert nnz == int(sa["cptr"][-1])
+    assert float((total - whole).abs().max() / whole.abs().max()) <= 1e-13

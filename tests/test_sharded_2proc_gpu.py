@@ -198,3 +198,38 @@ def test_mds_rows_two_ranks(weighted):
                          theta0=th0)
     assert G.rel(t0, rtr.objective_values) <= 1e-12
     assert G.rel(th0s, np.asarray(ref)) <= 1e-10
+
+
+def _pet_device_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import paper_1003_3272_b200 as M
+    from paper_1003_3272_b200 import parallel as P
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        _, y, nbrs = G.c2_inputs()
+        prob = M.SparsePetProblem(M.system_matrix_device(M.PetGeometry(64, 64)), y, 1e-5, nbrs)
+        lam, tr = P.pet_run_sharded(prob, M.MmConfig(max_iters=50, epsilon=1e-300),
+                                    M.Backend(dtype="fp64", fused=False))
+        lam = lam.cpu().numpy() if hasattr(lam, "cpu") else np.asarray(lam)
+        q.put((rank, tr.objective_values, lam, None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e), None, None))
+
+
+def test_pet_device_built_matrix_two_ranks():
+    """Ray shards of a DEVICE-BUILT sparse system matrix (SparsePetProblem):
+    each rank slices its CSR rows and the CSC restricted to its rays on the
+    device (pet._shard_device_sparse); equal to the unsharded run."""
+    import paper_1003_3272_b200 as M
+    out = _run_ranks(_pet_device_worker)
+    (_, t0, l0, _), (_, t1, l1, _) = out
+    assert np.array_equal(t0, t1) and np.array_equal(l0, l1)
+    _, y, nbrs = G.c2_inputs()
+    prob = M.SparsePetProblem(M.system_matrix_device(M.PetGeometry(64, 64)), y, 1e-5, nbrs)
+    ref, rtr = M.pet_run(prob, M.MmConfig(max_iters=50, epsilon=1e-300),
+                         M.Backend(dtype="fp64", fused=False))
+    ref = ref.cpu().numpy() if hasattr(ref, "cpu") else np.asarray(ref)
+    assert G.rel(t0, rtr.objective_values) <= 1e-12
+    assert G.rel(l0, ref) <= 1e-11
