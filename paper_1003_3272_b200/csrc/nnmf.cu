@@ -478,7 +478,7 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, bool tc, void* 
     size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
     size_t o_f = take(sizeof(double) * 4);
     size_t o_wp = take(P.S > 1 ? sizeof(double) * (size_t)P.S * r * (size_t)n : 0);
-    size_t o_tc = take(tc ? mmk_tc::ws_bytes(m, n) : 0);
+    size_t o_tc = take(tc ? mmk_tc::ws_bytes(m, n, r) : 0);
     if (base && L) {
         L->tc = reinterpret_cast<char*>(base) + o_tc;
         char* c = reinterpret_cast<char*>(base);
@@ -613,11 +613,11 @@ struct RunA {
         const T* V = (const T*)a.V;
         const T* W = (const T*)a.W;
         const long long rn = (long long)a.r * a.n;
-        if constexpr (std::is_same<T, float>::value && RMAX == 64) {
+        if constexpr (std::is_same<T, float>::value && (RMAX == 32 || RMAX == 64)) {
             if (a.mode == 0 && tc_region(MMK_F32, a.m, a.n, a.r, true) &&
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
-                return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, L.tc, L.GW,
-                                      a.red, a.st);
+                return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, a.r, L.tc,
+                                      L.GW, a.red, a.st);
             }
         }
         if (a.mode == 0 || a.mode == 1 || a.mode == 2 || a.mode == 4) {

@@ -997,6 +997,29 @@ __global__ void tc_objective_kernel(const double* __restrict__ part, int nparts,
     if (threadIdx.x == 0) *out = f;
 }
 
+// rank r < 64 on the rank-64 kernels: V (m x r) -> V64 (m x 64, zero
+// columns r..63) and back; the rank-64 reduction buffer's G block -> r x r
+__global__ void pad_cols_kernel(const float* __restrict__ src, int r, long long rows,
+                                float* __restrict__ dst) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * R) return;
+    const long long i = t / R;
+    const int k = (int)(t % R);
+    dst[t] = k < r ? src[i * r + k] : 0.f;
+}
+__global__ void unpad_cols_kernel(const float* __restrict__ src, int r, long long rows,
+                                  float* __restrict__ dst) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * r) return;
+    dst[t] = src[(t / r) * R + t % r];
+}
+__global__ void unpad_gram_kernel(const double* __restrict__ g64, const double* __restrict__ f64,
+                                  int r, double* __restrict__ g, double* __restrict__ f) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < r * r) g[t] = g64[(t / r) * R + t % r];
+    if (t == 0) *f = *f64;
+}
+
 struct TcPlan {
     int vgrid, wgrid, splits, rows_per_split;
 };
@@ -1116,7 +1139,9 @@ namespace mmk_tc {
 // The tensor-core path needs the pre-split copy of X (8 bytes per element)
 // next to X itself; shapes whose copy would pass 96 GiB take the SIMT path.
 bool shape_ok(int dtype, long long m, long long n, long long r) {
-    if (dtype != MMK_F32 || r != R) return false;
+    // ranks 17..64: ranks below 64 run on the rank-64 kernels with V and W
+    // zero-padded (exact: a zero component stays zero and adds nothing)
+    if (dtype != MMK_F32 || r < 17 || r > R) return false;
     if ((n & 7) || (m & 7) || m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
     return 8.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
@@ -1131,7 +1156,36 @@ bool eligible(int dtype, long long m, long long n, long long r, long long ldx, c
     return true;
 }
 
-size_t ws_bytes(long long m, long long n) { return tc_layout(m, n, nullptr, nullptr); }
+// rank < 64: the zero-padded operands after the rank-64 region
+struct PadWs {
+    float *V64, *V64o, *W64;
+    double *red64, *GW64;
+};
+size_t pad_layout(long long m, long long n, void* base, PadWs* L) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t oV = take(4 * (size_t)m * R), oVo = take(4 * (size_t)m * R);
+    const size_t oW = take(4 * (size_t)R * n);
+    const size_t oRed = take(8 * ((size_t)R * n + R * R + 2)), oG = take(8 * (size_t)R * R);
+    if (base && L) {
+        char* c = reinterpret_cast<char*>(base);
+        L->V64 = (float*)(c + oV);
+        L->V64o = (float*)(c + oVo);
+        L->W64 = (float*)(c + oW);
+        L->red64 = (double*)(c + oRed);
+        L->GW64 = (double*)(c + oG);
+    }
+    return off;
+}
+
+size_t ws_bytes(long long m, long long n, long long r) {
+    const size_t core = (tc_layout(m, n, nullptr, nullptr) + 255) & ~size_t(255);
+    return core + (r < R ? pad_layout(m, n, nullptr, nullptr) : 0);
+}
 
 void set_x_prepared(bool on) { t_x_prepared = on; }
 
@@ -1151,9 +1205,9 @@ int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcw
 
 // Phase A of one iteration on the tensor cores; writes V_out and
 // red = [P | G_V' | f-partial].
-int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
-           long long m, long long n, void* tcws, double* GW, double* red,
-           cudaStream_t st) {
+static int iter_a64(const float* X, long long ldx, const float* V, const float* W, float* V_out,
+                    long long m, long long n, void* tcws, double* GW, double* red,
+                    cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);
@@ -1206,6 +1260,34 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
                (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
                                                                     L.sc)));
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a");
+    return MMK_OK;
+}
+
+// Phase A of one iteration on the tensor cores (any rank 17..64)
+int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
+           long long m, long long n, long long r, void* tcws, double* GW, double* red,
+           cudaStream_t st) {
+    if (r == R) return iter_a64(X, ldx, V, W, V_out, m, n, tcws, GW, red, st);
+    PadWs Pd;
+    pad_layout(m, n, reinterpret_cast<char*>(tcws) +
+                         ((tc_layout(m, n, nullptr, nullptr) + 255) & ~size_t(255)), &Pd);
+    MMK_LAUNCH("nnmf_pad_v", st,
+               (pad_cols_kernel<<<ceil_div(m * R, 256), 256, 0, st>>>(V, (int)r, m, Pd.V64)));
+    cudaMemcpyAsync(Pd.W64, W, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(Pd.W64 + r * n, 0, sizeof(float) * (R - r) * n, st);
+    int rc = iter_a64(X, ldx, Pd.V64, Pd.W64, Pd.V64o, m, n, tcws, Pd.GW64, Pd.red64, st);
+    if (rc) return rc;
+    MMK_LAUNCH("nnmf_unpad_v", st,
+               (unpad_cols_kernel<<<ceil_div(m * r, 256), 256, 0, st>>>(Pd.V64o, (int)r, m,
+                                                                         V_out)));
+    // [P (r n) | G (r r) | f]: the first r rows of P are the padded P's
+    cudaMemcpyAsync(red, Pd.red64, sizeof(double) * r * n, cudaMemcpyDeviceToDevice, st);
+    MMK_LAUNCH("nnmf_unpad_gram", st,
+               (unpad_gram_kernel<<<ceil_div(r * r, 256), 256, 0, st>>>(
+                   Pd.red64 + (long long)R * n, Pd.red64 + (long long)R * n + R * R, (int)r,
+                   red + r * n, red + r * n + r * r)));
+    (void)GW;
+    MMK_CHECK_LAUNCH("nnmf_tc_iter_a_padded");
     return MMK_OK;
 }
 

@@ -10,9 +10,10 @@ namespace mmk_tc {
 bool shape_ok(int dtype, long long m, long long n, long long r);
 // ... and this X (row stride, alignment; MMK_NNMF_TC=0 disables the path)
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X);
-size_t ws_bytes(long long m, long long n);
+size_t ws_bytes(long long m, long long n, long long r);
+// r = 64, or 17..63 on the rank-64 kernels with zero-padded V / W
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
-           long long m, long long n, void* tcws, double* GW, double* red,
+           long long m, long long n, long long r, void* tcws, double* GW, double* red,
            cudaStream_t st);
 
 // Per-X preparation (sum x^2 / scale exponent, the pre-split copy): iter_a

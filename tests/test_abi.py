@@ -64,7 +64,9 @@ def test_nnmf_tc_workspace_policy():
     copy = 8 * 131072 * 16384
     c4 = ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 64)
     assert copy <= c4 < copy + (1 << 30)
-    for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 32)):
+    # ranks 17..63 run on the rank-64 kernels (zero-padded): same region
+    assert copy <= ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 32) < copy + (1 << 30)
+    for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 16), (0, 131072, 16384, 65)):
         assert ws("mmk_nnmf_ws_bytes", *args) < (1 << 30)
     assert ws("mmk_nnmf_op_ws_bytes", 0, 131072, 16384, 64) < (1 << 30)
     # 262144 x 65536: the copy would be 128 GiB -- SIMT path, no region

@@ -25,7 +25,8 @@ def f32(a):
 
 
 @pytest.mark.parametrize("m,n,r", [(1, 1, 1), (2, 9, 1), (7, 3, 5), (33, 65, 17), (64, 40, 33),
-                                   (130, 257, 64), (256, 264, 64), (50, 20, 100), (41, 19, 128)])
+                                   (130, 257, 64), (256, 264, 64), (50, 20, 100), (41, 19, 128),
+                                   (256, 264, 32), (136, 392, 48), (264, 136, 17)])
 @pytest.mark.parametrize("dtype,tol", [("fp64", 1e-9), ("fp32", 1e-4)])
 def test_nnmf_rank_buckets_and_shapes(m, n, r, dtype, tol):
     rng = np.random.default_rng(m * 1000 + n * 10 + r)
