@@ -153,6 +153,36 @@ __device__ __forceinline__ void issue_split_stage(uint32_t d, const uint8_t* xs,
     }
 }
 
+// the same, warp-converged (every lane calls it; one elected lane issues)
+__device__ __forceinline__ void issue_split_stage_e(uint32_t d, const uint8_t* xs,
+                                                    const uint8_t* bhl, bool first) {
+    const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
+    const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
+    const uint64_t al = tc::sdesc_sw128(xs + SXH, 16, 1024);
+    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
+    constexpr uint32_t id_lo = idesc_f16(BM, R);
+#pragma unroll
+    for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+        tc::mma_f16ss_e(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
+        tc::mma_f16ss_e(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
+    }
+}
+
+// Pipeline trace of CTA 0 (timing studies only: -DMMK_TC_TRACE, never in
+// the product build): clock64 per stage at 8 points, see TRACE_AT below
+#ifdef MMK_TC_TRACE
+__device__ unsigned long long g_tctrace[8][4096];
+#define TRACE_AT(what, it)                                                       \
+    do {                                                                         \
+        if (blockIdx.x == 0 && (it) < 4096) g_tctrace[what][it] = clock64();     \
+    } while (0)
+#else
+#define TRACE_AT(what, it) \
+    do {                   \
+    } while (0)
+#endif
+
 // Scales shared by the kernels of one iteration (device, in the workspace):
 // exponents of X (cached with sum x^2), W and V'; maxima as float bits.
 struct Scales {
@@ -270,6 +300,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     tc::tma_load_2d(oring + os * 2 * SOP, &mWh, &B.ofull[os], kb * BK, 0);
                     tc::tma_load_2d(oring + os * 2 * SOP + SOP, &mWl, &B.ofull[os], kb * BK, 0);
                     tc::mbar_wait(&B.xempty[xs], ((it / XSTV) & 1) ^ 1);
+                    TRACE_AT(0, it);
                     tc::mbar_expect_tx(&B.xfull[xs], SX);
                     tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], kb * BK, tile * BM);
                     tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], kb * BK, tile * BM);
@@ -277,7 +308,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {   // MMA issuer
+        {   // MMA issuer: the whole warp, one elected lane issues (tc::mma_f16ss_e)
             constexpr uint32_t id_res = idesc_f16(BM, ACC, 1);
             int it = 0;
             for (int p = 0; p < mine; ++p) {
@@ -290,22 +321,27 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     const int os = it % OST, xs = it % XSTV, rb = it % NRB;
                     tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
                     tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
+                    if (lane == 0) TRACE_AT(1, it);
                     tc::tc_fence_after();
                     const uint8_t* ob = oring + os * 2 * SOP;
-                    issue_split_stage(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
-                    tc::mma_commit(&B.xempty[xs]);
+                    issue_split_stage_e(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                    if (lane == 0) TRACE_AT(2, it);
+                    tc::mma_commit_e(&B.xempty[xs]);
                     tc::mbar_wait(&B.rempty[rb], ((it / NRB) & 1) ^ 1);
+                    if (lane == 0) TRACE_AT(3, it);
                     tc::tc_fence_after();
                     const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major, 2 atoms
                     const uint32_t dr = tmem + TM_RES + rb * ACC;
 #pragma unroll
                     for (int ks = 0; ks < R / 16; ++ks)
-                        tc::mma_f16ss(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res, ks ? 1u : 0u);
-                    tc::mma_commit(&B.rfull[rb]);
-                    tc::mma_commit(&B.oempty[os]);
+                        tc::mma_f16ss_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
+                                      ks ? 1u : 0u);
+                    tc::mma_commit_e(&B.rfull[rb]);
+                    tc::mma_commit_e(&B.oempty[os]);
+                    if (lane == 0) TRACE_AT(4, it);
                 }
-                tc::mma_commit(&B.dfull[b]);
-                tc::mma_commit(&B.vempty[b]);
+                tc::mma_commit_e(&B.dfull[b]);
+                tc::mma_commit_e(&B.vempty[b]);
             }
         }
     } else if (warp < 2 + NRES) {
@@ -327,8 +363,12 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 if ((it & 1) != g) continue;
                 // this row's 64 X values of the stage into registers, then release
                 // the slot (its other user is the Q MMA, which commits on xempty)
-                const int xs = it % XSTV, rb = it % NRB;
+                const int xs = it % XSTV;
+                const int rb = it % NRB;
+                const uint32_t rcol = (uint32_t)(rb * ACC);
+                const uint32_t rph = (uint32_t)((it / NRB) & 1);
                 tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
+                if (r == 0) TRACE_AT(5, it);
                 const uint32_t xh = tc::smem_u32(xring + xs * SX) + r * 128;
                 uint4 hv[8], lv[8];
 #pragma unroll
@@ -341,13 +381,14 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&B.xempty[xs]);
-                tc::mbar_wait(&B.rfull[rb], (it / NRB) & 1);
+                tc::mbar_wait(&B.rfull[rb], rph);
+                if (r == 0) TRACE_AT(6, it);
                 tc::tc_fence_after();
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {   // 16 columns at a time
                     float dh[16], dl[16];
-                    tc::tmem_ld16x2(tmem + TM_RES + rb * ACC + q * 16 + lane_off,
-                                    tmem + TM_RES + rb * ACC + R + q * 16 + lane_off, dh, dl);
+                    tc::tmem_ld16x2(tmem + TM_RES + rcol + q * 16 + lane_off,
+                                    tmem + TM_RES + rcol + R + q * 16 + lane_off, dh, dl);
                     float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
@@ -370,6 +411,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 }
                 tc::tc_fence_before();
                 __syncwarp();
+                if (r == 0) TRACE_AT(7, it);
                 if (lane == 0) tc::mbar_arrive(&B.rempty[rb]);
             }
         }
@@ -1241,9 +1283,8 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     MMK_LAUNCH("nnmf_split_v", st,
                (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
     MMK_LAUNCH("nnmf_vstep_tc", st,
-               (nnmf_vstep_tc<<<P.vgrid, kVThreads, SMEM_V, st>>>(mX, mX2, mWh, mWl, mVr, V,
-                                                                  L.GWf, V_out, L.sc, (int)m,
-                                                                  (int)n, L.part)));
+               (nnmf_vstep_tc<<<P.vgrid, kVThreads, SMEM_V, st>>>(mX, mX2, mWh, mWl, mVr, V, L.GWf, V_out,
+                                                       L.sc, (int)m, (int)n, L.part)));
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid,
@@ -1292,3 +1333,9 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 }
 
 }  // namespace mmk_tc
+
+#ifdef MMK_TC_TRACE
+extern "C" int mmk_tc_trace_read(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_tctrace, sizeof(g_tctrace));
+}
+#endif

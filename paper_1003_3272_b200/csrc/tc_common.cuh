@@ -159,6 +159,31 @@ __device__ __forceinline__ void mma_f16ts(uint32_t d_tmem, uint32_t a_tmem, uint
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-converged issue: the WHOLE warp executes the MMA loop (waits,
+// descriptor arithmetic -- warp-uniform values the compiler keeps in uniform
+// registers) and elect.sync picks the one lane that issues.  Issuing from a
+// lane-0-only branch instead makes the compiler wrap every tcgen05.mma in an
+// ELECT / R2UR / BRA.U.ANY loop, which paced the tensor-core NNMF V step
+// (measured: the MMA warp ~90 % busy issuing, not waiting).  The elected lane
+// is the same every time (all lanes active), so its commits track its MMAs.
+__device__ __forceinline__ void mma_f16ss_e(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
 // arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
@@ -288,19 +313,18 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                      : "memory");
 }
-// arrive (release at cluster scope) on an mbarrier given by its cluster address
+// arrive on an mbarrier given by its cluster address (another CTA's): the
+// default .release.cta form, as CUTLASS's ClusterBarrier.  The .release.cluster
+// form compiles to MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR before the arrive, and
+// its .acquire.cluster wait to a CCTL.IVALL (L1 invalidate) after -- hundreds
+// of cycles per cross-CTA hand-off.  Nothing passes through generic memory
+// here: TMEM is ordered by tcgen05.fence::before/after_thread_sync around
+// the arrive / wait, smem slots by their own (local) barriers.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
-        "@!P1 bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+    mbar_wait(bar, parity);
 }
 // 2-D tile load into this CTA's smem whose completion is counted on the
 // mbarrier `bar_cluster` of either CTA of the pair
@@ -331,6 +355,27 @@ __device__ __forceinline__ void mma_f16ss_pair(uint32_t d_tmem, uint64_t a_desc,
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// warp-converged forms (see mma_f16ss_e): the whole warp calls, one elected lane issues
+__device__ __forceinline__ void mma_f16ss_pair_e(uint32_t d_tmem, uint64_t a_desc,
+                                                 uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair_e(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "h"((unsigned short)3)
         : "memory");
 }
 // arrive on the mbarrier at the same offset in both CTAs once the pair's MMAs finish

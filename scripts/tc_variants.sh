@@ -22,11 +22,11 @@ if [ "$mode" = build ]; then
   done
 else
   cp $ROOT/paper_1003_3272_b200/libmmk.so /tmp/libmmk_orig.so
-  for rep in 1 2; do
+  for rep in $(seq ${REPS:-2}); do
   for name in "$@"; do
     cp $VD/libmmk_$name.so $ROOT/paper_1003_3272_b200/libmmk.so
     touch $ROOT/paper_1003_3272_b200/libmmk.so
-    timeout 300 python $ROOT/bench.py --no-suite --no-e2e --steps 30 --cpu-seconds 0 2>/dev/null | tail -1 | \
+    timeout 300 python $ROOT/bench.py --no-suite --no-e2e --steps ${STEPS:-30} --cpu-seconds 0 2>/dev/null | tail -1 | \
       python -c "
 import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']
 print('$name', 'it/s', round(d['value'],1), 'vstep', round(k['nnmf_vstep_tc']['avg_ms'],4), 'wstep', round(k['nnmf_wstep_tc']['avg_ms'],4), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])"
