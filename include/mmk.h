@@ -78,17 +78,21 @@ int mmk_prof_report(char *buf, size_t len);
  *            f_dev = red[f]
  * The row range is the caller's shard of X/V (rows are independent in the
  * V step; the W step is a sum over rows, hence the all-reduce of `red`).
- * The workspace (zero-filled by the caller before first use) caches per-X
- * data of the fp32 tensor-core path (rank 64) -- the scale exponent and the
- * pre-split fp16 hi / lo copy of X (8 bytes per element; shapes whose copy
- * would pass 96 GiB take the SIMT path) -- keyed by (X, m, n, ldx): zero it
- * again, or use a fresh one, if the contents of X change in place.
+ * The workspace (prepared by mmk_nnmf_ws_clear, or zero-filled, before first
+ * use) caches per-X data of the fp32 tensor-core path (ranks 17..64) -- the
+ * scale exponent and the pre-split fp16 hi / lo copy of X (4 bytes per
+ * element, row-major; shapes whose copy would pass 96 GiB take the SIMT
+ * path) -- keyed by (X, m, n, ldx): clear it again, or use a fresh one, if
+ * the contents of X change in place.  mmk_nnmf_ws_clear zeroes everything
+ * but the pre-split copy (written before it is read), on `stream`.
  * mmk_nnmf_ws_bytes sizes the workspace of iter / iter_a / the engine;
  * mmk_nnmf_op_ws_bytes the smaller one of the single operations below (they
  * run the SIMT kernels and never touch the tensor-core region).
  * ---------------------------------------------------------------------- */
 int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
 int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
+int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,
+                      void *stream);
 int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r);
 int mmk_nnmf_iter_a(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
                     void *V_out, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,

@@ -738,6 +738,31 @@ extern "C" int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, 
     return ws_bytes_for(dtype, m, n, r, false, out);
 }
 
+extern "C" int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    size_t need = 0;
+    int rc = ws_bytes_for(dtype, m, n, r, true, &need);
+    if (rc) return rc;
+    if (ws_bytes < need) {
+        mmk_host::set_error("NNMF workspace too small: %zu < %zu", ws_bytes, need);
+        return MMK_E_SHAPE;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char* c = reinterpret_cast<char*>(ws);
+    size_t b = ws_bytes, e = ws_bytes;   // the span left as is (none by default)
+    if (tc_region(dtype, m, n, (int)r, true)) {
+        Ws L;
+        ws_layout(make_plan(m, n, (int)r), m, n, (int)r, true, ws, &L);
+        mmk_tc::presplit_span(m, n, &b, &e);
+        b += (size_t)(reinterpret_cast<char*>(L.tc) - c);
+        e += (size_t)(reinterpret_cast<char*>(L.tc) - c);
+    }
+    cudaError_t ce = cudaMemsetAsync(c, 0, b, st);
+    if (ce == cudaSuccess && e < ws_bytes) ce = cudaMemsetAsync(c + e, 0, ws_bytes - e, st);
+    if (ce != cudaSuccess) return mmk_host::cuda_status(ce, "mmk_nnmf_ws_clear");
+    return MMK_OK;
+}
+
 // [P (r n) | G (r r) | f | device-error flag]
 extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 2; }
 

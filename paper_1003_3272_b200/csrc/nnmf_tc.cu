@@ -15,8 +15,9 @@
 // hi + lo are 8 bytes, fp16 hi + lo are 4.
 //
 // Pre-split X.  X is constant over a run, so its scaled fp16 hi / lo pair is
-// made ONCE per X (presplit_kernel): row-major for the V step, transposed for
-// the W step (8 bytes per element of X in HBM, 4 of them read per half step,
+// made ONCE per X (presplit_kernel), row-major: the V step reads it K-major,
+// the W step as an MN-major operand (4 bytes per element of X in HBM, all read
+// per half step,
 // as many as the fp32 X itself).  Both kernels stream [X_hi | X_lo] tiles
 // from TMA straight into SS MMAs.
 //
@@ -91,9 +92,18 @@ constexpr int kVThreads = 32 * (2 + NRES + 4);   // TMA, MMA, residual x8, epilo
 constexpr int kWThreads = 32 * (2 + 4);          // TMA, MMA, epilogue x4
 constexpr uint32_t SVH = BM * R * 2;        // 16 KB  V_h tile [128 rows x 64 ranks]
 constexpr uint32_t SMEM_V = XSTV * SX + OST * 2 * SOP + 2 * SVH + (MMK_TC_GW_SMEM ? SGW : 0) + 1024;
+// pair form: half-size operand slots and G_W read through L1 leave room for a
+// deeper X ring
+#ifndef MMK_TC_XSTV2
+#define MMK_TC_XSTV2 5
+#endif
+constexpr int XSTV2 = MMK_TC_XSTV2;
+constexpr int XSMAX = XSTV2 > XSTV ? XSTV2 : XSTV;
+constexpr uint32_t SMEM_V2 = XSTV2 * SX + OST * SOP + 2 * SVH + 1024;
 constexpr int OSTW = 3;                     // W step operand ring (a V'^T chunk feeds CB stages)
 constexpr uint32_t SMEM_W = XST * SX + OSTW * 2 * SOP + 1024;
 static_assert(SMEM_V + 2048 <= 232448, "dynamic + static shared memory per CTA");
+static_assert(SMEM_V2 + 2048 <= 232448, "dynamic + static shared memory per CTA (pair)");
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
 constexpr int CB = 2;                       // W step: 128-column blocks per item
 constexpr int TM_COLS = 512;
@@ -138,22 +148,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn = 0) {
 // along N (64 + 64 rows, K-major): per K16 step an SS MMA with N = 128 gives
 // D[:, 0:64] += X_hi.B_hi, D[:, 64:128] += X_hi.B_lo, and one with N = 64
 // adds X_lo.B_hi into D[:, 0:64].  The epilogue sums the two halves.
-__device__ __forceinline__ void issue_split_stage(uint32_t d, const uint8_t* xs,
-                                                  const uint8_t* bhl, bool first) {
-    const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
-    const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
-    const uint64_t al = tc::sdesc_sw128(xs + SXH, 16, 1024);
-    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
-    constexpr uint32_t id_lo = idesc_f16(BM, R);
-#pragma unroll
-    for (int ks = 0; ks < BK / 16; ++ks) {
-        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-        tc::mma_f16ss(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
-        tc::mma_f16ss(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
-    }
-}
-
-// the same, warp-converged (every lane calls it; one elected lane issues)
+// Issued warp-converged (every lane calls it; one elected lane issues)
 __device__ __forceinline__ void issue_split_stage_e(uint32_t d, const uint8_t* xs,
                                                     const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
@@ -166,6 +161,45 @@ __device__ __forceinline__ void issue_split_stage_e(uint32_t d, const uint8_t* x
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
         tc::mma_f16ss_e(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
         tc::mma_f16ss_e(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
+    }
+}
+
+// W-step stage with A MN-major: the X stage holds [X_hi | X_lo] as row-major
+// tiles of the pre-split X (K = 64 rows of X, M = 128 columns, the columns
+// contiguous: two 64-column boxes per half, 128B swizzle), read as A = X^T
+// directly -- no transposed copy of X.  LBO = the second 64-column box, SBO =
+// the next 8 rows; a K16 step advances 16 rows (2048 bytes).
+constexpr uint32_t SXB = BK * 64 * 2;   // 8 KB: one [64 rows x 64 columns] fp16 box
+__device__ __forceinline__ void issue_split_stage_mn(uint32_t d, const uint8_t* xs,
+                                                     const uint8_t* bhl, bool first) {
+    const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
+    const uint64_t ah = tc::sdesc_sw128(xs, SXB, 1024);
+    const uint64_t al = tc::sdesc_sw128(xs + SXH, SXB, 1024);
+    constexpr uint32_t id_hi = idesc_f16(BM, ACC) | (1u << 15);   // A MN-major
+    constexpr uint32_t id_lo = idesc_f16(BM, R) | (1u << 15);
+#pragma unroll
+    for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+        tc::mma_f16ss(d, ah + ks * (2048 >> 4), db0 + ks * 2, id_hi, acc);
+        tc::mma_f16ss(d, al + ks * (2048 >> 4), db0 + ks * 2, id_lo, 1);
+    }
+}
+
+// The same stage for a CTA pair (cta_group::2, M = 256, issued by the
+// leader): A = each CTA's own [X_hi | X_lo] stage (same offset), B = this
+// CTA's half of the W chunk (leader [W_hi], peer [W_lo]: N = 128 split
+// between the pair); per K16 step X_hi.[W_hi ; W_lo] and X_lo.[W_hi ; W_lo].
+__device__ __forceinline__ void issue_split_stage_pair(uint32_t d, const uint8_t* xs,
+                                                       const uint8_t* bh, bool first) {
+    const uint64_t db0 = tc::sdesc_sw128(bh, 16, 1024);
+    const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
+    const uint64_t al = tc::sdesc_sw128(xs + SXH, 16, 1024);
+    constexpr uint32_t id = idesc_f16(2 * BM, ACC);
+#pragma unroll
+    for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+        tc::mma_f16ss_pair_e(d, ah + ks * 2, db0 + ks * 2, id, acc);
+        tc::mma_f16ss_pair_e(d, al + ks * 2, db0 + ks * 2, id, 1);
     }
 }
 
@@ -207,11 +241,19 @@ struct Scales {
 //            as the stage lands (release -> xempty), then R'(it) from TMEM
 //   epilogue V' of the tile from Q (two accumulator sets: pass p's epilogue
 //            overlaps pass p + 1)
-// A single-CTA M = 128 MMA costs ~60-150 cycles whatever N is (measured), so
-// the 12 MMAs of a stage make this kernel tensor-issue bound (~1.75 ms at C4,
-// against ~1.3 ms for the 8 Q MMAs alone); DESIGN.md has the measurements.
+// Measured at C4 (scripts/vstep_time.py, profiles/r02/README.md): 1.69 ms,
+// against ~1.3 ms for the same kernel without the residual.  Variant builds
+// put ~0.26 ms on the R' MMAs and ~0.17 ms on the residual warps' X reads;
+// ncu shows no unit saturated (tensor pipe 42 %, tensor-core smem reads 51 %,
+// L1 55 %): per stage the MMA warp waits ~230 cycles for an R' buffer (two
+// fit in TMEM beside the two Q sets) and ~260 for X (a 4-deep ring fills the
+// 227 KB of shared memory).  The CTA-pair form below issues its 12 MMAs in
+// ~360 cycles instead of ~570 but is slower end to end (1.82 ms): the extra
+// X_lo.W_lo products raise power (lower clocks) and every stage crosses the
+// pair twice (forwarded X completion, remote rempty arrivals).
 struct VBars {
-    uint64_t xfull[XSTV], xempty[XSTV], ofull[OST], oempty[OST];
+    uint64_t xfull[XSMAX], xempty[XSMAX], ofull[OST], oempty[OST];
+    uint64_t pxfull[XSMAX];             // pair, leader: the peer's X stage landed (forwarded)
     uint64_t vfull[2], vempty[2];       // V_h tiles of a pass (TMA -> MMA)
     uint64_t dfull[2], dempty[2];       // Q accumulator sets: MMA -> epilogue
     uint64_t rfull[NRB], rempty[NRB];   // residual buffers: MMA -> residual warps
@@ -228,17 +270,41 @@ __device__ __forceinline__ int row_exp(const float4* vr) {
     return scale_exp(mx);
 }
 
+// PAIR (the default at C4): the kernel runs as CTA pairs (clusters of 2).
+// Pair q takes the 256-row units q, q + G/2, ...; CTA rank r of the pair
+// owns the 128-row tile 2u + r of unit u (its X stages, its V_h tile, its
+// TMEM lanes of Q and R').  Only the leader's MMA warp issues, with
+// tcgen05.mma.cta_group::2 (M = 256, one instruction for both tiles): a pair
+// MMA runs at the full tensor rate (64 cycles at N = 128, measured) where a
+// single-CTA M = 128 one costs ~110-175 cycles whatever N is, and with the
+// residual MMAs the single-CTA form is tensor-issue bound (12 MMAs per stage).
+// B (N = 128) is split between the pair: the W chunk's [W_hi] rows in the
+// leader's operand slot, [W_lo] at the same offset in the peer's -- read
+// K-major for Q and MN-major for R'.  Q's second MMA per K16 step is
+// X_lo.[W_hi ; W_lo] (N = 128: a pair MMA cannot split an N = 64 W_hi between
+// the CTAs), which adds the X_lo.W_lo product the single-CTA form omits.
+// Both CTAs' TMA loads complete on the LEADER's full barriers; commits are
+// multicast to the barriers of both CTAs; the epilogue and residual warps of
+// both CTAs arrive on the leader's dempty / rempty (cluster address).  The
+// residual warps read their X stage after the stage's R' commit (which the
+// MMA could only issue once the stage had landed: the peer never sees its own
+// xfull complete).
+template <bool PAIR>
 __global__ void __launch_bounds__(kVThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
               const __grid_constant__ CUtensorMap mVh, const float* __restrict__ V,
               const float* __restrict__ GWf, float* __restrict__ Vout, Scales* sc, int m, int n,
               double* __restrict__ part) {
+    constexpr uint32_t OSLOT = PAIR ? SOP : 2 * SOP;   // operand slot: pair = this CTA's half
+    constexpr int NARR = PAIR ? 8 : 4;                 // arrivals on dempty / rempty
+    constexpr int XS = PAIR ? XSTV2 : XSTV;            // X ring depth
+    constexpr bool GWS = !PAIR && MMK_TC_GW_SMEM;      // G_W staged in smem
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
-    uint8_t* oring = base + XSTV * SX;
-    uint8_t* vbuf = oring + OST * 2 * SOP;
+    uint8_t* oring = base + XS * SX;
+    uint8_t* vbuf = oring + OST * OSLOT;
     float* gws = reinterpret_cast<float*>(vbuf + 2 * SVH);
     __shared__ VBars B;
     __shared__ uint32_t tmem_base;
@@ -246,16 +312,21 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     __shared__ float vmx[kVThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (m + BM - 1) / BM, nk = (n + BK - 1) / BK;
-    const int G = (int)gridDim.x, me = (int)blockIdx.x;
-    const int mine = ntiles > me ? (ntiles - 1 - me) / G + 1 : 0;
+    const int rank = PAIR ? (int)tc::cluster_rank() : 0;
+    const int G = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const int me = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int units = PAIR ? (ntiles + 1) / 2 : ntiles;
+    const int mine = units > me ? (units - 1 - me) / G + 1 : 0;
+    auto tile_of = [&](int p) { return PAIR ? 2 * (me + p * G) + rank : me + p * G; };
     // G_W rounded to fp32 (gram_sum_kernel), staged for the denominator rows
-    if (MMK_TC_GW_SMEM)
+    if (GWS)
         for (int i = threadIdx.x; i < R * R / 4; i += kVThreads)
             reinterpret_cast<float4*>(gws)[i] = __ldg(reinterpret_cast<const float4*>(GWf) + i);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < XSTV; ++s) {
+        for (int s = 0; s < XS; ++s) {
             tc::mbar_init(&B.xfull[s], 1);
             tc::mbar_init(&B.xempty[s], 5);   // the residual group's 4 warps + the Q MMAs' commit
+            tc::mbar_init(&B.pxfull[s], 1);   // pair: the peer's forwarder
         }
         for (int s = 0; s < OST; ++s) {
             tc::mbar_init(&B.ofull[s], 1);
@@ -265,11 +336,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::mbar_init(&B.vfull[b], 1);
             tc::mbar_init(&B.vempty[b], 1);
             tc::mbar_init(&B.dfull[b], 1);
-            tc::mbar_init(&B.dempty[b], 4);   // epilogue warps
+            tc::mbar_init(&B.dempty[b], NARR);   // epilogue warps (of both CTAs)
         }
         for (int b = 0; b < NRB; ++b) {
             tc::mbar_init(&B.rfull[b], 1);
-            tc::mbar_init(&B.rempty[b], 4);   // the residual group that read it
+            tc::mbar_init(&B.rempty[b], NARR);   // the residual group(s) that read it
         }
         tc::fence_barrier_init();
         tc::tma_prefetch(&mX);
@@ -278,29 +349,57 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         tc::tma_prefetch(&mWl);
         tc::tma_prefetch(&mVh);
     }
-    if (warp == 1) tc::tmem_alloc<TM_COLS>(&tmem_base);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tc::tmem_alloc_pair<TM_COLS>(&tmem_base);
+        else
+            tc::tmem_alloc<TM_COLS>(&tmem_base);
+    }
     tc::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();   // barriers initialised, TMEM allocated in both
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
+    // the leader's copy of a barrier (pair: TMA completions and the peer's
+    // consumer arrivals are counted there)
+    auto lead = [](uint64_t* bar) { return tc::map_to_rank(bar, 0); };
+    auto arrive_lead = [&](uint64_t* bar) {
+        if (PAIR && rank != 0)
+            tc::mbar_arrive_cluster(lead(bar));
+        else
+            tc::mbar_arrive(bar);
+    };
     double acc = 0.0;   // residual warps: F'; epilogue warps: the correction terms
     float vmax = 0.f;
     if (warp == 0) {
         if (lane == 0) {   // TMA producer
             int it = 0;
             for (int p = 0; p < mine; ++p) {
-                const int tile = me + p * G, vb = p & 1;
+                const int tile = tile_of(p), vb = p & 1;
                 tc::mbar_wait(&B.vempty[vb], ((p >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&B.vfull[vb], SVH);
-                tc::tma_load_2d(vbuf + vb * SVH, &mVh, &B.vfull[vb], 0, tile * BM);
+                if constexpr (PAIR) {
+                    if (rank == 0) tc::mbar_expect_tx(&B.vfull[vb], 2 * SVH);
+                    tc::tma_load_2d_pair(vbuf + vb * SVH, &mVh, lead(&B.vfull[vb]), 0, tile * BM);
+                } else {
+                    tc::mbar_expect_tx(&B.vfull[vb], SVH);
+                    tc::tma_load_2d(vbuf + vb * SVH, &mVh, &B.vfull[vb], 0, tile * BM);
+                }
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XSTV;
+                    const int os = it % OST, xs = it % XS;
                     tc::mbar_wait(&B.oempty[os], ((it / OST) & 1) ^ 1);
-                    tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
-                    tc::tma_load_2d(oring + os * 2 * SOP, &mWh, &B.ofull[os], kb * BK, 0);
-                    tc::tma_load_2d(oring + os * 2 * SOP + SOP, &mWl, &B.ofull[os], kb * BK, 0);
-                    tc::mbar_wait(&B.xempty[xs], ((it / XSTV) & 1) ^ 1);
+                    if constexpr (PAIR) {   // this CTA's half of [W_hi ; W_lo]
+                        if (rank == 0) tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                        tc::tma_load_2d_pair(oring + os * OSLOT, rank == 0 ? &mWh : &mWl,
+                                             lead(&B.ofull[os]), kb * BK, 0);
+                    } else {
+                        tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                        tc::tma_load_2d(oring + os * OSLOT, &mWh, &B.ofull[os], kb * BK, 0);
+                        tc::tma_load_2d(oring + os * OSLOT + SOP, &mWl, &B.ofull[os], kb * BK, 0);
+                    }
+                    tc::mbar_wait(&B.xempty[xs], ((it / XS) & 1) ^ 1);
                     TRACE_AT(0, it);
+                    // own X stage -> own xfull (pair: the peer's forwarder
+                    // passes its completion on to the leader's pxfull)
                     tc::mbar_expect_tx(&B.xfull[xs], SX);
                     tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], kb * BK, tile * BM);
                     tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], kb * BK, tile * BM);
@@ -308,8 +407,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
         }
     } else if (warp == 1) {
-        {   // MMA issuer: the whole warp, one elected lane issues (tc::mma_f16ss_e)
-            constexpr uint32_t id_res = idesc_f16(BM, ACC, 1);
+        if (!PAIR || rank == 0) {   // MMA issuer: the whole warp, one elected lane issues
+            constexpr uint32_t id_res = idesc_f16(PAIR ? 2 * BM : BM, ACC, 1);
             int it = 0;
             for (int p = 0; p < mine; ++p) {
                 const int b = p & 1;
@@ -318,30 +417,60 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::tc_fence_after();
                 const uint64_t va = tc::sdesc_sw128(vbuf + b * SVH, 16, 1024);
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XSTV, rb = it % NRB;
+                    const int os = it % OST, xs = it % XS, rb = it % NRB;
                     tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
-                    tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
+                    tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
+                    if constexpr (PAIR) tc::mbar_wait(&B.pxfull[xs], (it / XS) & 1);
                     if (lane == 0) TRACE_AT(1, it);
                     tc::tc_fence_after();
-                    const uint8_t* ob = oring + os * 2 * SOP;
-                    issue_split_stage_e(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                    const uint8_t* ob = oring + os * OSLOT;
+                    if constexpr (PAIR)
+                        issue_split_stage_pair(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                    else
+                        issue_split_stage_e(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
                     if (lane == 0) TRACE_AT(2, it);
-                    tc::mma_commit_e(&B.xempty[xs]);
+                    if constexpr (PAIR)
+                        tc::mma_commit_pair_e(&B.xempty[xs]);
+                    else
+                        tc::mma_commit_e(&B.xempty[xs]);
                     tc::mbar_wait(&B.rempty[rb], ((it / NRB) & 1) ^ 1);
                     if (lane == 0) TRACE_AT(3, it);
                     tc::tc_fence_after();
-                    const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major, 2 atoms
+                    const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major
                     const uint32_t dr = tmem + TM_RES + rb * ACC;
 #pragma unroll
-                    for (int ks = 0; ks < R / 16; ++ks)
-                        tc::mma_f16ss_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
-                                      ks ? 1u : 0u);
-                    tc::mma_commit_e(&B.rfull[rb]);
-                    tc::mma_commit_e(&B.oempty[os]);
+                    for (int ks = 0; ks < R / 16; ++ks) {
+                        if constexpr (PAIR)
+                            tc::mma_f16ss_pair_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
+                                                 ks ? 1u : 0u);
+                        else
+                            tc::mma_f16ss_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
+                                            ks ? 1u : 0u);
+                    }
+                    if constexpr (PAIR) {
+                        tc::mma_commit_pair_e(&B.rfull[rb]);
+                        tc::mma_commit_pair_e(&B.oempty[os]);
+                    } else {
+                        tc::mma_commit_e(&B.rfull[rb]);
+                        tc::mma_commit_e(&B.oempty[os]);
+                    }
                     if (lane == 0) TRACE_AT(4, it);
                 }
-                tc::mma_commit_e(&B.dfull[b]);
-                tc::mma_commit_e(&B.vempty[b]);
+                if constexpr (PAIR) {
+                    tc::mma_commit_pair_e(&B.dfull[b]);
+                    tc::mma_commit_pair_e(&B.vempty[b]);
+                } else {
+                    tc::mma_commit_e(&B.dfull[b]);
+                    tc::mma_commit_e(&B.vempty[b]);
+                }
+            }
+        } else if (lane == 0) {
+            // the peer's forwarder: each of its X stages landed -> the leader's pxfull
+            const int total = mine * nk;
+            for (int it = 0; it < total; ++it) {
+                const int xs = it % XS;
+                tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
+                tc::mbar_arrive_cluster(lead(&B.pxfull[xs]));
             }
         }
     } else if (warp < 2 + NRES) {
@@ -354,7 +483,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         const int ex = sc->ex, ew = sc->ew;
         int it = 0;
         for (int p = 0; p < mine; ++p) {
-            const long long row = (long long)(me + p * G) * BM + r;
+            const long long row = (long long)tile_of(p) * BM + r;
             int ke = ex - (row < m ? row_exp(reinterpret_cast<const float4*>(V + row * R)) : 0) - ew;
             ke = ke < -126 ? -126 : (ke > 127 ? 127 : ke);
             const float nk2 = -exp2f((float)ke);
@@ -363,11 +492,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 if ((it & 1) != g) continue;
                 // this row's 64 X values of the stage into registers, then release
                 // the slot (its other user is the Q MMA, which commits on xempty)
-                const int xs = it % XSTV;
+                const int xs = it % XS;
                 const int rb = it % NRB;
                 const uint32_t rcol = (uint32_t)(rb * ACC);
                 const uint32_t rph = (uint32_t)((it / NRB) & 1);
-                tc::mbar_wait(&B.xfull[xs], (it / XSTV) & 1);
+                tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
                 if (r == 0) TRACE_AT(5, it);
                 const uint32_t xh = tc::smem_u32(xring + xs * SX) + r * 128;
                 uint4 hv[8], lv[8];
@@ -384,35 +513,41 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::mbar_wait(&B.rfull[rb], rph);
                 if (r == 0) TRACE_AT(6, it);
                 tc::tc_fence_after();
+                // R' in 8-column chunks, the load of chunk q + 1 in flight while
+                // chunk q is consumed (one TMEM round trip exposed per stage)
+                uint32_t th[2][8], tl[2][8];
+                const uint32_t tr0 = tmem + TM_RES + rcol + lane_off;
+                tc::tmem_ld8x2_nw(tr0, tr0 + R, th[0], tl[0]);
+                tc::tmem_wait_ld8x2(th[0], tl[0]);
+                float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {   // 16 columns at a time
-                    float dh[16], dl[16];
-                    tc::tmem_ld16x2(tmem + TM_RES + rcol + q * 16 + lane_off,
-                                    tmem + TM_RES + rcol + R + q * 16 + lane_off, dh, dl);
-                    float2 s2 = make_float2(0.f, 0.f);
+                for (int q = 0; q < 8; ++q) {   // columns 8q .. 8q + 7
+                    if (q < 7) tc::tmem_ld8x2_nw(tr0 + 8 * (q + 1), tr0 + R + 8 * (q + 1),
+                                                 th[(q + 1) & 1], tl[(q + 1) & 1]);
+                    if (!(q & 1)) s2 = make_float2(0.f, 0.f);
+                    const uint4 hq = hv[q], lq = lv[q];
+                    const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
+                    const uint32_t lw[4] = {lq.x, lq.y, lq.z, lq.w};
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const uint4 hq = hv[2 * q + half], lq = lv[2 * q + half];
-                        const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
-                        const uint32_t lw[4] = {lq.x, lq.y, lq.z, lq.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int k = half * 8 + 2 * e;
-                            const float2 xs2 = __fadd2_rn(
-                                __half22float2(*reinterpret_cast<const __half2*>(&hw[e])),
-                                __half22float2(*reinterpret_cast<const __half2*>(&lw[e])));
-                            const float2 rr = __fadd2_rn(make_float2(dh[k], dh[k + 1]),
-                                                         make_float2(dl[k], dl[k + 1]));
-                            const float2 d = __ffma2_rn(rr, nkk, xs2);
-                            s2 = __ffma2_rn(d, d, s2);
-                        }
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 xs2 = __fadd2_rn(
+                            __half22float2(*reinterpret_cast<const __half2*>(&hw[e])),
+                            __half22float2(*reinterpret_cast<const __half2*>(&lw[e])));
+                        const float2 rr = __fadd2_rn(
+                            make_float2(__uint_as_float(th[q & 1][2 * e]),
+                                        __uint_as_float(th[q & 1][2 * e + 1])),
+                            make_float2(__uint_as_float(tl[q & 1][2 * e]),
+                                        __uint_as_float(tl[q & 1][2 * e + 1])));
+                        const float2 d = __ffma2_rn(rr, nkk, xs2);
+                        s2 = __ffma2_rn(d, d, s2);
                     }
-                    acc += (double)(s2.x + s2.y);
+                    if (q & 1) acc += (double)(s2.x + s2.y);   // 16 terms per fold
+                    if (q < 7) tc::tmem_wait_ld8x2(th[(q + 1) & 1], tl[(q + 1) & 1]);
                 }
                 tc::tc_fence_before();
                 __syncwarp();
                 if (r == 0) TRACE_AT(7, it);
-                if (lane == 0) tc::mbar_arrive(&B.rempty[rb]);
+                if (lane == 0) arrive_lead(&B.rempty[rb]);
             }
         }
         acc *= exp2(-2.0 * ex);
@@ -424,12 +559,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const double qscale = exp2(-(double)(sc->ex + sc->ew));
         const uint32_t gws_s = tc::smem_u32(gws);
-        auto row_of = [&](int p) { return (long long)(me + p * G) * BM + quarter * 32 + lane; };
         for (int p = 0; p < mine; ++p) {
             const int b = p & 1;
             tc::mbar_wait(&B.dfull[b], (p >> 1) & 1);
             tc::tc_fence_after();
-            const long long row = row_of(p);
+            const long long row = (long long)tile_of(p) * BM + quarter * 32 + lane;
             const uint32_t ta = tmem + b * ACC + lane_off;
             const float4* vr = reinterpret_cast<const float4*>(V + (row < m ? row : 0) * R);
             const int ev = row < m ? row_exp(vr) : 0;
@@ -459,8 +593,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
 #pragma unroll
                             for (int c4 = 0; c4 < 2; ++c4) {
                                 const float4 gg =
-                                    MMK_TC_GW_SMEM
-                                        ? tc::lds128f(g4 + 16u * c4)
+                                    GWS ? tc::lds128f(g4 + 16u * c4)
                                         : __ldg(reinterpret_cast<const float4*>(GWf) +
                                                 (((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4));
                                 den[4 * c4] = fmaf(va[e], gg.x, den[4 * c4]);
@@ -499,7 +632,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             }
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&B.dempty[b]);
+            if (lane == 0) arrive_lead(&B.dempty[b]);
         }
     }
     // per-CTA share of f (residual + correction terms, fixed warp order) and max(V')
@@ -522,7 +655,12 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         part[blockIdx.x] = c;
         atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
     }
-    if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    if constexpr (PAIR) {
+        tc::cluster_sync();   // both CTAs done with the pair's TMEM
+        if (warp == 1) tc::tmem_free_pair<TM_COLS>(tmem);
+    } else {
+        if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
+    }
 }
 
 // V (m x 64 fp32) -> V_h = rn(V_i 2^ev_i) fp16 row-major (the A operand of
@@ -551,7 +689,8 @@ split_v_kernel(const float* __restrict__ V, __half* __restrict__ Vh, long long m
 // W step.  P^T partials: item (row split s, column super-block cs of CB x 128
 // columns) D[col][k] = sum_{rows of s} X[row][col] V'[row][k]; the V'^T chunk
 // (fp16 hi / lo, K-major along rows) is shared by the CB column blocks of an
-// item.  mX / mX2: fp16 hi / lo maps of the pre-split X^T (n x m).
+// item.  mX / mX2: fp16 hi / lo maps of the row-major pre-split X (m x n,
+// [64 rows x 64 columns] boxes; see issue_split_stage_mn).
 struct WBars {
     uint64_t xfull[XST], xempty[XST], ofull[OSTW], oempty[OSTW];
     uint64_t dfull[2], dempty[2];
@@ -623,11 +762,15 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     for (int j = 0; j < nacc; ++j, ++xit) {
                         const int xs = xit % XST;
                         tc::mbar_wait(&B.xempty[xs], ((xit / XST) & 1) ^ 1);
+                        // rows r0 + kb BK .. +64 of columns col0 + j BM .. +128
+                        // (two 64-column boxes of X_hi, then of X_lo)
                         tc::mbar_expect_tx(&B.xfull[xs], SX);
-                        tc::tma_load_2d(xring + xs * SX, &mX, &B.xfull[xs], r0 + kb * BK,
-                                        col0 + j * BM);
-                        tc::tma_load_2d(xring + xs * SX + SXH, &mX2, &B.xfull[xs], r0 + kb * BK,
-                                        col0 + j * BM);
+                        uint8_t* xd = xring + xs * SX;
+                        const int c0 = col0 + j * BM, rr = r0 + kb * BK;
+                        tc::tma_load_2d(xd, &mX, &B.xfull[xs], c0, rr);
+                        tc::tma_load_2d(xd + SXB, &mX, &B.xfull[xs], c0 + 64, rr);
+                        tc::tma_load_2d(xd + SXH, &mX2, &B.xfull[xs], c0, rr);
+                        tc::tma_load_2d(xd + SXH + SXB, &mX2, &B.xfull[xs], c0 + 64, rr);
                     }
                 }
             }
@@ -648,8 +791,8 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         const int xs = xit % XST;
                         tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
                         tc::tc_fence_after();
-                        issue_split_stage(tmem + (b * CB + j) * ACC, xring + xs * SX,
-                                          oring + os * 2 * SOP, kb == 0);
+                        issue_split_stage_mn(tmem + (b * CB + j) * ACC, xring + xs * SX,
+                                             oring + os * 2 * SOP, kb == 0);
                         tc::mma_commit(&B.xempty[xs]);
                     }
                     tc::mma_commit(&B.oempty[os]);
@@ -712,9 +855,10 @@ struct XXCache {
     unsigned long long pkey[4];   // X the pre-split copy was made from (presplit_kernel)
 };
 
-__global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
-                             XXCache* cache, double* __restrict__ part, float* __restrict__ mpart,
-                             unsigned int* counter, Scales* sc) {
+__global__ void __launch_bounds__(1024)
+sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
+             XXCache* cache, double* __restrict__ part, float* __restrict__ mpart,
+             unsigned int* counter, Scales* sc) {
     const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
     if (cache->key[0] == k0 && cache->key[1] == (unsigned long long)m &&
         cache->key[2] == (unsigned long long)n && cache->key[3] == (unsigned long long)ldx) {
@@ -725,14 +869,36 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
     __shared__ float sf[32];
     double s = 0.0;
     float mx = 0.f;
-    for (long long i = blockIdx.x; i < m; i += gridDim.x) {
-        const float* row = X + i * ldx;
-        for (long long j = threadIdx.x; j < n; j += blockDim.x) {
-            const float x = row[j];
-            const double v = x;
-            s = fma(v, v, s);
-            mx = fmaxf(mx, fabsf(x));
+    // float4 grid-stride over the m x n/4 quads (n % 8 == 0, ldx % 4 == 0,
+    // X 16-byte aligned: eligible()); 4 quads in flight per thread
+    const long long nq = n / 4, total = m * nq;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + 3 * stride < total; q += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long t = q + u * stride, row = t / nq, c4 = t - row * nq;
+            v[u] = __ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s = fma((double)v[u].x, (double)v[u].x, s);
+            s = fma((double)v[u].y, (double)v[u].y, s);
+            s = fma((double)v[u].z, (double)v[u].z, s);
+            s = fma((double)v[u].w, (double)v[u].w, s);
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
+                                 fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+        }
+    }
+    for (; q < total; q += stride) {
+        const long long row = q / nq, c4 = q - row * nq;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4);
+        s = fma((double)v.x, (double)v.x, s);
+        s = fma((double)v.y, (double)v.y, s);
+        s = fma((double)v.z, (double)v.z, s);
+        s = fma((double)v.w, (double)v.w, s);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
     s = block_sum(s, sd);
 #pragma unroll
@@ -762,54 +928,50 @@ __global__ void sumsq_kernel(const float* __restrict__ X, long long ldx, long lo
 }
 
 // Pre-split copy of X: X_hi = rn(x 2^ex), X_lo = rn(x 2^ex - X_hi) in fp16,
-// both row-major (m x n, V step) and transposed (n x m, W step).  Made once
-// per X (keyed like the sum-of-squares cache; runs after sumsq_kernel, whose
-// exponent it uses); later launches exit at the key check.
-constexpr int PS_TILE = 64;
+// row-major m x n (the V step reads [128 rows x 64 columns] boxes of it, the
+// W step [64 rows x 64 columns] boxes as an MN-major operand).  Made once per
+// X (keyed like the sum-of-squares cache; runs after sumsq_kernel, whose
+// exponent it uses); later launches exit at the key check.  float4 in, 8-byte
+// hi / lo out, 4 quads in flight per thread.
+__device__ __forceinline__ void split_quad(float4 v, float sc, uint2& h, uint2& l) {
+    split_pair(v.x * sc, v.y * sc, h.x, l.x);
+    split_pair(v.z * sc, v.w * sc, h.y, l.y);
+}
 __global__ void __launch_bounds__(256)
-presplit_kernel(const float* __restrict__ X, long long ldx, int m, int n, XXCache* cache,
-                __half* __restrict__ Xh, __half* __restrict__ Xl, __half* __restrict__ XTh,
-                __half* __restrict__ XTl, unsigned int* counter) {
+presplit_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
+                XXCache* cache, __half* __restrict__ Xh, __half* __restrict__ Xl,
+                unsigned int* counter) {
     const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
     if (cache->pkey[0] == k0 && cache->pkey[1] == (unsigned long long)m &&
         cache->pkey[2] == (unsigned long long)n && cache->pkey[3] == (unsigned long long)ldx)
         return;   // uniform across the grid
-    __shared__ float t[PS_TILE][PS_TILE + 1];
     const float sc = exp2f((float)cache->ex);
-    const int tr = (m + PS_TILE - 1) / PS_TILE, tcn = (n + PS_TILE - 1) / PS_TILE;
-    const long long ntiles = (long long)tr * tcn;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int r0 = (int)(tile / tcn) * PS_TILE, c0 = (int)(tile % tcn) * PS_TILE;
-        // row-major copy: 64 rows x 32 column pairs (m, n are multiples of 8)
-        for (int i = threadIdx.x; i < PS_TILE * PS_TILE / 2; i += blockDim.x) {
-            const int r = i >> 5, cp = i & 31, row = r0 + r, col = c0 + 2 * cp;
-            float a = 0.f, b = 0.f;
-            if (row < m && col < n) {
-                const float2 v = *reinterpret_cast<const float2*>(X + (long long)row * ldx + col);
-                a = v.x * sc;
-                b = v.y * sc;
-                uint32_t h, l;
-                split_pair(a, b, h, l);
-                const long long o = ((long long)row * n + col) / 2;
-                reinterpret_cast<uint32_t*>(Xh)[o] = h;
-                reinterpret_cast<uint32_t*>(Xl)[o] = l;
-            }
-            t[r][2 * cp] = a;
-            t[r][2 * cp + 1] = b;
+    const long long nq = n / 4, total = m * nq;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    uint2* H = reinterpret_cast<uint2*>(Xh);
+    uint2* L = reinterpret_cast<uint2*>(Xl);
+    long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + 3 * stride < total; q += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long t = q + u * stride, row = t / nq, c4 = t - row * nq;
+            v[u] = __ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4);
         }
-        __syncthreads();
-        // transposed copy: 64 columns x 32 row pairs
-        for (int i = threadIdx.x; i < PS_TILE * PS_TILE / 2; i += blockDim.x) {
-            const int c = i >> 5, rp = i & 31, col = c0 + c, row = r0 + 2 * rp;
-            if (col < n && row < m) {
-                uint32_t h, l;
-                split_pair(t[2 * rp][c], t[2 * rp + 1][c], h, l);
-                const long long o = ((long long)col * m + row) / 2;
-                reinterpret_cast<uint32_t*>(XTh)[o] = h;
-                reinterpret_cast<uint32_t*>(XTl)[o] = l;
-            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint2 h, l;
+            split_quad(v[u], sc, h, l);
+            H[q + u * stride] = h;   // quad t of the dense m x n copy
+            L[q + u * stride] = l;
         }
-        __syncthreads();
+    }
+    for (; q < total; q += stride) {
+        const long long row = q / nq, c4 = q - row * nq;
+        uint2 h, l;
+        split_quad(__ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4), sc, h, l);
+        H[q] = h;
+        L[q] = l;
     }
     if (arrive_last(counter, gridDim.x) && threadIdx.x == 0) {
         cache->pkey[1] = (unsigned long long)m;
@@ -1064,12 +1226,30 @@ __global__ void unpad_gram_kernel(const double* __restrict__ g64, const double* 
 
 struct TcPlan {
     int vgrid, wgrid, splits, rows_per_split;
+    bool vpair;   // V step as CTA pairs (cta_group::2)
 };
+
+// MMK_TC_PAIR=1 runs the V step as CTA pairs (cta_group::2; same results to
+// rounding -- Q gains the X_lo.W_lo product -- and 8 % slower at C4, see the
+// V-step notes above); single CTAs are the default
+bool vstep_pair_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MMK_TC_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 TcPlan tc_plan(long long m, long long n) {
     TcPlan P;
     const int ntiles = (int)((m + BM - 1) / BM);
-    P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
+    P.vpair = vstep_pair_enabled() && ntiles >= 2;
+    if (P.vpair) {
+        const int units = (ntiles + 1) / 2;
+        P.vgrid = 2 * (units < kNumSMs / 2 ? units : kNumSMs / 2);
+    } else {
+        P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
+    }
     const int ncb = (int)((n + BM - 1) / BM);
     const int ncs = (ncb + CB - 1) / CB;
     // split count minimising (wave quantisation loss) + (split-K partial
@@ -1118,7 +1298,7 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
 
 struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl, *Vh;
-    __half *Xh, *Xl, *XTh, *XTl;   // pre-split X
+    __half *Xh, *Xl;   // pre-split X (row-major)
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
     double *part, *sqpart, *gpart;
     XXCache* xx;
@@ -1147,13 +1327,11 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
     size_t oGF = take(4 * (size_t)R * R);
     const size_t xe = (size_t)m * n;
-    size_t oXh = take(2 * xe), oXl = take(2 * xe), oXTh = take(2 * xe), oXTl = take(2 * xe);
+    size_t oXh = take(2 * xe), oXl = take(2 * xe);
     if (base && L) {
         char* c = c_base(base);
         L->Xh = (__half*)(c + oXh);
         L->Xl = (__half*)(c + oXl);
-        L->XTh = (__half*)(c + oXTh);
-        L->XTl = (__half*)(c + oXTl);
         L->sqpart = (double*)(c + oS);
         L->mpart = (float*)(c + oM);
         L->xx = (XXCache*)(c + oC);
@@ -1178,7 +1356,7 @@ thread_local bool t_x_prepared = false;   // set while an engine captures its lo
 
 namespace mmk_tc {
 
-// The tensor-core path needs the pre-split copy of X (8 bytes per element)
+// The tensor-core path needs the pre-split copy of X (4 bytes per element)
 // next to X itself; shapes whose copy would pass 96 GiB take the SIMT path.
 bool shape_ok(int dtype, long long m, long long n, long long r) {
     // ranks 17..64: ranks below 64 run on the rank-64 kernels with V and W
@@ -1186,7 +1364,7 @@ bool shape_ok(int dtype, long long m, long long n, long long r) {
     if (dtype != MMK_F32 || r < 17 || r > R) return false;
     if ((n & 7) || (m & 7) || m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
-    return 8.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
+    return 4.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
 }
 
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X) {
@@ -1231,6 +1409,17 @@ size_t ws_bytes(long long m, long long n, long long r) {
 
 void set_x_prepared(bool on) { t_x_prepared = on; }
 
+// [begin, end) of the pre-split copy of X inside the tensor-core workspace:
+// it is always written (presplit_kernel, keyed in the zeroed header) before
+// it is read, so a workspace need not be zero-filled there
+void presplit_span(long long m, long long n, size_t* begin, size_t* end) {
+    TcWs L;
+    char* const base = reinterpret_cast<char*>(uintptr_t(1) << 20);   // any non-null base
+    tc_layout(m, n, base, &L);
+    *begin = (size_t)(reinterpret_cast<char*>(L.Xh) - base);
+    *end = *begin + 2 * 2 * (size_t)m * (size_t)n;   // X_hi, X_lo (adjacent, 256-aligned)
+}
+
 int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
               cudaStream_t st) {
     TcWs L;
@@ -1239,8 +1428,8 @@ int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcw
                (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
                                                            L.counter, L.sc)));
     MMK_LAUNCH("nnmf_presplit_cached", st,
-               (presplit_kernel<<<4 * kNumSMs, 256, 0, st>>>(X, ldx, (int)m, (int)n, L.xx, L.Xh,
-                                                             L.Xl, L.XTh, L.XTl, L.counter + 2)));
+               (presplit_kernel<<<8 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.Xh, L.Xl,
+                                                             L.counter + 2)));
     MMK_CHECK_LAUNCH("nnmf_prepare_x");
     return MMK_OK;
 }
@@ -1253,16 +1442,20 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     TcWs L;
     tc_layout(m, n, tcws, &L);
     const TcPlan P = tc_plan(m, n);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tc))) {
-        cudaFuncSetAttribute(nnmf_vstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_V);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wstep_tc))) {
+        cudaFuncSetAttribute(nnmf_vstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_V);
+        cudaFuncSetAttribute(nnmf_vstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_V2);
         cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
     }
     CUtensorMap mX, mX2, mWh, mWl, mVr, mXt, mXt2, mVh, mVl;
     int rc;
     if ((rc = mmk_host::make_map_f16(&mX, L.Xh, m, n, n, BM))) return rc;
     if ((rc = mmk_host::make_map_f16(&mX2, L.Xl, m, n, n, BM))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mXt, L.XTh, n, m, m, BM))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mXt2, L.XTl, n, m, m, BM))) return rc;
+    // the W step reads the same row-major copy in [64 rows x 64 columns] boxes
+    if ((rc = mmk_host::make_map_f16(&mXt, L.Xh, m, n, n, BK))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mXt2, L.Xl, m, n, n, BK))) return rc;
     if ((rc = mmk_host::make_map_f16(&mVr, L.Vh, m, R, R, BM))) return rc;
     if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, R, n, n, R))) return rc;
     if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, R, n, n, R))) return rc;
@@ -1282,9 +1475,29 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     gram32(W, n, true, L.gpart, GW, st, L.GWf);
     MMK_LAUNCH("nnmf_split_v", st,
                (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
-    MMK_LAUNCH("nnmf_vstep_tc", st,
-               (nnmf_vstep_tc<<<P.vgrid, kVThreads, SMEM_V, st>>>(mX, mX2, mWh, mWl, mVr, V, L.GWf, V_out,
-                                                       L.sc, (int)m, (int)n, L.part)));
+    if (P.vpair) {
+        // clusters of 2 CTAs (one TPC): the pair's MMAs run as cta_group::2
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P.vgrid);
+        cfg.blockDim = dim3(kVThreads);
+        cfg.dynamicSmemBytes = SMEM_V2;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        MMK_LAUNCH("nnmf_vstep_tc", st,
+                   (void)cudaLaunchKernelEx(&cfg, nnmf_vstep_tc<true>, mX, mX2, mWh, mWl, mVr, V,
+                                            (const float*)L.GWf, V_out, L.sc, (int)m, (int)n,
+                                            L.part));
+    } else {
+        MMK_LAUNCH("nnmf_vstep_tc", st,
+                   (nnmf_vstep_tc<false><<<P.vgrid, kVThreads, SMEM_V, st>>>(
+                       mX, mX2, mWh, mWl, mVr, V, L.GWf, V_out, L.sc, (int)m, (int)n, L.part)));
+    }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid,

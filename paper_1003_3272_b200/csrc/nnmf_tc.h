@@ -23,6 +23,8 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
               cudaStream_t st);
 void set_x_prepared(bool on);
+// [begin, end) of the pre-split copy of X in the tensor-core workspace
+void presplit_span(long long m, long long n, size_t* begin, size_t* end);
 // the NNMF workspace's tensor-core part for (dtype, m, n, r), or nullptr when
 // the tensor-core path does not apply (nnmf.cu)
 void* engine_tc_ws(int dtype, const void* X, long long ldx, long long m, long long n, long long r,

@@ -112,8 +112,12 @@ class _GpuNnmf(DeviceMm):
         self.x = problem.device_x(backend, torch) if x_dev is None else x_dev
         self.m, self.n = self.x.shape
         self.r = problem.rank
-        self.ws = torch.zeros(_lib.ws_bytes("mmk_nnmf_ws_bytes", self.code, self.m, self.n,
+        # everything but the pre-split copy of X is zeroed (mmk_nnmf_ws_clear):
+        # at C4 that copy is 8.6 GB a zero fill would write for nothing
+        self.ws = torch.empty(_lib.ws_bytes("mmk_nnmf_ws_bytes", self.code, self.m, self.n,
                                             self.r), dtype=torch.uint8, device=self.device)
+        _lib.call("mmk_nnmf_ws_clear", self.code, self.m, self.n, self.r, _lib.ptr(self.ws),
+                  self.ws.numel(), _lib.stream_handle(torch, self.device))
         self.red = torch.zeros(_lib.load().mmk_nnmf_reduce_len(self.n, self.r),
                                dtype=torch.float64, device=self.device)
         self._problem = problem

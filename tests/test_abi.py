@@ -56,12 +56,12 @@ def test_sass_has_no_legacy_fallback_symbols():
 
 def test_nnmf_tc_workspace_policy():
     """Only a full-iteration fp32 rank-64 workspace holds the tensor-core region
-    (the pre-split copy of X: fp16 hi / lo, row-major + transposed, 8 bytes per
-    element), and only while that copy stays within 96 GiB; fp64, other ranks
+    (the pre-split copy of X: fp16 hi / lo, row-major, 4 bytes per element),
+    and only while that copy stays within 96 GiB; fp64, other ranks
     and the single operations (mmk_nnmf_op_ws_bytes) never reserve it
     (a zero-filled 16 GiB region per single-op call)."""
     ws = _lib.ws_bytes
-    copy = 8 * 131072 * 16384
+    copy = 4 * 131072 * 16384
     c4 = ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 64)
     assert copy <= c4 < copy + (1 << 30)
     # ranks 17..63 run on the rank-64 kernels (zero-padded): same region
@@ -69,8 +69,8 @@ def test_nnmf_tc_workspace_policy():
     for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 16), (0, 131072, 16384, 65)):
         assert ws("mmk_nnmf_ws_bytes", *args) < (1 << 30)
     assert ws("mmk_nnmf_op_ws_bytes", 0, 131072, 16384, 64) < (1 << 30)
-    # 262144 x 65536: the copy would be 128 GiB -- SIMT path, no region
-    assert ws("mmk_nnmf_ws_bytes", 0, 262144, 65536, 64) < (1 << 32)
+    # 524288 x 65536: the copy would be 128 GiB -- SIMT path, no region
+    assert ws("mmk_nnmf_ws_bytes", 0, 524288, 65536, 64) < (1 << 33)
 
 
 def test_diagnostics_live_outside_the_solver_library():
