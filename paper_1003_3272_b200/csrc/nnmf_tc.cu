@@ -845,92 +845,73 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     if (warp == 1) tc::tmem_free<TM_COLS>(tmem);
 }
 
-// sum of x^2 and max(x) over X, cached in the workspace and keyed by
-// (X, m, n, ldx): X is constant over a run, so after the first call this is
-// a no-op launch.  The X scale exponent goes to sc->ex.
+// max |x| over X -> the X scale exponent (sc->ex), cached in the workspace
+// and keyed by (X, m, n, ldx): X is constant over a run, so after the first
+// call this is a no-op launch.
 struct XXCache {
-    double xx;
     unsigned long long key[4];
     int ex, pad_;
     unsigned long long pkey[4];   // X the pre-split copy was made from (presplit_kernel)
 };
 
-__global__ void __launch_bounds__(1024)
-sumsq_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
-             XXCache* cache, double* __restrict__ part, float* __restrict__ mpart,
-             unsigned int* counter, Scales* sc) {
+__global__ void __launch_bounds__(512)
+xmax_kernel(const float* __restrict__ X, long long ldx, long long m, long long n,
+            XXCache* cache, float* __restrict__ mpart, unsigned int* counter, Scales* sc) {
     const unsigned long long k0 = reinterpret_cast<unsigned long long>(X);
     if (cache->key[0] == k0 && cache->key[1] == (unsigned long long)m &&
         cache->key[2] == (unsigned long long)n && cache->key[3] == (unsigned long long)ldx) {
         if (blockIdx.x == 0 && threadIdx.x == 0) sc->ex = cache->ex;
         return;   // uniform across the grid: every block exits, the counter is untouched
     }
-    __shared__ double sd[32];
     __shared__ float sf[32];
-    double s = 0.0;
     float mx = 0.f;
     // float4 grid-stride over the m x n/4 quads (n % 8 == 0, ldx % 4 == 0,
-    // X 16-byte aligned: eligible()); 4 quads in flight per thread
+    // X 16-byte aligned: eligible()); 8 quads in flight per thread
     const long long nq = n / 4, total = m * nq;
     const long long stride = (long long)gridDim.x * blockDim.x;
     long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; q + 3 * stride < total; q += 4 * stride) {
-        float4 v[4];
+    for (; q + 7 * stride < total; q += 8 * stride) {
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const long long t = q + u * stride, row = t / nq, c4 = t - row * nq;
             v[u] = __ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            s = fma((double)v[u].x, (double)v[u].x, s);
-            s = fma((double)v[u].y, (double)v[u].y, s);
-            s = fma((double)v[u].z, (double)v[u].z, s);
-            s = fma((double)v[u].w, (double)v[u].w, s);
+        for (int u = 0; u < 8; ++u)
             mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)),
                                  fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
-        }
     }
     for (; q < total; q += stride) {
         const long long row = q / nq, c4 = q - row * nq;
         const float4 v = __ldg(reinterpret_cast<const float4*>(X + row * ldx) + c4);
-        s = fma((double)v.x, (double)v.x, s);
-        s = fma((double)v.y, (double)v.y, s);
-        s = fma((double)v.z, (double)v.z, s);
-        s = fma((double)v.w, (double)v.w, s);
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
-    s = block_sum(s, sd);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, sf[w]);
-        part[blockIdx.x] = s;
         mpart[blockIdx.x] = mx;
     }
-    if (arrive_last(counter, gridDim.x)) {
-        const double tot = block_sum_array(part, gridDim.x, sd);
-        if (threadIdx.x == 0) {
-            float g = 0.f;
-            for (unsigned int b = 0; b < gridDim.x; ++b) g = fmaxf(g, mpart[b]);
-            cache->xx = tot;
-            cache->ex = scale_exp(g);
-            sc->ex = cache->ex;
-            cache->key[1] = (unsigned long long)m;
-            cache->key[2] = (unsigned long long)n;
-            cache->key[3] = (unsigned long long)ldx;
-            __threadfence();
-            cache->key[0] = k0;
-        }
+    if (arrive_last(counter, gridDim.x) && threadIdx.x == 0) {
+        float g = 0.f;
+        for (unsigned int b = 0; b < gridDim.x; ++b) g = fmaxf(g, mpart[b]);
+        cache->ex = scale_exp(g);
+        sc->ex = cache->ex;
+        cache->key[1] = (unsigned long long)m;
+        cache->key[2] = (unsigned long long)n;
+        cache->key[3] = (unsigned long long)ldx;
+        __threadfence();
+        cache->key[0] = k0;
     }
 }
 
 // Pre-split copy of X: X_hi = rn(x 2^ex), X_lo = rn(x 2^ex - X_hi) in fp16,
 // row-major m x n (the V step reads [128 rows x 64 columns] boxes of it, the
 // W step [64 rows x 64 columns] boxes as an MN-major operand).  Made once per
-// X (keyed like the sum-of-squares cache; runs after sumsq_kernel, whose
+// X (keyed like the scale cache; runs after xmax_kernel, whose
 // exponent it uses); later launches exit at the key check.  float4 in, 8-byte
 // hi / lo out, 4 quads in flight per thread.
 __device__ __forceinline__ void split_quad(float4 v, float sc, uint2& h, uint2& l) {
@@ -1300,10 +1281,10 @@ struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl, *Vh;
     __half *Xh, *Xl;   // pre-split X (row-major)
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
-    double *part, *sqpart, *gpart;
+    double *part, *gpart;
     XXCache* xx;
     Scales* sc;
-    unsigned int* counter;   // [0] sumsq, [1] wmax, [2] presplit
+    unsigned int* counter;   // [0] xmax, [1] wmax, [2] presplit
 };
 
 inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
@@ -1321,8 +1302,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oVr = take(2 * (size_t)R * m);
     size_t oWp = take(4 * (size_t)P.splits * n * R);
     size_t oP = take(8 * (size_t)kNumSMs);
-    size_t oS = take(8 * (size_t)kNumSMs * 4);
-    size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) sumsq, then wmax
+    size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) xmax, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
     size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
     size_t oGF = take(4 * (size_t)R * R);
@@ -1332,7 +1312,6 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         char* c = c_base(base);
         L->Xh = (__half*)(c + oXh);
         L->Xl = (__half*)(c + oXl);
-        L->sqpart = (double*)(c + oS);
         L->mpart = (float*)(c + oM);
         L->xx = (XXCache*)(c + oC);
         L->sc = (Scales*)(c + oC + sizeof(XXCache));
@@ -1424,9 +1403,9 @@ int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcw
               cudaStream_t st) {
     TcWs L;
     tc_layout(m, n, tcws, &L);
-    MMK_LAUNCH("nnmf_sumsq_cached", st,
-               (sumsq_kernel<<<kNumSMs, 1024, 0, st>>>(X, ldx, m, n, L.xx, L.sqpart, L.mpart,
-                                                           L.counter, L.sc)));
+    MMK_LAUNCH("nnmf_xmax_cached", st,
+               (xmax_kernel<<<4 * kNumSMs, 512, 0, st>>>(X, ldx, m, n, L.xx, L.mpart, L.counter,
+                                                         L.sc)));
     MMK_LAUNCH("nnmf_presplit_cached", st,
                (presplit_kernel<<<8 * kNumSMs, 256, 0, st>>>(X, ldx, m, n, L.xx, L.Xh, L.Xl,
                                                              L.counter + 2)));
