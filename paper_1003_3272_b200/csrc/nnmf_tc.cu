@@ -1099,45 +1099,95 @@ __global__ void split_w_kernel(const float* __restrict__ W, __half* __restrict__
 }
 
 // V' (m x 64 fp32) -> V'^T hi / lo (64 x m fp16), scaled by 2^ev where ev
-// comes from max(V') of the V step; a block transposes 128 rows through
-// shared memory and writes 16-byte chunks (8 rows) of both outputs
+// comes from max(V') of the V step, AND this block's share of the Gram
+// V'^T V' (one read of V' for both).  A block takes the 128-row tiles
+// blockIdx.x, + gridDim.x, ...: each tile is loaded once (float4) into a
+// transposed copy T (for the 16-byte chunks (8 rows) of both fp16 outputs)
+// and a row-major copy S (for the Gram: thread (ty, tx) owns the 4 x 4 block
+// (4 ty, 4 tx), fp32 products of 8 rows folded into fp64, as gram32_kernel);
+// the block's partial goes to gpart[blockIdx.x] (gram_sum_kernel adds them).
+constexpr int kVprepBlocks = 2 * kNumSMs;
+constexpr uint32_t kVprepSmem = (R * (128 + 4) + 128 * (R + 4)) * 4;
 __global__ void __launch_bounds__(256)
-vprep_kernel(const float* __restrict__ V, __half* __restrict__ Vth, __half* __restrict__ Vtl,
-             long long m, Scales* sc) {
-    __shared__ float T[R][128 + 4];
-    const long long r0 = (long long)blockIdx.x * 128;
+vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
+                  __half* __restrict__ Vtl, long long m, Scales* sc, double* __restrict__ gpart) {
+    extern __shared__ __align__(16) float vsm[];
+    float(*T)[128 + 4] = reinterpret_cast<float(*)[128 + 4]>(vsm);
+    float(*S)[R + 4] = reinterpret_cast<float(*)[R + 4]>(vsm + R * (128 + 4));
     const int ev = scale_exp(__uint_as_float(sc->vmax_bits));
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->ev = ev;
     const float s = exp2f((float)ev);
-    for (int i = threadIdx.x; i < 128 * (R / 4); i += 256) {
-        const int rr = i / (R / 4), k4 = (i % (R / 4)) * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + k4);
-        T[k4][rr] = v.x * s;
-        T[k4 + 1][rr] = v.y * s;
-        T[k4 + 2][rr] = v.z * s;
-        T[k4 + 3][rr] = v.w * s;
-    }
-    __syncthreads();
-    // chunk c of rank k: rows r0 + 8c .. r0 + 8c + 7 (16 bytes of fp16)
-    for (int e = threadIdx.x; e < R * 16; e += 256) {
-        const int k = e / 16, c = e % 16;
-        const long long row = r0 + 8 * c;
-        if (row >= m) continue;
-        uint32_t h[4], l[4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) split_pair(T[k][8 * c + 2 * q], T[k][8 * c + 2 * q + 1], h[q], l[q]);
-        if (row + 8 <= m) {
-            *reinterpret_cast<uint4*>(Vth + (long long)k * m + row) = make_uint4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<uint4*>(Vtl + (long long)k * m + row) = make_uint4(l[0], l[1], l[2], l[3]);
-        } else {
-            for (int q = 0; q < 8 && row + q < m; ++q) {
-                const uint32_t hw = h[q / 2] >> (16 * (q & 1)), lw = l[q / 2] >> (16 * (q & 1));
-                Vth[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(hw & 0xffffu));
-                Vtl[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(lw & 0xffffu));
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const long long ntiles = (m + 127) / 128;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long r0 = tile * 128;
+        for (int i = threadIdx.x; i < 128 * (R / 4); i += 256) {
+            const int rr = i / (R / 4), k4 = (i % (R / 4)) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + k4);
+            *reinterpret_cast<float4*>(&S[rr][k4]) = v;
+            T[k4][rr] = v.x * s;
+            T[k4 + 1][rr] = v.y * s;
+            T[k4 + 2][rr] = v.z * s;
+            T[k4 + 3][rr] = v.w * s;
+        }
+        __syncthreads();
+        // chunk c of rank k: rows r0 + 8c .. r0 + 8c + 7 (16 bytes of fp16)
+        for (int e = threadIdx.x; e < R * 16; e += 256) {
+            const int k = e / 16, c = e % 16;
+            const long long row = r0 + 8 * c;
+            if (row >= m) continue;
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                split_pair(T[k][8 * c + 2 * q], T[k][8 * c + 2 * q + 1], h[q], l[q]);
+            if (row + 8 <= m) {
+                *reinterpret_cast<uint4*>(Vth + (long long)k * m + row) = make_uint4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<uint4*>(Vtl + (long long)k * m + row) = make_uint4(l[0], l[1], l[2], l[3]);
+            } else {
+                for (int q = 0; q < 8 && row + q < m; ++q) {
+                    const uint32_t hw = h[q / 2] >> (16 * (q & 1)), lw = l[q / 2] >> (16 * (q & 1));
+                    Vth[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(hw & 0xffffu));
+                    Vtl[(long long)k * m + row + q] = __ushort_as_half((unsigned short)(lw & 0xffffu));
+                }
             }
         }
+        // Gram share of the tile's 128 rows (rows past m are zero)
+#pragma unroll 1
+        for (int k8 = 0; k8 < 128; k8 += 8) {
+            float p[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) p[i][j] = 0.f;
+#pragma unroll
+            for (int kk = k8; kk < k8 + 8; ++kk) {
+                const float4 a = *reinterpret_cast<const float4*>(&S[kk][4 * ty]);
+                const float4 b = *reinterpret_cast<const float4*>(&S[kk][4 * tx]);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+                const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) p[i][j] = fmaf(av[i], bv[j], p[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += (double)p[i][j];
+        }
+        __syncthreads();
     }
+    double* pb = gpart + (long long)blockIdx.x * (R * R);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[i][j];
 }
 
 // red[k n + j] = sum_s wpart[s][j][k] (fixed split order); a block owns 32
@@ -1427,6 +1477,8 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
         cudaFuncSetAttribute(nnmf_vstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_V2);
         cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
+        cudaFuncSetAttribute(vprep_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kVprepSmem);
     }
     CUtensorMap mX, mX2, mWh, mWl, mVr, mXt, mXt2, mVh, mVl;
     int rc;
@@ -1481,9 +1533,15 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     MMK_LAUNCH("nnmf_objective_tc", st,
                (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid,
                                                         red + rn + (long long)R * R)));
-    gram32(V_out, m, false, L.gpart, red + rn, st);
-    MMK_LAUNCH("nnmf_vprep", st,
-               (vprep_kernel<<<ceil_div(m, 128), 256, 0, st>>>(V_out, L.Vth, L.Vtl, m, L.sc)));
+    {   // V'^T hi / lo for the W step and the Gram V'^T V' -> red (one read of V')
+        const int vb = (int)(ceil_div(m, 128) < kVprepBlocks ? ceil_div(m, 128) : kVprepBlocks);
+        MMK_LAUNCH("nnmf_vprep_gram", st,
+                   (vprep_gram_kernel<<<vb, 256, kVprepSmem, st>>>(V_out, L.Vth, L.Vtl, m, L.sc,
+                                                                   L.gpart)));
+        MMK_LAUNCH("nnmf_gram_sum", st,
+                   (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(L.gpart, vb, red + rn,
+                                                                   nullptr)));
+    }
     MMK_LAUNCH("nnmf_wstep_tc", st,
                (nnmf_wstep_tc<<<P.wgrid, kWThreads, SMEM_W, st>>>(mXt, mXt2, mVh, mVl, (int)m,
                                                                   (int)n, P.splits,
