@@ -75,23 +75,40 @@ class DeviceMm(MmProblem):
     def stream(self):
         return _lib.stream_handle(self.torch, self.device)
 
+    def _status_read(self):
+        """(f, error code, error index) of the last pass (sharded solvers
+        override it to agree on one record across ranks)."""
+        return self.status.read()
+
     def _check_error(self):
-        f, code, idx = self.status.read()
+        f, code, idx = self._status_read()
         _lib.raise_device_error(code, idx, self._messages())
         return f
 
     # ---- per-iteration protocol -----------------------------------------------
     def objective(self, state):
+        """f(state); the same pass computes the next state, cached for step().
+        An error only the update can raise (``_lib.update_only``) is held back
+        with it: the reference raises it from step(), which it never calls
+        from a converged or final state."""
         nxt = self._alloc_like(state)
         self._iterate(state, nxt, self.status.f_ptr, self.status.err_ptr)
-        f = self._check_error()
-        self._cache = (state, nxt)
+        f, code, idx = self._status_read()
+        pending = None
+        if code != 0 and _lib.update_only(idx):
+            pending = (code, idx)
+            self.status.clear_error()
+        else:
+            _lib.raise_device_error(code, idx, self._messages())
+        self._cache = (state, nxt, pending)
         return f
 
     def step(self, state):
         cached = self._cache
         if cached is not None and cached[0] is state:
             self._cache = None
+            if cached[2] is not None:
+                _lib.raise_device_error(*cached[2], self._messages())
             return cached[1]
         nxt = self._alloc_like(state)
         self._iterate(state, nxt, self.status.f_ptr, self.status.err_ptr)

@@ -243,8 +243,22 @@ def prof_report():
     return out
 
 
+UPDATE_SITE = 16   # csrc/mmk_common.cuh kUpdateSite: sites 16..31 are update-only errors
+
+
+def update_only(index):
+    """True for an error the reference raises only from its update (step):
+    MDS coincident pairs, PET negative discriminant / non-positive
+    intensities, the Poisson update's zero mean."""
+    return UPDATE_SITE <= (index >> ERR_SITE_SHIFT) < 2 * UPDATE_SITE
+
+
 def split_site(index):
-    return index >> ERR_SITE_SHIFT, index & ((1 << ERR_SITE_SHIFT) - 1)
+    """(site, offending index); update-only sites map to their base site."""
+    site = index >> ERR_SITE_SHIFT
+    if UPDATE_SITE <= site < 2 * UPDATE_SITE:
+        site -= UPDATE_SITE
+    return site, index & ((1 << ERR_SITE_SHIFT) - 1)
 
 
 def raise_device_error(code, index, messages):

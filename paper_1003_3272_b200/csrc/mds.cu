@@ -82,7 +82,7 @@ mds_rows_kernel(const T* __restrict__ Y, const T* __restrict__ Wt, long long ldy
             // the update needs d > 0 where w y > 0 (mds.py:127-128), the
             // gradient wherever w > 0 (stress_gradient mds.py:154-156)
             if (d2 <= T(0) && (do_grad ? w > T(0) : (do_update && wy > T(0))))
-                flag_error(err, MMK_E_NUMERICS, err_at(1, gi * n + j));
+                flag_error(err, MMK_E_NUMERICS, err_at_update(1, gi * n + j));
             if (wy > T(0) && d2 > T(0)) z = wy / sqrt(d2);
             zs[rr] += z;
             const T c = w - z;
@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(kMdsSmallThr) mds_small_kernel(MdsSmall<T> a) 
         if (a.Wt) wts[t] = a.Wt[(long long)(r0 + i) * a.ldy + j];
     }
     MmState st = mm_load(a.ctl);
+    int iter_local = 0;
     unsigned int epoch = a.epoch0;
     int slot = 0;
     for (;;) {
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kMdsSmallThr) mds_small_kernel(MdsSmall<T> a) 
                 T z = T(0);
                 if (wy > T(0)) {
                     if (d2 <= T(0))
-                        flag_error(a.err, MMK_E_NUMERICS, err_at(1, (long long)i * n + j));
+                        flag_error(a.err, MMK_E_NUMERICS, err_at_update(1, (long long)i * n + j));
                     else
                         z = wy / sqrt(d2);
                 }
@@ -359,17 +360,22 @@ __global__ void __launch_bounds__(kMdsSmallThr) mds_small_kernel(MdsSmall<T> a) 
             }
             __syncthreads();
         }
-        if (tid == 0) a.part[c] = stress;
+        // stress partials of this launch's iteration k in part[k & 1][.]: a CTA
+        // past this barrier may write the next iteration's while a slower one
+        // still reads these for the stopping rule (iter_local is uniform over
+        // the CTA; st advances in one thread)
+        double* const part = a.part + (iter_local & 1) * G;
+        if (tid == 0) part[c] = stress;
         grid_sync_flags(a.flags, ++epoch);
         if (warp == 0) {
             double s2 = 0.0;
-            for (int b = lane; b < G; b += 32) s2 += __ldcg(a.part + b);
+            for (int b = lane; b < G; b += 32) s2 += __ldcg(part + b);
             s2 = warp_sum(s2);
             if (lane == 0) {
                 const MmState before = st;
                 int reason = 0;
                 const int dcs =
-                    mm_step(st, slot, s2, *(volatile int64_t*)a.err != 0, a.rule, &reason);
+                    mm_step(st, slot, s2, err_class(a.err), a.rule, &reason);
                 if (c == 0) mm_record(a.ctl, a.trace, a.tstamp, before, st, slot, s2, dcs, reason);
                 decision = dcs;
             }
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(kMdsSmallThr) mds_small_kernel(MdsSmall<T> a) 
         const int dcs = decision;
         if (dcs != kMmContinue) return;
         slot ^= 1;
+        ++iter_local;
     }
 }
 
@@ -505,7 +512,7 @@ static int mds_prepare_t(const void* Y, const void* Wt, long long ldy, const dou
         return MMK_E_SHAPE;
     }
     const size_t fbytes = (sizeof(unsigned int) * 32 * G + 255) / 256 * 256;
-    void* scratch = scratch_take(fbytes + sizeof(double) * G, fbytes);
+    void* scratch = scratch_take(fbytes + 2 * sizeof(double) * G, fbytes);   // part [2][G]
     if (!scratch) return mmk_host::cuda_status(cudaErrorMemoryAllocation, "mds_small scratch");
     a.flags = reinterpret_cast<unsigned int*>(scratch);
     a.part = reinterpret_cast<double*>(reinterpret_cast<char*>(scratch) + fbytes);

@@ -172,7 +172,7 @@ __device__ __noinline__ void careful(const float* __restrict__ ys, const float* 
                     const float g = thp[k * npad + ig] - thp[k * npad + jg];
                     d2 = fmaf(g, g, d2);
                 }
-                if (d2 <= 0.f) flag_error(err, MMK_E_NUMERICS, err_at(1, ig * n + jg));
+                if (d2 <= 0.f) flag_error(err, MMK_E_NUMERICS, err_at_update(1, ig * n + jg));
             }
         }
     }

@@ -30,11 +30,14 @@ struct MmState {
 // advances the state and, after half 1, pauses every rule.batch iterations
 // (-> kMmPause) so the host can drain the trace.  Pure function of its
 // inputs, so every CTA of a persistent kernel can evaluate it redundantly.
-__device__ __forceinline__ int mm_step(MmState& st, int half, double f, bool err,
+// err: err_class of the pass's error record -- an objective-class error (1)
+// stops first, as the reference raises it while evaluating f; an update-only
+// one (2) only when the run would go on to step from this state.
+__device__ __forceinline__ int mm_step(MmState& st, int half, double f, int err,
                                        const mmk_stop_rule& rule, int* reason) {
     int why = 0;
     st.has_rel = false;
-    if (err) {
+    if (err == 1) {
         why = MMK_STOP_DEVICE_ERROR;
     } else if (!isfinite(f)) {
         why = MMK_STOP_NONFINITE;
@@ -49,6 +52,7 @@ __device__ __forceinline__ int mm_step(MmState& st, int half, double f, bool err
         }
     }
     if (!why && st.it >= rule.max_iters) why = MMK_STOP_CAP;
+    if (!why && err == 2) why = MMK_STOP_DEVICE_ERROR;
     *reason = why;
     if (why) return kMmStop;
     st.fprev = f;
@@ -101,7 +105,7 @@ __device__ __forceinline__ int mm_control(int half, long long* ctl, double* trac
     const MmState before = mm_load(ctl);
     MmState after = before;
     int reason = 0;
-    const int d = mm_step(after, half, f, *(volatile const long long*)err != 0, rule, &reason);
+    const int d = mm_step(after, half, f, err_class(err), rule, &reason);
     mm_record(ctl, trace, tstamp, before, after, half, f, d, reason);
     return d;
 }

@@ -20,11 +20,21 @@ int cuda_status(cudaError_t e, const char* what) {
 }  // namespace mmk_host
 
 namespace {
+// The flag rides in the all-reduced payload (summed over ranks): 1 for an
+// objective-class error, 2^-10 for an update-only one (mmk_common.cuh), so
+// the sum tells every rank whether any error is of the objective class.
 __global__ void err_flag_kernel(const int64_t* err, double* flag) {
-    *flag = (err != nullptr && err[0] != 0) ? 1.0 : 0.0;
+    double v = 0.0;
+    if (err != nullptr && err[0] != 0) v = mmk::err_update_only(err[1]) ? 1.0 / 1024.0 : 1.0;
+    *flag = v;
 }
 __global__ void peer_err_kernel(const double* flag, int64_t* err) {
-    if (*flag > 0.5 && err[0] == 0) err[0] = MMK_E_PEER;   // index stays at its reset value
+    if (*flag > 0.0 && err[0] == 0) {
+        err[0] = MMK_E_PEER;
+        // objective class: the index stays at its reset value; update-only:
+        // an update-class site, so this rank's stopping rule defers it too
+        if (*flag < 0.5) err[1] = (int64_t)mmk::kUpdateSite << 48;
+    }
 }
 }  // namespace
 

@@ -35,6 +35,28 @@ __device__ __forceinline__ void flag_error(int64_t* err, int code, long long ind
 __device__ __forceinline__ long long err_at(int site, long long index) {
     return ((long long)site << 48) | index;
 }
+// Sites 16..31 (site + kUpdateSite) mark errors the reference raises only from
+// the UPDATE (its step()): MDS coincident pairs, PET negative discriminant /
+// non-positive intensities, the Poisson update's zero mean.  A fused pass
+// evaluates f(state) and the update together, so such an error at a state the
+// reference would not step from (converged, or the iteration cap) must not
+// stop the run: the stopping rule checks them last (mm_step) and the host
+// defers them to step() (_engine.DeviceMm).  Objective-class errors have the
+// smaller sites, so atomicMin keeps them first.
+constexpr int kUpdateSite = 16;
+__device__ __forceinline__ long long err_at_update(int site, long long index) {
+    return err_at(site + kUpdateSite, index);
+}
+__host__ __device__ __forceinline__ bool err_update_only(long long index) {
+    const long long s = index >> 48;
+    return s >= kUpdateSite && s < 2 * kUpdateSite;
+}
+// 0: no error, 1: objective-class error, 2: update-only error
+__device__ __forceinline__ int err_class(const void* err) {
+    const volatile long long* e = reinterpret_cast<const volatile long long*>(err);
+    if (e[0] == 0) return 0;
+    return err_update_only(e[1]) ? 2 : 1;
+}
 
 // ---- reductions ------------------------------------------------------------
 template <typename T>

@@ -186,7 +186,7 @@ pois_wpart_kernel(const T* __restrict__ X, long long ldx, const T* __restrict__ 
             for (int k = 0; k < RMAX; ++k)
                 if (k < r) b = fma(vi[k], wj[k], b);
             if (b == T(0)) {
-                flag_error(err, MMK_E_NUMERICS, err_at(2, i * n + j));
+                flag_error(err, MMK_E_NUMERICS, err_at_update(2, i * n + j));
                 continue;
             }
             const T ratio = x / b;

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThr) nnmf_small_kernel(SmallNnmf<T> a) {
 #pragma unroll
                     for (int k = 0; k < R; ++k) b = fma(Vn[i * r + k], wj[k], b);
                     if (b == T(0)) {
-                        flag_error(a.err, MMK_E_NUMERICS, err_at(2, (long long)(row0 + i) * n + j));
+                        flag_error(a.err, MMK_E_NUMERICS, err_at_update(2, (long long)(row0 + i) * n + j));
                         continue;
                     }
                     const T ratio = x / b;

@@ -219,7 +219,7 @@ __device__ __forceinline__ double pixel_update(const T* __restrict__ lam, T* __r
                                                int flags, long long j, double bj, int64_t* err) {
     double pen = 0.0;
     const double lj = (double)lam[j];
-    if ((flags & MMK_PET_CHECK_POSITIVE) && !(lj > 0.0)) flag_error(err, MMK_E_DOMAIN, err_at(3, j));
+    if ((flags & MMK_PET_CHECK_POSITIVE) && !(lj > 0.0)) flag_error(err, MMK_E_DOMAIN, err_at_update(3, j));
     const int k0 = nptr[j], k1 = nptr[j + 1];
     double nbr = 0.0;
     // neighbours in batches of four: indices, then values, then the in-order
@@ -248,7 +248,7 @@ __device__ __forceinline__ double pixel_update(const T* __restrict__ lam, T* __r
             const double a = -2.0 * mu * deg;
             const double b = mu * (deg * lj + nbr) - 1.0;
             const double disc = b * b - 4.0 * a * c;
-            if (disc < 0.0) flag_error(err, MMK_E_NUMERICS, err_at(2, j));
+            if (disc < 0.0) flag_error(err, MMK_E_NUMERICS, err_at_update(2, j));
             const double sq = sqrt(disc);
             out = (b < 0.0) ? 2.0 * c / (sq - b) : (-b - sq) / ((a < 0.0) ? 2.0 * a : -1.0);
         }
@@ -666,10 +666,15 @@ __global__ void __launch_bounds__(kPetSmallThr) pet_small_kernel(PetSmall<T> a) 
         }
         if (lane == 0) wsum[warp] = ll;
         __syncthreads();
+        // partials of this launch's iteration k live in part[k & 1][.]: a CTA
+        // that has passed the last barrier of an iteration may already write
+        // the next one's while a slower CTA still reads these for the stopping
+        // rule (iter_local is uniform over the CTA; st advances in one thread)
+        double* const part = a.part + (iter_local & 1) * 2 * G;
         if (tid == 0) {
             double s2 = 0.0;
             for (int w = 0; w < kPetSmallThr / 32; ++w) s2 += wsum[w];
-            a.part[c] = s2;
+            part[c] = s2;
         }
         stamp(2);
         grid_sync_flags(a.flags, ++epoch);
@@ -712,7 +717,7 @@ __global__ void __launch_bounds__(kPetSmallThr) pet_small_kernel(PetSmall<T> a) 
         if (tid == 0) {
             double s2 = 0.0;
             for (int w = 0; w < kPetSmallThr / 32; ++w) s2 += wsum[w];
-            a.part[G + c] = s2;
+            part[G + c] = s2;
         }
         stamp(5);
         grid_sync_flags(a.flags, ++epoch);
@@ -721,8 +726,8 @@ __global__ void __launch_bounds__(kPetSmallThr) pet_small_kernel(PetSmall<T> a) 
         if (warp == 0) {
             double l2 = 0.0, p2 = 0.0;
             for (int b = lane; b < G; b += 32) {
-                l2 += __ldcg(a.part + b);
-                p2 += __ldcg(a.part + G + b);
+                l2 += __ldcg(part + b);
+                p2 += __ldcg(part + G + b);
             }
             l2 = warp_sum(l2);
             p2 = warp_sum(p2);
@@ -731,7 +736,7 @@ __global__ void __launch_bounds__(kPetSmallThr) pet_small_kernel(PetSmall<T> a) 
                 if (a.mu > 0.0) f -= 0.5 * a.mu * p2;
                 const MmState before = st;
                 int reason = 0;
-                const int dcs = mm_step(st, slot, f, *(volatile int64_t*)a.err != 0, a.rule, &reason);
+                const int dcs = mm_step(st, slot, f, err_class(a.err), a.rule, &reason);
                 if (c == 0) mm_record(a.ctl, a.trace, a.tstamp, before, st, slot, f, dcs, reason);
                 decision = dcs;
             }
@@ -982,7 +987,7 @@ static int pet_prepare_t(const int32_t* rptr, const int32_t* ridx, const void* r
         return MMK_E_SHAPE;
     }
     const size_t fbytes = (sizeof(unsigned int) * 32 * G + 255) / 256 * 256;
-    const size_t bytes = fbytes + sizeof(double) * ((size_t)d + 2 * (size_t)G);
+    const size_t bytes = fbytes + sizeof(double) * ((size_t)d + 4 * (size_t)G);   // part [2][2][G]
     void* scratch = scratch_take(bytes, fbytes);
     if (!scratch) return mmk_host::cuda_status(cudaErrorMemoryAllocation, "pet_small scratch");
     a.flags = reinterpret_cast<unsigned int*>(scratch);

@@ -201,16 +201,13 @@ def _shard(mm, group, iter_fns=None):
     comm = nccl_comm_ptr(group) if group is not None else None
     mm.comm = comm
     mm._fused = bool(mm.backend.fused) and comm is not None
-    base_check = mm._check_error
-
-    def _check_error():
-        f, code, _ = mm.status.read()
-        if code == 0:
-            return f
-        if group is not None:
-            _combine_error_records(mm.status, group)
-        return base_check()
-    mm._check_error = _check_error
+    def _status_read():
+        f, code, idx = mm.status.read()
+        if code == 0 or group is None:
+            return f, code, idx
+        _combine_error_records(mm.status, group)
+        return mm.status.read()
+    mm._status_read = _status_read
     return mm
 
 

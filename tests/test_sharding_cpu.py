@@ -120,3 +120,14 @@ def test_mds_tile_sharding_gloo(world):
         got, f = res[r]
         np.testing.assert_allclose(got, want, rtol=1e-11, atol=1e-13)
         assert abs(f - f_ref) <= 1e-12 * f_ref
+
+
+def test_update_only_error_sites():
+    """Sites 16..31 of the device error record are update-only errors
+    (csrc/mmk_common.cuh kUpdateSite); messages are keyed by the base site,
+    and the reset / peer index (int64 max) is not update-only."""
+    from paper_1003_3272_b200 import _lib
+    idx = (17 << 48) | 12345
+    assert _lib.update_only(idx) and _lib.split_site(idx) == (1, 12345)
+    assert not _lib.update_only((1 << 48) | 5) and _lib.split_site((1 << 48) | 5) == (1, 5)
+    assert not _lib.update_only(np.iinfo(np.int64).max)
