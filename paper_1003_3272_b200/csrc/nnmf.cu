@@ -21,6 +21,7 @@
 // large r (3xTF32 contraction of X on the tensor cores).
 #include "mmk_common.cuh"
 #include "nnmf_tc.h"
+#include "nnmf_tile.h"
 
 #include <type_traits>
 
@@ -532,6 +533,11 @@ struct K {
     static void vstep(const T* X, long long ldx, const T* V, const T* W, T* Vout, long long m,
                       long long n, int r, int flags, const Plan& P, const Ws& L, double* res_out,
                       cudaStream_t st) {
+        if (RMAX > 16 && RMAX <= 64 && mmk_tile::applies(r)) {   // ranks 17..64: nnmf_tile.cu
+            mmk_tile::vstep<T>(X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
+                               res_out, st);
+            return;
+        }
         const size_t wbytes = sizeof(T) * (size_t)r * (size_t)n;
         const bool full = wbytes <= kWFullBytes;
         if constexpr (RMAX <= 16) {
@@ -563,6 +569,17 @@ struct K {
     }
     static void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r,
                       const Plan& P, const Ws& L, double* red, cudaStream_t st) {
+        if (RMAX > 16 && RMAX <= 64 && mmk_tile::applies(r)) {   // ranks 17..64: nnmf_tile.cu
+            const int S = mmk_tile::wpart_splits<T>(m, n, P.S);
+            mmk_tile::wpart<T>(X, ldx, V, m, n, r, S, S > 1 ? L.wpart : red, st);
+            if (S > 1) {
+                const long long len = (long long)r * n;
+                MMK_LAUNCH("nnmf_wreduce", st,
+                           (nnmf_wreduce_kernel<<<ceil_div(len, 256), 256, 0, st>>>(L.wpart, S,
+                                                                                   len, red)));
+            }
+            return;
+        }
         dim3 grid(P.colblocks, P.S);
         double* dst = P.S > 1 ? L.wpart : red;
         MMK_LAUNCH("nnmf_wpart", st,

@@ -1,0 +1,313 @@
+// nnmf_tile.cu -- register-blocked CUDA-core kernels of the Frobenius NNMF
+// iteration for ranks 17..64: the fp64 path at any shape (BASELINE config 4
+// in fp64: 131072 x 16384, r = 64) and fp32 shapes the tensor-core path does
+// not take (nnmf_tc.cu).  Reference: nnmf_objective / nnmf_update_v /
+// nnmf_update_w (nnmf.py:75-110).
+//
+// The warp-per-row kernels of nnmf.cu keep a row's r dot products in
+// registers -- right for the paper shape (r = 10), but at r = 64 that is
+// 2 x 64 values per thread and the fp64 C4 V step spilled to 443 ms.  Here a
+// CTA owns a 64 x 64 output tile and every thread a 4 x 4 block of it
+// (rows / ranks ty + 16 i, tx + 16 j: the operand a thread reads from shared
+// memory is either a warp broadcast or 16 consecutive values -- one
+// wavefront), with the X / W chunks of the next K step prefetched into
+// registers while the current one is consumed.
+//
+//   nnmf_vstep_tile  rows [64 b, 64 b + 64): Q = X W^T (K = n in chunks of
+//                    32 columns), the residual sum (x - v.w)^2 of the same X
+//                    chunk (V tile resident in smem, the W chunk a second
+//                    time rank-major), then V' = V Q / (V G_W + 1e-300) (or
+//                    the gradient 2 (V G_W - Q)) -- the same fused
+//                    objective / update contract as nnmf_vstep_kernel
+//   nnmf_wpart_tile  P = V'^T X over a row split: 64 ranks x 64 columns per
+//                    CTA, K = 32 rows per chunk, partials [split][r][n] in
+//                    fp64 (reduced in split order by nnmf_wreduce_kernel)
+// Both sum in a fixed order: deterministic run to run.
+#include "mmk_common.cuh"
+#include "nnmf_tile.h"
+
+namespace {
+
+using namespace mmk;
+
+constexpr int TT = 256;   // threads
+constexpr int TR = 64;    // rows (V step) / ranks (W step) per CTA
+constexpr int TK = 32;    // K per chunk
+constexpr int RK = 64;    // rank tile (r <= 64)
+constexpr int TC = 64;    // columns per CTA (W step)
+enum { F_UPDATE = 1, F_RESID = 2, F_GRAD = 4 };   // as nnmf.cu VSTEP_*
+
+template <typename T>
+struct VSmem {
+    T xs[TR][TK + 1];    // X chunk [row][col]
+    T wa[TK][RK + 1];    // W chunk [col][rank] (Q operand)
+    T wb[RK][TK + 1];    // W chunk [rank][col] (residual operand)
+    T vs[TR][RK + 1];    // V tile [row][rank]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TT)
+nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
+                const T* __restrict__ W, const double* __restrict__ GW, T* __restrict__ Vout,
+                long long m, long long n, int r, int flags, double* __restrict__ respart,
+                unsigned int* counter, double* res_out) {
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    VSmem<T>& S = *reinterpret_cast<VSmem<T>*>(tile_smem);
+    __shared__ double sc[32];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long row0 = (long long)blockIdx.x * TR;
+    const bool resid = flags & F_RESID;
+    for (int e = tid; e < TR * RK; e += TT) {
+        const int i = e / RK, k = e % RK;
+        S.vs[i][k] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
+    }
+    // chunk loads: X rows tid/32 + 8u, column tid%32; W ranks tid/32 + 8u, same column
+    const int lr = tid >> 5, lc = tid & 31;
+    T xr[8], wr[8];
+    auto load = [&](long long j0) {
+        const long long j = j0 + lc;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = row0 + lr + 8 * u;
+            const int k = lr + 8 * u;
+            xr[u] = (i < m && j < n) ? X[i * ldx + j] : T(0);
+            wr[u] = (k < r && j < n) ? W[(long long)k * n + j] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            S.xs[lr + 8 * u][lc] = xr[u];
+            S.wb[lr + 8 * u][lc] = wr[u];
+            S.wa[lc][lr + 8 * u] = wr[u];
+        }
+    };
+    T q[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[i][j] = T(0);
+    double res = 0.0;
+    const long long nch = (n + TK - 1) / TK;
+    load(0);
+    store();
+    __syncthreads();
+    for (long long c = 0; c < nch; ++c) {
+        const long long j0 = c * TK;
+        if (c + 1 < nch) load(j0 + TK);   // in flight while this chunk is consumed
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            T a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = S.xs[ty + 16 * i][kk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = S.wa[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) q[i][j] = fma(a[i], b[j], q[i][j]);
+        }
+        if (resid) {   // rows ty + 16 i, chunk columns tx + 16 j (j < 2)
+            T rec[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rec[i][0] = rec[i][1] = T(0);
+#pragma unroll 8
+            for (int k = 0; k < RK; ++k) {
+                T a[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = S.vs[ty + 16 * i][k];
+                const T b0 = S.wb[k][tx], b1 = S.wb[k][tx + 16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    rec[i][0] = fma(a[i], b0, rec[i][0]);
+                    rec[i][1] = fma(a[i], b1, rec[i][1]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (row0 + ty + 16 * i < m && j0 + tx + 16 * j < n) {
+                        const double d = (double)S.xs[ty + 16 * i][tx + 16 * j] - (double)rec[i][j];
+                        res = fma(d, d, res);
+                    }
+                }
+        }
+        __syncthreads();
+        if (c + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+    if (flags & F_UPDATE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const long long row = row0 + ty + 16 * i;
+            double den[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int l = 0; l < r; ++l) {
+                const double vl = (double)S.vs[ty + 16 * i][l];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int k = tx + 16 * j;
+                    if (k < r) den[j] = fma(vl, GW[l * r + k], den[j]);
+                }
+            }
+            if (row >= m) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = tx + 16 * j;
+                if (k >= r) continue;
+                if (flags & F_GRAD) {   // 2 (V G_W - X W^T)
+                    Vout[row * r + k] = (T)(2.0 * (den[j] - (double)q[i][j]));
+                } else {
+                    const double vk = (double)S.vs[ty + 16 * i][k];
+                    Vout[row * r + k] = (T)(vk * ((double)q[i][j] / (den[j] + kDenomGuard)));
+                }
+            }
+        }
+    }
+    if (!resid) return;
+    const double bs = block_sum(res, sc);
+    if (tid == 0) respart[blockIdx.x] = bs;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(respart, gridDim.x, sc);
+        if (tid == 0) *res_out = tot;
+    }
+}
+
+template <typename T>
+struct WSmem {
+    T vs[TK][TR + 1];   // V' chunk [row][rank]
+    T xs[TK][TC + 1];   // X chunk [row][col]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TT)
+nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V, long long m,
+                long long n, int r, long long rows_per_split, double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    WSmem<T>& S = *reinterpret_cast<WSmem<T>*>(tile_smem);
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long c0 = (long long)blockIdx.x * TC;
+    const long long lo = (long long)blockIdx.y * rows_per_split;
+    const long long hi = lo + rows_per_split < m ? lo + rows_per_split : m;
+    // chunk loads: X rows tid/64 + 4u, column tid%64; V rows tid/64 + 4u, rank tid%64
+    const int lr = tid >> 6, lc = tid & 63;
+    T xr[8], vr[8];
+    auto load = [&](long long i0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = i0 + lr + 4 * u;
+            xr[u] = (i < hi && c0 + lc < n) ? X[i * ldx + c0 + lc] : T(0);
+            vr[u] = (i < hi && lc < r) ? V[i * r + lc] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            S.xs[lr + 4 * u][lc] = xr[u];
+            S.vs[lr + 4 * u][lc] = vr[u];
+        }
+    };
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    const long long nch = hi > lo ? (hi - lo + TK - 1) / TK : 0;
+    if (nch > 0) {
+        load(lo);
+        store();
+        __syncthreads();
+    }
+    for (long long c = 0; c < nch; ++c) {
+        if (c + 1 < nch) load(lo + (c + 1) * TK);
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            T a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = S.vs[kk][ty + 16 * i];   // ranks: broadcast
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = S.xs[kk][tx + 16 * j];   // columns: 16 consecutive
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+        if (c + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+    double* o = out + (long long)blockIdx.y * r * n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = ty + 16 * i;
+        if (k >= r) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long col = c0 + tx + 16 * j;
+            if (col < n) o[(long long)k * n + col] = (double)acc[i][j];
+        }
+    }
+}
+
+}  // namespace
+
+namespace mmk_tile {
+
+bool applies(long long r) { return r > 16 && r <= RK; }
+
+long long vstep_blocks(long long m) { return (m + TR - 1) / TR; }
+
+template <typename T>
+void vstep(const T* X, long long ldx, const T* V, const T* W, const double* GW, T* Vout,
+           long long m, long long n, int r, int flags, double* respart, unsigned int* counter,
+           double* res_out, cudaStream_t st) {
+    const size_t smem = sizeof(VSmem<T>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tile<T>)))
+        cudaFuncSetAttribute(nnmf_vstep_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    MMK_LAUNCH("nnmf_vstep_tile", st,
+               (nnmf_vstep_tile<T><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                   X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out)));
+}
+
+template <typename T>
+int wpart_splits(long long m, long long n, int max_splits) {
+    const long long cb = (n + TC - 1) / TC;
+    long long S = (2 * kNumSMs + cb - 1) / cb;
+    const long long smax = (m + TK - 1) / TK;
+    if (S > smax) S = smax;
+    if (S > max_splits) S = max_splits;
+    return S < 1 ? 1 : (int)S;
+}
+
+template <typename T>
+void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
+           double* out, cudaStream_t st) {
+    const size_t smem = sizeof(WSmem<T>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_tile<T>)))
+        cudaFuncSetAttribute(nnmf_wpart_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const long long rps = (m + S - 1) / S;
+    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
+    MMK_LAUNCH("nnmf_wpart_tile", st,
+               (nnmf_wpart_tile<T><<<grid, TT, smem, st>>>(X, ldx, V, m, n, r, rps, out)));
+}
+
+template void vstep<float>(const float*, long long, const float*, const float*, const double*,
+                           float*, long long, long long, int, int, double*, unsigned int*,
+                           double*, cudaStream_t);
+template void vstep<double>(const double*, long long, const double*, const double*,
+                            const double*, double*, long long, long long, int, int, double*,
+                            unsigned int*, double*, cudaStream_t);
+template int wpart_splits<float>(long long, long long, int);
+template int wpart_splits<double>(long long, long long, int);
+template void wpart<float>(const float*, long long, const float*, long long, long long, int, int,
+                           double*, cudaStream_t);
+template void wpart<double>(const double*, long long, const double*, long long, long long, int,
+                            int, double*, cudaStream_t);
+
+}  // namespace mmk_tile

@@ -1,0 +1,24 @@
+// nnmf_tile.h -- host interface of the register-blocked NNMF kernels
+// (nnmf_tile.cu): ranks 17..64, fp64 at any shape and the fp32 shapes the
+// tensor-core path does not take.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace mmk_tile {
+
+bool applies(long long r);
+long long vstep_blocks(long long m);   // CTAs (= partial slots) of vstep
+// the fused V step: flags as nnmf.cu VSTEP_UPDATE / VSTEP_RESID / VSTEP_GRAD
+template <typename T>
+void vstep(const T* X, long long ldx, const T* V, const T* W, const double* GW, T* Vout,
+           long long m, long long n, int r, int flags, double* respart, unsigned int* counter,
+           double* res_out, cudaStream_t st);
+// P = V^T X split over S row ranges -> out[S][r][n] (S = 1: the final P)
+template <typename T>
+int wpart_splits(long long m, long long n, int max_splits);
+template <typename T>
+void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
+           double* out, cudaStream_t st);
+
+}  // namespace mmk_tile
