@@ -1,0 +1,75 @@
+"""Register-blocked CUDA-core NNMF kernels for ranks 17..64
+(csrc/nnmf_tile.cu): fp64 at a large shape and fp32 shapes the tensor-core
+path does not take, against the same iterations in torch fp64 (cuBLAS DGEMM,
+not our kernels); the grouping of the reference (nnmf.py:84-110) up to
+rounding."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1003_3272_b200 as M
+from paper_1003_3272_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def torch_trace(x, v, w, iters):
+    xd, v, w = x.double(), v.double(), w.double()
+    trace = []
+    for _ in range(iters):
+        trace.append(float(((xd - v @ w) ** 2).sum()))
+        v = v * ((xd @ w.T) / (v @ (w @ w.T) + 1e-300))
+        w = w * ((v.T @ xd) / ((v.T @ v) @ w + 1e-300))
+    trace.append(float(((xd - v @ w) ** 2).sum()))
+    return np.array(trace), v @ w
+
+
+def run_profiled(x, r, dtype, iters, v0, w0, fused=True):
+    lib = _lib.load()
+    lib.mmk_prof_enable(1)
+    try:
+        st, tr = M.nnmf_run(M.NnmfProblem(x=x, rank=r),
+                            M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6),
+                            M.Backend(dtype=dtype, fused=fused), state0=M.FactorPair(v0, w0))
+        torch.cuda.synchronize()
+    finally:
+        lib.mmk_prof_enable(0)
+    return st, tr, _lib.prof_report()
+
+
+def test_fp64_large_shape_matches_torch_fp64():
+    """fp64, 32768 x 8192, r = 64 -- the shape class of BASELINE config 4 in
+    the reference's precision -- 4 iterations per-iteration (the launch
+    profiler sees every kernel): trace and V W to 1e-10."""
+    m, n, r, iters = 32768, 8192, 64, 4
+    g = torch.Generator(device="cuda").manual_seed(64)
+    x = torch.rand(m, n, device="cuda", generator=g, dtype=torch.float64)
+    v0 = torch.rand(m, r, device="cuda", generator=g, dtype=torch.float64)
+    w0 = torch.rand(r, n, device="cuda", generator=g, dtype=torch.float64)
+    st, tr, prof = run_profiled(x, r, "fp64", iters, v0, w0, fused=False)
+    assert "nnmf_vstep_tile" in prof and "nnmf_wpart_tile" in prof, sorted(prof)
+    want, vw = torch_trace(x, v0, w0, iters)
+    assert np.max(np.abs(tr.objective_values - want) / want) < 1e-10
+    got = st.v.double() @ st.w.double()
+    assert float((got - vw).norm() / vw.norm()) < 1e-10
+
+
+@pytest.mark.parametrize("m,n,r", [(1001, 777, 40), (2050, 3001, 17), (515, 4099, 64)])
+def test_fp32_shapes_off_the_tensor_cores(m, n, r):
+    """fp32 with m or n not a multiple of 8 (no TMA-aligned pre-split copy):
+    the tile kernels, 8 fused iterations, to 1e-4."""
+    iters = 8
+    g = torch.Generator(device="cuda").manual_seed(m + n + r)
+    x = torch.rand(m, n, device="cuda", generator=g)
+    v0 = torch.rand(m, r, device="cuda", generator=g)
+    w0 = torch.rand(r, n, device="cuda", generator=g)
+    st, tr, prof = run_profiled(x, r, "fp32", iters, v0, w0, fused=False)
+    assert "nnmf_vstep_tile" in prof and "nnmf_vstep_tc" not in prof, sorted(prof)
+    want, vw = torch_trace(x, v0, w0, iters)
+    assert np.max(np.abs(tr.objective_values - want) / want) < 1e-4
+    got = st.v.double() @ st.w.double()
+    assert float((got - vw).norm() / vw.norm()) < 1e-4
+    # and the fused device loop gives the same trace bitwise
+    _, tr2, _ = run_profiled(x, r, "fp32", iters, v0, w0, fused=True)
+    assert np.array_equal(tr.objective_values, tr2.objective_values)
