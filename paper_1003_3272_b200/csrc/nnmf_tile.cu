@@ -11,7 +11,10 @@
 // (rows / ranks ty + 16 i, tx + 16 j: the operand a thread reads from shared
 // memory is either a warp broadcast or 16 consecutive values -- one
 // wavefront), with the X / W chunks of the next K step prefetched into
-// registers while the current one is consumed.
+// registers while the current one is consumed.  A thread's 4 rows (V step)
+// or 4 ranks (W step) are contiguous in a transposed smem copy, so the
+// broadcast operand arrives as two 16-byte loads: the kernels are bound by
+// shared-memory wavefronts (ncu: L1 ~90 %, FP64 pipe ~47 % with scalar loads).
 //
 //   nnmf_vstep_tile  rows [64 b, 64 b + 64): Q = X W^T (K = n in chunks of
 //                    32 columns), the residual sum (x - v.w)^2 of the same X
@@ -37,13 +40,37 @@ constexpr int RK = 64;    // rank tile (r <= 64)
 constexpr int TC = 64;    // columns per CTA (W step)
 enum { F_UPDATE = 1, F_RESID = 2, F_GRAD = 4 };   // as nnmf.cu VSTEP_*
 
+// transposed rows padded by 16 bytes: 16-byte aligned for the vector loads,
+// and the transposing stores hit 8 bank groups per warp (4-way) instead of 4
 template <typename T>
 struct VSmem {
-    T xs[TR][TK + 1];    // X chunk [row][col]
+    static constexpr int TP = 16 / (int)sizeof(T);
+    T xt[TK][TR + TP];   // X chunk [col][row]
     T wa[TK][RK + 1];    // W chunk [col][rank] (Q operand)
     T wb[RK][TK + 1];    // W chunk [rank][col] (residual operand)
-    T vs[TR][RK + 1];    // V tile [row][rank]
+    T vt[RK][TR + TP];   // V tile [rank][row]
 };
+
+// the 4 consecutive values p[0..3] (16-byte aligned) as two / one vector loads
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, T (&a)[4]);
+template <>
+__device__ __forceinline__ void ld4<double>(const double* p, double (&a)[4]) {
+    const double2 u = *reinterpret_cast<const double2*>(p);
+    const double2 v = *reinterpret_cast<const double2*>(p + 2);
+    a[0] = u.x;
+    a[1] = u.y;
+    a[2] = v.x;
+    a[3] = v.y;
+}
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float (&a)[4]) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    a[0] = u.x;
+    a[1] = u.y;
+    a[2] = u.z;
+    a[3] = u.w;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(TT)
@@ -59,7 +86,7 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     const bool resid = flags & F_RESID;
     for (int e = tid; e < TR * RK; e += TT) {
         const int i = e / RK, k = e % RK;
-        S.vs[i][k] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
+        S.vt[k][i] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
     }
     // chunk loads: X rows tid/32 + 8u, column tid%32; W ranks tid/32 + 8u, same column
     const int lr = tid >> 5, lc = tid & 31;
@@ -77,7 +104,7 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     auto store = [&]() {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            S.xs[lr + 8 * u][lc] = xr[u];
+            S.xt[lc][lr + 8 * u] = xr[u];
             S.wb[lr + 8 * u][lc] = wr[u];
             S.wa[lc][lr + 8 * u] = wr[u];
         }
@@ -98,8 +125,7 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             T a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = S.xs[ty + 16 * i][kk];
+            ld4<T>(&S.xt[kk][4 * ty], a);   // rows 4 ty .. 4 ty + 3
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = S.wa[kk][tx + 16 * j];
 #pragma unroll
@@ -107,15 +133,14 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 #pragma unroll
                 for (int j = 0; j < 4; ++j) q[i][j] = fma(a[i], b[j], q[i][j]);
         }
-        if (resid) {   // rows ty + 16 i, chunk columns tx + 16 j (j < 2)
+        if (resid) {   // rows 4 ty + i, chunk columns tx + 16 j (j < 2)
             T rec[4][2];
 #pragma unroll
             for (int i = 0; i < 4; ++i) rec[i][0] = rec[i][1] = T(0);
 #pragma unroll 8
             for (int k = 0; k < RK; ++k) {
                 T a[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = S.vs[ty + 16 * i][k];
+                ld4<T>(&S.vt[k][4 * ty], a);
                 const T b0 = S.wb[k][tx], b1 = S.wb[k][tx + 16];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -124,14 +149,17 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 2; ++j) {
+                T xv[4];
+                ld4<T>(&S.xt[tx + 16 * j][4 * ty], xv);
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (row0 + ty + 16 * i < m && j0 + tx + 16 * j < n) {
-                        const double d = (double)S.xs[ty + 16 * i][tx + 16 * j] - (double)rec[i][j];
+                for (int i = 0; i < 4; ++i) {
+                    if (row0 + 4 * ty + i < m && j0 + tx + 16 * j < n) {
+                        const double d = (double)xv[i] - (double)rec[i][j];
                         res = fma(d, d, res);
                     }
                 }
+            }
         }
         __syncthreads();
         if (c + 1 < nch) {
@@ -142,10 +170,10 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     if (flags & F_UPDATE) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const long long row = row0 + ty + 16 * i;
+            const long long row = row0 + 4 * ty + i;
             double den[4] = {0.0, 0.0, 0.0, 0.0};
             for (int l = 0; l < r; ++l) {
-                const double vl = (double)S.vs[ty + 16 * i][l];
+                const double vl = (double)S.vt[l][4 * ty + i];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int k = tx + 16 * j;
@@ -160,7 +188,7 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                 if (flags & F_GRAD) {   // 2 (V G_W - X W^T)
                     Vout[row * r + k] = (T)(2.0 * (den[j] - (double)q[i][j]));
                 } else {
-                    const double vk = (double)S.vs[ty + 16 * i][k];
+                    const double vk = (double)S.vt[k][4 * ty + i];
                     Vout[row * r + k] = (T)(vk * ((double)q[i][j] / (den[j] + kDenomGuard)));
                 }
             }
@@ -177,8 +205,8 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 
 template <typename T>
 struct WSmem {
-    T vs[TK][TR + 1];   // V' chunk [row][rank]
-    T xs[TK][TC + 1];   // X chunk [row][col]
+    T vs[TK][TR + 16 / sizeof(T)];   // V' chunk [row][rank]
+    T xs[TK][TC + 1];                // X chunk [row][col]
 };
 
 template <typename T>
@@ -225,8 +253,7 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             T a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = S.vs[kk][ty + 16 * i];   // ranks: broadcast
+            ld4<T>(&S.vs[kk][4 * ty], a);   // ranks 4 ty .. 4 ty + 3 (warp broadcast)
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = S.xs[kk][tx + 16 * j];   // columns: 16 consecutive
 #pragma unroll
@@ -243,7 +270,7 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     double* o = out + (long long)blockIdx.y * r * n;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const int k = ty + 16 * i;
+        const int k = 4 * ty + i;
         if (k >= r) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
