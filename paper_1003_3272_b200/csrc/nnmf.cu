@@ -533,7 +533,7 @@ struct K {
     static void vstep(const T* X, long long ldx, const T* V, const T* W, T* Vout, long long m,
                       long long n, int r, int flags, const Plan& P, const Ws& L, double* res_out,
                       cudaStream_t st) {
-        if (RMAX > 16 && RMAX <= 64 && mmk_tile::applies(r)) {   // ranks 17..64: nnmf_tile.cu
+        if (RMAX > 16 && mmk_tile::applies(r)) {   // ranks 17..128: nnmf_tile.cu
             mmk_tile::vstep<T>(X, ldx, V, W, L.GW, Vout, m, n, r, flags, L.respart, L.counters,
                                res_out, st);
             return;
@@ -569,7 +569,7 @@ struct K {
     }
     static void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r,
                       const Plan& P, const Ws& L, double* red, cudaStream_t st) {
-        if (RMAX > 16 && RMAX <= 64 && mmk_tile::applies(r)) {   // ranks 17..64: nnmf_tile.cu
+        if (RMAX > 16 && mmk_tile::applies(r)) {   // ranks 17..128: nnmf_tile.cu
             const int S = mmk_tile::wpart_splits<T>(m, n, P.S);
             mmk_tile::wpart<T>(X, ldx, V, m, n, r, S, S > 1 ? L.wpart : red, st);
             if (S > 1) {

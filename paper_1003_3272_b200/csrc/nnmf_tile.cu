@@ -1,7 +1,8 @@
 // nnmf_tile.cu -- register-blocked CUDA-core kernels of the Frobenius NNMF
-// iteration for ranks 17..64: the fp64 path at any shape (BASELINE config 4
+// iteration for ranks 17..128 (rank tiles of 64 or 128): the fp64 path at any
+// shape (BASELINE config 4
 // in fp64: 131072 x 16384, r = 64) and fp32 shapes the tensor-core path does
-// not take (nnmf_tc.cu).  Reference: nnmf_objective / nnmf_update_v /
+// not take (nnmf_tc.cu: ranks 17..64, TMA-aligned shapes).  Reference: nnmf_objective / nnmf_update_v /
 // nnmf_update_w (nnmf.py:75-110).
 //
 // The warp-per-row kernels of nnmf.cu keep a row's r dot products in
@@ -36,13 +37,12 @@ using namespace mmk;
 constexpr int TT = 256;   // threads
 constexpr int TR = 64;    // rows (V step) / ranks (W step) per CTA
 constexpr int TK = 32;    // K per chunk
-constexpr int RK = 64;    // rank tile (r <= 64)
 constexpr int TC = 64;    // columns per CTA (W step)
 enum { F_UPDATE = 1, F_RESID = 2, F_GRAD = 4 };   // as nnmf.cu VSTEP_*
 
 // transposed rows padded by 16 bytes: 16-byte aligned for the vector loads,
 // and the transposing stores hit 8 bank groups per warp (4-way) instead of 4
-template <typename T>
+template <typename T, int RK>   // RK: rank tile, 64 or 128
 struct VSmem {
     static constexpr int TP = 16 / (int)sizeof(T);
     T xt[TK][TR + TP];   // X chunk [col][row]
@@ -72,14 +72,15 @@ __device__ __forceinline__ void ld4<float>(const float* p, float (&a)[4]) {
     a[3] = u.w;
 }
 
-template <typename T>
+template <typename T, int RK>
 __global__ void __launch_bounds__(TT)
 nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                 const T* __restrict__ W, const double* __restrict__ GW, T* __restrict__ Vout,
                 long long m, long long n, int r, int flags, double* __restrict__ respart,
                 unsigned int* counter, double* res_out) {
     extern __shared__ __align__(16) unsigned char tile_smem[];
-    VSmem<T>& S = *reinterpret_cast<VSmem<T>*>(tile_smem);
+    constexpr int RJ = RK / 16;   // ranks per thread: tx + 16 j
+    VSmem<T, RK>& S = *reinterpret_cast<VSmem<T, RK>*>(tile_smem);
     __shared__ double sc[32];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const long long row0 = (long long)blockIdx.x * TR;
@@ -90,30 +91,34 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
     // chunk loads: X rows tid/32 + 8u, column tid%32; W ranks tid/32 + 8u, same column
     const int lr = tid >> 5, lc = tid & 31;
-    T xr[8], wr[8];
+    T xr[8], wr[RK / 8];
     auto load = [&](long long j0) {
         const long long j = j0 + lc;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const long long i = row0 + lr + 8 * u;
-            const int k = lr + 8 * u;
             xr[u] = (i < m && j < n) ? X[i * ldx + j] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
+            const int k = lr + 8 * u;
             wr[u] = (k < r && j < n) ? W[(long long)k * n + j] : T(0);
         }
     };
     auto store = [&]() {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            S.xt[lc][lr + 8 * u] = xr[u];
+        for (int u = 0; u < 8; ++u) S.xt[lc][lr + 8 * u] = xr[u];
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
             S.wb[lr + 8 * u][lc] = wr[u];
             S.wa[lc][lr + 8 * u] = wr[u];
         }
     };
-    T q[4][4];
+    T q[4][RJ];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) q[i][j] = T(0);
+        for (int j = 0; j < RJ; ++j) q[i][j] = T(0);
     double res = 0.0;
     const long long nch = (n + TK - 1) / TK;
     load(0);
@@ -124,14 +129,14 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
         if (c + 1 < nch) load(j0 + TK);   // in flight while this chunk is consumed
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
-            T a[4], b[4];
+            T a[4], b[RJ];
             ld4<T>(&S.xt[kk][4 * ty], a);   // rows 4 ty .. 4 ty + 3
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = S.wa[kk][tx + 16 * j];
+            for (int j = 0; j < RJ; ++j) b[j] = S.wa[kk][tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) q[i][j] = fma(a[i], b[j], q[i][j]);
+                for (int j = 0; j < RJ; ++j) q[i][j] = fma(a[i], b[j], q[i][j]);
         }
         if (resid) {   // rows 4 ty + i, chunk columns tx + 16 j (j < 2)
             T rec[4][2];
@@ -171,18 +176,20 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const long long row = row0 + 4 * ty + i;
-            double den[4] = {0.0, 0.0, 0.0, 0.0};
+            double den[RJ];
+#pragma unroll
+            for (int j = 0; j < RJ; ++j) den[j] = 0.0;
             for (int l = 0; l < r; ++l) {
                 const double vl = (double)S.vt[l][4 * ty + i];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < RJ; ++j) {
                     const int k = tx + 16 * j;
                     if (k < r) den[j] = fma(vl, GW[l * r + k], den[j]);
                 }
             }
             if (row >= m) continue;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < RJ; ++j) {
                 const int k = tx + 16 * j;
                 if (k >= r) continue;
                 if (flags & F_GRAD) {   // 2 (V G_W - X W^T)
@@ -203,43 +210,47 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
 }
 
-template <typename T>
+template <typename T, int RK>
 struct WSmem {
-    T vs[TK][TR + 16 / sizeof(T)];   // V' chunk [row][rank]
+    T vs[TK][RK + 16 / sizeof(T)];   // V' chunk [row][rank]
     T xs[TK][TC + 1];                // X chunk [row][col]
 };
 
-template <typename T>
+template <typename T, int RK>
 __global__ void __launch_bounds__(TT)
 nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V, long long m,
                 long long n, int r, long long rows_per_split, double* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char tile_smem[];
-    WSmem<T>& S = *reinterpret_cast<WSmem<T>*>(tile_smem);
+    constexpr int RI = RK / 16;   // ranks per thread: RI ty .. RI ty + RI - 1
+    WSmem<T, RK>& S = *reinterpret_cast<WSmem<T, RK>*>(tile_smem);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const long long c0 = (long long)blockIdx.x * TC;
     const long long lo = (long long)blockIdx.y * rows_per_split;
     const long long hi = lo + rows_per_split < m ? lo + rows_per_split : m;
     // chunk loads: X rows tid/64 + 4u, column tid%64; V rows tid/64 + 4u, rank tid%64
     const int lr = tid >> 6, lc = tid & 63;
-    T xr[8], vr[8];
+    T xr[8], vr[8][RK / 64];
     auto load = [&](long long i0) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const long long i = i0 + lr + 4 * u;
             xr[u] = (i < hi && c0 + lc < n) ? X[i * ldx + c0 + lc] : T(0);
-            vr[u] = (i < hi && lc < r) ? V[i * r + lc] : T(0);
+#pragma unroll
+            for (int h = 0; h < RK / 64; ++h)
+                vr[u][h] = (i < hi && lc + 64 * h < r) ? V[i * r + lc + 64 * h] : T(0);
         }
     };
     auto store = [&]() {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             S.xs[lr + 4 * u][lc] = xr[u];
-            S.vs[lr + 4 * u][lc] = vr[u];
+#pragma unroll
+            for (int h = 0; h < RK / 64; ++h) S.vs[lr + 4 * u][lc + 64 * h] = vr[u][h];
         }
     };
-    T acc[4][4];
+    T acc[RI][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
     const long long nch = hi > lo ? (hi - lo + TK - 1) / TK : 0;
@@ -252,12 +263,18 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
         if (c + 1 < nch) load(lo + (c + 1) * TK);
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
-            T a[4], b[4];
-            ld4<T>(&S.vs[kk][4 * ty], a);   // ranks 4 ty .. 4 ty + 3 (warp broadcast)
+            T a[RI], b[4];
+#pragma unroll
+            for (int h = 0; h < RI / 4; ++h) {   // ranks RI ty .. (warp broadcast)
+                T a4[4];
+                ld4<T>(&S.vs[kk][RI * ty + 4 * h], a4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[4 * h + e] = a4[e];
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = S.xs[kk][tx + 16 * j];   // columns: 16 consecutive
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
@@ -269,8 +286,8 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
     double* o = out + (long long)blockIdx.y * r * n;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = 4 * ty + i;
+    for (int i = 0; i < RI; ++i) {
+        const int k = RI * ty + i;
         if (k >= r) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -284,21 +301,31 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 
 namespace mmk_tile {
 
-bool applies(long long r) { return r > 16 && r <= RK; }
+bool applies(long long r) { return r > 16 && r <= 128; }
 
 long long vstep_blocks(long long m) { return (m + TR - 1) / TR; }
+
+template <typename T, int RK>
+void vstep_rk(const T* X, long long ldx, const T* V, const T* W, const double* GW, T* Vout,
+              long long m, long long n, int r, int flags, double* respart, unsigned int* counter,
+              double* res_out, cudaStream_t st) {
+    const size_t smem = sizeof(VSmem<T, RK>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tile<T, RK>)))
+        cudaFuncSetAttribute(nnmf_vstep_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    MMK_LAUNCH("nnmf_vstep_tile", st,
+               (nnmf_vstep_tile<T, RK><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                   X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out)));
+}
 
 template <typename T>
 void vstep(const T* X, long long ldx, const T* V, const T* W, const double* GW, T* Vout,
            long long m, long long n, int r, int flags, double* respart, unsigned int* counter,
            double* res_out, cudaStream_t st) {
-    const size_t smem = sizeof(VSmem<T>);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tile<T>)))
-        cudaFuncSetAttribute(nnmf_vstep_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    MMK_LAUNCH("nnmf_vstep_tile", st,
-               (nnmf_vstep_tile<T><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
-                   X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out)));
+    if (r <= 64)
+        vstep_rk<T, 64>(X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out, st);
+    else
+        vstep_rk<T, 128>(X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out, st);
 }
 
 template <typename T>
@@ -311,17 +338,26 @@ int wpart_splits(long long m, long long n, int max_splits) {
     return S < 1 ? 1 : (int)S;
 }
 
-template <typename T>
-void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
-           double* out, cudaStream_t st) {
-    const size_t smem = sizeof(WSmem<T>);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_tile<T>)))
-        cudaFuncSetAttribute(nnmf_wpart_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <typename T, int RK>
+void wpart_rk(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
+              double* out, cudaStream_t st) {
+    const size_t smem = sizeof(WSmem<T, RK>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_tile<T, RK>)))
+        cudaFuncSetAttribute(nnmf_wpart_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     const long long rps = (m + S - 1) / S;
     dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
     MMK_LAUNCH("nnmf_wpart_tile", st,
-               (nnmf_wpart_tile<T><<<grid, TT, smem, st>>>(X, ldx, V, m, n, r, rps, out)));
+               (nnmf_wpart_tile<T, RK><<<grid, TT, smem, st>>>(X, ldx, V, m, n, r, rps, out)));
+}
+
+template <typename T>
+void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
+           double* out, cudaStream_t st) {
+    if (r <= 64)
+        wpart_rk<T, 64>(X, ldx, V, m, n, r, S, out, st);
+    else
+        wpart_rk<T, 128>(X, ldx, V, m, n, r, S, out, st);
 }
 
 template void vstep<float>(const float*, long long, const float*, const float*, const double*,

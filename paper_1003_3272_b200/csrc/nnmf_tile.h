@@ -1,5 +1,5 @@
 // nnmf_tile.h -- host interface of the register-blocked NNMF kernels
-// (nnmf_tile.cu): ranks 17..64, fp64 at any shape and the fp32 shapes the
+// (nnmf_tile.cu): ranks 17..128, fp64 at any shape and the fp32 shapes the
 // tensor-core path does not take.
 #pragma once
 

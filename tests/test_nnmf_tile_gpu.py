@@ -73,3 +73,37 @@ def test_fp32_shapes_off_the_tensor_cores(m, n, r):
     # and the fused device loop gives the same trace bitwise
     _, tr2, _ = run_profiled(x, r, "fp32", iters, v0, w0, fused=True)
     assert np.array_equal(tr.objective_values, tr2.objective_values)
+
+
+def test_rank128_large_shape_fp32():
+    """r = 128 at 65536 x 16384 in fp32 (the review's large-shape check of a
+    rank above the tensor-core path's 64): the 128-rank tiles, 5 fused
+    iterations against torch fp64, trace and V W to 1e-4."""
+    m, n, r, iters = 65536, 16384, 128, 5
+    g = torch.Generator(device="cuda").manual_seed(128)
+    x = torch.rand(m, n, device="cuda", generator=g)
+    v0 = torch.rand(m, r, device="cuda", generator=g)
+    w0 = torch.rand(r, n, device="cuda", generator=g)
+    st, tr, prof = run_profiled(x, r, "fp32", iters, v0, w0, fused=False)
+    assert "nnmf_vstep_tile" in prof and "nnmf_wpart_tile" in prof, sorted(prof)
+    want, vw = torch_trace(x, v0, w0, iters)
+    assert np.max(np.abs(tr.objective_values - want) / want) < 1e-4
+    got = st.v.double() @ st.w.double()
+    assert float((got - vw).norm() / vw.norm()) < 1e-4
+
+
+@pytest.mark.parametrize("r", [65, 100, 128])
+def test_fp64_ranks_above_64(r):
+    """fp64, ranks 65..128 (the 128-rank tiles, zero-padded ranks), 6
+    iterations against torch fp64 to 1e-10."""
+    m, n, iters = 3000, 2100, 6
+    g = torch.Generator(device="cuda").manual_seed(r)
+    x = torch.rand(m, n, device="cuda", generator=g, dtype=torch.float64)
+    v0 = torch.rand(m, r, device="cuda", generator=g, dtype=torch.float64)
+    w0 = torch.rand(r, n, device="cuda", generator=g, dtype=torch.float64)
+    st, tr, prof = run_profiled(x, r, "fp64", iters, v0, w0, fused=False)
+    assert "nnmf_vstep_tile" in prof, sorted(prof)
+    want, vw = torch_trace(x, v0, w0, iters)
+    assert np.max(np.abs(tr.objective_values - want) / want) < 1e-10
+    got = st.v.double() @ st.w.double()
+    assert float((got - vw).norm() / vw.norm()) < 1e-10
