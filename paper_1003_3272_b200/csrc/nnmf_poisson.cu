@@ -20,6 +20,7 @@
 // red = [P (r x n) | vs (r) | f-partial]; the caller all-reduces red; phase B
 // finishes W' redundantly on every rank.
 #include "mmk_common.cuh"
+#include "nnmf_tile.h"
 
 namespace {
 
@@ -316,7 +317,11 @@ int run_a(const Args& a) {
     }
     MMK_LAUNCH("pois_wsum", st,
                (pois_wsum_kernel<T><<<a.r, 256, 0, st>>>(W, a.n, L.wsum)));
-    if (RMAX <= 16 && P.rpw == 2)
+    const bool tile = RMAX > 16 && mmk_tile::applies(a.r);   // ranks 17..64: nnmf_tile.cu
+    if (tile)
+        mmk_tile::pois_vstep<T>(X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter,
+                                f_out, a.err, st);
+    else if (RMAX <= 16 && P.rpw == 2)
         MMK_LAUNCH("pois_vstep", st,
                    (pois_vstep_kernel<T, RMAX, 2><<<P.nvb, kThreads, 0, st>>>(
                        X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter, f_out,
@@ -331,14 +336,21 @@ int run_a(const Args& a) {
                (pois_colsum_kernel<T><<<P.csb, 256, 0, st>>>(Vo, a.m, a.r, P.csr, L.cpart)));
     MMK_LAUNCH("pois_colsum_reduce", st,
                (pois_colsum_reduce_kernel<<<1, 64, 0, st>>>(L.cpart, P.csb, a.r, a.red + rn)));
-    dim3 grid(P.colblocks, P.S);
-    double* dst = P.S > 1 ? L.wpart : a.red;
-    MMK_LAUNCH("pois_wpart", st,
-               (pois_wpart_kernel<T, RMAX><<<grid, kThreads, 0, st>>>(
-                   X, a.ldx, Vo, W, a.m, a.n, a.r, P.rows_per_split, dst, a.err)));
-    if (P.S > 1)
+    int S = P.S;
+    if (tile) {
+        S = mmk_tile::wpart_splits<T>(a.m, a.n, P.S);
+        mmk_tile::pois_wpart<T>(X, a.ldx, Vo, W, a.m, a.n, a.r, S, S > 1 ? L.wpart : a.red,
+                                a.err, st);
+    } else {
+        dim3 grid(P.colblocks, P.S);
+        double* dst = P.S > 1 ? L.wpart : a.red;
+        MMK_LAUNCH("pois_wpart", st,
+                   (pois_wpart_kernel<T, RMAX><<<grid, kThreads, 0, st>>>(
+                       X, a.ldx, Vo, W, a.m, a.n, a.r, P.rows_per_split, dst, a.err)));
+    }
+    if (S > 1)
         MMK_LAUNCH("pois_wreduce", st,
-                   (pois_wreduce_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(L.wpart, P.S, rn,
+                   (pois_wreduce_kernel<<<ceil_div(rn, 256), 256, 0, st>>>(L.wpart, S, rn,
                                                                           a.red)));
     MMK_CHECK_LAUNCH("pois_wstep");
     return MMK_OK;

@@ -297,6 +297,247 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Poisson loss (nnmf.py:178-265), ranks 17..64, the contract of
+// pois_vstep_kernel / pois_wpart_kernel (nnmf_poisson.cu): per X chunk the
+// reconstruction b = v.w of every element (K = r, as the residual above), the
+// objective terms x ln b - b, and the ratio x / b (0 where x = 0) written over
+// the X chunk in smem, then the same Q contraction with the ratio in place of
+// X; v' = v sqrt(q / (sum_j w_kj + 1e-300)).  A zero b under a positive count
+// flags site 1 (objective class) in the V step, site 2 (update only) in the W
+// step.
+template <typename T>
+__global__ void __launch_bounds__(TT)
+pois_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
+                const T* __restrict__ W, const double* __restrict__ wsum, T* __restrict__ Vout,
+                long long m, long long n, int r, double* __restrict__ fpart,
+                unsigned int* counter, double* f_out, int64_t* err) {
+    constexpr int RK = 64, RJ = 4;
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    VSmem<T, RK>& S = *reinterpret_cast<VSmem<T, RK>*>(tile_smem);
+    __shared__ double sc[32];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long row0 = (long long)blockIdx.x * TR;
+    for (int e = tid; e < TR * RK; e += TT) {
+        const int i = e / RK, k = e % RK;
+        S.vt[k][i] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
+    }
+    const int lr = tid >> 5, lc = tid & 31;
+    T xr[8], wr[RK / 8];
+    auto load = [&](long long j0) {
+        const long long j = j0 + lc;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = row0 + lr + 8 * u;
+            xr[u] = (i < m && j < n) ? X[i * ldx + j] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
+            const int k = lr + 8 * u;
+            wr[u] = (k < r && j < n) ? W[(long long)k * n + j] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) S.xt[lc][lr + 8 * u] = xr[u];
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
+            S.wb[lr + 8 * u][lc] = wr[u];
+            S.wa[lc][lr + 8 * u] = wr[u];
+        }
+    };
+    T q[4][RJ];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) q[i][j] = T(0);
+    double f = 0.0;
+    const long long nch = (n + TK - 1) / TK;
+    load(0);
+    store();
+    __syncthreads();
+    for (long long c = 0; c < nch; ++c) {
+        const long long j0 = c * TK;
+        if (c + 1 < nch) load(j0 + TK);
+        {   // b, objective terms and ratio for rows 4 ty + i, columns tx + 16 j
+            T rec[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rec[i][0] = rec[i][1] = T(0);
+#pragma unroll 8
+            for (int k = 0; k < RK; ++k) {
+                T a[4];
+                ld4<T>(&S.vt[k][4 * ty], a);
+                const T b0 = S.wb[k][tx], b1 = S.wb[k][tx + 16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    rec[i][0] = fma(a[i], b0, rec[i][0]);
+                    rec[i][1] = fma(a[i], b1, rec[i][1]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const long long col = j0 + tx + 16 * j;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const long long row = row0 + 4 * ty + i;
+                    T* xp = &S.xt[tx + 16 * j][4 * ty + i];
+                    const T x = *xp, b = rec[i][j];
+                    T ratio = T(0);
+                    if (row < m && col < n) {
+                        f -= (double)b;
+                        if (x > T(0)) {
+                            if (b == T(0)) {
+                                flag_error(err, MMK_E_NUMERICS, err_at(1, row * n + col));
+                            } else {
+                                f = fma((double)x, log((double)b), f);
+                                ratio = x / b;
+                            }
+                        }
+                    }
+                    *xp = ratio;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            T a[4], b[RJ];
+            ld4<T>(&S.xt[kk][4 * ty], a);   // ratios of rows 4 ty .. 4 ty + 3
+#pragma unroll
+            for (int j = 0; j < RJ; ++j) b[j] = S.wa[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < RJ; ++j) q[i][j] = fma(a[i], b[j], q[i][j]);
+        }
+        __syncthreads();
+        if (c + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const long long row = row0 + 4 * ty + i;
+        if (row >= m) continue;
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) {
+            const int k = tx + 16 * j;
+            if (k >= r) continue;
+            const double vk = (double)S.vt[k][4 * ty + i];
+            Vout[row * r + k] = (T)(vk * sqrt((double)q[i][j] / (wsum[k] + kDenomGuard)));
+        }
+    }
+    const double bs = block_sum(f, sc);
+    if (tid == 0) fpart[blockIdx.x] = bs;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(fpart, gridDim.x, sc);
+        if (tid == 0) *f_out = tot;
+    }
+}
+
+template <typename T>
+struct PWSmem {
+    T vs[TK][64 + 16 / sizeof(T)];   // V' chunk [row][rank]
+    T xs[TK][TC + 1];                // X chunk [row][col], then the ratios
+    T wt[64][TC + 1];                // W [rank][col] of this column block (resident)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TT)
+pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
+                const T* __restrict__ W, long long m, long long n, int r,
+                long long rows_per_split, double* __restrict__ out, int64_t* err) {
+    constexpr int RI = 4;
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    PWSmem<T>& S = *reinterpret_cast<PWSmem<T>*>(tile_smem);
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long c0 = (long long)blockIdx.x * TC;
+    const long long lo = (long long)blockIdx.y * rows_per_split;
+    const long long hi = lo + rows_per_split < m ? lo + rows_per_split : m;
+    for (int e = tid; e < 64 * TC; e += TT) {
+        const int k = e / TC, cc = e % TC;
+        S.wt[k][cc] = (k < r && c0 + cc < n) ? W[(long long)k * n + c0 + cc] : T(0);
+    }
+    const int lr = tid >> 6, lc = tid & 63;
+    T xr[8], vr[8];
+    auto load = [&](long long i0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = i0 + lr + 4 * u;
+            xr[u] = (i < hi && c0 + lc < n) ? X[i * ldx + c0 + lc] : T(0);
+            vr[u] = (i < hi && lc < r) ? V[i * r + lc] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            S.xs[lr + 4 * u][lc] = xr[u];
+            S.vs[lr + 4 * u][lc] = vr[u];
+        }
+    };
+    T acc[RI][4];
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    const long long nch = hi > lo ? (hi - lo + TK - 1) / TK : 0;
+    if (nch > 0) {
+        load(lo);
+        store();
+    }
+    __syncthreads();   // wt and the first chunk
+    for (long long ch = 0; ch < nch; ++ch) {
+        const long long i0 = lo + ch * TK;
+        if (ch + 1 < nch) load(i0 + TK);
+        // ratios of this thread's elements (rows lr + 4 u, column lc), in place
+#pragma unroll 2
+        for (int u = 0; u < 8; ++u) {
+            const int rl = lr + 4 * u;
+            const T x = S.xs[rl][lc];
+            T ratio = T(0);
+            if (x > T(0)) {
+                T b = T(0);
+#pragma unroll 8
+                for (int k = 0; k < 64; ++k) b = fma(S.vs[rl][k], S.wt[k][lc], b);
+                if (b == T(0))
+                    flag_error(err, MMK_E_NUMERICS, err_at_update(2, (i0 + rl) * n + c0 + lc));
+                else
+                    ratio = x / b;
+            }
+            S.xs[rl][lc] = ratio;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            T a[RI], b[4];
+            ld4<T>(&S.vs[kk][RI * ty], a);   // ranks RI ty .. (warp broadcast)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = S.xs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < RI; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+        if (ch + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+    double* o = out + (long long)blockIdx.y * r * n;
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+        const int k = RI * ty + i;
+        if (k >= r) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long col = c0 + tx + 16 * j;
+            if (col < n) o[(long long)k * n + col] = (double)acc[i][j];
+        }
+    }
+}
+
 }  // namespace
 
 namespace mmk_tile {
@@ -360,6 +601,43 @@ void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int 
         wpart_rk<T, 128>(X, ldx, V, m, n, r, S, out, st);
 }
 
+template <typename T>
+void pois_vstep(const T* X, long long ldx, const T* V, const T* W, const double* wsum, T* Vout,
+                long long m, long long n, int r, double* fpart, unsigned int* counter,
+                double* f_out, int64_t* err, cudaStream_t st) {
+    const size_t smem = sizeof(VSmem<T, 64>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_vstep_tile<T>)))
+        cudaFuncSetAttribute(pois_vstep_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    MMK_LAUNCH("pois_vstep_tile", st,
+               (pois_vstep_tile<T><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                   X, ldx, V, W, wsum, Vout, m, n, r, fpart, counter, f_out, err)));
+}
+
+template <typename T>
+void pois_wpart(const T* X, long long ldx, const T* V, const T* W, long long m, long long n,
+                int r, int S, double* out, int64_t* err, cudaStream_t st) {
+    const size_t smem = sizeof(PWSmem<T>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_wpart_tile<T>)))
+        cudaFuncSetAttribute(pois_wpart_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const long long rps = (m + S - 1) / S;
+    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
+    MMK_LAUNCH("pois_wpart_tile", st,
+               (pois_wpart_tile<T><<<grid, TT, smem, st>>>(X, ldx, V, W, m, n, r, rps, out,
+                                                            err)));
+}
+
+template void pois_vstep<float>(const float*, long long, const float*, const float*,
+                                const double*, float*, long long, long long, int, double*,
+                                unsigned int*, double*, int64_t*, cudaStream_t);
+template void pois_vstep<double>(const double*, long long, const double*, const double*,
+                                 const double*, double*, long long, long long, int, double*,
+                                 unsigned int*, double*, int64_t*, cudaStream_t);
+template void pois_wpart<float>(const float*, long long, const float*, const float*, long long,
+                                long long, int, int, double*, int64_t*, cudaStream_t);
+template void pois_wpart<double>(const double*, long long, const double*, const double*,
+                                 long long, long long, int, int, double*, int64_t*, cudaStream_t);
 template void vstep<float>(const float*, long long, const float*, const float*, const double*,
                            float*, long long, long long, int, int, double*, unsigned int*,
                            double*, cudaStream_t);
