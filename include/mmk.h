@@ -93,6 +93,11 @@ int mmk_nnmf_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
 int mmk_nnmf_op_ws_bytes(int dtype, int64_t m, int64_t n, int64_t r, size_t *out);
 int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,
                       void *stream);
+/* the per-X preparation of the tensor-core path enqueued on `stream` (a no-op
+ * when the path does not apply or X is already prepared in `ws`); call it
+ * before mmk_nnmf_engine_create so the GPU overlaps the graph construction */
+int mmk_nnmf_prepare(int dtype, const void *X, int64_t ldx, int64_t m, int64_t n, int64_t r,
+                     void *ws, size_t ws_bytes, void *stream);
 int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r);
 int mmk_nnmf_iter_a(int dtype, const void *X, int64_t ldx, const void *V, const void *W,
                     void *V_out, int64_t m, int64_t n, int64_t r, void *ws, size_t ws_bytes,

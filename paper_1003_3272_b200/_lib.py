@@ -43,6 +43,7 @@ _SIGS = {
     "mmk_nnmf_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_nnmf_op_ws_bytes": ([_i32, _i64, _i64, _i64, _c.POINTER(_sz)], _i32),
     "mmk_nnmf_ws_clear": ([_i32, _i64, _i64, _i64, _vp, _sz, _vp], _i32),
+    "mmk_nnmf_prepare": ([_i32, _vp, _i64, _i64, _i64, _i64, _vp, _sz, _vp], _i32),
     "mmk_nnmf_reduce_len": ([_i64, _i64], _i64),
     "mmk_nnmf_iter_a": ([_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp,
                          _vp], _i32),

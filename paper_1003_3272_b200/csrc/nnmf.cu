@@ -780,6 +780,21 @@ extern "C" int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, voi
     return MMK_OK;
 }
 
+// The per-X preparation of the tensor-core path (scale exponent, pre-split
+// copy of X) enqueued on `stream` now -- a no-op when the path does not apply
+// or X is already prepared in this workspace.  A run calls it before building
+// its device-loop engine, so the GPU works while the host captures and
+// instantiates the graph (the engine's own prologue then finds X prepared).
+extern "C" int mmk_nnmf_prepare(int dtype, const void* X, int64_t ldx, int64_t m, int64_t n,
+                                int64_t r, void* ws, size_t ws_bytes, void* stream) {
+    int rc = check(dtype, m, n, r, ldx, ws_bytes, true);
+    if (rc) return rc;
+    void* tcws = mmk_tc::engine_tc_ws(dtype, X, ldx, m, n, r, ws);
+    if (!tcws) return MMK_OK;
+    return mmk_tc::prepare_x(reinterpret_cast<const float*>(X), ldx, m, n, tcws,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
 // [P (r n) | G (r r) | f | device-error flag]
 extern "C" int64_t mmk_nnmf_reduce_len(int64_t n, int64_t r) { return r * n + r * r + 2; }
 

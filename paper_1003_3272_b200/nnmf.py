@@ -148,6 +148,10 @@ class _GpuNnmf(DeviceMm):
 
     def _engine_create(self, a, b, rule, trace, stamp, ctl, eng):
         self._keep = (a, b)
+        # the per-X preparation (tensor-core path) goes to the GPU first, so it
+        # runs while the host captures and instantiates the engine's graph
+        _lib.call("mmk_nnmf_prepare", self.code, _lib.ptr(self.x), self.x.stride(0), self.m,
+                  self.n, self.r, _lib.ptr(self.ws), self.ws.numel(), self.stream())
         _lib.call("mmk_nnmf_engine_create", self.code, _lib.ptr(self.x), self.x.stride(0),
                   _lib.ptr(a.v), _lib.ptr(a.w), _lib.ptr(b.v), _lib.ptr(b.w), self.m, self.n,
                   self.r, _lib.ptr(self.ws), self.ws.numel(), _lib.ptr(self.red), self.comm,
