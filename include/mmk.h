@@ -331,6 +331,9 @@ enum {
     MMK_CTL_FCUR = 4,        /* fp64 bits: f_dev of the iteration kernels */
     MMK_CTL_REL = 5,         /* fp64 bits: last relative change */
     MMK_CTL_SLOT = 6,        /* after a stop: 0 -> state in slot A, 1 -> slot B */
+    MMK_CTL_LAST = 7,        /* 1: the next pass is the last (iteration cap) and only its f
+                                is recorded -- the fp32 tensor-core NNMF engine skips the
+                                W half of that pass */
     MMK_CTL_LEN = 16
 };
 enum {

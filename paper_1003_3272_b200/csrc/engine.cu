@@ -270,10 +270,16 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
     };
     // tensor-core path: the per-X preparation runs once (engine prologue, on
     // the run's stream) instead of as a key check in every captured iteration
+    // and the W half of a pass that only needs its objective (the iteration
+    // cap, ctl[MMK_CTL_LAST] set by the control kernel) exits at launch
     void* tcws = mmk_tc::engine_tc_ws(dtype, X, ldx, m, n, r, ws);
-    if (tcws) mmk_tc::set_x_prepared(true);
+    if (tcws) {
+        mmk_tc::set_x_prepared(true);
+        mmk_tc::set_last_flag(ctl + MMK_CTL_LAST);
+    }
     const int rc = build(iter, rule, trace, tstamp, ctl, err_dev, engine);
     mmk_tc::set_x_prepared(false);
+    mmk_tc::set_last_flag(nullptr);
     if (rc == MMK_OK && tcws) {
         const float* Xf = reinterpret_cast<const float*>(X);
         reinterpret_cast<Engine*>(*engine)->prologue = [=](cudaStream_t s) {

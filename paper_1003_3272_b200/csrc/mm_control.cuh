@@ -107,6 +107,9 @@ __device__ __forceinline__ int mm_control(int half, long long* ctl, double* trac
     int reason = 0;
     const int d = mm_step(after, half, f, err_class(err), rule, &reason);
     mm_record(ctl, trace, tstamp, before, after, half, f, d, reason);
+    // the next pass evaluates f at the iteration cap: nothing after its
+    // objective is used (run_mm never steps from the final state)
+    ctl[MMK_CTL_LAST] = (d != kMmStop && after.it >= rule.max_iters) ? 1 : 0;
     return d;
 }
 

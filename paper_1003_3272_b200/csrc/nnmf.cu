@@ -338,11 +338,12 @@ __global__ void nnmf_wreduce_kernel(const double* __restrict__ part, int S, long
 // GRAD: write 2 (G_V W - V^T X) = 2 V^T (V W - X) instead of the update
 template <typename T, bool GRAD = false>
 __global__ void nnmf_wfinish_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
-                                    int r, const double* __restrict__ red, double* f_dev) {
+                                    int r, const double* __restrict__ red, double* f_dev,
+                                    const long long* __restrict__ skip = nullptr) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long rn = (long long)r * n;
     if (f_dev && t == 0) *f_dev = red[rn + (long long)r * r];
-    if (t >= rn) return;
+    if (t >= rn || (skip && *skip)) return;   // skip: the engine's final pass needs only f
     const int k = (int)(t / n);
     const long long j = t - (long long)k * n;
     const double* G = red + rn + (long long)k * r;
@@ -361,12 +362,14 @@ constexpr int kWf64Smem = 2 * 64 * 64 * 8;
 template <typename T>
 __global__ void __launch_bounds__(256)
 nnmf_wfinish64_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n,
-                      const double* __restrict__ red, double* f_dev) {
+                      const double* __restrict__ red, double* f_dev,
+                      const long long* __restrict__ skip) {
     extern __shared__ double wf_smem[];
     double(*Gt)[64] = reinterpret_cast<double(*)[64]>(wf_smem);            // Gt[l][k] = G[k][l]
     double(*Ws)[64] = reinterpret_cast<double(*)[64]>(wf_smem + 64 * 64);  // Ws[l][j]
     const long long rn = 64 * n;
     if (f_dev && blockIdx.x == 0 && threadIdx.x == 0) *f_dev = red[rn + 64 * 64];
+    if (skip && *skip) return;   // the engine's final pass (iteration cap) needs only f
     const long long j0 = (long long)blockIdx.x * 64;
     for (int i = threadIdx.x; i < 64 * 64; i += 256) {
         const int k = i / 64, l = i % 64;
@@ -689,13 +692,13 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
         }
         MMK_LAUNCH("nnmf_wfinish", st,
                    (nnmf_wfinish64_kernel<T><<<ceil_div(n, 64), 256, kWf64Smem, st>>>(
-                       (const T*)W, (T*)W_out, n, red, f_dev)));
+                       (const T*)W, (T*)W_out, n, red, f_dev, mmk_tc::last_flag())));
         MMK_CHECK_LAUNCH("nnmf_wfinish64_kernel");
         return MMK_OK;
     }
     MMK_LAUNCH("nnmf_wfinish", st,
                (nnmf_wfinish_kernel<T><<<ceil_div(rn, 256), 256, 0, st>>>(
-                   (const T*)W, (T*)W_out, n, r, red, f_dev)));
+                   (const T*)W, (T*)W_out, n, r, red, f_dev, mmk_tc::last_flag())));
     MMK_CHECK_LAUNCH("nnmf_wfinish_kernel");
     return MMK_OK;
 }

@@ -699,7 +699,9 @@ struct WBars {
 __global__ void __launch_bounds__(kWThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mVh, const __grid_constant__ CUtensorMap mVl,
-              int m, int n, int splits, int rows_per_split, float* __restrict__ wpart) {
+              int m, int n, int splits, int rows_per_split, float* __restrict__ wpart,
+              const long long* __restrict__ skip) {
+    if (skip && *skip) return;   // the engine's final pass (iteration cap): W half unused
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
@@ -1033,7 +1035,8 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
 // interleaved partials, combined in group order (deterministic)
 __global__ void __launch_bounds__(1024)
 gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out,
-                float* __restrict__ outf) {
+                float* __restrict__ outf, const long long* __restrict__ skip = nullptr) {
+    if (skip && *skip) return;
     __shared__ double sm[8][128];
     const int o = blockIdx.x * 128 + (threadIdx.x & 127), g = threadIdx.x >> 7;
     double s = 0.0;
@@ -1110,7 +1113,9 @@ constexpr int kVprepBlocks = 2 * kNumSMs;
 constexpr uint32_t kVprepSmem = (R * (128 + 4) + 128 * (R + 4)) * 4;
 __global__ void __launch_bounds__(256)
 vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
-                  __half* __restrict__ Vtl, long long m, Scales* sc, double* __restrict__ gpart) {
+                  __half* __restrict__ Vtl, long long m, Scales* sc, double* __restrict__ gpart,
+                  const long long* __restrict__ skip) {
+    if (skip && *skip) return;
     extern __shared__ __align__(16) float vsm[];
     float(*T)[128 + 4] = reinterpret_cast<float(*)[128 + 4]>(vsm);
     float(*S)[R + 4] = reinterpret_cast<float(*)[R + 4]>(vsm + R * (128 + 4));
@@ -1195,7 +1200,8 @@ vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
 // sums, transposed through shared memory for coalesced writes
 __global__ void __launch_bounds__(256)
 wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
-                  double* __restrict__ red, const Scales* sc) {
+                  double* __restrict__ red, const Scales* sc, const long long* __restrict__ skip) {
+    if (skip && *skip) return;
     __shared__ double T[R][32 + 1];
     // partials are in the scaled units of the split products: X 2^ex, V' 2^ev
     const double pscale = exp2(-(double)(sc->ex + sc->ev));
@@ -1380,6 +1386,9 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
 }
 
 thread_local bool t_x_prepared = false;   // set while an engine captures its loop
+// set while an engine captures its loop: ctl[MMK_CTL_LAST], read by the W-half
+// kernels at run time (they exit when the pass only needs its objective)
+thread_local const long long* t_last_flag = nullptr;
 
 }  // namespace
 
@@ -1437,6 +1446,8 @@ size_t ws_bytes(long long m, long long n, long long r) {
 }
 
 void set_x_prepared(bool on) { t_x_prepared = on; }
+void set_last_flag(const int64_t* p) { t_last_flag = reinterpret_cast<const long long*>(p); }
+const long long* last_flag() { return t_last_flag; }
 
 // [begin, end) of the pre-split copy of X inside the tensor-core workspace:
 // it is always written (presplit_kernel, keyed in the zeroed header) before
@@ -1537,19 +1548,20 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
         const int vb = (int)(ceil_div(m, 128) < kVprepBlocks ? ceil_div(m, 128) : kVprepBlocks);
         MMK_LAUNCH("nnmf_vprep_gram", st,
                    (vprep_gram_kernel<<<vb, 256, kVprepSmem, st>>>(V_out, L.Vth, L.Vtl, m, L.sc,
-                                                                   L.gpart)));
+                                                                   L.gpart, t_last_flag)));
         MMK_LAUNCH("nnmf_gram_sum", st,
                    (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(L.gpart, vb, red + rn,
-                                                                   nullptr)));
+                                                                   nullptr, t_last_flag)));
     }
     MMK_LAUNCH("nnmf_wstep_tc", st,
                (nnmf_wstep_tc<<<P.wgrid, kWThreads, SMEM_W, st>>>(mXt, mXt2, mVh, mVl, (int)m,
                                                                   (int)n, P.splits,
-                                                                  P.rows_per_split, L.wpart)));
+                                                                  P.rows_per_split, L.wpart,
+                                                                  t_last_flag)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
                (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
-                                                                    L.sc)));
+                                                                    L.sc, t_last_flag)));
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a");
     return MMK_OK;
 }

@@ -23,6 +23,10 @@ int iter_a(const float* X, long long ldx, const float* V, const float* W, float*
 int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
               cudaStream_t st);
 void set_x_prepared(bool on);
+// while an engine captures: ctl[MMK_CTL_LAST] for the W-half kernels (nullptr
+// otherwise); last_flag() is what the capture passes to them
+void set_last_flag(const int64_t* p);
+const long long* last_flag();
 // [begin, end) of the pre-split copy of X in the tensor-core workspace
 void presplit_span(long long m, long long n, size_t* begin, size_t* end);
 // the NNMF workspace's tensor-core part for (dtype, m, n, r), or nullptr when
