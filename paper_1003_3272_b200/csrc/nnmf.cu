@@ -23,6 +23,18 @@
 #include "nnmf_tc.h"
 #include "nnmf_tile.h"
 
+namespace mmk_ref {   // nnmf_ref.cu: fp64 single ops in the reference's arithmetic order
+size_t ws_bytes(long long m, long long n, long long r);
+int objective(const double* X, long long ldx, const double* V, const double* W, long long m,
+              long long n, long long r, void* ws, double* f_dev, cudaStream_t st);
+int update_v(const double* X, long long ldx, const double* V, const double* W, double* Vout,
+             long long m, long long n, long long r, void* ws, cudaStream_t st);
+int update_w(const double* X, long long ldx, const double* V, const double* W, double* Wout,
+             long long m, long long n, long long r, void* ws, cudaStream_t st);
+int gradient(const double* X, long long ldx, const double* V, const double* W, double* GV,
+             double* GW, long long m, long long n, long long r, void* ws, cudaStream_t st);
+}  // namespace mmk_ref
+
 #include <type_traits>
 
 namespace {
@@ -703,6 +715,9 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
     return MMK_OK;
 }
 
+// the fp64 single ops' reference-order region follows the op workspace
+inline size_t ref_offset(size_t op_bytes) { return (op_bytes + 255) & ~size_t(255); }
+
 int check(int dtype, long long m, long long n, long long r, long long ldx, size_t ws_bytes,
           bool iter) {
     if (dtype != MMK_F32 && dtype != MMK_F64) {
@@ -715,8 +730,9 @@ int check(int dtype, long long m, long long n, long long r, long long ldx, size_
         return MMK_E_SHAPE;
     }
     const Plan P = make_plan(m, n, (int)r);
-    const size_t need = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr,
-                                  nullptr);
+    size_t need = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr,
+                            nullptr);
+    if (!iter && dtype == MMK_F64) need = ref_offset(need) + mmk_ref::ws_bytes(m, n, r);
     if (ws_bytes < need) {
         mmk_host::set_error("NNMF workspace too small: %zu < %zu", ws_bytes, need);
         return MMK_E_SHAPE;
@@ -747,6 +763,7 @@ static int ws_bytes_for(int dtype, int64_t m, int64_t n, int64_t r, bool iter, s
     }
     const Plan P = make_plan(m, n, (int)r);
     *out = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr, nullptr);
+    if (!iter && dtype == MMK_F64) *out = ref_offset(*out) + mmk_ref::ws_bytes(m, n, r);
     return MMK_OK;
 }
 
@@ -840,11 +857,23 @@ extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* 
     return mmk_nnmf_iter_b(dtype, W, W_out, n, r, red, f_dev, err_dev, stream);
 }
 
+// the reference-order region of a single-op workspace (fp64)
+static void* ref_ws(void* ws, long long m, long long n, long long r) {
+    const size_t opb = ws_layout(make_plan(m, n, (int)r), m, n, (int)r, false, nullptr, nullptr);
+    return reinterpret_cast<char*>(ws) + ref_offset(opb);
+}
+
+// fp64 single operations run in the reference's arithmetic order
+// (nnmf_ref.cu: bitwise equal to mmkit's); fp32 ones on the fused kernels
 extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const void* V,
                                   const void* W, int64_t m, int64_t n, int64_t r, void* ws,
                                   size_t ws_bytes, double* f_dev, int64_t* err_dev, void* stream) {
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
+    if (dtype == MMK_F64)
+        return mmk_ref::objective((const double*)X, ldx, (const double*)V, (const double*)W, m,
+                                  n, r, ref_ws(ws, m, n, r), f_dev,
+                                  reinterpret_cast<cudaStream_t>(stream));
     Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, nullptr, f_dev, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 2};
     return run_a(dtype, a);
@@ -855,6 +884,10 @@ extern "C" int mmk_nnmf_update_v(int dtype, const void* X, int64_t ldx, const vo
                                  void* ws, size_t ws_bytes, int64_t* err_dev, void* stream) {
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
+    if (dtype == MMK_F64)
+        return mmk_ref::update_v((const double*)X, ldx, (const double*)V, (const double*)W,
+                                 (double*)V_out, m, n, r, ref_ws(ws, m, n, r),
+                                 reinterpret_cast<cudaStream_t>(stream));
     Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, nullptr, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 1};
     return run_a(dtype, a);
@@ -866,6 +899,10 @@ extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const vo
                                  void* stream) {
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
+    if (dtype == MMK_F64)
+        return mmk_ref::update_w((const double*)X, ldx, (const double*)V, (const double*)W,
+                                 (double*)W_out, m, n, r, ref_ws(ws, m, n, r),
+                                 reinterpret_cast<cudaStream_t>(stream));
     Args a{X, V, W, nullptr, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
            reinterpret_cast<cudaStream_t>(stream), 3};
     rc = run_a(dtype, a);
@@ -884,6 +921,9 @@ extern "C" int mmk_nnmf_gradient(int dtype, const void* X, int64_t ldx, const vo
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == MMK_F64)
+        return mmk_ref::gradient((const double*)X, ldx, (const double*)V, (const double*)W,
+                                 (double*)GV, (double*)GW, m, n, r, ref_ws(ws, m, n, r), st);
     Args a{X, V, W, GV, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev, st, 4};
     rc = run_a(dtype, a);
     if (rc) return rc;

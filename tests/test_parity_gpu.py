@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import golden_io as G
+from oracle import oracle as O
 import paper_1003_3272_b200 as M
 from paper_1003_3272_b200 import Backend, MmConfig
 
@@ -74,11 +75,32 @@ def test_nnmf_scalar_updates_and_fixed_point():
     x = np.array([[2.0]])
     assert M.nnmf_update_v(x, np.array([[1.0]]), np.array([[1.0]]))[0, 0] == 2.0
     assert M.nnmf_update_w(x, np.array([[2.0]]), np.array([[1.0]]))[0, 0] == 1.0
+    # the reference's bitwise fixed point (test_nnmf.py:46-52): X = VW from its
+    # own tree-summed matmul (the oracle's, bitwise the reference's); the fp64
+    # single ops run in the reference's arithmetic order (csrc/nnmf_ref.cu)
     rng = np.random.default_rng(1)
     v, w = rng.random((6, 3)), rng.random((3, 5))
-    x = v @ w
-    assert np.max(np.abs(M.nnmf_update_v(x, v, w) - v) / v) <= 1e-14
-    assert np.max(np.abs(M.nnmf_update_w(x, v, w) - w) / w) <= 1e-14
+    x = O.matmul(v, w)
+    assert np.array_equal(M.nnmf_update_v(x, v, w), v)
+    assert np.array_equal(M.nnmf_update_w(x, v, w), w)
+
+
+@pytest.mark.parametrize("m,n,r", [(6, 5, 3), (37, 29, 7), (130, 257, 64), (64, 2049, 5),
+                                   (1, 1, 1), (513, 3, 17)])
+def test_nnmf_fp64_single_ops_bitwise_reference(m, n, r):
+    """fp64 nnmf_objective / update_v / update_w / gradient equal the
+    reference's arithmetic bit for bit (the oracle is bitwise pinned to it):
+    tree-summed inner products, explicitly rounded elementwise ops, and the
+    halving-with-carry reduction of the objective over m n terms (the odd
+    sizes exercise the carried tails)."""
+    rng = np.random.default_rng(m * 1000 + n + r)
+    x, v, w = rng.random((m, n)) * 3.0, rng.random((m, r)), rng.random((r, n))
+    assert M.nnmf_objective(x, v, w) == O.nnmf_objective(x, v, w)
+    assert np.array_equal(M.nnmf_update_v(x, v, w), O.nnmf_update_v(x, v, w))
+    assert np.array_equal(M.nnmf_update_w(x, v, w), O.nnmf_update_w(x, v, w))
+    gv, gw = M.nnmf_gradient(x, v, w)
+    ov, ow = O.nnmf_gradient(x, v, w)
+    assert np.array_equal(gv, ov) and np.array_equal(gw, ow)
 
 
 def test_nnmf_zero_entries_absorb_and_domain():
