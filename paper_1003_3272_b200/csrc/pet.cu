@@ -1,5 +1,6 @@
 // pet.cu -- penalized Poisson MM for emission tomography (reference
-// pet.py:288-417), as a single pass over the system matrix E.
+// pet.py:288-417): forward projection, back-projection and the pixel update
+// of one MM iteration (dense E here; CSR / CSC E below).
 //
 // Phase A1 (pet_fwd_kernel): one warp per ray forms the forward projection
 // m_i = E_i . lam (vectorised row loads, fp64 accumulation), the count ratio
@@ -7,9 +8,12 @@
 // Phase A2 (pet_back_kernel): the back-projection b_j = sum_i e_ij r_i with a
 // thread per pixel over coalesced rows of E, split over ray ranges; the last
 // split block of each column block adds the split partials in order
-// (deterministic) into red = [b | loglik].  E is read twice per iteration; at
-// the paper shape (33 MB fp32) both reads are L2 hits.  A multi-GPU caller
-// all-reduces red across ray shards.
+// (deterministic) into red = [b | loglik].  E is read twice per iteration
+// (a single pass would need each CTA's full rows of E staged until their
+// ratios exist, then a cross-CTA reduction of per-CTA b partials); at the
+// paper shape (33 MB fp32) both reads are L2 hits, and the paper-shape runs
+// take the persistent engine below, which is latency-, not bandwidth-bound.
+// A multi-GPU caller all-reduces red across ray shards.
 //
 // Phase B (pet_pixel_kernel): per pixel c_j = lam_j b_j, neighbour sums over
 // the CSR lattice (pet.py:204-210), EM floor or positive-root update
