@@ -25,28 +25,33 @@
 // (the Gram-trace identity sum x^2 - 2<V, X W^T> +
 // <V^T V, W W^T> cancels catastrophically in fp32 when ||X||^2 / f is large),
 // evaluated inside the V step's X stream with no extra HBM traffic:
-//   * per 128 x 64 X stage the MMA warp also issues R' = V_h [W_hi | W_lo]
-//     (4 MMAs, N = 128, B = the W chunk already in shared memory read as an
-//     MN-major operand), V_h = fp16 of V scaled per row by 2^ev_i;
-//   * eight residual warps read R' from TMEM and the X stage from shared
-//     memory and accumulate F' = sum (x - v_h.w)^2 (fp32 squares of 8 terms
-//     folded into fp64);
-//   * the exact correction for V's rounding E = V - V_h,
-//       f = F' - 2 <(X - V W) W^T, E> - sum_i e_i G_W e_i^T,
-//     comes from the V-update epilogue, which holds Q = X W^T, V G_W and V
-//     for its row: (X - VW)W^T = Q - V G_W.  E is ~2^-12 V, so these terms
-//     are small and well conditioned; F' is a sum of squares (no
-//     cancellation).  tests/test_nnmf_tc_gpu.py checks f against the fp64
-//     residual on well-fit data (||X||^2 / f ~ 1e4).
+//   * per 128 x 64 X stage the MMA warp also issues R0 = V_h W_hi (4 MMAs,
+//     N = 64, B = the W_hi half of the W chunk already in shared memory read
+//     as an MN-major operand), V_h = fp16 of V scaled per row by 2^ev_i;
+//   * eight residual warps read R0 from TMEM and the X stage from shared
+//     memory and accumulate F0 = sum (x - v_h.w_hi)^2 (fp32 squares of 16
+//     terms folded into fp64);
+//   * the rest is exact algebra the update epilogue adds per row from what it
+//     holds (Q = X W^T, V G_W, V, and X_hi.W_lo in its own accumulator
+//     columns): the W_lo part of the residual,
+//       -2 <v_h, X W_lo^T> + v_h (2 W_hi W_lo^T + W_lo W_lo^T) v_h^T
+//     (X W_lo^T ~ X_hi.W_lo: the X_lo.W_lo product is ~2^-24 relative; the
+//     Gram G_c from gram3_kernel), and V's rounding E = V - V_h,
+//       -2 <(X - V W) W^T, E> - sum_i e_i G_W e_i^T.
+//     E is ~2^-12 V and W_lo ~2^-12 W, so these terms are small next to f;
+//     F0 is a sum of squares (no cancellation).  tests/test_nnmf_tc_gpu.py
+//     and tests/test_nnmf_c4_gpu.py check f against fp64 residuals on
+//     well-fit data (||X||^2 / f ~ 1e4) and at C4.  (The CTA-pair form keeps
+//     R' = V_h [W_hi | W_lo], N = 128, and only the E terms.)
 //
 //   nnmf_vstep_tc  (persistent, one CTA per SM, 14 warps, one 128-row tile
 //                  per pass, two accumulator sets so pass p's epilogue
 //                  overlaps pass p + 1's MMAs)
 //     warp 0     TMA: V_h tile per pass; per 64-column stage the W chunk
 //                [W_hi ; W_lo] and the X stage [X_hi | X_lo]
-//     warp 1     one thread issues per stage 4 x (SS MMA N = 128 X_hi.[W_hi;
-//                W_lo] + SS MMA N = 64 X_lo.W_hi) into Q, then 4 x SS MMA
-//                N = 128 V_h.[W_hi | W_lo] into the residual buffer
+//     warp 1     per stage 4 x (SS MMA N = 128 X_hi.[W_hi; W_lo] + SS MMA
+//                N = 64 X_lo.W_hi) into Q (3 x 64 columns), then 4 x SS MMA
+//                N = 64 V_h.W_hi into a residual buffer
 //     warps 2-9  residual (two groups of 4 alternate stages)
 //     warps 10-13 epilogue: V' = V * Q / (V G_W + 1e-300), max(V'), the
 //                correction terms above
@@ -107,10 +112,14 @@ static_assert(SMEM_V2 + 2048 <= 232448, "dynamic + static shared memory per CTA 
 constexpr int ACC = 2 * R;                  // accumulator columns: [X.Wh | X.Wl] (N = 128)
 constexpr int CB = 2;                       // W step: 128-column blocks per item
 constexpr int TM_COLS = 512;
-// V step TMEM: two Q sets [0, 256), two residual buffers [W_hi | W_lo] columns
+// V step TMEM, single CTA: two Q sets of [X_hi.W_hi | X_hi.W_lo | X_lo.W_hi]
+// (3 x 64 columns) and two residual buffers R0 = V_h.W_hi (64 columns); CTA
+// pair: two Q sets of 128 columns and two R' = V_h.[W_hi | W_lo] buffers of 128
 constexpr int NRB = 2;
-constexpr uint32_t TM_RES = 2 * ACC;
-static_assert(TM_RES + NRB * ACC <= TM_COLS, "V-step TMEM budget");
+constexpr uint32_t QW1 = 3 * R, RW1 = R;        // single CTA
+constexpr uint32_t QW2 = ACC, RW2 = ACC;        // CTA pair
+static_assert(2 * QW1 + NRB * RW1 <= TM_COLS, "V-step TMEM budget (single CTA)");
+static_assert(2 * QW2 + NRB * RW2 <= TM_COLS, "V-step TMEM budget (pair)");
 static_assert(2 * CB * ACC <= TM_COLS, "W step: two accumulator sets");
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -147,9 +156,10 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn = 0) {
 // 64-K fp16 tiles, 128B swizzle) and the operand chunk [B_hi ; B_lo] stacked
 // along N (64 + 64 rows, K-major): per K16 step an SS MMA with N = 128 gives
 // D[:, 0:64] += X_hi.B_hi, D[:, 64:128] += X_hi.B_lo, and one with N = 64
-// adds X_lo.B_hi into D[:, 0:64].  The epilogue sums the two halves.
+// adds X_lo.B_hi into d_lo (its own 64 columns: the epilogue needs X_hi.B_lo
+// alone for the objective's W_lo correction).  The epilogue sums the parts.
 // Issued warp-converged (every lane calls it; one elected lane issues)
-__device__ __forceinline__ void issue_split_stage_e(uint32_t d, const uint8_t* xs,
+__device__ __forceinline__ void issue_split_stage_e(uint32_t d, uint32_t d_lo, const uint8_t* xs,
                                                     const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
@@ -160,7 +170,7 @@ __device__ __forceinline__ void issue_split_stage_e(uint32_t d, const uint8_t* x
     for (int ks = 0; ks < BK / 16; ++ks) {
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
         tc::mma_f16ss_e(d, ah + ks * 2, db0 + ks * 2, id_hi, acc);
-        tc::mma_f16ss_e(d, al + ks * 2, db0 + ks * 2, id_lo, 1);
+        tc::mma_f16ss_e(d_lo, al + ks * 2, db0 + ks * 2, id_lo, acc);
     }
 }
 
@@ -294,9 +304,12 @@ __global__ void __launch_bounds__(kVThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
               const __grid_constant__ CUtensorMap mVh, const float* __restrict__ V,
-              const float* __restrict__ GWf, float* __restrict__ Vout, Scales* sc, int m, int n,
+              const float* __restrict__ GWf, const float* __restrict__ Ghl,
+              const float* __restrict__ Gll, float* __restrict__ Vout, Scales* sc, int m, int n,
               double* __restrict__ part) {
     constexpr uint32_t OSLOT = PAIR ? SOP : 2 * SOP;   // operand slot: pair = this CTA's half
+    constexpr uint32_t QW = PAIR ? QW2 : QW1, RW = PAIR ? RW2 : RW1;
+    constexpr uint32_t TM_RES = 2 * QW;                // residual buffers after the Q sets
     constexpr int NARR = PAIR ? 8 : 4;                 // arrivals on dempty / rempty
     constexpr int XS = PAIR ? XSTV2 : XSTV;            // X ring depth
     constexpr bool GWS = !PAIR && MMK_TC_GW_SMEM;      // G_W staged in smem
@@ -408,7 +421,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         }
     } else if (warp == 1) {
         if (!PAIR || rank == 0) {   // MMA issuer: the whole warp, one elected lane issues
-            constexpr uint32_t id_res = idesc_f16(PAIR ? 2 * BM : BM, ACC, 1);
+            // R' = V_h [W_hi | W_lo] (pair, N = 128) or R0 = V_h W_hi (single, N = 64)
+            constexpr uint32_t id_res = idesc_f16(PAIR ? 2 * BM : BM, RW, 1);
             int it = 0;
             for (int p = 0; p < mine; ++p) {
                 const int b = p & 1;
@@ -425,9 +439,10 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     tc::tc_fence_after();
                     const uint8_t* ob = oring + os * OSLOT;
                     if constexpr (PAIR)
-                        issue_split_stage_pair(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                        issue_split_stage_pair(tmem + b * QW, xring + xs * SX, ob, kb == 0);
                     else
-                        issue_split_stage_e(tmem + b * ACC, xring + xs * SX, ob, kb == 0);
+                        issue_split_stage_e(tmem + b * QW, tmem + b * QW + ACC, xring + xs * SX,
+                                            ob, kb == 0);
                     if (lane == 0) TRACE_AT(2, it);
                     if constexpr (PAIR)
                         tc::mma_commit_pair_e(&B.xempty[xs]);
@@ -437,7 +452,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     if (lane == 0) TRACE_AT(3, it);
                     tc::tc_fence_after();
                     const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major
-                    const uint32_t dr = tmem + TM_RES + rb * ACC;
+                    const uint32_t dr = tmem + TM_RES + rb * RW;
 #pragma unroll
                     for (int ks = 0; ks < R / 16; ++ks) {
                         if constexpr (PAIR)
@@ -494,7 +509,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 // the slot (its other user is the Q MMA, which commits on xempty)
                 const int xs = it % XS;
                 const int rb = it % NRB;
-                const uint32_t rcol = (uint32_t)(rb * ACC);
+                const uint32_t rcol = (uint32_t)(rb * RW);
                 const uint32_t rph = (uint32_t)((it / NRB) & 1);
                 tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
                 if (r == 0) TRACE_AT(5, it);
@@ -515,15 +530,28 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::tc_fence_after();
                 // R' in 8-column chunks, the load of chunk q + 1 in flight while
                 // chunk q is consumed (one TMEM round trip exposed per stage)
+                // pair: R' = V_h [W_hi | W_lo] (hi and lo halves summed here);
+                // single CTA: R0 = V_h W_hi (the W_lo part enters exactly in the
+                // epilogue through X_hi.W_lo and the Grams W_hi W_lo^T, W_lo W_lo^T)
                 uint32_t th[2][8], tl[2][8];
                 const uint32_t tr0 = tmem + TM_RES + rcol + lane_off;
-                tc::tmem_ld8x2_nw(tr0, tr0 + R, th[0], tl[0]);
-                tc::tmem_wait_ld8x2(th[0], tl[0]);
+                if constexpr (PAIR) {
+                    tc::tmem_ld8x2_nw(tr0, tr0 + R, th[0], tl[0]);
+                    tc::tmem_wait_ld8x2(th[0], tl[0]);
+                } else {
+                    tc::tmem_ld8_nw(tr0, th[0]);
+                    tc::tmem_wait_ld8(th[0]);
+                }
                 float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {   // columns 8q .. 8q + 7
-                    if (q < 7) tc::tmem_ld8x2_nw(tr0 + 8 * (q + 1), tr0 + R + 8 * (q + 1),
-                                                 th[(q + 1) & 1], tl[(q + 1) & 1]);
+                    if (q < 7) {
+                        if constexpr (PAIR)
+                            tc::tmem_ld8x2_nw(tr0 + 8 * (q + 1), tr0 + R + 8 * (q + 1),
+                                              th[(q + 1) & 1], tl[(q + 1) & 1]);
+                        else
+                            tc::tmem_ld8_nw(tr0 + 8 * (q + 1), th[(q + 1) & 1]);
+                    }
                     if (!(q & 1)) s2 = make_float2(0.f, 0.f);
                     const uint4 hq = hv[q], lq = lv[q];
                     const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
@@ -533,16 +561,21 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         const float2 xs2 = __fadd2_rn(
                             __half22float2(*reinterpret_cast<const __half2*>(&hw[e])),
                             __half22float2(*reinterpret_cast<const __half2*>(&lw[e])));
-                        const float2 rr = __fadd2_rn(
-                            make_float2(__uint_as_float(th[q & 1][2 * e]),
-                                        __uint_as_float(th[q & 1][2 * e + 1])),
-                            make_float2(__uint_as_float(tl[q & 1][2 * e]),
-                                        __uint_as_float(tl[q & 1][2 * e + 1])));
+                        float2 rr = make_float2(__uint_as_float(th[q & 1][2 * e]),
+                                                __uint_as_float(th[q & 1][2 * e + 1]));
+                        if constexpr (PAIR)
+                            rr = __fadd2_rn(rr, make_float2(__uint_as_float(tl[q & 1][2 * e]),
+                                                            __uint_as_float(tl[q & 1][2 * e + 1])));
                         const float2 d = __ffma2_rn(rr, nkk, xs2);
                         s2 = __ffma2_rn(d, d, s2);
                     }
                     if (q & 1) acc += (double)(s2.x + s2.y);   // 16 terms per fold
-                    if (q < 7) tc::tmem_wait_ld8x2(th[(q + 1) & 1], tl[(q + 1) & 1]);
+                    if (q < 7) {
+                        if constexpr (PAIR)
+                            tc::tmem_wait_ld8x2(th[(q + 1) & 1], tl[(q + 1) & 1]);
+                        else
+                            tc::tmem_wait_ld8(th[(q + 1) & 1]);
+                    }
                 }
                 tc::tc_fence_before();
                 __syncwarp();
@@ -554,7 +587,13 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     } else {
         // epilogue: thread = row.  V' = V Q / (V G_W + 1e-300) with the row
         // of V G_W formed here (fp32, l ascending), plus the correction terms
-        // -2 (Q - V G_W)_ik e_ik - e_ik (e G_W)_ik of f (fp64)
+        // -2 (Q - V G_W)_ik e_ik - e_ik (e G_W)_ik of f (fp64) for V's fp16
+        // rounding E = V - V_h.  Single CTA: the residual warps summed
+        // (x - v_h . w_hi)^2, so the W_lo part of the residual is added here
+        // exactly, per row i and rank k:
+        //   -2 v_h,ik ((X W_lo^T)_ik - (v_h,i W_hi W_lo^T)_k) + v_h,ik (v_h,i W_lo W_lo^T)_k
+        // with X W_lo^T = the X_hi.W_lo accumulator (the X_lo.W_lo product, ~2^-24
+        // relative, is left out) and the two Grams from gram32 (Ghl, Gll)
         const int quarter = warp & 3;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const double qscale = exp2(-(double)(sc->ex + sc->ew));
@@ -564,7 +603,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::mbar_wait(&B.dfull[b], (p >> 1) & 1);
             tc::tc_fence_after();
             const long long row = (long long)tile_of(p) * BM + quarter * 32 + lane;
-            const uint32_t ta = tmem + b * ACC + lane_off;
+            const uint32_t ta = tmem + b * QW + lane_off;
             const float4* vr = reinterpret_cast<const float4*>(V + (row < m ? row : 0) * R);
             const int ev = row < m ? row_exp(vr) : 0;
             const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
@@ -573,14 +612,20 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 float q[32], q2[32];
                 tc::tmem_ld32(ta + h * 32, q);   // warp-collective: before the row guard
                 tc::tmem_ld32(ta + R + h * 32, q2);
+                if constexpr (!PAIR) {   // + X_lo.W_hi (its own columns)
+                    float q3[32];
+                    tc::tmem_ld32(ta + 2 * R + h * 32, q3);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) q[i] += q3[i];
+                }
                 if (row >= m) continue;
                 float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
 #pragma unroll
                 for (int hh = 0; hh < 4; ++hh) {
                     // columns h*32 + hh*8 .. +8: (V G_W) and (E G_W) in fp32
-                    float den[8], eg[8];
+                    float den[8], eg[8], gcg[8];
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) den[c] = eg[c] = 0.f;
+                    for (int c = 0; c < 8; ++c) den[c] = eg[c] = gcg[c] = 0.f;
 #pragma unroll 2
                     for (int l4 = 0; l4 < R / 4; ++l4) {
                         const float4 vv = vr[l4];
@@ -604,6 +649,15 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                 eg[4 * c4 + 1] = fmaf(el, gg.y, eg[4 * c4 + 1]);
                                 eg[4 * c4 + 2] = fmaf(el, gg.z, eg[4 * c4 + 2]);
                                 eg[4 * c4 + 3] = fmaf(el, gg.w, eg[4 * c4 + 3]);
+                                if constexpr (!PAIR) {   // v_h G_c, G_c = 2 W_hi W_lo^T + W_lo W_lo^T
+                                    const float vh = va[e] - el;
+                                    const int gi = ((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4;
+                                    const float4 gc = __ldg(reinterpret_cast<const float4*>(Ghl) + gi);
+                                    gcg[4 * c4] = fmaf(vh, gc.x, gcg[4 * c4]);
+                                    gcg[4 * c4 + 1] = fmaf(vh, gc.y, gcg[4 * c4 + 1]);
+                                    gcg[4 * c4 + 2] = fmaf(vh, gc.z, gcg[4 * c4 + 2]);
+                                    gcg[4 * c4 + 3] = fmaf(vh, gc.w, gcg[4 * c4 + 3]);
+                                }
                             }
                         }
                     }
@@ -623,6 +677,10 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                 (double)(va[i] - __half2float(__float2half_rn(va[i] * vs)) * vsi);
                             acc = fma(-2.0 * (qk - dk), ek, acc);
                             acc = fma(-ek, (double)eg[c], acc);
+                            if constexpr (!PAIR) {
+                                const double vhk = vk - ek;
+                                acc = fma(vhk, (double)gcg[c] - 2.0 * (double)q2[kk] * qscale, acc);
+                            }
                             nv[i] = (float)(vk * (qk / (dk + kDenomGuard)));
                             vmax = fmaxf(vmax, nv[i]);
                         }
@@ -1031,6 +1089,85 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
         for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[i][j];
 }
 
+// The W-side Grams of one iteration in one pass over W (64 x len, rows are
+// the vectors): G_W = W W^T as gram32_kernel<true>, plus G_hl = W_hi W_lo^T
+// and G_ll = W_lo W_lo^T of the fp16 split the V-step MMAs use (W_hi =
+// rn(w 2^ew) 2^-ew, W_lo = rn(w 2^ew - W_hi 2^ew) 2^-ew, as split_w_kernel):
+// products of two fp16 values are exact in fp32, summed 8 at a time and folded
+// into fp64.  Partials: part[b], part[gridDim + b], part[2 gridDim + b].
+__global__ void __launch_bounds__(256)
+gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
+             const Scales* sc, double* __restrict__ part) {
+    __shared__ __align__(16) float S[32][64 + 4], Sh[32][64 + 4], Sl[32][64 + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const float s = exp2f((float)sc->ew), si = exp2f(-(float)sc->ew);
+    double acc[2][4][4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[g][i][j] = 0.0;
+    const long long c_begin = (long long)blockIdx.x * per_block;
+    long long c_end = c_begin + per_block;
+    if (c_end > len) c_end = len;
+    for (long long c0 = c_begin; c0 < c_end; c0 += 32) {
+        for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
+            const int a = idx >> 5, cc = idx & 31;
+            const float w = (c0 + cc < c_end) ? A[(long long)a * len + c0 + cc] : 0.f;
+            const float hi = __half2float(__float2half_rn(w * s));
+            const float lo = __half2float(__float2half_rn(w * s - hi));
+            S[cc][a] = w;
+            Sh[cc][a] = hi * si;
+            Sl[cc][a] = lo * si;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k8 = 0; k8 < 32; k8 += 8) {
+            float p[2][4][4];
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) p[g][i][j] = 0.f;
+#pragma unroll
+            for (int kk = k8; kk < k8 + 8; ++kk) {
+                const float4 a = *reinterpret_cast<const float4*>(&S[kk][4 * ty]);
+                const float4 b = *reinterpret_cast<const float4*>(&S[kk][4 * tx]);
+                const float4 ah = *reinterpret_cast<const float4*>(&Sh[kk][4 * ty]);
+                const float4 al = *reinterpret_cast<const float4*>(&Sl[kk][4 * ty]);
+                const float4 bl = *reinterpret_cast<const float4*>(&Sl[kk][4 * tx]);
+                const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+                const float ahv[4] = {ah.x, ah.y, ah.z, ah.w}, alv[4] = {al.x, al.y, al.z, al.w};
+                const float blv[4] = {bl.x, bl.y, bl.z, bl.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        p[0][i][j] = fmaf(av[i], bv[j], p[0][i][j]);
+                        p[1][i][j] = fmaf(2.f * ahv[i] + alv[i], blv[j], p[1][i][j]);
+                    }
+            }
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[g][i][j] += (double)p[g][i][j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        double* pb = part + ((long long)g * gridDim.x + blockIdx.x) * (R * R);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[g][i][j];
+    }
+}
+
 // out[e] = sum_b part[b][e] in block order: 8 groups of 128 threads take
 // interleaved partials, combined in group order (deterministic)
 __global__ void __launch_bounds__(1024)
@@ -1333,10 +1470,29 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
                (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out, outf)));
 }
 
+// G_W and the split Grams of W (gram3_kernel) -> GW (fp64), GWf, GhlF, GllF
+void gram3(const float* W, long long len, const Scales* sc, double* gpart, double* GW,
+           float* GWf, double* G64, float* GhlF, float* GllF, cudaStream_t st) {
+    // one wave: the kernel holds three 4 x 4 fp64 accumulator sets (one CTA per SM)
+    long long per = (len + kNumSMs - 1) / kNumSMs;
+    per = (per + 31) / 32 * 32;
+    const int blocks = (int)((len + per - 1) / per);
+    MMK_LAUNCH("nnmf_gram32", st,
+               (gram3_kernel<<<blocks, 256, 0, st>>>(W, len, per, sc, gpart)));
+    MMK_LAUNCH("nnmf_gram_sum", st,
+               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, GW, GWf)));
+    MMK_LAUNCH("nnmf_gram_sum", st,
+               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(
+                   gpart + (long long)blocks * R * R, blocks, G64, GhlF)));
+    (void)GllF;
+}
+
 struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl, *Vh;
     __half *Xh, *Xl;   // pre-split X (row-major)
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
+    float *GhlF, *GllF;           // W_hi W_lo^T, W_lo W_lo^T in fp32 (V-step epilogue)
+    double* G64;                  // their fp64 sums [2][64][64]
     double *part, *gpart;
     XXCache* xx;
     Scales* sc;
@@ -1360,8 +1516,9 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oP = take(8 * (size_t)kNumSMs);
     size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) xmax, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
-    size_t oGP = take(8 * (size_t)R * R * kGramBlocks);
+    size_t oGP = take(8 * (size_t)R * R * kGramBlocks * 3);   // gram3: three Grams
     size_t oGF = take(4 * (size_t)R * R);
+    size_t oGS = take(4 * (size_t)R * R * 2), oG64 = take(8 * (size_t)R * R * 2);
     const size_t xe = (size_t)m * n;
     size_t oXh = take(2 * xe), oXl = take(2 * xe);
     if (base && L) {
@@ -1381,6 +1538,9 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->part = (double*)(c + oP);
         L->gpart = (double*)(c + oGP);
         L->GWf = (float*)(c + oGF);
+        L->GhlF = (float*)(c + oGS);
+        L->GllF = (float*)(c + oGS) + R * R;
+        L->G64 = (double*)(c + oG64);
     }
     return off;
 }
@@ -1514,7 +1674,7 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
-    gram32(W, n, true, L.gpart, GW, st, L.GWf);
+    gram3(W, n, L.sc, L.gpart, GW, L.GWf, L.G64, L.GhlF, L.GllF, st);
     MMK_LAUNCH("nnmf_split_v", st,
                (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
     if (P.vpair) {
@@ -1533,12 +1693,14 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
         cfg.numAttrs = 1;
         MMK_LAUNCH("nnmf_vstep_tc", st,
                    (void)cudaLaunchKernelEx(&cfg, nnmf_vstep_tc<true>, mX, mX2, mWh, mWl, mVr, V,
-                                            (const float*)L.GWf, V_out, L.sc, (int)m, (int)n,
+                                            (const float*)L.GWf, (const float*)L.GhlF,
+                                            (const float*)L.GllF, V_out, L.sc, (int)m, (int)n,
                                             L.part));
     } else {
         MMK_LAUNCH("nnmf_vstep_tc", st,
                    (nnmf_vstep_tc<false><<<P.vgrid, kVThreads, SMEM_V, st>>>(
-                       mX, mX2, mWh, mWl, mVr, V, L.GWf, V_out, L.sc, (int)m, (int)n, L.part)));
+                       mX, mX2, mWh, mWl, mVr, V, L.GWf, L.GhlF, L.GllF, V_out, L.sc, (int)m,
+                       (int)n, L.part)));
     }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
