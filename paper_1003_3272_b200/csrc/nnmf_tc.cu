@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(kVThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
               const __grid_constant__ CUtensorMap mVh, const float* __restrict__ V,
-              const float* __restrict__ GWf, const float* __restrict__ Ghl,
-              const float* __restrict__ Gll, float* __restrict__ Vout, Scales* sc, int m, int n,
+              const float* __restrict__ GWf, const float* __restrict__ Gc,
+              float* __restrict__ Vout, Scales* sc, int m, int n,
               double* __restrict__ part) {
     constexpr uint32_t OSLOT = PAIR ? SOP : 2 * SOP;   // operand slot: pair = this CTA's half
     constexpr uint32_t QW = PAIR ? QW2 : QW1, RW = PAIR ? RW2 : RW1;
@@ -591,9 +591,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         // rounding E = V - V_h.  Single CTA: the residual warps summed
         // (x - v_h . w_hi)^2, so the W_lo part of the residual is added here
         // exactly, per row i and rank k:
-        //   -2 v_h,ik ((X W_lo^T)_ik - (v_h,i W_hi W_lo^T)_k) + v_h,ik (v_h,i W_lo W_lo^T)_k
+        //   v_h,ik ((v_h,i G_c)_k - 2 (X W_lo^T)_ik),  G_c = 2 W_hi W_lo^T + W_lo W_lo^T
         // with X W_lo^T = the X_hi.W_lo accumulator (the X_lo.W_lo product, ~2^-24
-        // relative, is left out) and the two Grams from gram32 (Ghl, Gll)
+        // relative, is left out) and G_c from gram3_kernel
         const int quarter = warp & 3;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const double qscale = exp2(-(double)(sc->ex + sc->ew));
@@ -652,7 +652,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                 if constexpr (!PAIR) {   // v_h G_c, G_c = 2 W_hi W_lo^T + W_lo W_lo^T
                                     const float vh = va[e] - el;
                                     const int gi = ((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4;
-                                    const float4 gc = __ldg(reinterpret_cast<const float4*>(Ghl) + gi);
+                                    const float4 gc = __ldg(reinterpret_cast<const float4*>(Gc) + gi);
                                     gcg[4 * c4] = fmaf(vh, gc.x, gcg[4 * c4]);
                                     gcg[4 * c4 + 1] = fmaf(vh, gc.y, gcg[4 * c4 + 1]);
                                     gcg[4 * c4 + 2] = fmaf(vh, gc.z, gcg[4 * c4 + 2]);
@@ -1090,11 +1090,12 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
 }
 
 // The W-side Grams of one iteration in one pass over W (64 x len, rows are
-// the vectors): G_W = W W^T as gram32_kernel<true>, plus G_hl = W_hi W_lo^T
-// and G_ll = W_lo W_lo^T of the fp16 split the V-step MMAs use (W_hi =
-// rn(w 2^ew) 2^-ew, W_lo = rn(w 2^ew - W_hi 2^ew) 2^-ew, as split_w_kernel):
-// products of two fp16 values are exact in fp32, summed 8 at a time and folded
-// into fp64.  Partials: part[b], part[gridDim + b], part[2 gridDim + b].
+// the vectors): G_W = W W^T as gram32_kernel<true>, plus G_c = (2 W_hi +
+// W_lo) W_lo^T = 2 W_hi W_lo^T + W_lo W_lo^T of the fp16 split the V-step MMAs
+// use (W_hi = rn(w 2^ew) 2^-ew, W_lo = rn(w 2^ew - W_hi 2^ew) 2^-ew, as
+// split_w_kernel), the Gram of the objective's W_lo correction.  fp32
+// products summed 8 at a time and folded into fp64.  Partials: part[b],
+// part[gridDim + b].
 __global__ void __launch_bounds__(256)
 gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
              const Scales* sc, double* __restrict__ part) {
@@ -1470,9 +1471,9 @@ void gram32(const float* A, long long len, bool vec_rows, double* gpart, double*
                (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out, outf)));
 }
 
-// G_W and the split Grams of W (gram3_kernel) -> GW (fp64), GWf, GhlF, GllF
+// G_W and G_c = 2 W_hi W_lo^T + W_lo W_lo^T (gram3_kernel) -> GW (fp64), GWf, GcF
 void gram3(const float* W, long long len, const Scales* sc, double* gpart, double* GW,
-           float* GWf, double* G64, float* GhlF, float* GllF, cudaStream_t st) {
+           float* GWf, double* G64, float* GcF, cudaStream_t st) {
     // one wave: the kernel holds three 4 x 4 fp64 accumulator sets (one CTA per SM)
     long long per = (len + kNumSMs - 1) / kNumSMs;
     per = (per + 31) / 32 * 32;
@@ -1483,16 +1484,15 @@ void gram3(const float* W, long long len, const Scales* sc, double* gpart, doubl
                (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, GW, GWf)));
     MMK_LAUNCH("nnmf_gram_sum", st,
                (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(
-                   gpart + (long long)blocks * R * R, blocks, G64, GhlF)));
-    (void)GllF;
+                   gpart + (long long)blocks * R * R, blocks, G64, GcF)));
 }
 
 struct TcWs {
     __half *Wh, *Wl, *Vth, *Vtl, *Vh;
     __half *Xh, *Xl;   // pre-split X (row-major)
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
-    float *GhlF, *GllF;           // W_hi W_lo^T, W_lo W_lo^T in fp32 (V-step epilogue)
-    double* G64;                  // their fp64 sums [2][64][64]
+    float* GcF;                   // G_c = 2 W_hi W_lo^T + W_lo W_lo^T in fp32 (V-step epilogue)
+    double* G64;                  // its fp64 sum
     double *part, *gpart;
     XXCache* xx;
     Scales* sc;
@@ -1516,9 +1516,9 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
     size_t oP = take(8 * (size_t)kNumSMs);
     size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) xmax, then wmax
     size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
-    size_t oGP = take(8 * (size_t)R * R * kGramBlocks * 3);   // gram3: three Grams
+    size_t oGP = take(8 * (size_t)R * R * kGramBlocks * 2);   // gram3: two Grams
     size_t oGF = take(4 * (size_t)R * R);
-    size_t oGS = take(4 * (size_t)R * R * 2), oG64 = take(8 * (size_t)R * R * 2);
+    size_t oGS = take(4 * (size_t)R * R), oG64 = take(8 * (size_t)R * R);
     const size_t xe = (size_t)m * n;
     size_t oXh = take(2 * xe), oXl = take(2 * xe);
     if (base && L) {
@@ -1538,8 +1538,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->part = (double*)(c + oP);
         L->gpart = (double*)(c + oGP);
         L->GWf = (float*)(c + oGF);
-        L->GhlF = (float*)(c + oGS);
-        L->GllF = (float*)(c + oGS) + R * R;
+        L->GcF = (float*)(c + oGS);
         L->G64 = (double*)(c + oG64);
     }
     return off;
@@ -1674,7 +1673,7 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
-    gram3(W, n, L.sc, L.gpart, GW, L.GWf, L.G64, L.GhlF, L.GllF, st);
+    gram3(W, n, L.sc, L.gpart, GW, L.GWf, L.G64, L.GcF, st);
     MMK_LAUNCH("nnmf_split_v", st,
                (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
     if (P.vpair) {
@@ -1693,14 +1692,13 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
         cfg.numAttrs = 1;
         MMK_LAUNCH("nnmf_vstep_tc", st,
                    (void)cudaLaunchKernelEx(&cfg, nnmf_vstep_tc<true>, mX, mX2, mWh, mWl, mVr, V,
-                                            (const float*)L.GWf, (const float*)L.GhlF,
-                                            (const float*)L.GllF, V_out, L.sc, (int)m, (int)n,
-                                            L.part));
+                                            (const float*)L.GWf, (const float*)L.GcF, V_out,
+                                            L.sc, (int)m, (int)n, L.part));
     } else {
         MMK_LAUNCH("nnmf_vstep_tc", st,
                    (nnmf_vstep_tc<false><<<P.vgrid, kVThreads, SMEM_V, st>>>(
-                       mX, mX2, mWh, mWl, mVr, V, L.GWf, L.GhlF, L.GllF, V_out, L.sc, (int)m,
-                       (int)n, L.part)));
+                       mX, mX2, mWh, mWl, mVr, V, L.GWf, L.GcF, V_out, L.sc, (int)m, (int)n,
+                       L.part)));
     }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
     MMK_LAUNCH("nnmf_objective_tc", st,
