@@ -362,10 +362,23 @@ def bench_nnmf_large(args, torch, world, rank, dev):
                for k, (c, ms) in prof.items()}
     return timing, roof, launches, e2e, {
         "kernels": kernels, "kernel_loop_ms_per_step": loop["ms_total"] / args.steps,
-        "value_path": ("nnmf_run_sharded (device-loop engine, NCCL all-reduce in its graph)"
-                       if world > 1 else "nnmf_run (device-loop engine)") +
+        "value_path": sharded_path("nnmf", world) +
                       " on X resident in HBM; one timed run of `steps` iterations after a "
                       "`warmup`-iteration run"}
+
+
+def sharded_path(name, world):
+    """How the timed run is driven: the in-graph NCCL all-reduce when every
+    rank has its own device, else (ranks sharing a device, gloo) run_mm's
+    per-iteration protocol with a host all-reduce per iteration -- that line
+    measures the protocol on one GPU, not the scaling."""
+    import torch.distributed as dist
+    if world == 1:
+        return f"{name}_run (device-loop engine)"
+    if dist.get_backend() == "nccl":
+        return f"{name}_run_sharded (device-loop engine, NCCL all-reduce in its graph)"
+    return (f"{name}_run_sharded (per-iteration protocol, gloo all-reduce on the host; "
+            f"{world} ranks share one device)")
 
 
 def nnmf_e2e(args, torch, be, x_dev, v0_dev, w0_dev, r):
@@ -480,8 +493,7 @@ def bench_mds_large(args, torch, world, rank, dev):
                        "-> host theta; second of two runs"}
     return timing, roof, launches, e2e, {
         "kernels": kernels,
-        "value_path": ("mds_run_sharded (device-loop engine, NCCL all-reduce in its graph)"
-                       if world > 1 else "mds_run (device-loop engine)") +
+        "value_path": sharded_path("mds", world) +
                       " on the packed tiles resident in HBM",
         "data": "synthetic (Y_ij = ||z_i - z_j||(1 + 0.05 e_ij), z ~ N(0, I_10), e from a "
                 "symmetric pair hash; theta0 uniform[-1,1]; datasets.distance_rows)"}

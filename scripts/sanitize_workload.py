@@ -3,7 +3,9 @@
 
   nnmf   SIMT (r = 10, fp32 + fp64), tensor cores (r = 64, fp32: pre-split X,
          V step with the residual pipeline, W step, split-K reduction),
-         Poisson, the persistent small engine and the graph engine
+         register-blocked tiles (fp64 r = 40 / 100, fp32 r = 72, Poisson
+         r = 24), fp64 single ops in the reference's order, Poisson, the
+         persistent small engine and the graph engine
   pet    dense and sparse projectors, device Siddon builder, persistent engine
   mds    rows kernel (fp32/fp64, weights), packed-triangle kernel (bulk-copy
          ring), votes -> packed tiles on the tensor cores
@@ -54,6 +56,21 @@ def main(which, paths):
         xp = np.floor(rng.random((120, 90)) * 5)
         for fused in fused_modes:
             M.nnmf_poisson_run(M.NnmfProblem(x=xp, rank=4), cfg, Backend(dtype="fp32", fused=fused))
+        # register-blocked tiles (round 2): fp64 r = 40 and r = 100, fp32 off the
+        # tensor cores (ragged m, n), Poisson r = 24
+        for dt, r in (("fp64", 40), ("fp64", 100), ("fp32", 72)):
+            xr = f32(rng.random((131, 97)))
+            for fused in fused_modes:
+                M.nnmf_run(M.NnmfProblem(x=xr, rank=r), cfg, Backend(dtype=dt, fused=fused),
+                           state0=M.FactorPair(f32(rng.random((131, r))), f32(rng.random((r, 97)))))
+        for fused in fused_modes:
+            M.nnmf_poisson_run(M.NnmfProblem(x=np.floor(rng.random((130, 70)) * 4), rank=24), cfg,
+                               Backend(dtype="fp64", fused=fused))
+        # fp64 single ops in the reference's order (nnmf_ref.cu)
+        vv, ww = rng.random((300, 10)), rng.random((10, 200))
+        M.nnmf_update_v(x, vv, ww, backend=Backend(dtype="fp64"))
+        M.nnmf_update_w(x, vv, ww, backend=Backend(dtype="fp64"))
+        M.nnmf_gradient(x, vv, ww, backend=Backend(dtype="fp64"))
         M.nnmf_update_v(x, f32(rng.random((300, 10))), f32(rng.random((10, 200))),
                         backend=Backend(dtype="fp32"))
         M.nnmf_objective(x, f32(rng.random((300, 10))), f32(rng.random((10, 200))),
