@@ -645,7 +645,7 @@ struct RunA {
         const T* V = (const T*)a.V;
         const T* W = (const T*)a.W;
         const long long rn = (long long)a.r * a.n;
-        if constexpr (std::is_same<T, float>::value && (RMAX == 32 || RMAX == 64)) {
+        if constexpr (std::is_same<T, float>::value && (RMAX == 32 || RMAX == 64 || RMAX == 128)) {
             if (a.mode == 0 && tc_region(MMK_F32, a.m, a.n, a.r, true) &&
                 mmk_tc::eligible(MMK_F32, a.m, a.n, a.r, a.ldx, a.X)) {
                 return mmk_tc::iter_a(X, a.ldx, V, W, (float*)a.V_out, a.m, a.n, a.r, L.tc,

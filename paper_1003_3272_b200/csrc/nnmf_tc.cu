@@ -122,6 +122,33 @@ static_assert(2 * QW1 + NRB * RW1 <= TM_COLS, "V-step TMEM budget (single CTA)")
 static_assert(2 * QW2 + NRB * RW2 <= TM_COLS, "V-step TMEM budget (pair)");
 static_assert(2 * CB * ACC <= TM_COLS, "W step: two accumulator sets");
 
+// Rank tiles of the tensor-core path: RK = 64 (ranks 17..64, the layout
+// above) and RK = 128 (ranks 65..128, zero-padded to 128).  At RK = 128 a
+// single-CTA Q set [hh | hl | lh] is 384 TMEM columns, so the V step keeps ONE
+// Q set (its epilogue copies Q out to a global scratch and releases the set
+// before the V' arithmetic) beside the two 64-column residual buffers, one
+// V_h tile buffer (32 KB) and a 3-deep X ring; the W step takes one 128-column
+// block per item (accumulator [X.V_hi | X.V_lo] = 256 columns, two sets).
+template <int RK>
+struct Tc {
+    static constexpr uint32_t SOP = RK * BK * 2;     // fp16 operand chunk [RK x 64] (hi; lo again)
+    static constexpr uint32_t SVH = BM * RK * 2;     // V_h tile [128 rows x RK ranks]
+    static constexpr int ACC = 2 * RK;               // [X.B_hi | X.B_lo] accumulator columns
+    static constexpr int NQ = RK == 64 ? 2 : 1;      // V step: Q accumulator sets
+    static constexpr int NVB = RK == 64 ? 2 : 1;     // V step: V_h tile buffers
+    static constexpr int XS = RK == 64 ? XSTV : 3;   // V step X ring (single CTA)
+    static constexpr bool GWS = RK == 64 && MMK_TC_GW_SMEM;   // G_W staged in smem
+    static constexpr uint32_t QW = 3 * RK;           // single-CTA Q set [hh | hl | lh]
+    static constexpr uint32_t SMEM_V =
+        XS * SX + OST * 2 * SOP + NVB * SVH + (GWS ? SGW : 0) + 1024;
+    static constexpr int CB = RK == 64 ? 2 : 1;      // W step: 128-column blocks per item
+    static constexpr uint32_t SMEM_W = XST * SX + OSTW * 2 * SOP + 1024;
+    static_assert(NQ * QW + NRB * BK <= TM_COLS, "V-step TMEM budget");
+    static_assert(2 * CB * ACC <= TM_COLS, "W-step TMEM budget");
+    static_assert(SMEM_V + 2048 <= 232448 && SMEM_W + 2048 <= 232448, "shared memory per CTA");
+};
+static_assert(Tc<64>::SMEM_V == SMEM_V && Tc<64>::SMEM_W == SMEM_W, "rank-64 layout");
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
@@ -159,13 +186,14 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn = 0) {
 // adds X_lo.B_hi into d_lo (its own 64 columns: the epilogue needs X_hi.B_lo
 // alone for the objective's W_lo correction).  The epilogue sums the parts.
 // Issued warp-converged (every lane calls it; one elected lane issues)
+template <int RK>
 __device__ __forceinline__ void issue_split_stage_e(uint32_t d, uint32_t d_lo, const uint8_t* xs,
                                                     const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const uint64_t ah = tc::sdesc_sw128(xs, 16, 1024);
     const uint64_t al = tc::sdesc_sw128(xs + SXH, 16, 1024);
-    constexpr uint32_t id_hi = idesc_f16(BM, ACC);
-    constexpr uint32_t id_lo = idesc_f16(BM, R);
+    constexpr uint32_t id_hi = idesc_f16(BM, 2 * RK);
+    constexpr uint32_t id_lo = idesc_f16(BM, RK);
 #pragma unroll
     for (int ks = 0; ks < BK / 16; ++ks) {
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
@@ -180,13 +208,14 @@ __device__ __forceinline__ void issue_split_stage_e(uint32_t d, uint32_t d_lo, c
 // directly -- no transposed copy of X.  LBO = the second 64-column box, SBO =
 // the next 8 rows; a K16 step advances 16 rows (2048 bytes).
 constexpr uint32_t SXB = BK * 64 * 2;   // 8 KB: one [64 rows x 64 columns] fp16 box
+template <int RK>
 __device__ __forceinline__ void issue_split_stage_mn(uint32_t d, const uint8_t* xs,
                                                      const uint8_t* bhl, bool first) {
     const uint64_t db0 = tc::sdesc_sw128(bhl, 16, 1024);
     const uint64_t ah = tc::sdesc_sw128(xs, SXB, 1024);
     const uint64_t al = tc::sdesc_sw128(xs + SXH, SXB, 1024);
-    constexpr uint32_t id_hi = idesc_f16(BM, ACC) | (1u << 15);   // A MN-major
-    constexpr uint32_t id_lo = idesc_f16(BM, R) | (1u << 15);
+    constexpr uint32_t id_hi = idesc_f16(BM, 2 * RK) | (1u << 15);   // A MN-major
+    constexpr uint32_t id_lo = idesc_f16(BM, RK) | (1u << 15);
 #pragma unroll
     for (int ks = 0; ks < BK / 16; ++ks) {
         const uint32_t acc = (first && ks == 0) ? 0u : 1u;
@@ -270,10 +299,11 @@ struct VBars {
 };
 
 // per-row exponent of V_h: max_k |v_ik| * 2^ev in [2^14, 2^15)
+template <int RK>
 __device__ __forceinline__ int row_exp(const float4* vr) {
     float mx = 0.f;
 #pragma unroll
-    for (int l4 = 0; l4 < R / 4; ++l4) {
+    for (int l4 = 0; l4 < RK / 4; ++l4) {
         const float4 v = vr[l4];
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
@@ -299,26 +329,30 @@ __device__ __forceinline__ int row_exp(const float4* vr) {
 // residual warps read their X stage after the stage's R' commit (which the
 // MMA could only issue once the stage had landed: the peer never sees its own
 // xfull complete).
-template <bool PAIR>
+template <bool PAIR, int RK>
 __global__ void __launch_bounds__(kVThreads, 1)
 nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mWh, const __grid_constant__ CUtensorMap mWl,
               const __grid_constant__ CUtensorMap mVh, const float* __restrict__ V,
               const float* __restrict__ GWf, const float* __restrict__ Gc,
               float* __restrict__ Vout, Scales* sc, int m, int n,
-              double* __restrict__ part) {
-    constexpr uint32_t OSLOT = PAIR ? SOP : 2 * SOP;   // operand slot: pair = this CTA's half
-    constexpr uint32_t QW = PAIR ? QW2 : QW1, RW = PAIR ? RW2 : RW1;
-    constexpr uint32_t TM_RES = 2 * QW;                // residual buffers after the Q sets
+              double* __restrict__ part, float* __restrict__ Qs) {
+    using C = Tc<RK>;
+    static_assert(!PAIR || RK == 64, "the CTA-pair form is rank-64 only");
+    constexpr uint32_t SOPK = C::SOP, SVHK = C::SVH;
+    constexpr uint32_t OSLOT = PAIR ? SOP : 2 * SOPK;  // operand slot: pair = this CTA's half
+    constexpr uint32_t QW = PAIR ? QW2 : C::QW, RW = PAIR ? RW2 : RW1;
+    constexpr int NQ = PAIR ? 2 : C::NQ, NVB = PAIR ? 2 : C::NVB;
+    constexpr uint32_t TM_RES = NQ * QW;               // residual buffers after the Q sets
     constexpr int NARR = PAIR ? 8 : 4;                 // arrivals on dempty / rempty
-    constexpr int XS = PAIR ? XSTV2 : XSTV;            // X ring depth
-    constexpr bool GWS = !PAIR && MMK_TC_GW_SMEM;      // G_W staged in smem
+    constexpr int XS = PAIR ? XSTV2 : C::XS;           // X ring depth
+    constexpr bool GWS = !PAIR && C::GWS;              // G_W staged in smem
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
     uint8_t* oring = base + XS * SX;
     uint8_t* vbuf = oring + OST * OSLOT;
-    float* gws = reinterpret_cast<float*>(vbuf + 2 * SVH);
+    float* gws = reinterpret_cast<float*>(vbuf + NVB * SVHK);
     __shared__ VBars B;
     __shared__ uint32_t tmem_base;
     __shared__ double red[kVThreads / 32];
@@ -388,14 +422,18 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         if (lane == 0) {   // TMA producer
             int it = 0;
             for (int p = 0; p < mine; ++p) {
-                const int tile = tile_of(p), vb = p & 1;
-                tc::mbar_wait(&B.vempty[vb], ((p >> 1) & 1) ^ 1);
+                const int tile = tile_of(p), vb = p % NVB;
+                tc::mbar_wait(&B.vempty[vb], ((p / NVB) & 1) ^ 1);
                 if constexpr (PAIR) {
                     if (rank == 0) tc::mbar_expect_tx(&B.vfull[vb], 2 * SVH);
                     tc::tma_load_2d_pair(vbuf + vb * SVH, &mVh, lead(&B.vfull[vb]), 0, tile * BM);
                 } else {
-                    tc::mbar_expect_tx(&B.vfull[vb], SVH);
-                    tc::tma_load_2d(vbuf + vb * SVH, &mVh, &B.vfull[vb], 0, tile * BM);
+                    // [128 rows x RK ranks] as RK / 64 column atoms of 128-byte rows
+                    tc::mbar_expect_tx(&B.vfull[vb], SVHK);
+#pragma unroll
+                    for (int a = 0; a < RK / 64; ++a)
+                        tc::tma_load_2d(vbuf + vb * SVHK + a * (SVHK / (RK / 64)), &mVh,
+                                        &B.vfull[vb], 64 * a, tile * BM);
                 }
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int os = it % OST, xs = it % XS;
@@ -405,9 +443,9 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         tc::tma_load_2d_pair(oring + os * OSLOT, rank == 0 ? &mWh : &mWl,
                                              lead(&B.ofull[os]), kb * BK, 0);
                     } else {
-                        tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
+                        tc::mbar_expect_tx(&B.ofull[os], 2 * SOPK);
                         tc::tma_load_2d(oring + os * OSLOT, &mWh, &B.ofull[os], kb * BK, 0);
-                        tc::tma_load_2d(oring + os * OSLOT + SOP, &mWl, &B.ofull[os], kb * BK, 0);
+                        tc::tma_load_2d(oring + os * OSLOT + SOPK, &mWl, &B.ofull[os], kb * BK, 0);
                     }
                     tc::mbar_wait(&B.xempty[xs], ((it / XS) & 1) ^ 1);
                     TRACE_AT(0, it);
@@ -425,11 +463,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             constexpr uint32_t id_res = idesc_f16(PAIR ? 2 * BM : BM, RW, 1);
             int it = 0;
             for (int p = 0; p < mine; ++p) {
-                const int b = p & 1;
-                tc::mbar_wait(&B.dempty[b], ((p >> 1) & 1) ^ 1);
-                tc::mbar_wait(&B.vfull[b], (p >> 1) & 1);
+                const int b = p % NQ, vb = p % NVB;
+                tc::mbar_wait(&B.dempty[b], ((p / NQ) & 1) ^ 1);
+                tc::mbar_wait(&B.vfull[vb], (p / NVB) & 1);
                 tc::tc_fence_after();
-                const uint64_t va = tc::sdesc_sw128(vbuf + b * SVH, 16, 1024);
+                const uint64_t va = tc::sdesc_sw128(vbuf + vb * SVHK, 16, 1024);
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int os = it % OST, xs = it % XS, rb = it % NRB;
                     tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
@@ -441,8 +479,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     if constexpr (PAIR)
                         issue_split_stage_pair(tmem + b * QW, xring + xs * SX, ob, kb == 0);
                     else
-                        issue_split_stage_e(tmem + b * QW, tmem + b * QW + ACC, xring + xs * SX,
-                                            ob, kb == 0);
+                        issue_split_stage_e<RK>(tmem + b * QW, tmem + b * QW + C::ACC,
+                                                xring + xs * SX, ob, kb == 0);
                     if (lane == 0) TRACE_AT(2, it);
                     if constexpr (PAIR)
                         tc::mma_commit_pair_e(&B.xempty[xs]);
@@ -451,16 +489,17 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     tc::mbar_wait(&B.rempty[rb], ((it / NRB) & 1) ^ 1);
                     if (lane == 0) TRACE_AT(3, it);
                     tc::tc_fence_after();
-                    const uint64_t wr = tc::sdesc_sw128(ob, SOP, 1024);   // MN-major
+                    const uint64_t wr = tc::sdesc_sw128(ob, PAIR ? SOP : SOPK, 1024);   // MN-major
                     const uint32_t dr = tmem + TM_RES + rb * RW;
 #pragma unroll
-                    for (int ks = 0; ks < R / 16; ++ks) {
+                    for (int ks = 0; ks < RK / 16; ++ks) {
+                        // K16 step ks of V_h: column atom ks / 4 (16 KB apart), 32 bytes in
+                        const uint64_t vk = va + (ks >> 2) * ((SVHK / (RK / 64)) >> 4) + (ks & 3) * 2;
                         if constexpr (PAIR)
-                            tc::mma_f16ss_pair_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
+                            tc::mma_f16ss_pair_e(dr, vk, wr + ks * (2048 >> 4), id_res,
                                                  ks ? 1u : 0u);
                         else
-                            tc::mma_f16ss_e(dr, va + ks * 2, wr + ks * (2048 >> 4), id_res,
-                                            ks ? 1u : 0u);
+                            tc::mma_f16ss_e(dr, vk, wr + ks * (2048 >> 4), id_res, ks ? 1u : 0u);
                     }
                     if constexpr (PAIR) {
                         tc::mma_commit_pair_e(&B.rfull[rb]);
@@ -473,10 +512,10 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 }
                 if constexpr (PAIR) {
                     tc::mma_commit_pair_e(&B.dfull[b]);
-                    tc::mma_commit_pair_e(&B.vempty[b]);
+                    tc::mma_commit_pair_e(&B.vempty[vb]);
                 } else {
                     tc::mma_commit_e(&B.dfull[b]);
-                    tc::mma_commit_e(&B.vempty[b]);
+                    tc::mma_commit_e(&B.vempty[vb]);
                 }
             }
         } else if (lane == 0) {
@@ -499,7 +538,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         int it = 0;
         for (int p = 0; p < mine; ++p) {
             const long long row = (long long)tile_of(p) * BM + r;
-            int ke = ex - (row < m ? row_exp(reinterpret_cast<const float4*>(V + row * R)) : 0) - ew;
+            int ke = ex - (row < m ? row_exp<RK>(reinterpret_cast<const float4*>(V + row * RK)) : 0) -
+                     ew;
             ke = ke < -126 ? -126 : (ke > 127 ? 127 : ke);
             const float nk2 = -exp2f((float)ke);
             const float2 nkk = make_float2(nk2, nk2);
@@ -599,27 +639,56 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
         const double qscale = exp2(-(double)(sc->ex + sc->ew));
         const uint32_t gws_s = tc::smem_u32(gws);
         for (int p = 0; p < mine; ++p) {
-            const int b = p & 1;
-            tc::mbar_wait(&B.dfull[b], (p >> 1) & 1);
+            const int b = p % NQ;
+            tc::mbar_wait(&B.dfull[b], (p / NQ) & 1);
             tc::tc_fence_after();
             const long long row = (long long)tile_of(p) * BM + quarter * 32 + lane;
             const uint32_t ta = tmem + b * QW + lane_off;
-            const float4* vr = reinterpret_cast<const float4*>(V + (row < m ? row : 0) * R);
-            const int ev = row < m ? row_exp(vr) : 0;
-            const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                float q[32], q2[32];
-                tc::tmem_ld32(ta + h * 32, q);   // warp-collective: before the row guard
-                tc::tmem_ld32(ta + R + h * 32, q2);
+            // Q part h (32 columns): q = X.W_hi (+ X_lo.W_hi), q2 = X_hi.W_lo
+            auto load_q = [&](int h, float* q, float* q2) {
+                tc::tmem_ld32(ta + h * 32, q);   // warp-collective: before any row guard
+                tc::tmem_ld32(ta + RK + h * 32, q2);
                 if constexpr (!PAIR) {   // + X_lo.W_hi (its own columns)
                     float q3[32];
-                    tc::tmem_ld32(ta + 2 * R + h * 32, q3);
+                    tc::tmem_ld32(ta + 2 * RK + h * 32, q3);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) q[i] += q3[i];
                 }
+            };
+            if constexpr (NQ == 1) {
+                // one Q set (RK = 128): copy it out as [q | q2] rows of the
+                // scratch and hand the set back to the MMA warp; the V'
+                // arithmetic is vfinish_kernel's (G_W and G_c staged in its
+                // shared memory -- here they would not fit beside the rings)
+                float4* qrow = reinterpret_cast<float4*>(Qs + (row < m ? row : 0) * (2 * RK));
+#pragma unroll 1
+                for (int h = 0; h < RK / 32; ++h) {
+                    float q[32], q2[32];
+                    load_q(h, q, q2);
+                    if (row < m) {
+#pragma unroll
+                        for (int k4 = 0; k4 < 8; ++k4) {
+                            qrow[h * 8 + k4] = make_float4(q[4 * k4], q[4 * k4 + 1], q[4 * k4 + 2],
+                                                           q[4 * k4 + 3]);
+                            qrow[RK / 4 + h * 8 + k4] = make_float4(q2[4 * k4], q2[4 * k4 + 1],
+                                                                    q2[4 * k4 + 2], q2[4 * k4 + 3]);
+                        }
+                    }
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_lead(&B.dempty[b]);
+                continue;
+            }
+            const float4* vr = reinterpret_cast<const float4*>(V + (row < m ? row : 0) * RK);
+            const int ev = row < m ? row_exp<RK>(vr) : 0;
+            const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
+#pragma unroll 1
+            for (int h = 0; h < RK / 32; ++h) {
+                float q[32], q2[32];
+                load_q(h, q, q2);
                 if (row >= m) continue;
-                float4* o = reinterpret_cast<float4*>(Vout + row * R + h * 32);
+                float4* o = reinterpret_cast<float4*>(Vout + row * RK + h * 32);
 #pragma unroll
                 for (int hh = 0; hh < 4; ++hh) {
                     // columns h*32 + hh*8 .. +8: (V G_W) and (E G_W) in fp32
@@ -627,20 +696,20 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
 #pragma unroll
                     for (int c = 0; c < 8; ++c) den[c] = eg[c] = gcg[c] = 0.f;
 #pragma unroll 2
-                    for (int l4 = 0; l4 < R / 4; ++l4) {
+                    for (int l4 = 0; l4 < RK / 4; ++l4) {
                         const float4 vv = vr[l4];
                         const float va[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float el = va[e] - __half2float(__float2half_rn(va[e] * vs)) * vsi;
                             const uint32_t g4 =
-                                gws_s + 4u * (uint32_t)((4 * l4 + e) * R + h * 32 + hh * 8);
+                                gws_s + 4u * (uint32_t)((4 * l4 + e) * RK + h * 32 + hh * 8);
 #pragma unroll
                             for (int c4 = 0; c4 < 2; ++c4) {
                                 const float4 gg =
                                     GWS ? tc::lds128f(g4 + 16u * c4)
                                         : __ldg(reinterpret_cast<const float4*>(GWf) +
-                                                (((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4));
+                                                (((4 * l4 + e) * RK + h * 32 + hh * 8) / 4 + c4));
                                 den[4 * c4] = fmaf(va[e], gg.x, den[4 * c4]);
                                 den[4 * c4 + 1] = fmaf(va[e], gg.y, den[4 * c4 + 1]);
                                 den[4 * c4 + 2] = fmaf(va[e], gg.z, den[4 * c4 + 2]);
@@ -651,7 +720,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                 eg[4 * c4 + 3] = fmaf(el, gg.w, eg[4 * c4 + 3]);
                                 if constexpr (!PAIR) {   // v_h G_c, G_c = 2 W_hi W_lo^T + W_lo W_lo^T
                                     const float vh = va[e] - el;
-                                    const int gi = ((4 * l4 + e) * R + h * 32 + hh * 8) / 4 + c4;
+                                    const int gi = ((4 * l4 + e) * RK + h * 32 + hh * 8) / 4 + c4;
                                     const float4 gc = __ldg(reinterpret_cast<const float4*>(Gc) + gi);
                                     gcg[4 * c4] = fmaf(vh, gc.x, gcg[4 * c4]);
                                     gcg[4 * c4 + 1] = fmaf(vh, gc.y, gcg[4 * c4 + 1]);
@@ -688,9 +757,11 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                     }
                 }
             }
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive_lead(&B.dempty[b]);
+            if constexpr (NQ == 2) {
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_lead(&B.dempty[b]);
+            }
         }
     }
     // per-CTA share of f (residual + correction terms, fixed warp order) and max(V')
@@ -721,18 +792,20 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     }
 }
 
-// V (m x 64 fp32) -> V_h = rn(V_i 2^ev_i) fp16 row-major (the A operand of
-// the residual MMAs), ev_i = scale_exp(max_k |v_ik|); 16 threads per row
+// V (m x RK fp32) -> V_h = rn(V_i 2^ev_i) fp16 row-major (the A operand of
+// the residual MMAs), ev_i = scale_exp(max_k |v_ik|); RK / 4 threads per row
+template <int RK>
 __global__ void __launch_bounds__(256)
 split_v_kernel(const float* __restrict__ V, __half* __restrict__ Vh, long long m) {
+    constexpr int TPR = RK / 4;   // threads per row (16 or 32)
     const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
-    const long long row = t >> 4;
-    const int c4 = (int)(t & 15);
+    const long long row = t / TPR;
+    const int c4 = (int)(t % TPR);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row < m) v = reinterpret_cast<const float4*>(V + row * R)[c4];
+    if (row < m) v = reinterpret_cast<const float4*>(V + row * RK)[c4];
     float mx = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = TPR / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (row >= m) return;
     const float s = exp2f((float)scale_exp(mx));
     const __half2 a = __floats2half2_rn(v.x * s, v.y * s);
@@ -740,7 +813,145 @@ split_v_kernel(const float* __restrict__ V, __half* __restrict__ Vh, long long m
     uint2 o;
     o.x = *reinterpret_cast<const uint32_t*>(&a);
     o.y = *reinterpret_cast<const uint32_t*>(&b);
-    reinterpret_cast<uint2*>(Vh + row * R)[c4] = o;
+    reinterpret_cast<uint2*>(Vh + row * RK)[c4] = o;
+}
+
+// RK = 128: the V' arithmetic of the V step (its rank-64 epilogue above, the
+// same terms) as a pass over the [q | q2] rows the V step copied out.  Block
+// (x, y) takes the 64 columns y * 64 .. of every 256-row tile x, x + gridDim.x,
+// ...: that half of G_W and G_c (fp32, 64 KB) and the tile of V (coalesced
+// load, padded rows, 132 KB) are staged in shared memory; a thread per row,
+// so every G read is a warp-wide broadcast and every V read hits 32 distinct
+// banks.  V' = V Q / (V G_W + 1e-300), the correction terms of f for V's fp16
+// rounding and the W_lo part of the residual -> part[y gridDim.x + x] (fixed
+// order), max V' -> sc->vmax_bits.
+constexpr int kVfinThreads = 256;
+constexpr int kVfinCols = 64;
+template <int RK>
+constexpr uint32_t vfinish_smem() {
+    return (2 * RK * kVfinCols + kVfinThreads * (RK + 1)) * 4;
+}
+template <int RK>
+__global__ void __launch_bounds__(kVfinThreads, 1)
+vfinish_kernel(const float* __restrict__ Qs, const float* __restrict__ V,
+               const float* __restrict__ GWf, const float* __restrict__ Gc,
+               float* __restrict__ Vout, Scales* sc, long long m, double* __restrict__ part) {
+    constexpr int ROWS = kVfinThreads, NC = kVfinCols;
+    extern __shared__ __align__(16) float fsm[];
+    float* vt = fsm + 2 * RK * NC;   // [ROWS][RK + 1]
+    const int cb = (int)blockIdx.y * NC;   // first column of this block's half
+    for (int i = threadIdx.x; i < RK * NC / 4; i += kVfinThreads) {
+        const int l = i / (NC / 4), c4 = (i % (NC / 4)) * 4;
+        reinterpret_cast<float4*>(fsm)[i] =
+            __ldg(reinterpret_cast<const float4*>(GWf + (long long)l * RK + cb + c4));
+        reinterpret_cast<float4*>(fsm + RK * NC)[i] =
+            __ldg(reinterpret_cast<const float4*>(Gc + (long long)l * RK + cb + c4));
+    }
+    const uint32_t gw_s = tc::smem_u32(fsm), gc_s = tc::smem_u32(fsm + RK * NC);
+    const double qscale = exp2(-(double)(sc->ex + sc->ew));
+    double acc = 0.0;
+    float vmax = 0.f;
+    for (long long r0 = (long long)blockIdx.x * ROWS; r0 < m; r0 += (long long)gridDim.x * ROWS) {
+        __syncthreads();   // the previous tile's readers are done (and G is staged)
+        for (int i = threadIdx.x; i < ROWS * (RK / 4); i += kVfinThreads) {
+            const int rr = i / (RK / 4), c4 = (i % (RK / 4)) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r0 + rr < m) v = __ldg(reinterpret_cast<const float4*>(V + (r0 + rr) * RK + c4));
+            float* d = vt + rr * (RK + 1) + c4;
+            d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+        }
+        __syncthreads();
+        const long long row = r0 + threadIdx.x;
+        if (row >= m) continue;
+        const float* vrow = vt + threadIdx.x * (RK + 1);
+        float mx = 0.f;
+#pragma unroll 8
+        for (int k = 0; k < RK; ++k) mx = fmaxf(mx, fabsf(vrow[k]));
+        const int ev = scale_exp(mx);
+        const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
+        const float4* qrow = reinterpret_cast<const float4*>(Qs + row * (2 * RK));
+        float4* o = reinterpret_cast<float4*>(Vout + row * RK);
+#pragma unroll 1
+        for (int c0 = 0; c0 < NC; c0 += 8) {   // this pass's 8 columns (of the half)
+            // column pairs (c, c + 1) as packed fp32x2 FMAs (the same two fp32 FMAs)
+            float2 den2[4], eg2[4], gcg2[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) den2[c] = eg2[c] = gcg2[c] = make_float2(0.f, 0.f);
+#pragma unroll 4
+            for (int l = 0; l < RK; ++l) {
+                const float va = vrow[l];
+                const float el = va - __half2float(__float2half_rn(va * vs)) * vsi;
+                const float vh = va - el;
+                const float2 va2 = make_float2(va, va), el2 = make_float2(el, el),
+                             vh2 = make_float2(vh, vh);
+                const uint32_t off = 4u * (uint32_t)(l * NC + c0);
+#pragma unroll
+                for (int c4 = 0; c4 < 2; ++c4) {
+                    const float4 gg = tc::lds128f(gw_s + off + 16u * c4);
+                    const float4 gc = tc::lds128f(gc_s + off + 16u * c4);
+                    const float2 g0 = make_float2(gg.x, gg.y), g1 = make_float2(gg.z, gg.w);
+                    const float2 h0 = make_float2(gc.x, gc.y), h1 = make_float2(gc.z, gc.w);
+                    den2[2 * c4] = __ffma2_rn(va2, g0, den2[2 * c4]);
+                    den2[2 * c4 + 1] = __ffma2_rn(va2, g1, den2[2 * c4 + 1]);
+                    eg2[2 * c4] = __ffma2_rn(el2, g0, eg2[2 * c4]);
+                    eg2[2 * c4 + 1] = __ffma2_rn(el2, g1, eg2[2 * c4 + 1]);
+                    gcg2[2 * c4] = __ffma2_rn(vh2, h0, gcg2[2 * c4]);
+                    gcg2[2 * c4 + 1] = __ffma2_rn(vh2, h1, gcg2[2 * c4 + 1]);
+                }
+            }
+            float den[8], eg[8], gcg[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                den[2 * c] = den2[c].x, den[2 * c + 1] = den2[c].y;
+                eg[2 * c] = eg2[c].x, eg[2 * c + 1] = eg2[c].y;
+                gcg[2 * c] = gcg2[c].x, gcg[2 * c + 1] = gcg2[c].y;
+            }
+#pragma unroll
+            for (int kq = 0; kq < 2; ++kq) {
+                const int k4 = (cb + c0) / 4 + kq;   // float4 index in the row
+                const float4 qv = qrow[k4], q2v = qrow[RK / 4 + k4];
+                const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+                const float q2a[4] = {q2v.x, q2v.y, q2v.z, q2v.w};
+                float nv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int c = 4 * kq + i;
+                    const float vf = vrow[4 * k4 + i];
+                    const double vk = (double)vf;
+                    const double qk = ((double)qa[i] + (double)q2a[i]) * qscale;
+                    const double dk = (double)den[c];
+                    const double ek = (double)(vf - __half2float(__float2half_rn(vf * vs)) * vsi);
+                    acc = fma(-2.0 * (qk - dk), ek, acc);
+                    acc = fma(-ek, (double)eg[c], acc);
+                    acc = fma(vk - ek, (double)gcg[c] - 2.0 * (double)q2a[i] * qscale, acc);
+                    nv[i] = (float)(vk * (qk / (dk + kDenomGuard)));
+                    vmax = fmaxf(vmax, nv[i]);
+                }
+                o[k4] = make_float4(nv[0], nv[1], nv[2], nv[3]);
+            }
+        }
+    }
+    // block share of f (fixed order) and max(V')
+    __shared__ double red[kVfinThreads / 32];
+    __shared__ float vmx[kVfinThreads / 32];
+    acc = warp_sum(acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = acc;
+        vmx[threadIdx.x >> 5] = vmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double c = 0.0;
+        float mx = 0.f;
+        for (int w = 0; w < kVfinThreads / 32; ++w) {
+            c += red[w];
+            mx = fmaxf(mx, vmx[w]);
+        }
+        part[blockIdx.y * gridDim.x + blockIdx.x] = c;
+        atomicMax(&sc->vmax_bits, __float_as_uint(mx));   // V' >= 0: bit order = value order
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -754,12 +965,15 @@ struct WBars {
     uint64_t dfull[2], dempty[2];
 };
 
+template <int RK>
 __global__ void __launch_bounds__(kWThreads, 1)
 nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mX2,
               const __grid_constant__ CUtensorMap mVh, const __grid_constant__ CUtensorMap mVl,
               int m, int n, int splits, int rows_per_split, float* __restrict__ wpart,
               const long long* __restrict__ skip) {
     if (skip && *skip) return;   // the engine's final pass (iteration cap): W half unused
+    constexpr int CB = Tc<RK>::CB, ACC = Tc<RK>::ACC;
+    constexpr uint32_t SOP = Tc<RK>::SOP;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
@@ -851,8 +1065,8 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         const int xs = xit % XST;
                         tc::mbar_wait(&B.xfull[xs], (xit / XST) & 1);
                         tc::tc_fence_after();
-                        issue_split_stage_mn(tmem + (b * CB + j) * ACC, xring + xs * SX,
-                                             oring + os * 2 * SOP, kb == 0);
+                        issue_split_stage_mn<RK>(tmem + (b * CB + j) * ACC, xring + xs * SX,
+                                                 oring + os * 2 * SOP, kb == 0);
                         tc::mma_commit(&B.xempty[xs]);
                     }
                     tc::mma_commit(&B.oempty[os]);
@@ -872,15 +1086,15 @@ nnmf_wstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::tc_fence_after();
             for (int j = 0; j < nacc; ++j) {
                 const long long col = (long long)((item % ncs) * CB + j) * BM + quarter * 32 + lane;
-                float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * R);
+                float4* o = reinterpret_cast<float4*>(wpart + ((long long)s * n + col) * RK);
                 const uint32_t ta = tmem + (b * CB + j) * ACC + lane_off;
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < RK / 32; ++h) {
                     float v[32];
                     if (nkb > 0) {
                         float v2[32];
                         tc::tmem_ld32(ta + h * 32, v);
-                        tc::tmem_ld32(ta + R + h * 32, v2);
+                        tc::tmem_ld32(ta + RK + h * 32, v2);
 #pragma unroll
                         for (int k = 0; k < 32; ++k) v[k] += v2[k];   // scaled units (see wreduce)
                     } else {
@@ -1023,16 +1237,20 @@ presplit_kernel(const float* __restrict__ X, long long ldx, long long m, long lo
     }
 }
 
-// Rank-64 Gram G = sum_c a_c a_c^T of fp32 vectors a_c (VEC_ROWS: A is
-// 64 x len, the vectors are columns of the row-major W; else A is len x 64,
-// the rows of V).  Products are formed in fp32 and summed 8 at a time in
-// fp32, then folded into fp64 accumulators (4 x 4 per thread); each block
-// writes its partial, gram_sum_kernel adds the partials in block order.
-template <bool VEC_ROWS>
+// Gram G = sum_c a_c a_c^T of fp32 vectors a_c of RK components (VEC_ROWS:
+// A is RK x len, the vectors are columns of the row-major W; else A is len x
+// RK, the rows of V).  A block computes the 64 x 64 quadrant (blockIdx.y / QN,
+// blockIdx.y % QN) of G (one quadrant at RK = 64).  Products are formed in
+// fp32 and summed 8 at a time in fp32, then folded into fp64 accumulators
+// (4 x 4 per thread); each block writes its partial, gram_sum_kernel adds
+// the partials in block order.
+template <bool VEC_ROWS, int RK>
 __global__ void __launch_bounds__(256)
 gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
               double* __restrict__ part) {
-    __shared__ __align__(16) float S[32][64 + 4];
+    constexpr int QN = RK / 64;
+    __shared__ __align__(16) float S[QN][32][64 + 4];   // [quadrant half][vector][component]
+    const int qi = (int)blockIdx.y / QN, qj = (int)blockIdx.y % QN;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double acc[4][4];
 #pragma unroll
@@ -1044,16 +1262,16 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
     if (c_end > len) c_end = len;
     for (long long c0 = c_begin; c0 < c_end; c0 += 32) {
         if (VEC_ROWS) {
-            for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
+            for (int idx = threadIdx.x; idx < 32 * RK; idx += 256) {
                 const int a = idx >> 5, cc = idx & 31;
-                S[cc][a] = (c0 + cc < c_end) ? A[(long long)a * len + c0 + cc] : 0.f;
+                S[a >> 6][cc][a & 63] = (c0 + cc < c_end) ? A[(long long)a * len + c0 + cc] : 0.f;
             }
         } else {
-            for (int idx = threadIdx.x; idx < 32 * 16; idx += 256) {
-                const int cc = idx >> 4, a4 = (idx & 15) * 4;
+            for (int idx = threadIdx.x; idx < 32 * (RK / 4); idx += 256) {
+                const int cc = idx / (RK / 4), a4 = (idx % (RK / 4)) * 4;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (c0 + cc < c_end) v = *reinterpret_cast<const float4*>(A + (c0 + cc) * 64 + a4);
-                *reinterpret_cast<float4*>(&S[cc][a4]) = v;
+                if (c0 + cc < c_end) v = *reinterpret_cast<const float4*>(A + (c0 + cc) * RK + a4);
+                *reinterpret_cast<float4*>(&S[a4 >> 6][cc][a4 & 63]) = v;
             }
         }
         __syncthreads();
@@ -1066,8 +1284,8 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
                 for (int j = 0; j < 4; ++j) p[i][j] = 0.f;
 #pragma unroll
             for (int kk = k8; kk < k8 + 8; ++kk) {
-                const float4 a = *reinterpret_cast<const float4*>(&S[kk][4 * ty]);
-                const float4 b = *reinterpret_cast<const float4*>(&S[kk][4 * tx]);
+                const float4 a = *reinterpret_cast<const float4*>(&S[qi][kk][4 * ty]);
+                const float4 b = *reinterpret_cast<const float4*>(&S[qj][kk][4 * tx]);
                 const float av[4] = {a.x, a.y, a.z, a.w};
                 const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -1082,24 +1300,29 @@ gram32_kernel(const float* __restrict__ A, long long len, long long per_block,
         }
         __syncthreads();
     }
-    double* pb = part + (long long)blockIdx.x * (R * R);
+    double* pb = part + (long long)blockIdx.x * (RK * RK);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[i][j];
+        for (int j = 0; j < 4; ++j) pb[(64 * qi + 4 * ty + i) * RK + 64 * qj + 4 * tx + j] = acc[i][j];
 }
 
-// The W-side Grams of one iteration in one pass over W (64 x len, rows are
+// The W-side Grams of one iteration in one pass over W (RK x len, rows are
 // the vectors): G_W = W W^T as gram32_kernel<true>, plus G_c = (2 W_hi +
 // W_lo) W_lo^T = 2 W_hi W_lo^T + W_lo W_lo^T of the fp16 split the V-step MMAs
 // use (W_hi = rn(w 2^ew) 2^-ew, W_lo = rn(w 2^ew - W_hi 2^ew) 2^-ew, as
 // split_w_kernel), the Gram of the objective's W_lo correction.  fp32
-// products summed 8 at a time and folded into fp64.  Partials: part[b],
-// part[gridDim + b].
+// products summed 8 at a time and folded into fp64.  A block computes the
+// 64 x 64 quadrant (blockIdx.y / QN, blockIdx.y % QN) of both.  Partials:
+// part[b], part[gridDim.x + b].
+template <int RK>
 __global__ void __launch_bounds__(256)
 gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
              const Scales* sc, double* __restrict__ part) {
-    __shared__ __align__(16) float S[32][64 + 4], Sh[32][64 + 4], Sl[32][64 + 4];
+    constexpr int QN = RK / 64;
+    // rows of quadrant row qi (w, 2 w_hi + w_lo) and of quadrant column qj (w, w_lo)
+    __shared__ __align__(16) float Sa[32][64 + 4], Sc[32][64 + 4], Sb[32][64 + 4], Sl[32][64 + 4];
+    const int qi = (int)blockIdx.y / QN, qj = (int)blockIdx.y % QN;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const float s = exp2f((float)sc->ew), si = exp2f(-(float)sc->ew);
     double acc[2][4][4];
@@ -1113,14 +1336,19 @@ gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
     long long c_end = c_begin + per_block;
     if (c_end > len) c_end = len;
     for (long long c0 = c_begin; c0 < c_end; c0 += 32) {
-        for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
-            const int a = idx >> 5, cc = idx & 31;
-            const float w = (c0 + cc < c_end) ? A[(long long)a * len + c0 + cc] : 0.f;
+        for (int idx = threadIdx.x; idx < 2 * 32 * 64; idx += 256) {
+            const int side = idx >> 11, a = (idx >> 5) & 63, cc = idx & 31;
+            const int row = 64 * (side ? qj : qi) + a;
+            const float w = (c0 + cc < c_end) ? A[(long long)row * len + c0 + cc] : 0.f;
             const float hi = __half2float(__float2half_rn(w * s));
             const float lo = __half2float(__float2half_rn(w * s - hi));
-            S[cc][a] = w;
-            Sh[cc][a] = hi * si;
-            Sl[cc][a] = lo * si;
+            if (side) {
+                Sb[cc][a] = w;
+                Sl[cc][a] = lo * si;
+            } else {
+                Sa[cc][a] = w;
+                Sc[cc][a] = 2.f * (hi * si) + lo * si;
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -1134,20 +1362,19 @@ gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
                     for (int j = 0; j < 4; ++j) p[g][i][j] = 0.f;
 #pragma unroll
             for (int kk = k8; kk < k8 + 8; ++kk) {
-                const float4 a = *reinterpret_cast<const float4*>(&S[kk][4 * ty]);
-                const float4 b = *reinterpret_cast<const float4*>(&S[kk][4 * tx]);
-                const float4 ah = *reinterpret_cast<const float4*>(&Sh[kk][4 * ty]);
-                const float4 al = *reinterpret_cast<const float4*>(&Sl[kk][4 * ty]);
+                const float4 a = *reinterpret_cast<const float4*>(&Sa[kk][4 * ty]);
+                const float4 b = *reinterpret_cast<const float4*>(&Sb[kk][4 * tx]);
+                const float4 ac = *reinterpret_cast<const float4*>(&Sc[kk][4 * ty]);
                 const float4 bl = *reinterpret_cast<const float4*>(&Sl[kk][4 * tx]);
                 const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-                const float ahv[4] = {ah.x, ah.y, ah.z, ah.w}, alv[4] = {al.x, al.y, al.z, al.w};
+                const float acv[4] = {ac.x, ac.y, ac.z, ac.w};
                 const float blv[4] = {bl.x, bl.y, bl.z, bl.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         p[0][i][j] = fmaf(av[i], bv[j], p[0][i][j]);
-                        p[1][i][j] = fmaf(2.f * ahv[i] + alv[i], blv[j], p[1][i][j]);
+                        p[1][i][j] = fmaf(acv[i], blv[j], p[1][i][j]);
                     }
             }
 #pragma unroll
@@ -1161,16 +1388,18 @@ gram3_kernel(const float* __restrict__ A, long long len, long long per_block,
     }
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
-        double* pb = part + ((long long)g * gridDim.x + blockIdx.x) * (R * R);
+        double* pb = part + ((long long)g * gridDim.x + blockIdx.x) * (RK * RK);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) pb[(4 * ty + i) * R + 4 * tx + j] = acc[g][i][j];
+            for (int j = 0; j < 4; ++j)
+                pb[(64 * qi + 4 * ty + i) * RK + 64 * qj + 4 * tx + j] = acc[g][i][j];
     }
 }
 
 // out[e] = sum_b part[b][e] in block order: 8 groups of 128 threads take
 // interleaved partials, combined in group order (deterministic)
+template <int RK>
 __global__ void __launch_bounds__(1024)
 gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out,
                 float* __restrict__ outf, const long long* __restrict__ skip = nullptr) {
@@ -1179,7 +1408,7 @@ gram_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict_
     const int o = blockIdx.x * 128 + (threadIdx.x & 127), g = threadIdx.x >> 7;
     double s = 0.0;
 #pragma unroll 4
-    for (int b = g; b < nparts; b += 8) s += part[(long long)b * (R * R) + o];
+    for (int b = g; b < nparts; b += 8) s += part[(long long)b * (RK * RK) + o];
     sm[g][threadIdx.x & 127] = s;
     __syncthreads();
     if (g == 0) {
@@ -1247,12 +1476,20 @@ __global__ void split_w_kernel(const float* __restrict__ W, __half* __restrict__
 // and a row-major copy S (for the Gram: thread (ty, tx) owns the 4 x 4 block
 // (4 ty, 4 tx), fp32 products of 8 rows folded into fp64, as gram32_kernel);
 // the block's partial goes to gpart[blockIdx.x] (gram_sum_kernel adds them).
+// RK = 128: the transposed split only (GRAM = false; the Gram of V' is
+// gram32_kernel's, one more read of V').
 constexpr int kVprepBlocks = 2 * kNumSMs;
-constexpr uint32_t kVprepSmem = (R * (128 + 4) + 128 * (R + 4)) * 4;
+template <int RK, bool GRAM>
+constexpr uint32_t vprep_smem() {
+    return (RK * (128 + 4) + (GRAM ? 128 * (RK + 4) : 0)) * 4;
+}
+template <int RK, bool GRAM>
 __global__ void __launch_bounds__(256)
 vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
                   __half* __restrict__ Vtl, long long m, Scales* sc, double* __restrict__ gpart,
                   const long long* __restrict__ skip) {
+    static_assert(!GRAM || RK == 64, "the fused Gram is rank-64 only");
+    constexpr int R = RK;
     if (skip && *skip) return;
     extern __shared__ __align__(16) float vsm[];
     float(*T)[128 + 4] = reinterpret_cast<float(*)[128 + 4]>(vsm);
@@ -1273,7 +1510,7 @@ vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
             const int rr = i / (R / 4), k4 = (i % (R / 4)) * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (r0 + rr < m) v = *reinterpret_cast<const float4*>(V + (r0 + rr) * R + k4);
-            *reinterpret_cast<float4*>(&S[rr][k4]) = v;
+            if (GRAM) *reinterpret_cast<float4*>(&S[rr][k4]) = v;
             T[k4][rr] = v.x * s;
             T[k4 + 1][rr] = v.y * s;
             T[k4 + 2][rr] = v.z * s;
@@ -1302,7 +1539,7 @@ vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
         }
         // Gram share of the tile's 128 rows (rows past m are zero)
 #pragma unroll 1
-        for (int k8 = 0; k8 < 128; k8 += 8) {
+        for (int k8 = 0; k8 < (GRAM ? 128 : 0); k8 += 8) {
             float p[4][4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -1326,6 +1563,7 @@ vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
         }
         __syncthreads();
     }
+    if (!GRAM) return;
     double* pb = gpart + (long long)blockIdx.x * (R * R);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -1334,30 +1572,32 @@ vprep_gram_kernel(const float* __restrict__ V, __half* __restrict__ Vth,
 }
 
 // red[k n + j] = sum_s wpart[s][j][k] (fixed split order); a block owns 32
-// columns j: coalesced reads of the [32 j][64 k] slab of every split, fp64
+// columns j: coalesced reads of the [32 j][RK k] slab of every split, fp64
 // sums, transposed through shared memory for coalesced writes
+template <int RK>
 __global__ void __launch_bounds__(256)
 wreduce_tc_kernel(const float* __restrict__ wpart, int splits, long long n,
                   double* __restrict__ red, const Scales* sc, const long long* __restrict__ skip) {
+    constexpr int R = RK, NQ8 = RK / 8;   // slab elements per thread
     if (skip && *skip) return;
     __shared__ double T[R][32 + 1];
     // partials are in the scaled units of the split products: X 2^ex, V' 2^ev
     const double pscale = exp2(-(double)(sc->ex + sc->ev));
     const long long j0 = (long long)blockIdx.x * 32;
-    double acc[8];
+    double acc[NQ8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    // element e = q * 256 + tid of the slab: j = e / 64, k = e % 64
+    for (int q = 0; q < NQ8; ++q) acc[q] = 0.0;
+    // element e = q * 256 + tid of the slab: j = e / RK, k = e % RK
     for (int sp = 0; sp < splits; ++sp) {
         const float* src = wpart + ((long long)sp * n + j0) * R;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NQ8; ++q) {
             const int e = q * 256 + threadIdx.x;
             if (j0 + e / R < n) acc[q] += (double)src[e];
         }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NQ8; ++q) {
         const int e = q * 256 + threadIdx.x;
         T[e % R][e / R] = acc[q] * pscale;
     }
@@ -1376,37 +1616,40 @@ __global__ void tc_objective_kernel(const double* __restrict__ part, int nparts,
     if (threadIdx.x == 0) *out = f;
 }
 
-// rank r < 64 on the rank-64 kernels: V (m x r) -> V64 (m x 64, zero
-// columns r..63) and back; the rank-64 reduction buffer's G block -> r x r
-__global__ void pad_cols_kernel(const float* __restrict__ src, int r, long long rows,
+// rank r < RK on the rank-RK kernels: V (m x r) -> V_RK (m x RK, zero
+// columns r..RK-1) and back; the rank-RK reduction buffer's G block -> r x r
+__global__ void pad_cols_kernel(const float* __restrict__ src, int r, int rk, long long rows,
                                 float* __restrict__ dst) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rows * R) return;
-    const long long i = t / R;
-    const int k = (int)(t % R);
+    if (t >= rows * rk) return;
+    const long long i = t / rk;
+    const int k = (int)(t % rk);
     dst[t] = k < r ? src[i * r + k] : 0.f;
 }
-__global__ void unpad_cols_kernel(const float* __restrict__ src, int r, long long rows,
+__global__ void unpad_cols_kernel(const float* __restrict__ src, int r, int rk, long long rows,
                                   float* __restrict__ dst) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= rows * r) return;
-    dst[t] = src[(t / r) * R + t % r];
+    dst[t] = src[(t / r) * rk + t % r];
 }
-__global__ void unpad_gram_kernel(const double* __restrict__ g64, const double* __restrict__ f64,
-                                  int r, double* __restrict__ g, double* __restrict__ f) {
+__global__ void unpad_gram_kernel(const double* __restrict__ gk, const double* __restrict__ fk,
+                                  int r, int rk, double* __restrict__ g, double* __restrict__ f) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < r * r) g[t] = g64[(t / r) * R + t % r];
-    if (t == 0) *f = *f64;
+    if (t < r * r) g[t] = gk[(t / r) * rk + t % r];
+    if (t == 0) *f = *fk;
 }
+
+// the rank tile of rank r: 64 for ranks 17..64, 128 for 65..128
+inline int rank_tile(long long r) { return r <= 64 ? 64 : 128; }
 
 struct TcPlan {
     int vgrid, wgrid, splits, rows_per_split;
     bool vpair;   // V step as CTA pairs (cta_group::2)
 };
 
-// MMK_TC_PAIR=1 runs the V step as CTA pairs (cta_group::2; same results to
-// rounding -- Q gains the X_lo.W_lo product -- and 8 % slower at C4, see the
-// V-step notes above); single CTAs are the default
+// MMK_TC_PAIR=1 runs the rank-64 V step as CTA pairs (cta_group::2; same
+// results to rounding -- Q gains the X_lo.W_lo product -- and 8 % slower at
+// C4, see the V-step notes above); single CTAs are the default
 bool vstep_pair_enabled() {
     static const bool on = [] {
         const char* e = getenv("MMK_TC_PAIR");
@@ -1415,20 +1658,21 @@ bool vstep_pair_enabled() {
     return on;
 }
 
-TcPlan tc_plan(long long m, long long n) {
+TcPlan tc_plan(long long m, long long n, int rk) {
     TcPlan P;
     const int ntiles = (int)((m + BM - 1) / BM);
-    P.vpair = vstep_pair_enabled() && ntiles >= 2;
+    P.vpair = rk == 64 && vstep_pair_enabled() && ntiles >= 2;
     if (P.vpair) {
         const int units = (ntiles + 1) / 2;
         P.vgrid = 2 * (units < kNumSMs / 2 ? units : kNumSMs / 2);
     } else {
         P.vgrid = ntiles < kNumSMs ? ntiles : kNumSMs;
     }
+    const int cb = rk == 64 ? Tc<64>::CB : Tc<128>::CB;
     const int ncb = (int)((n + BM - 1) / BM);
-    const int ncs = (ncb + CB - 1) / CB;
+    const int ncs = (ncb + cb - 1) / cb;
     // split count minimising (wave quantisation loss) + (split-K partial
-    // traffic: S fp32 partials of n x 64 written and read back, relative to
+    // traffic: S fp32 partials of n x rk written and read back, relative to
     // one pass over X); rows per split >= 4 K-blocks
     const int max_splits = (int)((m + 4 * BK - 1) / (4 * BK));
     int best = 1;
@@ -1437,7 +1681,7 @@ TcPlan tc_plan(long long m, long long n) {
         const int items = ncs * S;
         const int waves = (items + kNumSMs - 1) / kNumSMs;
         const double eff = (double)items / ((double)waves * kNumSMs);
-        const double partial = 2.0 * S * (double)n * R * 4.0 / ((double)m * n * 4.0);
+        const double partial = 2.0 * S * (double)n * rk * 4.0 / ((double)m * n * 4.0);
         const double cost = 1.0 / eff + partial;
         if (cost < best_cost - 1e-12) {
             best_cost = cost;
@@ -1455,36 +1699,40 @@ TcPlan tc_plan(long long m, long long n) {
 
 constexpr int kGramBlocks = 2 * kNumSMs;
 
-// G = Gram of A (see gram32_kernel) into out (fp64 64 x 64)
+// G = Gram of A (see gram32_kernel) into out (fp64 RK x RK)
+template <int RK>
 void gram32(const float* A, long long len, bool vec_rows, double* gpart, double* out,
             cudaStream_t st, float* outf = nullptr) {
     long long per = (len + kGramBlocks - 1) / kGramBlocks;
     per = (per + 31) / 32 * 32;
     const int blocks = (int)((len + per - 1) / per);
+    const dim3 grid(blocks, (RK / 64) * (RK / 64));
     if (vec_rows)
         MMK_LAUNCH("nnmf_gram32", st,
-                   (gram32_kernel<true><<<blocks, 256, 0, st>>>(A, len, per, gpart)));
+                   (gram32_kernel<true, RK><<<grid, 256, 0, st>>>(A, len, per, gpart)));
     else
         MMK_LAUNCH("nnmf_gram32", st,
-                   (gram32_kernel<false><<<blocks, 256, 0, st>>>(A, len, per, gpart)));
+                   (gram32_kernel<false, RK><<<grid, 256, 0, st>>>(A, len, per, gpart)));
     MMK_LAUNCH("nnmf_gram_sum", st,
-               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, out, outf)));
+               (gram_sum_kernel<RK><<<RK * RK / 128, 1024, 0, st>>>(gpart, blocks, out, outf)));
 }
 
 // G_W and G_c = 2 W_hi W_lo^T + W_lo W_lo^T (gram3_kernel) -> GW (fp64), GWf, GcF
+template <int RK>
 void gram3(const float* W, long long len, const Scales* sc, double* gpart, double* GW,
            float* GWf, double* G64, float* GcF, cudaStream_t st) {
-    // one wave: the kernel holds three 4 x 4 fp64 accumulator sets (one CTA per SM)
+    // one wave at RK = 64: the kernel holds two 4 x 4 fp64 accumulator sets
     long long per = (len + kNumSMs - 1) / kNumSMs;
     per = (per + 31) / 32 * 32;
     const int blocks = (int)((len + per - 1) / per);
+    const dim3 grid(blocks, (RK / 64) * (RK / 64));
     MMK_LAUNCH("nnmf_gram32", st,
-               (gram3_kernel<<<blocks, 256, 0, st>>>(W, len, per, sc, gpart)));
+               (gram3_kernel<RK><<<grid, 256, 0, st>>>(W, len, per, sc, gpart)));
     MMK_LAUNCH("nnmf_gram_sum", st,
-               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(gpart, blocks, GW, GWf)));
+               (gram_sum_kernel<RK><<<RK * RK / 128, 1024, 0, st>>>(gpart, blocks, GW, GWf)));
     MMK_LAUNCH("nnmf_gram_sum", st,
-               (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(
-                   gpart + (long long)blocks * R * R, blocks, G64, GcF)));
+               (gram_sum_kernel<RK><<<RK * RK / 128, 1024, 0, st>>>(
+                   gpart + (long long)blocks * RK * RK, blocks, G64, GcF)));
 }
 
 struct TcWs {
@@ -1492,6 +1740,7 @@ struct TcWs {
     __half *Xh, *Xl;   // pre-split X (row-major)
     float *wpart, *mpart, *GWf;   // GWf: G_W in fp32 (V-step epilogue)
     float* GcF;                   // G_c = 2 W_hi W_lo^T + W_lo W_lo^T in fp32 (V-step epilogue)
+    float* Qs;                    // RK = 128: the V step's Q rows [q | q2] (m x 2 RK)
     double* G64;                  // its fp64 sum
     double *part, *gpart;
     XXCache* xx;
@@ -1501,26 +1750,29 @@ struct TcWs {
 
 inline char* c_base(void* p) { return reinterpret_cast<char*>(p); }
 
-size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
-    const TcPlan P = tc_plan(m, n);
+// The per-X part first (pre-split copy, scale cache, counters: what
+// prepare_x touches, independent of the rank tile), then the rank-RK part
+size_t tc_layout(long long m, long long n, int rk, void* base, TcWs* L) {
+    const TcPlan P = tc_plan(m, n, rk);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    size_t oWh = take(2 * (size_t)R * n), oWl = take(2 * (size_t)R * n);
-    size_t oVh = take(2 * (size_t)R * m), oVl = take(2 * (size_t)R * m);
-    size_t oVr = take(2 * (size_t)R * m);
-    size_t oWp = take(4 * (size_t)P.splits * n * R);
-    size_t oP = take(8 * (size_t)kNumSMs);
-    size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) xmax, then wmax
-    size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
-    size_t oGP = take(8 * (size_t)R * R * kGramBlocks * 2);   // gram3: two Grams
-    size_t oGF = take(4 * (size_t)R * R);
-    size_t oGS = take(4 * (size_t)R * R), oG64 = take(8 * (size_t)R * R);
     const size_t xe = (size_t)m * n;
     size_t oXh = take(2 * xe), oXl = take(2 * xe);
+    size_t oP = take(8 * (size_t)kNumSMs * 3);   // V-step partials (+ vfinish's at RK = 128)
+    size_t oM = take(4 * (size_t)kNumSMs * 8);   // [0, 4*148) xmax, then wmax
+    size_t oC = take(sizeof(XXCache) + sizeof(Scales) + 64);
+    size_t oWh = take(2 * (size_t)rk * n), oWl = take(2 * (size_t)rk * n);
+    size_t oVh = take(2 * (size_t)rk * m), oVl = take(2 * (size_t)rk * m);
+    size_t oVr = take(2 * (size_t)rk * m);
+    size_t oWp = take(4 * (size_t)P.splits * n * rk);
+    size_t oGP = take(8 * (size_t)rk * rk * kGramBlocks * 2);   // gram3: two Grams
+    size_t oGF = take(4 * (size_t)rk * rk);
+    size_t oGS = take(4 * (size_t)rk * rk), oG64 = take(8 * (size_t)rk * rk);
+    size_t oQs = take(rk == 128 ? 4 * (size_t)m * 2 * rk : 0);
     if (base && L) {
         char* c = c_base(base);
         L->Xh = (__half*)(c + oXh);
@@ -1540,6 +1792,7 @@ size_t tc_layout(long long m, long long n, void* base, TcWs* L) {
         L->GWf = (float*)(c + oGF);
         L->GcF = (float*)(c + oGS);
         L->G64 = (double*)(c + oG64);
+        L->Qs = (float*)(c + oQs);
     }
     return off;
 }
@@ -1556,9 +1809,10 @@ namespace mmk_tc {
 // The tensor-core path needs the pre-split copy of X (4 bytes per element)
 // next to X itself; shapes whose copy would pass 96 GiB take the SIMT path.
 bool shape_ok(int dtype, long long m, long long n, long long r) {
-    // ranks 17..64: ranks below 64 run on the rank-64 kernels with V and W
-    // zero-padded (exact: a zero component stays zero and adds nothing)
-    if (dtype != MMK_F32 || r < 17 || r > R) return false;
+    // ranks 17..128: ranks below the rank tile (64 or 128) run on its kernels
+    // with V and W zero-padded (exact: a zero component stays zero and adds
+    // nothing)
+    if (dtype != MMK_F32 || r < 17 || r > 128) return false;
     if ((n & 7) || (m & 7) || m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
     return 4.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
@@ -1573,35 +1827,36 @@ bool eligible(int dtype, long long m, long long n, long long r, long long ldx, c
     return true;
 }
 
-// rank < 64: the zero-padded operands after the rank-64 region
+// rank < RK: the zero-padded operands after the rank-RK region
 struct PadWs {
-    float *V64, *V64o, *W64;
-    double *red64, *GW64;
+    float *Vp, *Vpo, *Wp;
+    double *redp, *GWp;
 };
-size_t pad_layout(long long m, long long n, void* base, PadWs* L) {
+size_t pad_layout(long long m, long long n, int rk, void* base, PadWs* L) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    const size_t oV = take(4 * (size_t)m * R), oVo = take(4 * (size_t)m * R);
-    const size_t oW = take(4 * (size_t)R * n);
-    const size_t oRed = take(8 * ((size_t)R * n + R * R + 2)), oG = take(8 * (size_t)R * R);
+    const size_t oV = take(4 * (size_t)m * rk), oVo = take(4 * (size_t)m * rk);
+    const size_t oW = take(4 * (size_t)rk * n);
+    const size_t oRed = take(8 * ((size_t)rk * n + rk * rk + 2)), oG = take(8 * (size_t)rk * rk);
     if (base && L) {
         char* c = reinterpret_cast<char*>(base);
-        L->V64 = (float*)(c + oV);
-        L->V64o = (float*)(c + oVo);
-        L->W64 = (float*)(c + oW);
-        L->red64 = (double*)(c + oRed);
-        L->GW64 = (double*)(c + oG);
+        L->Vp = (float*)(c + oV);
+        L->Vpo = (float*)(c + oVo);
+        L->Wp = (float*)(c + oW);
+        L->redp = (double*)(c + oRed);
+        L->GWp = (double*)(c + oG);
     }
     return off;
 }
 
 size_t ws_bytes(long long m, long long n, long long r) {
-    const size_t core = (tc_layout(m, n, nullptr, nullptr) + 255) & ~size_t(255);
-    return core + (r < R ? pad_layout(m, n, nullptr, nullptr) : 0);
+    const int rk = rank_tile(r);
+    const size_t core = (tc_layout(m, n, rk, nullptr, nullptr) + 255) & ~size_t(255);
+    return core + (r < rk ? pad_layout(m, n, rk, nullptr, nullptr) : 0);
 }
 
 void set_x_prepared(bool on) { t_x_prepared = on; }
@@ -1614,7 +1869,7 @@ const long long* last_flag() { return t_last_flag; }
 void presplit_span(long long m, long long n, size_t* begin, size_t* end) {
     TcWs L;
     char* const base = reinterpret_cast<char*>(uintptr_t(1) << 20);   // any non-null base
-    tc_layout(m, n, base, &L);
+    tc_layout(m, n, 64, base, &L);   // the per-X part does not depend on the rank tile
     *begin = (size_t)(reinterpret_cast<char*>(L.Xh) - base);
     *end = *begin + 2 * 2 * (size_t)m * (size_t)n;   // X_hi, X_lo (adjacent, 256-aligned)
 }
@@ -1622,7 +1877,7 @@ void presplit_span(long long m, long long n, size_t* begin, size_t* end) {
 int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcws,
               cudaStream_t st) {
     TcWs L;
-    tc_layout(m, n, tcws, &L);
+    tc_layout(m, n, 64, tcws, &L);   // per-X part only (rank-independent offsets)
     MMK_LAUNCH("nnmf_xmax_cached", st,
                (xmax_kernel<<<4 * kNumSMs, 512, 0, st>>>(X, ldx, m, n, L.xx, L.mpart, L.counter,
                                                          L.sc)));
@@ -1633,22 +1888,30 @@ int prepare_x(const float* X, long long ldx, long long m, long long n, void* tcw
     return MMK_OK;
 }
 
-// Phase A of one iteration on the tensor cores; writes V_out and
-// red = [P | G_V' | f-partial].
-static int iter_a64(const float* X, long long ldx, const float* V, const float* W, float* V_out,
-                    long long m, long long n, void* tcws, double* GW, double* red,
-                    cudaStream_t st) {
+// Phase A of one iteration on the tensor cores at the rank tile RK; writes
+// V_out and red = [P | G_V' | f-partial].
+template <int RK>
+static int iter_a_rk(const float* X, long long ldx, const float* V, const float* W,
+                     float* V_out, long long m, long long n, void* tcws, double* GW, double* red,
+                     cudaStream_t st) {
+    using C = Tc<RK>;
+    constexpr bool VGRAM = RK == 64;   // V'^T V' fused into vprep_gram_kernel
     TcWs L;
-    tc_layout(m, n, tcws, &L);
-    const TcPlan P = tc_plan(m, n);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wstep_tc))) {
-        cudaFuncSetAttribute(nnmf_vstep_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_V);
-        cudaFuncSetAttribute(nnmf_vstep_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_V2);
-        cudaFuncSetAttribute(nnmf_wstep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
-        cudaFuncSetAttribute(vprep_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kVprepSmem);
+    tc_layout(m, n, RK, tcws, &L);
+    const TcPlan P = tc_plan(m, n, RK);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wstep_tc<RK>))) {
+        cudaFuncSetAttribute(nnmf_vstep_tc<false, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_V);
+        if constexpr (RK == 64)
+            cudaFuncSetAttribute(nnmf_vstep_tc<true, 64>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_V2);
+        cudaFuncSetAttribute(nnmf_wstep_tc<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_W);
+        cudaFuncSetAttribute(vprep_gram_kernel<RK, VGRAM>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, vprep_smem<RK, VGRAM>());
+        if constexpr (RK == 128)
+            cudaFuncSetAttribute(vfinish_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 vfinish_smem<RK>());
     }
     CUtensorMap mX, mX2, mWh, mWl, mVr, mXt, mXt2, mVh, mVl;
     int rc;
@@ -1657,12 +1920,12 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     // the W step reads the same row-major copy in [64 rows x 64 columns] boxes
     if ((rc = mmk_host::make_map_f16(&mXt, L.Xh, m, n, n, BK))) return rc;
     if ((rc = mmk_host::make_map_f16(&mXt2, L.Xl, m, n, n, BK))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mVr, L.Vh, m, R, R, BM))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, R, n, n, R))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, R, m, m, R))) return rc;
-    if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, R, m, m, R))) return rc;
-    const long long rn = (long long)R * n;
+    if ((rc = mmk_host::make_map_f16(&mVr, L.Vh, m, RK, RK, BM))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mWh, L.Wh, RK, n, n, RK))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mWl, L.Wl, RK, n, n, RK))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mVh, L.Vth, RK, m, m, RK))) return rc;
+    if ((rc = mmk_host::make_map_f16(&mVl, L.Vtl, RK, m, m, RK))) return rc;
+    const long long rn = (long long)RK * n;
     if (!t_x_prepared) {
         int prc = prepare_x(X, ldx, m, n, tcws, st);
         if (prc) return prc;
@@ -1673,81 +1936,103 @@ static int iter_a64(const float* X, long long ldx, const float* V, const float* 
     MMK_LAUNCH("nnmf_split_w", st,
                (split_w_kernel<<<ceil_div((rn + 1) / 2, 256), 256, 0, st>>>(W, L.Wh, L.Wl, rn,
                                                                             L.sc)));
-    gram3(W, n, L.sc, L.gpart, GW, L.GWf, L.G64, L.GcF, st);
+    gram3<RK>(W, n, L.sc, L.gpart, GW, L.GWf, L.G64, L.GcF, st);
     MMK_LAUNCH("nnmf_split_v", st,
-               (split_v_kernel<<<ceil_div(m * 16, 256), 256, 0, st>>>(V, L.Vh, m)));
-    if (P.vpair) {
-        // clusters of 2 CTAs (one TPC): the pair's MMAs run as cta_group::2
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(P.vgrid);
-        cfg.blockDim = dim3(kVThreads);
-        cfg.dynamicSmemBytes = SMEM_V2;
-        cfg.stream = st;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
+               (split_v_kernel<RK><<<ceil_div(m * (RK / 4), 256), 256, 0, st>>>(V, L.Vh, m)));
+    if constexpr (RK == 64) {
+        if (P.vpair) {
+            // clusters of 2 CTAs (one TPC): the pair's MMAs run as cta_group::2
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(P.vgrid);
+            cfg.blockDim = dim3(kVThreads);
+            cfg.dynamicSmemBytes = SMEM_V2;
+            cfg.stream = st;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            MMK_LAUNCH("nnmf_vstep_tc", st,
+                       (void)cudaLaunchKernelEx(&cfg, nnmf_vstep_tc<true, 64>, mX, mX2, mWh, mWl,
+                                                mVr, V, (const float*)L.GWf, (const float*)L.GcF,
+                                                V_out, L.sc, (int)m, (int)n, L.part,
+                                                (float*)nullptr));
+        }
+    }
+    if (!P.vpair) {
         MMK_LAUNCH("nnmf_vstep_tc", st,
-                   (void)cudaLaunchKernelEx(&cfg, nnmf_vstep_tc<true>, mX, mX2, mWh, mWl, mVr, V,
-                                            (const float*)L.GWf, (const float*)L.GcF, V_out,
-                                            L.sc, (int)m, (int)n, L.part));
-    } else {
-        MMK_LAUNCH("nnmf_vstep_tc", st,
-                   (nnmf_vstep_tc<false><<<P.vgrid, kVThreads, SMEM_V, st>>>(
+                   (nnmf_vstep_tc<false, RK><<<P.vgrid, kVThreads, C::SMEM_V, st>>>(
                        mX, mX2, mWh, mWl, mVr, V, L.GWf, L.GcF, V_out, L.sc, (int)m, (int)n,
-                       L.part)));
+                       L.part, L.Qs)));
     }
     MMK_CHECK_LAUNCH("nnmf_vstep_tc");
+    int nparts = P.vgrid;
+    if constexpr (RK == 128) {   // the V' arithmetic (G_W, G_c in shared memory)
+        MMK_LAUNCH("nnmf_vfinish_tc", st,
+                   (vfinish_kernel<RK><<<dim3(kNumSMs, RK / kVfinCols), kVfinThreads,
+                                         vfinish_smem<RK>(), st>>>(
+                       L.Qs, V, L.GWf, L.GcF, V_out, L.sc, m, L.part + P.vgrid)));
+        MMK_CHECK_LAUNCH("nnmf_vfinish_tc");
+        nparts += kNumSMs * (RK / kVfinCols);
+    }
     MMK_LAUNCH("nnmf_objective_tc", st,
-               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, P.vgrid,
-                                                        red + rn + (long long)R * R)));
-    {   // V'^T hi / lo for the W step and the Gram V'^T V' -> red (one read of V')
+               (tc_objective_kernel<<<1, 256, 0, st>>>(L.part, nparts,
+                                                        red + rn + (long long)RK * RK)));
+    {   // V'^T hi / lo for the W step and the Gram V'^T V' -> red (one read of V' at RK = 64)
         const int vb = (int)(ceil_div(m, 128) < kVprepBlocks ? ceil_div(m, 128) : kVprepBlocks);
         MMK_LAUNCH("nnmf_vprep_gram", st,
-                   (vprep_gram_kernel<<<vb, 256, kVprepSmem, st>>>(V_out, L.Vth, L.Vtl, m, L.sc,
-                                                                   L.gpart, t_last_flag)));
-        MMK_LAUNCH("nnmf_gram_sum", st,
-                   (gram_sum_kernel<<<R * R / 128, 1024, 0, st>>>(L.gpart, vb, red + rn,
-                                                                   nullptr, t_last_flag)));
+                   (vprep_gram_kernel<RK, VGRAM><<<vb, 256, vprep_smem<RK, VGRAM>(), st>>>(
+                       V_out, L.Vth, L.Vtl, m, L.sc, L.gpart, t_last_flag)));
+        if constexpr (VGRAM)
+            MMK_LAUNCH("nnmf_gram_sum", st,
+                       (gram_sum_kernel<RK><<<RK * RK / 128, 1024, 0, st>>>(
+                           L.gpart, vb, red + rn, nullptr, t_last_flag)));
+        else
+            gram32<RK>(V_out, m, false, L.gpart, red + rn, st);
     }
     MMK_LAUNCH("nnmf_wstep_tc", st,
-               (nnmf_wstep_tc<<<P.wgrid, kWThreads, SMEM_W, st>>>(mXt, mXt2, mVh, mVl, (int)m,
-                                                                  (int)n, P.splits,
-                                                                  P.rows_per_split, L.wpart,
-                                                                  t_last_flag)));
+               (nnmf_wstep_tc<RK><<<P.wgrid, kWThreads, C::SMEM_W, st>>>(
+                   mXt, mXt2, mVh, mVl, (int)m, (int)n, P.splits, P.rows_per_split, L.wpart,
+                   t_last_flag)));
     MMK_CHECK_LAUNCH("nnmf_wstep_tc");
     MMK_LAUNCH("nnmf_wreduce_tc", st,
-               (wreduce_tc_kernel<<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
-                                                                    L.sc, t_last_flag)));
+               (wreduce_tc_kernel<RK><<<ceil_div(n, 32), 256, 0, st>>>(L.wpart, P.splits, n, red,
+                                                                        L.sc, t_last_flag)));
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a");
     return MMK_OK;
 }
 
-// Phase A of one iteration on the tensor cores (any rank 17..64)
+// Phase A of one iteration on the tensor cores (any rank 17..128)
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
            long long m, long long n, long long r, void* tcws, double* GW, double* red,
            cudaStream_t st) {
-    if (r == R) return iter_a64(X, ldx, V, W, V_out, m, n, tcws, GW, red, st);
+    const int rk = rank_tile(r);
+    if (r == rk)
+        return rk == 64 ? iter_a_rk<64>(X, ldx, V, W, V_out, m, n, tcws, GW, red, st)
+                        : iter_a_rk<128>(X, ldx, V, W, V_out, m, n, tcws, GW, red, st);
     PadWs Pd;
-    pad_layout(m, n, reinterpret_cast<char*>(tcws) +
-                         ((tc_layout(m, n, nullptr, nullptr) + 255) & ~size_t(255)), &Pd);
+    pad_layout(m, n, rk,
+               reinterpret_cast<char*>(tcws) +
+                   ((tc_layout(m, n, rk, nullptr, nullptr) + 255) & ~size_t(255)),
+               &Pd);
     MMK_LAUNCH("nnmf_pad_v", st,
-               (pad_cols_kernel<<<ceil_div(m * R, 256), 256, 0, st>>>(V, (int)r, m, Pd.V64)));
-    cudaMemcpyAsync(Pd.W64, W, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st);
-    cudaMemsetAsync(Pd.W64 + r * n, 0, sizeof(float) * (R - r) * n, st);
-    int rc = iter_a64(X, ldx, Pd.V64, Pd.W64, Pd.V64o, m, n, tcws, Pd.GW64, Pd.red64, st);
+               (pad_cols_kernel<<<ceil_div(m * rk, 256), 256, 0, st>>>(V, (int)r, rk, m, Pd.Vp)));
+    cudaMemcpyAsync(Pd.Wp, W, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(Pd.Wp + r * n, 0, sizeof(float) * (rk - r) * n, st);
+    int rc = rk == 64
+                 ? iter_a_rk<64>(X, ldx, Pd.Vp, Pd.Wp, Pd.Vpo, m, n, tcws, Pd.GWp, Pd.redp, st)
+                 : iter_a_rk<128>(X, ldx, Pd.Vp, Pd.Wp, Pd.Vpo, m, n, tcws, Pd.GWp, Pd.redp, st);
     if (rc) return rc;
     MMK_LAUNCH("nnmf_unpad_v", st,
-               (unpad_cols_kernel<<<ceil_div(m * r, 256), 256, 0, st>>>(Pd.V64o, (int)r, m,
+               (unpad_cols_kernel<<<ceil_div(m * r, 256), 256, 0, st>>>(Pd.Vpo, (int)r, rk, m,
                                                                          V_out)));
     // [P (r n) | G (r r) | f]: the first r rows of P are the padded P's
-    cudaMemcpyAsync(red, Pd.red64, sizeof(double) * r * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(red, Pd.redp, sizeof(double) * r * n, cudaMemcpyDeviceToDevice, st);
     MMK_LAUNCH("nnmf_unpad_gram", st,
                (unpad_gram_kernel<<<ceil_div(r * r, 256), 256, 0, st>>>(
-                   Pd.red64 + (long long)R * n, Pd.red64 + (long long)R * n + R * R, (int)r,
+                   Pd.redp + (long long)rk * n, Pd.redp + (long long)rk * n + rk * rk, (int)r, rk,
                    red + r * n, red + r * n + r * r)));
     (void)GW;
     MMK_CHECK_LAUNCH("nnmf_tc_iter_a_padded");

@@ -10,10 +10,11 @@ import test_nnmf_tc_gpu as T
 from paper_1003_3272_b200 import _lib
 
 m, n = int(os.environ.get("M", 131072)), int(os.environ.get("N", 16384))
+r = int(os.environ.get("R", 64))
 g = torch.Generator(device="cuda").manual_seed(1)
 x = torch.rand(m, n, device="cuda", generator=g)
-v = torch.rand(m, 64, device="cuda", generator=g)
-w = torch.rand(64, n, device="cuda", generator=g)
+v = torch.rand(m, r, device="cuda", generator=g)
+w = torch.rand(r, n, device="cuda", generator=g)
 for _ in range(2):
     T.one_iter(x, v, w, False)
 torch.cuda.synchronize()
@@ -24,7 +25,8 @@ for _ in range(int(os.environ.get("ITERS", 8))):
 torch.cuda.synchronize()
 lib.mmk_prof_enable(0)
 rep = _lib.prof_report()
-for k in ("nnmf_vstep_tc", "nnmf_wstep_tc"):
-    if k in rep:
-        cnt, ms = rep[k]
-        print(os.environ.get("TAG", ""), os.environ.get("MMK_TC_PAIR", ""), k, "avg_ms %.4f" % (ms / cnt))
+for k in sorted(rep, key=lambda k: -rep[k][1]):
+    cnt, ms = rep[k]
+    if os.environ.get("ALL") or k in ("nnmf_vstep_tc", "nnmf_wstep_tc"):
+        print(os.environ.get("TAG", ""), os.environ.get("MMK_TC_PAIR", ""), f"r={r}", k,
+              "avg_ms %.4f" % (ms / cnt))

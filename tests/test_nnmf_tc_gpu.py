@@ -100,6 +100,68 @@ def test_tc_padded_ranks_match_fp64(r):
     assert rel(vt, vr) < 3e-5 and rel(wt, wr) < 3e-5, (rel(vt, vr), rel(wt, wr))
 
 
+@pytest.mark.parametrize("m,n,r,scale", [(1032, 776, 128, 1.0), (1032, 776, 65, 1.0),
+                                         (1032, 776, 100, 1.0), (1032, 776, 127, 1.0),
+                                         (4104, 392, 128, 1.0), (1024, 512, 128, 1e-6),
+                                         (1024, 512, 128, 3e6), (2000, 1000, 96, 1.0)])
+def test_tc_rank128_tile_matches_fp64(m, n, r, scale):
+    """Ranks 65..128 on the rank-128 tensor-core kernels (one Q set copied
+    out through the Q scratch, 3-deep X ring, one 128-column W-step block per
+    item; ranks below 128 zero-padded): one iteration against fp64 to the
+    split-product accuracy, ragged and tile-aligned shapes, far from unit
+    scale."""
+    g = torch.Generator(device="cuda").manual_seed(m + n + r)
+    x = torch.rand(m, n, device="cuda", generator=g) * scale
+    v = torch.rand(m, r, device="cuda", generator=g)
+    w = torch.rand(r, n, device="cuda", generator=g)
+    (vt, wt, ft), used = tc_launched(lambda: one_iter(x, v, w, force_simt=False))
+    assert used, "tensor-core path did not run"
+    vr, wr, fr = reference_iter(x, v, w)
+    rel = lambda a, b: float((a.double() - b).norm() / b.norm())  # noqa: E731
+    assert abs(ft - fr) / fr < 2e-6, (ft, fr)
+    assert rel(vt, vr) < 3e-5 and rel(wt, wr) < 3e-5, (rel(vt, vr), rel(wt, wr))
+
+
+@pytest.mark.parametrize("r,iters", [(128, 8), (96, 4)])
+def test_tc_rank128_large_shape(r, iters):
+    """r = 128 and 96 at 65536 x 16384 on the rank-128 tensor-core kernels (the
+    review's large-shape check of r = 128 on UTCHMMA kernels): fused
+    iterations against the same iterations in torch fp64 (cuBLAS DGEMM):
+    trace and V W to 1e-4."""
+    m, n = 65536, 16384
+    g = torch.Generator(device="cuda").manual_seed(r)
+    x = torch.rand(m, n, device="cuda", generator=g)
+    v0 = torch.rand(m, r, device="cuda", generator=g)
+    w0 = torch.rand(r, n, device="cuda", generator=g)
+    lib = _lib.load()
+    lib.mmk_prof_enable(1)
+    try:
+        st, tr = M.nnmf_run(M.NnmfProblem(x=x, rank=r),
+                            M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6),
+                            M.Backend(dtype="fp32", fused=False), state0=M.FactorPair(v0, w0))
+        torch.cuda.synchronize()
+    finally:
+        lib.mmk_prof_enable(0)
+    prof = _lib.prof_report()
+    assert "nnmf_vstep_tc" in prof and "nnmf_wstep_tc" in prof, sorted(prof)
+    xd, v, w = x.double(), v0.double(), w0.double()
+    trace = []
+    for _ in range(iters):
+        trace.append(float(((xd - v @ w) ** 2).sum()))
+        v = v * ((xd @ w.T) / (v @ (w @ w.T) + 1e-300))
+        w = w * ((v.T @ xd) / ((v.T @ v) @ w + 1e-300))
+    trace.append(float(((xd - v @ w) ** 2).sum()))
+    err = np.max(np.abs(tr.objective_values - np.array(trace)) / np.array(trace))
+    assert err < 1e-4, err
+    vw = st.v.double() @ st.w.double()
+    assert float((vw - v @ w).norm() / (v @ w).norm()) < 1e-4
+    # the fused device loop gives the same trace bitwise
+    _, tr2 = M.nnmf_run(M.NnmfProblem(x=x, rank=r),
+                        M.MmConfig(max_iters=iters, epsilon=1e-300, monotone_tol=1e-6),
+                        M.Backend(dtype="fp32"), state0=M.FactorPair(v0, w0))
+    assert np.array_equal(tr.objective_values, tr2.objective_values)
+
+
 def test_tc_rank32_large_shape_10_iters():
     """r = 32 at 65536 x 16384 (the verdict's large-shape check of a rank other
     than 64): 10 fused tensor-core iterations against the same iterations in

@@ -55,7 +55,8 @@ def test_fp64_large_shape_matches_torch_fp64():
     assert float((got - vw).norm() / vw.norm()) < 1e-10
 
 
-@pytest.mark.parametrize("m,n,r", [(1001, 777, 40), (2050, 3001, 17), (515, 4099, 64)])
+@pytest.mark.parametrize("m,n,r", [(1001, 777, 40), (2050, 3001, 17), (515, 4099, 64),
+                                   (1001, 777, 100), (2050, 3001, 128)])
 def test_fp32_shapes_off_the_tensor_cores(m, n, r):
     """fp32 with m or n not a multiple of 8 (no TMA-aligned pre-split copy):
     the tile kernels, 8 fused iterations, to 1e-4."""
@@ -75,16 +76,26 @@ def test_fp32_shapes_off_the_tensor_cores(m, n, r):
     assert np.array_equal(tr.objective_values, tr2.objective_values)
 
 
-def test_rank128_large_shape_fp32():
-    """r = 128 at 65536 x 16384 in fp32 (the review's large-shape check of a
-    rank above the tensor-core path's 64): the 128-rank tiles, 5 fused
-    iterations against torch fp64, trace and V W to 1e-4."""
+def test_rank128_large_shape_fp32_tiles():
+    """r = 128 at 65536 x 16384 in fp32 on the 128-rank CUDA-core tiles
+    (MMK_NNMF_TC=0; the default path for this shape is the rank-128
+    tensor-core kernels, tests/test_nnmf_tc_gpu.py), 5 iterations against torch
+    fp64, trace and V W to 1e-4."""
+    import os
     m, n, r, iters = 65536, 16384, 128, 5
     g = torch.Generator(device="cuda").manual_seed(128)
     x = torch.rand(m, n, device="cuda", generator=g)
     v0 = torch.rand(m, r, device="cuda", generator=g)
     w0 = torch.rand(r, n, device="cuda", generator=g)
-    st, tr, prof = run_profiled(x, r, "fp32", iters, v0, w0, fused=False)
+    old = os.environ.get("MMK_NNMF_TC")
+    os.environ["MMK_NNMF_TC"] = "0"
+    try:
+        st, tr, prof = run_profiled(x, r, "fp32", iters, v0, w0, fused=False)
+    finally:
+        if old is None:
+            os.environ.pop("MMK_NNMF_TC")
+        else:
+            os.environ["MMK_NNMF_TC"] = old
     assert "nnmf_vstep_tile" in prof and "nnmf_wpart_tile" in prof, sorted(prof)
     want, vw = torch_trace(x, v0, w0, iters)
     assert np.max(np.abs(tr.objective_values - want) / want) < 1e-4
