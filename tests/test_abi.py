@@ -55,19 +55,23 @@ def test_sass_has_no_legacy_fallback_symbols():
 
 
 def test_nnmf_tc_workspace_policy():
-    """Only a full-iteration fp32 rank-64 workspace holds the tensor-core region
-    (the pre-split copy of X: fp16 hi / lo, row-major, 4 bytes per element),
-    and only while that copy stays within 96 GiB; fp64, other ranks
-    and the single operations (mmk_nnmf_op_ws_bytes) never reserve it
-    (a zero-filled 16 GiB region per single-op call)."""
+    """Only a full-iteration fp32 workspace of rank 17..128 holds the
+    tensor-core region (the pre-split copy of X: fp16 hi / lo, row-major, 4
+    bytes per element), and only while that copy stays within 96 GiB; fp64,
+    ranks <= 16 and the single operations (mmk_nnmf_op_ws_bytes) never
+    reserve it (a zero-filled 16 GiB region per single-op call)."""
     ws = _lib.ws_bytes
     copy = 4 * 131072 * 16384
     c4 = ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 64)
     assert copy <= c4 < copy + (1 << 30)
     # ranks 17..63 run on the rank-64 kernels (zero-padded): same region
     assert copy <= ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, 32) < copy + (1 << 30)
-    for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 16), (0, 131072, 16384, 65)):
+    for args in ((1, 131072, 16384, 64), (0, 131072, 16384, 16), (1, 131072, 16384, 128)):
         assert ws("mmk_nnmf_ws_bytes", *args) < (1 << 30)
+    # ranks 65..128 run on the rank-128 kernels: the same copy plus the
+    # rank-128 operands and the V step's Q rows (m x 256 fp32, 128 MiB here)
+    for r in (65, 128):
+        assert copy <= ws("mmk_nnmf_ws_bytes", 0, 131072, 16384, r) < copy + (1 << 30)
     assert ws("mmk_nnmf_op_ws_bytes", 0, 131072, 16384, 64) < (1 << 30)
     # 524288 x 65536: the copy would be 128 GiB -- SIMT path, no region
     assert ws("mmk_nnmf_ws_bytes", 0, 524288, 65536, 64) < (1 << 33)
