@@ -2,7 +2,7 @@
 """MM iterations/sec on B200 (BASELINE.json metric), one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload nnmf-large|mds-large|pet-large|nnmf-mid]
+                    [--workload nnmf-large|mds-large|pet-large|nnmf-mid|nnmf-r128]
 
 --gpus N > 1 without a torchrun environment re-launches this script under
 torch.distributed.run with N ranks on this node (one per GPU; on a box with
@@ -41,6 +41,8 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     "nnmf-large": dict(solver="nnmf", m=131072, n=16384, r=64, label="BASELINE config 4"),
+    "nnmf-r128": dict(solver="nnmf", m=131072, n=16384, r=128,
+                      label="BASELINE config 4's X at rank 128 (the rank-128 tensor-core tile)"),
     "nnmf-mid": dict(solver="nnmf", m=16384, n=4096, r=64,
                      label="BASELINE config 4 at 1/32 of the size (CI of the sharded path)"),
     "mds-large": dict(solver="mds", n=65536, dim=3, label="BASELINE config 5"),
@@ -288,7 +290,8 @@ def workload_config(args, W, world=1):
     cfg.update({k: v for k, v in W.items() if k not in ("solver", "label")})
     kind = {"mds": "tiles-sharded", "pet": "replicas"}.get(W["solver"], "rows-sharded")
     cfg["parallelism"] = f"{kind} x{world}" if world > 1 else "single-gpu"
-    cfg["l2"] = ("inputs larger than L2" if args.workload in ("nnmf-large", "mds-large")
+    cfg["l2"] = ("inputs larger than L2" if args.workload in ("nnmf-large", "nnmf-r128",
+                                                               "mds-large")
                  else "L2-resident (no flush: the solver re-reads a cache-sized matrix "
                       "every iteration by design)")
     return cfg
@@ -344,8 +347,13 @@ def bench_nnmf_large(args, torch, world, rank, dev):
     alg = {  # algorithmic HBM bytes per launch
         "nnmf_vstep": ml * n * es + 2 * ml * r * es + r * n * es,
         "nnmf_wpart": ml * n * es + ml * r * es,
-        # X once (as X_hi + X_lo) + V read + V' written + V_h read + W_hi/W_lo chunks
-        "nnmf_vstep_tc": ml * n * 4 + 2 * ml * r * 4 + ml * r * 2 + 2 * r * n * 4,
+        # X once (as X_hi + X_lo) + V read + V' written + V_h read + W_hi/W_lo chunks;
+        # rank 128: the Q rows [q | q2] written instead of V' (nnmf_vfinish_tc
+        # reads them and V, writes V')
+        "nnmf_vstep_tc": (ml * n * 4 + 2 * ml * r * 4 + ml * r * 2 + 2 * r * n * 4 if r <= 64
+                          else ml * n * 4 + ml * r * 4 + ml * r * 2 + 2 * r * n * 4 +
+                          ml * 2 * r * 4),
+        "nnmf_vfinish_tc": ml * 2 * r * 4 + 2 * ml * r * 4,
         # X once + V'_hi/V'_lo read + fp32 split-K partials written
         "nnmf_wstep_tc": ml * n * 4 + 2 * ml * r * 4,
         # CUDA-core tile kernels (ranks 17..64, fp64): algorithmic FLOPs --
@@ -354,7 +362,7 @@ def bench_nnmf_large(args, torch, world, rank, dev):
         "nnmf_wpart_tile": 2 * ml * n * r,
     }
     launches = sum(c for c, _ in prof.values()) // args.steps
-    roof = roofline(prof, alg, "hbm", "dominant")
+    roof = roofline(prof, alg, "hbm", args.workload)
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = nnmf_e2e(args, torch, be, x, v0, w0, r)
@@ -460,7 +468,7 @@ def bench_mds_large(args, torch, world, rank, dev):
     prof = time_steps(args, torch, dev, step, world)["prof"]
     alg = {"mds_tri": (t1 - t0) * 128 * 128 * 4 + 2 * dim * n * 4}
     launches = sum(c for c, _ in prof.values()) // args.steps
-    roof = roofline(prof, alg, "hbm", "dominant")
+    roof = roofline(prof, alg, "hbm", args.workload)
     kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
                for k, (c, ms) in prof.items()}
     mm._check_error()
@@ -535,7 +543,7 @@ def bench_pet_large(args, torch, world, rank, dev):
     alg = {"pet_sfwd": nnz * 8 + (geo.n_rays + 1) * 4 + geo.n_rays * 12,
            "pet_sback_pixel": nnz * 8 + (geo.n_pixels + 1) * 4 + geo.n_pixels * 8}
     launches = sum(c for c, _ in prof.values()) // args.steps
-    roof = roofline(prof, alg, "hbm", "dominant")
+    roof = roofline(prof, alg, "hbm", args.workload)
     kernels = {k: {"launches_per_step": c // args.steps, "avg_ms": ms / c}
                for k, (c, ms) in prof.items()}
     mm._check_error()
@@ -612,7 +620,7 @@ FP64_PEAK_TFLOPS = 40.0
 FLOP_KERNELS = {"nnmf_vstep_tile": True, "nnmf_wpart_tile": True}
 
 
-def roofline(prof, alg, bound, _label):
+def roofline(prof, alg, bound, workload):
     hbm, bf16, kind = peaks()
     name = max(prof, key=lambda k: prof[k][1])
     cnt, ms = prof[name]
@@ -635,7 +643,12 @@ def roofline(prof, alg, bound, _label):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get(name)
+            t = json.load(fh)
+        # per-workload captures ("kernel@workload"); the bare kernel names are
+        # the captures of the headline workloads
+        traffic = t.get(f"{name}@{workload}",
+                        t.get(name) if workload in ("nnmf-large", "mds-large", "pet-large")
+                        else None)
     return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "alg_bytes": alg[name],
             "avg_ms": avg_ms, "peak_kind": kind}
@@ -743,7 +756,7 @@ def run_ours(args):
     from paper_1003_3272_b200 import build as B
     B.build()
     W = WORKLOADS[args.workload]
-    if args.workload in ("nnmf-large", "nnmf-mid"):
+    if args.workload in ("nnmf-large", "nnmf-mid", "nnmf-r128"):
         timing, roof, launches, e2e, extra = bench_nnmf_large(args, torch, world, rank, dev)
     elif args.workload == "mds-large":
         timing, roof, launches, e2e, extra = bench_mds_large(args, torch, world, rank, dev)
