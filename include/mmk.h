@@ -79,7 +79,7 @@ int mmk_prof_report(char *buf, size_t len);
  * The row range is the caller's shard of X/V (rows are independent in the
  * V step; the W step is a sum over rows, hence the all-reduce of `red`).
  * The workspace (prepared by mmk_nnmf_ws_clear, or zero-filled, before first
- * use) caches per-X data of the fp32 tensor-core path (ranks 17..64) -- the
+ * use) caches per-X data of the fp32 tensor-core path (ranks 17..128) -- the
  * scale exponent and the pre-split fp16 hi / lo copy of X (4 bytes per
  * element, row-major; shapes whose copy would pass 96 GiB take the SIMT
  * path) -- keyed by (X, m, n, ldx): clear it again, or use a fresh one, if

@@ -440,7 +440,7 @@ struct Ws {
     double* respart;
     double* wpart;
     double* fscratch;
-    void* tc;                // tensor-core path scratch (fp32 rank 64 only)
+    void* tc;                // tensor-core path scratch (fp32 ranks 17..128)
 };
 
 // the tensor-core region (pre-split X, operand copies) is reserved only for

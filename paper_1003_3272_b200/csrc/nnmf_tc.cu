@@ -1,5 +1,6 @@
 // nnmf_tc.cu -- tensor-core (tcgen05, kind::f16) path of the NNMF MM
-// iteration for large fp32 problems with rank 64 (BASELINE config 4).
+// iteration for large fp32 problems, ranks 17..128 on rank tiles of 64
+// (BASELINE config 4) and 128 (see Tc<RK> below).
 // Reference: nnmf_objective / nnmf_update_v / nnmf_update_w (nnmf.py:75-110)
 // and the V-then-W step of _FrobeniusNnmf (nnmf.py:153-156).
 //

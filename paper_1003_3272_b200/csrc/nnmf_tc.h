@@ -5,13 +5,14 @@
 
 namespace mmk_tc {
 
-// dtype / shape admit the tensor-core path (fp32, rank 64, m and n multiples
+// dtype / shape admit the tensor-core path (fp32, ranks 17..128 on rank tiles
+// of 64 and 128, m and n multiples
 // of 8, >= 128, the pre-split copy of X within its memory cap)
 bool shape_ok(int dtype, long long m, long long n, long long r);
 // ... and this X (row stride, alignment; MMK_NNMF_TC=0 disables the path)
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X);
 size_t ws_bytes(long long m, long long n, long long r);
-// r = 64, or 17..63 on the rank-64 kernels with zero-padded V / W
+// r = 64 / 128, or 17..127 on the rank-64 / rank-128 kernels with zero-padded V / W
 int iter_a(const float* X, long long ldx, const float* V, const float* W, float* V_out,
            long long m, long long n, long long r, void* tcws, double* GW, double* red,
            cudaStream_t st);

@@ -2,7 +2,7 @@
 // iteration for ranks 17..128 (rank tiles of 64 or 128): the fp64 path at any
 // shape (BASELINE config 4
 // in fp64: 131072 x 16384, r = 64) and fp32 shapes the tensor-core path does
-// not take (nnmf_tc.cu: ranks 17..64, TMA-aligned shapes).  Reference: nnmf_objective / nnmf_update_v /
+// not take (nnmf_tc.cu: fp32 ranks 17..128, TMA-aligned shapes).  Reference: nnmf_objective / nnmf_update_v /
 // nnmf_update_w (nnmf.py:75-110).
 //
 // The warp-per-row kernels of nnmf.cu keep a row's r dot products in

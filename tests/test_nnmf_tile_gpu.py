@@ -1,4 +1,4 @@
-"""Register-blocked CUDA-core NNMF kernels for ranks 17..64
+"""Register-blocked CUDA-core NNMF kernels for ranks 17..128
 (csrc/nnmf_tile.cu): fp64 at a large shape and fp32 shapes the tensor-core
 path does not take, against the same iterations in torch fp64 (cuBLAS DGEMM,
 not our kernels); the grouping of the reference (nnmf.py:84-110) up to
