@@ -1,7 +1,7 @@
 // nnmf_poisson.cu -- NNMF under the Poisson log fit (reference nnmf.py:178-265),
 // the square-root multiplicative MM updates, CUDA cores (FFMA / DFMA).
 //
-// One MM iteration from (V, W), X m x n, rank r <= 64:
+// One MM iteration from (V, W), X m x n, rank r <= 128 (ranks above 16 on nnmf_tile.cu):
 //   pois_wsum_kernel    ws_k = sum_j w_kj                         (fp64)
 //   pois_vstep_kernel   per row i of X (one warp per row pair, W chunks in smem):
 //                         b_ij = v_i . w_j, ratio = x_ij / b_ij (x_ij > 0, else 0),
@@ -28,7 +28,7 @@ using namespace mmk;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxPoisRank = 64;
+constexpr int kMaxPoisRank = 128;
 
 // ws_k = sum_j w_kj: one block per k, fixed-shape tree
 template <typename T>
@@ -317,31 +317,36 @@ int run_a(const Args& a) {
     }
     MMK_LAUNCH("pois_wsum", st,
                (pois_wsum_kernel<T><<<a.r, 256, 0, st>>>(W, a.n, L.wsum)));
-    const bool tile = RMAX > 16 && mmk_tile::applies(a.r);   // ranks 17..64: nnmf_tile.cu
-    if (tile)
+    const bool tile = RMAX > 16 && mmk_tile::applies(a.r);   // ranks 17..128: nnmf_tile.cu
+    int S = P.S;
+    if constexpr (RMAX > 64) {   // ranks above 64 always take the tiles
+        if (!tile) return MMK_E_SHAPE;
+    }
+    if (tile) {
         mmk_tile::pois_vstep<T>(X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter,
                                 f_out, a.err, st);
-    else if (RMAX <= 16 && P.rpw == 2)
-        MMK_LAUNCH("pois_vstep", st,
-                   (pois_vstep_kernel<T, RMAX, 2><<<P.nvb, kThreads, 0, st>>>(
-                       X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter, f_out,
-                       a.err)));
-    else
-        MMK_LAUNCH("pois_vstep", st,
-                   (pois_vstep_kernel<T, RMAX, 1><<<P.nvb, kThreads, 0, st>>>(
-                       X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter, f_out,
-                       a.err)));
+    } else if constexpr (RMAX <= 64) {
+        if (RMAX <= 16 && P.rpw == 2)
+            MMK_LAUNCH("pois_vstep", st,
+                       (pois_vstep_kernel<T, RMAX, 2><<<P.nvb, kThreads, 0, st>>>(
+                           X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter, f_out,
+                           a.err)));
+        else
+            MMK_LAUNCH("pois_vstep", st,
+                       (pois_vstep_kernel<T, RMAX, 1><<<P.nvb, kThreads, 0, st>>>(
+                           X, a.ldx, V, W, L.wsum, Vo, a.m, a.n, a.r, L.fpart, L.counter, f_out,
+                           a.err)));
+    }
     MMK_CHECK_LAUNCH("pois_vstep");
     MMK_LAUNCH("pois_colsum", st,
                (pois_colsum_kernel<T><<<P.csb, 256, 0, st>>>(Vo, a.m, a.r, P.csr, L.cpart)));
     MMK_LAUNCH("pois_colsum_reduce", st,
-               (pois_colsum_reduce_kernel<<<1, 64, 0, st>>>(L.cpart, P.csb, a.r, a.red + rn)));
-    int S = P.S;
+               (pois_colsum_reduce_kernel<<<1, 128, 0, st>>>(L.cpart, P.csb, a.r, a.red + rn)));
     if (tile) {
         S = mmk_tile::wpart_splits<T>(a.m, a.n, P.S);
         mmk_tile::pois_wpart<T>(X, a.ldx, Vo, W, a.m, a.n, a.r, S, S > 1 ? L.wpart : a.red,
                                 a.err, st);
-    } else {
+    } else if constexpr (RMAX <= 64) {
         dim3 grid(P.colblocks, P.S);
         double* dst = P.S > 1 ? L.wpart : a.red;
         MMK_LAUNCH("pois_wpart", st,
@@ -362,7 +367,8 @@ int dispatch(const Args& a) {
     if (a.r <= 8) return run_a<T, 8>(a);
     if (a.r <= 16) return run_a<T, 16>(a);
     if (a.r <= 32) return run_a<T, 32>(a);
-    return run_a<T, 64>(a);
+    if (a.r <= 64) return run_a<T, 64>(a);
+    return run_a<T, 128>(a);
 }
 
 int check(int dtype, long long m, long long n, long long r, long long ldx, size_t ws_bytes) {

@@ -298,7 +298,7 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 }
 
 // ---------------------------------------------------------------------------
-// Poisson loss (nnmf.py:178-265), ranks 17..64, the contract of
+// Poisson loss (nnmf.py:178-265), ranks 17..128 (rank tiles of 64 and 128), the contract of
 // pois_vstep_kernel / pois_wpart_kernel (nnmf_poisson.cu): per X chunk the
 // reconstruction b = v.w of every element (K = r, as the residual above), the
 // objective terms x ln b - b, and the ratio x / b (0 where x = 0) written over
@@ -306,13 +306,13 @@ nnmf_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 // X; v' = v sqrt(q / (sum_j w_kj + 1e-300)).  A zero b under a positive count
 // flags site 1 (objective class) in the V step, site 2 (update only) in the W
 // step.
-template <typename T>
+template <typename T, int RK>
 __global__ void __launch_bounds__(TT)
 pois_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                 const T* __restrict__ W, const double* __restrict__ wsum, T* __restrict__ Vout,
                 long long m, long long n, int r, double* __restrict__ fpart,
                 unsigned int* counter, double* f_out, int64_t* err) {
-    constexpr int RK = 64, RJ = 4;
+    constexpr int RJ = RK / 16;   // ranks per thread (tx + 16 j)
     extern __shared__ __align__(16) unsigned char tile_smem[];
     VSmem<T, RK>& S = *reinterpret_cast<VSmem<T, RK>*>(tile_smem);
     __shared__ double sc[32];
@@ -436,44 +436,48 @@ pois_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
 }
 
-template <typename T>
+template <typename T, int RK>
 struct PWSmem {
-    T vs[TK][64 + 16 / sizeof(T)];   // V' chunk [row][rank]
+    T vs[TK][RK + 16 / sizeof(T)];   // V' chunk [row][rank]
     T xs[TK][TC + 1];                // X chunk [row][col], then the ratios
-    T wt[64][TC + 1];                // W [rank][col] of this column block (resident)
+    T wt[RK][TC + 1];                // W [rank][col] of this column block (resident)
 };
 
-template <typename T>
+template <typename T, int RK>
 __global__ void __launch_bounds__(TT)
 pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                 const T* __restrict__ W, long long m, long long n, int r,
                 long long rows_per_split, double* __restrict__ out, int64_t* err) {
-    constexpr int RI = 4;
+    constexpr int RI = RK / 16;   // ranks per thread (RI ty + i)
+    constexpr int VH = RK / 64;   // V' values per thread and row (ranks lc + 64 h)
     extern __shared__ __align__(16) unsigned char tile_smem[];
-    PWSmem<T>& S = *reinterpret_cast<PWSmem<T>*>(tile_smem);
+    PWSmem<T, RK>& S = *reinterpret_cast<PWSmem<T, RK>*>(tile_smem);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const long long c0 = (long long)blockIdx.x * TC;
     const long long lo = (long long)blockIdx.y * rows_per_split;
     const long long hi = lo + rows_per_split < m ? lo + rows_per_split : m;
-    for (int e = tid; e < 64 * TC; e += TT) {
+    for (int e = tid; e < RK * TC; e += TT) {
         const int k = e / TC, cc = e % TC;
         S.wt[k][cc] = (k < r && c0 + cc < n) ? W[(long long)k * n + c0 + cc] : T(0);
     }
     const int lr = tid >> 6, lc = tid & 63;
-    T xr[8], vr[8];
+    T xr[8], vr[8][VH];
     auto load = [&](long long i0) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const long long i = i0 + lr + 4 * u;
             xr[u] = (i < hi && c0 + lc < n) ? X[i * ldx + c0 + lc] : T(0);
-            vr[u] = (i < hi && lc < r) ? V[i * r + lc] : T(0);
+#pragma unroll
+            for (int h = 0; h < VH; ++h)
+                vr[u][h] = (i < hi && lc + 64 * h < r) ? V[i * r + lc + 64 * h] : T(0);
         }
     };
     auto store = [&]() {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             S.xs[lr + 4 * u][lc] = xr[u];
-            S.vs[lr + 4 * u][lc] = vr[u];
+#pragma unroll
+            for (int h = 0; h < VH; ++h) S.vs[lr + 4 * u][lc + 64 * h] = vr[u][h];
         }
     };
     T acc[RI][4];
@@ -499,7 +503,7 @@ pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
             if (x > T(0)) {
                 T b = T(0);
 #pragma unroll 8
-                for (int k = 0; k < 64; ++k) b = fma(S.vs[rl][k], S.wt[k][lc], b);
+                for (int k = 0; k < RK; ++k) b = fma(S.vs[rl][k], S.wt[k][lc], b);
                 if (b == T(0))
                     flag_error(err, MMK_E_NUMERICS, err_at_update(2, (i0 + rl) * n + c0 + lc));
                 else
@@ -511,7 +515,13 @@ pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 #pragma unroll 8
         for (int kk = 0; kk < TK; ++kk) {
             T a[RI], b[4];
-            ld4<T>(&S.vs[kk][RI * ty], a);   // ranks RI ty .. (warp broadcast)
+#pragma unroll
+            for (int h = 0; h < RI / 4; ++h) {   // ranks RI ty .. (warp broadcast)
+                T a4[4];
+                ld4<T>(&S.vs[kk][RI * ty + 4 * h], a4);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[4 * h + i] = a4[i];
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = S.xs[kk][tx + 16 * j];
 #pragma unroll
@@ -601,31 +611,50 @@ void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int 
         wpart_rk<T, 128>(X, ldx, V, m, n, r, S, out, st);
 }
 
+template <typename T, int RK>
+void pois_vstep_rk(const T* X, long long ldx, const T* V, const T* W, const double* wsum,
+                   T* Vout, long long m, long long n, int r, double* fpart, unsigned int* counter,
+                   double* f_out, int64_t* err, cudaStream_t st) {
+    const size_t smem = sizeof(VSmem<T, RK>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_vstep_tile<T, RK>)))
+        cudaFuncSetAttribute(pois_vstep_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    MMK_LAUNCH("pois_vstep_tile", st,
+               (pois_vstep_tile<T, RK><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                   X, ldx, V, W, wsum, Vout, m, n, r, fpart, counter, f_out, err)));
+}
+
 template <typename T>
 void pois_vstep(const T* X, long long ldx, const T* V, const T* W, const double* wsum, T* Vout,
                 long long m, long long n, int r, double* fpart, unsigned int* counter,
                 double* f_out, int64_t* err, cudaStream_t st) {
-    const size_t smem = sizeof(VSmem<T, 64>);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_vstep_tile<T>)))
-        cudaFuncSetAttribute(pois_vstep_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (r <= 64)
+        pois_vstep_rk<T, 64>(X, ldx, V, W, wsum, Vout, m, n, r, fpart, counter, f_out, err, st);
+    else
+        pois_vstep_rk<T, 128>(X, ldx, V, W, wsum, Vout, m, n, r, fpart, counter, f_out, err, st);
+}
+
+template <typename T, int RK>
+void pois_wpart_rk(const T* X, long long ldx, const T* V, const T* W, long long m, long long n,
+                   int r, int S, double* out, int64_t* err, cudaStream_t st) {
+    const size_t smem = sizeof(PWSmem<T, RK>);
+    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_wpart_tile<T, RK>)))
+        cudaFuncSetAttribute(pois_wpart_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-    MMK_LAUNCH("pois_vstep_tile", st,
-               (pois_vstep_tile<T><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
-                   X, ldx, V, W, wsum, Vout, m, n, r, fpart, counter, f_out, err)));
+    const long long rps = (m + S - 1) / S;
+    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
+    MMK_LAUNCH("pois_wpart_tile", st,
+               (pois_wpart_tile<T, RK><<<grid, TT, smem, st>>>(X, ldx, V, W, m, n, r, rps, out,
+                                                                err)));
 }
 
 template <typename T>
 void pois_wpart(const T* X, long long ldx, const T* V, const T* W, long long m, long long n,
                 int r, int S, double* out, int64_t* err, cudaStream_t st) {
-    const size_t smem = sizeof(PWSmem<T>);
-    if (mmk_host::first_on_device(reinterpret_cast<const void*>(pois_wpart_tile<T>)))
-        cudaFuncSetAttribute(pois_wpart_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    const long long rps = (m + S - 1) / S;
-    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
-    MMK_LAUNCH("pois_wpart_tile", st,
-               (pois_wpart_tile<T><<<grid, TT, smem, st>>>(X, ldx, V, W, m, n, r, rps, out,
-                                                            err)));
+    if (r <= 64)
+        pois_wpart_rk<T, 64>(X, ldx, V, W, m, n, r, S, out, err, st);
+    else
+        pois_wpart_rk<T, 128>(X, ldx, V, W, m, n, r, S, out, err, st);
 }
 
 template void pois_vstep<float>(const float*, long long, const float*, const float*,

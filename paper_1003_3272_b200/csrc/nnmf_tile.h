@@ -21,7 +21,7 @@ template <typename T>
 void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
            double* out, cudaStream_t st);
 
-// Poisson loss (ranks 17..64): the fused V step (objective x ln b - b, ratio
+// Poisson loss (ranks 17..128): the fused V step (objective x ln b - b, ratio
 // x / b, v' = v sqrt(q / wsum)) and P = V'^T (X / (V' W)) over S row splits
 template <typename T>
 void pois_vstep(const T* X, long long ldx, const T* V, const T* W, const double* wsum, T* Vout,

@@ -143,11 +143,15 @@ def torch_poisson(x, v, w, iters):
 
 @pytest.mark.parametrize("dtype,tol,m,n,r", [("fp64", 1e-10, 2050, 3001, 40),
                                              ("fp64", 1e-10, 1000, 777, 64),
-                                             ("fp32", 1e-4, 16384, 8192, 64)])
+                                             ("fp32", 1e-4, 16384, 8192, 64),
+                                             ("fp64", 1e-10, 1000, 777, 100),
+                                             ("fp64", 1e-10, 2050, 1001, 128),
+                                             ("fp32", 1e-4, 8192, 4096, 128)])
 def test_poisson_tiles_match_torch(dtype, tol, m, n, r):
-    """Poisson NNMF on the tile kernels (ranks 17..64; the warp-per-row kernels
-    spilled at r = 64: 58.6 ms per V step at 32768 x 8192), count-like data
-    with zeros, 5 iterations against torch fp64."""
+    """Poisson NNMF on the tile kernels (ranks 17..128, rank tiles of 64 and
+    128; the warp-per-row kernels spilled at r = 64: 58.6 ms per V step at
+    32768 x 8192), count-like data with zeros, 5 iterations against torch
+    fp64."""
     iters = 5
     tdt = torch.float64 if dtype == "fp64" else torch.float32
     g = torch.Generator(device="cuda").manual_seed(m + r)
