@@ -27,6 +27,8 @@
 //                    CTA, K = 32 rows per chunk, partials [split][r][n] in
 //                    fp64 (reduced in split order by nnmf_wreduce_kernel)
 // Both sum in a fixed order: deterministic run to run.
+#include <type_traits>
+
 #include "mmk_common.cuh"
 #include "nnmf_tile.h"
 
@@ -199,6 +201,169 @@ nnmf_vstep_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
                     Vout[row * r + k] = (T)(vk * ((double)q[i][j] / (den[j] + kDenomGuard)));
                 }
             }
+        }
+    }
+    if (!resid) return;
+    const double bs = block_sum(res, sc);
+    if (tid == 0) respart[blockIdx.x] = bs;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = block_sum_array(respart, gridDim.x, sc);
+        if (tid == 0) *res_out = tot;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 on the FP64 tensor cores (DMMA, mma.sync m8n8k4 .f64): the same CTA
+// tiles, shared-memory layouts and contract as nnmf_vstep_tile /
+// nnmf_wpart_tile, with the three contractions -- Q = X W^T, the residual's
+// V W and P = V'^T X -- as 8 x 8 x 4 fp64 MMAs (exact fp64 products, fp64
+// accumulation; the order of the K sums differs from the FMA kernels only by
+// rounding).  Fragments (PTX m8n8k4 .f64, lane = 4 g + t): A[g][t], B[t][g],
+// C[g][2t + {0, 1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int RK>
+__global__ void __launch_bounds__(TT)
+nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __restrict__ V,
+                const double* __restrict__ W, const double* __restrict__ GW,
+                double* __restrict__ Vout, long long m, long long n, int r, int flags,
+                double* __restrict__ respart, unsigned int* counter, double* res_out) {
+    using T = double;
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    constexpr int NT = RK / 16;   // Q n-tiles (8 ranks) per warp: warp (wm, wn) = 16 rows x RK/2
+    VSmem<T, RK>& S = *reinterpret_cast<VSmem<T, RK>*>(tile_smem);
+    __shared__ double sc[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
+    const long long row0 = (long long)blockIdx.x * TR;
+    const bool resid = flags & F_RESID;
+    for (int e = tid; e < TR * RK; e += TT) {
+        const int i = e / RK, k = e % RK;
+        S.vt[k][i] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
+    }
+    const int lr = tid >> 5, lc = tid & 31;
+    T xr[8], wr[RK / 8];
+    auto load = [&](long long j0) {
+        const long long j = j0 + lc;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = row0 + lr + 8 * u;
+            xr[u] = (i < m && j < n) ? X[i * ldx + j] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
+            const int k = lr + 8 * u;
+            wr[u] = (k < r && j < n) ? W[(long long)k * n + j] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) S.xt[lc][lr + 8 * u] = xr[u];
+#pragma unroll
+        for (int u = 0; u < RK / 8; ++u) {
+            S.wb[lr + 8 * u][lc] = wr[u];
+            S.wa[lc][lr + 8 * u] = wr[u];
+        }
+    };
+    T q[2][NT][2];   // Q tiles: rows 16 wm + 8 mt + g, ranks wn RK/2 + 8 nt + 2 t + e
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) q[a][b][0] = q[a][b][1] = T(0);
+    double res = 0.0;
+    const long long nch = (n + TK - 1) / TK;
+    load(0);
+    store();
+    __syncthreads();
+    for (long long c = 0; c < nch; ++c) {
+        const long long j0 = c * TK;
+        if (c + 1 < nch) load(j0 + TK);   // in flight while this chunk is consumed
+#pragma unroll 2
+        for (int kk = 0; kk < TK; kk += 4) {
+            T a[2], b[NT];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) a[mt] = S.xt[kk + t][16 * wm + 8 * mt + g];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) b[nt] = S.wa[kk + t][wn * (RK / 2) + 8 * nt + g];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma884(q[mt][nt][0], q[mt][nt][1], a[mt], b[nt]);
+        }
+        if (resid) {   // V W of the chunk: rows 16 wm + 8 mt + g, columns 16 wn + 8 nt + 2 t + e
+            T rec[2][2][2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) rec[a][b][0] = rec[a][b][1] = T(0);
+#pragma unroll 4
+            for (int ks = 0; ks < RK; ks += 4) {
+                T a[2], b[2];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) a[mt] = S.vt[ks + t][16 * wm + 8 * mt + g];
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) b[nt] = S.wb[ks + t][16 * wn + 8 * nt + g];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt)
+                        dmma884(rec[mt][nt][0], rec[mt][nt][1], a[mt], b[nt]);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int il = 16 * wm + 8 * mt + g, jl = 16 * wn + 8 * nt + 2 * t + e;
+                        if (row0 + il < m && j0 + jl < n) {
+                            const double d = S.xt[jl][il] - rec[mt][nt][e];
+                            res = fma(d, d, res);
+                        }
+                    }
+        }
+        __syncthreads();
+        if (c + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+    if (flags & F_UPDATE) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const int il = 16 * wm + 8 * mt + g;
+            const long long row = row0 + il;
+            double den[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) den[nt][0] = den[nt][1] = 0.0;
+            for (int l = 0; l < r; ++l) {
+                const double vl = S.vt[l][il];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int k = wn * (RK / 2) + 8 * nt + 2 * t + e;
+                        if (k < r) den[nt][e] = fma(vl, GW[l * r + k], den[nt][e]);
+                    }
+            }
+            if (row >= m) continue;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int k = wn * (RK / 2) + 8 * nt + 2 * t + e;
+                    if (k >= r) continue;
+                    if (flags & F_GRAD) {   // 2 (V G_W - X W^T)
+                        Vout[row * r + k] = 2.0 * (den[nt][e] - q[mt][nt][e]);
+                    } else {
+                        const double vk = S.vt[k][il];
+                        Vout[row * r + k] = vk * (q[mt][nt][e] / (den[nt][e] + kDenomGuard));
+                    }
+                }
         }
     }
     if (!resid) return;
@@ -548,6 +713,89 @@ pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
     }
 }
 
+// P = V'^T X over a row split on the FP64 tensor cores (see nnmf_vstep_dmma):
+// RK ranks x 64 columns per CTA, warp (wm, wn) = RK/4 ranks x 32 columns.
+template <int RK>
+__global__ void __launch_bounds__(TT)
+nnmf_wpart_dmma(const double* __restrict__ X, long long ldx, const double* __restrict__ V,
+                long long m, long long n, int r, long long rows_per_split,
+                double* __restrict__ out) {
+    using T = double;
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    constexpr int MT = RK / 32;   // m-tiles (8 ranks) per warp
+    WSmem<T, RK>& S = *reinterpret_cast<WSmem<T, RK>*>(tile_smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
+    const long long c0 = (long long)blockIdx.x * TC;
+    const long long lo = (long long)blockIdx.y * rows_per_split;
+    const long long hi = lo + rows_per_split < m ? lo + rows_per_split : m;
+    const int lr = tid >> 6, lc = tid & 63;
+    T xr[8], vr[8][RK / 64];
+    auto load = [&](long long i0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = i0 + lr + 4 * u;
+            xr[u] = (i < hi && c0 + lc < n) ? X[i * ldx + c0 + lc] : T(0);
+#pragma unroll
+            for (int h = 0; h < RK / 64; ++h)
+                vr[u][h] = (i < hi && lc + 64 * h < r) ? V[i * r + lc + 64 * h] : T(0);
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            S.xs[lr + 4 * u][lc] = xr[u];
+#pragma unroll
+            for (int h = 0; h < RK / 64; ++h) S.vs[lr + 4 * u][lc + 64 * h] = vr[u][h];
+        }
+    };
+    T acc[MT][4][2];   // ranks wm RK/4 + 8 mt + g, columns 32 wn + 8 nt + 2 t + e
+#pragma unroll
+    for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = T(0);
+    const long long nch = hi > lo ? (hi - lo + TK - 1) / TK : 0;
+    if (nch > 0) {
+        load(lo);
+        store();
+        __syncthreads();
+    }
+    for (long long c = 0; c < nch; ++c) {
+        if (c + 1 < nch) load(lo + (c + 1) * TK);
+#pragma unroll 2
+        for (int kk = 0; kk < TK; kk += 4) {
+            T a[MT], b[4];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) a[mt] = S.vs[kk + t][wm * (RK / 4) + 8 * mt + g];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) b[nt] = S.xs[kk + t][32 * wn + 8 * nt + g];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                    dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+        }
+        __syncthreads();
+        if (c + 1 < nch) {
+            store();
+            __syncthreads();
+        }
+    }
+    double* o = out + (long long)blockIdx.y * r * n;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int k = wm * (RK / 4) + 8 * mt + g;
+        if (k >= r) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long col = c0 + 32 * wn + 8 * nt + 2 * t + e;
+                if (col < n) o[(long long)k * n + col] = acc[mt][nt][e];
+            }
+    }
+}
+
 }  // namespace
 
 namespace mmk_tile {
@@ -561,6 +809,15 @@ void vstep_rk(const T* X, long long ldx, const T* V, const T* W, const double* G
               long long m, long long n, int r, int flags, double* respart, unsigned int* counter,
               double* res_out, cudaStream_t st) {
     const size_t smem = sizeof(VSmem<T, RK>);
+    if constexpr (std::is_same<T, double>::value) {   // fp64: the DMMA form
+        if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_dmma<RK>)))
+            cudaFuncSetAttribute(nnmf_vstep_dmma<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        MMK_LAUNCH("nnmf_vstep_tile", st,
+                   (nnmf_vstep_dmma<RK><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                       X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out)));
+        return;
+    }
     if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_tile<T, RK>)))
         cudaFuncSetAttribute(nnmf_vstep_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -593,6 +850,16 @@ template <typename T, int RK>
 void wpart_rk(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
               double* out, cudaStream_t st) {
     const size_t smem = sizeof(WSmem<T, RK>);
+    if constexpr (std::is_same<T, double>::value) {   // fp64: the DMMA form
+        if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_dmma<RK>)))
+            cudaFuncSetAttribute(nnmf_wpart_dmma<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        const long long rps = (m + S - 1) / S;
+        dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
+        MMK_LAUNCH("nnmf_wpart_tile", st,
+                   (nnmf_wpart_dmma<RK><<<grid, TT, smem, st>>>(X, ldx, V, m, n, r, rps, out)));
+        return;
+    }
     if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_tile<T, RK>)))
         cudaFuncSetAttribute(nnmf_wpart_tile<T, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

@@ -82,22 +82,24 @@ def test_in_graph_nccl_engine(group, monkeypatch):
     assert np.array_equal(st.v.cpu().numpy(), ref.v)
 
 
-@pytest.mark.parametrize("poisson", [False, True])
-def test_nnmf_sharded_fused_engine_equals_unsharded(group, poisson):
+@pytest.mark.parametrize("poisson,r", [(False, 64), (True, 64), (False, 128), (True, 100)])
+def test_nnmf_sharded_fused_engine_equals_unsharded(group, poisson, r):
     """The public sharded solver on the device-loop engine (Backend(fused=True),
     NCCL group): the all-reduce of the phase-A buffer captured inside the CUDA
     graph, one collective per iteration; bitwise equal to nnmf_run (the graph
-    engine there too: a tensor-core-size problem, so no persistent engine)."""
+    engine there too: a tensor-core-size problem, so no persistent engine).
+    r = 128: the rank-128 tensor-core tile; Poisson r = 100: its 128-rank
+    CUDA-core tiles."""
     rng = np.random.default_rng(14)
     m, n = 2048, 1024
     x = np.floor(rng.random((m, n)) * 5.0) if poisson else rng.random((m, n))
-    v0, w0 = rng.random((m, 64)), rng.random((64, n))
+    v0, w0 = rng.random((m, r)), rng.random((r, n))
     be = Backend(dtype="fp32", fused=True)
     cfg = MmConfig(max_iters=12, epsilon=1e-300, monotone_tol=1e-6)
     xd = torch.tensor(x, dtype=torch.float32, device="cuda")
-    st, tr = P.nnmf_run_sharded(xd, 64, cfg, be, group=group, state0=(v0, w0), poisson=poisson)
+    st, tr = P.nnmf_run_sharded(xd, r, cfg, be, group=group, state0=(v0, w0), poisson=poisson)
     run = M.nnmf_poisson_run if poisson else M.nnmf_run
-    ref, rtr = run(M.NnmfProblem(x=xd, rank=64), cfg, be, state0=M.FactorPair(v0, w0))
+    ref, rtr = run(M.NnmfProblem(x=xd, rank=r), cfg, be, state0=M.FactorPair(v0, w0))
     assert tr.iters == 12
     assert np.array_equal(tr.objective_values, rtr.objective_values)
     assert torch.equal(st.v, ref.v) and torch.equal(st.w, ref.w)
