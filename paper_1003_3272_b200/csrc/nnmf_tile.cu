@@ -226,6 +226,17 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
+// DMMA tiles keep every operand in its natural orientation with rows padded
+// to a stride of 4 (mod 16) doubles: the fragment reads [k + t][base + g] and
+// [base + g][k + t] of a 16-lane phase then hit 16 distinct bank pairs, and
+// the chunk stores (consecutive lanes, consecutive columns) are conflict-free.
+template <int RK>
+struct VSmemD {
+    double xs[TR][TK + 4];   // X chunk [row][col]
+    double wb[RK][TK + 4];   // W chunk [rank][col]
+    double v[TR][RK + 4];    // V tile [row][rank]
+};
+
 template <int RK>
 __global__ void __launch_bounds__(TT)
 nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __restrict__ V,
@@ -235,7 +246,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
     using T = double;
     extern __shared__ __align__(16) unsigned char tile_smem[];
     constexpr int NT = RK / 16;   // Q n-tiles (8 ranks) per warp: warp (wm, wn) = 16 rows x RK/2
-    VSmem<T, RK>& S = *reinterpret_cast<VSmem<T, RK>*>(tile_smem);
+    VSmemD<RK>& S = *reinterpret_cast<VSmemD<RK>*>(tile_smem);
     __shared__ double sc[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
@@ -243,7 +254,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
     const bool resid = flags & F_RESID;
     for (int e = tid; e < TR * RK; e += TT) {
         const int i = e / RK, k = e % RK;
-        S.vt[k][i] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
+        S.v[i][k] = (row0 + i < m && k < r) ? V[(row0 + i) * r + k] : T(0);
     }
     const int lr = tid >> 5, lc = tid & 31;
     T xr[8], wr[RK / 8];
@@ -262,12 +273,9 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
     };
     auto store = [&]() {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) S.xt[lc][lr + 8 * u] = xr[u];
+        for (int u = 0; u < 8; ++u) S.xs[lr + 8 * u][lc] = xr[u];
 #pragma unroll
-        for (int u = 0; u < RK / 8; ++u) {
-            S.wb[lr + 8 * u][lc] = wr[u];
-            S.wa[lc][lr + 8 * u] = wr[u];
-        }
+        for (int u = 0; u < RK / 8; ++u) S.wb[lr + 8 * u][lc] = wr[u];
     };
     T q[2][NT][2];   // Q tiles: rows 16 wm + 8 mt + g, ranks wn RK/2 + 8 nt + 2 t + e
 #pragma unroll
@@ -286,9 +294,9 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
         for (int kk = 0; kk < TK; kk += 4) {
             T a[2], b[NT];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) a[mt] = S.xt[kk + t][16 * wm + 8 * mt + g];
+            for (int mt = 0; mt < 2; ++mt) a[mt] = S.xs[16 * wm + 8 * mt + g][kk + t];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) b[nt] = S.wa[kk + t][wn * (RK / 2) + 8 * nt + g];
+            for (int nt = 0; nt < NT; ++nt) b[nt] = S.wb[wn * (RK / 2) + 8 * nt + g][kk + t];
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -304,7 +312,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
             for (int ks = 0; ks < RK; ks += 4) {
                 T a[2], b[2];
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) a[mt] = S.vt[ks + t][16 * wm + 8 * mt + g];
+                for (int mt = 0; mt < 2; ++mt) a[mt] = S.v[16 * wm + 8 * mt + g][ks + t];
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) b[nt] = S.wb[ks + t][16 * wn + 8 * nt + g];
 #pragma unroll
@@ -321,7 +329,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
                     for (int e = 0; e < 2; ++e) {
                         const int il = 16 * wm + 8 * mt + g, jl = 16 * wn + 8 * nt + 2 * t + e;
                         if (row0 + il < m && j0 + jl < n) {
-                            const double d = S.xt[jl][il] - rec[mt][nt][e];
+                            const double d = S.xs[il][jl] - rec[mt][nt][e];
                             res = fma(d, d, res);
                         }
                     }
@@ -341,7 +349,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) den[nt][0] = den[nt][1] = 0.0;
             for (int l = 0; l < r; ++l) {
-                const double vl = S.vt[l][il];
+                const double vl = S.v[il][l];
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -360,7 +368,7 @@ nnmf_vstep_dmma(const double* __restrict__ X, long long ldx, const double* __res
                     if (flags & F_GRAD) {   // 2 (V G_W - X W^T)
                         Vout[row * r + k] = 2.0 * (den[nt][e] - q[mt][nt][e]);
                     } else {
-                        const double vk = S.vt[k][il];
+                        const double vk = S.v[il][k];
                         Vout[row * r + k] = vk * (q[mt][nt][e] / (den[nt][e] + kDenomGuard));
                     }
                 }
@@ -716,6 +724,11 @@ pois_wpart_tile(const T* __restrict__ X, long long ldx, const T* __restrict__ V,
 // P = V'^T X over a row split on the FP64 tensor cores (see nnmf_vstep_dmma):
 // RK ranks x 64 columns per CTA, warp (wm, wn) = RK/4 ranks x 32 columns.
 template <int RK>
+struct WSmemD {
+    double vs[TK][RK + 4];   // V' chunk [row][rank]
+    double xs[TK][TC + 4];   // X chunk [row][col]
+};
+template <int RK>
 __global__ void __launch_bounds__(TT)
 nnmf_wpart_dmma(const double* __restrict__ X, long long ldx, const double* __restrict__ V,
                 long long m, long long n, int r, long long rows_per_split,
@@ -723,7 +736,7 @@ nnmf_wpart_dmma(const double* __restrict__ X, long long ldx, const double* __res
     using T = double;
     extern __shared__ __align__(16) unsigned char tile_smem[];
     constexpr int MT = RK / 32;   // m-tiles (8 ranks) per warp
-    WSmem<T, RK>& S = *reinterpret_cast<WSmem<T, RK>*>(tile_smem);
+    WSmemD<RK>& S = *reinterpret_cast<WSmemD<RK>*>(tile_smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
     const long long c0 = (long long)blockIdx.x * TC;
@@ -810,11 +823,12 @@ void vstep_rk(const T* X, long long ldx, const T* V, const T* W, const double* G
               double* res_out, cudaStream_t st) {
     const size_t smem = sizeof(VSmem<T, RK>);
     if constexpr (std::is_same<T, double>::value) {   // fp64: the DMMA form
+        const size_t dsm = sizeof(VSmemD<RK>);
         if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_vstep_dmma<RK>)))
             cudaFuncSetAttribute(nnmf_vstep_dmma<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+                                 (int)dsm);
         MMK_LAUNCH("nnmf_vstep_tile", st,
-                   (nnmf_vstep_dmma<RK><<<(unsigned)vstep_blocks(m), TT, smem, st>>>(
+                   (nnmf_vstep_dmma<RK><<<(unsigned)vstep_blocks(m), TT, dsm, st>>>(
                        X, ldx, V, W, GW, Vout, m, n, r, flags, respart, counter, res_out)));
         return;
     }
@@ -851,13 +865,14 @@ void wpart_rk(const T* X, long long ldx, const T* V, long long m, long long n, i
               double* out, cudaStream_t st) {
     const size_t smem = sizeof(WSmem<T, RK>);
     if constexpr (std::is_same<T, double>::value) {   // fp64: the DMMA form
+        const size_t dsm = sizeof(WSmemD<RK>);
         if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_dmma<RK>)))
             cudaFuncSetAttribute(nnmf_wpart_dmma<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+                                 (int)dsm);
         const long long rps = (m + S - 1) / S;
         dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)S);
         MMK_LAUNCH("nnmf_wpart_tile", st,
-                   (nnmf_wpart_dmma<RK><<<grid, TT, smem, st>>>(X, ldx, V, m, n, r, rps, out)));
+                   (nnmf_wpart_dmma<RK><<<grid, TT, dsm, st>>>(X, ldx, V, m, n, r, rps, out)));
         return;
     }
     if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wpart_tile<T, RK>)))
