@@ -91,6 +91,9 @@ constexpr int XSTV = MMK_TC_XSTV;           // V step X ring
 #ifndef MMK_TC_OST
 #define MMK_TC_OST 3
 #endif
+#ifndef MMK_TC_DEFER_R0
+#define MMK_TC_DEFER_R0 0
+#endif
 constexpr int OST = MMK_TC_OST;             // operand ring (V step: one W chunk per X stage,
                                             // held until the residual MMAs finish)
 constexpr int NRES = 8;                     // residual warps (two groups of 4)
@@ -469,27 +472,15 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 tc::mbar_wait(&B.vfull[vb], (p / NVB) & 1);
                 tc::tc_fence_after();
                 const uint64_t va = tc::sdesc_sw128(vbuf + vb * SVHK, 16, 1024);
-                for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XS, rb = it % NRB;
-                    tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
-                    tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
-                    if constexpr (PAIR) tc::mbar_wait(&B.pxfull[xs], (it / XS) & 1);
-                    if (lane == 0) TRACE_AT(1, it);
+                // R0 MMAs of stage s (after its Q MMAs, or -- DEFER -- after the
+                // Q MMAs of stage s + 1 of the same tile, so a late residual
+                // buffer does not hold back the Q stream that frees X slots)
+                auto issue_r0 = [&](int s_it) {
+                    const int os = s_it % OST, rb = s_it % NRB;
+                    tc::mbar_wait(&B.rempty[rb], ((s_it / NRB) & 1) ^ 1);
+                    if (lane == 0) TRACE_AT(3, s_it);
                     tc::tc_fence_after();
                     const uint8_t* ob = oring + os * OSLOT;
-                    if constexpr (PAIR)
-                        issue_split_stage_pair(tmem + b * QW, xring + xs * SX, ob, kb == 0);
-                    else
-                        issue_split_stage_e<RK>(tmem + b * QW, tmem + b * QW + C::ACC,
-                                                xring + xs * SX, ob, kb == 0);
-                    if (lane == 0) TRACE_AT(2, it);
-                    if constexpr (PAIR)
-                        tc::mma_commit_pair_e(&B.xempty[xs]);
-                    else
-                        tc::mma_commit_e(&B.xempty[xs]);
-                    tc::mbar_wait(&B.rempty[rb], ((it / NRB) & 1) ^ 1);
-                    if (lane == 0) TRACE_AT(3, it);
-                    tc::tc_fence_after();
                     const uint64_t wr = tc::sdesc_sw128(ob, PAIR ? SOP : SOPK, 1024);   // MN-major
                     const uint32_t dr = tmem + TM_RES + rb * RW;
 #pragma unroll
@@ -509,8 +500,34 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                         tc::mma_commit_e(&B.rfull[rb]);
                         tc::mma_commit_e(&B.oempty[os]);
                     }
-                    if (lane == 0) TRACE_AT(4, it);
+                    if (lane == 0) TRACE_AT(4, s_it);
+                };
+                constexpr bool DEFER = !PAIR && MMK_TC_DEFER_R0;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int os = it % OST, xs = it % XS;
+                    tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
+                    tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
+                    if constexpr (PAIR) tc::mbar_wait(&B.pxfull[xs], (it / XS) & 1);
+                    if (lane == 0) TRACE_AT(1, it);
+                    tc::tc_fence_after();
+                    const uint8_t* ob = oring + os * OSLOT;
+                    if constexpr (PAIR)
+                        issue_split_stage_pair(tmem + b * QW, xring + xs * SX, ob, kb == 0);
+                    else
+                        issue_split_stage_e<RK>(tmem + b * QW, tmem + b * QW + C::ACC,
+                                                xring + xs * SX, ob, kb == 0);
+                    if (lane == 0) TRACE_AT(2, it);
+                    if constexpr (PAIR)
+                        tc::mma_commit_pair_e(&B.xempty[xs]);
+                    else
+                        tc::mma_commit_e(&B.xempty[xs]);
+                    if constexpr (DEFER) {
+                        if (kb > 0) issue_r0(it - 1);
+                    } else {
+                        issue_r0(it);
+                    }
                 }
+                if constexpr (DEFER) issue_r0(it - 1);
                 if constexpr (PAIR) {
                     tc::mma_commit_pair_e(&B.dfull[b]);
                     tc::mma_commit_pair_e(&B.vempty[vb]);
