@@ -104,7 +104,7 @@ constexpr uint32_t SMEM_V = XSTV * SX + OST * 2 * SOP + 2 * SVH + (MMK_TC_GW_SME
 // pair form: half-size operand slots and G_W read through L1 leave room for a
 // deeper X ring
 #ifndef MMK_TC_XSTV2
-#define MMK_TC_XSTV2 5
+#define MMK_TC_XSTV2 4   // even: see Tc::XS
 #endif
 constexpr int XSTV2 = MMK_TC_XSTV2;
 constexpr int XSMAX = XSTV2 > XSTV ? XSTV2 : XSTV;
@@ -140,16 +140,23 @@ struct Tc {
     static constexpr int ACC = 2 * RK;               // [X.B_hi | X.B_lo] accumulator columns
     static constexpr int NQ = RK == 64 ? 2 : 1;      // V step: Q accumulator sets
     static constexpr int NVB = RK == 64 ? 2 : 1;     // V step: V_h tile buffers
-    static constexpr int XS = RK == 64 ? XSTV : 3;   // V step X ring (single CTA)
+    // V step X ring (single CTA): EVEN, because the two residual groups take
+    // alternate stages -- with an odd depth a group's next use of a slot can
+    // come two phases after its previous one (the other group's stage in
+    // between), and its parity wait would pass on the stale phase
+    static constexpr int XS = RK == 64 ? XSTV : 4;
+    static constexpr int OST = RK == 64 ? MMK_TC_OST : 2;   // V step operand ring
     static constexpr bool GWS = RK == 64 && MMK_TC_GW_SMEM;   // G_W staged in smem
     static constexpr uint32_t QW = 3 * RK;           // single-CTA Q set [hh | hl | lh]
     static constexpr uint32_t SMEM_V =
         XS * SX + OST * 2 * SOP + NVB * SVH + (GWS ? SGW : 0) + 1024;
+    static_assert(XS % 2 == 0, "the residual groups alternate stages: even X ring");
     static constexpr int CB = RK == 64 ? 2 : 1;      // W step: 128-column blocks per item
     static constexpr uint32_t SMEM_W = XST * SX + OSTW * 2 * SOP + 1024;
     static_assert(NQ * QW + NRB * BK <= TM_COLS, "V-step TMEM budget");
     static_assert(2 * CB * ACC <= TM_COLS, "W-step TMEM budget");
     static_assert(SMEM_V + 2048 <= 232448 && SMEM_W + 2048 <= 232448, "shared memory per CTA");
+    static_assert(OST <= ::OST, "VBars holds up to OST operand slots");
 };
 static_assert(Tc<64>::SMEM_V == SMEM_V && Tc<64>::SMEM_W == SMEM_W, "rank-64 layout");
 
@@ -350,12 +357,15 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
     constexpr uint32_t TM_RES = NQ * QW;               // residual buffers after the Q sets
     constexpr int NARR = PAIR ? 8 : 4;                 // arrivals on dempty / rempty
     constexpr int XS = PAIR ? XSTV2 : C::XS;           // X ring depth
+    constexpr int OSL = PAIR ? OST : C::OST;           // operand ring depth
+    static_assert(XS % 2 == 0, "the residual groups alternate stages: even X ring");
+    static_assert(XS <= XSMAX && OSL <= OST, "VBars sizes");
     constexpr bool GWS = !PAIR && C::GWS;              // G_W staged in smem
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = align1024(smem_raw);
     uint8_t* xring = base;
     uint8_t* oring = base + XS * SX;
-    uint8_t* vbuf = oring + OST * OSLOT;
+    uint8_t* vbuf = oring + OSL * OSLOT;
     float* gws = reinterpret_cast<float*>(vbuf + NVB * SVHK);
     __shared__ VBars B;
     __shared__ uint32_t tmem_base;
@@ -379,7 +389,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
             tc::mbar_init(&B.xempty[s], 5);   // the residual group's 4 warps + the Q MMAs' commit
             tc::mbar_init(&B.pxfull[s], 1);   // pair: the peer's forwarder
         }
-        for (int s = 0; s < OST; ++s) {
+        for (int s = 0; s < OSL; ++s) {
             tc::mbar_init(&B.ofull[s], 1);
             tc::mbar_init(&B.oempty[s], 1);
         }
@@ -440,8 +450,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                                         &B.vfull[vb], 64 * a, tile * BM);
                 }
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XS;
-                    tc::mbar_wait(&B.oempty[os], ((it / OST) & 1) ^ 1);
+                    const int os = it % OSL, xs = it % XS;
+                    tc::mbar_wait(&B.oempty[os], ((it / OSL) & 1) ^ 1);
                     if constexpr (PAIR) {   // this CTA's half of [W_hi ; W_lo]
                         if (rank == 0) tc::mbar_expect_tx(&B.ofull[os], 2 * SOP);
                         tc::tma_load_2d_pair(oring + os * OSLOT, rank == 0 ? &mWh : &mWl,
@@ -476,7 +486,7 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 // Q MMAs of stage s + 1 of the same tile, so a late residual
                 // buffer does not hold back the Q stream that frees X slots)
                 auto issue_r0 = [&](int s_it) {
-                    const int os = s_it % OST, rb = s_it % NRB;
+                    const int os = s_it % OSL, rb = s_it % NRB;
                     tc::mbar_wait(&B.rempty[rb], ((s_it / NRB) & 1) ^ 1);
                     if (lane == 0) TRACE_AT(3, s_it);
                     tc::tc_fence_after();
@@ -504,8 +514,8 @@ nnmf_vstep_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CU
                 };
                 constexpr bool DEFER = !PAIR && MMK_TC_DEFER_R0;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int os = it % OST, xs = it % XS;
-                    tc::mbar_wait(&B.ofull[os], (it / OST) & 1);
+                    const int os = it % OSL, xs = it % XS;
+                    tc::mbar_wait(&B.ofull[os], (it / OSL) & 1);
                     tc::mbar_wait(&B.xfull[xs], (it / XS) & 1);
                     if constexpr (PAIR) tc::mbar_wait(&B.pxfull[xs], (it / XS) & 1);
                     if (lane == 0) TRACE_AT(1, it);

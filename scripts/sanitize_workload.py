@@ -53,19 +53,27 @@ def main(which, paths):
         for fused in fused_modes:
             M.nnmf_run(M.NnmfProblem(x=xt, rank=64), cfg, Backend(dtype="fp32", fused=fused),
                        state0=st0)
+        # rank-128 tensor-core tile (one Q set copied out, vfinish_kernel, one
+        # W-step block per item): r = 128 and r = 100 (zero-padded), ragged tiles
+        for r in (128, 100):
+            st1 = M.FactorPair(f32(rng.random((520, r))), f32(rng.random((r, 392))))
+            for fused in fused_modes:
+                M.nnmf_run(M.NnmfProblem(x=xt, rank=r), cfg, Backend(dtype="fp32", fused=fused),
+                           state0=st1)
         xp = np.floor(rng.random((120, 90)) * 5)
         for fused in fused_modes:
             M.nnmf_poisson_run(M.NnmfProblem(x=xp, rank=4), cfg, Backend(dtype="fp32", fused=fused))
-        # register-blocked tiles (round 2): fp64 r = 40 and r = 100, fp32 off the
-        # tensor cores (ragged m, n), Poisson r = 24
+        # register-blocked tiles (round 2): fp64 r = 40 and r = 100 (DMMA), fp32 off
+        # the tensor cores (ragged m, n), Poisson r = 24 and r = 100
         for dt, r in (("fp64", 40), ("fp64", 100), ("fp32", 72)):
             xr = f32(rng.random((131, 97)))
             for fused in fused_modes:
                 M.nnmf_run(M.NnmfProblem(x=xr, rank=r), cfg, Backend(dtype=dt, fused=fused),
                            state0=M.FactorPair(f32(rng.random((131, r))), f32(rng.random((r, 97)))))
-        for fused in fused_modes:
-            M.nnmf_poisson_run(M.NnmfProblem(x=np.floor(rng.random((130, 70)) * 4), rank=24), cfg,
-                               Backend(dtype="fp64", fused=fused))
+        for pr in (24, 100):
+            for fused in fused_modes:
+                M.nnmf_poisson_run(M.NnmfProblem(x=np.floor(rng.random((130, 70)) * 4), rank=pr),
+                                   cfg, Backend(dtype="fp64", fused=fused))
         # fp64 single ops in the reference's order (nnmf_ref.cu)
         vv, ww = rng.random((300, 10)), rng.random((10, 200))
         M.nnmf_update_v(x, vv, ww, backend=Backend(dtype="fp64"))
