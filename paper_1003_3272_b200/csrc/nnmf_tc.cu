@@ -91,6 +91,12 @@ constexpr int XSTV = MMK_TC_XSTV;           // V step X ring
 #ifndef MMK_TC_OST
 #define MMK_TC_OST 3
 #endif
+#ifndef MMK_TC_XS128   // rank-128 tile: X ring / operand ring depths (224 KB of smem)
+#define MMK_TC_XS128 4
+#endif
+#ifndef MMK_TC_OST128
+#define MMK_TC_OST128 2
+#endif
 #ifndef MMK_TC_DEFER_R0
 #define MMK_TC_DEFER_R0 0
 #endif
@@ -144,8 +150,8 @@ struct Tc {
     // alternate stages -- with an odd depth a group's next use of a slot can
     // come two phases after its previous one (the other group's stage in
     // between), and its parity wait would pass on the stale phase
-    static constexpr int XS = RK == 64 ? XSTV : 4;
-    static constexpr int OST = RK == 64 ? MMK_TC_OST : 2;   // V step operand ring
+    static constexpr int XS = RK == 64 ? XSTV : MMK_TC_XS128;
+    static constexpr int OST = RK == 64 ? MMK_TC_OST : MMK_TC_OST128;   // V step operand ring
     static constexpr bool GWS = RK == 64 && MMK_TC_GW_SMEM;   // G_W staged in smem
     static constexpr uint32_t QW = 3 * RK;           // single-CTA Q set [hh | hl | lh]
     static constexpr uint32_t SMEM_V =
