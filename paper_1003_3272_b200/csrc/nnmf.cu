@@ -431,6 +431,7 @@ struct Plan {
     int S;                   // W-step row splits
     long long rows_per_split;
     int colblocks;
+    int Sd;                  // fp64 DMMA W part: max row splits (partial buffer bound)
 };
 
 struct Ws {
@@ -475,6 +476,7 @@ Plan make_plan(long long m, long long n, int r) {
     if (S < 1) S = 1;
     P.rows_per_split = ceil_div(m > 0 ? m : 1, S);
     P.S = ceil_div(m > 0 ? m : 1, P.rows_per_split);
+    P.Sd = mmk_tile::applies(r) ? mmk_tile::kDmmaMaxSplits : 1;
     return P;
 }
 
@@ -493,7 +495,8 @@ size_t ws_layout(const Plan& P, long long m, long long n, int r, bool tc, void* 
     size_t o_gp = take(sizeof(double) * rr * gblocks);
     size_t o_rp = take(sizeof(double) * (size_t)P.nvb);
     size_t o_f = take(sizeof(double) * 4);
-    size_t o_wp = take(P.S > 1 ? sizeof(double) * (size_t)P.S * r * (size_t)n : 0);
+    const int sw = P.S > P.Sd ? P.S : P.Sd;   // split-K partials (SIMT / FMA tiles, or DMMA)
+    size_t o_wp = take(sw > 1 ? sizeof(double) * (size_t)sw * r * (size_t)n : 0);
     size_t o_tc = take(tc ? mmk_tc::ws_bytes(m, n, r) : 0);
     if (base && L) {
         L->tc = reinterpret_cast<char*>(base) + o_tc;
@@ -585,7 +588,9 @@ struct K {
     static void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r,
                       const Plan& P, const Ws& L, double* red, cudaStream_t st) {
         if (RMAX > 16 && mmk_tile::applies(r)) {   // ranks 17..128: nnmf_tile.cu
-            const int S = mmk_tile::wpart_splits<T>(m, n, P.S);
+            const int S = std::is_same<T, double>::value
+                              ? mmk_tile::wpart_splits_dmma(m, n, r, P.Sd)
+                              : mmk_tile::wpart_splits<T>(m, n, P.S);
             mmk_tile::wpart<T>(X, ldx, V, m, n, r, S, S > 1 ? L.wpart : red, st);
             if (S > 1) {
                 const long long len = (long long)r * n;

@@ -860,6 +860,26 @@ int wpart_splits(long long m, long long n, int max_splits) {
     return S < 1 ? 1 : (int)S;
 }
 
+int wpart_splits_dmma(long long m, long long n, int r, int max_splits) {
+    // resident CTAs per SM: rank tile 64 -> 2 (35 KB smem, 94 registers), 128 -> 1
+    const long long slots = (long long)kNumSMs * (r <= 64 ? 2 : 1);
+    const long long cb = (n + TC - 1) / TC;
+    const long long smax = (m + 4 * TK - 1) / (4 * TK);   // >= 4 row chunks per CTA
+    int best = 1;
+    double best_t = 1e300;
+    for (int S = 1; S <= max_splits && S <= smax; ++S) {
+        // a CTA covers m / S rows: time ~ waves * m / S, plus the S r n fp64
+        // partials written and read back (relative to one pass over X)
+        const long long waves = (cb * S + slots - 1) / slots;
+        const double t = (double)waves / S + 2.0 * S * (double)r / (double)m;
+        if (t < best_t - 1e-12) {
+            best_t = t;
+            best = S;
+        }
+    }
+    return best;
+}
+
 template <typename T, int RK>
 void wpart_rk(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
               double* out, cudaStream_t st) {

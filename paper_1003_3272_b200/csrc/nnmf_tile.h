@@ -17,6 +17,10 @@ void vstep(const T* X, long long ldx, const T* V, const T* W, const double* GW, 
 // P = V^T X split over S row ranges -> out[S][r][n] (S = 1: the final P)
 template <typename T>
 int wpart_splits(long long m, long long n, int max_splits);
+// fp64 (DMMA) Frobenius W part: S chosen by wave efficiency over the
+// resident CTA slots plus the partial traffic, S <= max_splits
+int wpart_splits_dmma(long long m, long long n, int r, int max_splits);
+constexpr int kDmmaMaxSplits = 16;
 template <typename T>
 void wpart(const T* X, long long ldx, const T* V, long long m, long long n, int r, int S,
            double* out, cudaStream_t st);
