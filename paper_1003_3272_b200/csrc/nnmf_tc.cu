@@ -854,25 +854,29 @@ split_v_kernel(const float* __restrict__ V, __half* __restrict__ Vh, long long m
 // same terms) as a pass over the [q | q2] rows the V step copied out.  Block
 // (x, y) takes the 64 columns y * 64 .. of every 256-row tile x, x + gridDim.x,
 // ...: that half of G_W and G_c (fp32, 64 KB) and the tile of V (coalesced
-// load, padded rows, 132 KB) are staged in shared memory; a thread per row,
-// so every G read is a warp-wide broadcast and every V read hits 32 distinct
-// banks.  V' = V Q / (V G_W + 1e-300), the correction terms of f for V's fp16
-// rounding and the W_lo part of the residual -> part[y gridDim.x + x] (fixed
-// order), max V' -> sc->vmax_bits.
-constexpr int kVfinThreads = 256;
+// load, 133 KB) are staged in shared memory.  Two threads per row -- lanes l
+// and l + 16 of a warp -- split the rank sums by parity of the rank index and
+// combine them with one shuffle per 8-column chunk; the V rows are padded to a
+// stride of 2 (mod 32) words so the two halves read even / odd banks, and the
+// G reads are broadcasts (two rows of G per warp load).  V' = V Q / (V G_W +
+// 1e-300), the correction terms of f for V's fp16 rounding and the W_lo part
+// of the residual -> part[y gridDim.x + x] (fixed order), max V' ->
+// sc->vmax_bits.
+constexpr int kVfinThreads = 512;
+constexpr int kVfinRows = kVfinThreads / 2;
 constexpr int kVfinCols = 64;
 template <int RK>
 constexpr uint32_t vfinish_smem() {
-    return (2 * RK * kVfinCols + kVfinThreads * (RK + 1)) * 4;
+    return (2 * RK * kVfinCols + kVfinRows * (RK + 2)) * 4;
 }
 template <int RK>
 __global__ void __launch_bounds__(kVfinThreads, 1)
 vfinish_kernel(const float* __restrict__ Qs, const float* __restrict__ V,
                const float* __restrict__ GWf, const float* __restrict__ Gc,
                float* __restrict__ Vout, Scales* sc, long long m, double* __restrict__ part) {
-    constexpr int ROWS = kVfinThreads, NC = kVfinCols;
+    constexpr int ROWS = kVfinRows, NC = kVfinCols, VS = RK + 2;
     extern __shared__ __align__(16) float fsm[];
-    float* vt = fsm + 2 * RK * NC;   // [ROWS][RK + 1]
+    float* vt = fsm + 2 * RK * NC;   // [ROWS][RK + 2]
     const int cb = (int)blockIdx.y * NC;   // first column of this block's half
     for (int i = threadIdx.x; i < RK * NC / 4; i += kVfinThreads) {
         const int l = i / (NC / 4), c4 = (i % (NC / 4)) * 4;
@@ -883,6 +887,8 @@ vfinish_kernel(const float* __restrict__ Qs, const float* __restrict__ V,
     }
     const uint32_t gw_s = tc::smem_u32(fsm), gc_s = tc::smem_u32(fsm + RK * NC);
     const double qscale = exp2(-(double)(sc->ex + sc->ew));
+    const int lane = threadIdx.x & 31, h = lane >> 4;           // rank parity of this thread
+    const int rl = (threadIdx.x >> 5) * 16 + (lane & 15);        // row in the tile
     double acc = 0.0;
     float vmax = 0.f;
     for (long long r0 = (long long)blockIdx.x * ROWS; r0 < m; r0 += (long long)gridDim.x * ROWS) {
@@ -891,28 +897,29 @@ vfinish_kernel(const float* __restrict__ Qs, const float* __restrict__ V,
             const int rr = i / (RK / 4), c4 = (i % (RK / 4)) * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (r0 + rr < m) v = __ldg(reinterpret_cast<const float4*>(V + (r0 + rr) * RK + c4));
-            float* d = vt + rr * (RK + 1) + c4;
+            float* d = vt + rr * VS + c4;
             d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
         }
         __syncthreads();
-        const long long row = r0 + threadIdx.x;
-        if (row >= m) continue;
-        const float* vrow = vt + threadIdx.x * (RK + 1);
+        const long long row = r0 + rl;
+        const bool valid = row < m;   // rows past m: zeros, no output (shuffles stay converged)
+        const float* vrow = vt + rl * VS;
         float mx = 0.f;
 #pragma unroll 8
-        for (int k = 0; k < RK; ++k) mx = fmaxf(mx, fabsf(vrow[k]));
+        for (int k = h; k < RK; k += 2) mx = fmaxf(mx, fabsf(vrow[k]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         const int ev = scale_exp(mx);
         const float vs = exp2f((float)ev), vsi = exp2f(-(float)ev);
-        const float4* qrow = reinterpret_cast<const float4*>(Qs + row * (2 * RK));
-        float4* o = reinterpret_cast<float4*>(Vout + row * RK);
+        const float4* qrow = reinterpret_cast<const float4*>(Qs + (valid ? row : 0) * (2 * RK));
+        float4* o = reinterpret_cast<float4*>(Vout + (valid ? row : 0) * RK);
 #pragma unroll 1
         for (int c0 = 0; c0 < NC; c0 += 8) {   // this pass's 8 columns (of the half)
-            // column pairs (c, c + 1) as packed fp32x2 FMAs (the same two fp32 FMAs)
+            // column pairs (c, c + 1) as packed fp32x2 FMAs; ranks l = 2 i + h
             float2 den2[4], eg2[4], gcg2[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) den2[c] = eg2[c] = gcg2[c] = make_float2(0.f, 0.f);
 #pragma unroll 4
-            for (int l = 0; l < RK; ++l) {
+            for (int l = h; l < RK; l += 2) {
                 const float va = vrow[l];
                 const float el = va - __half2float(__float2half_rn(va * vs)) * vsi;
                 const float vh = va - el;
@@ -933,15 +940,26 @@ vfinish_kernel(const float* __restrict__ Qs, const float* __restrict__ V,
                     gcg2[2 * c4 + 1] = __ffma2_rn(vh2, h1, gcg2[2 * c4 + 1]);
                 }
             }
+            // the two rank halves (even + odd, in that order on both lanes)
             float den[8], eg[8], gcg[8];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                den[2 * c] = den2[c].x, den[2 * c + 1] = den2[c].y;
-                eg[2 * c] = eg2[c].x, eg[2 * c + 1] = eg2[c].y;
-                gcg[2 * c] = gcg2[c].x, gcg[2 * c + 1] = gcg2[c].y;
-            }
+                const float2 a[3] = {den2[c], eg2[c], gcg2[c]};
+                float2 t[3];
 #pragma unroll
-            for (int kq = 0; kq < 2; ++kq) {
+                for (int u = 0; u < 3; ++u) {
+                    const float ox = __shfl_xor_sync(0xffffffffu, a[u].x, 16);
+                    const float oy = __shfl_xor_sync(0xffffffffu, a[u].y, 16);
+                    t[u] = h ? make_float2(ox + a[u].x, oy + a[u].y)
+                             : make_float2(a[u].x + ox, a[u].y + oy);
+                }
+                den[2 * c] = t[0].x, den[2 * c + 1] = t[0].y;
+                eg[2 * c] = t[1].x, eg[2 * c + 1] = t[1].y;
+                gcg[2 * c] = t[2].x, gcg[2 * c + 1] = t[2].y;
+            }
+            if (!valid) continue;
+            {   // this thread's 4 of the 8 columns: kq = h
+                const int kq = h;
                 const int k4 = (cb + c0) / 4 + kq;   // float4 index in the row
                 const float4 qv = qrow[k4], q2v = qrow[RK / 4 + k4];
                 const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
