@@ -210,25 +210,27 @@ def test_tc_run_parity_30_iters():
     assert np.linalg.norm(vw32 - vw64) / np.linalg.norm(vw64) < 1e-4
 
 
-def test_tc_deterministic():
+@pytest.mark.parametrize("r", [64, 128, 100])
+def test_tc_deterministic(r):
     g = torch.Generator(device="cuda").manual_seed(9)
     x = torch.rand(3000, 640, device="cuda", generator=g)
-    v = torch.rand(3000, 64, device="cuda", generator=g)
-    w = torch.rand(64, 640, device="cuda", generator=g)
+    v = torch.rand(3000, r, device="cuda", generator=g)
+    w = torch.rand(r, 640, device="cuda", generator=g)
     a = one_iter(x, v, w, False)
     b = one_iter(x, v, w, False)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and a[2] == b[2]
 
 
-def test_tc_strided_x_equals_contiguous():
+@pytest.mark.parametrize("r", [64, 128])
+def test_tc_strided_x_equals_contiguous(r):
     """X given as a column slice of a wider matrix (row stride ldx > n): the
     scale pass and the pre-split copy follow ldx, so V', W' and f equal the
     contiguous copy's bit for bit."""
     g = torch.Generator(device="cuda").manual_seed(21)
     m, n = 1536, 640
     wide = torch.rand(m, n + 64, device="cuda", generator=g)
-    v = torch.rand(m, 64, device="cuda", generator=g)
-    w = torch.rand(64, n, device="cuda", generator=g)
+    v = torch.rand(m, r, device="cuda", generator=g)
+    w = torch.rand(r, n, device="cuda", generator=g)
     xs = wide[:, :n]
     assert xs.stride(0) == n + 64
     (a, used) = tc_launched(lambda: one_iter(xs, v, w, force_simt=False))

@@ -103,6 +103,26 @@ def test_rank128_large_shape_fp32_tiles():
     assert float((got - vw).norm() / vw.norm()) < 1e-4
 
 
+@pytest.mark.parametrize("r", [40, 64, 100, 128])
+def test_fp64_dmma_deterministic_and_fused_equal(r):
+    """fp64 on the DMMA tiles: two runs bitwise equal, and the fused device
+    loop equals the per-iteration path bit for bit (same kernels, fixed
+    split-K order)."""
+    m, n, iters = 2050, 1001, 5
+    g = torch.Generator(device="cuda").manual_seed(r + 7)
+    x = torch.rand(m, n, device="cuda", generator=g, dtype=torch.float64)
+    v0 = torch.rand(m, r, device="cuda", generator=g, dtype=torch.float64)
+    w0 = torch.rand(r, n, device="cuda", generator=g, dtype=torch.float64)
+    a, ta, prof = run_profiled(x, r, "fp64", iters, v0, w0, fused=False)
+    b, tb, _ = run_profiled(x, r, "fp64", iters, v0, w0, fused=False)
+    c, tc_, _ = run_profiled(x, r, "fp64", iters, v0, w0, fused=True)
+    assert "nnmf_vstep_tile" in prof, sorted(prof)
+    assert np.array_equal(ta.objective_values, tb.objective_values)
+    assert np.array_equal(ta.objective_values, tc_.objective_values)
+    assert torch.equal(a.v, b.v) and torch.equal(a.w, b.w)
+    assert torch.equal(a.v, c.v) and torch.equal(a.w, c.w)
+
+
 @pytest.mark.parametrize("r", [65, 100, 128])
 def test_fp64_ranks_above_64(r):
     """fp64, ranks 65..128 (the 128-rank tiles, zero-padded ranks), 6
