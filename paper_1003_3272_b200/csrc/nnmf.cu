@@ -452,7 +452,7 @@ bool tc_region(int dtype, long long m, long long n, int r, bool iter) {
     return iter && mmk_tc::shape_ok(dtype, m, n, r);
 }
 
-Plan make_plan(long long m, long long n, int r) {
+Plan make_plan(long long m, long long n, int r, int dtype) {
     Plan P;
     P.rpw = r <= 16 ? 2 : 1;
     P.nvb = ceil_div(m > 0 ? m : 1, kWarps * P.rpw);
@@ -476,7 +476,9 @@ Plan make_plan(long long m, long long n, int r) {
     if (S < 1) S = 1;
     P.rows_per_split = ceil_div(m > 0 ? m : 1, S);
     P.S = ceil_div(m > 0 ? m : 1, P.rows_per_split);
-    P.Sd = mmk_tile::applies(r) ? mmk_tile::kDmmaMaxSplits : 1;
+    // fp64 ranks 17..128 run the DMMA tiles, whose W part picks up to
+    // kDmmaMaxSplits row splits (wpart_splits_dmma); other paths use P.S
+    P.Sd = (dtype == MMK_F64 && mmk_tile::applies(r)) ? mmk_tile::kDmmaMaxSplits : 1;
     return P;
 }
 
@@ -641,9 +643,9 @@ struct Args {
 template <typename T, int RMAX>
 struct RunA {
     static int run(const Args& a) {
-        const Plan P = make_plan(a.m, a.n, a.r);
-        Ws L;
         const int dt = std::is_same<T, float>::value ? MMK_F32 : MMK_F64;
+        const Plan P = make_plan(a.m, a.n, a.r, dt);
+        Ws L;
         ws_layout(P, a.m, a.n, a.r, tc_region(dt, a.m, a.n, a.r, a.mode == 0), a.ws, &L);
         using KK = K<T, RMAX>;
         const T* X = (const T*)a.X;
@@ -734,7 +736,7 @@ int check(int dtype, long long m, long long n, long long r, long long ldx, size_
                             m, n, r, ldx, kMaxRank);
         return MMK_E_SHAPE;
     }
-    const Plan P = make_plan(m, n, (int)r);
+    const Plan P = make_plan(m, n, (int)r, dtype);
     size_t need = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr,
                             nullptr);
     if (!iter && dtype == MMK_F64) need = ref_offset(need) + mmk_ref::ws_bytes(m, n, r);
@@ -757,7 +759,7 @@ void* mmk_tc::engine_tc_ws(int dtype, const void* X, long long ldx, long long m,
     if (!tc_region(dtype, m, n, (int)r, true) || !eligible(MMK_F32, m, n, r, ldx, X))
         return nullptr;
     Ws L;
-    ws_layout(make_plan(m, n, (int)r), m, n, (int)r, true, ws, &L);
+    ws_layout(make_plan(m, n, (int)r, dtype), m, n, (int)r, true, ws, &L);
     return L.tc;
 }
 
@@ -766,7 +768,7 @@ static int ws_bytes_for(int dtype, int64_t m, int64_t n, int64_t r, bool iter, s
         mmk_host::set_error("unsupported NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
     }
-    const Plan P = make_plan(m, n, (int)r);
+    const Plan P = make_plan(m, n, (int)r, dtype);
     *out = ws_layout(P, m, n, (int)r, tc_region(dtype, m, n, (int)r, iter), nullptr, nullptr);
     if (!iter && dtype == MMK_F64) *out = ref_offset(*out) + mmk_ref::ws_bytes(m, n, r);
     return MMK_OK;
@@ -794,7 +796,7 @@ extern "C" int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, voi
     size_t b = ws_bytes, e = ws_bytes;   // the span left as is (none by default)
     if (tc_region(dtype, m, n, (int)r, true)) {
         Ws L;
-        ws_layout(make_plan(m, n, (int)r), m, n, (int)r, true, ws, &L);
+        ws_layout(make_plan(m, n, (int)r, dtype), m, n, (int)r, true, ws, &L);
         mmk_tc::presplit_span(m, n, &b, &e);
         b += (size_t)(reinterpret_cast<char*>(L.tc) - c);
         e += (size_t)(reinterpret_cast<char*>(L.tc) - c);
@@ -864,7 +866,8 @@ extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* 
 
 // the reference-order region of a single-op workspace (fp64)
 static void* ref_ws(void* ws, long long m, long long n, long long r) {
-    const size_t opb = ws_layout(make_plan(m, n, (int)r), m, n, (int)r, false, nullptr, nullptr);
+    const size_t opb = ws_layout(make_plan(m, n, (int)r, MMK_F64), m, n, (int)r, false, nullptr,
+                                 nullptr);
     return reinterpret_cast<char*>(ws) + ref_offset(opb);
 }
 
