@@ -1867,7 +1867,10 @@ bool shape_ok(int dtype, long long m, long long n, long long r) {
     if (dtype != MMK_F32 || r < 17 || r > 128) return false;
     if ((n & 7) || (m & 7) || m < BM || n < BM) return false;
     if (m > 0x7fffffffLL || n > 0x7fffffffLL) return false;
-    return 4.0 * (double)m * (double)n <= 96.0 * (1ull << 30);
+    // the pre-split copy, plus at the 128-rank tile the V step's Q rows
+    // (m x 256 fp32)
+    const double q_rows = r > 64 ? 1024.0 * (double)m : 0.0;
+    return 4.0 * (double)m * (double)n + q_rows <= 96.0 * (1ull << 30);
 }
 
 bool eligible(int dtype, long long m, long long n, long long r, long long ldx, const void* X) {
