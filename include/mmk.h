@@ -78,6 +78,9 @@ int mmk_prof_report(char *buf, size_t len);
  *            f_dev = red[f]
  * The row range is the caller's shard of X/V (rows are independent in the
  * V step; the W step is a sum over rows, hence the all-reduce of `red`).
+ * Ranks 1..128 (MMK_E_SHAPE above).  fp32 ranks 17..128 with m, n multiples
+ * of 8 run on the tensor cores (rank tiles of 64 and 128); fp64 ranks 17..128
+ * on the FP64 tensor cores (DMMA tiles); ranks <= 16 on warp-per-row kernels.
  * The workspace (prepared by mmk_nnmf_ws_clear, or zero-filled, before first
  * use) caches per-X data of the fp32 tensor-core path (ranks 17..128) -- the
  * scale exponent and the pre-split fp16 hi / lo copy of X (4 bytes per
@@ -126,7 +129,7 @@ int mmk_nnmf_gradient(int dtype, const void *X, int64_t ldx, const void *V, cons
                       size_t ws_bytes, double *red, int64_t *err_dev, void *stream);
 
 /* ------------------------------------------------------------------------
- * NNMF, Poisson log fit (nnmf.py:178-265), rank <= 64.  Square-root
+ * NNMF, Poisson log fit (nnmf.py:178-265), rank <= 128.  Square-root
  * multiplicative MM: V' = V sqrt((R W^T) / (rowsum W + guard)) with
  * R = X / (VW) masked to x > 0, then W' = W sqrt((V'^T R') / (colsum V' +
  * guard)) with R' = X / (V'W).
