@@ -422,6 +422,67 @@ nnmf_wfinish64_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n
     }
 }
 
+// The same for ranks 65..128 at the 128-rank tile (G^T 128 KB + the W slab 64
+// KB of shared memory, zero beyond r; 8 x 4 register tiles, l ascending as
+// nnmf_wfinish_kernel, so the denominators are the same fp64 sums).
+constexpr int kWf128Smem = (128 * 128 + 128 * 64) * 8;
+template <typename T>
+__global__ void __launch_bounds__(256)
+nnmf_wfinish128_kernel(const T* __restrict__ W, T* __restrict__ Wout, long long n, int r,
+                       const double* __restrict__ red, double* f_dev,
+                       const long long* __restrict__ skip) {
+    extern __shared__ double wf_smem[];
+    double(*Gt)[128] = reinterpret_cast<double(*)[128]>(wf_smem);            // Gt[l][k] = G[k][l]
+    double(*Ws)[64] = reinterpret_cast<double(*)[64]>(wf_smem + 128 * 128);  // Ws[l][j]
+    const long long rn = (long long)r * n;
+    if (f_dev && blockIdx.x == 0 && threadIdx.x == 0) *f_dev = red[rn + (long long)r * r];
+    if (skip && *skip) return;   // the engine's final pass (iteration cap) needs only f
+    const long long j0 = (long long)blockIdx.x * 64;
+    for (int i = threadIdx.x; i < 128 * 128; i += 256) {
+        const int l = i / 128, k = i % 128;
+        Gt[l][k] = (k < r && l < r) ? red[rn + (long long)k * r + l] : 0.0;
+    }
+    for (int i = threadIdx.x; i < 128 * 64; i += 256) {
+        const int l = i / 64, jj = i % 64;
+        Ws[l][jj] = (l < r && j0 + jj < n) ? (double)W[(long long)l * n + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // ranks 8 ty .., columns 4 tx ..
+    double acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll 4
+    for (int l = 0; l < 128; ++l) {
+        double av[8], bv[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 a = *reinterpret_cast<const double2*>(&Gt[l][8 * ty + 2 * h]);
+            av[2 * h] = a.x, av[2 * h + 1] = a.y;
+        }
+        const double2 b01 = *reinterpret_cast<const double2*>(&Ws[l][4 * tx]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Ws[l][4 * tx + 2]);
+        bv[0] = b01.x, bv[1] = b01.y, bv[2] = b23.x, bv[3] = b23.y;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = 8 * ty + i;
+        if (k >= r) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long col = j0 + 4 * tx + j;
+            if (col < n)
+                Wout[(long long)k * n + col] =
+                    (T)(Ws[k][4 * tx + j] * (red[(long long)k * n + col] / (acc[i][j] + kDenomGuard)));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 struct Plan {
     int g64w_blocks, g64w_cpb, g64v_blocks, g64v_cpb;   // rank-64 Gram split-K
@@ -713,6 +774,17 @@ int finish_b(const void* W, void* W_out, long long n, int r, const double* red, 
                    (nnmf_wfinish64_kernel<T><<<ceil_div(n, 64), 256, kWf64Smem, st>>>(
                        (const T*)W, (T*)W_out, n, red, f_dev, mmk_tc::last_flag())));
         MMK_CHECK_LAUNCH("nnmf_wfinish64_kernel");
+        return MMK_OK;
+    }
+    if (r > 64) {
+        if (mmk_host::first_on_device(reinterpret_cast<const void*>(nnmf_wfinish128_kernel<T>))) {
+            cudaFuncSetAttribute(nnmf_wfinish128_kernel<T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kWf128Smem);
+        }
+        MMK_LAUNCH("nnmf_wfinish", st,
+                   (nnmf_wfinish128_kernel<T><<<ceil_div(n, 64), 256, kWf128Smem, st>>>(
+                       (const T*)W, (T*)W_out, n, r, red, f_dev, mmk_tc::last_flag())));
+        MMK_CHECK_LAUNCH("nnmf_wfinish128_kernel");
         return MMK_OK;
     }
     MMK_LAUNCH("nnmf_wfinish", st,
