@@ -209,6 +209,7 @@ extern "C" int mmk_allgather(const void* send, void* recv, int64_t count, int dt
 }
 
 extern "C" int mmk_engine_run(void* eng, void* stream) {
+    MMK_NVTX("mmk_engine_run");
     Engine* e = reinterpret_cast<Engine*>(eng);
     if (!e) {
         mmk_host::set_error("null engine");
@@ -242,6 +243,7 @@ extern "C" int mmk_nnmf_engine_create(int dtype, const void* X, int64_t ldx, voi
                                       void* ws, size_t ws_bytes, double* red, void* comm,
                                       const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
                                       int64_t* ctl, int64_t* err_dev, void** engine) {
+    MMK_NVTX("mmk_nnmf_engine_create");
     if (!comm && mmk_small::nnmf_eligible(dtype, m, n, r, ldx)) {
         // small problems: the whole loop in one persistent kernel per batch
         Engine* e = new Engine();
@@ -295,6 +297,7 @@ extern "C" int mmk_pet_engine_create(int dtype, const void* E, int64_t lde, cons
                                      void* ws, size_t ws_bytes, double* red, void* comm,
                                      const mmk_stop_rule* rule, double* trace, int64_t* tstamp,
                                      int64_t* ctl, int64_t* err_dev, void** engine) {
+    MMK_NVTX("mmk_pet_engine_create");
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_pet_reduce_len(p);
     auto iter = [=](cudaStream_t s, int dir) -> int {
@@ -320,6 +323,7 @@ extern "C" int mmk_mds_engine_create(int dtype, const void* Y, const void* Wt, i
                                      size_t ws_bytes, void* comm, const mmk_stop_rule* rule,
                                      double* trace, int64_t* tstamp, int64_t* ctl,
                                      int64_t* err_dev, void** engine) {
+    MMK_NVTX("mmk_mds_engine_create");
     if (!comm && row0 == 0 && rows == n && mmk_small::mds_eligible(dtype, n, dim, Wt != nullptr)) {
         // small problems: the whole loop in one persistent kernel per batch
         Engine* e = new Engine();
@@ -364,6 +368,7 @@ extern "C" int mmk_mds_tri_engine_create(const float* packed, int64_t t0, int64_
                                          const mmk_stop_rule* rule, double* trace,
                                          int64_t* tstamp, int64_t* ctl, int64_t* err_dev,
                                          void** engine) {
+    MMK_NVTX("mmk_mds_tri_engine_create");
     double* f_dev = reinterpret_cast<double*>(ctl + MMK_CTL_FCUR);
     const int64_t rl = mmk_mds_tri_reduce_len(n, dim);
     auto iter = [=](cudaStream_t s, int dir) -> int {
@@ -386,6 +391,7 @@ extern "C" int mmk_nnmf_poisson_engine_create(int dtype, const void* X, int64_t 
                                               void* comm, const mmk_stop_rule* rule,
                                               double* trace, int64_t* tstamp, int64_t* ctl,
                                               int64_t* err_dev, void** engine) {
+    MMK_NVTX("mmk_nnmf_poisson_engine_create");
     if (!comm && mmk_small::nnmf_eligible(dtype, m, n, r, ldx)) {
         Engine* e = new Engine();
         int rc = mmk_small::nnmf_prepare(dtype, X, ldx, VA, WA, VB, WB, m, n, (int)r, rule, trace,
@@ -424,6 +430,7 @@ extern "C" int mmk_pet_sparse_engine_create(int dtype, const int32_t* rptr, cons
                                             void* comm, const mmk_stop_rule* rule, double* trace,
                                             int64_t* tstamp, int64_t* ctl, int64_t* err_dev,
                                             void** engine) {
+    MMK_NVTX("mmk_pet_sparse_engine_create");
     if (!comm && mmk_small::pet_eligible(dtype, d, p)) {
         // small problems: the whole loop in one persistent kernel per batch
         Engine* e = new Engine();

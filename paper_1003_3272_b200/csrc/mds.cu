@@ -438,6 +438,7 @@ extern "C" int mmk_mds_iter(int dtype, const void* Y, const void* Wt, int64_t ld
                             int64_t dim, int64_t n, int64_t row0, int64_t rows, int flags,
                             void* ws, size_t ws_bytes, double* f_dev, int64_t* err_dev,
                             void* stream) {
+    MMK_NVTX("mmk_mds_iter");
     if (dim < 1 || dim > kMaxDim) {
         mmk_host::set_error("embedding dimension %lld outside [1, %d]", (long long)dim, kMaxDim);
         return MMK_E_SHAPE;

@@ -578,6 +578,7 @@ extern "C" int mmk_mds_tri_ws_bytes(int64_t n, int64_t dim, int64_t t0, int64_t 
 extern "C" int mmk_mds_tri_pack(const float* Y, int64_t ldy, int64_t n, int64_t row0, int64_t rows,
                                 float* packed, int64_t t0, int64_t t1, int validate,
                                 int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_mds_tri_pack");
     int rc = check_tri(n, 1, t0, t1);
     if (rc) return rc;
     if (row0 < 0 || row0 % TB || rows < 1 || row0 + rows > n || ldy < n) {
@@ -597,6 +598,7 @@ extern "C" int mmk_mds_tri_pack(const float* Y, int64_t ldy, int64_t n, int64_t 
 extern "C" int mmk_mds_tri_iter_a(const float* packed, int64_t t0, int64_t t1, const float* theta,
                                   int64_t dim, int64_t n, void* ws, size_t ws_bytes, double* red,
                                   int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_mds_tri_iter_a");
     int rc = check_tri(n, dim, t0, t1);
     if (rc) return rc;
     const size_t need = tri_layout(tri_plan(n, t0, t1), (int)dim, nullptr, nullptr);
@@ -618,6 +620,7 @@ extern "C" int mmk_mds_tri_iter_a(const float* packed, int64_t t0, int64_t t1, c
 extern "C" int mmk_mds_tri_iter_b(const float* theta, float* theta_out, int64_t dim, int64_t n,
                                   const double* red, double* f_dev, int64_t* err_dev,
                                   void* stream) {
+    MMK_NVTX("mmk_mds_tri_iter_b");
     if (dim < 1 || dim > kMaxTriDim || n < 2) {
         mmk_host::set_error("bad packed-triangle MDS shape: n=%lld dim=%lld", (long long)n,
                             (long long)dim);
@@ -636,6 +639,7 @@ extern "C" int mmk_mds_tri_iter(const float* packed, int64_t t0, int64_t t1, con
                                 float* theta_out, int64_t dim, int64_t n, void* ws,
                                 size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                                 void* stream) {
+    MMK_NVTX("mmk_mds_tri_iter");
     mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_mds_tri_iter_a(packed, t0, t1, theta, dim, n, ws, ws_bytes, red, err_dev, stream);
     if (rc) return rc;

@@ -231,6 +231,7 @@ extern "C" int mmk_mds_votes_bytes(int64_t q, int64_t m, size_t* out) {
 extern "C" int mmk_mds_votes_tri(int dtype, const void* votes, int64_t q, int64_t m,
                                  float* packed, int64_t t0, int64_t t1, void* ws,
                                  size_t ws_bytes, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_mds_votes_tri");
     const long long T = (q + TB - 1) / TB;
     if (q < 2 || m < 1 || t0 < 0 || t1 <= t0 || t1 > T * (T + 1) / 2 || (m + 31) / 32 * 32 * 2 >= (1LL << 20)) {
         mmk_host::set_error("bad vote matrix %lld x %lld or tile range [%lld, %lld)",

@@ -12,6 +12,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "../../include/mmk.h"
@@ -155,6 +156,18 @@ struct NoFlag {
     bool prev;
 };
 }  // namespace mmk_host
+
+namespace mmk_host {
+// NVTX range over a C-ABI entry point (named ranges on an Nsight Systems
+// timeline; a pointer check when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace mmk_host
+#define MMK_NVTX(name) const mmk_host::NvtxRange _mmk_nvtx_range(name)
 
 // Bracket one kernel launch for the opt-in profiler (mmk_prof_enable).
 #define MMK_LAUNCH(name, st, ...)                                           \

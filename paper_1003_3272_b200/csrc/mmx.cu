@@ -23,6 +23,7 @@ f64_to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst, long 
 }  // namespace
 
 extern "C" int mmk_f64_to_f32(const double* src, float* dst, int64_t n, void* stream) {
+    MMK_NVTX("mmk_f64_to_f32");
     if (n < 0 || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)) {
         mmk_host::set_error("f64->f32: n=%lld, buffers must be 16-byte aligned", (long long)n);
         return MMK_E_SHAPE;

@@ -886,6 +886,7 @@ extern "C" int mmk_nnmf_ws_clear(int dtype, int64_t m, int64_t n, int64_t r, voi
 // instantiates the graph (the engine's own prologue then finds X prepared).
 extern "C" int mmk_nnmf_prepare(int dtype, const void* X, int64_t ldx, int64_t m, int64_t n,
                                 int64_t r, void* ws, size_t ws_bytes, void* stream) {
+    MMK_NVTX("mmk_nnmf_prepare");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, true);
     if (rc) return rc;
     void* tcws = mmk_tc::engine_tc_ws(dtype, X, ldx, m, n, r, ws);
@@ -901,6 +902,7 @@ extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void
                                const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
                                void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
                                void* stream) {
+    MMK_NVTX("mmk_nnmf_iter_a");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, true);
     if (rc) return rc;
     Args a{X, V, W, V_out, nullptr, ldx, m, n, (int)r, ws, red, nullptr, err_dev,
@@ -913,6 +915,7 @@ extern "C" int mmk_nnmf_iter_a(int dtype, const void* X, int64_t ldx, const void
 
 extern "C" int mmk_nnmf_iter_b(int dtype, const void* W, void* W_out, int64_t n, int64_t r,
                                const double* red, double* f_dev, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_iter_b");
     if (r < 1 || n < 1) {
         mmk_host::set_error("bad NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
@@ -929,6 +932,7 @@ extern "C" int mmk_nnmf_iter(int dtype, const void* X, int64_t ldx, const void* 
                              void* V_out, void* W_out, int64_t m, int64_t n, int64_t r, void* ws,
                              size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                              void* stream) {
+    MMK_NVTX("mmk_nnmf_iter");
     mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_nnmf_iter_a(dtype, X, ldx, V, W, V_out, m, n, r, ws, ws_bytes, red, err_dev,
                              stream);
@@ -948,6 +952,7 @@ static void* ref_ws(void* ws, long long m, long long n, long long r) {
 extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const void* V,
                                   const void* W, int64_t m, int64_t n, int64_t r, void* ws,
                                   size_t ws_bytes, double* f_dev, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_objective");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     if (dtype == MMK_F64)
@@ -962,6 +967,7 @@ extern "C" int mmk_nnmf_objective(int dtype, const void* X, int64_t ldx, const v
 extern "C" int mmk_nnmf_update_v(int dtype, const void* X, int64_t ldx, const void* V,
                                  const void* W, void* V_out, int64_t m, int64_t n, int64_t r,
                                  void* ws, size_t ws_bytes, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_update_v");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     if (dtype == MMK_F64)
@@ -977,6 +983,7 @@ extern "C" int mmk_nnmf_update_w(int dtype, const void* X, int64_t ldx, const vo
                                  const void* W, void* W_out, int64_t m, int64_t n, int64_t r,
                                  void* ws, size_t ws_bytes, double* red, int64_t* err_dev,
                                  void* stream) {
+    MMK_NVTX("mmk_nnmf_update_w");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     if (dtype == MMK_F64)
@@ -998,6 +1005,7 @@ extern "C" int mmk_nnmf_gradient(int dtype, const void* X, int64_t ldx, const vo
                                  const void* W, void* GV, void* GW, int64_t m, int64_t n,
                                  int64_t r, void* ws, size_t ws_bytes, double* red,
                                  int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_gradient");
     int rc = check(dtype, m, n, r, ldx, ws_bytes, false);
     if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

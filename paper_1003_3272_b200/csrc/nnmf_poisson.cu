@@ -410,6 +410,7 @@ extern "C" int mmk_nnmf_poisson_iter_a(int dtype, const void* X, int64_t ldx, co
                                        const void* W, void* V_out, int64_t m, int64_t n,
                                        int64_t r, void* ws, size_t ws_bytes, double* red,
                                        int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_poisson_iter_a");
     int rc = check(dtype, m, n, r, ldx, ws_bytes);
     if (rc) return rc;
     Args a{X, V, W, V_out, ldx, m, n, (int)r, ws, red, err_dev,
@@ -423,6 +424,7 @@ extern "C" int mmk_nnmf_poisson_iter_a(int dtype, const void* X, int64_t ldx, co
 extern "C" int mmk_nnmf_poisson_iter_b(int dtype, const void* W, void* W_out, int64_t n,
                                        int64_t r, const double* red, double* f_dev,
                                        int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_poisson_iter_b");
     if (r < 1 || r > kMaxPoisRank || n < 1) {
         mmk_host::set_error("bad Poisson NNMF shape n=%lld r=%lld", (long long)n, (long long)r);
         return MMK_E_SHAPE;
@@ -450,6 +452,7 @@ extern "C" int mmk_nnmf_poisson_iter(int dtype, const void* X, int64_t ldx, cons
                                      const void* W, void* V_out, void* W_out, int64_t m,
                                      int64_t n, int64_t r, void* ws, size_t ws_bytes, double* red,
                                      double* f_dev, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_nnmf_poisson_iter");
     mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_nnmf_poisson_iter_a(dtype, X, ldx, V, W, V_out, m, n, r, ws, ws_bytes, red,
                                      err_dev, stream);

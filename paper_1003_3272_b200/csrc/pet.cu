@@ -773,6 +773,7 @@ extern "C" int64_t mmk_pet_reduce_len(int64_t p) { return p + 2; }
 extern "C" int mmk_pet_iter_a(int dtype, const void* E, int64_t lde, const void* y,
                               const void* lam, int64_t d, int64_t p, void* ws, size_t ws_bytes,
                               double* red, int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_pet_iter_a");
     if (p < 1 || d < 0 || (d > 0 && lde < p)) {
         mmk_host::set_error("bad PET shape d=%lld p=%lld lde=%lld", (long long)d, (long long)p,
                             (long long)lde);
@@ -801,6 +802,7 @@ extern "C" int mmk_pet_iter_b(int dtype, const void* lam, void* lam_out, int64_t
                               const int32_t* nbr_ptr, const int32_t* nbr_idx, double mu, int flags,
                               const double* red, void* ws, size_t ws_bytes, double* f_dev,
                               int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_pet_iter_b");
     if (p < 1) {
         mmk_host::set_error("bad PET pixel count %lld", (long long)p);
         return MMK_E_SHAPE;
@@ -825,6 +827,7 @@ extern "C" int mmk_pet_iter(int dtype, const void* E, int64_t lde, const void* y
                             const int32_t* nbr_idx, double mu, int flags, void* ws,
                             size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                             void* stream) {
+    MMK_NVTX("mmk_pet_iter");
     mmk_host::NoFlag one_gpu;   // no collective between the phases
     int rc = mmk_pet_iter_a(dtype, E, lde, y, lam, d, p, ws, ws_bytes, red, err_dev, stream);
     if (rc) return rc;
@@ -845,6 +848,7 @@ extern "C" int mmk_pet_sparse_iter_a(int dtype, const int32_t* rptr, const int32
                                      const void* cval, const void* y, const void* lam, int64_t d,
                                      int64_t p, void* ws, size_t ws_bytes, double* red,
                                      int64_t* err_dev, void* stream) {
+    MMK_NVTX("mmk_pet_sparse_iter_a");
     if (p < 1 || d < 0) {
         mmk_host::set_error("bad sparse PET shape d=%lld p=%lld", (long long)d, (long long)p);
         return MMK_E_SHAPE;
@@ -885,6 +889,7 @@ extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t
                                    const int32_t* nbr_idx, double mu, int flags, void* ws,
                                    size_t ws_bytes, double* red, double* f_dev, int64_t* err_dev,
                                    void* stream) {
+    MMK_NVTX("mmk_pet_sparse_iter");
     if (d == 0 || (dtype != MMK_F32 && dtype != MMK_F64)) {
         mmk_host::NoFlag one_gpu;
         int rc = mmk_pet_sparse_iter_a(dtype, rptr, ridx, rval, cptr, cidx, cval, y, lam, d, p,
@@ -929,6 +934,7 @@ extern "C" int mmk_pet_sparse_iter(int dtype, const int32_t* rptr, const int32_t
 extern "C" int mmk_pet_gradient(int dtype, const void* lam, void* grad, int64_t p,
                                 const int32_t* nbr_ptr, const int32_t* nbr_idx, double mu,
                                 const double* colsum, const double* red, void* stream) {
+    MMK_NVTX("mmk_pet_gradient");
     if (p < 1 || (dtype != MMK_F32 && dtype != MMK_F64)) {
         mmk_host::set_error("bad PET gradient call: dtype %d p=%lld", dtype, (long long)p);
         return MMK_E_SHAPE;

@@ -144,6 +144,7 @@ pet_siddon_kernel(const double* __restrict__ det, int n_det, int side,
 
 extern "C" int mmk_pet_siddon(const double* det, int n_det, int side, const double* lines,
                               int cap, int* idx, double* val, int* cnt, void* stream) {
+    MMK_NVTX("mmk_pet_siddon");
     if (n_det < 2 || side < 1 || cap < 2 * side + 3) {
         mmk_host::set_error("bad Siddon geometry: detectors=%d side=%d cap=%d (cap >= 2 side + 3)",
                             n_det, side, cap);
