@@ -169,9 +169,12 @@ struct NvtxRange {
 }  // namespace mmk_host
 #define MMK_NVTX(name) const mmk_host::NvtxRange _mmk_nvtx_range(name)
 
-// Bracket one kernel launch for the opt-in profiler (mmk_prof_enable).
+// Bracket one kernel launch for the opt-in profiler (mmk_prof_enable), in an
+// NVTX range named after the kernel (the launch call on the host timeline;
+// launches replayed from a CUDA graph do not pass through here).
 #define MMK_LAUNCH(name, st, ...)                                           \
     do {                                                                    \
+        const mmk_host::NvtxRange _nvtx(name);                              \
         const bool _p = mmk_host::prof_on();                                \
         if (_p) mmk_host::prof_start(name, st);                             \
         __VA_ARGS__;                                                        \
